@@ -1,0 +1,341 @@
+"""Pins for the CPU oracle (oracle/): values the paper prints, closed forms,
+invariants (Lemma 1, Theorems 1 and 2), special cases that reduce to textbook or
+library routines, and brute force on tiny inputs. None of these re-types the
+oracle's own loops: each compares it with something the paper or mathematics
+fixes independently. CPU only."""
+import itertools
+
+import numpy as np
+import pytest
+
+import cksgen
+import oracle
+from conftest import load_bit_rows, load_hex_keys, mask_from, positions
+
+
+# ---- independent helpers (integer arithmetic, not the oracle's bit loops) ----
+
+def int_dbit(a: bytes, b: bytes):
+    """Most significant differing bit via integer XOR and bit_length (closed form)."""
+    x = int.from_bytes(a, "big") ^ int.from_bytes(b, "big")
+    return None if x == 0 else 8 * len(a) - x.bit_length()
+
+
+def py_sorted_perm(keys, rid=None):
+    n = keys.shape[0]
+    rid = np.arange(n, dtype=np.uint32) if rid is None else rid
+    rows = sorted(range(n), key=lambda i: (bytes(keys[i]), int(rid[i])))
+    return np.array([rid[i] for i in rows], dtype=np.uint32)
+
+
+def planes_to_ints(planes):
+    np_, n = planes.shape
+    return [sum(int(planes[q, i]) << (32 * q) for q in range(np_)) for i in range(n)]
+
+
+# ---- Fig. 2 worked example (Sec. 3.1) --------------------------------
+
+FIG2 = load_hex_keys("fig2_keys.txt")
+
+
+def bits12(p):
+    return {x for x in p if x < 12}
+
+
+def test_fig2_distinction_positions():
+    # P:218 "bit positions 1, 2, 5 and 7 are distinction bit positions"
+    perm = oracle.sort_keys(FIG2)
+    assert list(perm) == list(range(6))                      # rows are key_0 < ... < key_5
+    dbit, mask = oracle.adjacent_dbits(FIG2, perm)
+    assert positions(mask) == {1, 2, 5, 7}
+    # D_1 = D_4 = 5, D_2 = 1; D_3 = 7
+    assert dbit[1] == 5 and dbit[4] == 5 and dbit[2] == 1 and dbit[3] == 7
+    assert dbit[0] == oracle.NONE16
+    # Theorem 1: all pairs give the same set
+    assert positions(oracle.dbits_all_pairs(FIG2)) == {1, 2, 5, 7}
+
+
+def test_fig2_lemma1_examples():
+    # D-bit(key_1, key_3) = 1 and D-bit(key_0, key_2) = 1
+    assert oracle.dbit_pair(FIG2[1], FIG2[3]) == 1
+    assert oracle.dbit_pair(FIG2[0], FIG2[2]) == 1
+
+
+def test_fig2_variant_and_invariant():
+    # invariant {0,3,4,8,9,10}, variant {1,2,5,6,7,11}
+    v = bits12(positions(oracle.variant_bitmap(FIG2)))
+    assert v == {1, 2, 5, 6, 7, 11}
+    assert set(range(12)) - v == {0, 3, 4, 8, 9, 10}
+    # 6 and 11 variant but not distinction; every distinction bit is variant
+    assert {6, 11} <= v and not ({6, 11} & {1, 2, 5, 7})
+
+
+def test_fig2_deletion_narrative():
+    # delete key_3 -> 7 not a distinction position, still variant
+    k = np.delete(FIG2, 3, axis=0)
+    _, d = oracle.adjacent_dbits(k, oracle.sort_keys(k))
+    assert positions(d) == {1, 2, 5}
+    assert 7 in positions(oracle.variant_bitmap(k))
+    # ... also delete key_0: distinction positions unchanged, 7 becomes invariant
+    k2 = np.delete(k, 0, axis=0)
+    _, d2 = oracle.adjacent_dbits(k2, oracle.sort_keys(k2))
+    assert positions(d2) == {1, 2, 5}
+    assert 7 not in positions(oracle.variant_bitmap(k2))
+
+
+def test_fig2_compressed_keys_and_order():
+    # Fig. 2(b) / Theorem 2: compressed keys on positions {1,2,5,7}
+    mask = mask_from({1, 2, 5, 7}, 2)
+    planes = oracle.compress(FIG2, mask)
+    assert planes.shape == (1, 6)
+    assert list(planes[0]) == [0b0001, 0b0010, 0b1000, 0b1001, 0b1010, 0b1100]
+    assert list(oracle.sort_packed(planes)) == list(range(6))
+
+
+def test_fig2_doffset():
+    # P:479 D-offset[i] = position of the (i+1)-st 1
+    assert list(oracle.doffset(mask_from({1, 2, 5, 7}, 2))) == [1, 2, 5, 7]
+    assert oracle.doffset(np.zeros(2, np.uint8)).size == 0
+
+
+# ---- Remark 1 -------------------------------------------------
+
+def test_remark1_not_minimal():
+    keys = load_hex_keys("remark1_keys.txt")
+    _, d = oracle.adjacent_dbits(keys, oracle.sort_keys(keys))
+    assert positions(d) == {0, 1, 3}
+    order = list(oracle.sort_keys(keys))
+
+    def determines(sub):
+        m = mask_from(sub, 1)
+        return list(oracle.sort_packed(oracle.compress(keys, m))) == order and \
+            len(set(planes_to_ints(oracle.compress(keys, m)))) == 4
+    minimal = [set(s) for r in range(0, 5) for s in itertools.combinations(range(4), r) if determines(s)]
+    best = min(len(s) for s in minimal)
+    assert best == 2 and [s for s in minimal if len(s) == 2] == [{2, 3}]
+    assert determines({0, 1, 3})
+
+
+# ---- Table 3 and the Sec. 5.1 segmentation ------------
+
+def test_table3_bitmap_facts():
+    m = load_bit_rows("table3_indbtab_dbitmap.txt")
+    assert m.size == 35                                   # INDBTAB keys are 35 B (Table 2)
+    assert oracle.popcount(m) == 56
+    last_byte = max(p // 8 for p in positions(m)) + 1     # 1-based byte number
+    assert last_byte == 22                                # P:603 "in the 22nd byte"
+    assert (oracle.popcount(m) + 7) // 8 == 7             # "stored in 7 bytes"
+    st, bits = oracle.pext_segments(m)
+    assert list(st + 1) == [3, 11, 19] and list(bits) == [15, 26, 15]
+    assert sum(bits) == 56
+
+
+def test_pext_pipeline_equals_bit_loop():
+    # Sec. 5.1 PEXT pipeline vs the plain concatenation of P:223
+    rng = np.random.default_rng(7)
+    for B in (1, 3, 8, 13, 35, 64):
+        keys = rng.integers(0, 256, size=(300, B), dtype=np.uint8)
+        for density in (0.05, 0.3, 0.9):
+            mask = np.packbits(rng.random(8 * B) < density)
+            a = oracle.compress(keys, mask)
+            b = oracle.compress(keys, mask, pext=True)
+            assert np.array_equal(a, b)
+    t3 = load_bit_rows("table3_indbtab_dbitmap.txt")
+    keys = rng.integers(0, 256, size=(500, 35), dtype=np.uint8)
+    assert np.array_equal(oracle.compress(keys, t3), oracle.compress(keys, t3, pext=True))
+
+
+# ---- D-bit, Lemma 1, Theorem 1 --------------------------------------------------
+
+def test_dbit_pair_closed_form():
+    rng = np.random.default_rng(1)
+    for B in (1, 2, 5, 16, 33):
+        for _ in range(300):
+            a = rng.integers(0, 256, B, dtype=np.uint8)
+            b = a.copy()
+            j = rng.integers(0, B)
+            b[j:] = rng.integers(0, 256, B - j, dtype=np.uint8)
+            d = oracle.dbit_pair(a, b)
+            e = int_dbit(bytes(a), bytes(b))
+            assert (d == -1 and e is None) or d == e
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_lemma1_and_theorem1_bruteforce(seed):
+    rng = np.random.default_rng(seed)
+    B = int(rng.integers(1, 6))
+    n = int(rng.integers(2, 65))
+    keys = rng.integers(0, 256, size=(n, B), dtype=np.uint8)
+    keys &= rng.integers(0, 256, size=B, dtype=np.uint8)          # shared zero bits
+    keys = np.unique(keys, axis=0)                                 # Lemma 1 is stated for distinct keys
+    rng.shuffle(keys)
+    perm = oracle.sort_keys(keys)
+    s = keys[perm]
+    dbit, d = oracle.adjacent_dbits(keys, perm)
+    for i in range(len(s)):
+        for j in range(i + 1, len(s)):
+            assert int_dbit(bytes(s[i]), bytes(s[j])) == int(dbit[i + 1:j + 1].min())   # Lemma 1
+    assert positions(d) == positions(oracle.dbits_all_pairs(keys))                      # Theorem 1
+
+
+def test_sort_keys_matches_library_sort():
+    rng = np.random.default_rng(3)
+    keys = cksgen.uniform(2000, 5, seed=11, dup_ppm=100000)
+    assert np.array_equal(oracle.sort_keys(keys), py_sorted_perm(keys))
+    rid = rng.permutation(2000).astype(np.uint32)
+    assert np.array_equal(oracle.sort_keys(keys, rid=rid), py_sorted_perm(keys, rid))
+    assert np.array_equal(oracle.sort_keys(keys, threads=4), py_sorted_perm(keys))
+
+
+@pytest.mark.slow
+def test_theorem1_cfg1_all_pairs():
+    # cfg1 at full size: all 2.1e9 pairs == sorted adjacency
+    keys = cksgen.config(1)
+    _, d = oracle.adjacent_dbits(keys, oracle.sort_keys(keys, threads=oracle.threads_default()))
+    assert positions(d) == positions(oracle.dbits_all_pairs(keys))
+
+
+# ---- special cases with closed forms ----------------------------------------------
+
+def test_special_cases():
+    # all 2^16 distinct 2-byte keys -> every bit is a distinction bit
+    k = cksgen.consecutive(1 << 16, 2, shuffle_seed=5)
+    _, d = oracle.adjacent_dbits(k, oracle.sort_keys(k))
+    assert positions(d) == set(range(16))
+    # consecutive integers 0..2^k-1 -> the low k bits
+    for kk in (1, 5, 9):
+        k = cksgen.consecutive(1 << kk, 4, shuffle_seed=kk)
+        _, d = oracle.adjacent_dbits(k, oracle.sort_keys(k))
+        assert positions(d) == set(range(32 - kk, 32))
+    # all equal / n <= 1 -> empty
+    for n in (0, 1, 7):
+        k = cksgen.all_equal(n, 9, seed=2)
+        _, d = oracle.adjacent_dbits(k, oracle.sort_keys(k))
+        assert positions(d) == set()
+        assert positions(oracle.byteocc_superset(k)) == set()
+        assert positions(oracle.variant_bitmap(k)) == set()
+
+
+def test_identity_mask_compress_is_the_key():
+    # all-ones mask over an 8-byte key -> compressed key == key word
+    k = cksgen.uniform(500, 8, seed=4)
+    planes = oracle.compress(k, np.full(8, 0xFF, np.uint8))
+    vals = planes_to_ints(planes)
+    assert vals == [int.from_bytes(bytes(r), "big") for r in k]
+
+
+def test_cfg2_numeric_crosscheck():
+    # textbook numeric path: sort the uint64 values, D = {clz64(u_i ^ u_{i+1})}
+    k = cksgen.config(2, n=200_000)
+    u = np.sort(k.view(">u8").ravel().astype(np.uint64))
+    x = u[1:] ^ u[:-1]
+    x = x[x != 0]
+    exp = {64 - int(v).bit_length() for v in np.unique(x)}
+    _, d = oracle.adjacent_dbits(k, oracle.sort_keys(k))
+    assert positions(d) == exp
+    assert len(exp) <= 23                                # 22 low bits + <= 1 carry position
+
+
+# ---- supersets: D subset of D+ subset of V, closed forms for D+ -------------------
+
+def test_superset_chain_and_closed_forms():
+    for keys in (cksgen.config(1, n=5000), cksgen.config(3, n=20000), cksgen.config(4, n=20000),
+                 cksgen.config(5, n=20000), cksgen.config(2, n=20000)):
+        _, d = oracle.adjacent_dbits(keys, oracle.sort_keys(keys))
+        dp = positions(oracle.byteocc_superset(keys))
+        v = positions(oracle.variant_bitmap(keys))
+        D = positions(d)
+        assert D <= dp <= v
+        assert min(v) in D                               # first variant bit separates some pair
+    # ACGT bytes: per-byte D+ = {3,5,6} (A 0x41, C 0x43, G 0x47, T 0x54)
+    g = cksgen.genome(50_000, seed=9)
+    dp = positions(oracle.byteocc_superset(g))
+    assert dp == {8 * j + t for j in range(32) for t in (3, 5, 6)}
+    # ASCII digits '0'..'9' -> low nibble {4,5,6,7} (cf. Table 3's 00001111 bytes)
+    rng = np.random.default_rng(0)
+    dig = (0x30 + rng.integers(0, 10, size=(5000, 6))).astype(np.uint8)
+    assert positions(oracle.byteocc_superset(dig)) == {8 * j + t for j in range(6) for t in (4, 5, 6, 7)}
+
+
+# ---- Theorem 2: compressed order == full-key order (with row-id tie-break) ----------
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_theorem2_on_configs(cfg):
+    keys = cksgen.config(cfg, n=30_000)
+    permK = oracle.sort_keys(keys)
+    assert np.array_equal(permK, py_sorted_perm(keys))
+    _, d = oracle.adjacent_dbits(keys, permK)
+    rng = np.random.default_rng(cfg)
+    B = keys.shape[1]
+    masks = [d, oracle.byteocc_superset(keys), oracle.variant_bitmap(keys),
+             d | np.packbits(rng.random(8 * B) < 0.2)]          # superset safety
+    for m in masks:
+        planes = oracle.compress(keys, m)
+        assert np.array_equal(oracle.sort_packed(planes), permK)
+    # injectivity on distinct keys
+    u = np.unique(keys, axis=0)
+    pl = oracle.compress(u, d)
+    assert len(set(planes_to_ints(pl))) == u.shape[0]
+
+
+def test_negative_mask_missing_a_distinction_bit():
+    # clearing one true D-bit must break Theorem 2's equality for a witness input
+    keys = FIG2[::-1].copy()                 # reversed rows: row-id tie-break cannot rescue the order
+    permK = oracle.sort_keys(keys)
+    for p in (1, 2, 5, 7):
+        m = mask_from({1, 2, 5, 7} - {p}, 2)
+        assert not np.array_equal(oracle.sort_packed(oracle.compress(keys, m)), permK)
+
+
+# ---- adjacency on compressed keys ------------------------------------
+
+@pytest.mark.parametrize("cfg", [1, 3, 5])
+def test_adjacent_compressed_equals_full_key_dbits(cfg):
+    keys = cksgen.config(cfg, n=20_000)
+    permK = oracle.sort_keys(keys)
+    dfull, d = oracle.adjacent_dbits(keys, permK)
+    sup = oracle.byteocc_superset(keys)
+    m = oracle.popcount(sup)
+    planes = oracle.compress(keys, sup)
+    sp = planes[:, oracle.sort_packed(planes)]
+    dc, mask = oracle.adjacent_compressed(sp, m, sup)
+    assert np.array_equal(dc, dfull)
+    assert np.array_equal(mask, d)                      # new D subset of old, here == exact D
+
+
+# ---- bulk load -----------------------------------------------------------
+
+@pytest.mark.parametrize("n,fanout,fill", [(1, 64, 1.0), (64, 64, 1.0), (65, 64, 1.0),
+                                           (20_000, 64, 1.0), (5000, 14, 0.9), (3000, 9, 0.9)])
+def test_bulkload_structure(n, fanout, fill):
+    keys = cksgen.config(3, n=n)
+    perm = oracle.sort_keys(keys)
+    dbit, _ = oracle.adjacent_dbits(keys, perm)
+    t = oracle.bulkload(perm, dbit, keys, fanout, fill)
+    per = int(np.floor(fanout * fill))
+    # closed forms: leaf count ceil(n/per); height = levels until one node
+    assert t["level_nodes"][0] == -(-n // per)
+    h, c = 1, -(-n // per)
+    while c > 1:
+        c = -(-c // per)
+        h += 1
+    assert t["height"] == h and t["level_nodes"][-1] == 1
+    L0 = int(t["level_nodes"][0])
+    leaf_rids = t["entry_rid"][:L0, :per].ravel()
+    assert np.array_equal(leaf_rids[leaf_rids != 0xFFFFFFFF], perm)      # leaf scan == perm
+    assert t["node_cnt"][:L0].sum() == n
+    # inner D-bits: the direct formula == range-min of D_k (Lemma 1)
+    off, span = L0, per
+    for lvl in range(1, t["height"]):
+        nodes = int(t["level_nodes"][lvl])
+        ent = t["entry_rid"][off:off + nodes, :per].ravel()
+        edb = t["entry_dbit"][off:off + nodes, :per].ravel()
+        cnt = int(t["node_cnt"][off:off + nodes].sum())
+        for x in range(1, cnt):
+            lo, hi = x * span, min((x + 1) * span, n) - 1   # (prev entry's highest, this highest]
+            expect = int(dbit[lo:hi + 1].min())
+            assert edb[x] == expect
+            assert ent[x] == perm[hi]
+        assert edb[0] == oracle.NONE16
+        off += nodes
+        span *= per
