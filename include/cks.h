@@ -1,0 +1,205 @@
+/*
+ * cks.h -- C ABI of libcks.so, the B200 (sm_100a) compressed key sort.
+ *
+ * Paper: "Compressed Key Sort and Fast Index Reconstruction", arXiv 2009.11543.
+ * Citations "P:n" are lines of the paper text with their section.
+ *
+ * CONVENTIONS (DESIGN.md Sec. 2 readings R3-R5, R8-R9)
+ *   keys     device u8[n][key_bytes], row-major; byte 0 is most significant and bit
+ *            position p is bit (7 - p%8) of byte p/8, position 0 = MSB.
+ *            Row id of key i is i unless row ids are passed explicitly.
+ *   mask     HOST u8[key_bytes] in the same bit layout as a key: 1 = (possibly) a
+ *            distinction bit position (the D-bitmap). m = popcount(mask).
+ *   packed   device u32[ceil(m/32)][n], structure-of-arrays "planes": plane q holds
+ *            bits [32q, 32q+32) of P, where P = Compress(key) read as an
+ *            unsigned m-bit integer whose MOST significant bit is the mask's first
+ *            (smallest) position. m = 0 means zero planes.
+ *   perm     device u32[n]; perm[i] = row id of the i-th smallest (key, row id).
+ *   dbit     device u16[n]; dbit[i] = D_i = D-bit(sorted key_{i-1}, sorted key_i)
+ *            (P:176), CKS_DBIT_NONE for i = 0 and for equal adjacent keys.
+ *
+ * OWNERSHIP  The caller allocates and owns every pointer it passes (device
+ *            pointers may come from torch.empty(..., device="cuda")). The library
+ *            never frees caller memory. A cks_ctx owns internal scratch, grown on
+ *            demand and freed by cks_ctx_destroy; pointers it returns as "views"
+ *            stay valid until the next call on the same context.
+ * STREAMS    All device work is ordered on the context's stream (borrowed from the
+ *            caller, e.g. torch.cuda.current_stream().cuda_stream; NULL = legacy
+ *            default stream). Calls that return host results (masks, popcounts,
+ *            heights) synchronise that stream before returning and say so.
+ * ERRORS     Every call returns CKS_OK (0) or a positive error code:
+ *              CKS_EINVAL  null pointer with n > 0, key_bytes not in [1, 512],
+ *                          fanout < 2, fill not in (0, 1], floor(fanout*fill) < 2,
+ *                          bits > 8*512, unknown kind;
+ *              CKS_ERANGE  n >= 2^32 (row ids are u32), or a prior mask that is not
+ *                          a superset of the true distinction bits (detected when
+ *                          the sorted order contradicts it);
+ *              CKS_ENOMEM  scratch allocation failed;
+ *              CKS_ECUDA   a CUDA runtime error (text in cks_last_error).
+ *            Duplicated keys are NOT an error (reading R3). n = 0 is a valid no-op.
+ *            m = 0 (n <= 1 or all keys equal) is valid: zero planes, identity perm.
+ *            No call falls back to the CPU.
+ */
+#ifndef CKS_H
+#define CKS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKS_OK 0
+#define CKS_EINVAL 1
+#define CKS_ERANGE 2
+#define CKS_ENOMEM 3
+#define CKS_ECUDA 4
+
+#define CKS_DBIT_NONE 0xFFFFu
+#define CKS_MAX_KEY_BYTES 512u
+#define CKS_MAX_LEVELS 40
+
+/* superset masks for the first build (reading R2) */
+#define CKS_SUPERSET_VARIANT 0   /* V: OR of key XOR key_0 */
+#define CKS_SUPERSET_BYTEOCC 1   /* D+: per byte, D-bits of the set of occurring byte values */
+
+typedef struct cks_ctx cks_ctx;
+
+/* ---- context ---------------------------------------------------------------- */
+
+/* Create a context on CUDA `device` using `stream` (cudaStream_t, may be NULL). */
+int cks_ctx_create(int device, void* stream, cks_ctx** out);
+int cks_ctx_destroy(cks_ctx* ctx);
+/* Replace the borrowed stream used by subsequent calls. */
+int cks_ctx_set_stream(cks_ctx* ctx, void* stream);
+/* 1 = record per-stage CUDA events in cks_build (read with cks_ctx_stage_ms). */
+int cks_ctx_set_timing(cks_ctx* ctx, int enable);
+/* Stage times (ms) of the last timed cks_build: a1 mask, a3 compress+hist, a5 sort,
+ * a6 adjacency, a7 repack, a8 bulk load, total. Synchronises. Returns count written. */
+int cks_ctx_stage_ms(cks_ctx* ctx, float* out, int max);
+/* Number of kernels libcks launched since the context was created. */
+uint64_t cks_ctx_launches(const cks_ctx* ctx);
+const char* cks_strerror(int code);
+const char* cks_last_error(const cks_ctx* ctx);
+
+/* ---- a1: superset mask -------------------------------------------------------------
+ * One pass over the keys; writes the chosen superset M of the distinction bits
+ * (kind = CKS_SUPERSET_VARIANT: variant bitmap V, P:365/P:413;
+ *  kind = CKS_SUPERSET_BYTEOCC: D+ = union over byte positions j of the D-bits of the
+ *  set of byte values occurring at j -- "extended distinction bit positions").
+ * mask_out: host u8[key_bytes]; popcount_out: host, may be NULL. Synchronises. */
+int cks_superset_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
+                      int kind, uint8_t* mask_out, uint32_t* popcount_out);
+
+/* ---- exact D (first build; rebuild recompute) ------------------------
+ * Exact distinction bits D = {D_1..D_{n}} over the sorted order (Theorem 1).
+ * Runs: superset mask (or `prior_mask`, host u8[key_bytes], which MUST be a superset of
+ * D, e.g. the previous D-bitmap) -> compress -> ONE stable sort -> adjacency.
+ * If perm_out (device u32[n]) is non-NULL it receives the permutation of that same sort.
+ * mask_out: host u8[key_bytes]; popcount_out: host, may be NULL. Synchronises. */
+int cks_distinction_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
+                         const uint8_t* prior_mask, uint8_t* mask_out, uint32_t* popcount_out,
+                         uint32_t* perm_out);
+
+/* ---- a2+a3: compress (Sec. 5.1) -------------------------------------------
+ * packed_out[q][i] = plane q of Compress_mask(key_i), input row order.
+ * mask: host u8[key_bytes]; packed_out: device u32[ceil(m/32)][n] (may be NULL if m=0).
+ * Asynchronous. */
+int cks_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
+                 const uint8_t* mask, uint32_t* packed_out);
+
+/* ---- a4+a5: sort ------------------------------------------------------------
+ * Stable LSD radix sort of (P, row id) by P, ties by row id (Theorem 2).
+ * packed: device u32[ceil(packed_bits/32)][n] (not modified); packed_bits = m.
+ * row_ids: device u32[n] or NULL (= 0..n-1). Non-NULL row ids are sorted first as the
+ *   least significant digits, the paper's record-ID bits in the sort key.
+ * perm_out: device u32[n]. sorted_packed_out: device planes like `packed`, or NULL.
+ * Asynchronous. */
+int cks_sort(cks_ctx* ctx, const uint32_t* packed, uint32_t packed_bits, uint64_t n,
+             const uint32_t* row_ids, uint32_t* perm_out, uint32_t* sorted_packed_out);
+
+/* ---- a6: adjacency / recompute ---------------------------------------------
+ * Over sorted packed keys compressed with `sort_mask` (host u8[key_bytes], popcount =
+ * packed_bits): D_i = D-offset[D-bit(Compress(key_{i-1}), Compress(key_i))] and the new
+ * D-bitmap (a subset of sort_mask). mask_out: host u8[key_bytes];
+ * popcount_out: host, may be NULL; dbit_out: device u16[n] or NULL. Synchronises. */
+int cks_adjacent_dbits(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t packed_bits,
+                       uint64_t n, const uint8_t* sort_mask, uint32_t key_bytes,
+                       uint8_t* mask_out, uint32_t* popcount_out, uint16_t* dbit_out);
+
+/* ---- a8: bottom-up bulk load (Sec. 5.3) -----------------------------------------
+ * Nodes have `fanout` slots filled with per_node = floor(fanout*fill) entries.
+ * Level 0 = leaves; levels are concatenated leaves first (level_offset[l]).
+ *   node_cnt[node]              entries used in the node
+ *   entry_rid[node][fanout]     leaf: row id of the entry's key; inner: row id of the
+ *                               highest key under the child
+ *   entry_dbit[node][fanout]    leaf: D_i against the global predecessor;
+ *                               inner: D-bit of the child's highest key vs the previous
+ *                               entry's highest key at that level, computed as
+ *                               the range-min of D_k (Lemma 1); CKS_DBIT_NONE for
+ *                               the first entry of a level and for equal keys.
+ *   entry_child[(node-level_offset[1])][fanout]  inner nodes only: global index of child
+ * Empty slots hold 0xFFFFFFFF / CKS_DBIT_NONE. */
+typedef struct {
+    uint64_t n;
+    uint32_t fanout;
+    uint32_t per_node;
+    uint32_t height;                          /* number of levels; 0 when n = 0 */
+    uint32_t reserved;
+    uint64_t level_nodes[CKS_MAX_LEVELS];
+    uint64_t level_offset[CKS_MAX_LEVELS];
+    uint64_t total_nodes;
+    uint64_t inner_nodes;                     /* total_nodes - level_nodes[0] */
+} cks_tree_shape;
+
+typedef struct {
+    uint32_t* node_cnt;                       /* device u32[total_nodes] */
+    uint32_t* entry_rid;                      /* device u32[total_nodes*fanout] */
+    uint16_t* entry_dbit;                     /* device u16[total_nodes*fanout] or NULL */
+    uint32_t* entry_child;                    /* device u32[inner_nodes*fanout] or NULL */
+} cks_tree;
+
+/* Host-only arithmetic; no context needed. */
+int cks_bulkload_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* out);
+
+/* perm: device u32[n] (sorted row ids); dbit: device u16[n] D_i or NULL (then leaf and
+ * inner D-bits are not produced: entry_dbit must be NULL too). Asynchronous. */
+int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n,
+                 uint32_t fanout, float fill, const cks_tree* out);
+
+/* ---- fused first build: a1 -> a2 -> a3 -> a4 -> a5 -> a6 -> a7 -> a8 -----------------------
+ * The benchmarked step. ONE sort on the superset mask (or prior_mask); exact D from the
+ * adjacency pass; packed keys repacked to exact D (skipped when M = D); bulk load. */
+typedef struct {
+    /* inputs (caller-owned buffers) */
+    uint8_t* mask;            /* host u8[key_bytes]: receives exact D */
+    uint32_t* perm;           /* device u32[n] */
+    uint16_t* dbit;           /* device u16[n] or NULL (library scratch is used) */
+    cks_tree tree;            /* device arrays, or node_cnt == NULL to skip the bulk load */
+    uint32_t fanout;          /* bulk load fanout (>= 2) */
+    float fill;               /* bulk load fill in (0, 1] */
+    int superset_kind;        /* CKS_SUPERSET_BYTEOCC (default) or CKS_SUPERSET_VARIANT */
+    /* outputs */
+    uint32_t popcount;        /* |D| */
+    uint32_t sort_bits;       /* |M|, the width the sort ran on */
+    uint32_t height;          /* tree height (0 if skipped) */
+    uint32_t passes;          /* LSD digit passes run */
+    const uint32_t* packed;   /* VIEW (ctx-owned): sorted P_D planes u32[ceil(|D|/32)][n] */
+} cks_build_out;
+
+/* keys: device u8[n][key_bytes]; prior_mask: host u8[key_bytes] superset or NULL.
+ * Synchronises (twice: after the superset mask and after the adjacency pass). */
+int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
+              const uint8_t* prior_mask, cks_build_out* out);
+
+/* Same as cks_build with HOST buffers: host_keys u8[n][key_bytes] (pinned or pageable)
+ * is copied to ctx-owned device memory in chunks that overlap the superset-mask pass;
+ * out->perm is a HOST u32[n] filled by a device->host copy; out->dbit and out->tree
+ * must be NULL/skipped (device-side results stay in ctx scratch). Synchronises. */
+int cks_build_host(cks_ctx* ctx, const uint8_t* host_keys, uint64_t n, uint32_t key_bytes,
+                   const uint8_t* prior_mask, cks_build_out* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKS_H */

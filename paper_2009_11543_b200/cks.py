@@ -1,0 +1,341 @@
+"""Thin ctypes binding of libcks.so (include/cks.h). Argument marshalling only:
+torch tensors provide device memory and the current CUDA stream; every step of the
+path runs in the library's CUDA kernels. There is no CPU fallback -- if libcks.so is
+missing or no CUDA device is present, calls raise.
+
+Names follow the C ABI: superset_mask, distinction_mask, compress, sort,
+adjacent_dbits, bulkload_shape, bulkload, build, build_host.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+import torch
+
+from . import _build
+
+SO_PATH = _build.SO
+CKS_OK, CKS_EINVAL, CKS_ERANGE, CKS_ENOMEM, CKS_ECUDA = 0, 1, 2, 3, 4
+DBIT_NONE = 0xFFFF
+MAX_LEVELS = 40
+SUPERSET_VARIANT, SUPERSET_BYTEOCC = 0, 1
+
+_lib = None
+_lock = threading.Lock()
+_ctx = {}
+
+
+class CksError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"cks error {code}: {msg}")
+        self.code = code
+
+
+class TreeShape(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("fanout", ctypes.c_uint32), ("per_node", ctypes.c_uint32),
+                ("height", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("level_nodes", ctypes.c_uint64 * MAX_LEVELS), ("level_offset", ctypes.c_uint64 * MAX_LEVELS),
+                ("total_nodes", ctypes.c_uint64), ("inner_nodes", ctypes.c_uint64)]
+
+
+class Tree(ctypes.Structure):
+    _fields_ = [("node_cnt", ctypes.c_void_p), ("entry_rid", ctypes.c_void_p),
+                ("entry_dbit", ctypes.c_void_p), ("entry_child", ctypes.c_void_p)]
+
+
+class BuildOut(ctypes.Structure):
+    _fields_ = [("mask", ctypes.c_void_p), ("perm", ctypes.c_void_p), ("dbit", ctypes.c_void_p),
+                ("tree", Tree), ("fanout", ctypes.c_uint32), ("fill", ctypes.c_float),
+                ("superset_kind", ctypes.c_int), ("popcount", ctypes.c_uint32),
+                ("sort_bits", ctypes.c_uint32), ("height", ctypes.c_uint32), ("passes", ctypes.c_uint32),
+                ("packed", ctypes.c_void_p)]
+
+
+EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing",
+           "cks_ctx_stage_ms", "cks_ctx_launches", "cks_strerror", "cks_last_error",
+           "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
+           "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_build", "cks_build_host"]
+
+
+def load_library(path: str | None = None):
+    """Load libcks.so (raises if it was not built: run __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or SO_PATH
+    if not os.path.exists(path):
+        raise RuntimeError(f"libcks.so not found at {path}; build it with `python __graft_entry__.py build`")
+    L = ctypes.CDLL(path)
+    p, u64, u32, i32, f32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_float
+    L.cks_ctx_create.argtypes = [i32, p, ctypes.POINTER(p)]
+    L.cks_ctx_destroy.argtypes = [p]
+    L.cks_ctx_set_stream.argtypes = [p, p]
+    L.cks_ctx_set_timing.argtypes = [p, i32]
+    L.cks_ctx_stage_ms.argtypes = [p, ctypes.POINTER(f32), i32]
+    L.cks_ctx_launches.argtypes = [p]
+    L.cks_ctx_launches.restype = u64
+    L.cks_strerror.argtypes = [i32]
+    L.cks_strerror.restype = ctypes.c_char_p
+    L.cks_last_error.argtypes = [p]
+    L.cks_last_error.restype = ctypes.c_char_p
+    L.cks_superset_mask.argtypes = [p, p, u64, u32, i32, p, ctypes.POINTER(u32)]
+    L.cks_distinction_mask.argtypes = [p, p, u64, u32, p, p, ctypes.POINTER(u32), p]
+    L.cks_compress.argtypes = [p, p, u64, u32, p, p]
+    L.cks_sort.argtypes = [p, p, u32, u64, p, p, p]
+    L.cks_adjacent_dbits.argtypes = [p, p, u32, u64, p, u32, p, ctypes.POINTER(u32), p]
+    L.cks_bulkload_shape.argtypes = [u64, u32, f32, ctypes.POINTER(TreeShape)]
+    L.cks_bulkload.argtypes = [p, p, p, u64, u32, f32, ctypes.POINTER(Tree)]
+    L.cks_build.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
+    L.cks_build_host.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
+    for name in EXPORTS:
+        getattr(L, name).restype = getattr(L, name).restype or i32
+    _lib = L
+    return L
+
+
+def _context(device: int | None = None):
+    L = load_library()
+    if not torch.cuda.is_available():
+        raise RuntimeError("libcks needs a CUDA device (no CPU fallback)")
+    dev = torch.cuda.current_device() if device is None else device
+    with _lock:
+        c = _ctx.get(dev)
+        if c is None:
+            c = ctypes.c_void_p()
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = L.cks_ctx_create(dev, ctypes.c_void_p(stream), ctypes.byref(c))
+            if rc != CKS_OK:
+                raise CksError(rc, L.cks_strerror(rc).decode())
+            _ctx[dev] = c
+    L.cks_ctx_set_stream(c, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    return L, c
+
+
+def _check(L, c, rc):
+    if rc != CKS_OK:
+        raise CksError(rc, f"{L.cks_strerror(rc).decode()}: {L.cks_last_error(c).decode()}")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _keys(keys: torch.Tensor):
+    if keys.dtype != torch.uint8 or keys.dim() != 2 or not keys.is_cuda or not keys.is_contiguous():
+        raise ValueError("keys must be a contiguous cuda uint8 tensor [n, key_bytes]")
+    return keys.shape[0], keys.shape[1]
+
+
+def _host_mask(mask, B: int) -> np.ndarray:
+    m = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8))
+    if m.size != B:
+        raise ValueError(f"mask must have {B} bytes")
+    return m
+
+
+def popcount(mask) -> int:
+    return int(np.unpackbits(np.asarray(mask, dtype=np.uint8)).sum())
+
+
+def nplanes(bits: int) -> int:
+    return (bits + 31) // 32
+
+
+def launches() -> int:
+    L, c = _context()
+    return int(L.cks_ctx_launches(c))
+
+
+def set_timing(enable: bool):
+    L, c = _context()
+    L.cks_ctx_set_timing(c, 1 if enable else 0)
+
+
+def stage_ms() -> list[float]:
+    L, c = _context()
+    buf = (ctypes.c_float * 8)()
+    k = L.cks_ctx_stage_ms(c, buf, 8)
+    return [float(buf[i]) for i in range(k)]
+
+
+def superset_mask(keys: torch.Tensor, kind: int = SUPERSET_BYTEOCC) -> np.ndarray:
+    n, B = _keys(keys)
+    L, c = _context(keys.device.index)
+    mask = np.zeros(B, np.uint8)
+    pc = ctypes.c_uint32()
+    _check(L, c, L.cks_superset_mask(c, _ptr(keys), n, B, kind, mask.ctypes.data, ctypes.byref(pc)))
+    return mask
+
+
+def distinction_mask(keys: torch.Tensor, prior_mask=None, want_perm: bool = True):
+    """(exact D mask [B] uint8, perm tensor or None)."""
+    n, B = _keys(keys)
+    L, c = _context(keys.device.index)
+    mask = np.zeros(B, np.uint8)
+    pm = None if prior_mask is None else _host_mask(prior_mask, B)
+    perm = torch.empty(n, dtype=torch.int32, device=keys.device) if want_perm else None
+    pc = ctypes.c_uint32()
+    _check(L, c, L.cks_distinction_mask(c, _ptr(keys), n, B, None if pm is None else pm.ctypes.data,
+                                        mask.ctypes.data, ctypes.byref(pc), _ptr(perm)))
+    return mask, perm
+
+
+def compress(keys: torch.Tensor, mask) -> torch.Tensor:
+    """SoA planes int32[ceil(m/32)][n] (bit patterns of u32) of Compress_mask(key)."""
+    n, B = _keys(keys)
+    L, c = _context(keys.device.index)
+    m = _host_mask(mask, B)
+    out = torch.empty((nplanes(popcount(m)), n), dtype=torch.int32, device=keys.device)
+    _check(L, c, L.cks_compress(c, _ptr(keys), n, B, m.ctypes.data, _ptr(out) if out.numel() else None))
+    return out
+
+
+def sort(packed: torch.Tensor, bits: int, row_ids: torch.Tensor | None = None, want_sorted: bool = False):
+    """(perm int32[n], sorted planes or None)."""
+    n = packed.shape[1]
+    L, c = _context(packed.device.index)
+    if packed.dtype != torch.int32 or not packed.is_contiguous() or packed.shape[0] != nplanes(bits):
+        raise ValueError("packed must be contiguous int32 [ceil(bits/32), n]")
+    perm = torch.empty(n, dtype=torch.int32, device=packed.device)
+    srt = torch.empty_like(packed) if want_sorted else None
+    if row_ids is not None and (row_ids.dtype != torch.int32 or row_ids.numel() != n):
+        raise ValueError("row_ids must be int32 [n]")
+    _check(L, c, L.cks_sort(c, _ptr(packed) if packed.numel() else None, bits, n, _ptr(row_ids), _ptr(perm),
+                            _ptr(srt) if srt is not None and srt.numel() else None))
+    return perm, srt
+
+
+def adjacent_dbits(sorted_packed: torch.Tensor, bits: int, sort_mask, want_dbit: bool = True):
+    """(exact D mask [B], dbit int16[n] or None) from sorted planes."""
+    n = sorted_packed.shape[1]
+    sm = np.ascontiguousarray(np.asarray(sort_mask, dtype=np.uint8))
+    B = sm.size
+    L, c = _context(sorted_packed.device.index)
+    mask = np.zeros(B, np.uint8)
+    dbit = torch.empty(n, dtype=torch.int16, device=sorted_packed.device) if want_dbit else None
+    pc = ctypes.c_uint32()
+    _check(L, c, L.cks_adjacent_dbits(c, _ptr(sorted_packed) if sorted_packed.numel() else None, bits, n,
+                                      sm.ctypes.data, B, mask.ctypes.data, ctypes.byref(pc), _ptr(dbit)))
+    return mask, dbit
+
+
+def bulkload_shape(n: int, fanout: int, fill: float = 1.0) -> TreeShape:
+    s = TreeShape()
+    rc = load_library().cks_bulkload_shape(n, fanout, fill, ctypes.byref(s))
+    if rc != CKS_OK:
+        raise CksError(rc, "bad bulk-load shape")
+    return s
+
+
+def alloc_tree(shape: TreeShape, device, with_dbit: bool = True, with_child: bool = True) -> dict:
+    T, f = int(shape.total_nodes), int(shape.fanout)
+    return dict(
+        node_cnt=torch.empty(max(T, 1), dtype=torch.int32, device=device),
+        entry_rid=torch.empty(max(T * f, 1), dtype=torch.int32, device=device),
+        entry_dbit=torch.empty(max(T * f, 1), dtype=torch.int16, device=device) if with_dbit else None,
+        entry_child=torch.empty(max(int(shape.inner_nodes) * f, 1), dtype=torch.int32, device=device)
+        if with_child else None)
+
+
+def _tree_struct(t: dict) -> Tree:
+    return Tree(t["node_cnt"].data_ptr(), t["entry_rid"].data_ptr(),
+                t["entry_dbit"].data_ptr() if t.get("entry_dbit") is not None else None,
+                t["entry_child"].data_ptr() if t.get("entry_child") is not None else None)
+
+
+def bulkload(perm: torch.Tensor, dbit: torch.Tensor | None, fanout: int = 64, fill: float = 1.0,
+             with_child: bool = True) -> dict:
+    n = perm.numel()
+    L, c = _context(perm.device.index)
+    shape = bulkload_shape(n, fanout, fill)
+    t = alloc_tree(shape, perm.device, with_dbit=dbit is not None, with_child=with_child)
+    tr = _tree_struct(t)
+    _check(L, c, L.cks_bulkload(c, _ptr(perm), _ptr(dbit), n, fanout, fill, ctypes.byref(tr)))
+    t["shape"] = shape
+    return t
+
+
+class Builder:
+    """Preallocated fused first build (cks_build) for repeated steps on one key shape."""
+
+    def __init__(self, n: int, B: int, device, fanout: int = 64, fill: float = 1.0,
+                 superset_kind: int = SUPERSET_BYTEOCC, tree: bool = True, dbit: bool = True):
+        self.n, self.B = n, B
+        self.mask = np.zeros(B, np.uint8)
+        self.perm = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+        self.dbit = torch.empty(max(n, 1), dtype=torch.int16, device=device) if dbit else None
+        self.shape = bulkload_shape(n, fanout, fill)
+        self.tree = alloc_tree(self.shape, device) if tree else None
+        self.out = BuildOut()
+        self.out.mask = self.mask.ctypes.data
+        self.out.perm = self.perm.data_ptr()
+        self.out.dbit = self.dbit.data_ptr() if self.dbit is not None else None
+        if self.tree is not None:
+            self.out.tree = _tree_struct(self.tree)
+        self.out.fanout = fanout
+        self.out.fill = fill
+        self.out.superset_kind = superset_kind
+
+    def __call__(self, keys: torch.Tensor, prior_mask=None) -> "Builder":
+        n, B = _keys(keys)
+        assert (n, B) == (self.n, self.B)
+        L, c = _context(keys.device.index)
+        pm = None if prior_mask is None else _host_mask(prior_mask, B)
+        _check(L, c, L.cks_build(c, _ptr(keys), n, B, None if pm is None else pm.ctypes.data,
+                                 ctypes.byref(self.out)))
+        return self
+
+    def packed(self) -> torch.Tensor | None:
+        """Copy of the sorted P_D planes (ctx-owned view -> new tensor)."""
+        npd = nplanes(int(self.out.popcount))
+        if npd == 0 or self.n == 0:
+            return torch.empty((0, self.n), dtype=torch.int32, device=self.perm.device)
+        from_ptr = int(self.out.packed)
+        out = torch.empty((npd, self.n), dtype=torch.int32, device=self.perm.device)
+        cudart_copy(out, from_ptr, npd * self.n * 4)
+        return out
+
+
+def cudart_copy(dst: torch.Tensor, src_ptr: int, nbytes: int):
+    """Device-to-device copy from a raw pointer on the current stream (via torch)."""
+    # wrap the raw pointer as a tensor view using the CUDA array interface
+    class _View:
+        __cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<i4", "data": (src_ptr, True),
+                                    "version": 3, "strides": None, "stream": None}
+    src = torch.as_tensor(_View(), device=dst.device)
+    dst.view(-1).copy_(src)
+
+
+def build(keys: torch.Tensor, prior_mask=None, fanout: int = 64, fill: float = 1.0,
+          superset_kind: int = SUPERSET_BYTEOCC, tree: bool = True) -> dict:
+    n, B = _keys(keys)
+    b = Builder(n, B, keys.device, fanout, fill, superset_kind, tree)
+    b(keys, prior_mask)
+    o = b.out
+    return dict(mask=b.mask.copy(), popcount=int(o.popcount), sort_bits=int(o.sort_bits), passes=int(o.passes),
+                perm=b.perm[:n], dbit=b.dbit[:n] if b.dbit is not None else None, packed=b.packed(),
+                tree=b.tree, shape=b.shape, height=int(o.height))
+
+
+def build_host(host_keys: np.ndarray, prior_mask=None, superset_kind: int = SUPERSET_BYTEOCC,
+               perm_out: np.ndarray | None = None, device: int | None = None) -> dict:
+    """Fused build from HOST keys (numpy uint8 [n, B], ideally pinned) -> host perm."""
+    k = np.ascontiguousarray(host_keys)
+    if k.dtype != np.uint8 or k.ndim != 2:
+        raise ValueError("host_keys must be uint8 [n, B]")
+    n, B = k.shape
+    L, c = _context(device)
+    mask = np.zeros(B, np.uint8)
+    perm = perm_out if perm_out is not None else np.empty(n, np.uint32)
+    o = BuildOut()
+    o.mask = mask.ctypes.data
+    o.perm = perm.ctypes.data
+    o.superset_kind = superset_kind
+    o.fanout, o.fill = 64, 1.0
+    pm = None if prior_mask is None else _host_mask(prior_mask, B)
+    _check(L, c, L.cks_build_host(c, k.ctypes.data if n else None, n, B, None if pm is None else pm.ctypes.data,
+                                  ctypes.byref(o)))
+    return dict(mask=mask, popcount=int(o.popcount), sort_bits=int(o.sort_bits), perm=perm)

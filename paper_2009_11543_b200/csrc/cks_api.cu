@@ -1,0 +1,672 @@
+// cks_api.cu -- the C ABI of libcks.so (include/cks.h): argument checks, scratch
+// management, host planning and the stream-ordered launch sequence of each call.
+// Every step of the path runs in the kernels of k_*.cu; the host only plans (mask ->
+// gather masks / D-offset table, a few hundred bytes) and orchestrates.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/cks.h"
+#include "cks_internal.h"
+
+using namespace cks;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+enum Stage { ST_BEGIN = 0, ST_MASK, ST_COMPRESS, ST_SORT, ST_ADJ, ST_REPACK, ST_BULK, ST_N };
+
+}  // namespace
+
+struct cks_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    char err[512] = {0};
+    uint64_t launches = 0;
+    uint32_t epoch = 1;
+    bool timing = false;
+    bool timed = false;
+    cudaEvent_t ev[ST_N] = {};
+    cudaEvent_t plan_ev[3] = {};      // guards the pinned staging slots
+    // scratch
+    DevBuf occ, masks8, planeA, planeB, ridA, ridB, hist, base, status, counters, dacc, moff, dbit,
+        rmin0, rmin1, plan[3], keys, perm_scratch;
+    size_t status_tiles = 0;
+    // pinned host staging
+    GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
+    uint16_t* h_moff = nullptr;
+    uint32_t* h_small = nullptr;      // 4 KiB: masks, dacc words
+};
+
+namespace {
+
+int fail(cks_ctx* c, int code, const char* fmt, ...) {
+    if (c) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(c->err, sizeof(c->err), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define CK(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(ctx, CKS_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),  \
+                        __FILE__, __LINE__);                                              \
+    } while (0)
+
+#define LAUNCH(expr)        \
+    do {                    \
+        ctx->launches++;    \
+        CK(expr);           \
+    } while (0)
+
+#define TRY(expr)                   \
+    do {                            \
+        int r_ = (expr);            \
+        if (r_ != CKS_OK) return r_; \
+    } while (0)
+
+int ensure(cks_ctx* ctx, DevBuf& b, size_t bytes, bool zero = false) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return CKS_OK;
+    if (b.p) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    size_t cap = bytes + bytes / 8;                          // a little headroom
+    cudaError_t e = cudaMalloc(&b.p, cap);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, CKS_ENOMEM, "cudaMalloc(%zu): %s", cap, cudaGetErrorString(e));
+    }
+    b.cap = cap;
+    if (zero) CK(cudaMemsetAsync(b.p, 0, cap, ctx->stream));
+    return CKS_OK;
+}
+
+template <class T>
+T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
+
+uint32_t popcount_mask(const uint8_t* m, uint32_t B) {
+    uint32_t c = 0;
+    for (uint32_t j = 0; j < B; j++) c += (uint32_t)__builtin_popcount(m[j]);
+    return c;
+}
+
+int check_keys(cks_ctx* ctx, const void* keys, uint64_t n, uint32_t B) {
+    if (!ctx) return CKS_EINVAL;
+    if (B < 1 || B > CKS_MAX_KEY_BYTES) return fail(ctx, CKS_EINVAL, "key_bytes %u not in [1,512]", B);
+    if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n = %llu >= 2^32", (unsigned long long)n);
+    if (n > 0 && !keys) return fail(ctx, CKS_EINVAL, "keys is NULL with n > 0");
+    return CKS_OK;
+}
+
+void mark(cks_ctx* ctx, Stage s) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[s], ctx->stream);
+}
+
+// Upload a gather plan through pinned slot `slot` (waits for the slot's previous copy).
+int upload_plan(cks_ctx* ctx, int slot, GatherPlan** dplan) {
+    TRY(ensure(ctx, ctx->plan[slot], sizeof(GatherPlan)));
+    size_t bytes = offsetof(GatherPlan, step) + sizeof(GatherStep) * ctx->h_plan[slot]->nsteps;
+    CK(cudaMemcpyAsync(ctx->plan[slot].p, ctx->h_plan[slot], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->plan_ev[slot], ctx->stream));
+    *dplan = as<GatherPlan>(ctx->plan[slot]);
+    return CKS_OK;
+}
+int claim_slot(cks_ctx* ctx, int slot) {
+    CK(cudaEventSynchronize(ctx->plan_ev[slot]));
+    return CKS_OK;
+}
+
+// a1: superset mask into host `mask_out`; returns popcount via *m.
+int run_superset(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, int kind,
+                 uint8_t* mask_out, uint32_t* m, bool keys_ready = true) {
+    if (kind != CKS_SUPERSET_VARIANT && kind != CKS_SUPERSET_BYTEOCC)
+        return fail(ctx, CKS_EINVAL, "unknown superset kind %d", kind);
+    TRY(ensure(ctx, ctx->occ, (size_t)B * 8 * 4));
+    TRY(ensure(ctx, ctx->masks8, (size_t)B * 2));
+    if (keys_ready) {
+        CK(cudaMemsetAsync(ctx->occ.p, 0, (size_t)B * 8 * 4, ctx->stream));
+        if (n) LAUNCH(launch_occupancy(keys, n, B, as<uint32_t>(ctx->occ), ctx->sms, ctx->stream));
+    }
+    LAUNCH(launch_occ_finalize(as<uint32_t>(ctx->occ), B, n, as<uint8_t>(ctx->masks8),
+                               as<uint8_t>(ctx->masks8) + B, ctx->stream));
+    CK(cudaEventSynchronize(ctx->plan_ev[2]));
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->masks8.p, (size_t)B * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(ctx->h_small) + (kind == CKS_SUPERSET_BYTEOCC ? 0 : B);
+    memcpy(mask_out, src, B);
+    *m = popcount_mask(mask_out, B);
+    return CKS_OK;
+}
+
+// a2 + a3
+int run_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* mask,
+                 uint32_t* planes) {
+    TRY(claim_slot(ctx, 0));
+    plan_compress(mask, B, ctx->h_plan[0]);
+    uint32_t m = ctx->h_plan[0]->out_bits, np = (m + 31) / 32;
+    if (n == 0 || m == 0) return CKS_OK;
+    GatherPlan* dplan;
+    TRY(upload_plan(ctx, 0, &dplan));
+    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0]->nsteps, np, planes, ctx->stream));
+    return CKS_OK;
+}
+
+// a4 + a5. `in_planes` (np planes) is not modified. `in_rid` NULL = implicit ids; when
+// non-NULL its rid_passes digits are sorted first. Sorted planes land in `final_planes`
+// (NULL = ctx scratch; returned via *sorted_view), row ids in `final_rid`.
+// `avoid` (may be NULL) is a scratch buffer holding the input planes; the pass sequence
+// never writes it before the first pass has read it.
+int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint32_t np, uint32_t key_passes, uint64_t n,
+             const uint32_t* in_rid, uint32_t rid_passes, uint32_t* final_planes, uint32_t* final_rid,
+             const uint32_t** sorted_view) {
+    const uint32_t P = key_passes + (in_rid ? rid_passes : 0);
+    if (sorted_view) *sorted_view = in_planes;
+    if (n == 0) return CKS_OK;
+    if (P == 0) {                                        // nothing to sort: identity order
+        if (in_rid) CK(cudaMemcpyAsync(final_rid, in_rid, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        else LAUNCH(launch_iota(final_rid, n, ctx->stream));
+        if (final_planes && np)
+            CK(cudaMemcpyAsync(final_planes, in_planes, (size_t)np * n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        return CKS_OK;
+    }
+    const size_t pbytes = (size_t)np * n * 4;
+    TRY(ensure(ctx, ctx->planeA, pbytes));
+    TRY(ensure(ctx, ctx->planeB, pbytes));
+    TRY(ensure(ctx, ctx->ridA, n * 4));
+    TRY(ensure(ctx, ctx->ridB, n * 4));
+    TRY(ensure(ctx, ctx->hist, (size_t)P * 256 * 4));
+    TRY(ensure(ctx, ctx->base, (size_t)P * 256 * 4));
+    TRY(ensure(ctx, ctx->counters, (size_t)P * 4));
+    uint64_t tiles = onesweep_tiles(n);
+    if (ctx->status_tiles < tiles) {
+        TRY(ensure(ctx, ctx->status, (size_t)tiles * 256 * 8, /*zero=*/true));
+        ctx->status_tiles = ctx->status.cap / (256 * 8);
+    }
+    CK(cudaMemsetAsync(ctx->hist.p, 0, (size_t)P * 256 * 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)P * 4, ctx->stream));
+    LAUNCH(launch_hist(in_planes, n, key_passes, in_rid, rid_passes, as<uint32_t>(ctx->hist), ctx->sms,
+                       ctx->stream));
+    ctx->launches += (P + 31) / 32 - 1;                  // launch_hist runs one kernel per 32 passes
+    LAUNCH(launch_scan(as<uint32_t>(ctx->hist), P, as<uint32_t>(ctx->base), ctx->stream));
+
+    const uint32_t* cur_p = in_planes;
+    const uint32_t* cur_r = in_rid;
+    for (uint32_t t = 0; t < P; t++) {
+        const bool last = t == P - 1;
+        const bool odd = ((P - 1 - t) & 1) != 0;
+        uint32_t* out_p = odd ? as<uint32_t>(ctx->planeA) : (last && final_planes ? final_planes : as<uint32_t>(ctx->planeB));
+        uint32_t* out_r = last ? final_rid : (odd ? as<uint32_t>(ctx->ridA) : as<uint32_t>(ctx->ridB));
+        OnesweepArgs a;
+        a.in_planes = cur_p;
+        a.out_planes = out_p;
+        a.in_rid = cur_r;
+        a.out_rid = out_r;
+        a.n = n;
+        a.nplanes = np;
+        uint32_t hist_index;
+        if (in_rid && t < rid_passes) {                  // row-id digits first (least significant)
+            a.digit_plane = -1;
+            a.shift = 8 * t;
+            hist_index = key_passes + t;
+        } else {
+            uint32_t p = in_rid ? t - rid_passes : t;
+            a.digit_plane = (int32_t)(p >> 2);
+            a.shift = 8 * (p & 3);
+            hist_index = p;
+        }
+        a.bucket_base = as<uint32_t>(ctx->base) + (size_t)hist_index * 256;
+        a.tile_counter = as<uint32_t>(ctx->counters) + t;
+        a.status = as<unsigned long long>(ctx->status);
+        if (ctx->epoch >= 0x7FFFFFF0u) {                 // flag namespace exhausted: reset
+            CK(cudaMemsetAsync(ctx->status.p, 0, ctx->status.cap, ctx->stream));
+            ctx->epoch = 1;
+        }
+        a.epoch = ctx->epoch++;
+        LAUNCH(launch_onesweep(a, ctx->stream));
+        cur_p = out_p;
+        cur_r = out_r;
+    }
+    if (sorted_view) *sorted_view = cur_p;
+    return CKS_OK;
+}
+
+// a6: exact D from sorted planes compressed with `sort_mask` (host).
+int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint32_t m, uint64_t n, const uint8_t* sort_mask,
+                 uint32_t B, uint8_t* mask_out, uint16_t* dbit) {
+    const uint32_t nwords = (8 * B + 31) / 32;
+    TRY(ensure(ctx, ctx->dacc, (size_t)nwords * 4));
+    TRY(ensure(ctx, ctx->moff, (size_t)(m + 1) * 2));
+    CK(cudaEventSynchronize(ctx->plan_ev[1]));
+    uint32_t t = 0;
+    for (uint32_t p = 0; p < 8 * B; p++)
+        if ((sort_mask[p >> 3] >> (7 - (p & 7))) & 1) ctx->h_moff[t++] = (uint16_t)p;
+    if (t != m) return fail(ctx, CKS_EINVAL, "packed_bits %u != popcount(sort_mask) %u", m, t);
+    if (m) CK(cudaMemcpyAsync(ctx->moff.p, ctx->h_moff, (size_t)m * 2, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->plan_ev[1], ctx->stream));
+    CK(cudaMemsetAsync(ctx->dacc.p, 0, (size_t)nwords * 4, ctx->stream));
+    if (n && m) {
+        LAUNCH(launch_adjacent(sorted, n, m, as<uint16_t>(ctx->moff), B, dbit, as<uint32_t>(ctx->dacc),
+                               ctx->sms, ctx->stream));
+    } else if (n && dbit) {
+        LAUNCH(launch_fill_u16(dbit, n, (uint16_t)CKS_DBIT_NONE, ctx->stream));
+    }
+    CK(cudaEventSynchronize(ctx->plan_ev[2]));
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->dacc.p, (size_t)nwords * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (uint32_t j = 0; j < B; j++) mask_out[j] = (uint8_t)(ctx->h_small[j >> 2] >> (24 - 8 * (j & 3)));
+    return CKS_OK;
+}
+
+int tree_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* s) {
+    if (!s || fanout < 2 || !(fill > 0.f) || fill > 1.f) return CKS_EINVAL;
+    uint32_t per = (uint32_t)((double)fanout * (double)fill);
+    if (per < 2) return CKS_EINVAL;
+    memset(s, 0, sizeof(*s));
+    s->n = n;
+    s->fanout = fanout;
+    s->per_node = per;
+    uint64_t c = n, off = 0;
+    uint32_t h = 0;
+    while (c > 0) {
+        c = (c + per - 1) / per;
+        if (h >= CKS_MAX_LEVELS) return CKS_ERANGE;
+        s->level_nodes[h] = c;
+        s->level_offset[h] = off;
+        off += c;
+        h++;
+        if (c <= 1) break;
+    }
+    s->height = h;
+    s->total_nodes = off;
+    s->inner_nodes = h ? off - s->level_nodes[0] : 0;
+    return CKS_OK;
+}
+
+// a8
+int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
+                 float fill, const cks_tree* t, uint32_t* height) {
+    cks_tree_shape s;
+    int rc = tree_shape(n, fanout, fill, &s);
+    if (rc != CKS_OK) return fail(ctx, rc, "bad bulk-load shape (fanout %u, fill %f)", fanout, (double)fill);
+    if (height) *height = s.height;
+    if (n == 0) return CKS_OK;
+    if (!t || !t->node_cnt || !t->entry_rid) return fail(ctx, CKS_EINVAL, "tree arrays are NULL");
+    if (t->entry_dbit && !dbit) return fail(ctx, CKS_EINVAL, "entry_dbit requested without dbit");
+    const uint32_t per = s.per_node;
+    BulkLevel L{};
+    L.entries = n;
+    L.nodes = s.level_nodes[0];
+    L.node_off = 0;
+    L.span = 1;
+    LAUNCH(launch_bulk_leaves(perm, dbit, L, fanout, per, t->node_cnt, t->entry_rid, t->entry_dbit, nullptr,
+                              ctx->stream));
+    if (s.height > 1 && dbit) {
+        TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
+        TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+    }
+    const uint16_t* rbelow = dbit;
+    uint64_t span = per;
+    for (uint32_t l = 1; l < s.height; l++) {
+        BulkLevel I{};
+        I.entries = s.level_nodes[l - 1];
+        I.nodes = s.level_nodes[l];
+        I.node_off = s.level_offset[l];
+        I.below_off = s.level_offset[l - 1];
+        I.span = span;
+        uint16_t* rout = dbit ? ((l & 1) ? as<uint16_t>(ctx->rmin0) : as<uint16_t>(ctx->rmin1)) : nullptr;
+        LAUNCH(launch_bulk_inner(perm, rbelow, I, n, fanout, per, t->node_cnt, t->entry_rid, t->entry_dbit,
+                                 t->entry_child, s.level_offset[1], rout, ctx->stream));
+        rbelow = rout;
+        span *= per;
+    }
+    return CKS_OK;
+}
+
+bool same_mask(const uint8_t* a, const uint8_t* b, uint32_t B) { return memcmp(a, b, B) == 0; }
+
+// Everything after the sort mask is known: a3 .. a8 on device keys.
+int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* M,
+                    uint32_t m, cks_build_out* out, bool check_superset) {
+    const uint32_t np = (m + 31) / 32, k = (m + 7) / 8;
+    out->sort_bits = m;
+    out->passes = k;
+    uint16_t* dbit = out->dbit;
+    if (!dbit && n) {
+        TRY(ensure(ctx, ctx->dbit, n * 2));
+        dbit = as<uint16_t>(ctx->dbit);
+    }
+    // a3: compress into whichever plane buffer the first LSD pass does not write
+    const size_t pbytes = (size_t)np * n * 4;
+    TRY(ensure(ctx, ctx->planeA, pbytes));
+    TRY(ensure(ctx, ctx->planeB, pbytes));
+    uint32_t* cbuf = (((k - 1) & 1) != 0 || k == 0) ? as<uint32_t>(ctx->planeB) : as<uint32_t>(ctx->planeA);
+    if (k == 0) cbuf = as<uint32_t>(ctx->planeB);
+    TRY(run_compress(ctx, keys, n, B, M, cbuf));
+    mark(ctx, ST_COMPRESS);
+    // a4 + a5
+    const uint32_t* sorted = nullptr;
+    TRY(run_sort(ctx, cbuf, np, k, n, nullptr, 0, nullptr, out->perm, &sorted));
+    mark(ctx, ST_SORT);
+    // a6
+    TRY(run_adjacent(ctx, sorted, m, n, M, B, out->mask, dbit));
+    out->popcount = popcount_mask(out->mask, B);
+    for (uint32_t j = 0; j < B; j++)
+        if (out->mask[j] & ~M[j])
+            return fail(ctx, CKS_ERANGE, "adjacency produced a bit outside the sort mask (byte %u)", j);
+    (void)check_superset;
+    mark(ctx, ST_ADJ);
+    // a7: repack P_M -> P_D
+    out->packed = sorted;
+    if (!same_mask(out->mask, M, B) && out->popcount > 0) {
+        std::vector<uint32_t> sub(np, 0);
+        uint32_t t = 0;                                   // compressed index from the MSB
+        for (uint32_t p = 0; p < 8 * B; p++) {
+            if (!((M[p >> 3] >> (7 - (p & 7))) & 1)) continue;
+            uint32_t b = m - 1 - t;                       // bit of P_M
+            if ((out->mask[p >> 3] >> (7 - (p & 7))) & 1) sub[b >> 5] |= 1u << (b & 31);
+            t++;
+        }
+        TRY(claim_slot(ctx, 1));
+        plan_repack(sub.data(), np, ctx->h_plan[1]);
+        GatherPlan* dplan;
+        TRY(upload_plan(ctx, 1, &dplan));
+        uint32_t* dst = (sorted == as<uint32_t>(ctx->planeA)) ? as<uint32_t>(ctx->planeB) : as<uint32_t>(ctx->planeA);
+        LAUNCH(launch_repack(sorted, n, dplan, ctx->h_plan[1]->nsteps, (out->popcount + 31) / 32, dst, ctx->stream));
+        out->packed = dst;
+    } else if (out->popcount == 0) {
+        out->packed = nullptr;
+    }
+    mark(ctx, ST_REPACK);
+    // a8
+    out->height = 0;
+    if (out->tree.node_cnt) {
+        cks_tree tr = out->tree;
+        TRY(run_bulkload(ctx, out->perm, dbit, n, out->fanout, out->fill, &tr, &out->height));
+    }
+    mark(ctx, ST_BULK);
+    return CKS_OK;
+}
+
+int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* prior,
+                 cks_build_out* out, bool keys_ready_for_mask) {
+    std::vector<uint8_t> M(B, 0);
+    uint32_t m = 0;
+    if (prior) {
+        memcpy(M.data(), prior, B);
+        m = popcount_mask(M.data(), B);
+    } else {
+        int kind = out->superset_kind;
+        TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask));
+    }
+    mark(ctx, ST_MASK);
+    return build_from_mask(ctx, keys, n, B, M.data(), m, out, prior != nullptr);
+}
+
+}  // namespace
+
+// ======================================================================================
+extern "C" {
+
+int cks_ctx_create(int device, void* stream, cks_ctx** out) {
+    if (!out) return CKS_EINVAL;
+    *out = nullptr;
+    cks_ctx* ctx = new (std::nothrow) cks_ctx();
+    if (!ctx) return CKS_ENOMEM;
+    ctx->device = device;
+    ctx->stream = (cudaStream_t)stream;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return CKS_ECUDA;
+    }
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    bool ok = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; i < ST_N && ok; i++) ok = cudaEventCreate(&ctx->ev[i]) == cudaSuccess;
+    for (int i = 0; i < 3 && ok; i++) ok = cudaEventCreateWithFlags(&ctx->plan_ev[i], cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < 2 && ok; i++) ok = cudaMallocHost(&ctx->h_plan[i], sizeof(GatherPlan)) == cudaSuccess;
+    if (ok) ok = cudaMallocHost(&ctx->h_moff, kMaxBits * 2) == cudaSuccess;
+    if (ok) ok = cudaMallocHost(&ctx->h_small, 8192) == cudaSuccess;
+    for (int i = 0; i < 3 && ok; i++) ok = cudaEventRecord(ctx->plan_ev[i], ctx->stream) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        cks_ctx_destroy(ctx);
+        return CKS_ECUDA;
+    }
+    *out = ctx;
+    return CKS_OK;
+}
+
+int cks_ctx_destroy(cks_ctx* ctx) {
+    if (!ctx) return CKS_EINVAL;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    DevBuf* bufs[] = {&ctx->occ, &ctx->masks8, &ctx->planeA, &ctx->planeB, &ctx->ridA, &ctx->ridB,
+                      &ctx->hist, &ctx->base, &ctx->status, &ctx->counters, &ctx->dacc, &ctx->moff,
+                      &ctx->dbit, &ctx->rmin0, &ctx->rmin1, &ctx->plan[0], &ctx->plan[1], &ctx->plan[2],
+                      &ctx->keys, &ctx->perm_scratch};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    for (int i = 0; i < ST_N; i++)
+        if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+    for (int i = 0; i < 3; i++)
+        if (ctx->plan_ev[i]) cudaEventDestroy(ctx->plan_ev[i]);
+    for (int i = 0; i < 2; i++)
+        if (ctx->h_plan[i]) cudaFreeHost(ctx->h_plan[i]);
+    if (ctx->h_moff) cudaFreeHost(ctx->h_moff);
+    if (ctx->h_small) cudaFreeHost(ctx->h_small);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+    return CKS_OK;
+}
+
+int cks_ctx_set_stream(cks_ctx* ctx, void* stream) {
+    if (!ctx) return CKS_EINVAL;
+    if ((cudaStream_t)stream != ctx->stream) {
+        // keep the pinned staging guards valid on the new stream
+        cudaStreamSynchronize(ctx->stream);
+        ctx->stream = (cudaStream_t)stream;
+        for (int i = 0; i < 3; i++) cudaEventRecord(ctx->plan_ev[i], ctx->stream);
+    }
+    return CKS_OK;
+}
+
+int cks_ctx_set_timing(cks_ctx* ctx, int enable) {
+    if (!ctx) return CKS_EINVAL;
+    ctx->timing = enable != 0;
+    return CKS_OK;
+}
+
+int cks_ctx_stage_ms(cks_ctx* ctx, float* out, int max) {
+    if (!ctx || !out) return 0;
+    if (!ctx->timed) return 0;
+    cudaEventSynchronize(ctx->ev[ST_BULK]);
+    int k = 0;
+    for (int s = ST_MASK; s < ST_N && k < max; s++) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[s - 1], ctx->ev[s]);
+        out[k++] = ms;
+    }
+    if (k < max) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[ST_BEGIN], ctx->ev[ST_BULK]);
+        out[k++] = ms;
+    }
+    return k;
+}
+
+uint64_t cks_ctx_launches(const cks_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* cks_strerror(int code) {
+    switch (code) {
+        case CKS_OK: return "ok";
+        case CKS_EINVAL: return "invalid argument";
+        case CKS_ERANGE: return "out of range";
+        case CKS_ENOMEM: return "out of device memory";
+        case CKS_ECUDA: return "CUDA error";
+        default: return "unknown error";
+    }
+}
+
+const char* cks_last_error(const cks_ctx* ctx) { return ctx ? ctx->err : "no context"; }
+
+int cks_superset_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, int kind,
+                      uint8_t* mask_out, uint32_t* popcount_out) {
+    TRY(check_keys(ctx, keys, n, B));
+    if (!mask_out) return fail(ctx, CKS_EINVAL, "mask_out is NULL");
+    CK(cudaSetDevice(ctx->device));
+    uint32_t m = 0;
+    TRY(run_superset(ctx, keys, n, B, kind, mask_out, &m));
+    if (popcount_out) *popcount_out = m;
+    return CKS_OK;
+}
+
+int cks_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* mask,
+                 uint32_t* packed_out) {
+    TRY(check_keys(ctx, keys, n, B));
+    if (!mask) return fail(ctx, CKS_EINVAL, "mask is NULL");
+    uint32_t m = popcount_mask(mask, B);
+    if (n && m && !packed_out) return fail(ctx, CKS_EINVAL, "packed_out is NULL");
+    CK(cudaSetDevice(ctx->device));
+    return run_compress(ctx, keys, n, B, mask, packed_out);
+}
+
+int cks_sort(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t n, const uint32_t* row_ids,
+             uint32_t* perm_out, uint32_t* sorted_packed_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
+    if (bits > kMaxBits) return fail(ctx, CKS_EINVAL, "packed_bits %u > %u", bits, kMaxBits);
+    if (n && (!perm_out || (bits && !packed))) return fail(ctx, CKS_EINVAL, "NULL buffer with n > 0");
+    CK(cudaSetDevice(ctx->device));
+    const uint32_t np = (bits + 31) / 32, k = (bits + 7) / 8;
+    TRY(run_sort(ctx, packed, np, k, n, row_ids, 4, sorted_packed_out, perm_out, nullptr));
+    return CKS_OK;
+}
+
+int cks_adjacent_dbits(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bits, uint64_t n,
+                       const uint8_t* sort_mask, uint32_t B, uint8_t* mask_out, uint32_t* popcount_out,
+                       uint16_t* dbit_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (B < 1 || B > CKS_MAX_KEY_BYTES) return fail(ctx, CKS_EINVAL, "key_bytes %u not in [1,512]", B);
+    if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
+    if (n && bits && !sorted_packed) return fail(ctx, CKS_EINVAL, "sorted_packed is NULL");
+    if (!sort_mask || !mask_out) return fail(ctx, CKS_EINVAL, "mask pointer is NULL");
+    CK(cudaSetDevice(ctx->device));
+    TRY(run_adjacent(ctx, sorted_packed, bits, n, sort_mask, B, mask_out, dbit_out));
+    if (popcount_out) *popcount_out = popcount_mask(mask_out, B);
+    return CKS_OK;
+}
+
+int cks_bulkload_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* out) {
+    return tree_shape(n, fanout, fill, out);
+}
+
+int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
+                 float fill, const cks_tree* out) {
+    if (!ctx) return CKS_EINVAL;
+    if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
+    if (n && !perm) return fail(ctx, CKS_EINVAL, "perm is NULL");
+    CK(cudaSetDevice(ctx->device));
+    return run_bulkload(ctx, perm, dbit, n, fanout, fill, out, nullptr);
+}
+
+int cks_distinction_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* prior,
+                         uint8_t* mask_out, uint32_t* popcount_out, uint32_t* perm_out) {
+    TRY(check_keys(ctx, keys, n, B));
+    if (!mask_out) return fail(ctx, CKS_EINVAL, "mask_out is NULL");
+    CK(cudaSetDevice(ctx->device));
+    cks_build_out o;
+    memset(&o, 0, sizeof(o));
+    o.mask = mask_out;
+    o.superset_kind = CKS_SUPERSET_BYTEOCC;
+    o.perm = perm_out;
+    if (!perm_out && n) {                 // the last LSD pass still needs somewhere to put row ids
+        TRY(ensure(ctx, ctx->perm_scratch, n * 4));
+        o.perm = as<uint32_t>(ctx->perm_scratch);
+    }
+    TRY(build_common(ctx, keys, n, B, prior, &o, true));
+    if (popcount_out) *popcount_out = o.popcount;
+    return CKS_OK;
+}
+
+int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* prior,
+              cks_build_out* out) {
+    TRY(check_keys(ctx, keys, n, B));
+    if (!out || !out->mask || (n && !out->perm)) return fail(ctx, CKS_EINVAL, "NULL output");
+    CK(cudaSetDevice(ctx->device));
+    ctx->timed = ctx->timing;
+    mark(ctx, ST_BEGIN);
+    return build_common(ctx, keys, n, B, prior, out, true);
+}
+
+int cks_build_host(cks_ctx* ctx, const uint8_t* host_keys, uint64_t n, uint32_t B, const uint8_t* prior,
+                   cks_build_out* out) {
+    TRY(check_keys(ctx, host_keys, n, B));
+    if (!out || !out->mask || (n && !out->perm)) return fail(ctx, CKS_EINVAL, "NULL output");
+    if (out->dbit || out->tree.node_cnt) return fail(ctx, CKS_EINVAL, "cks_build_host: dbit/tree must be NULL");
+    CK(cudaSetDevice(ctx->device));
+    ctx->timed = ctx->timing;
+    mark(ctx, ST_BEGIN);
+    const size_t bytes = (size_t)n * B;
+    TRY(ensure(ctx, ctx->keys, bytes));
+    const uint8_t* dkeys = as<uint8_t>(ctx->keys);
+    // H2D in chunks on the copy stream; the superset-mask pass of chunk c overlaps the
+    // copy of chunk c+1 (occupancy is order-independent, so partial passes just OR).
+    const bool want_mask = prior == nullptr;
+    if (want_mask) {
+        TRY(ensure(ctx, ctx->occ, (size_t)B * 8 * 4));
+        CK(cudaMemsetAsync(ctx->occ.p, 0, (size_t)B * 8 * 4, ctx->stream));
+    }
+    uint64_t chunk_keys = ((64ull << 20) / B) & ~15ull;
+    if (chunk_keys == 0) chunk_keys = 16;
+    std::vector<cudaEvent_t> evs;
+    for (uint64_t k0 = 0; k0 < n; k0 += chunk_keys) {
+        uint64_t kc = std::min<uint64_t>(chunk_keys, n - k0);
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+        CK(cudaMemcpyAsync((void*)(dkeys + k0 * B), host_keys + k0 * B, kc * B, cudaMemcpyHostToDevice,
+                           ctx->copy_stream));
+        CK(cudaEventRecord(e, ctx->copy_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, e, 0));
+        if (want_mask)
+            LAUNCH(launch_occupancy(dkeys + k0 * B, kc, B, as<uint32_t>(ctx->occ), ctx->sms, ctx->stream));
+    }
+    uint32_t* host_perm = out->perm;
+    cks_build_out o = *out;
+    if (n) {
+        TRY(ensure(ctx, ctx->perm_scratch, n * 4));
+        o.perm = as<uint32_t>(ctx->perm_scratch);
+    }
+    int rc = build_common(ctx, dkeys, n, B, prior, &o, /*keys_ready_for_mask=*/false);
+    if (rc == CKS_OK && n) {
+        cudaError_t e = cudaMemcpyAsync(host_perm, o.perm, n * 4, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e != cudaSuccess) rc = fail(ctx, CKS_ECUDA, "D2H perm: %s", cudaGetErrorString(e));
+    }
+    cudaError_t se = cudaStreamSynchronize(ctx->stream);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    if (rc == CKS_OK && se != cudaSuccess) rc = fail(ctx, CKS_ECUDA, "sync: %s", cudaGetErrorString(se));
+    if (rc != CKS_OK) return rc;
+    o.perm = host_perm;
+    *out = o;
+    return CKS_OK;
+}
+
+}  // extern "C"

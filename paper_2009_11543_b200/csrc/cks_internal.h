@@ -1,0 +1,95 @@
+// cks_internal.h -- shared declarations of the libcks kernels and the host layer.
+// Not part of the public ABI (that is include/cks.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define CKS_NONE_INTERNAL 0xFFFFu
+
+namespace cks {
+
+constexpr uint32_t kMaxKeyBytes = 512;
+constexpr uint32_t kMaxBits = 8 * kMaxKeyBytes;
+constexpr uint32_t kMaxWords = kMaxKeyBytes / 4;        // 32-bit words per key
+constexpr uint32_t kMaxPlanes = kMaxBits / 32;          // u32 planes of a packed key
+constexpr int kSortThreads = 256;                       // one thread per 8-bit digit value
+constexpr int kRadix = 256;
+
+// One step of the word-level bit gather (Sec. 5.1 PEXT, done in software):
+// the bits of source word `src` selected by `mask` are moved to the low end of the
+// word with five masked shifts (mv[s] selects the bits that move right by 2^s; the
+// classic parallel-suffix compress), giving `cnt` bits. Steps are listed from the
+// least significant end of P upward, so a thread just appends `cnt` bits each step.
+struct GatherStep {
+    uint32_t src;      // compress: 32-bit big-endian word index in the key; repack: plane index
+    uint32_t mask;
+    uint32_t mv[5];
+    uint32_t cnt;
+};
+
+struct GatherPlan {
+    uint32_t nsteps;
+    uint32_t out_bits;     // total bits = sum cnt
+    GatherStep step[kMaxWords > kMaxPlanes ? kMaxWords : kMaxPlanes];
+};
+
+// Host-side planning (cks_plan.cpp).
+void plan_compress(const uint8_t* mask, uint32_t key_bytes, GatherPlan* plan);
+void plan_repack(const uint32_t* sub_words /* u32[np_in], bit b of word q = P_M bit 32q+b kept */,
+                 uint32_t np_in, GatherPlan* plan);
+
+// ---- kernel launchers (stream-ordered, return cudaGetLastError) ------------------
+cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32_t* occ,
+                             int sms, cudaStream_t st);
+cudaError_t launch_occ_finalize(const uint32_t* occ, uint32_t B, uint64_t n, uint8_t* dplus,
+                                uint8_t* variant, cudaStream_t st);
+cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
+                            uint32_t nsteps, uint32_t out_planes, uint32_t* planes, cudaStream_t st);
+cudaError_t launch_repack(const uint32_t* in_planes, uint64_t n, const GatherPlan* dplan,
+                          uint32_t nsteps, uint32_t out_planes, uint32_t* out, cudaStream_t st);
+// histograms of all LSD digits: digit p = bits [8p, 8p+8) of P (p < key_passes) followed
+// by, if rid != NULL, the row-id digits (rid_passes of them) at indices key_passes+.
+cudaError_t launch_hist(const uint32_t* planes, uint64_t n, uint32_t key_passes,
+                        const uint32_t* rid, uint32_t rid_passes, uint32_t* hist, int sms,
+                        cudaStream_t st);
+cudaError_t launch_scan(const uint32_t* hist, uint32_t passes, uint32_t* base, cudaStream_t st);
+
+struct OnesweepArgs {
+    const uint32_t* in_planes;   // plane q at in_planes + q*n
+    uint32_t* out_planes;
+    const uint32_t* in_rid;      // NULL = implicit row id (input index)
+    uint32_t* out_rid;
+    uint64_t n;
+    uint32_t nplanes;            // planes carried
+    int32_t digit_plane;         // plane holding the digit; -1 = digit taken from the row id
+    uint32_t shift;              // digit = (word >> shift) & 0xFF
+    const uint32_t* bucket_base; // u32[256] global exclusive bases of this pass
+    uint32_t* tile_counter;      // zeroed before the pass
+    unsigned long long* status;  // u64[num_tiles][256] look-back words
+    uint32_t epoch;              // flag namespace of this pass
+};
+cudaError_t launch_onesweep(const OnesweepArgs& a, cudaStream_t st);
+uint64_t onesweep_tiles(uint64_t n);
+
+cudaError_t launch_adjacent(const uint32_t* planes, uint64_t n, uint32_t m, const uint16_t* moff,
+                            uint32_t B, uint16_t* dbit_out, uint32_t* dacc /* u32[ceil(8B/32)] */,
+                            int sms, cudaStream_t st);
+cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
+cudaError_t launch_fill_u16(uint16_t* out, uint64_t n, uint16_t v, cudaStream_t st);
+
+struct BulkLevel {
+    uint64_t entries;      // entries at this level (= n for leaves, nodes below otherwise)
+    uint64_t nodes;
+    uint64_t node_off;     // global node index of the first node of the level
+    uint64_t below_off;    // global node index of the first node of the level below
+    uint64_t span;         // sorted keys covered per entry
+};
+cudaError_t launch_bulk_leaves(const uint32_t* perm, const uint16_t* dbit, const BulkLevel& L,
+                               uint32_t fanout, uint32_t per, uint32_t* node_cnt, uint32_t* rid,
+                               uint16_t* edbit, uint16_t* rmin, cudaStream_t st);
+cudaError_t launch_bulk_inner(const uint32_t* perm, const uint16_t* rmin_below, const BulkLevel& L,
+                              uint64_t n, uint32_t fanout, uint32_t per, uint32_t* node_cnt,
+                              uint32_t* rid, uint16_t* edbit, uint32_t* child, uint64_t inner_off,
+                              uint16_t* rmin, cudaStream_t st);
+
+}  // namespace cks

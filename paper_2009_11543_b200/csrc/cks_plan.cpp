@@ -1,0 +1,57 @@
+// cks_plan.cpp -- host-side planning of the bit gather (a2).
+//
+// For each 32-bit source word with a non-zero selection mask we precompute the five
+// "move" masks of the parallel-suffix compress: at step k the selected bits that still
+// have an odd number of unselected positions (in units of 2^k) below them move right by
+// 2^k. Applying the five steps to (x & mask) leaves the selected bits, in order, in the
+// low popcount(mask) bits -- what PEXT does in hardware.
+#include <string.h>
+
+#include "cks_internal.h"
+
+namespace cks {
+
+static void move_masks(uint32_t m, uint32_t mv[5]) {
+    uint32_t mk = ~m << 1;                 // count unselected positions to the right
+    for (int k = 0; k < 5; k++) {
+        uint32_t mp = mk ^ (mk << 1);      // parallel suffix (prefix-from-the-right) parity
+        mp ^= mp << 2;
+        mp ^= mp << 4;
+        mp ^= mp << 8;
+        mp ^= mp << 16;
+        uint32_t v = mp & m;               // bits that move by 2^k at this step
+        mv[k] = v;
+        m = (m ^ v) | (v >> (1u << k));
+        mk &= ~mp;
+    }
+}
+
+static void add_step(GatherPlan* plan, uint32_t src, uint32_t mask) {
+    GatherStep& s = plan->step[plan->nsteps++];
+    s.src = src;
+    s.mask = mask;
+    move_masks(mask, s.mv);
+    s.cnt = (uint32_t)__builtin_popcount(mask);
+    plan->out_bits += s.cnt;
+}
+
+void plan_compress(const uint8_t* mask, uint32_t B, GatherPlan* plan) {
+    memset(plan, 0, sizeof(GatherPlan));
+    uint32_t words = (B + 3) / 4;
+    for (int w = (int)words - 1; w >= 0; w--) {           // least significant end of P first
+        uint32_t mw = 0;
+        for (uint32_t b = 0; b < 4; b++) {
+            uint32_t j = (uint32_t)w * 4 + b;
+            mw = (mw << 8) | (j < B ? mask[j] : 0u);
+        }
+        if (mw) add_step(plan, (uint32_t)w, mw);
+    }
+}
+
+void plan_repack(const uint32_t* sub_words, uint32_t np_in, GatherPlan* plan) {
+    memset(plan, 0, sizeof(GatherPlan));
+    for (uint32_t q = 0; q < np_in; q++)
+        if (sub_words[q]) add_step(plan, q, sub_words[q]);
+}
+
+}  // namespace cks

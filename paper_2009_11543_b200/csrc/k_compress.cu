@@ -1,0 +1,192 @@
+// k_compress.cu -- a3: Compress(key) = the key's bits at the mask positions,
+// concatenated in position order (extraction pipeline Sec. 5.1),
+// and a7: repack of sorted P_M to P_D.
+//
+// The paper extracts with x86 PEXT on 8-byte mask segments. There is no
+// PEXT on the GPU; each 32-bit big-endian key word with a non-zero mask word is
+// compressed in registers with five masked shifts (parallel-suffix compress; move
+// masks precomputed on the host per word), and the fields are appended from the least
+// significant end of P upward, emitting a u32 plane whenever 32 bits are complete.
+//
+// Layout: keys u8[n][B] -> planes u32[np][n] (plane q = bits [32q, 32q+32) of P).
+// Keys are staged through shared memory with coalesced 16-byte loads; each row is
+// padded to an odd number of 16-byte units so a thread's 16-byte reads of its own row
+// are bank-conflict free (8 lanes per phase hit 8 distinct 16-byte bank groups).
+#include "cks_internal.h"
+
+namespace cks {
+
+__device__ __forceinline__ int4 ld_stream16c(const void* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+__device__ __forceinline__ uint32_t gather_word(uint32_t x, const GatherStep& s) {
+    x &= s.mask;
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+        uint32_t t = x & s.mv[k];
+        x = (x ^ t) | (t >> (1u << k));
+    }
+    return x;
+}
+
+constexpr int kCompressThreads = 256;
+
+// B % 16 == 0 and keys 16-byte aligned: shared-memory staged tile of 256 keys.
+__global__ void __launch_bounds__(kCompressThreads)
+k_compress_tiled(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
+                 const GatherPlan* __restrict__ plan, uint32_t nsteps, uint32_t np,
+                 uint32_t* __restrict__ planes) {
+    extern __shared__ int4 s_tile[];                      // [256][S16] int4 units
+    __shared__ GatherStep s_step[kMaxWords];
+    for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
+    const uint32_t U = B >> 4;                            // 16-byte units per key
+    const uint32_t S16 = U | 1;                           // odd row stride (units)
+    const uint64_t ntiles = (n + kCompressThreads - 1) / kCompressThreads;
+    __syncthreads();
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t k0 = tile * kCompressThreads;
+        const uint32_t tk = (uint32_t)(n - k0 < (uint64_t)kCompressThreads ? n - k0 : (uint64_t)kCompressThreads);
+        const int4* src = reinterpret_cast<const int4*>(keys + k0 * B);
+        const uint32_t units = tk * U;
+        for (uint32_t c = threadIdx.x; c < units; c += kCompressThreads) {
+            uint32_t r = c / U, u = c - r * U;
+            s_tile[r * S16 + u] = ld_stream16c(src + c);
+        }
+        __syncthreads();
+        if (threadIdx.x < tk) {
+            const int4* row = s_tile + threadIdx.x * S16;
+            const uint64_t i = k0 + threadIdx.x;
+            unsigned long long acc = 0;
+            uint32_t accbits = 0, q = 0;
+            int cur_u = -1;
+            int4 cur = make_int4(0, 0, 0, 0);
+            for (uint32_t s = 0; s < nsteps; s++) {
+                const GatherStep& g = s_step[s];
+                int u = (int)(g.src >> 2);
+                if (u != cur_u) { cur = row[u]; cur_u = u; }
+                uint32_t sel = g.src & 3;
+                uint32_t w = sel == 0 ? (uint32_t)cur.x : sel == 1 ? (uint32_t)cur.y
+                           : sel == 2 ? (uint32_t)cur.z : (uint32_t)cur.w;
+                uint32_t x = gather_word(bswap32(w), g);
+                acc |= (unsigned long long)x << accbits;
+                accbits += g.cnt;
+                if (accbits >= 32) {
+                    planes[(uint64_t)q * n + i] = (uint32_t)acc;
+                    acc >>= 32;
+                    accbits -= 32;
+                    q++;
+                }
+            }
+            if (accbits) planes[(uint64_t)q * n + i] = (uint32_t)acc;
+        }
+        __syncthreads();
+    }
+}
+
+// Generic path: any B (word assembled from bytes, zero beyond B), any alignment.
+__global__ void __launch_bounds__(kCompressThreads)
+k_compress_generic(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
+                   const GatherPlan* __restrict__ plan, uint32_t nsteps, uint32_t np,
+                   uint32_t* __restrict__ planes) {
+    __shared__ GatherStep s_step[kMaxWords];
+    for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint8_t* k = keys + i * B;
+        unsigned long long acc = 0;
+        uint32_t accbits = 0, q = 0;
+        for (uint32_t s = 0; s < nsteps; s++) {
+            const GatherStep& g = s_step[s];
+            uint32_t w = 0;
+            for (uint32_t b = 0; b < 4; b++) {
+                uint32_t j = g.src * 4 + b;
+                w = (w << 8) | (j < B ? k[j] : 0u);
+            }
+            uint32_t x = gather_word(w, g);
+            acc |= (unsigned long long)x << accbits;
+            accbits += g.cnt;
+            if (accbits >= 32) {
+                planes[(uint64_t)q * n + i] = (uint32_t)acc;
+                acc >>= 32;
+                accbits -= 32;
+                q++;
+            }
+        }
+        if (accbits) planes[(uint64_t)q * n + i] = (uint32_t)acc;
+    }
+}
+
+// a7 repack: source words are the planes of P_M (plane 0 least significant), each
+// gathered by the sub-mask of P_M bits that are exact-D positions.
+__global__ void __launch_bounds__(kCompressThreads)
+k_repack(const uint32_t* __restrict__ in, uint64_t n, const GatherPlan* __restrict__ plan,
+         uint32_t nsteps, uint32_t np, uint32_t* __restrict__ out) {
+    __shared__ GatherStep s_step[kMaxPlanes];
+    for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        unsigned long long acc = 0;
+        uint32_t accbits = 0, q = 0;
+        for (uint32_t s = 0; s < nsteps; s++) {
+            const GatherStep& g = s_step[s];
+            uint32_t x = gather_word(in[(uint64_t)g.src * n + i], g);
+            acc |= (unsigned long long)x << accbits;
+            accbits += g.cnt;
+            if (accbits >= 32) {
+                out[(uint64_t)q * n + i] = (uint32_t)acc;
+                acc >>= 32;
+                accbits -= 32;
+                q++;
+            }
+        }
+        if (accbits) out[(uint64_t)q * n + i] = (uint32_t)acc;
+    }
+}
+
+static int grid_for(uint64_t work, int per_sm, int sms) {
+    uint64_t want = (work + 255) / 256;
+    uint64_t cap = (uint64_t)sms * per_sm;
+    if (want == 0) want = 1;
+    return (int)(want < cap ? want : cap);
+}
+
+cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
+                            uint32_t nsteps, uint32_t np, uint32_t* planes, cudaStream_t st) {
+    if (n == 0 || np == 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if ((B & 15) == 0 && ((uintptr_t)keys & 15) == 0) {
+        uint32_t S16 = (B >> 4) | 1;
+        size_t smem = (size_t)kCompressThreads * S16 * 16;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_compress_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = smem <= 24 * 1024 ? 8 : smem <= 48 * 1024 ? 4 : smem <= 100 * 1024 ? 2 : 1;
+        k_compress_tiled<<<grid_for(n, per_sm, sms), kCompressThreads, smem, st>>>(keys, n, B, dplan,
+                                                                                   nsteps, np, planes);
+    } else {
+        k_compress_generic<<<grid_for(n, 8, sms), kCompressThreads, 0, st>>>(keys, n, B, dplan, nsteps,
+                                                                             np, planes);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_repack(const uint32_t* in, uint64_t n, const GatherPlan* dplan, uint32_t nsteps,
+                          uint32_t np, uint32_t* out, cudaStream_t st) {
+    if (n == 0 || np == 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_repack<<<grid_for(n, 8, sms), kCompressThreads, 0, st>>>(in, n, dplan, nsteps, np, out);
+    return cudaGetLastError();
+}
+
+}  // namespace cks

@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path (through the C ABI via the ctypes binding) against the CPU
+oracle, element by element, bit-exact (integer work: no tolerance). Sizes span several
+4096-key sort tiles plus a ragged tail; edge cases cover empty, single, all-equal and
+degenerate masks; full-size configs are checked on properties that pin the result
+uniquely (the (key, row id) order is total, so a valid sorted permutation is THE oracle
+permutation) plus sampled oracle values."""
+import numpy as np
+import pytest
+
+import cksgen
+import oracle
+from conftest import mask_from, positions
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():                       # collected on CPU, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2009_11543_b200 import cks  # noqa: E402
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def u16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def planes_dev(planes):
+    return dev(np.ascontiguousarray(planes).view(np.int32))
+
+
+RAGGED = [0, 1, 2, 3, 31, 4095, 4096, 4097, 100_003]
+
+
+# ---- a1: superset masks --------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_superset_masks_configs(cfg):
+    keys = cksgen.config(cfg, n=150_001)
+    d = dev(keys)
+    assert np.array_equal(cks.superset_mask(d, cks.SUPERSET_BYTEOCC), oracle.byteocc_superset(keys))
+    assert np.array_equal(cks.superset_mask(d, cks.SUPERSET_VARIANT), oracle.variant_bitmap(keys))
+
+
+@pytest.mark.parametrize("B", [1, 2, 3, 5, 8, 12, 16, 24, 48, 64, 100, 512])
+@pytest.mark.parametrize("n", [0, 1, 7, 5000])
+def test_superset_masks_shapes(B, n):
+    keys = cksgen.lowcard(n, B, seed=B * 7 + n, values=5)
+    d = dev(keys)
+    assert np.array_equal(cks.superset_mask(d, cks.SUPERSET_BYTEOCC), oracle.byteocc_superset(keys))
+    assert np.array_equal(cks.superset_mask(d, cks.SUPERSET_VARIANT), oracle.variant_bitmap(keys))
+
+
+def test_superset_mask_unaligned_keys():
+    keys = cksgen.uniform(3001, 16, seed=3)
+    big = torch.zeros(3001 * 16 + 16, dtype=torch.uint8, device="cuda")
+    view = big[5:5 + 3001 * 16].view(3001, 16)           # 5-byte offset: generic path
+    view.copy_(dev(keys))
+    assert np.array_equal(cks.superset_mask(view), oracle.byteocc_superset(keys))
+
+
+# ---- a3: compress ---------------------------------------------------------------------
+
+@pytest.mark.parametrize("B", [1, 3, 8, 16, 32, 35, 64, 128])
+def test_compress_random_masks(B):
+    rng = np.random.default_rng(B)
+    keys = cksgen.uniform(20_011, B, seed=B)
+    d = dev(keys)
+    for density in (0.02, 0.3, 1.0):
+        mask = np.packbits(rng.random(8 * B) < density)
+        got = u32(cks.compress(d, mask))
+        assert np.array_equal(got, oracle.compress(keys, mask))
+
+
+def test_compress_table3_mask():
+    from conftest import load_bit_rows
+    m = load_bit_rows("table3_indbtab_dbitmap.txt")
+    keys = cksgen.uniform(9000, 35, seed=35)
+    assert np.array_equal(u32(cks.compress(dev(keys), m)), oracle.compress(keys, m))
+
+
+# ---- a5: sort -------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", RAGGED)
+@pytest.mark.parametrize("bits", [1, 8, 23, 32, 33, 96, 150])
+def test_sort_vs_oracle(n, bits):
+    rng = np.random.default_rng(n + bits)
+    np_ = (bits + 31) // 32
+    planes = rng.integers(0, 2 ** 32, size=(np_, n), dtype=np.uint64).astype(np.uint32)
+    if np_:
+        top = bits - 32 * (np_ - 1)
+        planes[-1] &= np.uint32((1 << top) - 1) if top < 32 else np.uint32(0xFFFFFFFF)
+        if n > 10:                                            # duplicates
+            planes[:, n // 2:] = planes[:, : n - n // 2]
+    perm, srt = cks.sort(planes_dev(planes), bits, want_sorted=True)
+    ref = oracle.sort_packed(planes)
+    assert np.array_equal(u32(perm), ref)
+    if n:
+        assert np.array_equal(u32(srt), planes[:, ref])
+
+
+@pytest.mark.parametrize("n", [5, 4097, 60_000])
+def test_sort_with_user_row_ids(n):
+    rng = np.random.default_rng(n)
+    planes = (rng.integers(0, 64, size=(1, n))).astype(np.uint32)            # many ties
+    rid = rng.permutation(np.arange(10, 10 + n, dtype=np.uint32))
+    perm, _ = cks.sort(planes_dev(planes), 6, row_ids=dev(rid.view(np.int32)))
+    assert np.array_equal(u32(perm), oracle.sort_packed(planes, rid=rid))
+
+
+def test_sort_skewed_digits():
+    n = 200_000
+    planes = np.zeros((2, n), np.uint32)
+    planes[0, ::1000] = 7                                      # one digit value dominates
+    perm, _ = cks.sort(planes_dev(planes), 40)
+    assert np.array_equal(u32(perm), oracle.sort_packed(planes))
+
+
+# ---- a6: adjacency ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", [1, 3, 4, 5])
+def test_adjacent_dbits_vs_oracle(cfg):
+    keys = cksgen.config(cfg, n=30_000)
+    sup = oracle.byteocc_superset(keys)
+    m = oracle.popcount(sup)
+    planes = oracle.compress(keys, sup)
+    sp = planes[:, oracle.sort_packed(planes)]
+    mask, dbit = cks.adjacent_dbits(planes_dev(sp), m, sup)
+    rd, rm = oracle.adjacent_compressed(sp, m, sup)
+    assert np.array_equal(mask, rm)
+    assert np.array_equal(u16(dbit), rd)
+
+
+# ---- a8: bulk load -----------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,fanout,fill", [(1, 64, 1.0), (64, 64, 1.0), (65, 64, 1.0), (4097, 64, 1.0),
+                                           (300_000, 64, 1.0), (50_000, 14, 0.9), (20_000, 9, 0.9),
+                                           (1000, 2, 1.0)])
+def test_bulkload_vs_oracle(n, fanout, fill):
+    keys = cksgen.config(5, n=n)
+    perm = oracle.sort_keys(keys)
+    dbit, _ = oracle.adjacent_dbits(keys, perm)
+    t = cks.bulkload(dev(perm.view(np.int32)), dev(dbit.view(np.int16)), fanout, fill)
+    ref = oracle.bulkload(perm, dbit, keys, fanout, fill)
+    T = int(t["shape"].total_nodes)
+    L0 = int(t["shape"].level_nodes[0])
+    assert t["shape"].height == ref["height"]
+    assert np.array_equal(u32(t["node_cnt"])[:T], ref["node_cnt"])
+    assert np.array_equal(u32(t["entry_rid"])[:T * fanout], ref["entry_rid"].ravel())
+    assert np.array_equal(u16(t["entry_dbit"])[:T * fanout], ref["entry_dbit"].ravel())
+    assert np.array_equal(u32(t["entry_child"])[:(T - L0) * fanout], ref["entry_child"][L0:].ravel())
+
+
+# ---- exact D and the fused build -----------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_distinction_mask_vs_oracle(cfg):
+    keys = cksgen.config(cfg, n=100_003)
+    mask, perm = cks.distinction_mask(dev(keys))
+    permK = oracle.sort_keys(keys, threads=oracle.threads_default())
+    _, D = oracle.adjacent_dbits(keys, permK)
+    assert np.array_equal(mask, D)
+    assert np.array_equal(u32(perm), permK)
+
+
+def check_build(keys, r, threads=None):
+    ref = oracle.first_build(keys, threads=threads or oracle.threads_default())
+    assert np.array_equal(r["mask"], ref["mask"])
+    assert r["popcount"] == ref["m"]
+    assert np.array_equal(u32(r["perm"]), ref["perm"])
+    assert np.array_equal(ref["perm_packed"], ref["perm"])         # Theorem 2 on the oracle side
+    assert np.array_equal(u16(r["dbit"]), ref["dbit"])
+    n = keys.shape[0]
+    if n:
+        assert np.array_equal(u32(r["packed"]), ref["planes"][:, ref["perm"]])
+    if r["tree"] is not None and n:
+        t = oracle.bulkload(ref["perm"], ref["dbit"], keys, int(r["shape"].fanout),
+                            float(r["shape"].per_node) / float(r["shape"].fanout))
+        T, f = int(r["shape"].total_nodes), int(r["shape"].fanout)
+        assert np.array_equal(u32(r["tree"]["entry_rid"])[:T * f], t["entry_rid"].ravel())
+        assert np.array_equal(u16(r["tree"]["entry_dbit"])[:T * f], t["entry_dbit"].ravel())
+        assert np.array_equal(u32(r["tree"]["node_cnt"])[:T], t["node_cnt"])
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_build_configs_vs_oracle(cfg):
+    keys = cksgen.config(cfg, n=200_003 if cfg > 1 else None)
+    r = cks.build(dev(keys))
+    check_build(keys, r)
+    if cfg == 5:
+        assert r["sort_bits"] == r["popcount"]                   # ACGT: D+ == D, no repack
+
+
+@pytest.mark.parametrize("kind", [cks.SUPERSET_VARIANT, cks.SUPERSET_BYTEOCC])
+def test_build_superset_kinds(kind):
+    keys = cksgen.config(3, n=50_000)
+    check_build(keys, cks.build(dev(keys), superset_kind=kind))
+
+
+def test_rebuild_with_prior_mask():
+    # rebuild: extract by the current D-bitmap (here the exact D plus stale bits,
+    # as after deletes P:402), sort, recompute -> new D is a subset of the old one
+    keys = cksgen.config(4, n=80_000)
+    ref = oracle.first_build(keys)
+    rng = np.random.default_rng(1)
+    stale = ref["mask"] | np.packbits(rng.random(8 * 64) < 0.1)
+    r = cks.build(dev(keys), prior_mask=stale)
+    assert positions(r["mask"]) <= positions(stale)
+    check_build(keys, r)
+    # after deletions the old D stays a valid (extended) mask
+    sub = keys[::3].copy()
+    r2 = cks.build(dev(sub), prior_mask=ref["mask"])
+    check_build(sub, r2)
+
+
+@pytest.mark.parametrize("maker", ["empty", "one", "two_equal", "two", "all_equal", "all16", "consecutive",
+                                   "prefix_heavy", "B1", "B3", "B512"])
+def test_build_edge_cases(maker):
+    keys = {
+        "empty": lambda: np.zeros((0, 16), np.uint8),
+        "one": lambda: cksgen.uniform(1, 16, seed=1),
+        "two_equal": lambda: cksgen.all_equal(2, 8, seed=2),
+        "two": lambda: cksgen.uniform(2, 8, seed=3),
+        "all_equal": lambda: cksgen.all_equal(10_000, 32, seed=4),
+        "all16": lambda: cksgen.consecutive(1 << 16, 2, shuffle_seed=5),
+        "consecutive": lambda: cksgen.consecutive(70_000, 8, start=12345, shuffle_seed=6),
+        "prefix_heavy": lambda: cksgen.prefix_heavy(50_000, 64, seed=7),
+        "B1": lambda: cksgen.uniform(3000, 1, seed=8),
+        "B3": lambda: cksgen.uniform(9000, 3, seed=9, dup_ppm=50_000),
+        "B512": lambda: cksgen.lowcard(3000, 512, seed=10, values=3),
+    }[maker]()
+    r = cks.build(dev(keys) if keys.shape[0] else torch.zeros((0, keys.shape[1]), dtype=torch.uint8,
+                                                               device="cuda"))
+    check_build(keys, r)
+    if maker == "all16":
+        assert positions(r["mask"]) == set(range(16))
+    if maker in ("all_equal", "two_equal", "one", "empty"):
+        assert r["popcount"] == 0
+
+
+def test_build_host_e2e_path():
+    keys = cksgen.config(5, n=300_007)
+    r = cks.build_host(keys)
+    ref = oracle.first_build(keys, threads=oracle.threads_default())
+    assert np.array_equal(r["mask"], ref["mask"])
+    assert np.array_equal(r["perm"], ref["perm"])
+
+
+def test_build_repeatable_and_stream():
+    keys = dev(cksgen.config(2, n=123_457))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        a = cks.build(keys)
+        b = cks.build(keys)
+    s.synchronize()
+    assert np.array_equal(u32(a["perm"]), u32(b["perm"]))
+    assert np.array_equal(a["mask"], b["mask"])
+
+
+# ---- full-size configs (the launch configuration bench.py times) ----------------------------
+
+def verify_sorted_perm(keys, perm):
+    n, B = keys.shape
+    assert perm.shape == (n,)
+    assert np.bincount(perm, minlength=n).max() == 1 if n else True
+    s = keys[perm]
+    W = (B + 7) // 8
+    pad = np.zeros((n, 8 * W), np.uint8)
+    pad[:, :B] = s
+    w = pad.view(">u8")
+    lt = np.zeros(n - 1, bool)
+    eq = np.ones(n - 1, bool)
+    for j in range(W):
+        a, b = w[:-1, j], w[1:, j]
+        lt |= eq & (a < b)
+        eq &= a == b
+    assert np.all(lt | (eq & (perm[:-1] < perm[1:]))), "GPU permutation is not the (key, row id) order"
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_full_size_config(cfg):
+    keys = cksgen.config(cfg)
+    d = dev(keys)
+    b = cks.Builder(keys.shape[0], keys.shape[1], d.device)
+    b(d)
+    perm = u32(b.perm)
+    verify_sorted_perm(keys, perm)                       # unique total order => == oracle perm
+    dbit_ref, D = oracle.adjacent_dbits(keys, perm)      # P:176 on the verified order
+    assert np.array_equal(b.mask, D)
+    assert np.array_equal(u16(b.dbit), dbit_ref)
+    assert np.array_equal(b.mask & ~oracle.byteocc_superset(keys), np.zeros_like(b.mask))
+    rng = np.random.default_rng(cfg)
+    idx = np.sort(rng.choice(keys.shape[0], 20_000, replace=False))
+    packed = u32(b.packed())
+    assert np.array_equal(packed[:, idx], oracle.compress(keys[perm[idx]], b.mask))
+    T = int(b.shape.total_nodes)
+    rid = u32(b.tree["entry_rid"])[:T * 64]
+    assert np.array_equal(rid[:keys.shape[0]], perm)          # fill 1.0: leaf slots in order == perm
