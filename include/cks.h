@@ -74,8 +74,9 @@ int cks_ctx_destroy(cks_ctx* ctx);
 int cks_ctx_set_stream(cks_ctx* ctx, void* stream);
 /* 1 = record per-stage CUDA events in cks_build (read with cks_ctx_stage_ms). */
 int cks_ctx_set_timing(cks_ctx* ctx, int enable);
-/* Stage times (ms) of the last timed cks_build: a1 mask, a3 compress+hist, a5 sort,
- * a6 adjacency, a7 repack, a8 bulk load, total. Synchronises. Returns count written. */
+/* Stage times (ms) of the last timed cks_build: a1 mask, a3 compress, a4 histograms+scan,
+ * a5 LSD passes, a6 adjacency, a7 repack, a8 bulk load, total. Synchronises. Returns the
+ * count written (0 if timing was off). */
 int cks_ctx_stage_ms(cks_ctx* ctx, float* out, int max);
 /* Number of kernels libcks launched since the context was created. */
 uint64_t cks_ctx_launches(const cks_ctx* ctx);

@@ -303,7 +303,7 @@ def cudart_copy(dst: torch.Tensor, src_ptr: int, nbytes: int):
     """Device-to-device copy from a raw pointer on the current stream (via torch)."""
     # wrap the raw pointer as a tensor view using the CUDA array interface
     class _View:
-        __cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<i4", "data": (src_ptr, True),
+        __cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<i4", "data": (src_ptr, False),
                                     "version": 3, "strides": None, "stream": None}
     src = torch.as_tensor(_View(), device=dst.device)
     dst.view(-1).copy_(src)

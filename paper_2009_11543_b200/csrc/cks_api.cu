@@ -21,7 +21,7 @@ struct DevBuf {
     size_t cap = 0;
 };
 
-enum Stage { ST_BEGIN = 0, ST_MASK, ST_COMPRESS, ST_SORT, ST_ADJ, ST_REPACK, ST_BULK, ST_N };
+enum Stage { ST_BEGIN = 0, ST_MASK, ST_COMPRESS, ST_HIST, ST_SORT, ST_ADJ, ST_REPACK, ST_BULK, ST_N };
 
 }  // namespace
 
@@ -206,6 +206,7 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint32_t np, uint32_t key_
                        ctx->stream));
     ctx->launches += (P + 31) / 32 - 1;                  // launch_hist runs one kernel per 32 passes
     LAUNCH(launch_scan(as<uint32_t>(ctx->hist), P, as<uint32_t>(ctx->base), ctx->stream));
+    mark(ctx, ST_HIST);
 
     const uint32_t* cur_p = in_planes;
     const uint32_t* cur_r = in_rid;
