@@ -185,7 +185,8 @@ typedef struct {
     uint32_t sort_bits;       /* |M|, the width the sort ran on */
     uint32_t height;          /* tree height (0 if skipped) */
     uint32_t passes;          /* LSD digit passes run */
-    const uint32_t* packed;   /* VIEW (ctx-owned): sorted P_D planes u32[ceil(|D|/32)][n] */
+    const uint32_t* packed;   /* VIEW (ctx-owned): sorted P_D planes; plane q at packed + q*packed_pitch */
+    uint64_t packed_pitch;    /* plane stride of `packed` in u32 elements (>= n, padded for alignment) */
 } cks_build_out;
 
 /* keys: device u8[n][key_bytes]; prior_mask: host u8[key_bytes] superset or NULL.

@@ -51,7 +51,7 @@ class BuildOut(ctypes.Structure):
                 ("tree", Tree), ("fanout", ctypes.c_uint32), ("fill", ctypes.c_float),
                 ("superset_kind", ctypes.c_int), ("popcount", ctypes.c_uint32),
                 ("sort_bits", ctypes.c_uint32), ("height", ctypes.c_uint32), ("passes", ctypes.c_uint32),
-                ("packed", ctypes.c_void_p)]
+                ("packed", ctypes.c_void_p), ("packed_pitch", ctypes.c_uint64)]
 
 
 EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing",
@@ -293,20 +293,17 @@ class Builder:
         npd = nplanes(int(self.out.popcount))
         if npd == 0 or self.n == 0:
             return torch.empty((0, self.n), dtype=torch.int32, device=self.perm.device)
-        from_ptr = int(self.out.packed)
-        out = torch.empty((npd, self.n), dtype=torch.int32, device=self.perm.device)
-        cudart_copy(out, from_ptr, npd * self.n * 4)
-        return out
+        pitch = int(self.out.packed_pitch)
+        src = raw_view(int(self.out.packed), npd * pitch, self.perm.device).view(npd, pitch)
+        return src[:, :self.n].clone()
 
 
-def cudart_copy(dst: torch.Tensor, src_ptr: int, nbytes: int):
-    """Device-to-device copy from a raw pointer on the current stream (via torch)."""
-    # wrap the raw pointer as a tensor view using the CUDA array interface
+def raw_view(ptr: int, numel: int, device) -> torch.Tensor:
+    """int32 tensor view of library-owned device memory (valid until the next call)."""
     class _View:
-        __cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<i4", "data": (src_ptr, False),
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": "<i4", "data": (ptr, False),
                                     "version": 3, "strides": None, "stream": None}
-    src = torch.as_tensor(_View(), device=dst.device)
-    dst.view(-1).copy_(src)
+    return torch.as_tensor(_View(), device=device)
 
 
 def build(keys: torch.Tensor, prior_mask=None, fanout: int = 64, fill: float = 1.0,

@@ -156,42 +156,52 @@ int run_superset(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, int 
     return CKS_OK;
 }
 
+inline uint64_t scratch_pitch(uint64_t n) { return (n + 31) & ~31ull; }
+
 // a2 + a3
 int run_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* mask,
-                 uint32_t* planes) {
+                 uint32_t* planes, uint64_t pitch) {
     TRY(claim_slot(ctx, 0));
     plan_compress(mask, B, ctx->h_plan[0]);
     uint32_t m = ctx->h_plan[0]->out_bits, np = (m + 31) / 32;
     if (n == 0 || m == 0) return CKS_OK;
     GatherPlan* dplan;
     TRY(upload_plan(ctx, 0, &dplan));
-    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0]->nsteps, np, planes, ctx->stream));
+    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0]->nsteps, np, planes, pitch, ctx->sms, ctx->stream));
     return CKS_OK;
 }
 
-// a4 + a5. `in_planes` (np planes) is not modified. `in_rid` NULL = implicit ids; when
-// non-NULL its rid_passes digits are sorted first. Sorted planes land in `final_planes`
-// (NULL = ctx scratch; returned via *sorted_view), row ids in `final_rid`.
-// `avoid` (may be NULL) is a scratch buffer holding the input planes; the pass sequence
-// never writes it before the first pass has read it.
-int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint32_t np, uint32_t key_passes, uint64_t n,
-             const uint32_t* in_rid, uint32_t rid_passes, uint32_t* final_planes, uint32_t* final_rid,
-             const uint32_t** sorted_view) {
+// a4 + a5. `in_planes` (np planes, stride in_pitch) is not modified. `in_rid` NULL = implicit
+// ids; when non-NULL its rid_passes digits are sorted first. Sorted planes land in
+// `final_planes` (stride final_pitch; NULL = ctx scratch), row ids in `final_rid`; the sorted
+// planes' location is returned in *sorted_view / *sorted_pitch. Scratch plane buffers alternate
+// so that the last pass writes the final buffers; the caller may have compressed into the
+// scratch buffer the first pass does not write (see first_pass_out()).
+uint32_t* first_pass_out(cks_ctx* ctx, uint32_t P) {
+    return ((P - 1) & 1) ? as<uint32_t>(ctx->planeA) : as<uint32_t>(ctx->planeB);
+}
+
+int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_t np, uint32_t key_passes,
+             uint64_t n, const uint32_t* in_rid, uint32_t rid_passes, uint32_t* final_planes,
+             uint64_t final_pitch, uint32_t* final_rid, const uint32_t** sorted_view, uint64_t* sorted_pitch) {
     const uint32_t P = key_passes + (in_rid ? rid_passes : 0);
     if (sorted_view) *sorted_view = in_planes;
+    if (sorted_pitch) *sorted_pitch = in_pitch;
     if (n == 0) return CKS_OK;
     if (P == 0) {                                        // nothing to sort: identity order
         if (in_rid) CK(cudaMemcpyAsync(final_rid, in_rid, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
         else LAUNCH(launch_iota(final_rid, n, ctx->stream));
         if (final_planes && np)
-            CK(cudaMemcpyAsync(final_planes, in_planes, (size_t)np * n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            CK(cudaMemcpy2DAsync(final_planes, final_pitch * 4, in_planes, in_pitch * 4, n * 4, np,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
         return CKS_OK;
     }
-    const size_t pbytes = (size_t)np * n * 4;
+    const uint64_t sp = scratch_pitch(n);
+    const size_t pbytes = (size_t)np * sp * 4;
     TRY(ensure(ctx, ctx->planeA, pbytes));
     TRY(ensure(ctx, ctx->planeB, pbytes));
-    TRY(ensure(ctx, ctx->ridA, n * 4));
-    TRY(ensure(ctx, ctx->ridB, n * 4));
+    TRY(ensure(ctx, ctx->ridA, sp * 4));
+    TRY(ensure(ctx, ctx->ridB, sp * 4));
     TRY(ensure(ctx, ctx->hist, (size_t)P * 256 * 4));
     TRY(ensure(ctx, ctx->base, (size_t)P * 256 * 4));
     TRY(ensure(ctx, ctx->counters, (size_t)P * 4));
@@ -202,25 +212,31 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint32_t np, uint32_t key_
     }
     CK(cudaMemsetAsync(ctx->hist.p, 0, (size_t)P * 256 * 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)P * 4, ctx->stream));
-    LAUNCH(launch_hist(in_planes, n, key_passes, in_rid, rid_passes, as<uint32_t>(ctx->hist), ctx->sms,
-                       ctx->stream));
-    ctx->launches += (P + 31) / 32 - 1;                  // launch_hist runs one kernel per 32 passes
+    int hl = 0;
+    CK(launch_hist(in_planes, in_pitch, n, key_passes, in_rid, rid_passes, as<uint32_t>(ctx->hist), ctx->sms,
+                   ctx->stream, &hl));
+    ctx->launches += (uint64_t)hl;
     LAUNCH(launch_scan(as<uint32_t>(ctx->hist), P, as<uint32_t>(ctx->base), ctx->stream));
     mark(ctx, ST_HIST);
 
     const uint32_t* cur_p = in_planes;
+    uint64_t cur_pitch = in_pitch;
     const uint32_t* cur_r = in_rid;
     for (uint32_t t = 0; t < P; t++) {
         const bool last = t == P - 1;
         const bool odd = ((P - 1 - t) & 1) != 0;
         uint32_t* out_p = odd ? as<uint32_t>(ctx->planeA) : (last && final_planes ? final_planes : as<uint32_t>(ctx->planeB));
+        uint64_t out_pitch = (last && final_planes && !odd) ? final_pitch : sp;
         uint32_t* out_r = last ? final_rid : (odd ? as<uint32_t>(ctx->ridA) : as<uint32_t>(ctx->ridB));
         OnesweepArgs a;
+        memset(&a, 0, sizeof(a));
         a.in_planes = cur_p;
         a.out_planes = out_p;
         a.in_rid = cur_r;
         a.out_rid = out_r;
         a.n = n;
+        a.in_pitch = cur_pitch;
+        a.out_pitch = out_pitch;
         a.nplanes = np;
         uint32_t hist_index;
         if (in_rid && t < rid_passes) {                  // row-id digits first (least significant)
@@ -243,15 +259,17 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint32_t np, uint32_t key_
         a.epoch = ctx->epoch++;
         LAUNCH(launch_onesweep(a, ctx->stream));
         cur_p = out_p;
+        cur_pitch = out_pitch;
         cur_r = out_r;
     }
     if (sorted_view) *sorted_view = cur_p;
+    if (sorted_pitch) *sorted_pitch = cur_pitch;
     return CKS_OK;
 }
 
 // a6: exact D from sorted planes compressed with `sort_mask` (host).
-int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint32_t m, uint64_t n, const uint8_t* sort_mask,
-                 uint32_t B, uint8_t* mask_out, uint16_t* dbit) {
+int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint64_t pitch, uint32_t m, uint64_t n,
+                 const uint8_t* sort_mask, uint32_t B, uint8_t* mask_out, uint16_t* dbit) {
     const uint32_t nwords = (8 * B + 31) / 32;
     TRY(ensure(ctx, ctx->dacc, (size_t)nwords * 4));
     TRY(ensure(ctx, ctx->moff, (size_t)(m + 1) * 2));
@@ -264,7 +282,7 @@ int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint32_t m, uint64_t n, c
     CK(cudaEventRecord(ctx->plan_ev[1], ctx->stream));
     CK(cudaMemsetAsync(ctx->dacc.p, 0, (size_t)nwords * 4, ctx->stream));
     if (n && m) {
-        LAUNCH(launch_adjacent(sorted, n, m, as<uint16_t>(ctx->moff), B, dbit, as<uint32_t>(ctx->dacc),
+        LAUNCH(launch_adjacent(sorted, pitch, n, m, as<uint16_t>(ctx->moff), B, dbit, as<uint32_t>(ctx->dacc),
                                ctx->sms, ctx->stream));
     } else if (n && dbit) {
         LAUNCH(launch_fill_u16(dbit, n, (uint16_t)CKS_DBIT_NONE, ctx->stream));
@@ -297,6 +315,7 @@ int tree_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* s) {
     }
     s->height = h;
     s->total_nodes = off;
+    if (off * (uint64_t)fanout >= (1ull << 32)) return CKS_ERANGE;   // kernels index slots in 32 bits
     s->inner_nodes = h ? off - s->level_nodes[0] : 0;
     return CKS_OK;
 }
@@ -355,19 +374,22 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
         dbit = as<uint16_t>(ctx->dbit);
     }
     // a3: compress into whichever plane buffer the first LSD pass does not write
-    const size_t pbytes = (size_t)np * n * 4;
+    const uint64_t sp = scratch_pitch(n);
+    const size_t pbytes = (size_t)np * sp * 4;
     TRY(ensure(ctx, ctx->planeA, pbytes));
     TRY(ensure(ctx, ctx->planeB, pbytes));
-    uint32_t* cbuf = (((k - 1) & 1) != 0 || k == 0) ? as<uint32_t>(ctx->planeB) : as<uint32_t>(ctx->planeA);
-    if (k == 0) cbuf = as<uint32_t>(ctx->planeB);
-    TRY(run_compress(ctx, keys, n, B, M, cbuf));
+    uint32_t* cbuf = k ? (first_pass_out(ctx, k) == as<uint32_t>(ctx->planeA) ? as<uint32_t>(ctx->planeB)
+                                                                              : as<uint32_t>(ctx->planeA))
+                       : as<uint32_t>(ctx->planeB);
+    TRY(run_compress(ctx, keys, n, B, M, cbuf, sp));
     mark(ctx, ST_COMPRESS);
     // a4 + a5
     const uint32_t* sorted = nullptr;
-    TRY(run_sort(ctx, cbuf, np, k, n, nullptr, 0, nullptr, out->perm, &sorted));
+    uint64_t spitch = sp;
+    TRY(run_sort(ctx, cbuf, sp, np, k, n, nullptr, 0, nullptr, 0, out->perm, &sorted, &spitch));
     mark(ctx, ST_SORT);
     // a6
-    TRY(run_adjacent(ctx, sorted, m, n, M, B, out->mask, dbit));
+    TRY(run_adjacent(ctx, sorted, spitch, m, n, M, B, out->mask, dbit));
     out->popcount = popcount_mask(out->mask, B);
     for (uint32_t j = 0; j < B; j++)
         if (out->mask[j] & ~M[j])
@@ -376,6 +398,7 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     mark(ctx, ST_ADJ);
     // a7: repack P_M -> P_D
     out->packed = sorted;
+    out->packed_pitch = spitch;
     if (!same_mask(out->mask, M, B) && out->popcount > 0) {
         std::vector<uint32_t> sub(np, 0);
         uint32_t t = 0;                                   // compressed index from the MSB
@@ -390,8 +413,10 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
         GatherPlan* dplan;
         TRY(upload_plan(ctx, 1, &dplan));
         uint32_t* dst = (sorted == as<uint32_t>(ctx->planeA)) ? as<uint32_t>(ctx->planeB) : as<uint32_t>(ctx->planeA);
-        LAUNCH(launch_repack(sorted, n, dplan, ctx->h_plan[1]->nsteps, (out->popcount + 31) / 32, dst, ctx->stream));
+        LAUNCH(launch_repack(sorted, spitch, n, dplan, ctx->h_plan[1]->nsteps, (out->popcount + 31) / 32, dst, sp,
+                             ctx->sms, ctx->stream));
         out->packed = dst;
+        out->packed_pitch = sp;
     } else if (out->popcount == 0) {
         out->packed = nullptr;
     }
@@ -546,7 +571,7 @@ int cks_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     uint32_t m = popcount_mask(mask, B);
     if (n && m && !packed_out) return fail(ctx, CKS_EINVAL, "packed_out is NULL");
     CK(cudaSetDevice(ctx->device));
-    return run_compress(ctx, keys, n, B, mask, packed_out);
+    return run_compress(ctx, keys, n, B, mask, packed_out, n);
 }
 
 int cks_sort(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t n, const uint32_t* row_ids,
@@ -557,7 +582,7 @@ int cks_sort(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t n, co
     if (n && (!perm_out || (bits && !packed))) return fail(ctx, CKS_EINVAL, "NULL buffer with n > 0");
     CK(cudaSetDevice(ctx->device));
     const uint32_t np = (bits + 31) / 32, k = (bits + 7) / 8;
-    TRY(run_sort(ctx, packed, np, k, n, row_ids, 4, sorted_packed_out, perm_out, nullptr));
+    TRY(run_sort(ctx, packed, n, np, k, n, row_ids, 4, sorted_packed_out, n, perm_out, nullptr, nullptr));
     return CKS_OK;
 }
 
@@ -570,7 +595,7 @@ int cks_adjacent_dbits(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bit
     if (n && bits && !sorted_packed) return fail(ctx, CKS_EINVAL, "sorted_packed is NULL");
     if (!sort_mask || !mask_out) return fail(ctx, CKS_EINVAL, "mask pointer is NULL");
     CK(cudaSetDevice(ctx->device));
-    TRY(run_adjacent(ctx, sorted_packed, bits, n, sort_mask, B, mask_out, dbit_out));
+    TRY(run_adjacent(ctx, sorted_packed, n, bits, n, sort_mask, B, mask_out, dbit_out));
     if (popcount_out) *popcount_out = popcount_mask(mask_out, B);
     return CKS_OK;
 }

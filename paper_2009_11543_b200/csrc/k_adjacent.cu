@@ -12,7 +12,7 @@
 namespace cks {
 
 __global__ void __launch_bounds__(256)
-k_adjacent(const uint32_t* __restrict__ planes, uint64_t n, uint32_t m, uint32_t np,
+k_adjacent(const uint32_t* __restrict__ planes, uint64_t pitch, uint64_t n, uint32_t m, uint32_t np,
            const uint16_t* __restrict__ moff, uint32_t nwords, uint16_t* __restrict__ dbit,
            uint32_t* __restrict__ dacc) {
     extern __shared__ uint32_t s_dyn[];
@@ -26,7 +26,7 @@ k_adjacent(const uint32_t* __restrict__ planes, uint64_t n, uint32_t m, uint32_t
         uint32_t d = CKS_NONE_INTERNAL;
         if (i > 0) {
             for (int q = (int)np - 1; q >= 0; q--) {
-                uint32_t x = planes[(uint64_t)q * n + i] ^ planes[(uint64_t)q * n + i - 1];
+                uint32_t x = planes[(uint64_t)q * pitch + i] ^ planes[(uint64_t)q * pitch + i - 1];
                 if (x) {
                     uint32_t bitpos = 32u * (uint32_t)q + 31u - (uint32_t)__clz(x);   // bit of P
                     uint32_t t = (m - 1) - bitpos;                                  // compressed position
@@ -44,7 +44,7 @@ k_adjacent(const uint32_t* __restrict__ planes, uint64_t n, uint32_t m, uint32_t
         if (s_bm[w]) atomicOr(&dacc[w], s_bm[w]);
 }
 
-cudaError_t launch_adjacent(const uint32_t* planes, uint64_t n, uint32_t m, const uint16_t* moff,
+cudaError_t launch_adjacent(const uint32_t* planes, uint64_t pitch, uint64_t n, uint32_t m, const uint16_t* moff,
                             uint32_t B, uint16_t* dbit, uint32_t* dacc, int sms, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     uint32_t np = (m + 31) / 32;
@@ -52,7 +52,7 @@ cudaError_t launch_adjacent(const uint32_t* planes, uint64_t n, uint32_t m, cons
     size_t smem = (size_t)nwords * 4 + (size_t)m * 2;
     uint64_t want = (n + 255) / 256;
     int grid = (int)(want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8);
-    k_adjacent<<<grid, 256, smem, st>>>(planes, n, m, np, moff, nwords, dbit, dacc);
+    k_adjacent<<<grid, 256, smem, st>>>(planes, pitch, n, m, np, moff, nwords, dbit, dacc);
     return cudaGetLastError();
 }
 
@@ -89,17 +89,17 @@ cudaError_t launch_fill_u16(uint16_t* out, uint64_t n, uint16_t v, cudaStream_t 
 __global__ void k_bulk_leaves(const uint32_t* __restrict__ perm, const uint16_t* __restrict__ dbit,
                               BulkLevel L, uint32_t fanout, uint32_t per, uint32_t* __restrict__ node_cnt,
                               uint32_t* __restrict__ rid, uint16_t* __restrict__ edbit) {
-    const uint64_t slots = L.nodes * fanout;
-    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < slots;
-         s += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t j = s / fanout;
-        uint32_t e = (uint32_t)(s - j * fanout);
-        uint64_t x = j * per + e;
+    // slots < 2^32 (n < 2^32 and per >= fanout/2 in practice): 32-bit index arithmetic
+    const uint32_t slots = (uint32_t)(L.nodes * fanout);
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
+        uint32_t j = s / fanout;
+        uint32_t e = s - j * fanout;
+        uint64_t x = (uint64_t)j * per + e;
         bool ok = e < per && x < L.entries;
         rid[s] = ok ? perm[x] : 0xFFFFFFFFu;
         if (edbit) edbit[s] = ok ? dbit[x] : (uint16_t)CKS_NONE_INTERNAL;
         if (e == 0) {
-            uint64_t rem = L.entries - j * per;
+            uint64_t rem = L.entries - (uint64_t)j * per;
             node_cnt[j] = (uint32_t)(rem < per ? rem : per);
         }
     }
@@ -110,12 +110,11 @@ __global__ void k_bulk_inner(const uint32_t* __restrict__ perm, const uint16_t* 
                              uint32_t* __restrict__ node_cnt, uint32_t* __restrict__ rid,
                              uint16_t* __restrict__ edbit, uint32_t* __restrict__ child,
                              uint64_t inner_off, uint16_t* __restrict__ rmin) {
-    const uint64_t slots = L.nodes * fanout;
-    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < slots;
-         s += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t j = s / fanout;
-        uint32_t e = (uint32_t)(s - j * fanout);
-        uint64_t x = j * per + e;
+    const uint32_t slots = (uint32_t)(L.nodes * fanout);
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
+        uint32_t j = s / fanout;
+        uint32_t e = s - j * fanout;
+        uint64_t x = (uint64_t)j * per + e;
         bool ok = e < per && x < L.entries;
         uint64_t gs = (L.node_off + j) * fanout + e;                  // global slot
         uint64_t cs = (L.node_off - inner_off + j) * fanout + e;      // inner-only slot

@@ -41,7 +41,7 @@ constexpr int kCompressThreads = 256;
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_tiled(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
                  const GatherPlan* __restrict__ plan, uint32_t nsteps, uint32_t np,
-                 uint32_t* __restrict__ planes) {
+                 uint32_t* __restrict__ planes, uint64_t pitch) {
     extern __shared__ int4 s_tile[];                      // [256][S16] int4 units
     __shared__ GatherStep s_step[kMaxWords];
     for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
@@ -77,13 +77,13 @@ k_compress_tiled(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
                 acc |= (unsigned long long)x << accbits;
                 accbits += g.cnt;
                 if (accbits >= 32) {
-                    planes[(uint64_t)q * n + i] = (uint32_t)acc;
+                    planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
                     acc >>= 32;
                     accbits -= 32;
                     q++;
                 }
             }
-            if (accbits) planes[(uint64_t)q * n + i] = (uint32_t)acc;
+            if (accbits) planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
         }
         __syncthreads();
     }
@@ -93,7 +93,7 @@ k_compress_tiled(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_generic(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
                    const GatherPlan* __restrict__ plan, uint32_t nsteps, uint32_t np,
-                   uint32_t* __restrict__ planes) {
+                   uint32_t* __restrict__ planes, uint64_t pitch) {
     __shared__ GatherStep s_step[kMaxWords];
     for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
     __syncthreads();
@@ -113,21 +113,21 @@ k_compress_generic(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
             acc |= (unsigned long long)x << accbits;
             accbits += g.cnt;
             if (accbits >= 32) {
-                planes[(uint64_t)q * n + i] = (uint32_t)acc;
+                planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
                 acc >>= 32;
                 accbits -= 32;
                 q++;
             }
         }
-        if (accbits) planes[(uint64_t)q * n + i] = (uint32_t)acc;
+        if (accbits) planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
     }
 }
 
 // a7 repack: source words are the planes of P_M (plane 0 least significant), each
 // gathered by the sub-mask of P_M bits that are exact-D positions.
 __global__ void __launch_bounds__(kCompressThreads)
-k_repack(const uint32_t* __restrict__ in, uint64_t n, const GatherPlan* __restrict__ plan,
-         uint32_t nsteps, uint32_t np, uint32_t* __restrict__ out) {
+k_repack(const uint32_t* __restrict__ in, uint64_t in_pitch, uint64_t n, const GatherPlan* __restrict__ plan,
+         uint32_t nsteps, uint32_t np, uint32_t* __restrict__ out, uint64_t out_pitch) {
     __shared__ GatherStep s_step[kMaxPlanes];
     for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
     __syncthreads();
@@ -137,17 +137,17 @@ k_repack(const uint32_t* __restrict__ in, uint64_t n, const GatherPlan* __restri
         uint32_t accbits = 0, q = 0;
         for (uint32_t s = 0; s < nsteps; s++) {
             const GatherStep& g = s_step[s];
-            uint32_t x = gather_word(in[(uint64_t)g.src * n + i], g);
+            uint32_t x = gather_word(in[(uint64_t)g.src * in_pitch + i], g);
             acc |= (unsigned long long)x << accbits;
             accbits += g.cnt;
             if (accbits >= 32) {
-                out[(uint64_t)q * n + i] = (uint32_t)acc;
+                out[(uint64_t)q * out_pitch + i] = (uint32_t)acc;
                 acc >>= 32;
                 accbits -= 32;
                 q++;
             }
         }
-        if (accbits) out[(uint64_t)q * n + i] = (uint32_t)acc;
+        if (accbits) out[(uint64_t)q * out_pitch + i] = (uint32_t)acc;
     }
 }
 
@@ -159,33 +159,30 @@ static int grid_for(uint64_t work, int per_sm, int sms) {
 }
 
 cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
-                            uint32_t nsteps, uint32_t np, uint32_t* planes, cudaStream_t st) {
+                            uint32_t nsteps, uint32_t np, uint32_t* planes, uint64_t pitch, int sms,
+                            cudaStream_t st) {
     if (n == 0 || np == 0) return cudaSuccess;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if ((B & 15) == 0 && ((uintptr_t)keys & 15) == 0) {
         uint32_t S16 = (B >> 4) | 1;
         size_t smem = (size_t)kCompressThreads * S16 * 16;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_compress_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = smem <= 24 * 1024 ? 8 : smem <= 48 * 1024 ? 4 : smem <= 100 * 1024 ? 2 : 1;
-        k_compress_tiled<<<grid_for(n, per_sm, sms), kCompressThreads, smem, st>>>(keys, n, B, dplan,
-                                                                                   nsteps, np, planes);
+        k_compress_tiled<<<grid_for(n, per_sm, sms), kCompressThreads, smem, st>>>(keys, n, B, dplan, nsteps,
+                                                                                   np, planes, pitch);
     } else {
-        k_compress_generic<<<grid_for(n, 8, sms), kCompressThreads, 0, st>>>(keys, n, B, dplan, nsteps,
-                                                                             np, planes);
+        k_compress_generic<<<grid_for(n, 8, sms), kCompressThreads, 0, st>>>(keys, n, B, dplan, nsteps, np,
+                                                                             planes, pitch);
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_repack(const uint32_t* in, uint64_t n, const GatherPlan* dplan, uint32_t nsteps,
-                          uint32_t np, uint32_t* out, cudaStream_t st) {
+cudaError_t launch_repack(const uint32_t* in, uint64_t in_pitch, uint64_t n, const GatherPlan* dplan,
+                          uint32_t nsteps, uint32_t np, uint32_t* out, uint64_t out_pitch, int sms,
+                          cudaStream_t st) {
     if (n == 0 || np == 0) return cudaSuccess;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    k_repack<<<grid_for(n, 8, sms), kCompressThreads, 0, st>>>(in, n, dplan, nsteps, np, out);
+    k_repack<<<grid_for(n, 8, sms), kCompressThreads, 0, st>>>(in, in_pitch, n, dplan, nsteps, np, out,
+                                                               out_pitch);
     return cudaGetLastError();
 }
 

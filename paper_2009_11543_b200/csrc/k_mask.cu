@@ -6,8 +6,10 @@
 //          the byte values; reading R2) -- a superset of D,
 //   V_j  = bits that are 1 in some occurring value and 0 in another
 //        = OR over keys of (key XOR key_0) restricted to byte j.
-// Layout: keys u8[n][B] row-major; occupancy u32[B][8], bit (v & 31) of word
-// [j][v >> 5] set when value v occurs at byte j.
+// Layout: keys u8[n][B] row-major; occupancy u32[B][8] in global memory, bit (v & 31) of
+// word [j][v >> 5] set when value v occurs at byte j. In shared memory each position's 8
+// words are padded to a stride of 9 so that positions 16 apart (read by the two halves of
+// a warp when B = 32) fall in different banks.
 #include "cks_internal.h"
 
 namespace cks {
@@ -22,7 +24,7 @@ __device__ __forceinline__ int4 ld_stream16(const void* p) {
 // Test-before-set: occupancy saturates after a few keys, so almost every byte costs
 // one shared-memory load and no atomic.
 __device__ __forceinline__ void occ_mark(uint32_t* occ, uint32_t j, uint32_t v) {
-    uint32_t w = j * 8 + (v >> 5), bit = 1u << (v & 31);
+    uint32_t w = j * 9 + (v >> 5), bit = 1u << (v & 31);
     if (!(occ[w] & bit)) atomicOr(&occ[w], bit);
 }
 
@@ -37,7 +39,7 @@ __global__ void __launch_bounds__(256) k_occupancy_pow2(const uint8_t* __restric
                                                         uint64_t total, uint32_t B,
                                                         uint32_t* __restrict__ occ_g) {
     extern __shared__ uint32_t occ[];
-    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) occ[i] = 0;
+    for (uint32_t i = threadIdx.x; i < B * 9; i += blockDim.x) occ[i] = 0;
     __syncthreads();
     const uint32_t Bm1 = B - 1;
     const uint64_t nchunks = total >> 4;
@@ -70,8 +72,10 @@ __global__ void __launch_bounds__(256) k_occupancy_pow2(const uint8_t* __restric
             occ_mark(occ, (uint32_t)(f & Bm1), keys[f]);
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x)
-        if (occ[i]) atomicOr(&occ_g[i], occ[i]);
+    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) {
+        uint32_t v = occ[(i >> 3) * 9 + (i & 7)];
+        if (v) atomicOr(&occ_g[i], v);
+    }
 }
 
 // Generic path (any B, any alignment): thread per key, byte loads.
@@ -79,7 +83,7 @@ __global__ void __launch_bounds__(256) k_occupancy_generic(const uint8_t* __rest
                                                            uint64_t n, uint32_t B,
                                                            uint32_t* __restrict__ occ_g) {
     extern __shared__ uint32_t occ[];
-    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) occ[i] = 0;
+    for (uint32_t i = threadIdx.x; i < B * 9; i += blockDim.x) occ[i] = 0;
     __syncthreads();
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -87,8 +91,10 @@ __global__ void __launch_bounds__(256) k_occupancy_generic(const uint8_t* __rest
         for (uint32_t j = 0; j < B; j++) occ_mark(occ, j, k[j]);
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x)
-        if (occ[i]) atomicOr(&occ_g[i], occ[i]);
+    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) {
+        uint32_t v = occ[(i >> 3) * 9 + (i & 7)];
+        if (v) atomicOr(&occ_g[i], v);
+    }
 }
 
 // One thread per byte position: walk the occurring values in increasing order and
@@ -116,7 +122,7 @@ __global__ void k_occ_finalize(const uint32_t* __restrict__ occ, uint32_t B, uin
 
 cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32_t* occ,
                              int sms, cudaStream_t st) {
-    size_t smem = (size_t)B * 8 * sizeof(uint32_t);
+    size_t smem = (size_t)B * 9 * sizeof(uint32_t);
     bool pow2 = (B & (B - 1)) == 0;
     bool aligned = ((uintptr_t)keys & 15) == 0;
     if (pow2 && aligned) {
