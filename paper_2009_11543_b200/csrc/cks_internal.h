@@ -76,6 +76,7 @@ struct OnesweepArgs {
     uint32_t epoch;              // flag namespace of this pass
     uint32_t slots;              // shared-memory stream slots (set by the launcher)
     uint32_t tma;                // 1 = inputs aligned for 1-D bulk copies (set by the launcher)
+    uint32_t debug;              // timing experiments only (CKS_OS_DEBUG): bit0 skip look-back, bit1 skip streams > 0
 };
 cudaError_t launch_onesweep(const OnesweepArgs& a, cudaStream_t st);
 uint64_t onesweep_tiles(uint64_t n);

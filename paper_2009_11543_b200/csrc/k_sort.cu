@@ -178,7 +178,7 @@ constexpr int kMaxSlots = 8;
 // preceding tiles (status words: flag in the high half, count in the low half; flags
 // carry the pass epoch so the array never needs clearing). Every stream is then permuted
 // through shared memory into digit order and written out in coalesced runs.
-template <int ITEMS>
+template <int ITEMS, int RANK>
 __global__ void __launch_bounds__(kSortThreads)
 k_onesweep(const OnesweepArgs a) {
     constexpr int TILE = kSortThreads * ITEMS;
@@ -198,7 +198,7 @@ k_onesweep(const OnesweepArgs a) {
     const int np = (int)a.nplanes, dp = a.digit_plane;
     const int S = np + 1;                                       // streams
     const int loaded = S - (a.in_rid == nullptr ? 1 : 0);       // implicit row id is last, never loaded
-    const int nslots = loaded < a.slots ? loaded : a.slots;
+    const int nslots = loaded < (int)a.slots ? loaded : (int)a.slots;
 
     auto src_of = [&](int k) -> const uint32_t* {
         int id = stream_id(k, dp, np);
@@ -222,16 +222,18 @@ k_onesweep(const OnesweepArgs a) {
 #pragma unroll
     for (int k = 0; k < kWarps; k++) s_hist[k][tid] = 0;
     __syncthreads();
-    const uint64_t tile = s_tile;
-    const uint64_t base = tile * TILE;
+    const uint32_t tile = s_tile;
+    const uint64_t base = (uint64_t)tile * TILE;
     const uint32_t tile_n = (uint32_t)(n - base < (uint64_t)TILE ? n - base : (uint64_t)TILE);
     const bool use_tma = a.tma && tile_n == (uint32_t)TILE;
 
-    // make stream k available in its slot
-    auto acquire = [&](int k) {
-        uint32_t* slot = stage + (size_t)(k % nslots) * TILE;
+    // streams are consumed in order 0, 1, 2, ...; stream k lives in slot k mod nslots and is
+    // that slot's (k / nslots)-th fill, tracked incrementally (no division)
+    int cur_slot = 0, cur_round = 0;
+    auto acquire = [&](int k) -> const uint32_t* {
+        uint32_t* slot = stage + (size_t)cur_slot * TILE;
         if (use_tma) {
-            mbar_wait(&s_bar[k % nslots], (uint32_t)(k / nslots) & 1u);
+            mbar_wait(&s_bar[cur_slot], (uint32_t)cur_round & 1u);
         } else {
             const uint32_t* src = src_of(k) + base;
             for (uint32_t i = tid; i < tile_n; i += kSortThreads) slot[i] = __ldg(src + i);
@@ -239,58 +241,69 @@ k_onesweep(const OnesweepArgs a) {
         }
         return slot;
     };
-    auto refill = [&](int k_done) {                              // slot of k_done is free
+    auto release = [&](int k_done) {                            // slot of k_done is free: refill it
         int nk = k_done + nslots;
         if (use_tma && tid == 0 && nk < loaded) {
             fence_proxy_async();
-            tma_load_1d(stage + (size_t)(nk % nslots) * TILE, src_of(nk) + base, TILE * 4, &s_bar[nk % nslots]);
+            tma_load_1d(stage + (size_t)cur_slot * TILE, src_of(nk) + base, TILE * 4, &s_bar[cur_slot]);
         }
+        if (++cur_slot == nslots) { cur_slot = 0; cur_round++; }
     };
 
-    // ---- rank the digit within each warp (warp-striped items: index w*32*ITEMS + i*32 + lane)
+    // ---- rank the digit within each warp (warp-striped items: index w*32*ITEMS + i*32 + lane);
+    // all match_any are issued back to back, then the per-warp counters are walked in item order
     const uint32_t* dslot = (dp < 0 && a.in_rid == nullptr) ? nullptr : acquire(0);
     const uint32_t wofs = (uint32_t)warp * 32 * ITEMS;
     uint32_t* h = s_hist[warp];
     const uint32_t ltm = lanemask_lt();
     uint32_t pos[ITEMS];
+    uint32_t dg[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
         uint32_t idx = wofs + i * 32 + lane;
-        bool valid = idx < tile_n;
-        uint32_t key = valid ? (dslot ? dslot[idx] : (uint32_t)(base + idx)) : 0u;
-        uint32_t d = (key >> a.shift) & 0xFF;
-        // peers = lanes with the same digit: intersect the 8 bit-plane ballots
-        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+        uint32_t key = idx < tile_n ? (dslot ? dslot[idx] : (uint32_t)(base + idx)) : 0u;
+        dg[i] = idx < tile_n ? (key >> a.shift) & 0xFF : 0x100u;
+    }
 #pragma unroll
-        for (int b = 0; b < 8; b++) {
-            uint32_t bit = (d >> b) & 1u;
-            uint32_t bal = __ballot_sync(0xffffffffu, bit);
-            peers &= bit ? bal : ~bal;
+    for (int i = 0; i < ITEMS; i++) {
+        const bool valid = dg[i] < 0x100u;
+        uint32_t peers;
+        if (RANK == 0) {                       // intersect the 8 bit-plane ballots
+            peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                uint32_t bit = (dg[i] >> b) & 1u;
+                uint32_t bal = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bal : ~bal;
+            }
+        } else {
+            peers = __match_any_sync(0xffffffffu, dg[i]);
+            if (!valid) peers = 0;
         }
-        uint32_t lower = __popc(peers & ltm);
-        uint32_t cnt = valid ? h[d] : 0;
-        pos[i] = cnt + lower;
-        __syncwarp();
-        if (valid && lower == 0) h[d] = cnt + __popc(peers);
-        __syncwarp();
+        // the group's leader (lowest lane) reserves popc(peers) slots of the warp's counter
+        // for its digit; shared-memory atomics of one warp are applied in issue order, so
+        // items keep their order without a per-item warp barrier
+        const uint32_t lower = __popc(peers & ltm);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (valid && lower == 0) old = atomicAdd(&h[dg[i]], (uint32_t)__popc(peers));
+        old = __shfl_sync(0xffffffffu, old, leader < 0 ? lane : leader);
+        pos[i] = old + lower;
     }
     __syncthreads();
 
     // ---- per digit (thread = digit): warp offsets and tile total; publish the aggregate
-    const uint32_t total = [&] {
-        uint32_t t = 0;
+    uint32_t total = 0;
 #pragma unroll
-        for (int k = 0; k < kWarps; k++) {
-            uint32_t c = s_hist[k][tid];
-            s_hist[k][tid] = t;
-            t += c;
-        }
-        return t;
-    }();
+    for (int k = 0; k < kWarps; k++) {
+        uint32_t c = s_hist[k][tid];
+        s_hist[k][tid] = total;
+        total += c;
+    }
     const unsigned long long FA = (unsigned long long)(2u * a.epoch + 1u) << 32;
     const unsigned long long FP = (unsigned long long)(2u * a.epoch + 2u) << 32;
-    unsigned long long* my = a.status + tile * kRadix + tid;
-    st_relaxed_u64(my, (tile == 0 ? FP : FA) | total);
+    unsigned long long* const col = a.status + tid;             // status of tile j, digit tid: col[j*256]
+    st_relaxed_u64(col + (size_t)tile * kRadix, (tile == 0 ? FP : FA) | total);
     const uint32_t excl = block_exclusive_scan256(total, s_warp);
     s_local[tid] = excl;
     __syncthreads();
@@ -298,27 +311,26 @@ k_onesweep(const OnesweepArgs a) {
     // ---- stream 0 into tile (digit) order before the look-back: it needs local offsets only
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
-        uint32_t idx = wofs + i * 32 + lane;
-        if (idx < tile_n) {
+        if (dg[i] < 0x100u) {
+            uint32_t idx = wofs + i * 32 + lane;
             uint32_t key = dslot ? dslot[idx] : (uint32_t)(base + idx);
-            uint32_t d = (key >> a.shift) & 0xFF;
-            pos[i] += s_local[d] + s_hist[warp][d];
+            pos[i] += s_local[dg[i]] + s_hist[warp][dg[i]];
             s_buf[pos[i]] = key;
-            s_dig[pos[i]] = (uint8_t)d;
+            s_dig[pos[i]] = (uint8_t)dg[i];
         }
     }
 
     // ---- decoupled look-back for digit tid, 8 predecessors per round trip
     {
         uint32_t prefix = 0;
-        if (tile > 0) {
-            int64_t j = (int64_t)tile - 1;                       // nearest predecessor not yet summed
+        if (tile > 0 && !(a.debug & 1)) {
+            int j = (int)tile - 1;                               // nearest predecessor not yet summed
             constexpr int WIN = 8;
             while (true) {
                 unsigned long long v[WIN];
 #pragma unroll
                 for (int k = 0; k < WIN; k++)
-                    v[k] = (j - k >= 0) ? ld_relaxed_u64(a.status + (uint64_t)(j - k) * kRadix + tid) : FP;
+                    v[k] = (j - k >= 0) ? ld_relaxed_u64(col + (uint32_t)(j - k) * kRadix) : FP;
                 bool done = false;
                 int k = 0;
                 for (; k < WIN; k++) {
@@ -331,12 +343,12 @@ k_onesweep(const OnesweepArgs a) {
                 if (k == 0) __nanosleep(16);                     // nearest one not ready: back off
                 j -= k;
             }
-            st_relaxed_u64(my, FP | (unsigned long long)(prefix + total));
+            st_relaxed_u64(col + (size_t)tile * kRadix, FP | (unsigned long long)(prefix + total));
         }
         s_gbase[tid] = a.bucket_base[tid] + prefix - excl;
     }
     __syncthreads();
-    if (dslot) refill(0);
+    if (dslot) release(0);
     uint32_t dest[ITEMS];
     {
         uint32_t* out = dst_of(0);
@@ -351,31 +363,256 @@ k_onesweep(const OnesweepArgs a) {
     }
 
     // ---- the other streams follow the same permutation
-    for (int k = 1; k < S; k++) {
+    for (int k = 1; k < ((a.debug & 2) ? 1 : S); k++) {
         __syncthreads();                                         // s_buf free again
-        const bool implicit = stream_id(k, dp, np) < 0 && a.in_rid == nullptr;
+        const bool implicit = k == S - 1 && a.in_rid == nullptr && dp >= 0;
         if (implicit) {
 #pragma unroll
-            for (int i = 0; i < ITEMS; i++) {
-                uint32_t idx = wofs + i * 32 + lane;
-                if (idx < tile_n) s_buf[pos[i]] = (uint32_t)(base + idx);
-            }
+            for (int i = 0; i < ITEMS; i++)
+                if (dg[i] < 0x100u) s_buf[pos[i]] = (uint32_t)(base + wofs + i * 32 + lane);
         } else {
             const uint32_t* slot = acquire(k);
 #pragma unroll
-            for (int i = 0; i < ITEMS; i++) {
-                uint32_t idx = wofs + i * 32 + lane;
-                if (idx < tile_n) s_buf[pos[i]] = slot[idx];
-            }
+            for (int i = 0; i < ITEMS; i++)
+                if (dg[i] < 0x100u) s_buf[pos[i]] = slot[wofs + i * 32 + lane];
         }
         __syncthreads();
-        if (!implicit) refill(k);
+        if (!implicit) release(k);
         uint32_t* out = dst_of(k);
 #pragma unroll
         for (int r = 0; r < ITEMS; r++) {
             uint32_t s = r * kSortThreads + tid;
             if (s < tile_n) out[dest[r]] = s_buf[s];
         }
+    }
+}
+
+// Persistent variant: grid = resident CTAs; each CTA loops over dynamically claimed tiles.
+// The shared-memory stream slots form one ring that runs across tile boundaries: when a
+// stream is consumed its slot is refilled (TMA) with the next stream in sequence -- the
+// next stream of this tile or the first streams of the tile claimed next -- so the loads
+// of tile t+1 overlap the look-back and write-out of tile t. The next tile is claimed only
+// once the current tile has published its aggregate (just before its look-back): claiming
+// earlier makes later tiles wait on a claimed-but-unstarted tile. Each CTA processes its
+// claims in order, so the smallest unfinished tile is always some CTA's current tile and
+// the look-back cannot deadlock.
+template <int ITEMS>
+__global__ void __launch_bounds__(kSortThreads, ITEMS == 8 ? 4 : 2)
+k_onesweep_persist(const OnesweepArgs a) {
+    constexpr int TILE = kSortThreads * ITEMS;
+    extern __shared__ __align__(128) uint8_t s_dyn[];
+    uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                  // [R][TILE]
+    uint32_t* s_buf = ring + (size_t)a.slots * TILE;                         // [TILE]
+    uint32_t (*s_hist)[kRadix] = reinterpret_cast<uint32_t (*)[kRadix]>(s_buf + TILE);  // [8][256]
+    uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_buf + TILE + kWarps * kRadix);        // [TILE]
+    __shared__ uint32_t s_local[kRadix];
+    __shared__ uint32_t s_gbase[kRadix];
+    __shared__ uint32_t s_warp[kWarps];
+    __shared__ uint32_t s_cur;
+    __shared__ __align__(8) uint64_t s_bar[kMaxSlots];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t n = a.n;
+    const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
+    const int np = (int)a.nplanes, dp = a.digit_plane;
+    const int S = np + 1;                                       // streams per tile
+    const int L = S - (a.in_rid == nullptr ? 1 : 0);            // streams loaded per tile
+    const int R = L < (int)a.slots ? L : (int)a.slots;          // ring slots (<= L: one tile ahead)
+
+    auto src_of = [&](int k) -> const uint32_t* {
+        int id = stream_id(k, dp, np);
+        return id >= 0 ? a.in_planes + (uint64_t)id * a.in_pitch : a.in_rid;
+    };
+    auto dst_of = [&](int k) -> uint32_t* {
+        int id = stream_id(k, dp, np);
+        return id >= 0 ? a.out_planes + (uint64_t)id * a.out_pitch : a.out_rid;
+    };
+    auto full = [&](uint32_t t) { return a.tma && t < ntiles && (uint64_t)(t + 1) * TILE <= n; };
+
+    // producer state (thread 0): next stream to issue is stream p_k of tile (p_sel ? next : cur)
+    int p_k = 0, p_sel = 0, p_slot = 0;
+    uint32_t t_cur = 0, t_next = 0;
+    if (tid == 0) {
+        for (int sl = 0; sl < R; sl++) mbar_init(&s_bar[sl], 1);
+        mbar_fence_init();
+        t_cur = atomicAdd(a.tile_counter, 1u);
+        s_cur = t_cur;
+        for (int sl = 0; sl < R; sl++) {                        // prologue: first R streams of t_cur
+            if (full(t_cur)) tma_load_1d(ring + (size_t)sl * TILE, src_of(sl) + (uint64_t)t_cur * TILE, TILE * 4, &s_bar[sl]);
+        }
+        p_k = R;
+        if (p_k == L) { p_k = 0; p_sel = 1; }
+    }
+    auto produce = [&]() {                                      // thread 0: refill slot p_slot
+        const uint32_t t = p_sel ? t_next : t_cur;
+        if (full(t)) {
+            fence_proxy_async();
+            tma_load_1d(ring + (size_t)p_slot * TILE, src_of(p_k) + (uint64_t)t * TILE, TILE * 4, &s_bar[p_slot]);
+        }
+        if (++p_slot == R) p_slot = 0;
+        if (++p_k == L) { p_k = 0; p_sel++; }
+    };
+
+    int c_slot = 0, c_round = 0;                                // consumer ring position (all threads)
+    const uint32_t wofs = (uint32_t)warp * 32 * ITEMS;
+    const uint32_t ltm = lanemask_lt();
+    const unsigned long long FA = (unsigned long long)(2u * a.epoch + 1u) << 32;
+    const unsigned long long FP = (unsigned long long)(2u * a.epoch + 2u) << 32;
+    unsigned long long* const col = a.status + tid;
+
+    __syncthreads();
+    while (true) {
+        const uint32_t tile = s_cur;
+        if (tile >= ntiles) break;
+#pragma unroll
+        for (int k = 0; k < kWarps; k++) s_hist[k][tid] = 0;
+        const uint64_t base = (uint64_t)tile * TILE;
+        const uint32_t tile_n = (uint32_t)(n - base < (uint64_t)TILE ? n - base : (uint64_t)TILE);
+        const bool tma_t = full(tile);
+        __syncthreads();
+
+        auto acquire = [&](int k) -> const uint32_t* {
+            uint32_t* slot = ring + (size_t)c_slot * TILE;
+            if (tma_t) {
+                mbar_wait(&s_bar[c_slot], (uint32_t)c_round & 1u);
+            } else {
+                const uint32_t* src = src_of(k) + base;
+                for (uint32_t i = tid; i < tile_n; i += kSortThreads) slot[i] = __ldg(src + i);
+                __syncthreads();
+            }
+            return slot;
+        };
+        auto release = [&]() {                                  // after a __syncthreads
+            if (tid == 0) produce();
+            if (++c_slot == R) { c_slot = 0; c_round++; }
+        };
+
+        // ---- rank (ballots; warp-striped items)
+        const uint32_t* dslot = acquire(0);
+        uint32_t* h = s_hist[warp];
+        uint32_t pos[ITEMS];
+        uint32_t dg[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            uint32_t idx = wofs + i * 32 + lane;
+            dg[i] = idx < tile_n ? (dslot[idx] >> a.shift) & 0xFF : 0x100u;
+        }
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const bool valid = dg[i] < 0x100u;
+            uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                uint32_t bit = (dg[i] >> b) & 1u;
+                uint32_t bal = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bal : ~bal;
+            }
+            uint32_t lower = __popc(peers & ltm);
+            uint32_t cnt = valid ? h[dg[i]] : 0;
+            pos[i] = cnt + lower;
+            __syncwarp();
+            if (valid && lower == 0) h[dg[i]] = cnt + __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+
+        // ---- per digit: warp offsets, tile total, publish aggregate, local scan
+        uint32_t total = 0;
+#pragma unroll
+        for (int k = 0; k < kWarps; k++) {
+            uint32_t c = s_hist[k][tid];
+            s_hist[k][tid] = total;
+            total += c;
+        }
+        st_relaxed_u64(col + (size_t)tile * kRadix, (tile == 0 ? FP : FA) | total);
+        const uint32_t excl = block_exclusive_scan256(total, s_warp);
+        s_local[tid] = excl;
+        __syncthreads();
+
+        // ---- stream 0 into digit order (local offsets only)
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            if (dg[i] < 0x100u) {
+                uint32_t idx = wofs + i * 32 + lane;
+                pos[i] += s_local[dg[i]] + s_hist[warp][dg[i]];
+                s_buf[pos[i]] = dslot[idx];
+                s_dig[pos[i]] = (uint8_t)dg[i];
+            }
+        }
+
+        if (tid == 0) t_next = atomicAdd(a.tile_counter, 1u);   // claim the next tile now
+        // ---- decoupled look-back, 8 predecessors per round trip
+        {
+            uint32_t prefix = 0;
+            if (tile > 0) {
+                int j = (int)tile - 1;
+                constexpr int WIN = 8;
+                while (true) {
+                    unsigned long long v[WIN];
+#pragma unroll
+                    for (int k = 0; k < WIN; k++)
+                        v[k] = (j - k >= 0) ? ld_relaxed_u64(col + (uint32_t)(j - k) * kRadix) : FP;
+                    bool done = false;
+                    int k = 0;
+                    for (; k < WIN; k++) {
+                        unsigned long long f = v[k] & 0xFFFFFFFF00000000ull;
+                        if (f == FP) { prefix += (uint32_t)v[k]; done = true; break; }
+                        if (f != FA) break;
+                        prefix += (uint32_t)v[k];
+                    }
+                    if (done) break;
+                    if (k == 0) __nanosleep(16);
+                    j -= k;
+                }
+                st_relaxed_u64(col + (size_t)tile * kRadix, FP | (unsigned long long)(prefix + total));
+            }
+            s_gbase[tid] = a.bucket_base[tid] + prefix - excl;
+        }
+        __syncthreads();
+        release();
+        uint32_t dest[ITEMS];
+        {
+            uint32_t* out = dst_of(0);
+#pragma unroll
+            for (int r = 0; r < ITEMS; r++) {
+                uint32_t s = r * kSortThreads + tid;
+                if (s < tile_n) {
+                    dest[r] = s_gbase[s_dig[s]] + s;
+                    out[dest[r]] = s_buf[s];
+                }
+            }
+        }
+
+        // ---- the other streams
+        for (int k = 1; k < S; k++) {
+            __syncthreads();
+            const bool implicit = k == S - 1 && a.in_rid == nullptr;
+            if (implicit) {
+#pragma unroll
+                for (int i = 0; i < ITEMS; i++)
+                    if (dg[i] < 0x100u) s_buf[pos[i]] = (uint32_t)(base + wofs + i * 32 + lane);
+            } else {
+                const uint32_t* slot = acquire(k);
+#pragma unroll
+                for (int i = 0; i < ITEMS; i++)
+                    if (dg[i] < 0x100u) s_buf[pos[i]] = slot[wofs + i * 32 + lane];
+            }
+            __syncthreads();
+            if (!implicit) release();
+            uint32_t* out = dst_of(k);
+#pragma unroll
+            for (int r = 0; r < ITEMS; r++) {
+                uint32_t s = r * kSortThreads + tid;
+                if (s < tile_n) out[dest[r]] = s_buf[s];
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {                                          // advance: next becomes current
+            t_cur = t_next;
+            p_sel--;
+            s_cur = t_cur;
+        }
+        __syncthreads();
     }
 }
 
@@ -399,19 +636,50 @@ uint64_t onesweep_tiles(uint64_t n) {
     return (n + t - 1) / t;
 }
 
-template <int ITEMS>
+static int g_rank = -1;
+
+template <int ITEMS, int RANK>
 static cudaError_t launch_os(OnesweepArgs a, cudaStream_t st) {
     constexpr int TILE = kSortThreads * ITEMS;
     int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
-    if (a.slots > streams) a.slots = streams > 0 ? streams : 1;
+    if ((int)a.slots > streams) a.slots = streams > 0 ? streams : 1;
     size_t smem = (size_t)a.slots * TILE * 4 + (size_t)TILE * 4 + kWarps * kRadix * 4 + TILE;
     static size_t configured = 0;
     if (smem > configured) {
-        cudaFuncSetAttribute(k_onesweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_onesweep<ITEMS, RANK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = smem;
     }
     uint64_t tiles = (a.n + TILE - 1) / TILE;
-    k_onesweep<ITEMS><<<(unsigned)tiles, kSortThreads, smem, st>>>(a);
+    k_onesweep<ITEMS, RANK><<<(unsigned)tiles, kSortThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+static int g_persist = -1;
+
+template <int ITEMS>
+static cudaError_t launch_osp(OnesweepArgs a, cudaStream_t st) {
+    constexpr int TILE = kSortThreads * ITEMS;
+    int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
+    if ((int)a.slots > streams) a.slots = streams > 0 ? streams : 1;
+    size_t smem = (size_t)a.slots * TILE * 4 + (size_t)TILE * 4 + kWarps * kRadix * 4 + TILE;
+    static size_t configured = 0;
+    static int dev_sms = 0;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_onesweep_persist<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    if (!dev_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep_persist<ITEMS>, kSortThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t tiles = (a.n + TILE - 1) / TILE;
+    uint64_t grid = (uint64_t)dev_sms * per_sm;
+    if (grid > tiles) grid = tiles;
+    k_onesweep_persist<ITEMS><<<(unsigned)grid, kSortThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -419,12 +687,22 @@ cudaError_t launch_onesweep(const OnesweepArgs& args, cudaStream_t st) {
     if (args.n == 0) return cudaSuccess;
     OnesweepArgs a = args;
     onesweep_tile_keys();
+    if (g_rank < 0) {
+        const char* e = getenv("CKS_OS_RANK");
+        g_rank = e ? (atoi(e) ? 1 : 0) : 0;
+        const char* p = getenv("CKS_OS_PERSIST");
+        g_persist = p ? (atoi(p) ? 1 : 0) : 1;
+    }
     a.slots = (uint32_t)g_slots;
+    static int dbg = -1;
+    if (dbg < 0) { const char* e = getenv("CKS_OS_DEBUG"); dbg = e ? atoi(e) : 0; }
+    a.debug = (uint32_t)dbg;
     // 1-D bulk copies need 16-byte aligned sources and plane strides
     a.tma = ((uintptr_t)a.in_planes % 16 == 0) && (a.in_pitch % 4 == 0) &&
             (a.in_rid == nullptr || (uintptr_t)a.in_rid % 16 == 0);
-    if (g_items == 8) return launch_os<8>(a, st);
-    return launch_os<16>(a, st);
+    if (g_persist) return g_items == 8 ? launch_osp<8>(a, st) : launch_osp<16>(a, st);
+    if (g_items == 8) return g_rank ? launch_os<8, 1>(a, st) : launch_os<8, 0>(a, st);
+    return g_rank ? launch_os<16, 1>(a, st) : launch_os<16, 0>(a, st);
 }
 
 }  // namespace cks
