@@ -3,6 +3,7 @@
 // Every step of the path runs in the kernels of k_*.cu; the host only plans (mask ->
 // gather masks / D-offset table, a few hundred bytes) and orchestrates.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -39,7 +40,8 @@ struct cks_ctx {
     cudaEvent_t plan_ev[3] = {};      // guards the pinned staging slots
     // scratch
     DevBuf occ, masks8, planeA, planeB, ridA, ridB, hist, base, status, counters, dacc, moff, dbit,
-        rmin0, rmin1, plan[3], keys, perm_scratch;
+        rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total;
+    int algo = -1;                    // LSD pass: 0 = onesweep (look-back), 1 = reduce-then-scan
     size_t status_tiles = 0;
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
@@ -210,13 +212,25 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
         TRY(ensure(ctx, ctx->status, (size_t)tiles * 256 * 8, /*zero=*/true));
         ctx->status_tiles = ctx->status.cap / (256 * 8);
     }
-    CK(cudaMemsetAsync(ctx->hist.p, 0, (size_t)P * 256 * 4, ctx->stream));
-    CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)P * 4, ctx->stream));
-    int hl = 0;
-    CK(launch_hist(in_planes, in_pitch, n, key_passes, in_rid, rid_passes, as<uint32_t>(ctx->hist), ctx->sms,
-                   ctx->stream, &hl));
-    ctx->launches += (uint64_t)hl;
-    LAUNCH(launch_scan(as<uint32_t>(ctx->hist), P, as<uint32_t>(ctx->base), ctx->stream));
+    if (ctx->algo < 0) {
+        const char* e = getenv("CKS_SORT_ALGO");
+        ctx->algo = e ? atoi(e) : 1;
+    }
+    uint64_t lsd_tiles = 0, lsd_chunks = 0;
+    if (ctx->algo == 1) {
+        lsd_sizes(n, &lsd_tiles, &lsd_chunks);
+        TRY(ensure(ctx, ctx->tile_off, (size_t)lsd_tiles * 256 * 4));
+        TRY(ensure(ctx, ctx->chunk_tot, (size_t)lsd_chunks * 256 * 4));
+        TRY(ensure(ctx, ctx->total, 256 * 4));
+    } else {
+        CK(cudaMemsetAsync(ctx->hist.p, 0, (size_t)P * 256 * 4, ctx->stream));
+        CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)P * 4, ctx->stream));
+        int hl = 0;
+        CK(launch_hist(in_planes, in_pitch, n, key_passes, in_rid, rid_passes, as<uint32_t>(ctx->hist), ctx->sms,
+                       ctx->stream, &hl));
+        ctx->launches += (uint64_t)hl;
+        LAUNCH(launch_scan(as<uint32_t>(ctx->hist), P, as<uint32_t>(ctx->base), ctx->stream));
+    }
     mark(ctx, ST_HIST);
 
     const uint32_t* cur_p = in_planes;
@@ -248,6 +262,30 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
             a.digit_plane = (int32_t)(p >> 2);
             a.shift = 8 * (p & 3);
             hist_index = p;
+        }
+        if (ctx->algo == 1) {
+            LsdPassArgs la;
+            memset(&la, 0, sizeof(la));
+            la.in_planes = cur_p;
+            la.out_planes = out_p;
+            la.in_rid = cur_r;
+            la.out_rid = out_r;
+            la.n = n;
+            la.in_pitch = cur_pitch;
+            la.out_pitch = out_pitch;
+            la.nplanes = np;
+            la.digit_plane = a.digit_plane;
+            la.shift = a.shift;
+            la.tile_off = as<uint32_t>(ctx->tile_off);
+            la.chunk_tot = as<uint32_t>(ctx->chunk_tot);
+            la.total = as<uint32_t>(ctx->total);
+            int nl = 0;
+            CK(launch_lsd_pass(la, ctx->sms, ctx->stream, &nl));
+            ctx->launches += (uint64_t)nl;
+            cur_p = out_p;
+            cur_pitch = out_pitch;
+            cur_r = out_r;
+            continue;
         }
         a.bucket_base = as<uint32_t>(ctx->base) + (size_t)hist_index * 256;
         a.tile_counter = as<uint32_t>(ctx->counters) + t;
@@ -487,7 +525,7 @@ int cks_ctx_destroy(cks_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->occ, &ctx->masks8, &ctx->planeA, &ctx->planeB, &ctx->ridA, &ctx->ridB,
                       &ctx->hist, &ctx->base, &ctx->status, &ctx->counters, &ctx->dacc, &ctx->moff,
                       &ctx->dbit, &ctx->rmin0, &ctx->rmin1, &ctx->plan[0], &ctx->plan[1], &ctx->plan[2],
-                      &ctx->keys, &ctx->perm_scratch};
+                      &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int i = 0; i < ST_N; i++)

@@ -82,6 +82,29 @@ cudaError_t launch_onesweep(const OnesweepArgs& a, cudaStream_t st);
 uint64_t onesweep_tiles(uint64_t n);
 uint64_t onesweep_tile_keys();
 
+// Reduce-then-scan LSD pass (k_lsd.cu): upsweep -> chunk scan -> persistent downsweep.
+struct LsdPassArgs {
+    const uint32_t* in_planes;
+    uint32_t* out_planes;
+    const uint32_t* in_rid;      // NULL = implicit row id (input index)
+    uint32_t* out_rid;
+    uint64_t n;
+    uint64_t in_pitch;
+    uint64_t out_pitch;
+    uint32_t nplanes;
+    int32_t digit_plane;         // -1 = digit taken from the row id
+    uint32_t shift;
+    uint32_t* tile_off;          // u32[tiles][256] scratch
+    uint32_t* chunk_tot;         // u32[chunks][256] scratch
+    uint32_t* total;             // u32[256] scratch
+    uint32_t chunk_tiles;        // set by the launcher
+    uint32_t slots;              // set by the launcher
+    uint32_t tma;                // set by the launcher
+    uint32_t debug;              // timing experiments only (CKS_LSD_DEBUG): 1 identity scatter, 2 skip ranking
+};
+cudaError_t launch_lsd_pass(const LsdPassArgs& a, int sms, cudaStream_t st, int* launches);
+void lsd_sizes(uint64_t n, uint64_t* tiles, uint64_t* chunks);
+
 cudaError_t launch_adjacent(const uint32_t* planes, uint64_t pitch, uint64_t n, uint32_t m, const uint16_t* moff,
                             uint32_t B, uint16_t* dbit_out, uint32_t* dacc /* u32[ceil(8B/32)] */,
                             int sms, cudaStream_t st);

@@ -1,0 +1,429 @@
+// k_lsd.cu -- a5: one stable LSD digit pass as reduce-then-scan ("sort the pairs").
+//
+// Three kernels per 8-bit digit, no inter-tile waiting:
+//   k_upsweep    CTA per chunk of CT consecutive tiles: per-tile digit counts (per-warp
+//                shared-memory bins), stored as within-chunk exclusive offsets
+//                tile_off[tile][256]; chunk totals chunk_tot[chunk][256]; digit totals
+//                accumulated into total[256] with one atomic per digit per chunk.
+//   k_chunk_scan bucket base of every digit (exclusive scan of total[]) plus the exclusive
+//                scan of chunk totals over chunks, in place: chunk_tot -> chunk_base.
+//   k_downsweep  persistent CTAs over a static tile schedule (tile = blockIdx + i*grid).
+//                All streams of the tile (digit word, other planes, row id) are fetched by
+//                1-D TMA bulk copies into a ring of shared-memory slots that runs ahead
+//                across tiles (the next tile of a CTA is known statically), so the loads of
+//                the next tile overlap the work on this one. The digit is ranked per warp
+//                (bit-plane ballots; the group leader reserves slots with a shared atomic,
+//                applied in issue order: stable); the resulting tile permutation is stored
+//                once as a u16 source index per output slot, and every stream is gathered
+//                from its slot in that order and written in coalesced runs to
+//                chunk_base[chunk][d] + tile_off[tile][d] + rank.
+// Compared with a single-kernel "onesweep" pass this reads the digit words twice (+4 B/key)
+// but has no decoupled look-back and no dynamic tile counter on the critical path.
+#include <stdlib.h>
+
+#include "cks_internal.h"
+
+namespace cks {
+
+namespace {
+
+constexpr int kW = kSortThreads / 32;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ uint32_t lt_mask() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ uint32_t scan256(uint32_t v, uint32_t* s_warp) {      // exclusive
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t t = lane < kW ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < kW; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < kW) s_warp[lane] = t;
+    }
+    __syncthreads();
+    uint32_t r = (warp ? s_warp[warp - 1] : 0) + x - v;
+    __syncthreads();
+    return r;
+}
+// stream k of a pass: 0 = digit word, then the other planes in order, then the row id
+__device__ __forceinline__ int stream_plane(int k, int dp, int np) {
+    if (k == 0) return dp;
+    int idx = k - 1;
+    int others = np - (dp >= 0 ? 1 : 0);
+    if (idx < others) return idx + ((dp >= 0 && idx >= dp) ? 1 : 0);
+    return -1;
+}
+
+}  // namespace
+
+// ---- upsweep ------------------------------------------------------------------------------
+template <int ITEMS>
+__global__ void __launch_bounds__(kSortThreads)
+k_upsweep(const LsdPassArgs a) {
+    constexpr int TILE = kSortThreads * ITEMS;
+    __shared__ uint32_t bins[kW][kRadix];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint64_t n = a.n;
+    const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
+    const uint32_t t0 = blockIdx.x * a.chunk_tiles;
+    const uint32_t t1 = min(t0 + a.chunk_tiles, ntiles);
+    const uint32_t* src = a.digit_plane >= 0 ? a.in_planes + (uint64_t)a.digit_plane * a.in_pitch : a.in_rid;
+    uint32_t running = 0;
+    uint32_t w[ITEMS];
+    auto load = [&](uint32_t t) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            uint64_t idx = (uint64_t)t * TILE + i * kSortThreads + tid;
+            w[i] = idx < n ? (src ? __ldg(src + idx) : (uint32_t)idx) : 0xFFFFFFFFu;
+        }
+    };
+    if (t0 < t1) load(t0);
+    for (uint32_t t = t0; t < t1; t++) {
+#pragma unroll
+        for (int k = 0; k < kW; k++) bins[k][tid] = 0;
+        __syncthreads();
+        const uint64_t tb = (uint64_t)t * TILE;
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++)
+            if (tb + i * kSortThreads + tid < n) atomicAdd(&bins[warp][(w[i] >> a.shift) & 0xFF], 1u);
+        if (t + 1 < t1) load(t + 1);                         // next tile's words in flight
+        __syncthreads();
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < kW; k++) c += bins[k][tid];
+        a.tile_off[(uint64_t)t * kRadix + tid] = running;
+        running += c;
+        __syncthreads();
+    }
+    a.chunk_tot[(uint64_t)blockIdx.x * kRadix + tid] = running;
+    if (running) atomicAdd(&a.total[tid], running);
+}
+
+// ---- chunk scan: CTA per group of 32 digits, warps split the chunks ------------------------
+__global__ void __launch_bounds__(1024)
+k_chunk_scan(const LsdPassArgs a, uint32_t nchunks) {
+    __shared__ uint32_t s_part[32][33];
+    __shared__ uint32_t s_base[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t d = blockIdx.x * 32 + lane;
+    if (warp == 0) {                                         // bucket base of digit d
+        uint32_t run = 0;
+        for (uint32_t e = 0; e < blockIdx.x * 32; e++) run += a.total[e];
+        uint32_t x = a.total[d];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        s_base[lane] = run + x - a.total[d];
+    }
+    const uint32_t per = (nchunks + 31) / 32;
+    const uint32_t c0 = warp * per, c1 = min(c0 + per, nchunks);
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (uint32_t c = c0; c < c1; c++) sum += a.chunk_tot[(uint64_t)c * kRadix + d];
+    s_part[warp][lane] = sum;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t run = s_base[lane];
+        for (int k = 0; k < 32; k++) {
+            uint32_t v = s_part[k][lane];
+            s_part[k][lane] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    uint32_t run = s_part[warp][lane];
+#pragma unroll 8
+    for (uint32_t c = c0; c < c1; c++) {
+        uint32_t* p = a.chunk_tot + (uint64_t)c * kRadix + d;
+        uint32_t v = *p;
+        *p = run;
+        run += v;
+    }
+}
+
+// ---- downsweep ----------------------------------------------------------------------------
+template <int ITEMS>
+__global__ void __launch_bounds__(kSortThreads, ITEMS == 8 ? 4 : 2)
+k_downsweep(const LsdPassArgs a) {
+    constexpr int TILE = kSortThreads * ITEMS;
+    extern __shared__ __align__(128) uint8_t s_dyn[];
+    uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                   // [R][TILE]
+    uint32_t (*s_hist)[kRadix] = reinterpret_cast<uint32_t (*)[kRadix]>(ring + (size_t)a.slots * TILE); // [8][256]
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(&s_hist[kW][0]);                     // [TILE]
+    uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_src + TILE);                         // [TILE]
+    __shared__ uint32_t s_local[kRadix];
+    __shared__ uint32_t s_gbase[kRadix];
+    __shared__ uint32_t s_warp[kW];
+    __shared__ __align__(8) uint64_t s_bar[8];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t n = a.n;
+    const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
+    const uint32_t G = gridDim.x;
+    const int np = (int)a.nplanes, dp = a.digit_plane;
+    const int S = np + 1;
+    const bool implicit_rid = a.in_rid == nullptr;
+    const int L = S - (implicit_rid ? 1 : 0);                   // loaded streams per tile
+    const int R = L < (int)a.slots ? L : (int)a.slots;
+
+    auto src_of = [&](int k) -> const uint32_t* {
+        int id = stream_plane(k, dp, np);
+        return id >= 0 ? a.in_planes + (uint64_t)id * a.in_pitch : a.in_rid;
+    };
+    auto dst_of = [&](int k) -> uint32_t* {
+        int id = stream_plane(k, dp, np);
+        return id >= 0 ? a.out_planes + (uint64_t)id * a.out_pitch : a.out_rid;
+    };
+    auto full = [&](uint32_t t) { return a.tma && t < ntiles && (uint64_t)(t + 1) * TILE <= n; };
+
+    // producer (thread 0): next stream to issue is stream p_k of tile p_t into slot p_slot
+    uint32_t p_t = blockIdx.x;
+    int p_k = 0, p_slot = 0;
+    auto produce = [&]() {
+        if (full(p_t)) {
+            proxy_fence();
+            bulk_load(ring + (size_t)p_slot * TILE, src_of(p_k) + (uint64_t)p_t * TILE, TILE * 4, &s_bar[p_slot]);
+        }
+        if (++p_slot == R) p_slot = 0;
+        if (++p_k == L) { p_k = 0; p_t += G; }
+    };
+    if (tid == 0) {
+        for (int sl = 0; sl < R; sl++) bar_init(&s_bar[sl]);
+        bar_fence_init();
+        for (int sl = 0; sl < R; sl++) produce();
+    }
+    __syncthreads();
+
+    int c_slot = 0, c_round = 0;
+    const uint32_t wofs = (uint32_t)warp * 32 * ITEMS;
+    const uint32_t ltm = lt_mask();
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += G) {
+        const uint64_t base = (uint64_t)tile * TILE;
+        const uint32_t tile_n = (uint32_t)(n - base < (uint64_t)TILE ? n - base : (uint64_t)TILE);
+        const bool tma_t = full(tile);
+        // global position of this tile's first key of digit tid (loads overlap the ranking)
+        const uint32_t goff = a.chunk_tot[(uint64_t)(tile / a.chunk_tiles) * kRadix + tid] +
+                              a.tile_off[(uint64_t)tile * kRadix + tid];
+#pragma unroll
+        for (int k = 0; k < kW; k++) s_hist[k][tid] = 0;
+        __syncthreads();
+
+        auto acquire = [&](int k) -> const uint32_t* {
+            uint32_t* slot = ring + (size_t)c_slot * TILE;
+            if (tma_t) {
+                bar_wait(&s_bar[c_slot], (uint32_t)c_round & 1u);
+            } else {
+                const uint32_t* src = src_of(k) + base;
+                for (uint32_t i = tid; i < tile_n; i += kSortThreads) slot[i] = __ldg(src + i);
+                __syncthreads();
+            }
+            return slot;
+        };
+        auto release = [&]() {                                   // call after a __syncthreads
+            if (tid == 0) produce();
+            if (++c_slot == R) { c_slot = 0; c_round++; }
+        };
+
+        // ---- rank within warps
+        const uint32_t* dslot = acquire(0);
+        if (a.debug & 2) goto skip_rank;
+        {
+        uint32_t* h = s_hist[warp];
+        uint32_t pos[ITEMS];
+        uint32_t dg[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            uint32_t idx = wofs + i * 32 + lane;
+            dg[i] = idx < tile_n ? (dslot[idx] >> a.shift) & 0xFF : 0x100u;
+        }
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const bool valid = dg[i] < 0x100u;
+            uint32_t peers;
+            if (a.debug & 4) {
+                peers = __match_any_sync(0xffffffffu, dg[i]);
+                if (!valid) peers = 0;
+            } else {
+                peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+                for (int b = 0; b < 8; b++) {
+                    uint32_t bit = (dg[i] >> b) & 1u;
+                    uint32_t bal = __ballot_sync(0xffffffffu, bit);
+                    peers &= bit ? bal : ~bal;
+                }
+            }
+            const uint32_t lower = __popc(peers & ltm);
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (valid && lower == 0) old = atomicAdd(&h[dg[i]], (uint32_t)__popc(peers));
+            old = __shfl_sync(0xffffffffu, old, leader < 0 ? lane : leader);
+            pos[i] = old + lower;
+        }
+        __syncthreads();
+
+        // ---- warp offsets, tile-local digit offsets, global bases
+        uint32_t total = 0;
+#pragma unroll
+        for (int k = 0; k < kW; k++) {
+            uint32_t c = s_hist[k][tid];
+            s_hist[k][tid] = total;
+            total += c;
+        }
+        const uint32_t excl = scan256(total, s_warp);
+        s_local[tid] = excl;
+        s_gbase[tid] = goff - excl;
+        __syncthreads();
+
+        // ---- digit order of the tile: for every output slot s, the tile index of its key
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            if (dg[i] < 0x100u) {
+                uint32_t p = pos[i] + s_local[dg[i]] + s_hist[warp][dg[i]];
+                s_src[p] = (uint16_t)(wofs + i * 32 + lane);
+                s_dig[p] = (uint8_t)dg[i];
+            }
+        }
+        __syncthreads();
+        }
+        skip_rank:
+        uint32_t dest[ITEMS], from[ITEMS];
+#pragma unroll
+        for (int r = 0; r < ITEMS; r++) {
+            uint32_t s = r * kSortThreads + tid;
+            if (s < tile_n) {
+                from[r] = (a.debug & 3) ? s : s_src[s];
+                dest[r] = (a.debug & 3) ? (uint32_t)base + s : s_gbase[s_dig[s]] + s;
+            }
+        }
+        // ---- every stream: gather from its slot in digit order, write coalesced runs
+        {
+            uint32_t* out = dst_of(0);
+#pragma unroll
+            for (int r = 0; r < ITEMS; r++)
+                if (r * kSortThreads + tid < tile_n) out[dest[r]] = dslot[from[r]];
+        }
+        __syncthreads();
+        release();
+        for (int k = 1; k < S; k++) {
+            uint32_t* out = dst_of(k);
+            if (k == S - 1 && implicit_rid) {
+#pragma unroll
+                for (int r = 0; r < ITEMS; r++)
+                    if (r * kSortThreads + tid < tile_n) out[dest[r]] = (uint32_t)base + from[r];
+            } else {
+                const uint32_t* slot = acquire(k);
+#pragma unroll
+                for (int r = 0; r < ITEMS; r++)
+                    if (r * kSortThreads + tid < tile_n) out[dest[r]] = slot[from[r]];
+                __syncthreads();
+                release();
+            }
+        }
+    }
+}
+
+// ---- launch ---------------------------------------------------------------------------------
+
+static int g_lsd_items = 0, g_lsd_slots = 0, g_lsd_chunk = 0;
+
+static void lsd_config() {
+    if (g_lsd_items) return;
+    const char* e = getenv("CKS_LSD_ITEMS");
+    g_lsd_items = e ? atoi(e) : 16;
+    if (g_lsd_items != 8 && g_lsd_items != 16) g_lsd_items = 16;
+    const char* s = getenv("CKS_LSD_SLOTS");
+    g_lsd_slots = s ? atoi(s) : 4;
+    if (g_lsd_slots < 1) g_lsd_slots = 1;
+    if (g_lsd_slots > 8) g_lsd_slots = 8;
+    const char* c = getenv("CKS_LSD_CHUNK");
+    g_lsd_chunk = c ? atoi(c) : 16;
+    if (g_lsd_chunk < 1) g_lsd_chunk = 1;
+}
+
+uint64_t lsd_tile_keys() {
+    lsd_config();
+    return (uint64_t)kSortThreads * g_lsd_items;
+}
+
+void lsd_sizes(uint64_t n, uint64_t* tiles, uint64_t* chunks) {
+    uint64_t t = lsd_tile_keys();
+    *tiles = (n + t - 1) / t;
+    *chunks = (*tiles + g_lsd_chunk - 1) / g_lsd_chunk;
+}
+
+template <int ITEMS>
+static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, int* launches) {
+    constexpr int TILE = kSortThreads * ITEMS;
+    const uint64_t tiles = (a.n + TILE - 1) / TILE;
+    const uint64_t chunks = (tiles + a.chunk_tiles - 1) / a.chunk_tiles;
+    cudaMemsetAsync(a.total, 0, kRadix * 4, st);
+    k_upsweep<ITEMS><<<(unsigned)chunks, kSortThreads, 0, st>>>(a);
+    k_chunk_scan<<<kRadix / 32, 1024, 0, st>>>(a, (uint32_t)chunks);
+    int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
+    if ((int)a.slots > streams) a.slots = streams > 0 ? streams : 1;
+    size_t smem = (size_t)a.slots * TILE * 4 + kW * kRadix * 4 + (size_t)TILE * 3;
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_downsweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_downsweep<ITEMS>, kSortThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)sms * per_sm;
+    if (grid > tiles) grid = tiles;
+    k_downsweep<ITEMS><<<(unsigned)grid, kSortThreads, smem, st>>>(a);
+    *launches = 3;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lsd_pass(const LsdPassArgs& args, int sms, cudaStream_t st, int* launches) {
+    *launches = 0;
+    if (args.n == 0) return cudaSuccess;
+    lsd_config();
+    LsdPassArgs a = args;
+    a.slots = (uint32_t)g_lsd_slots;
+    a.chunk_tiles = (uint32_t)g_lsd_chunk;
+    static int dbg = -1;
+    if (dbg < 0) { const char* e = getenv("CKS_LSD_DEBUG"); dbg = e ? atoi(e) : 0; }
+    a.debug = (uint32_t)dbg;
+    a.tma = ((uintptr_t)a.in_planes % 16 == 0) && (a.in_pitch % 4 == 0) &&
+            (a.in_rid == nullptr || (uintptr_t)a.in_rid % 16 == 0);
+    return g_lsd_items == 8 ? lsd_pass<8>(a, sms, st, launches) : lsd_pass<16>(a, sms, st, launches);
+}
+
+}  // namespace cks
