@@ -374,13 +374,15 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
     L.nodes = s.level_nodes[0];
     L.node_off = 0;
     L.span = 1;
-    LAUNCH(launch_bulk_leaves(perm, dbit, L, fanout, per, t->node_cnt, t->entry_rid, t->entry_dbit, nullptr,
-                              ctx->stream));
-    if (s.height > 1 && dbit) {
+    // per-node minima of D_k (rmin) ping-pong between two scratch buffers, level by level
+    const bool mins = dbit && s.height > 1;
+    if (mins) {
         TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
         TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
     }
-    const uint16_t* rbelow = dbit;
+    LAUNCH(launch_bulk_leaves(perm, dbit, L, fanout, per, t->node_cnt, t->entry_rid, t->entry_dbit,
+                              mins ? as<uint16_t>(ctx->rmin0) : nullptr, ctx->sms, ctx->stream));
+    const uint16_t* rbelow = mins ? as<uint16_t>(ctx->rmin0) : nullptr;
     uint64_t span = per;
     for (uint32_t l = 1; l < s.height; l++) {
         BulkLevel I{};
@@ -389,9 +391,9 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
         I.node_off = s.level_offset[l];
         I.below_off = s.level_offset[l - 1];
         I.span = span;
-        uint16_t* rout = dbit ? ((l & 1) ? as<uint16_t>(ctx->rmin0) : as<uint16_t>(ctx->rmin1)) : nullptr;
+        uint16_t* rout = mins ? ((l & 1) ? as<uint16_t>(ctx->rmin1) : as<uint16_t>(ctx->rmin0)) : nullptr;
         LAUNCH(launch_bulk_inner(perm, rbelow, I, n, fanout, per, t->node_cnt, t->entry_rid, t->entry_dbit,
-                                 t->entry_child, s.level_offset[1], rout, ctx->stream));
+                                 t->entry_child, s.level_offset[1], rout, ctx->sms, ctx->stream));
         rbelow = rout;
         span *= per;
     }

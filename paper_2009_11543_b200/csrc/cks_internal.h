@@ -120,10 +120,10 @@ struct BulkLevel {
 };
 cudaError_t launch_bulk_leaves(const uint32_t* perm, const uint16_t* dbit, const BulkLevel& L,
                                uint32_t fanout, uint32_t per, uint32_t* node_cnt, uint32_t* rid,
-                               uint16_t* edbit, uint16_t* rmin, cudaStream_t st);
+                               uint16_t* edbit, uint16_t* rmin, int sms, cudaStream_t st);
 cudaError_t launch_bulk_inner(const uint32_t* perm, const uint16_t* rmin_below, const BulkLevel& L,
                               uint64_t n, uint32_t fanout, uint32_t per, uint32_t* node_cnt,
                               uint32_t* rid, uint16_t* edbit, uint32_t* child, uint64_t inner_off,
-                              uint16_t* rmin, cudaStream_t st);
+                              uint16_t* rmin, int sms, cudaStream_t st);
 
 }  // namespace cks

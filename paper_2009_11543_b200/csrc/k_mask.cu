@@ -120,12 +120,73 @@ __global__ void k_occ_finalize(const uint32_t* __restrict__ occ, uint32_t B, uin
     }
 }
 
+// Specialised path for a compile-time key width B in {8, 16, 32, 64} (16-byte aligned
+// keys): each 16-byte chunk covers byte positions j0 + 0..15 (j0 = 16c mod B, 0 for B <= 16),
+// so every byte's occupancy word is a compile-time offset from one row pointer; the
+// test-before-set is one shared load, one test and one predicated shared reduction (no
+// branch). Loads of U chunks are issued before any test.
+__device__ __forceinline__ void red_or_if(uint32_t* p, uint32_t bit, uint32_t cur) {
+    asm volatile("{\n .reg .pred q;\n setp.eq.u32 q, %2, 0;\n @q red.shared.or.b32 [%0], %1;\n}"
+                 ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(bit), "r"(cur & bit) : "memory");
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) k_occupancy_fixed(const uint8_t* __restrict__ keys, uint64_t nchunks,
+                                                         uint32_t* __restrict__ occ_g) {
+    __shared__ uint32_t occ[B * 9];
+    for (uint32_t i = threadIdx.x; i < B * 9; i += blockDim.x) occ[i] = 0;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    constexpr int U = 2;
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += U * stride) {
+        int4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            v[u] = (c + u * stride < nchunks) ? ld_stream16(keys + ((c + u * stride) << 4)) : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (c + u * stride >= nchunks) break;
+            const uint32_t j0 = B > 16 ? (uint32_t)(((c + u * stride) << 4) & (B - 1)) : 0u;
+            uint32_t* row = occ + j0 * 9;
+            const uint32_t w[4] = {(uint32_t)v[u].x, (uint32_t)v[u].y, (uint32_t)v[u].z, (uint32_t)v[u].w};
+            uint32_t* ptr[16];
+            uint32_t bit[16], cur[16];
+#pragma unroll
+            for (int b = 0; b < 16; b++) {
+                const uint32_t x = w[b >> 2] >> (8 * (b & 3));
+                const int jr = B >= 16 ? b : (b & (B - 1));
+                ptr[b] = row + jr * 9 + ((x >> 5) & 7);
+                bit[b] = 1u << (x & 31);
+            }
+#pragma unroll
+            for (int b = 0; b < 16; b++) cur[b] = *ptr[b];
+#pragma unroll
+            for (int b = 0; b < 16; b++) red_or_if(ptr[b], bit[b], cur[b]);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) {
+        uint32_t x = occ[(i >> 3) * 9 + (i & 7)];
+        if (x) atomicOr(&occ_g[i], x);
+    }
+}
+
 cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32_t* occ,
                              int sms, cudaStream_t st) {
     size_t smem = (size_t)B * 9 * sizeof(uint32_t);
     bool pow2 = (B & (B - 1)) == 0;
     bool aligned = ((uintptr_t)keys & 15) == 0;
-    if (pow2 && aligned) {
+    if (aligned && (B == 8 || B == 16 || B == 32 || B == 64) && ((n * B) & 15) == 0) {
+        uint64_t nchunks = (n * B) >> 4;
+        uint64_t want = (nchunks + 255) / 256;
+        int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
+        switch (B) {
+            case 8: k_occupancy_fixed<8><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+            case 16: k_occupancy_fixed<16><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+            case 32: k_occupancy_fixed<32><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+            default: k_occupancy_fixed<64><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+        }
+    } else if (pow2 && aligned) {
         uint64_t nchunks = (n * B) >> 4;
         uint64_t want = (nchunks + 255) / 256;
         int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
