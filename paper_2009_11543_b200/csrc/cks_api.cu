@@ -169,7 +169,7 @@ int run_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     if (n == 0 || m == 0) return CKS_OK;
     GatherPlan* dplan;
     TRY(upload_plan(ctx, 0, &dplan));
-    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0]->nsteps, np, planes, pitch, ctx->sms, ctx->stream));
+    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, planes, pitch, ctx->sms, ctx->stream));
     return CKS_OK;
 }
 

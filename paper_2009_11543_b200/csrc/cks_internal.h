@@ -47,7 +47,7 @@ cudaError_t launch_occ_finalize(const uint32_t* occ, uint32_t B, uint64_t n, uin
 // elements; user buffers have pitch n, library scratch pads the pitch to 32 elements so every
 // plane is 128-byte aligned for TMA).
 cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
-                            uint32_t nsteps, uint32_t out_planes, uint32_t* planes, uint64_t pitch,
+                            const GatherPlan* hplan, uint32_t out_planes, uint32_t* planes, uint64_t pitch,
                             int sms, cudaStream_t st);
 cudaError_t launch_repack(const uint32_t* in_planes, uint64_t in_pitch, uint64_t n, const GatherPlan* dplan,
                           uint32_t nsteps, uint32_t out_planes, uint32_t* out, uint64_t out_pitch, int sms,

@@ -12,6 +12,8 @@
 // Keys are staged through shared memory with coalesced 16-byte loads; each row is
 // padded to an odd number of 16-byte units so a thread's 16-byte reads of its own row
 // are bank-conflict free (8 lanes per phase hit 8 distinct 16-byte bank groups).
+#include <string.h>
+
 #include "cks_internal.h"
 
 namespace cks {
@@ -151,6 +153,77 @@ k_repack(const uint32_t* __restrict__ in, uint64_t in_pitch, uint64_t n, const G
     }
 }
 
+// Fixed key width B in {8, 16, 32, 64}, 16-byte aligned keys: the per-word gather masks are
+// a kernel parameter (constant bank) indexed by compile-time word numbers, the word loop is
+// fully unrolled, and each thread loads its own key with 8- or 16-byte loads (for B >= 32 the
+// later loads of a key hit the sectors its first load brought into L1).
+template <int NW>
+struct FixedPlan {
+    uint32_t mask[NW];
+    uint32_t mv[NW][5];
+    uint32_t cnt[NW];
+};
+
+template <int B>
+__global__ void __launch_bounds__(kCompressThreads)
+k_compress_fixed(const uint8_t* __restrict__ keys, uint64_t n, const __grid_constant__ FixedPlan<B / 4> plan,
+                 uint32_t* __restrict__ planes, uint64_t pitch) {
+    constexpr int NW = B / 4;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t w[NW];
+        if (B == 8) {
+            uint2 v = __ldg(reinterpret_cast<const uint2*>(keys + i * B));
+            w[0] = v.x;
+            w[1] = v.y;
+        } else {
+#pragma unroll
+            for (int u = 0; u < B / 16; u++) {
+                uint4 v = __ldg(reinterpret_cast<const uint4*>(keys + i * B) + u);
+                w[4 * u + 0] = v.x;
+                w[4 * u + 1] = v.y;
+                w[4 * u + 2] = v.z;
+                w[4 * u + 3] = v.w;
+            }
+        }
+        unsigned long long acc = 0;
+        uint32_t accbits = 0, q = 0;
+#pragma unroll
+        for (int k = NW - 1; k >= 0; k--) {                      // least significant end of P first
+            if (plan.mask[k] == 0) continue;
+            uint32_t x = bswap32(w[k]) & plan.mask[k];
+#pragma unroll
+            for (int s = 0; s < 5; s++) {
+                uint32_t t = x & plan.mv[k][s];
+                x = (x ^ t) | (t >> (1u << s));
+            }
+            acc |= (unsigned long long)x << accbits;
+            accbits += plan.cnt[k];
+            if (accbits >= 32) {
+                planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
+                acc >>= 32;
+                accbits -= 32;
+                q++;
+            }
+        }
+        if (accbits) planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
+    }
+}
+
+template <int B>
+static void launch_fixed(const uint8_t* keys, uint64_t n, const GatherPlan* hplan, uint32_t* planes, uint64_t pitch,
+                         int grid, cudaStream_t st) {
+    FixedPlan<B / 4> fp;
+    memset(&fp, 0, sizeof(fp));
+    for (uint32_t s = 0; s < hplan->nsteps; s++) {
+        const GatherStep& g = hplan->step[s];
+        fp.mask[g.src] = g.mask;
+        for (int k = 0; k < 5; k++) fp.mv[g.src][k] = g.mv[k];
+        fp.cnt[g.src] = g.cnt;
+    }
+    k_compress_fixed<B><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch);
+}
+
 static int grid_for(uint64_t work, int per_sm, int sms) {
     uint64_t want = (work + 255) / 256;
     uint64_t cap = (uint64_t)sms * per_sm;
@@ -159,9 +232,20 @@ static int grid_for(uint64_t work, int per_sm, int sms) {
 }
 
 cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
-                            uint32_t nsteps, uint32_t np, uint32_t* planes, uint64_t pitch, int sms,
+                            const GatherPlan* hplan, uint32_t np, uint32_t* planes, uint64_t pitch, int sms,
                             cudaStream_t st) {
     if (n == 0 || np == 0) return cudaSuccess;
+    const uint32_t nsteps = hplan->nsteps;
+    if (((uintptr_t)keys & 15) == 0 && (B == 8 || B == 16 || B == 32 || B == 64)) {
+        int grid = grid_for(n, 8, sms);
+        switch (B) {
+            case 8: launch_fixed<8>(keys, n, hplan, planes, pitch, grid, st); break;
+            case 16: launch_fixed<16>(keys, n, hplan, planes, pitch, grid, st); break;
+            case 32: launch_fixed<32>(keys, n, hplan, planes, pitch, grid, st); break;
+            default: launch_fixed<64>(keys, n, hplan, planes, pitch, grid, st); break;
+        }
+        return cudaGetLastError();
+    }
     if ((B & 15) == 0 && ((uintptr_t)keys & 15) == 0) {
         uint32_t S16 = (B >> 4) | 1;
         size_t smem = (size_t)kCompressThreads * S16 * 16;

@@ -120,24 +120,23 @@ __global__ void k_occ_finalize(const uint32_t* __restrict__ occ, uint32_t B, uin
     }
 }
 
-// Specialised path for a compile-time key width B in {8, 16, 32, 64} (16-byte aligned
-// keys): each 16-byte chunk covers byte positions j0 + 0..15 (j0 = 16c mod B, 0 for B <= 16),
-// so every byte's occupancy word is a compile-time offset from one row pointer; the
-// test-before-set is one shared load, one test and one predicated shared reduction (no
-// branch). Loads of U chunks are issued before any test.
-__device__ __forceinline__ void red_or_if(uint32_t* p, uint32_t bit, uint32_t cur) {
-    asm volatile("{\n .reg .pred q;\n setp.eq.u32 q, %2, 0;\n @q red.shared.or.b32 [%0], %1;\n}"
-                 ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(bit), "r"(cur & bit) : "memory");
-}
+// Specialised path for a compile-time key width B in {8, 16, 32, 64} (16-byte aligned keys).
+// Occupancy is kept as one flag BYTE per (position, value) in shared memory, so marking a
+// byte is a plain store of 1 -- no load, no test, no atomic (every writer stores the same
+// value): extract the byte (PRMT), add it to the position's row, store. Rows are padded by 4
+// bytes so positions 16 apart (the two halves of a warp when B = 32) use different banks.
+// Each thread keeps U 16-byte chunks in flight. The flags are folded into the u32 bitsets
+// at the end.
+constexpr int kRowBytes = 260;
 
 template <int B>
-__global__ void __launch_bounds__(256) k_occupancy_fixed(const uint8_t* __restrict__ keys, uint64_t nchunks,
+__global__ void __launch_bounds__(256) k_occupancy_bytes(const uint8_t* __restrict__ keys, uint64_t nchunks,
                                                          uint32_t* __restrict__ occ_g) {
-    __shared__ uint32_t occ[B * 9];
-    for (uint32_t i = threadIdx.x; i < B * 9; i += blockDim.x) occ[i] = 0;
+    __shared__ __align__(16) uint8_t flag[B * kRowBytes];
+    for (uint32_t i = threadIdx.x; i < B * kRowBytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(flag)[i] = 0;
     __syncthreads();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    constexpr int U = 2;
+    constexpr int U = 4;
     for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += U * stride) {
         int4 v[U];
 #pragma unroll
@@ -147,27 +146,30 @@ __global__ void __launch_bounds__(256) k_occupancy_fixed(const uint8_t* __restri
         for (int u = 0; u < U; u++) {
             if (c + u * stride >= nchunks) break;
             const uint32_t j0 = B > 16 ? (uint32_t)(((c + u * stride) << 4) & (B - 1)) : 0u;
-            uint32_t* row = occ + j0 * 9;
+            uint8_t* row = flag + j0 * kRowBytes;
             const uint32_t w[4] = {(uint32_t)v[u].x, (uint32_t)v[u].y, (uint32_t)v[u].z, (uint32_t)v[u].w};
-            uint32_t* ptr[16];
-            uint32_t bit[16], cur[16];
 #pragma unroll
             for (int b = 0; b < 16; b++) {
-                const uint32_t x = w[b >> 2] >> (8 * (b & 3));
                 const int jr = B >= 16 ? b : (b & (B - 1));
-                ptr[b] = row + jr * 9 + ((x >> 5) & 7);
-                bit[b] = 1u << (x & 31);
+                const uint32_t val = __byte_perm(w[b >> 2], 0, 0x4440 + (b & 3));
+                row[jr * kRowBytes + val] = 1;
             }
-#pragma unroll
-            for (int b = 0; b < 16; b++) cur[b] = *ptr[b];
-#pragma unroll
-            for (int b = 0; b < 16; b++) red_or_if(ptr[b], bit[b], cur[b]);
         }
     }
     __syncthreads();
+    // fold: thread per (position, word): 32 flags -> one u32
     for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) {
-        uint32_t x = occ[(i >> 3) * 9 + (i & 7)];
-        if (x) atomicOr(&occ_g[i], x);
+        const uint8_t* f = flag + (i >> 3) * kRowBytes + (i & 7) * 32;
+        uint32_t bits = 0;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+            uint32_t q = *reinterpret_cast<const uint32_t*>(f + k);
+            bits |= ((q & 0xFF) ? 1u : 0u) << k;
+            bits |= ((q & 0xFF00) ? 1u : 0u) << (k + 1);
+            bits |= ((q & 0xFF0000) ? 1u : 0u) << (k + 2);
+            bits |= ((q & 0xFF000000) ? 1u : 0u) << (k + 3);
+        }
+        if (bits) atomicOr(&occ_g[i], bits);
     }
 }
 
@@ -181,10 +183,10 @@ cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32
         uint64_t want = (nchunks + 255) / 256;
         int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
         switch (B) {
-            case 8: k_occupancy_fixed<8><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
-            case 16: k_occupancy_fixed<16><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
-            case 32: k_occupancy_fixed<32><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
-            default: k_occupancy_fixed<64><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+            case 8: k_occupancy_bytes<8><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+            case 16: k_occupancy_bytes<16><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+            case 32: k_occupancy_bytes<32><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+            default: k_occupancy_bytes<64><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
         }
     } else if (pow2 && aligned) {
         uint64_t nchunks = (n * B) >> 4;
