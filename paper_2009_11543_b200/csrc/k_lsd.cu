@@ -176,21 +176,64 @@ k_chunk_scan(const LsdPassArgs a, uint32_t nchunks) {
 }
 
 // ---- downsweep ----------------------------------------------------------------------------
+// Warp match of an NB-bit label: lanes whose label equals this lane's (bit-plane ballots;
+// and+setp fold into one LOP3 with a predicate output, so ~4 SASS per bit).
+template <int NB>
+__device__ __forceinline__ uint32_t match_bits(uint32_t d) {
+    uint32_t peers = 0xFFFFFFFFu;
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        uint32_t m;
+        asm("{\n .reg .pred p;\n .reg .b32 t;\n and.b32 t, %1, %2;\n setp.ne.u32 p, t, 0;\n"
+            " vote.sync.ballot.b32 %0, p, 0xffffffff;\n @!p not.b32 %0, %0;\n}"
+            : "=r"(m) : "r"(d), "r"(1u << b));
+        peers &= m;
+    }
+    return peers;
+}
+
+// One tile of the downsweep. FULL = TILE keys and the streams arrived by TMA; otherwise
+// `tile_n` keys (lanes past the end carry label 256 and take positions nobody reads).
+template <int ITEMS, bool FULL>
+__device__ __forceinline__ void rank_tile(const uint32_t* dslot, uint32_t shift, uint32_t tile_n, uint32_t wofs,
+                                          uint32_t lane, uint32_t ltm, uint32_t* h, uint32_t (&dg)[ITEMS],
+                                          uint32_t (&pos)[ITEMS]) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const uint32_t idx = wofs + i * 32 + lane;
+        dg[i] = (FULL || idx < tile_n) ? (dslot[idx] >> shift) & 0xFF : 0x100u;
+    }
+    uint32_t peers[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) peers[i] = match_bits<FULL ? 8 : 9>(dg[i]);
+    // warp-private bins: every peer reads the running count, then the group's lowest lane
+    // (unique per label) adds the group size -- in issue order, so the rank is stable
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const uint32_t lower = __popc(peers[i] & ltm);
+        const uint32_t old = h[dg[i]];
+        __syncwarp();
+        if (lower == 0) h[dg[i]] = old + __popc(peers[i]);
+        __syncwarp();
+        pos[i] = old + lower;
+    }
+}
+
 template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads, ITEMS == 8 ? 4 : 2)
 k_downsweep(const LsdPassArgs a) {
     constexpr int TILE = kSortThreads * ITEMS;
+    constexpr int HW = kRadix + 8;                            // bin row (+ label 256 of tail lanes)
     extern __shared__ __align__(128) uint8_t s_dyn[];
-    uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                   // [R][TILE]
-    uint32_t (*s_hist)[kRadix] = reinterpret_cast<uint32_t (*)[kRadix]>(ring + (size_t)a.slots * TILE); // [8][256]
-    uint16_t* s_src = reinterpret_cast<uint16_t*>(&s_hist[kW][0]);                     // [TILE]
-    uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_src + TILE);                         // [TILE]
-    __shared__ uint32_t s_local[kRadix];
-    __shared__ uint32_t s_gbase[kRadix];
+    uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                                   // [R][TILE]
+    uint32_t* s_hist = ring + (size_t)a.slots * TILE;                                     // [kW][HW]
+    uint32_t* s_dst = s_hist + kW * HW;                                                   // [TILE]
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_dst + TILE);                          // [TILE]
     __shared__ uint32_t s_warp[kW];
-    __shared__ __align__(8) uint64_t s_bar[8];
+    __shared__ uint32_t s_gb[kRadix];
+    __shared__ __align__(8) uint64_t s_bar[16];
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t n = a.n;
     const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
     const uint32_t G = gridDim.x;
@@ -198,7 +241,7 @@ k_downsweep(const LsdPassArgs a) {
     const int S = np + 1;
     const bool implicit_rid = a.in_rid == nullptr;
     const int L = S - (implicit_rid ? 1 : 0);                   // loaded streams per tile
-    const int R = L < (int)a.slots ? L : (int)a.slots;
+    const int R = (int)a.slots;
 
     auto src_of = [&](int k) -> const uint32_t* {
         int id = stream_plane(k, dp, np);
@@ -210,8 +253,7 @@ k_downsweep(const LsdPassArgs a) {
     };
     auto full = [&](uint32_t t) { return a.tma && t < ntiles && (uint64_t)(t + 1) * TILE <= n; };
 
-    // producer (thread 0): next stream to issue is stream p_k of tile p_t into slot p_slot
-    uint32_t p_t = blockIdx.x;
+    uint32_t p_t = blockIdx.x;                                   // producer (thread 0) cursor
     int p_k = 0, p_slot = 0;
     auto produce = [&]() {
         if (full(p_t)) {
@@ -229,19 +271,15 @@ k_downsweep(const LsdPassArgs a) {
     __syncthreads();
 
     int c_slot = 0, c_round = 0;
-    const uint32_t wofs = (uint32_t)warp * 32 * ITEMS;
+    const uint32_t wofs = warp * 32 * ITEMS;
     const uint32_t ltm = lt_mask();
+    uint32_t* h = s_hist + warp * HW;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += G) {
         const uint64_t base = (uint64_t)tile * TILE;
         const uint32_t tile_n = (uint32_t)(n - base < (uint64_t)TILE ? n - base : (uint64_t)TILE);
         const bool tma_t = full(tile);
-        // global position of this tile's first key of digit tid (loads overlap the ranking)
         const uint32_t goff = a.chunk_tot[(uint64_t)(tile / a.chunk_tiles) * kRadix + tid] +
                               a.tile_off[(uint64_t)tile * kRadix + tid];
-#pragma unroll
-        for (int k = 0; k < kW; k++) s_hist[k][tid] = 0;
-        __syncthreads();
-
         auto acquire = [&](int k) -> const uint32_t* {
             uint32_t* slot = ring + (size_t)c_slot * TILE;
             if (tma_t) {
@@ -253,105 +291,68 @@ k_downsweep(const LsdPassArgs a) {
             }
             return slot;
         };
-        auto release = [&]() {                                   // call after a __syncthreads
+        auto release = [&]() {                                   // after a __syncthreads
             if (tid == 0) produce();
             if (++c_slot == R) { c_slot = 0; c_round++; }
         };
 
-        // ---- rank within warps
+        // ---- rank: warp-private bins (each warp clears its own row)
+#pragma unroll
+        for (int j = lane; j < HW; j += 32) h[j] = 0;
+        __syncwarp();
         const uint32_t* dslot = acquire(0);
-        if (a.debug & 2) goto skip_rank;
+        uint32_t dg[ITEMS], pos[ITEMS];
+        if (tile_n == TILE) rank_tile<ITEMS, true>(dslot, a.shift, tile_n, wofs, lane, ltm, h, dg, pos);
+        else rank_tile<ITEMS, false>(dslot, a.shift, tile_n, wofs, lane, ltm, h, dg, pos);
+        __syncthreads();
+
+        // ---- digit tid: warp offsets, tile-local base, global base
         {
-        uint32_t* h = s_hist[warp];
-        uint32_t pos[ITEMS];
-        uint32_t dg[ITEMS];
+            uint32_t c[kW], total = 0;
 #pragma unroll
-        for (int i = 0; i < ITEMS; i++) {
-            uint32_t idx = wofs + i * 32 + lane;
-            dg[i] = idx < tile_n ? (dslot[idx] >> a.shift) & 0xFF : 0x100u;
-        }
+            for (int k = 0; k < kW; k++) { c[k] = s_hist[k * HW + tid]; total += c[k]; }
+            const uint32_t excl = scan256(total, s_warp);
+            // row k of the bins becomes the tile position of warp k's first key of digit tid;
+            // slot p of digit tid goes to global position p + (goff - excl)
+            uint32_t run = excl;
 #pragma unroll
-        for (int i = 0; i < ITEMS; i++) {
-            const bool valid = dg[i] < 0x100u;
-            uint32_t peers;
-            if (a.debug & 4) {
-                peers = __match_any_sync(0xffffffffu, dg[i]);
-                if (!valid) peers = 0;
-            } else {
-                peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-                for (int b = 0; b < 8; b++) {
-                    uint32_t bit = (dg[i] >> b) & 1u;
-                    uint32_t bal = __ballot_sync(0xffffffffu, bit);
-                    peers &= bit ? bal : ~bal;
-                }
-            }
-            const uint32_t lower = __popc(peers & ltm);
-            const int leader = __ffs(peers) - 1;
-            uint32_t old = 0;
-            if (valid && lower == 0) old = atomicAdd(&h[dg[i]], (uint32_t)__popc(peers));
-            old = __shfl_sync(0xffffffffu, old, leader < 0 ? lane : leader);
-            pos[i] = old + lower;
+            for (int k = 0; k < kW; k++) { s_hist[k * HW + tid] = run; run += c[k]; }
+            s_gb[tid] = goff - excl;
         }
         __syncthreads();
-
-        // ---- warp offsets, tile-local digit offsets, global bases
-        uint32_t total = 0;
-#pragma unroll
-        for (int k = 0; k < kW; k++) {
-            uint32_t c = s_hist[k][tid];
-            s_hist[k][tid] = total;
-            total += c;
-        }
-        const uint32_t excl = scan256(total, s_warp);
-        s_local[tid] = excl;
-        s_gbase[tid] = goff - excl;
-        __syncthreads();
-
-        // ---- digit order of the tile: for every output slot s, the tile index of its key
+        // ---- tile permutation: slot p <- key (warp, item, lane); its global destination
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
-            if (dg[i] < 0x100u) {
-                uint32_t p = pos[i] + s_local[dg[i]] + s_hist[warp][dg[i]];
+            if (tile_n == TILE || dg[i] < 0x100u) {
+                const uint32_t p = pos[i] + h[dg[i]];
                 s_src[p] = (uint16_t)(wofs + i * 32 + lane);
-                s_dig[p] = (uint8_t)dg[i];
+                s_dst[p] = p + s_gb[dg[i]];
             }
         }
         __syncthreads();
-        }
-        skip_rank:
-        uint32_t dest[ITEMS], from[ITEMS];
+        uint32_t from[ITEMS], dest[ITEMS];
 #pragma unroll
         for (int r = 0; r < ITEMS; r++) {
-            uint32_t s = r * kSortThreads + tid;
-            if (s < tile_n) {
-                from[r] = (a.debug & 3) ? s : s_src[s];
-                dest[r] = (a.debug & 3) ? (uint32_t)base + s : s_gbase[s_dig[s]] + s;
-            }
+            const uint32_t s = r * kSortThreads + tid;
+            from[r] = s_src[s];
+            dest[r] = s_dst[s];
         }
         // ---- every stream: gather from its slot in digit order, write coalesced runs
-        {
-            uint32_t* out = dst_of(0);
-#pragma unroll
-            for (int r = 0; r < ITEMS; r++)
-                if (r * kSortThreads + tid < tile_n) out[dest[r]] = dslot[from[r]];
-        }
-        __syncthreads();
-        release();
-        for (int k = 1; k < S; k++) {
+        for (int k = 0; k < S; k++) {
             uint32_t* out = dst_of(k);
             if (k == S - 1 && implicit_rid) {
+                const uint32_t b32 = (uint32_t)base;
 #pragma unroll
                 for (int r = 0; r < ITEMS; r++)
-                    if (r * kSortThreads + tid < tile_n) out[dest[r]] = (uint32_t)base + from[r];
-            } else {
-                const uint32_t* slot = acquire(k);
-#pragma unroll
-                for (int r = 0; r < ITEMS; r++)
-                    if (r * kSortThreads + tid < tile_n) out[dest[r]] = slot[from[r]];
-                __syncthreads();
-                release();
+                    if (tile_n == TILE || r * kSortThreads + tid < tile_n) out[dest[r]] = b32 + from[r];
+                continue;
             }
+            const uint32_t* slot = k == 0 ? dslot : acquire(k);
+#pragma unroll
+            for (int r = 0; r < ITEMS; r++)
+                if (tile_n == TILE || r * kSortThreads + tid < tile_n) out[dest[r]] = slot[from[r]];
+            __syncthreads();
+            release();
         }
     }
 }
@@ -368,7 +369,7 @@ static void lsd_config() {
     const char* s = getenv("CKS_LSD_SLOTS");
     g_lsd_slots = s ? atoi(s) : 4;
     if (g_lsd_slots < 1) g_lsd_slots = 1;
-    if (g_lsd_slots > 8) g_lsd_slots = 8;
+    if (g_lsd_slots > 16) g_lsd_slots = 16;
     const char* c = getenv("CKS_LSD_CHUNK");
     g_lsd_chunk = c ? atoi(c) : 16;
     if (g_lsd_chunk < 1) g_lsd_chunk = 1;
@@ -394,8 +395,8 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, int* launch
     k_upsweep<ITEMS><<<(unsigned)chunks, kSortThreads, 0, st>>>(a);
     k_chunk_scan<<<kRadix / 32, 1024, 0, st>>>(a, (uint32_t)chunks);
     int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
-    if ((int)a.slots > streams) a.slots = streams > 0 ? streams : 1;
-    size_t smem = (size_t)a.slots * TILE * 4 + kW * kRadix * 4 + (size_t)TILE * 3;
+    if ((int)a.slots > 2 * streams) a.slots = streams > 0 ? 2 * streams : 1;
+    size_t smem = (size_t)a.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 6;
     static size_t configured = 0;
     if (smem > configured) {
         cudaFuncSetAttribute(k_downsweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -418,9 +419,6 @@ cudaError_t launch_lsd_pass(const LsdPassArgs& args, int sms, cudaStream_t st, i
     LsdPassArgs a = args;
     a.slots = (uint32_t)g_lsd_slots;
     a.chunk_tiles = (uint32_t)g_lsd_chunk;
-    static int dbg = -1;
-    if (dbg < 0) { const char* e = getenv("CKS_LSD_DEBUG"); dbg = e ? atoi(e) : 0; }
-    a.debug = (uint32_t)dbg;
     a.tma = ((uintptr_t)a.in_planes % 16 == 0) && (a.in_pitch % 4 == 0) &&
             (a.in_rid == nullptr || (uintptr_t)a.in_rid % 16 == 0);
     return g_lsd_items == 8 ? lsd_pass<8>(a, sms, st, launches) : lsd_pass<16>(a, sms, st, launches);
