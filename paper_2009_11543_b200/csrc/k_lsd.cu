@@ -21,6 +21,8 @@
 // but has no decoupled look-back and no dynamic tile counter on the critical path.
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "cks_internal.h"
 
 namespace cks {
@@ -89,42 +91,64 @@ __device__ __forceinline__ int stream_plane(int k, int dp, int np) {
 }  // namespace
 
 // ---- upsweep ------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t digit_of(uint32_t w, uint32_t sel) {   // byte `sel` of w
+    return __byte_perm(w, 0u, 0x4440u | sel);
+}
+
 template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads)
 k_upsweep(const LsdPassArgs a) {
     constexpr int TILE = kSortThreads * ITEMS;
+    constexpr int V = ITEMS / 4;                              // uint4 loads per thread per tile
     __shared__ uint32_t bins[kW][kRadix];
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t n = a.n;
     const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
     const uint32_t t0 = blockIdx.x * a.chunk_tiles;
     const uint32_t t1 = min(t0 + a.chunk_tiles, ntiles);
     const uint32_t* src = a.digit_plane >= 0 ? a.in_planes + (uint64_t)a.digit_plane * a.in_pitch : a.in_rid;
+    const uint32_t sel = a.shift >> 3;
+    const bool vec = src && ((uintptr_t)src % 16 == 0);
+    uint32_t* hb = bins[warp];
     uint32_t running = 0;
-    uint32_t w[ITEMS];
-    auto load = [&](uint32_t t) {
+    uint4 w[V];
+    auto load = [&](uint32_t t) {                            // full, aligned tiles only
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + (uint64_t)t * TILE);
 #pragma unroll
-        for (int i = 0; i < ITEMS; i++) {
-            uint64_t idx = (uint64_t)t * TILE + i * kSortThreads + tid;
-            w[i] = idx < n ? (src ? __ldg(src + idx) : (uint32_t)idx) : 0xFFFFFFFFu;
-        }
+        for (int v = 0; v < V; v++) w[v] = __ldg(s4 + v * kSortThreads + tid);
     };
-    if (t0 < t1) load(t0);
+    auto is_fast = [&](uint32_t t) { return vec && (uint64_t)(t + 1) * TILE <= n; };
+    if (t0 < t1 && is_fast(t0)) load(t0);
     for (uint32_t t = t0; t < t1; t++) {
 #pragma unroll
-        for (int k = 0; k < kW; k++) bins[k][tid] = 0;
-        __syncthreads();
-        const uint64_t tb = (uint64_t)t * TILE;
+        for (int j = lane; j < kRadix; j += 32) hb[j] = 0;
+        __syncwarp();
+        if (is_fast(t)) {
+            uint4 c[V];
 #pragma unroll
-        for (int i = 0; i < ITEMS; i++)
-            if (tb + i * kSortThreads + tid < n) atomicAdd(&bins[warp][(w[i] >> a.shift) & 0xFF], 1u);
-        if (t + 1 < t1) load(t + 1);                         // next tile's words in flight
-        __syncthreads();
-        uint32_t c = 0;
+            for (int v = 0; v < V; v++) c[v] = w[v];
+            if (t + 1 < t1 && is_fast(t + 1)) load(t + 1);    // next tile's words in flight
 #pragma unroll
-        for (int k = 0; k < kW; k++) c += bins[k][tid];
+            for (int v = 0; v < V; v++) {
+                atomicAdd(&hb[digit_of(c[v].x, sel)], 1u);
+                atomicAdd(&hb[digit_of(c[v].y, sel)], 1u);
+                atomicAdd(&hb[digit_of(c[v].z, sel)], 1u);
+                atomicAdd(&hb[digit_of(c[v].w, sel)], 1u);
+            }
+        } else {
+            const uint64_t tb = (uint64_t)t * TILE;
+            for (int i = 0; i < ITEMS; i++) {
+                const uint64_t idx = tb + (uint64_t)i * kSortThreads + tid;
+                if (idx < n) atomicAdd(&hb[digit_of(src ? __ldg(src + idx) : (uint32_t)idx, sel)], 1u);
+            }
+            if (t + 1 < t1 && is_fast(t + 1)) load(t + 1);
+        }
+        __syncthreads();
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int k = 0; k < kW; k++) cnt += bins[k][tid];
         a.tile_off[(uint64_t)t * kRadix + tid] = running;
-        running += c;
+        running += cnt;
         __syncthreads();
     }
     a.chunk_tot[(uint64_t)blockIdx.x * kRadix + tid] = running;
@@ -177,7 +201,7 @@ k_chunk_scan(const LsdPassArgs a, uint32_t nchunks) {
 
 // ---- downsweep ----------------------------------------------------------------------------
 // Warp match of an NB-bit label: lanes whose label equals this lane's (bit-plane ballots;
-// and+setp fold into one LOP3 with a predicate output, so ~4 SASS per bit).
+// ptxas turns the bit tests into one R2P per 7 bits, so ~3 SASS per bit).
 template <int NB>
 __device__ __forceinline__ uint32_t match_bits(uint32_t d) {
     uint32_t peers = 0xFFFFFFFFu;
@@ -192,33 +216,6 @@ __device__ __forceinline__ uint32_t match_bits(uint32_t d) {
     return peers;
 }
 
-// One tile of the downsweep. FULL = TILE keys and the streams arrived by TMA; otherwise
-// `tile_n` keys (lanes past the end carry label 256 and take positions nobody reads).
-template <int ITEMS, bool FULL>
-__device__ __forceinline__ void rank_tile(const uint32_t* dslot, uint32_t shift, uint32_t tile_n, uint32_t wofs,
-                                          uint32_t lane, uint32_t ltm, uint32_t* h, uint32_t (&dg)[ITEMS],
-                                          uint32_t (&pos)[ITEMS]) {
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
-        const uint32_t idx = wofs + i * 32 + lane;
-        dg[i] = (FULL || idx < tile_n) ? (dslot[idx] >> shift) & 0xFF : 0x100u;
-    }
-    uint32_t peers[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) peers[i] = match_bits<FULL ? 8 : 9>(dg[i]);
-    // warp-private bins: every peer reads the running count, then the group's lowest lane
-    // (unique per label) adds the group size -- in issue order, so the rank is stable
-#pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
-        const uint32_t lower = __popc(peers[i] & ltm);
-        const uint32_t old = h[dg[i]];
-        __syncwarp();
-        if (lower == 0) h[dg[i]] = old + __popc(peers[i]);
-        __syncwarp();
-        pos[i] = old + lower;
-    }
-}
-
 template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads, ITEMS == 8 ? 4 : 2)
 k_downsweep(const LsdPassArgs a) {
@@ -228,7 +225,7 @@ k_downsweep(const LsdPassArgs a) {
     uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                                   // [R][TILE]
     uint32_t* s_hist = ring + (size_t)a.slots * TILE;                                     // [kW][HW]
     uint32_t* s_dst = s_hist + kW * HW;                                                   // [TILE]
-    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_dst + TILE);                          // [TILE]
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_dst + TILE);                          // [TILE] byte offsets
     __shared__ uint32_t s_warp[kW];
     __shared__ uint32_t s_gb[kRadix];
     __shared__ __align__(8) uint64_t s_bar[16];
@@ -242,6 +239,8 @@ k_downsweep(const LsdPassArgs a) {
     const bool implicit_rid = a.in_rid == nullptr;
     const int L = S - (implicit_rid ? 1 : 0);                   // loaded streams per tile
     const int R = (int)a.slots;
+    const uint32_t sel = a.shift >> 3;
+    const uint32_t nfull = a.tma ? (uint32_t)(n / TILE) : 0u;   // tiles [0, nfull) arrive by TMA
 
     auto src_of = [&](int k) -> const uint32_t* {
         int id = stream_plane(k, dp, np);
@@ -251,12 +250,11 @@ k_downsweep(const LsdPassArgs a) {
         int id = stream_plane(k, dp, np);
         return id >= 0 ? a.out_planes + (uint64_t)id * a.out_pitch : a.out_rid;
     };
-    auto full = [&](uint32_t t) { return a.tma && t < ntiles && (uint64_t)(t + 1) * TILE <= n; };
 
     uint32_t p_t = blockIdx.x;                                   // producer (thread 0) cursor
     int p_k = 0, p_slot = 0;
     auto produce = [&]() {
-        if (full(p_t)) {
+        if (p_t < nfull) {
             proxy_fence();
             bulk_load(ring + (size_t)p_slot * TILE, src_of(p_k) + (uint64_t)p_t * TILE, TILE * 4, &s_bar[p_slot]);
         }
@@ -274,15 +272,17 @@ k_downsweep(const LsdPassArgs a) {
     const uint32_t wofs = warp * 32 * ITEMS;
     const uint32_t ltm = lt_mask();
     uint32_t* h = s_hist + warp * HW;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += G) {
+
+    // one tile; FULL = TILE keys delivered by TMA (the hot path), else the generic tail path
+    auto tile_body = [&](auto full_tag, uint32_t tile) {
+        constexpr bool FULL = decltype(full_tag)::value;
         const uint64_t base = (uint64_t)tile * TILE;
-        const uint32_t tile_n = (uint32_t)(n - base < (uint64_t)TILE ? n - base : (uint64_t)TILE);
-        const bool tma_t = full(tile);
+        const uint32_t tile_n = FULL ? (uint32_t)TILE : (uint32_t)min((uint64_t)TILE, n - base);
         const uint32_t goff = a.chunk_tot[(uint64_t)(tile / a.chunk_tiles) * kRadix + tid] +
                               a.tile_off[(uint64_t)tile * kRadix + tid];
         auto acquire = [&](int k) -> const uint32_t* {
             uint32_t* slot = ring + (size_t)c_slot * TILE;
-            if (tma_t) {
+            if (FULL) {
                 bar_wait(&s_bar[c_slot], (uint32_t)c_round & 1u);
             } else {
                 const uint32_t* src = src_of(k) + base;
@@ -296,14 +296,32 @@ k_downsweep(const LsdPassArgs a) {
             if (++c_slot == R) { c_slot = 0; c_round++; }
         };
 
-        // ---- rank: warp-private bins (each warp clears its own row)
+        // ---- rank within the warp: warp-private bins (each warp clears its own row)
 #pragma unroll
         for (int j = lane; j < HW; j += 32) h[j] = 0;
         __syncwarp();
         const uint32_t* dslot = acquire(0);
         uint32_t dg[ITEMS], pos[ITEMS];
-        if (tile_n == TILE) rank_tile<ITEMS, true>(dslot, a.shift, tile_n, wofs, lane, ltm, h, dg, pos);
-        else rank_tile<ITEMS, false>(dslot, a.shift, tile_n, wofs, lane, ltm, h, dg, pos);
+        {
+            uint32_t peers[ITEMS];
+#pragma unroll
+            for (int i = 0; i < ITEMS; i++) {
+                const uint32_t idx = wofs + i * 32 + lane;
+                dg[i] = (FULL || idx < tile_n) ? digit_of(dslot[idx], sel) : 0x100u;
+                peers[i] = match_bits<FULL ? 8 : 9>(dg[i]);
+            }
+            // every peer reads the running count, then the group's lowest lane (unique per
+            // label) adds the group size -- items in order, so the rank is stable
+#pragma unroll
+            for (int i = 0; i < ITEMS; i++) {
+                const uint32_t lower = __popc(peers[i] & ltm);
+                const uint32_t old = h[dg[i]];
+                __syncwarp();
+                if (lower == 0) h[dg[i]] = old + __popc(peers[i]);
+                __syncwarp();
+                pos[i] = old + lower;
+            }
+        }
         __syncthreads();
 
         // ---- digit tid: warp offsets, tile-local base, global base
@@ -320,12 +338,12 @@ k_downsweep(const LsdPassArgs a) {
             s_gb[tid] = goff - excl;
         }
         __syncthreads();
-        // ---- tile permutation: slot p <- key (warp, item, lane); its global destination
+        // ---- tile permutation: slot p <- key (warp, item, lane), and its global destination
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
-            if (tile_n == TILE || dg[i] < 0x100u) {
+            if (FULL || dg[i] < 0x100u) {
                 const uint32_t p = pos[i] + h[dg[i]];
-                s_src[p] = (uint16_t)(wofs + i * 32 + lane);
+                s_src[p] = (uint16_t)((wofs + i * 32 + lane) * 4);
                 s_dst[p] = p + s_gb[dg[i]];
             }
         }
@@ -344,16 +362,22 @@ k_downsweep(const LsdPassArgs a) {
                 const uint32_t b32 = (uint32_t)base;
 #pragma unroll
                 for (int r = 0; r < ITEMS; r++)
-                    if (tile_n == TILE || r * kSortThreads + tid < tile_n) out[dest[r]] = b32 + from[r];
+                    if (FULL || r * kSortThreads + tid < tile_n) out[dest[r]] = b32 + (from[r] >> 2);
                 continue;
             }
-            const uint32_t* slot = k == 0 ? dslot : acquire(k);
+            const uint8_t* slot = reinterpret_cast<const uint8_t*>(k == 0 ? dslot : acquire(k));
 #pragma unroll
             for (int r = 0; r < ITEMS; r++)
-                if (tile_n == TILE || r * kSortThreads + tid < tile_n) out[dest[r]] = slot[from[r]];
+                if (FULL || r * kSortThreads + tid < tile_n)
+                    out[dest[r]] = *reinterpret_cast<const uint32_t*>(slot + from[r]);
             __syncthreads();
             release();
         }
+    };
+
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += G) {
+        if (tile < nfull) tile_body(std::true_type{}, tile);
+        else tile_body(std::false_type{}, tile);
     }
 }
 
