@@ -217,15 +217,14 @@ __device__ __forceinline__ uint32_t match_bits(uint32_t d) {
 }
 
 template <int ITEMS>
-__global__ void __launch_bounds__(kSortThreads, ITEMS == 8 ? 4 : 2)
+__global__ void __launch_bounds__(kSortThreads, ITEMS == 8 ? 3 : 2)
 k_downsweep(const LsdPassArgs a) {
     constexpr int TILE = kSortThreads * ITEMS;
     constexpr int HW = kRadix + 8;                            // bin row (+ label 256 of tail lanes)
     extern __shared__ __align__(128) uint8_t s_dyn[];
     uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                                   // [R][TILE]
     uint32_t* s_hist = ring + (size_t)a.slots * TILE;                                     // [kW][HW]
-    uint32_t* s_dst = s_hist + kW * HW;                                                   // [TILE]
-    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_dst + TILE);                          // [TILE] byte offsets
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_hist + kW * HW);                      // [TILE] byte offsets
     __shared__ uint32_t s_warp[kW];
     __shared__ uint32_t s_gb[kRadix];
     __shared__ __align__(8) uint64_t s_bar[16];
@@ -310,15 +309,14 @@ k_downsweep(const LsdPassArgs a) {
                 dg[i] = (FULL || idx < tile_n) ? digit_of(dslot[idx], sel) : 0x100u;
                 peers[i] = match_bits<FULL ? 8 : 9>(dg[i]);
             }
-            // every peer reads the running count, then the group's lowest lane (unique per
-            // label) adds the group size -- items in order, so the rank is stable
+            // the group's lowest lane (unique per label) reserves the group's places in the
+            // warp-private bin and broadcasts the old count -- items in order: stable
 #pragma unroll
             for (int i = 0; i < ITEMS; i++) {
                 const uint32_t lower = __popc(peers[i] & ltm);
-                const uint32_t old = h[dg[i]];
-                __syncwarp();
-                if (lower == 0) h[dg[i]] = old + __popc(peers[i]);
-                __syncwarp();
+                uint32_t old = 0;
+                if (lower == 0) old = atomicAdd(&h[dg[i]], (uint32_t)__popc(peers[i]));
+                old = __shfl_sync(0xFFFFFFFFu, old, __ffs(peers[i]) - 1);
                 pos[i] = old + lower;
             }
         }
@@ -338,25 +336,32 @@ k_downsweep(const LsdPassArgs a) {
             s_gb[tid] = goff - excl;
         }
         __syncthreads();
-        // ---- tile permutation: slot p <- key (warp, item, lane), and its global destination
+        // ---- tile permutation: slot p <- key (warp, item, lane), as a byte offset in a slot
 #pragma unroll
-        for (int i = 0; i < ITEMS; i++) {
-            if (FULL || dg[i] < 0x100u) {
-                const uint32_t p = pos[i] + h[dg[i]];
-                s_src[p] = (uint16_t)((wofs + i * 32 + lane) * 4);
-                s_dst[p] = p + s_gb[dg[i]];
-            }
-        }
+        for (int i = 0; i < ITEMS; i++)
+            if (FULL || dg[i] < 0x100u) s_src[pos[i] + h[dg[i]]] = (uint16_t)((wofs + i * 32 + lane) * 4);
         __syncthreads();
         uint32_t from[ITEMS], dest[ITEMS];
+        // ---- stream 0 (the digit word): gather in digit order; the gathered word's digit
+        // gives the slot's global destination (consecutive slots share digits: no conflicts)
+        {
+            uint32_t* out = dst_of(0);
+            const uint8_t* slot = reinterpret_cast<const uint8_t*>(dslot);
 #pragma unroll
-        for (int r = 0; r < ITEMS; r++) {
-            const uint32_t s = r * kSortThreads + tid;
-            from[r] = s_src[s];
-            dest[r] = s_dst[s];
+            for (int r = 0; r < ITEMS; r++) {
+                const uint32_t s = r * kSortThreads + tid;
+                if (FULL || s < tile_n) {
+                    from[r] = s_src[s];
+                    const uint32_t w = *reinterpret_cast<const uint32_t*>(slot + from[r]);
+                    dest[r] = s + s_gb[digit_of(w, sel)];
+                    out[dest[r]] = w;
+                }
+            }
+            __syncthreads();
+            release();
         }
-        // ---- every stream: gather from its slot in digit order, write coalesced runs
-        for (int k = 0; k < S; k++) {
+        // ---- the other streams: same gather, same destinations
+        for (int k = 1; k < S; k++) {
             uint32_t* out = dst_of(k);
             if (k == S - 1 && implicit_rid) {
                 const uint32_t b32 = (uint32_t)base;
@@ -365,7 +370,7 @@ k_downsweep(const LsdPassArgs a) {
                     if (FULL || r * kSortThreads + tid < tile_n) out[dest[r]] = b32 + (from[r] >> 2);
                 continue;
             }
-            const uint8_t* slot = reinterpret_cast<const uint8_t*>(k == 0 ? dslot : acquire(k));
+            const uint8_t* slot = reinterpret_cast<const uint8_t*>(acquire(k));
 #pragma unroll
             for (int r = 0; r < ITEMS; r++)
                 if (FULL || r * kSortThreads + tid < tile_n)
@@ -420,7 +425,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, int* launch
     k_chunk_scan<<<kRadix / 32, 1024, 0, st>>>(a, (uint32_t)chunks);
     int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
     if ((int)a.slots > 2 * streams) a.slots = streams > 0 ? 2 * streams : 1;
-    size_t smem = (size_t)a.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 6;
+    size_t smem = (size_t)a.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 2;
     static size_t configured = 0;
     if (smem > configured) {
         cudaFuncSetAttribute(k_downsweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
