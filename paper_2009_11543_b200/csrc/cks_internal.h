@@ -100,6 +100,8 @@ struct LsdPassArgs {
     uint32_t chunk_tiles;        // set by the launcher
     uint32_t slots;              // set by the launcher
     uint32_t tma;                // set by the launcher
+    uint32_t tile_begin;         // first tile this launch covers (set by the launcher)
+    uint32_t debug;              // timing experiments only (CKS_LSD_DEBUG); results are wrong when set
 };
 cudaError_t launch_lsd_pass(const LsdPassArgs& a, int sms, cudaStream_t st, int* launches);
 void lsd_sizes(uint64_t n, uint64_t* tiles, uint64_t* chunks);

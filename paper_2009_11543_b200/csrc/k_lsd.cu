@@ -250,7 +250,7 @@ k_downsweep(const LsdPassArgs a) {
         return id >= 0 ? a.out_planes + (uint64_t)id * a.out_pitch : a.out_rid;
     };
 
-    uint32_t p_t = blockIdx.x;                                   // producer (thread 0) cursor
+    uint32_t p_t = a.tile_begin + blockIdx.x;                    // producer (thread 0) cursor
     int p_k = 0, p_slot = 0;
     auto produce = [&]() {
         if (p_t < nfull) {
@@ -310,15 +310,21 @@ k_downsweep(const LsdPassArgs a) {
                 peers[i] = match_bits<FULL ? 8 : 9>(dg[i]);
             }
             // the group's lowest lane (unique per label) reserves the group's places in the
-            // warp-private bin and broadcasts the old count -- items in order: stable
+            // warp-private bin (predicated atomics, all issued before any result is used;
+            // shared atomics of one warp apply in issue order: stable), then broadcasts
+            uint32_t old[ITEMS];
+            const uint32_t hbase = smem_addr(h);
 #pragma unroll
             for (int i = 0; i < ITEMS; i++) {
                 const uint32_t lower = __popc(peers[i] & ltm);
-                uint32_t old = 0;
-                if (lower == 0) old = atomicAdd(&h[dg[i]], (uint32_t)__popc(peers[i]));
-                old = __shfl_sync(0xFFFFFFFFu, old, __ffs(peers[i]) - 1);
-                pos[i] = old + lower;
+                asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %1, 0;\n mov.u32 %0, 0;\n"
+                             " @p atom.shared.add.u32 %0, [%2], %3;\n}"
+                             : "=r"(old[i]) : "r"(lower), "r"(hbase + dg[i] * 4), "r"((uint32_t)__popc(peers[i]))
+                             : "memory");
+                pos[i] = lower;
             }
+#pragma unroll
+            for (int i = 0; i < ITEMS; i++) pos[i] += __shfl_sync(0xFFFFFFFFu, old[i], __ffs(peers[i]) - 1);
         }
         __syncthreads();
 
@@ -380,15 +386,239 @@ k_downsweep(const LsdPassArgs a) {
         }
     };
 
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += G) {
+    for (uint32_t tile = a.tile_begin + blockIdx.x; tile < ntiles; tile += G) {
         if (tile < nfull) tile_body(std::true_type{}, tile);
         else tile_body(std::false_type{}, tile);
     }
 }
 
+// ---- warp-specialised downsweep (full TMA tiles) -------------------------------------------
+// Three roles in one persistent CTA per SM, pipelined across the CTA's tiles:
+//   producer warp  issues the 1-D TMA bulk loads of every stream of every tile, in order,
+//                  into a ring of R slots (waits on the slot's `empty` barrier);
+//   ranker warps   (8) rank tile j's digit word and publish the tile permutation
+//                  s_src[j&1] and global bases s_gb[j&1] (barrier `ranked[j&1]`);
+//   writer warps   (8) gather every stream of tile j in digit order and store it in
+//                  coalesced runs, releasing each slot (`empty`) as they go.
+// So while the writers move tile j the rankers already work on tile j+1 and the producer
+// keeps the next loads in flight: the store stream never waits for a ranking phase.
+constexpr int kWsWarps = 17;                     // 8 rankers + 8 writers + 1 producer
+constexpr int kWsThreads = kWsWarps * 32;
+constexpr uint32_t kDigitSlots = 3;              // digit-word ring (ranked one tile ahead)
+
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_init_n(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+// exclusive scan over the 256 ranker threads (named barrier 1)
+__device__ __forceinline__ uint32_t scan256_rankers(uint32_t v, uint32_t* s_warp, uint32_t rt) {
+    const uint32_t lane = rt & 31, warp = rt >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    named_sync(1, 256);
+    if (warp == 0) {
+        uint32_t t = lane < (uint32_t)kW ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < kW; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= (uint32_t)o) t += y;
+        }
+        if (lane < (uint32_t)kW) s_warp[lane] = t;
+    }
+    named_sync(1, 256);
+    uint32_t r = (warp ? s_warp[warp - 1] : 0) + x - v;
+    named_sync(1, 256);
+    return r;
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kWsThreads, 1)
+k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
+    constexpr int TILE = kSortThreads * ITEMS;
+    constexpr int HW = kRadix + 8;
+    extern __shared__ __align__(128) uint8_t s_dyn[];
+    uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                                   // [R][TILE]
+    uint32_t* s_hist = ring + (size_t)(kDigitSlots + a.slots) * TILE;                     // [kW][HW]
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_hist + kW * HW);                      // [2][TILE]
+    __shared__ uint32_t s_gb[2][kRadix];
+    __shared__ uint32_t s_warp[kW];
+    __shared__ __align__(8) uint64_t s_full[kDigitSlots + 16];
+    __shared__ __align__(8) uint64_t s_empty[kDigitSlots + 16];
+    __shared__ __align__(8) uint64_t s_ranked[2];
+    __shared__ __align__(8) uint64_t s_written[2];
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t G = gridDim.x;
+    const int np = (int)a.nplanes, dp = a.digit_plane;
+    const int S = np + 1;
+    const bool implicit_rid = a.in_rid == nullptr;
+    const uint32_t L = (uint32_t)(S - (implicit_rid ? 1 : 0));   // loaded streams per tile
+    const uint32_t R = a.slots;                                  // data-ring slots
+    const uint32_t sel = a.shift >> 3;
+    const uint32_t my_tiles = blockIdx.x < nfull ? (nfull - blockIdx.x + G - 1) / G : 0;
+
+    auto src_of = [&](int k) -> const uint32_t* {
+        int id = stream_plane(k, dp, np);
+        return id >= 0 ? a.in_planes + (uint64_t)id * a.in_pitch : a.in_rid;
+    };
+    auto dst_of = [&](int k) -> uint32_t* {
+        int id = stream_plane(k, dp, np);
+        return id >= 0 ? a.out_planes + (uint64_t)id * a.out_pitch : a.out_rid;
+    };
+
+    if (tid == 0) {
+        for (uint32_t s = 0; s < kDigitSlots + R; s++) { bar_init_n(&s_full[s], 1); bar_init_n(&s_empty[s], kW); }
+        for (int b = 0; b < 2; b++) { bar_init_n(&s_ranked[b], kW); bar_init_n(&s_written[b], kW); }
+        bar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == 2 * kW) {
+        // ---------------- producer: digit words one tile ahead in their own 3-slot ring
+        // (D0, D1, then after the data streams of tile j the digit word of tile j+2), the
+        // other streams in order through the data ring
+        if (lane == 0) {
+            auto issue_digit = [&](uint32_t j) {
+                const uint32_t s = j % kDigitSlots;
+                if (j >= kDigitSlots) bar_wait(&s_empty[s], ((j / kDigitSlots) - 1) & 1u);
+                proxy_fence();
+                bulk_load(ring + (size_t)s * TILE, src_of(0) + (uint64_t)(blockIdx.x + j * G) * TILE, TILE * 4,
+                          &s_full[s]);
+            };
+            uint32_t y = 0;                                  // data item counter
+            for (uint32_t j = 0; j < my_tiles && j < 2; j++) issue_digit(j);
+            for (uint32_t j = 0; j < my_tiles; j++) {
+                const uint64_t off = (uint64_t)(blockIdx.x + j * G) * TILE;
+                for (uint32_t k = 1; k < L; k++, y++) {
+                    const uint32_t s = kDigitSlots + y % R;
+                    if (y >= R) bar_wait(&s_empty[s], ((y / R) - 1) & 1u);
+                    proxy_fence();
+                    bulk_load(ring + (size_t)s * TILE, src_of((int)k) + off, TILE * 4, &s_full[s]);
+                }
+                if (j + 2 < my_tiles) issue_digit(j + 2);
+            }
+        }
+        return;
+    }
+
+    if (warp < kW) {
+        // ---------------- rankers: thread rt is digit rt in the per-digit phases
+        const uint32_t rt = tid;
+        const uint32_t wofs = warp * 32 * ITEMS;
+        const uint32_t ltm = lt_mask();
+        uint32_t* h = s_hist + warp * HW;
+        const uint32_t hbase = smem_addr(h);
+        for (uint32_t j = 0; j < my_tiles; j++) {
+            const uint32_t tile = blockIdx.x + j * G;
+            const uint32_t buf = j & 1;
+            const uint32_t goff = a.chunk_tot[(uint64_t)(tile / a.chunk_tiles) * kRadix + rt] +
+                                  a.tile_off[(uint64_t)tile * kRadix + rt];
+            const uint32_t* dslot = ring + (size_t)(j % kDigitSlots) * TILE;
+#pragma unroll
+            for (int q = lane; q < HW; q += 32) h[q] = 0;
+            __syncwarp();
+            bar_wait(&s_full[j % kDigitSlots], (j / kDigitSlots) & 1u);
+            uint32_t dg[ITEMS], pos[ITEMS];
+            {
+                uint32_t peers[ITEMS];
+#pragma unroll
+                for (int i = 0; i < ITEMS; i++) {
+                    dg[i] = digit_of(dslot[wofs + i * 32 + lane], sel);
+                    peers[i] = match_bits<8>(dg[i]);
+                }
+                uint32_t old[ITEMS];
+#pragma unroll
+                for (int i = 0; i < ITEMS; i++) {
+                    const uint32_t lower = __popc(peers[i] & ltm);
+                    asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %1, 0;\n mov.u32 %0, 0;\n"
+                                 " @p atom.shared.add.u32 %0, [%2], %3;\n}"
+                                 : "=r"(old[i]) : "r"(lower), "r"(hbase + dg[i] * 4), "r"((uint32_t)__popc(peers[i]))
+                                 : "memory");
+                    pos[i] = lower;
+                }
+#pragma unroll
+                for (int i = 0; i < ITEMS; i++) pos[i] += __shfl_sync(0xFFFFFFFFu, old[i], __ffs(peers[i]) - 1);
+            }
+            named_sync(1, 256);
+            {
+                uint32_t c[kW], total = 0;
+#pragma unroll
+                for (int k = 0; k < kW; k++) { c[k] = s_hist[k * HW + rt]; total += c[k]; }
+                const uint32_t excl = scan256_rankers(total, s_warp, rt);
+                uint32_t run = excl;
+#pragma unroll
+                for (int k = 0; k < kW; k++) { s_hist[k * HW + rt] = run; run += c[k]; }
+                if (j >= 2) bar_wait(&s_written[buf], ((j >> 1) - 1) & 1u);   // writers done with tile j-2
+                s_gb[buf][rt] = goff - excl;
+            }
+            named_sync(1, 256);
+            uint16_t* src = s_src + buf * TILE;
+#pragma unroll
+            for (int i = 0; i < ITEMS; i++) src[(a.debug & 2) ? wofs + i * 32 + lane : pos[i] + h[dg[i]]] = (uint16_t)((wofs + i * 32 + lane) * 4);
+            __syncwarp();
+            if (lane == 0) bar_arrive(&s_ranked[buf]);
+        }
+        return;
+    }
+
+    // ---------------- writers: thread wt owns output slots r*256 + wt
+    const uint32_t wt = tid - kSortThreads;
+    uint32_t y = 0;                                              // data item counter
+    for (uint32_t j = 0; j < my_tiles; j++) {
+        const uint32_t tile = blockIdx.x + j * G;
+        const uint32_t buf = j & 1;
+        bar_wait(&s_ranked[buf], (j >> 1) & 1u);
+        const uint16_t* src = s_src + buf * TILE;
+        uint32_t from[ITEMS], dest[ITEMS];
+#pragma unroll
+        for (int r = 0; r < ITEMS; r++) from[r] = src[r * kSortThreads + wt];
+        {
+            const uint32_t slot = j % kDigitSlots;
+            bar_wait(&s_full[slot], (j / kDigitSlots) & 1u);
+            const uint8_t* sl = reinterpret_cast<const uint8_t*>(ring + (size_t)slot * TILE);
+            uint32_t* out = dst_of(0);
+#pragma unroll
+            for (int r = 0; r < ITEMS; r++) {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(sl + from[r]);
+                dest[r] = (a.debug & 1) ? tile * (uint32_t)TILE + r * kSortThreads + wt : r * kSortThreads + wt + s_gb[buf][digit_of(w, sel)];
+                out[dest[r]] = w;
+            }
+            __syncwarp();
+            if (lane == 0) { bar_arrive(&s_written[buf]); bar_arrive(&s_empty[slot]); }
+        }
+        for (int k = 1; k < S; k++) {
+            uint32_t* out = dst_of(k);
+            if (k == S - 1 && implicit_rid) {
+                const uint32_t b32 = tile * (uint32_t)TILE;
+#pragma unroll
+                for (int r = 0; r < ITEMS; r++) out[dest[r]] = b32 + (from[r] >> 2);
+                continue;
+            }
+            const uint32_t slot = kDigitSlots + y % R;
+            bar_wait(&s_full[slot], (y / R) & 1u);
+            y++;
+            const uint8_t* sl = reinterpret_cast<const uint8_t*>(ring + (size_t)slot * TILE);
+#pragma unroll
+            for (int r = 0; r < ITEMS; r++) out[dest[r]] = *reinterpret_cast<const uint32_t*>(sl + from[r]);
+            __syncwarp();
+            if (lane == 0) bar_arrive(&s_empty[slot]);
+        }
+    }
+}
+
 // ---- launch ---------------------------------------------------------------------------------
 
-static int g_lsd_items = 0, g_lsd_slots = 0, g_lsd_chunk = 0;
+static int g_lsd_items = 0, g_lsd_slots = 0, g_lsd_chunk = 0, g_lsd_ws = 1;
 
 static void lsd_config() {
     if (g_lsd_items) return;
@@ -401,6 +631,8 @@ static void lsd_config() {
     if (g_lsd_slots > 16) g_lsd_slots = 16;
     const char* c = getenv("CKS_LSD_CHUNK");
     g_lsd_chunk = c ? atoi(c) : 16;
+    const char* w = getenv("CKS_LSD_WS");
+    g_lsd_ws = w ? atoi(w) : 1;
     if (g_lsd_chunk < 1) g_lsd_chunk = 1;
 }
 
@@ -423,7 +655,31 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, int* launch
     cudaMemsetAsync(a.total, 0, kRadix * 4, st);
     k_upsweep<ITEMS><<<(unsigned)chunks, kSortThreads, 0, st>>>(a);
     k_chunk_scan<<<kRadix / 32, 1024, 0, st>>>(a, (uint32_t)chunks);
-    int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
+    const int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
+    const uint64_t nfull = a.n / TILE;
+    int nl = 2;
+    if (g_lsd_ws && a.tma && nfull > 0) {
+        // warp-specialised kernel over the full tiles, one persistent CTA per SM
+        constexpr size_t fixed = (size_t)kW * (kRadix + 8) * 4 + (size_t)2 * TILE * 2;
+        const int max_slots = (int)((200u * 1024u - fixed) / ((size_t)TILE * 4));
+        int R = 2 * (streams - 1);                           // data ring: the non-digit streams
+        if (R > max_slots - (int)kDigitSlots) R = max_slots - (int)kDigitSlots;
+        if (R > 16) R = 16;
+        if (R < 1) R = 1;
+        LsdPassArgs w = a;
+        w.slots = (uint32_t)R;
+        const size_t smem = (size_t)(kDigitSlots + R) * TILE * 4 + fixed;
+        static size_t configured_ws = 0;
+        if (smem > configured_ws) {
+            cudaFuncSetAttribute(k_downsweep_ws<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured_ws = smem;
+        }
+        const uint64_t grid = nfull < (uint64_t)sms ? nfull : (uint64_t)sms;
+        k_downsweep_ws<ITEMS><<<(unsigned)grid, kWsThreads, smem, st>>>(w, (uint32_t)nfull);
+        nl++;
+        if (nfull == tiles) { *launches = nl; return cudaGetLastError(); }
+        a.tile_begin = (uint32_t)nfull;                      // the partial last tile
+    }
     if ((int)a.slots > 2 * streams) a.slots = streams > 0 ? 2 * streams : 1;
     size_t smem = (size_t)a.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 2;
     static size_t configured = 0;
@@ -435,9 +691,10 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, int* launch
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_downsweep<ITEMS>, kSortThreads, smem);
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)sms * per_sm;
-    if (grid > tiles) grid = tiles;
+    if (grid > tiles - a.tile_begin) grid = tiles - a.tile_begin;
     k_downsweep<ITEMS><<<(unsigned)grid, kSortThreads, smem, st>>>(a);
-    *launches = 3;
+    nl++;
+    *launches = nl;
     return cudaGetLastError();
 }
 
@@ -448,6 +705,9 @@ cudaError_t launch_lsd_pass(const LsdPassArgs& args, int sms, cudaStream_t st, i
     LsdPassArgs a = args;
     a.slots = (uint32_t)g_lsd_slots;
     a.chunk_tiles = (uint32_t)g_lsd_chunk;
+    static int dbg = -1;
+    if (dbg < 0) { const char* e = getenv("CKS_LSD_DEBUG"); dbg = e ? atoi(e) : 0; }
+    a.debug = (uint32_t)dbg;
     a.tma = ((uintptr_t)a.in_planes % 16 == 0) && (a.in_pitch % 4 == 0) &&
             (a.in_rid == nullptr || (uintptr_t)a.in_rid % 16 == 0);
     return g_lsd_items == 8 ? lsd_pass<8>(a, sms, st, launches) : lsd_pass<16>(a, sms, st, launches);
