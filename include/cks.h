@@ -169,8 +169,14 @@ int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
                  uint32_t fanout, float fill, const cks_tree* out);
 
 /* ---- fused first build: a1 -> a2 -> a3 -> a4 -> a5 -> a6 -> a7 -> a8 -----------------------
- * The benchmarked step. ONE sort on the superset mask (or prior_mask); exact D from the
- * adjacency pass; packed keys repacked to exact D (skipped when M = D); bulk load. */
+ * The benchmarked step. The superset mask M (or prior_mask) is compressed once; the sort
+ * runs by distinguishing prefixes ("sort by distinguishing prefixes",
+ * P:603): LSD over the first 64 bits of P_M for all keys, then only the keys still tied
+ * with a neighbour are re-sorted by (run, next 64 bits), round after round. A pair's D-bit
+ * comes from the round that separates it, so the exact D and the D_i fall out of the sort;
+ * P_D in sorted order is then compressed from the key rows (or repacked from the sorted
+ * chunk when one chunk held all of P_M); bulk load. Environment CKS_REFINE=0 selects the
+ * plain single sort over all m bits (one adjacency pass, repack skipped when M = D). */
 typedef struct {
     /* inputs (caller-owned buffers) */
     uint8_t* mask;            /* host u8[key_bytes]: receives exact D */
@@ -187,10 +193,14 @@ typedef struct {
     uint32_t passes;          /* LSD digit passes run */
     const uint32_t* packed;   /* VIEW (ctx-owned): sorted P_D planes; plane q at packed + q*packed_pitch */
     uint64_t packed_pitch;    /* plane stride of `packed` in u32 elements (>= n, padded for alignment) */
+    uint32_t rounds;          /* prefix-refinement rounds run (0 = plain single sort) */
+    uint32_t reserved0;
+    uint64_t refined_keys;    /* keys re-sorted in rounds >= 1 (summed over rounds) */
 } cks_build_out;
 
 /* keys: device u8[n][key_bytes]; prior_mask: host u8[key_bytes] superset or NULL.
- * Synchronises (twice: after the superset mask and after the adjacency pass). */
+ * Synchronises: after the superset mask, once per refinement round (to size the next
+ * round) and after the exact D is known. */
 int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
               const uint8_t* prior_mask, cks_build_out* out);
 

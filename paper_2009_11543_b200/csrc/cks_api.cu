@@ -31,6 +31,8 @@ struct cks_ctx {
     int sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;   // partial tail tile of an LSD pass
+    cudaEvent_t aux_ev[2] = {};
     char err[512] = {0};
     uint64_t launches = 0;
     uint32_t epoch = 1;
@@ -40,13 +42,17 @@ struct cks_ctx {
     cudaEvent_t plan_ev[3] = {};      // guards the pinned staging slots
     // scratch
     DevBuf occ, masks8, planeA, planeB, ridA, ridB, hist, base, status, counters, dacc, moff, dbit,
-        rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total;
-    int algo = -1;                    // LSD pass: 0 = onesweep (look-back), 1 = reduce-then-scan
+        rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
+        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, tie, keep, done, rcnt, rtot;   // NEXT-1
+    int algo = -1;                    // LSD pass: 1 = reduce-then-scan (default), 0 = onesweep
+                                      // (decoupled look-back; measured slower)
     size_t status_tiles = 0;
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
     uint16_t* h_moff = nullptr;
     uint32_t* h_small = nullptr;      // 4 KiB: masks, dacc words
+    uint32_t* h_tot = nullptr;        // refinement: (members, runs) of the next round
+    int refine = -1;                  // first build by distinguishing prefixes (NEXT-1)
 };
 
 namespace {
@@ -162,14 +168,14 @@ inline uint64_t scratch_pitch(uint64_t n) { return (n + 31) & ~31ull; }
 
 // a2 + a3
 int run_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* mask,
-                 uint32_t* planes, uint64_t pitch) {
+                 uint32_t* planes, uint64_t pitch, uint32_t lead = 0, const uint32_t* rows = nullptr) {
     TRY(claim_slot(ctx, 0));
     plan_compress(mask, B, ctx->h_plan[0]);
     uint32_t m = ctx->h_plan[0]->out_bits, np = (m + 31) / 32;
     if (n == 0 || m == 0) return CKS_OK;
     GatherPlan* dplan;
     TRY(upload_plan(ctx, 0, &dplan));
-    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, planes, pitch, ctx->sms, ctx->stream));
+    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, planes, pitch, ctx->sms, ctx->stream, lead, rows));
     return CKS_OK;
 }
 
@@ -183,10 +189,15 @@ uint32_t* first_pass_out(cks_ctx* ctx, uint32_t P) {
     return ((P - 1) & 1) ? as<uint32_t>(ctx->planeA) : as<uint32_t>(ctx->planeB);
 }
 
+// digit0: key digits below it are known to be constant (left-alignment padding, an absent
+// plane) and are not sorted.
 int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_t np, uint32_t key_passes,
              uint64_t n, const uint32_t* in_rid, uint32_t rid_passes, uint32_t* final_planes,
-             uint64_t final_pitch, uint32_t* final_rid, const uint32_t** sorted_view, uint64_t* sorted_pitch) {
-    const uint32_t P = key_passes + (in_rid ? rid_passes : 0);
+             uint64_t final_pitch, uint32_t* final_rid, const uint32_t** sorted_view, uint64_t* sorted_pitch,
+             uint32_t digit0 = 0) {
+    if (digit0 > key_passes) digit0 = key_passes;
+    const uint32_t Pfull = key_passes + (in_rid ? rid_passes : 0);
+    const uint32_t P = Pfull - digit0;
     if (sorted_view) *sorted_view = in_planes;
     if (sorted_pitch) *sorted_pitch = in_pitch;
     if (n == 0) return CKS_OK;
@@ -204,32 +215,35 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
     TRY(ensure(ctx, ctx->planeB, pbytes));
     TRY(ensure(ctx, ctx->ridA, sp * 4));
     TRY(ensure(ctx, ctx->ridB, sp * 4));
-    TRY(ensure(ctx, ctx->hist, (size_t)P * 256 * 4));
-    TRY(ensure(ctx, ctx->base, (size_t)P * 256 * 4));
-    TRY(ensure(ctx, ctx->counters, (size_t)P * 4));
-    uint64_t tiles = onesweep_tiles(n);
-    if (ctx->status_tiles < tiles) {
-        TRY(ensure(ctx, ctx->status, (size_t)tiles * 256 * 8, /*zero=*/true));
-        ctx->status_tiles = ctx->status.cap / (256 * 8);
-    }
+    TRY(ensure(ctx, ctx->hist, (size_t)Pfull * 256 * 4));
+    TRY(ensure(ctx, ctx->base, (size_t)Pfull * 256 * 4));
+    TRY(ensure(ctx, ctx->counters, (size_t)Pfull * 4));
     if (ctx->algo < 0) {
         const char* e = getenv("CKS_SORT_ALGO");
         ctx->algo = e ? atoi(e) : 1;
     }
+    if (ctx->algo == 0) {
+        const uint64_t tiles = onesweep_tiles(n);
+        if (ctx->status_tiles < tiles) {
+            TRY(ensure(ctx, ctx->status, (size_t)tiles * 256 * 8, /*zero=*/true));
+            ctx->status_tiles = ctx->status.cap / (256 * 8);
+        }
+    }
     uint64_t lsd_tiles = 0, lsd_chunks = 0;
-    if (ctx->algo == 1) {
+    if (ctx->algo != 0) {
         lsd_sizes(n, &lsd_tiles, &lsd_chunks);
         TRY(ensure(ctx, ctx->tile_off, (size_t)lsd_tiles * 256 * 4));
         TRY(ensure(ctx, ctx->chunk_tot, (size_t)lsd_chunks * 256 * 4));
         TRY(ensure(ctx, ctx->total, 256 * 4));
-    } else {
-        CK(cudaMemsetAsync(ctx->hist.p, 0, (size_t)P * 256 * 4, ctx->stream));
-        CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)P * 4, ctx->stream));
+    }
+    if (ctx->algo == 0) {
+        CK(cudaMemsetAsync(ctx->hist.p, 0, (size_t)Pfull * 256 * 4, ctx->stream));
+        CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)Pfull * 4, ctx->stream));
         int hl = 0;
         CK(launch_hist(in_planes, in_pitch, n, key_passes, in_rid, rid_passes, as<uint32_t>(ctx->hist), ctx->sms,
                        ctx->stream, &hl));
         ctx->launches += (uint64_t)hl;
-        LAUNCH(launch_scan(as<uint32_t>(ctx->hist), P, as<uint32_t>(ctx->base), ctx->stream));
+        LAUNCH(launch_scan(as<uint32_t>(ctx->hist), Pfull, as<uint32_t>(ctx->base), ctx->stream));
     }
     mark(ctx, ST_HIST);
 
@@ -258,12 +272,12 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
             a.shift = 8 * t;
             hist_index = key_passes + t;
         } else {
-            uint32_t p = in_rid ? t - rid_passes : t;
+            uint32_t p = (in_rid ? t - rid_passes : t) + digit0;
             a.digit_plane = (int32_t)(p >> 2);
             a.shift = 8 * (p & 3);
             hist_index = p;
         }
-        if (ctx->algo == 1) {
+        if (ctx->algo != 0) {
             LsdPassArgs la;
             memset(&la, 0, sizeof(la));
             la.in_planes = cur_p;
@@ -280,7 +294,11 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
             la.chunk_tot = as<uint32_t>(ctx->chunk_tot);
             la.total = as<uint32_t>(ctx->total);
             int nl = 0;
-            CK(launch_lsd_pass(la, ctx->sms, ctx->stream, &nl));
+            LsdAux aux;
+            aux.stream = ctx->aux_stream;
+            aux.fork = ctx->aux_ev[0];
+            aux.join = ctx->aux_ev[1];
+            CK(launch_lsd_pass(la, ctx->sms, ctx->stream, aux, &nl));
             ctx->launches += (uint64_t)nl;
             cur_p = out_p;
             cur_pitch = out_pitch;
@@ -305,11 +323,10 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
     return CKS_OK;
 }
 
-// a6: exact D from sorted planes compressed with `sort_mask` (host).
-int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint64_t pitch, uint32_t m, uint64_t n,
-                 const uint8_t* sort_mask, uint32_t B, uint8_t* mask_out, uint16_t* dbit) {
-    const uint32_t nwords = (8 * B + 31) / 32;
-    TRY(ensure(ctx, ctx->dacc, (size_t)nwords * 4));
+bool same_mask(const uint8_t* a, const uint8_t* b, uint32_t B) { return memcmp(a, b, B) == 0; }
+
+// D-offset table of the sort mask: moff[t] = key position of the (t+1)-st mask bit.
+int upload_moff(cks_ctx* ctx, const uint8_t* sort_mask, uint32_t B, uint32_t m) {
     TRY(ensure(ctx, ctx->moff, (size_t)(m + 1) * 2));
     CK(cudaEventSynchronize(ctx->plan_ev[1]));
     uint32_t t = 0;
@@ -318,6 +335,25 @@ int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint64_t pitch, uint32_t 
     if (t != m) return fail(ctx, CKS_EINVAL, "packed_bits %u != popcount(sort_mask) %u", m, t);
     if (m) CK(cudaMemcpyAsync(ctx->moff.p, ctx->h_moff, (size_t)m * 2, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaEventRecord(ctx->plan_ev[1], ctx->stream));
+    return CKS_OK;
+}
+
+// D accumulated on the device (u32 words, key bit p = bit 31 - p%32 of word p/32) -> host mask
+int read_dacc(cks_ctx* ctx, uint32_t B, uint8_t* mask_out) {
+    const uint32_t nwords = (8 * B + 31) / 32;
+    CK(cudaEventSynchronize(ctx->plan_ev[2]));
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->dacc.p, (size_t)nwords * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (uint32_t j = 0; j < B; j++) mask_out[j] = (uint8_t)(ctx->h_small[j >> 2] >> (24 - 8 * (j & 3)));
+    return CKS_OK;
+}
+
+// a6: exact D from sorted planes compressed with `sort_mask` (host).
+int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint64_t pitch, uint32_t m, uint64_t n,
+                 const uint8_t* sort_mask, uint32_t B, uint8_t* mask_out, uint16_t* dbit) {
+    const uint32_t nwords = (8 * B + 31) / 32;
+    TRY(ensure(ctx, ctx->dacc, (size_t)nwords * 4));
+    TRY(upload_moff(ctx, sort_mask, B, m));
     CK(cudaMemsetAsync(ctx->dacc.p, 0, (size_t)nwords * 4, ctx->stream));
     if (n && m) {
         LAUNCH(launch_adjacent(sorted, pitch, n, m, as<uint16_t>(ctx->moff), B, dbit, as<uint32_t>(ctx->dacc),
@@ -325,10 +361,167 @@ int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint64_t pitch, uint32_t 
     } else if (n && dbit) {
         LAUNCH(launch_fill_u16(dbit, n, (uint16_t)CKS_DBIT_NONE, ctx->stream));
     }
-    CK(cudaEventSynchronize(ctx->plan_ev[2]));
-    CK(cudaMemcpyAsync(ctx->h_small, ctx->dacc.p, (size_t)nwords * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    for (uint32_t j = 0; j < B; j++) mask_out[j] = (uint8_t)(ctx->h_small[j >> 2] >> (24 - 8 * (j & 3)));
+    return read_dacc(ctx, B, mask_out);
+}
+
+// Sub-mask of P_M bits that are exact-D positions, for the repack (a7). P_M bit of the
+// compressed index t (0 = first mask position) is m - 1 - t + lead.
+static void repack_words(const uint8_t* M, const uint8_t* D, uint32_t B, uint32_t m, uint32_t lead,
+                         std::vector<uint32_t>& sub) {
+    uint32_t t = 0;
+    for (uint32_t p = 0; p < 8 * B; p++) {
+        if (!((M[p >> 3] >> (7 - (p & 7))) & 1)) continue;
+        const uint32_t b = m - 1 - t + lead;
+        if ((D[p >> 3] >> (7 - (p & 7))) & 1) sub[b >> 5] |= 1u << (b & 31);
+        t++;
+    }
+}
+
+// NEXT-1: first build by distinguishing prefixes (k_refine.cu). Outputs perm, dbit, the
+// exact D (out->mask) and P_D in sorted order (out->packed).
+int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* M, uint32_t m,
+                 cks_build_out* out, uint16_t* dbit) {
+    const uint32_t np = (m + 31) / 32, nch = (np + 1) / 2, lead = 32 * np - m;
+    const uint64_t sp = scratch_pitch(n);
+    const uint32_t nwords = (8 * B + 31) / 32;
+    // a3: P_M left-aligned (the first mask position is bit 31 of the top plane), so chunk r
+    // is planes np-1-2r (high word) and np-2-2r (low word)
+    TRY(ensure(ctx, ctx->pm, (size_t)np * sp * 4));
+    uint32_t* pm = as<uint32_t>(ctx->pm);
+    TRY(run_compress(ctx, keys, n, B, M, pm, sp, lead));
+    mark(ctx, ST_COMPRESS);
+    mark(ctx, ST_HIST);
+    TRY(upload_moff(ctx, M, B, m));
+    TRY(ensure(ctx, ctx->dacc, (size_t)nwords * 4));
+    CK(cudaMemsetAsync(ctx->dacc.p, 0, (size_t)nwords * 4, ctx->stream));
+    TRY(ensure(ctx, ctx->tie, n + 16));
+    const uint16_t* moff = as<uint16_t>(ctx->moff);
+    uint32_t* dacc = as<uint32_t>(ctx->dacc);
+    uint8_t* tie = as<uint8_t>(ctx->tie);
+
+    // round 0: every key by chunk 0
+    const uint32_t np0 = np >= 2 ? 2 : 1;
+    const uint32_t* sorted0 = nullptr;
+    uint64_t sp0 = sp;
+    TRY(run_sort(ctx, pm + (uint64_t)(np - np0) * sp, sp, np0, 4 * np0, n, nullptr, 0, nullptr, 0, out->perm,
+                 &sorted0, &sp0, np <= 2 ? lead / 8 : 0));
+    LAUNCH(launch_ref_adj(np0 == 2 ? sorted0 : nullptr, sorted0 + (uint64_t)(np0 - 1) * sp0, nullptr, nullptr, n, 0,
+                          moff, m, B, dbit, tie, dacc, true, ctx->sms, ctx->stream));
+    out->rounds = 1;
+    out->refined_keys = 0;
+    out->passes = 4 * np0 - (np <= 2 ? lead / 8 : 0);
+    // rounds 1..: the tied runs. Short runs (and runs of equal keys) are finished in place by
+    // comparing their remaining bits; the others are re-sorted by (run, chunk r).
+    uint64_t nr = n;
+    const uint32_t* pos = nullptr;                               // list of round r-1 (null: all keys)
+    if (nch > 1) {
+        DevBuf* pb[3] = {&ctx->posA, &ctx->posB, &ctx->posC};
+        DevBuf* sb[3] = {&ctx->segA, &ctx->segB, &ctx->segC};
+        for (int i = 0; i < 3; i++) {
+            TRY(ensure(ctx, *pb[i], sp * 4));
+            TRY(ensure(ctx, *sb[i], sp * 4));
+        }
+        TRY(ensure(ctx, ctx->runoff, sp * 4));
+        TRY(ensure(ctx, ctx->keep, n + 16));
+        TRY(ensure(ctx, ctx->done, n + 16));
+        TRY(ensure(ctx, ctx->rcnt, (size_t)(ref_tiles(n) + 1) * 8));
+        TRY(ensure(ctx, ctx->rtot, 16));
+    }
+    auto counts = [&](uint64_t* a, uint64_t* b) -> int {
+        CK(cudaMemcpyAsync(ctx->h_tot, ctx->rtot.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        *a = ctx->h_tot[0];
+        *b = ctx->h_tot[1];
+        return CKS_OK;
+    };
+    const bool log = getenv("CKS_REFINE_LOG") != nullptr;
+    int li = -1;                                                 // buffer of the current list
+    for (uint32_t r = 1; r < nch; r++) {
+        const int ai = li == 0 ? 1 : 0;                          // (1)'s output
+        const int bi = li < 0 ? 1 : 3 - li - ai;                 // (3)'s output, the next list
+        uint32_t* posA_ = as<uint32_t>(ai == 0 ? ctx->posA : ai == 1 ? ctx->posB : ctx->posC);
+        uint32_t* segA_ = as<uint32_t>(ai == 0 ? ctx->segA : ai == 1 ? ctx->segB : ctx->segC);
+        uint32_t* posB_ = as<uint32_t>(bi == 0 ? ctx->posA : bi == 1 ? ctx->posB : ctx->posC);
+        uint32_t* segB_ = as<uint32_t>(bi == 0 ? ctx->segA : bi == 1 ? ctx->segB : ctx->segC);
+        // (1) the tied runs of the current list
+        LAUNCH(launch_ref_compact(tie, nr, pos, as<uint32_t>(ctx->rcnt), as<uint32_t>(ctx->rtot), posA_, segA_,
+                                  as<uint32_t>(ctx->runoff), ctx->stream));
+        uint64_t nn = 0, nseg = 0;
+        TRY(counts(&nn, &nseg));
+        if (nn == 0) break;
+        // (2) finish short runs and runs of equal keys in place
+        const int qtop = (int)np - 1 - 2 * (int)r;
+        LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, posA_, segA_, as<uint32_t>(ctx->runoff), nseg, nn, out->perm,
+                                dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), ctx->sms, ctx->stream));
+        // (3) the runs left for an LSD round
+        LAUNCH(launch_ref_compact(as<uint8_t>(ctx->keep), nn, posA_, as<uint32_t>(ctx->rcnt), as<uint32_t>(ctx->rtot),
+                                  posB_, segB_, nullptr, ctx->stream));
+        uint64_t n2 = 0, nseg2 = 0;
+        TRY(counts(&n2, &nseg2));
+        if (log)
+            fprintf(stderr, "[cks refine] round %u: %llu tied keys in %llu runs; %llu keys in %llu runs left for LSD\n",
+                    r, (unsigned long long)nn, (unsigned long long)nseg, (unsigned long long)n2,
+                    (unsigned long long)nseg2);
+        out->refined_keys += nn;
+        if (n2 == 0) break;
+        out->rounds = r + 1;
+        // (4) LSD round: the left runs by (run, chunk r)
+        const int qhi = (int)np - 1 - 2 * (int)r, qlo = (int)np - 2 - 2 * (int)r;
+        const uint64_t cp = scratch_pitch(n2);
+        TRY(ensure(ctx, ctx->cmp, (size_t)3 * cp * 4));
+        TRY(ensure(ctx, ctx->crid, cp * 4));
+        TRY(ensure(ctx, ctx->crid2, cp * 4));
+        LAUNCH(launch_ref_gather(pm, sp, qhi, qlo, posB_, segB_, out->perm, n2, as<uint32_t>(ctx->cmp), cp,
+                                 as<uint32_t>(ctx->crid), ctx->sms, ctx->stream));
+        const uint32_t segbits = nseg2 > 1 ? 32u - (uint32_t)__builtin_clz((uint32_t)(nseg2 - 1)) : 0u;
+        uint32_t d0 = 0;
+        if (qlo < 0) d0 = 4 + lead / 8;                  // single-plane chunk: high word = plane 0
+        else if (qlo == 0) d0 = lead / 8;                // low word = plane 0 holds the padding
+        const uint32_t* sv = nullptr;
+        uint64_t svp = cp;
+        out->passes += 8 + (segbits + 7) / 8 - d0;
+        TRY(run_sort(ctx, as<uint32_t>(ctx->cmp), cp, 3, 8 + (segbits + 7) / 8, n2, as<uint32_t>(ctx->crid), 0,
+                     nullptr, 0, as<uint32_t>(ctx->crid2), &sv, &svp, d0));
+        LAUNCH(launch_ref_put(out->perm, posB_, as<uint32_t>(ctx->crid2), n2, ctx->sms, ctx->stream));
+        LAUNCH(launch_ref_adj(qlo >= 0 ? sv : nullptr, sv + svp, sv + 2 * svp, posB_, n2, 64 * r, moff, m, B, dbit,
+                              tie, dacc, false, ctx->sms, ctx->stream));
+        pos = posB_;
+        nr = n2;
+        li = bi;
+    }
+    mark(ctx, ST_SORT);
+    TRY(read_dacc(ctx, B, out->mask));
+    out->popcount = popcount_mask(out->mask, B);
+    for (uint32_t j = 0; j < B; j++)
+        if (out->mask[j] & ~M[j])
+            return fail(ctx, CKS_ERANGE, "adjacency produced a bit outside the sort mask (byte %u)", j);
+    mark(ctx, ST_ADJ);
+    // a7: P_D in sorted order -- from the sorted chunk when one chunk held all of P_M,
+    // otherwise compressed again from the key rows in sorted order
+    const uint32_t npd = (out->popcount + 31) / 32;
+    out->packed = nullptr;
+    out->packed_pitch = sp;
+    if (out->popcount > 0) {
+        TRY(ensure(ctx, ctx->pd, (size_t)npd * sp * 4));
+        uint32_t* pd = as<uint32_t>(ctx->pd);
+        if (nch == 1 && lead == 0 && same_mask(out->mask, M, B)) {
+            out->packed = sorted0;
+            out->packed_pitch = sp0;
+        } else if (nch == 1) {
+            std::vector<uint32_t> sub(np, 0);
+            repack_words(M, out->mask, B, m, lead, sub);
+            TRY(claim_slot(ctx, 1));
+            plan_repack(sub.data(), np, ctx->h_plan[1]);
+            GatherPlan* dplan;
+            TRY(upload_plan(ctx, 1, &dplan));
+            LAUNCH(launch_repack(sorted0, sp0, n, dplan, ctx->h_plan[1]->nsteps, npd, pd, sp, ctx->sms, ctx->stream));
+            out->packed = pd;
+        } else {
+            TRY(run_compress(ctx, keys, n, B, out->mask, pd, sp, 0, out->perm));
+            out->packed = pd;
+        }
+    }
+    mark(ctx, ST_REPACK);
     return CKS_OK;
 }
 
@@ -400,18 +593,35 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
     return CKS_OK;
 }
 
-bool same_mask(const uint8_t* a, const uint8_t* b, uint32_t B) { return memcmp(a, b, B) == 0; }
-
 // Everything after the sort mask is known: a3 .. a8 on device keys.
 int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* M,
                     uint32_t m, cks_build_out* out, bool check_superset) {
     const uint32_t np = (m + 31) / 32, k = (m + 7) / 8;
     out->sort_bits = m;
     out->passes = k;
+    out->rounds = 0;
+    out->refined_keys = 0;
     uint16_t* dbit = out->dbit;
     if (!dbit && n) {
         TRY(ensure(ctx, ctx->dbit, n * 2));
         dbit = as<uint16_t>(ctx->dbit);
+    }
+    if (ctx->refine < 0) {
+        const char* e = getenv("CKS_REFINE");
+        ctx->refine = e ? atoi(e) : 1;
+    }
+    // 1 = auto: by prefixes when P_M spans more than two 64-bit chunks (m > 128); below that
+    // the first chunk already covers most of P_M and the single sort carrying all planes is
+    // cheaper than the refinement rounds plus the final gather of P_D
+    if (n && m && (ctx->refine == 2 || (ctx->refine == 1 && m > 128))) {
+        TRY(build_refine(ctx, keys, n, B, M, m, out, dbit));
+        out->height = 0;
+        if (out->tree.node_cnt) {
+            cks_tree tr = out->tree;
+            TRY(run_bulkload(ctx, out->perm, dbit, n, out->fanout, out->fill, &tr, &out->height));
+        }
+        mark(ctx, ST_BULK);
+        return CKS_OK;
     }
     // a3: compress into whichever plane buffer the first LSD pass does not write
     const uint64_t sp = scratch_pitch(n);
@@ -441,13 +651,7 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     out->packed_pitch = spitch;
     if (!same_mask(out->mask, M, B) && out->popcount > 0) {
         std::vector<uint32_t> sub(np, 0);
-        uint32_t t = 0;                                   // compressed index from the MSB
-        for (uint32_t p = 0; p < 8 * B; p++) {
-            if (!((M[p >> 3] >> (7 - (p & 7))) & 1)) continue;
-            uint32_t b = m - 1 - t;                       // bit of P_M
-            if ((out->mask[p >> 3] >> (7 - (p & 7))) & 1) sub[b >> 5] |= 1u << (b & 31);
-            t++;
-        }
+        repack_words(M, out->mask, B, m, 0, sub);
         TRY(claim_slot(ctx, 1));
         plan_repack(sub.data(), np, ctx->h_plan[1]);
         GatherPlan* dplan;
@@ -505,11 +709,14 @@ int cks_ctx_create(int device, void* stream, cks_ctx** out) {
     }
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     bool ok = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+    if (ok) ok = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; i < 2 && ok; i++) ok = cudaEventCreateWithFlags(&ctx->aux_ev[i], cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < ST_N && ok; i++) ok = cudaEventCreate(&ctx->ev[i]) == cudaSuccess;
     for (int i = 0; i < 3 && ok; i++) ok = cudaEventCreateWithFlags(&ctx->plan_ev[i], cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < 2 && ok; i++) ok = cudaMallocHost(&ctx->h_plan[i], sizeof(GatherPlan)) == cudaSuccess;
     if (ok) ok = cudaMallocHost(&ctx->h_moff, kMaxBits * 2) == cudaSuccess;
     if (ok) ok = cudaMallocHost(&ctx->h_small, 8192) == cudaSuccess;
+    if (ok) ok = cudaMallocHost(&ctx->h_tot, 64) == cudaSuccess;
     for (int i = 0; i < 3 && ok; i++) ok = cudaEventRecord(ctx->plan_ev[i], ctx->stream) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -527,7 +734,10 @@ int cks_ctx_destroy(cks_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->occ, &ctx->masks8, &ctx->planeA, &ctx->planeB, &ctx->ridA, &ctx->ridB,
                       &ctx->hist, &ctx->base, &ctx->status, &ctx->counters, &ctx->dacc, &ctx->moff,
                       &ctx->dbit, &ctx->rmin0, &ctx->rmin1, &ctx->plan[0], &ctx->plan[1], &ctx->plan[2],
-                      &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total};
+                      &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total,
+                      &ctx->pm, &ctx->pd, &ctx->cmp, &ctx->crid, &ctx->crid2, &ctx->posA, &ctx->posB,
+                      &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->tie, &ctx->keep, &ctx->done,
+                      &ctx->rcnt, &ctx->rtot};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int i = 0; i < ST_N; i++)
@@ -538,7 +748,11 @@ int cks_ctx_destroy(cks_ctx* ctx) {
         if (ctx->h_plan[i]) cudaFreeHost(ctx->h_plan[i]);
     if (ctx->h_moff) cudaFreeHost(ctx->h_moff);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
+    if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+    for (int i = 0; i < 2; i++)
+        if (ctx->aux_ev[i]) cudaEventDestroy(ctx->aux_ev[i]);
     delete ctx;
     return CKS_OK;
 }

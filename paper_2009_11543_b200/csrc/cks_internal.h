@@ -46,9 +46,11 @@ cudaError_t launch_occ_finalize(const uint32_t* occ, uint32_t B, uint64_t n, uin
 // Planes are u32 SoA arrays: plane q of a packed array starts at ptr + q*pitch (pitch in
 // elements; user buffers have pitch n, library scratch pads the pitch to 32 elements so every
 // plane is 128-byte aligned for TMA).
+// lead: P is stored shifted left by `lead` bits (left-aligned planes when lead = 32*np - m);
+// rows != NULL: key i is keys[rows[i]] (compress in a given order).
 cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
                             const GatherPlan* hplan, uint32_t out_planes, uint32_t* planes, uint64_t pitch,
-                            int sms, cudaStream_t st);
+                            int sms, cudaStream_t st, uint32_t lead = 0, const uint32_t* rows = nullptr);
 cudaError_t launch_repack(const uint32_t* in_planes, uint64_t in_pitch, uint64_t n, const GatherPlan* dplan,
                           uint32_t nsteps, uint32_t out_planes, uint32_t* out, uint64_t out_pitch, int sms,
                           cudaStream_t st);
@@ -103,13 +105,35 @@ struct LsdPassArgs {
     uint32_t tile_begin;         // first tile this launch covers (set by the launcher)
     uint32_t debug;              // timing experiments only (CKS_LSD_DEBUG); results are wrong when set
 };
-cudaError_t launch_lsd_pass(const LsdPassArgs& a, int sms, cudaStream_t st, int* launches);
+// optional side stream for the partial last tile (runs concurrently with the full tiles)
+struct LsdAux {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+cudaError_t launch_lsd_pass(const LsdPassArgs& a, int sms, cudaStream_t st, const LsdAux& aux, int* launches);
 void lsd_sizes(uint64_t n, uint64_t* tiles, uint64_t* chunks);
 
 cudaError_t launch_adjacent(const uint32_t* planes, uint64_t pitch, uint64_t n, uint32_t m, const uint16_t* moff,
                             uint32_t B, uint16_t* dbit_out, uint32_t* dacc /* u32[ceil(8B/32)] */,
                             int sms, cudaStream_t st);
 cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
+
+// NEXT-1 prefix refinement (k_refine.cu)
+uint64_t ref_tiles(uint64_t nr);
+cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_t* seg, const uint32_t* pos,
+                           uint64_t nr, uint32_t cbase, const uint16_t* moff, uint32_t m, uint32_t B,
+                           uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st);
+cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* pos, uint32_t* cnt, uint32_t* tot,
+                               uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, cudaStream_t st);
+cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
+                             const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
+                             uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
+                             int sms, cudaStream_t st);
+cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, int qhi, int qlo, const uint32_t* pos,
+                              const uint32_t* seg, const uint32_t* perm, uint64_t nr, uint32_t* out, uint64_t opitch,
+                              uint32_t* orid, int sms, cudaStream_t st);
+cudaError_t launch_ref_put(uint32_t* perm, const uint32_t* pos, const uint32_t* rid, uint64_t nr, int sms,
+                           cudaStream_t st);
 cudaError_t launch_fill_u16(uint16_t* out, uint64_t n, uint16_t v, cudaStream_t st);
 
 struct BulkLevel {

@@ -43,7 +43,7 @@ constexpr int kCompressThreads = 256;
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_tiled(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
                  const GatherPlan* __restrict__ plan, uint32_t nsteps, uint32_t np,
-                 uint32_t* __restrict__ planes, uint64_t pitch) {
+                 uint32_t* __restrict__ planes, uint64_t pitch, uint32_t lead) {
     extern __shared__ int4 s_tile[];                      // [256][S16] int4 units
     __shared__ GatherStep s_step[kMaxWords];
     for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
@@ -65,7 +65,7 @@ k_compress_tiled(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
             const int4* row = s_tile + threadIdx.x * S16;
             const uint64_t i = k0 + threadIdx.x;
             unsigned long long acc = 0;
-            uint32_t accbits = 0, q = 0;
+            uint32_t accbits = lead, q = 0;
             int cur_u = -1;
             int4 cur = make_int4(0, 0, 0, 0);
             for (uint32_t s = 0; s < nsteps; s++) {
@@ -95,15 +95,15 @@ k_compress_tiled(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_generic(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
                    const GatherPlan* __restrict__ plan, uint32_t nsteps, uint32_t np,
-                   uint32_t* __restrict__ planes, uint64_t pitch) {
+                   uint32_t* __restrict__ planes, uint64_t pitch, uint32_t lead, const uint32_t* __restrict__ rows) {
     __shared__ GatherStep s_step[kMaxWords];
     for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
     __syncthreads();
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint8_t* k = keys + i * B;
+        const uint8_t* k = keys + (rows ? (uint64_t)rows[i] : i) * B;
         unsigned long long acc = 0;
-        uint32_t accbits = 0, q = 0;
+        uint32_t accbits = lead, q = 0;
         for (uint32_t s = 0; s < nsteps; s++) {
             const GatherStep& g = s_step[s];
             uint32_t w = 0;
@@ -167,19 +167,20 @@ struct FixedPlan {
 template <int B>
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_fixed(const uint8_t* __restrict__ keys, uint64_t n, const __grid_constant__ FixedPlan<B / 4> plan,
-                 uint32_t* __restrict__ planes, uint64_t pitch) {
+                 uint32_t* __restrict__ planes, uint64_t pitch, uint32_t lead, const uint32_t* __restrict__ rows) {
     constexpr int NW = B / 4;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t w[NW];
+        const uint8_t* kp = keys + (rows ? (uint64_t)__ldg(rows + i) : i) * B;
         if (B == 8) {
-            uint2 v = __ldg(reinterpret_cast<const uint2*>(keys + i * B));
+            uint2 v = __ldg(reinterpret_cast<const uint2*>(kp));
             w[0] = v.x;
             w[1] = v.y;
         } else {
 #pragma unroll
             for (int u = 0; u < B / 16; u++) {
-                uint4 v = __ldg(reinterpret_cast<const uint4*>(keys + i * B) + u);
+                uint4 v = __ldg(reinterpret_cast<const uint4*>(kp) + u);
                 w[4 * u + 0] = v.x;
                 w[4 * u + 1] = v.y;
                 w[4 * u + 2] = v.z;
@@ -187,7 +188,7 @@ k_compress_fixed(const uint8_t* __restrict__ keys, uint64_t n, const __grid_cons
             }
         }
         unsigned long long acc = 0;
-        uint32_t accbits = 0, q = 0;
+        uint32_t accbits = lead, q = 0;
 #pragma unroll
         for (int k = NW - 1; k >= 0; k--) {                      // least significant end of P first
             if (plan.mask[k] == 0) continue;
@@ -212,7 +213,7 @@ k_compress_fixed(const uint8_t* __restrict__ keys, uint64_t n, const __grid_cons
 
 template <int B>
 static void launch_fixed(const uint8_t* keys, uint64_t n, const GatherPlan* hplan, uint32_t* planes, uint64_t pitch,
-                         int grid, cudaStream_t st) {
+                         uint32_t lead, const uint32_t* rows, int grid, cudaStream_t st) {
     FixedPlan<B / 4> fp;
     memset(&fp, 0, sizeof(fp));
     for (uint32_t s = 0; s < hplan->nsteps; s++) {
@@ -221,7 +222,7 @@ static void launch_fixed(const uint8_t* keys, uint64_t n, const GatherPlan* hpla
         for (int k = 0; k < 5; k++) fp.mv[g.src][k] = g.mv[k];
         fp.cnt[g.src] = g.cnt;
     }
-    k_compress_fixed<B><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch);
+    k_compress_fixed<B><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, lead, rows);
 }
 
 static int grid_for(uint64_t work, int per_sm, int sms) {
@@ -233,30 +234,30 @@ static int grid_for(uint64_t work, int per_sm, int sms) {
 
 cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
                             const GatherPlan* hplan, uint32_t np, uint32_t* planes, uint64_t pitch, int sms,
-                            cudaStream_t st) {
+                            cudaStream_t st, uint32_t lead, const uint32_t* rows) {
     if (n == 0 || np == 0) return cudaSuccess;
     const uint32_t nsteps = hplan->nsteps;
     if (((uintptr_t)keys & 15) == 0 && (B == 8 || B == 16 || B == 32 || B == 64)) {
         int grid = grid_for(n, 8, sms);
         switch (B) {
-            case 8: launch_fixed<8>(keys, n, hplan, planes, pitch, grid, st); break;
-            case 16: launch_fixed<16>(keys, n, hplan, planes, pitch, grid, st); break;
-            case 32: launch_fixed<32>(keys, n, hplan, planes, pitch, grid, st); break;
-            default: launch_fixed<64>(keys, n, hplan, planes, pitch, grid, st); break;
+            case 8: launch_fixed<8>(keys, n, hplan, planes, pitch, lead, rows, grid, st); break;
+            case 16: launch_fixed<16>(keys, n, hplan, planes, pitch, lead, rows, grid, st); break;
+            case 32: launch_fixed<32>(keys, n, hplan, planes, pitch, lead, rows, grid, st); break;
+            default: launch_fixed<64>(keys, n, hplan, planes, pitch, lead, rows, grid, st); break;
         }
         return cudaGetLastError();
     }
-    if ((B & 15) == 0 && ((uintptr_t)keys & 15) == 0) {
+    if ((B & 15) == 0 && ((uintptr_t)keys & 15) == 0 && !rows) {
         uint32_t S16 = (B >> 4) | 1;
         size_t smem = (size_t)kCompressThreads * S16 * 16;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_compress_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = smem <= 24 * 1024 ? 8 : smem <= 48 * 1024 ? 4 : smem <= 100 * 1024 ? 2 : 1;
         k_compress_tiled<<<grid_for(n, per_sm, sms), kCompressThreads, smem, st>>>(keys, n, B, dplan, nsteps,
-                                                                                   np, planes, pitch);
+                                                                                   np, planes, pitch, lead);
     } else {
         k_compress_generic<<<grid_for(n, 8, sms), kCompressThreads, 0, st>>>(keys, n, B, dplan, nsteps, np,
-                                                                             planes, pitch);
+                                                                             planes, pitch, lead, rows);
     }
     return cudaGetLastError();
 }

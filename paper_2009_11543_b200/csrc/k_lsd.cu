@@ -648,7 +648,7 @@ void lsd_sizes(uint64_t n, uint64_t* tiles, uint64_t* chunks) {
 }
 
 template <int ITEMS>
-static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, int* launches) {
+static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAux& aux, int* launches) {
     constexpr int TILE = kSortThreads * ITEMS;
     const uint64_t tiles = (a.n + TILE - 1) / TILE;
     const uint64_t chunks = (tiles + a.chunk_tiles - 1) / a.chunk_tiles;
@@ -675,9 +675,29 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, int* launch
             configured_ws = smem;
         }
         const uint64_t grid = nfull < (uint64_t)sms ? nfull : (uint64_t)sms;
+        const bool tail = nfull != tiles;
+        if (tail && aux.stream) {
+            // the partial last tile runs concurrently on the aux stream (its offsets are
+            // already known from the upsweep)
+            LsdPassArgs tl = a;
+            tl.tile_begin = (uint32_t)nfull;
+            if ((int)tl.slots > 2 * streams) tl.slots = streams > 0 ? 2 * streams : 1;
+            const size_t tsm = (size_t)tl.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 2;
+            static size_t configured_t = 0;
+            if (tsm > configured_t) {
+                cudaFuncSetAttribute(k_downsweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+                configured_t = tsm;
+            }
+            cudaEventRecord(aux.fork, st);
+            cudaStreamWaitEvent(aux.stream, aux.fork, 0);
+            k_downsweep<ITEMS><<<1, kSortThreads, tsm, aux.stream>>>(tl);
+            cudaEventRecord(aux.join, aux.stream);
+            nl++;
+        }
         k_downsweep_ws<ITEMS><<<(unsigned)grid, kWsThreads, smem, st>>>(w, (uint32_t)nfull);
         nl++;
-        if (nfull == tiles) { *launches = nl; return cudaGetLastError(); }
+        if (tail && aux.stream) cudaStreamWaitEvent(st, aux.join, 0);
+        if (!tail || aux.stream) { *launches = nl; return cudaGetLastError(); }
         a.tile_begin = (uint32_t)nfull;                      // the partial last tile
     }
     if ((int)a.slots > 2 * streams) a.slots = streams > 0 ? 2 * streams : 1;
@@ -698,7 +718,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, int* launch
     return cudaGetLastError();
 }
 
-cudaError_t launch_lsd_pass(const LsdPassArgs& args, int sms, cudaStream_t st, int* launches) {
+cudaError_t launch_lsd_pass(const LsdPassArgs& args, int sms, cudaStream_t st, const LsdAux& aux, int* launches) {
     *launches = 0;
     if (args.n == 0) return cudaSuccess;
     lsd_config();
@@ -710,7 +730,7 @@ cudaError_t launch_lsd_pass(const LsdPassArgs& args, int sms, cudaStream_t st, i
     a.debug = (uint32_t)dbg;
     a.tma = ((uintptr_t)a.in_planes % 16 == 0) && (a.in_pitch % 4 == 0) &&
             (a.in_rid == nullptr || (uintptr_t)a.in_rid % 16 == 0);
-    return g_lsd_items == 8 ? lsd_pass<8>(a, sms, st, launches) : lsd_pass<16>(a, sms, st, launches);
+    return g_lsd_items == 8 ? lsd_pass<8>(a, sms, st, aux, launches) : lsd_pass<16>(a, sms, st, aux, launches);
 }
 
 }  // namespace cks

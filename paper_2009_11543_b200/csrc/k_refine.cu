@@ -1,0 +1,342 @@
+// k_refine.cu -- NEXT-1: first-build sort by distinguishing prefixes.
+//
+// The paper builds from compressed keys and notes that sorting needs only the bits that
+// distinguish neighbours ("sort by distinguishing prefixes"; Theorem 2).
+// The first build here sorts on 64-bit chunks of the superset-compressed key P_M, most
+// significant chunk first:
+//   round 0  LSD-sort all keys by chunk 0 (k_lsd.cu), carrying only that chunk + row id;
+//   round r  the keys whose chunks 0..r-1 tie with a neighbour ("runs") are gathered into a
+//            compact list (chunk r of P_M by row id, run index), LSD-sorted by (run, chunk r)
+//            -- stable, so ties keep row-id order -- and written back into their run's
+//            positions, which are contiguous in the global order.
+// A pair of neighbours is separated in the first round whose chunk differs; its D-bit
+// is the first differing bit of that chunk, mapped through the M-offset table
+// (P:479): D_i = moff[64 r + clz64(chunk_i XOR chunk_{i-1})]. Pairs equal in every chunk
+// are duplicates (D_i = none, reading R3). The union of the D_i is the exact D.
+//
+// Kernels: k_ref_adj (round adjacency: D_i, tie flags, D accumulation), k_ref_count /
+// k_ref_scan / k_ref_scatter (compaction of the tied runs into the next round's list),
+// k_ref_gather (chunk r of the listed rows), k_ref_put (sorted row ids back into place).
+#include "cks_internal.h"
+
+namespace cks {
+
+namespace {
+constexpr int kRefThreads = 256;
+constexpr int kRefItems = 16;                    // elements per thread in the compaction
+constexpr int kRefTile = kRefThreads * kRefItems;
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane) {
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    return x - v;
+}
+}  // namespace
+
+// Round adjacency over a sorted list of nr chunks (lo may be NULL: single-plane chunk;
+// seg NULL: one segment; pos NULL: element k sits at global position k).
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_adj(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, const uint32_t* __restrict__ seg,
+          const uint32_t* __restrict__ pos, uint64_t nr, uint32_t cbase, const uint16_t* __restrict__ moff,
+          uint32_t m, uint32_t nwords, uint16_t* __restrict__ dbit, uint8_t* __restrict__ tie,
+          uint32_t* __restrict__ dacc, int round0) {
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* s_bm = s_dyn;                                          // [nwords]
+    uint16_t* s_moff = reinterpret_cast<uint16_t*>(s_dyn + nwords);  // [m]
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
+    for (uint32_t t = threadIdx.x; t < m; t += blockDim.x) s_moff[t] = moff[t];
+    __syncthreads();
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = pos ? pos[k] : k;
+        uint8_t t = 0;
+        if (k == 0) {
+            if (round0) dbit[g] = CKS_NONE_INTERNAL;
+        } else if (!seg || seg[k] == seg[k - 1]) {
+            const unsigned long long x = ((unsigned long long)(hi[k] ^ hi[k - 1]) << 32) |
+                                         (lo ? (unsigned long long)(lo[k] ^ lo[k - 1]) : 0ull);
+            if (x) {
+                const uint32_t d = s_moff[cbase + (uint32_t)__clzll((long long)x)];
+                dbit[g] = (uint16_t)d;
+                const uint32_t w = d >> 5, b = 0x80000000u >> (d & 31);
+                if (!(s_bm[w] & b)) atomicOr(&s_bm[w], b);
+            } else {
+                t = 1;
+                if (round0) dbit[g] = CKS_NONE_INTERNAL;
+            }
+        }
+        // (segment starts of later rounds keep the D_i found in an earlier round)
+        tie[k] = t;
+    }
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
+        if (s_bm[w]) atomicOr(&dacc[w], s_bm[w]);
+}
+
+// Element k belongs to a tied run if it ties with its predecessor or its successor; it
+// starts a run if it does not tie with its predecessor.
+__device__ __forceinline__ void ref_flags(const uint8_t* tie, uint64_t nr, uint64_t k, uint32_t& member,
+                                          uint32_t& start) {
+    if (k >= nr) { member = start = 0; return; }
+    const uint32_t a = tie[k], b = k + 1 < nr ? tie[k + 1] : 0u;
+    member = a | b;
+    start = member & (a ^ 1u);
+}
+
+// per tile of kRefTile elements: (members, run starts)
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_count(const uint8_t* __restrict__ tie, uint64_t nr, uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t s_red[2][kRefThreads / 32];
+    const uint64_t k0 = (uint64_t)blockIdx.x * kRefTile + (uint64_t)threadIdx.x * kRefItems;
+    uint32_t cm = 0, cs = 0;
+#pragma unroll
+    for (int i = 0; i < kRefItems; i++) {
+        uint32_t mb, st;
+        ref_flags(tie, nr, k0 + i, mb, st);
+        cm += mb;
+        cs += st;
+    }
+    cm = __reduce_add_sync(0xffffffffu, cm);
+    cs = __reduce_add_sync(0xffffffffu, cs);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { s_red[0][warp] = cm; s_red[1][warp] = cs; }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        uint32_t s = 0;
+        for (int w = 0; w < kRefThreads / 32; w++) s += s_red[threadIdx.x][w];
+        cnt[2 * (uint64_t)blockIdx.x + threadIdx.x] = s;
+    }
+}
+
+// exclusive scan of the tile counts in place (one CTA); totals to tot[0..1]
+__global__ void __launch_bounds__(1024)
+k_ref_scan(uint32_t* __restrict__ cnt, uint32_t ntiles, uint32_t* __restrict__ tot) {
+    __shared__ uint32_t s_w[2][32];
+    __shared__ uint32_t s_carry[2];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 2) s_carry[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint32_t b0 = 0; b0 < ntiles; b0 += 1024) {
+        const uint32_t b = b0 + threadIdx.x;
+        uint32_t v[2];
+        for (int c = 0; c < 2; c++) v[c] = b < ntiles ? cnt[2 * (uint64_t)b + c] : 0u;
+        uint32_t e[2];
+        for (int c = 0; c < 2; c++) {
+            e[c] = warp_excl_scan(v[c], lane);
+            if (lane == 31) s_w[c][warp] = e[c] + v[c];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            for (int c = 0; c < 2; c++) {
+                const uint32_t x = s_w[c][lane];
+                const uint32_t ex = warp_excl_scan(x, lane);
+                s_w[c][lane] = ex;
+            }
+        }
+        __syncthreads();
+        for (int c = 0; c < 2; c++) {
+            const uint32_t r = s_carry[c] + s_w[c][warp] + e[c];
+            if (b < ntiles) cnt[2 * (uint64_t)b + c] = r;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023)
+            for (int c = 0; c < 2; c++) s_carry[c] += s_w[c][31] + e[c] + v[c];
+        __syncthreads();
+    }
+    if (threadIdx.x < 2) tot[threadIdx.x] = s_carry[threadIdx.x];
+}
+
+// write the next round's list: global position and run index of every tied element
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_scatter(const uint8_t* __restrict__ tie, uint64_t nr, const uint32_t* __restrict__ pos,
+              const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pos_next, uint32_t* __restrict__ seg_next,
+              uint32_t* __restrict__ run_off) {
+    __shared__ uint32_t s_w[2][kRefThreads / 32];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t k0 = (uint64_t)blockIdx.x * kRefTile + (uint64_t)threadIdx.x * kRefItems;
+    uint32_t mb[kRefItems], st[kRefItems], cm = 0, cs = 0;
+#pragma unroll
+    for (int i = 0; i < kRefItems; i++) {
+        ref_flags(tie, nr, k0 + i, mb[i], st[i]);
+        cm += mb[i];
+        cs += st[i];
+    }
+    const uint32_t em = warp_excl_scan(cm, lane), es = warp_excl_scan(cs, lane);
+    if (lane == 31) { s_w[0][warp] = em + cm; s_w[1][warp] = es + cs; }
+    __syncthreads();
+    uint32_t bm = cnt[2 * (uint64_t)blockIdx.x], bs = cnt[2 * (uint64_t)blockIdx.x + 1];
+    for (uint32_t w = 0; w < warp; w++) { bm += s_w[0][w]; bs += s_w[1][w]; }
+    uint32_t om = bm + em, os = bs + es;                    // os = run starts before this thread
+#pragma unroll
+    for (int i = 0; i < kRefItems; i++) {
+        os += st[i];
+        if (mb[i]) {
+            const uint64_t k = k0 + i;
+            pos_next[om] = pos ? pos[k] : (uint32_t)k;
+            seg_next[om] = os - 1;
+            if (st[i] && run_off) run_off[os - 1] = om;
+            om++;
+        }
+    }
+}
+
+// chunk r (hi = plane qhi, lo = plane qlo or none) of the listed rows, plus run and row id
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_gather(const uint32_t* __restrict__ pm, uint64_t pitch, int qhi, int qlo, const uint32_t* __restrict__ pos,
+             const uint32_t* __restrict__ seg, const uint32_t* __restrict__ perm, uint64_t nr,
+             uint32_t* __restrict__ out, uint64_t opitch, uint32_t* __restrict__ orid) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t row = perm[pos[k]];
+        out[k] = qlo >= 0 ? __ldg(pm + (uint64_t)qlo * pitch + row) : 0u;
+        out[opitch + k] = __ldg(pm + (uint64_t)qhi * pitch + row);
+        out[2 * opitch + k] = seg[k];
+        orid[k] = row;
+    }
+}
+
+// Finish small tied runs in place. Thread per run s of the list (members run_off[s] ..
+// run_off[s+1]-1 at the contiguous global positions pos[run_off[s]] + j): a run of at most
+// kLocal keys is sorted by its remaining P_M bits (planes qtop .. 0; the earlier chunks tie)
+// with the row id as tie-break -- the stable order -- and its D_i are taken from the first
+// differing remaining bit. A longer run whose keys are all equal is already in row-id order
+// (duplicates). Every other run is flagged for the next LSD round (keep[k] = 1 for its
+// members but the first: the compaction's tie convention).
+constexpr uint32_t kLocal = 16;
+constexpr uint32_t kDupCheck = 64;
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* __restrict__ moff,
+            const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
+            uint32_t* __restrict__ perm, uint16_t* __restrict__ dbit, uint32_t* __restrict__ dacc,
+            uint8_t* __restrict__ done) {
+    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k0 = run_off[s];
+        const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
+        const uint32_t L = k1 - k0;
+        const uint32_t p0 = pos[k0];
+        // -1: a < b, 1: a > b, 0: equal remaining bits; *t = first differing compressed index
+        auto cmp = [&](uint32_t a, uint32_t b, uint32_t* t) -> int {
+            for (int q = qtop; q >= 0; q--) {
+                const uint32_t wa = __ldg(pm + (uint64_t)q * pitch + a), wb = __ldg(pm + (uint64_t)q * pitch + b);
+                if (wa != wb) {
+                    if (t) *t = 32u * (np - 1 - (uint32_t)q) + (uint32_t)__clz(wa ^ wb);
+                    return wa < wb ? -1 : 1;
+                }
+            }
+            return 0;
+        };
+        if (L <= kLocal) {
+            uint32_t rows[kLocal];
+#pragma unroll
+            for (uint32_t j = 0; j < kLocal; j++) rows[j] = j < L ? perm[p0 + j] : 0u;
+            for (uint32_t j = 1; j < L; j++) {                   // insertion sort, stable by row id
+                const uint32_t x = rows[j];
+                uint32_t i = j;
+                while (i > 0) {
+                    const int c = cmp(rows[i - 1], x, nullptr);
+                    if (c < 0 || (c == 0 && rows[i - 1] < x)) break;
+                    rows[i] = rows[i - 1];
+                    i--;
+                }
+                rows[i] = x;
+            }
+            for (uint32_t j = 0; j < L; j++) {
+                perm[p0 + j] = rows[j];
+                if (j == 0) continue;
+                uint32_t tt = 0;
+                if (cmp(rows[j - 1], rows[j], &tt) != 0) {
+                    const uint32_t d = moff[tt];
+                    dbit[p0 + j] = (uint16_t)d;
+                    atomicOr(&dacc[d >> 5], 0x80000000u >> (d & 31));
+                }
+            }
+        } else {
+            // a moderately long run of equal keys is finished too (row-id order = stable order)
+            bool dup = L <= kDupCheck;
+            const uint32_t r0 = perm[p0];
+            for (uint32_t j = 1; dup && j < L; j++) dup = cmp(r0, perm[p0 + j], nullptr) == 0;
+            done[s] = dup ? 1 : 0;
+            continue;
+        }
+        done[s] = 1;
+    }
+}
+
+// keep[k] = 1 for the members of unfinished runs except each run's first (the tie convention
+// of the compaction), 0 otherwise
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_keep(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ run_off, const uint8_t* __restrict__ done,
+           uint64_t nn, uint8_t* __restrict__ keep) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nn; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = seg[k];
+        keep[k] = (!done[s] && run_off[s] != (uint32_t)k) ? 1 : 0;
+    }
+}
+
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_put(uint32_t* __restrict__ perm, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ rid, uint64_t nr) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += (uint64_t)gridDim.x * blockDim.x)
+        perm[pos[k]] = rid[k];
+}
+
+// ---- launchers --------------------------------------------------------------------------------
+
+static unsigned grid_of(uint64_t work, int sms) {
+    uint64_t g = (work + kRefThreads - 1) / kRefThreads;
+    const uint64_t cap = (uint64_t)sms * 8;
+    if (g > cap) g = cap;
+    return (unsigned)(g ? g : 1);
+}
+
+uint64_t ref_tiles(uint64_t nr) { return (nr + kRefTile - 1) / kRefTile; }
+
+cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_t* seg, const uint32_t* pos,
+                           uint64_t nr, uint32_t cbase, const uint16_t* moff, uint32_t m, uint32_t B,
+                           uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st) {
+    if (nr == 0) return cudaSuccess;
+    const uint32_t nwords = (8 * B + 31) / 32;
+    const size_t smem = (size_t)nwords * 4 + (size_t)m * 2 + 16;
+    k_ref_adj<<<grid_of(nr, sms), kRefThreads, smem, st>>>(lo, hi, seg, pos, nr, cbase, moff, m, nwords, dbit, tie,
+                                                           dacc, round0 ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* pos, uint32_t* cnt, uint32_t* tot,
+                               uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, cudaStream_t st) {
+    const uint64_t tiles = ref_tiles(nr);
+    if (tiles == 0) return cudaMemsetAsync(tot, 0, 8, st);
+    k_ref_count<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, cnt);
+    k_ref_scan<<<1, 1024, 0, st>>>(cnt, (uint32_t)tiles, tot);
+    k_ref_scatter<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, pos, cnt, pos_next, seg_next, run_off);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
+                             const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
+                             uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
+                             int sms, cudaStream_t st) {
+    if (nseg == 0) return cudaSuccess;
+    k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn, perm,
+                                                            dbit, dacc, done);
+    k_ref_keep<<<grid_of(nn, sms), kRefThreads, 0, st>>>(seg, run_off, done, nn, keep);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, int qhi, int qlo, const uint32_t* pos,
+                              const uint32_t* seg, const uint32_t* perm, uint64_t nr, uint32_t* out, uint64_t opitch,
+                              uint32_t* orid, int sms, cudaStream_t st) {
+    if (nr == 0) return cudaSuccess;
+    k_ref_gather<<<grid_of(nr, sms), kRefThreads, 0, st>>>(pm, pitch, qhi, qlo, pos, seg, perm, nr, out, opitch, orid);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_put(uint32_t* perm, const uint32_t* pos, const uint32_t* rid, uint64_t nr, int sms,
+                           cudaStream_t st) {
+    if (nr == 0) return cudaSuccess;
+    k_ref_put<<<grid_of(nr, sms), kRefThreads, 0, st>>>(perm, pos, rid, nr);
+    return cudaGetLastError();
+}
+
+}  // namespace cks
