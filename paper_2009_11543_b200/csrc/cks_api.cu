@@ -399,17 +399,27 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     uint32_t* dacc = as<uint32_t>(ctx->dacc);
     uint8_t* tie = as<uint8_t>(ctx->tie);
 
-    // round 0: every key by chunk 0
-    const uint32_t np0 = np >= 2 ? 2 : 1;
+    // round 0: every key by chunk 0. With three planes the third is carried through the
+    // round-0 passes (4 more bytes per key per pass), which is cheaper than gathering the key
+    // rows again at the end: P_M then comes out in sorted order (and stays so: the rounds
+    // that reorder runs move its planes too).
+    const bool carry = np == 3;
+    const uint32_t np0 = carry ? 3 : (np >= 2 ? 2 : 1);
+    const uint32_t dig0 = carry ? 4 : (np <= 2 ? lead / 8 : 0);
     const uint32_t* sorted0 = nullptr;
     uint64_t sp0 = sp;
-    TRY(run_sort(ctx, pm + (uint64_t)(np - np0) * sp, sp, np0, 4 * np0, n, nullptr, 0, nullptr, 0, out->perm,
-                 &sorted0, &sp0, np <= 2 ? lead / 8 : 0));
-    LAUNCH(launch_ref_adj(np0 == 2 ? sorted0 : nullptr, sorted0 + (uint64_t)(np0 - 1) * sp0, nullptr, nullptr, n, 0,
-                          moff, m, B, dbit, tie, dacc, true, ctx->sms, ctx->stream));
+    uint32_t* carried = nullptr;
+    if (carry) {
+        TRY(ensure(ctx, ctx->pd, (size_t)np * sp * 4));
+        carried = as<uint32_t>(ctx->pd);
+    }
+    TRY(run_sort(ctx, pm + (uint64_t)(np - np0) * sp, sp, np0, 4 * np0, n, nullptr, 0, carried, sp, out->perm,
+                 &sorted0, &sp0, dig0));
+    LAUNCH(launch_ref_adj(np0 >= 2 ? sorted0 + (uint64_t)(np0 - 2) * sp0 : nullptr, sorted0 + (uint64_t)(np0 - 1) * sp0,
+                          nullptr, nullptr, n, 0, moff, m, B, dbit, tie, dacc, true, ctx->sms, ctx->stream));
     out->rounds = 1;
     out->refined_keys = 0;
-    out->passes = 4 * np0 - (np <= 2 ? lead / 8 : 0);
+    out->passes = 4 * np0 - dig0;
     // rounds 1..: the tied runs. Short runs (and runs of equal keys) are finished in place by
     // comparing their remaining bits; the others are re-sorted by (run, chunk r).
     uint64_t nr = n;
@@ -452,7 +462,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         // (2) finish short runs and runs of equal keys in place
         const int qtop = (int)np - 1 - 2 * (int)r;
         LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, posA_, segA_, as<uint32_t>(ctx->runoff), nseg, nn, out->perm,
-                                dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), ctx->sms, ctx->stream));
+                                dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B, ctx->sms,
+                                ctx->stream));
         // (3) the runs left for an LSD round
         LAUNCH(launch_ref_compact(as<uint8_t>(ctx->keep), nn, posA_, as<uint32_t>(ctx->rcnt), as<uint32_t>(ctx->rtot),
                                   posB_, segB_, nullptr, ctx->stream));
@@ -482,7 +493,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         out->passes += 8 + (segbits + 7) / 8 - d0;
         TRY(run_sort(ctx, as<uint32_t>(ctx->cmp), cp, 3, 8 + (segbits + 7) / 8, n2, as<uint32_t>(ctx->crid), 0,
                      nullptr, 0, as<uint32_t>(ctx->crid2), &sv, &svp, d0));
-        LAUNCH(launch_ref_put(out->perm, posB_, as<uint32_t>(ctx->crid2), n2, ctx->sms, ctx->stream));
+        LAUNCH(launch_ref_put(out->perm, posB_, as<uint32_t>(ctx->crid2), n2, pm, sp, np, carried, ctx->sms,
+                              ctx->stream));
         LAUNCH(launch_ref_adj(qlo >= 0 ? sv : nullptr, sv + svp, sv + 2 * svp, posB_, n2, 64 * r, moff, m, B, dbit,
                               tie, dacc, false, ctx->sms, ctx->stream));
         pos = posB_;
@@ -502,12 +514,12 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     out->packed = nullptr;
     out->packed_pitch = sp;
     if (out->popcount > 0) {
-        TRY(ensure(ctx, ctx->pd, (size_t)npd * sp * 4));
-        uint32_t* pd = as<uint32_t>(ctx->pd);
-        if (nch == 1 && lead == 0 && same_mask(out->mask, M, B)) {
+        if (!carry) TRY(ensure(ctx, ctx->pd, (size_t)npd * sp * 4));
+        uint32_t* pd = carry ? pm : as<uint32_t>(ctx->pd);       // (P_M in row order is no longer needed)
+        if ((nch == 1 || carry) && lead == 0 && same_mask(out->mask, M, B)) {
             out->packed = sorted0;
             out->packed_pitch = sp0;
-        } else if (nch == 1) {
+        } else if (nch == 1 || carry) {
             std::vector<uint32_t> sub(np, 0);
             repack_words(M, out->mask, B, m, lead, sub);
             TRY(claim_slot(ctx, 1));
@@ -610,10 +622,9 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
         const char* e = getenv("CKS_REFINE");
         ctx->refine = e ? atoi(e) : 1;
     }
-    // 1 = auto: by prefixes when P_M spans more than two 64-bit chunks (m > 128); below that
-    // the first chunk already covers most of P_M and the single sort carrying all planes is
-    // cheaper than the refinement rounds plus the final gather of P_D
-    if (n && m && (ctx->refine == 2 || (ctx->refine == 1 && m > 128))) {
+    // 1 = auto: by prefixes whenever P_M is wider than one 64-bit chunk (m > 64); for m <= 64
+    // round 0 would be the whole sort anyway
+    if (n && m && (ctx->refine == 2 || (ctx->refine == 1 && m > 64))) {
         TRY(build_refine(ctx, keys, n, B, M, m, out, dbit));
         out->height = 0;
         if (out->tree.node_cnt) {

@@ -396,14 +396,17 @@ k_downsweep(const LsdPassArgs a) {
 // Three roles in one persistent CTA per SM, pipelined across the CTA's tiles:
 //   producer warp  issues the 1-D TMA bulk loads of every stream of every tile, in order,
 //                  into a ring of R slots (waits on the slot's `empty` barrier);
-//   ranker warps   (8) rank tile j's digit word and publish the tile permutation
-//                  s_src[j&1] and global bases s_gb[j&1] (barrier `ranked[j&1]`);
+//   ranker warps   (16, 8 keys per lane) rank tile j's digit word and publish the tile
+//                  permutation s_src[j&1] and global bases s_gb[j&1] (barrier `ranked[j&1]`);
 //   writer warps   (8) gather every stream of tile j in digit order and store it in
 //                  coalesced runs, releasing each slot (`empty`) as they go.
 // So while the writers move tile j the rankers already work on tile j+1 and the producer
 // keeps the next loads in flight: the store stream never waits for a ranking phase.
-constexpr int kWsWarps = 17;                     // 8 rankers + 8 writers + 1 producer
+constexpr int kRW = 16;                          // ranker warps: ranking is latency-bound, so
+constexpr int kWW = 8;                           // it gets twice the warps of the writers
+constexpr int kWsWarps = kRW + kWW + 1;          // + 1 producer
 constexpr int kWsThreads = kWsWarps * 32;
+constexpr int kRT = kRW * 32;                    // ranker threads
 constexpr uint32_t kDigitSlots = 3;              // digit-word ring (ranked one tile ahead)
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
@@ -415,8 +418,8 @@ __device__ __forceinline__ void bar_init_n(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void bar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
-// exclusive scan over the 256 ranker threads (named barrier 1)
-__device__ __forceinline__ uint32_t scan256_rankers(uint32_t v, uint32_t* s_warp, uint32_t rt) {
+// exclusive scan over the kRT ranker threads (named barrier 1)
+__device__ __forceinline__ uint32_t scan_rankers(uint32_t v, uint32_t* s_warp, uint32_t rt) {
     const uint32_t lane = rt & 31, warp = rt >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -425,19 +428,19 @@ __device__ __forceinline__ uint32_t scan256_rankers(uint32_t v, uint32_t* s_warp
         if (lane >= (uint32_t)o) x += y;
     }
     if (lane == 31) s_warp[warp] = x;
-    named_sync(1, 256);
+    named_sync(1, kRT);
     if (warp == 0) {
-        uint32_t t = lane < (uint32_t)kW ? s_warp[lane] : 0;
+        uint32_t t = lane < (uint32_t)kRW ? s_warp[lane] : 0;
 #pragma unroll
-        for (int o = 1; o < kW; o <<= 1) {
+        for (int o = 1; o < kRW; o <<= 1) {
             uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
             if (lane >= (uint32_t)o) t += y;
         }
-        if (lane < (uint32_t)kW) s_warp[lane] = t;
+        if (lane < (uint32_t)kRW) s_warp[lane] = t;
     }
-    named_sync(1, 256);
+    named_sync(1, kRT);
     uint32_t r = (warp ? s_warp[warp - 1] : 0) + x - v;
-    named_sync(1, 256);
+    named_sync(1, kRT);
     return r;
 }
 
@@ -448,10 +451,10 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
     constexpr int HW = kRadix + 8;
     extern __shared__ __align__(128) uint8_t s_dyn[];
     uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                                   // [R][TILE]
-    uint32_t* s_hist = ring + (size_t)(kDigitSlots + a.slots) * TILE;                     // [kW][HW]
-    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_hist + kW * HW);                      // [2][TILE]
+    uint32_t* s_hist = ring + (size_t)(kDigitSlots + a.slots) * TILE;                     // [kRW][HW]
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_hist + kRW * HW);                     // [2][TILE]
     __shared__ uint32_t s_gb[2][kRadix];
-    __shared__ uint32_t s_warp[kW];
+    __shared__ uint32_t s_warp[kRW];
     __shared__ __align__(8) uint64_t s_full[kDigitSlots + 16];
     __shared__ __align__(8) uint64_t s_empty[kDigitSlots + 16];
     __shared__ __align__(8) uint64_t s_ranked[2];
@@ -477,13 +480,13 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
     };
 
     if (tid == 0) {
-        for (uint32_t s = 0; s < kDigitSlots + R; s++) { bar_init_n(&s_full[s], 1); bar_init_n(&s_empty[s], kW); }
-        for (int b = 0; b < 2; b++) { bar_init_n(&s_ranked[b], kW); bar_init_n(&s_written[b], kW); }
+        for (uint32_t s = 0; s < kDigitSlots + R; s++) { bar_init_n(&s_full[s], 1); bar_init_n(&s_empty[s], kWW); }
+        for (int b = 0; b < 2; b++) { bar_init_n(&s_ranked[b], kRW); bar_init_n(&s_written[b], kWW); }
         bar_fence_init();
     }
     __syncthreads();
 
-    if (warp == 2 * kW) {
+    if (warp == kRW + kWW) {
         // ---------------- producer: digit words one tile ahead in their own 3-slot ring
         // (D0, D1, then after the data streams of tile j the digit word of tile j+2), the
         // other streams in order through the data ring
@@ -511,34 +514,36 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
         return;
     }
 
-    if (warp < kW) {
-        // ---------------- rankers: thread rt is digit rt in the per-digit phases
+    if (warp < kRW) {
+        // ---------------- rankers: thread rt < 256 is digit rt in the per-digit phases
+        constexpr int RI = TILE / kRT;                           // keys per ranker lane
         const uint32_t rt = tid;
-        const uint32_t wofs = warp * 32 * ITEMS;
+        const uint32_t wofs = warp * 32 * RI;
         const uint32_t ltm = lt_mask();
         uint32_t* h = s_hist + warp * HW;
         const uint32_t hbase = smem_addr(h);
         for (uint32_t j = 0; j < my_tiles; j++) {
             const uint32_t tile = blockIdx.x + j * G;
             const uint32_t buf = j & 1;
-            const uint32_t goff = a.chunk_tot[(uint64_t)(tile / a.chunk_tiles) * kRadix + rt] +
-                                  a.tile_off[(uint64_t)tile * kRadix + rt];
+            const uint32_t goff = rt < kRadix ? a.chunk_tot[(uint64_t)(tile / a.chunk_tiles) * kRadix + rt] +
+                                                    a.tile_off[(uint64_t)tile * kRadix + rt]
+                                              : 0u;
             const uint32_t* dslot = ring + (size_t)(j % kDigitSlots) * TILE;
 #pragma unroll
             for (int q = lane; q < HW; q += 32) h[q] = 0;
             __syncwarp();
             bar_wait(&s_full[j % kDigitSlots], (j / kDigitSlots) & 1u);
-            uint32_t dg[ITEMS], pos[ITEMS];
+            uint32_t dg[RI], pos[RI];
             {
-                uint32_t peers[ITEMS];
+                uint32_t peers[RI];
 #pragma unroll
-                for (int i = 0; i < ITEMS; i++) {
+                for (int i = 0; i < RI; i++) {
                     dg[i] = digit_of(dslot[wofs + i * 32 + lane], sel);
                     peers[i] = match_bits<8>(dg[i]);
                 }
-                uint32_t old[ITEMS];
+                uint32_t old[RI];
 #pragma unroll
-                for (int i = 0; i < ITEMS; i++) {
+                for (int i = 0; i < RI; i++) {
                     const uint32_t lower = __popc(peers[i] & ltm);
                     asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %1, 0;\n mov.u32 %0, 0;\n"
                                  " @p atom.shared.add.u32 %0, [%2], %3;\n}"
@@ -547,24 +552,29 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
                     pos[i] = lower;
                 }
 #pragma unroll
-                for (int i = 0; i < ITEMS; i++) pos[i] += __shfl_sync(0xFFFFFFFFu, old[i], __ffs(peers[i]) - 1);
+                for (int i = 0; i < RI; i++) pos[i] += __shfl_sync(0xFFFFFFFFu, old[i], __ffs(peers[i]) - 1);
             }
-            named_sync(1, 256);
+            named_sync(1, kRT);
             {
-                uint32_t c[kW], total = 0;
+                uint32_t c[kRW], total = 0;
+                if (rt < kRadix) {
 #pragma unroll
-                for (int k = 0; k < kW; k++) { c[k] = s_hist[k * HW + rt]; total += c[k]; }
-                const uint32_t excl = scan256_rankers(total, s_warp, rt);
-                uint32_t run = excl;
+                    for (int k = 0; k < kRW; k++) { c[k] = s_hist[k * HW + rt]; total += c[k]; }
+                }
+                const uint32_t excl = scan_rankers(total, s_warp, rt);
+                if (rt < kRadix) {
+                    uint32_t run = excl;
 #pragma unroll
-                for (int k = 0; k < kW; k++) { s_hist[k * HW + rt] = run; run += c[k]; }
-                if (j >= 2) bar_wait(&s_written[buf], ((j >> 1) - 1) & 1u);   // writers done with tile j-2
-                s_gb[buf][rt] = goff - excl;
+                    for (int k = 0; k < kRW; k++) { s_hist[k * HW + rt] = run; run += c[k]; }
+                    if (j >= 2) bar_wait(&s_written[buf], ((j >> 1) - 1) & 1u);   // writers done with tile j-2
+                    s_gb[buf][rt] = goff - excl;
+                }
             }
-            named_sync(1, 256);
+            named_sync(1, kRT);
             uint16_t* src = s_src + buf * TILE;
 #pragma unroll
-            for (int i = 0; i < ITEMS; i++) src[(a.debug & 2) ? wofs + i * 32 + lane : pos[i] + h[dg[i]]] = (uint16_t)((wofs + i * 32 + lane) * 4);
+            for (int i = 0; i < RI; i++)
+                src[(a.debug & 2) ? wofs + i * 32 + lane : pos[i] + h[dg[i]]] = (uint16_t)((wofs + i * 32 + lane) * 4);
             __syncwarp();
             if (lane == 0) bar_arrive(&s_ranked[buf]);
         }
@@ -572,7 +582,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
     }
 
     // ---------------- writers: thread wt owns output slots r*256 + wt
-    const uint32_t wt = tid - kSortThreads;
+    const uint32_t wt = tid - kRT;
     uint32_t y = 0;                                              // data item counter
     for (uint32_t j = 0; j < my_tiles; j++) {
         const uint32_t tile = blockIdx.x + j * G;
@@ -660,7 +670,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
     int nl = 2;
     if (g_lsd_ws && a.tma && nfull > 0) {
         // warp-specialised kernel over the full tiles, one persistent CTA per SM
-        constexpr size_t fixed = (size_t)kW * (kRadix + 8) * 4 + (size_t)2 * TILE * 2;
+        constexpr size_t fixed = (size_t)kRW * (kRadix + 8) * 4 + (size_t)2 * TILE * 2;
         const int max_slots = (int)((200u * 1024u - fixed) / ((size_t)TILE * 4));
         int R = 2 * (streams - 1);                           // data ring: the non-digit streams
         if (R > max_slots - (int)kDigitSlots) R = max_slots - (int)kDigitSlots;

@@ -197,7 +197,8 @@ k_ref_gather(const uint32_t* __restrict__ pm, uint64_t pitch, int qhi, int qlo, 
     }
 }
 
-// Finish small tied runs in place. Thread per run s of the list (members run_off[s] ..
+// Finish small tied runs in place (carried: P_M in sorted order at carried, planes of pitch
+// `pitch`; only used when the remaining bits are its plane 0). Thread per run s of the list (members run_off[s] ..
 // run_off[s+1]-1 at the contiguous global positions pos[run_off[s]] + j): a run of at most
 // kLocal keys is sorted by its remaining P_M bits (planes qtop .. 0; the earlier chunks tie)
 // with the row id as tie-break -- the stable order -- and its D_i are taken from the first
@@ -210,8 +211,15 @@ __global__ void __launch_bounds__(kRefThreads)
 k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* __restrict__ moff,
             const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
             uint32_t* __restrict__ perm, uint16_t* __restrict__ dbit, uint32_t* __restrict__ dacc,
-            uint8_t* __restrict__ done) {
-    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += (uint64_t)gridDim.x * blockDim.x) {
+            uint8_t* __restrict__ done, uint32_t* __restrict__ carried, uint32_t nwords) {
+    __shared__ uint32_t s_bm[kMaxBits / 32];                         // D bits found by this block
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
+    __syncthreads();
+    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t sweeps = (nseg + nthreads - 1) / nthreads;       // uniform trip count (block barrier below)
+    for (uint64_t it = 0; it < sweeps; it++) {
+        const uint64_t s = it * nthreads + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (s >= nseg) continue;
         const uint32_t k0 = run_off[s];
         const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
         const uint32_t L = k1 - k0;
@@ -227,7 +235,32 @@ k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qt
             }
             return 0;
         };
-        if (L <= kLocal) {
+        if (carried && L <= kLocal) {
+            // P_M is carried in sorted order and the remainder is its plane 0 (qtop == 0): sort the
+            // run's (plane-0 word, row id) pairs read at its contiguous positions, no row gathers
+            uint32_t rows[kLocal], w[kLocal];
+            for (uint32_t j = 0; j < L; j++) { rows[j] = perm[p0 + j]; w[j] = carried[p0 + j]; }
+            for (uint32_t j = 1; j < L; j++) {
+                const uint32_t x = rows[j], y = w[j];
+                uint32_t i = j;
+                while (i > 0 && (w[i - 1] > y || (w[i - 1] == y && rows[i - 1] > x))) {
+                    rows[i] = rows[i - 1];
+                    w[i] = w[i - 1];
+                    i--;
+                }
+                rows[i] = x;
+                w[i] = y;
+            }
+            for (uint32_t j = 0; j < L; j++) {
+                perm[p0 + j] = rows[j];
+                carried[p0 + j] = w[j];
+                if (j == 0 || w[j] == w[j - 1]) continue;
+                const uint32_t d = moff[32u * (np - 1) + (uint32_t)__clz(w[j] ^ w[j - 1])];
+                dbit[p0 + j] = (uint16_t)d;
+                const uint32_t b = 0x80000000u >> (d & 31);
+                if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
+            }
+        } else if (L <= kLocal) {
             uint32_t rows[kLocal];
 #pragma unroll
             for (uint32_t j = 0; j < kLocal; j++) rows[j] = j < L ? perm[p0 + j] : 0u;
@@ -249,7 +282,8 @@ k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qt
                 if (cmp(rows[j - 1], rows[j], &tt) != 0) {
                     const uint32_t d = moff[tt];
                     dbit[p0 + j] = (uint16_t)d;
-                    atomicOr(&dacc[d >> 5], 0x80000000u >> (d & 31));
+                    const uint32_t b = 0x80000000u >> (d & 31);
+                    if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
                 }
             }
         } else {
@@ -262,6 +296,9 @@ k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qt
         }
         done[s] = 1;
     }
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
+        if (s_bm[w]) atomicOr(&dacc[w], s_bm[w]);
 }
 
 // keep[k] = 1 for the members of unfinished runs except each run's first (the tie convention
@@ -275,10 +312,17 @@ k_ref_keep(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ run_of
     }
 }
 
+// sorted row ids back to their run's positions (and, when P_M is carried in sorted order,
+// its planes for those rows)
 __global__ void __launch_bounds__(kRefThreads)
-k_ref_put(uint32_t* __restrict__ perm, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ rid, uint64_t nr) {
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += (uint64_t)gridDim.x * blockDim.x)
-        perm[pos[k]] = rid[k];
+k_ref_put(uint32_t* __restrict__ perm, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ rid, uint64_t nr,
+          const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, uint32_t* __restrict__ carried) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = pos[k], r = rid[k];
+        perm[p] = r;
+        if (carried)
+            for (uint32_t q = 0; q < np; q++) carried[(uint64_t)q * pitch + p] = __ldg(pm + (uint64_t)q * pitch + r);
+    }
 }
 
 // ---- launchers --------------------------------------------------------------------------------
@@ -316,10 +360,11 @@ cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* 
 cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
                              const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
-                             int sms, cudaStream_t st) {
+                             uint32_t* carried, uint32_t B, int sms, cudaStream_t st) {
     if (nseg == 0) return cudaSuccess;
+    const uint32_t nwords = (8 * B + 31) / 32;
     k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn, perm,
-                                                            dbit, dacc, done);
+                                                            dbit, dacc, done, carried, nwords);
     k_ref_keep<<<grid_of(nn, sms), kRefThreads, 0, st>>>(seg, run_off, done, nn, keep);
     return cudaGetLastError();
 }
@@ -332,10 +377,10 @@ cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, int qhi, int q
     return cudaGetLastError();
 }
 
-cudaError_t launch_ref_put(uint32_t* perm, const uint32_t* pos, const uint32_t* rid, uint64_t nr, int sms,
-                           cudaStream_t st) {
+cudaError_t launch_ref_put(uint32_t* perm, const uint32_t* pos, const uint32_t* rid, uint64_t nr, const uint32_t* pm,
+                           uint64_t pitch, uint32_t np, uint32_t* carried, int sms, cudaStream_t st) {
     if (nr == 0) return cudaSuccess;
-    k_ref_put<<<grid_of(nr, sms), kRefThreads, 0, st>>>(perm, pos, rid, nr);
+    k_ref_put<<<grid_of(nr, sms), kRefThreads, 0, st>>>(perm, pos, rid, nr, pm, pitch, np, carried);
     return cudaGetLastError();
 }
 

@@ -5,7 +5,7 @@ h = next(i for i, r in enumerate(rows) if 'Kernel Name' in r)
 hdr = rows[h]; body = rows[h + 1:]
 ik, iv, iid = hdr.index('Kernel Name'), hdr.index('Metric Value'), hdr.index('ID')
 seq = [(int(r[iid]), r[ik], float(r[iv].replace(',', ''))) for r in body if len(r) == len(hdr)]
-steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+
 # split at occupancy kernel launches (first kernel of a build)
 starts = [i for i, (_, k, _) in enumerate(seq) if 'k_occupancy' in k]
 last = seq[starts[-1]:] if starts else seq
