@@ -38,23 +38,14 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def algorithmic_bytes(n: int, B: int, m: int, d: int, fanout_per: int, with_tree: bool = True):
-    """SURVEY 8(d) per-key bytes: B (a1) + (B+W) (a3) + W (a4 hist read) + k*2*(W+4) - 4 (a5)
-    + W (a6) + [W + W_D if repack] (a7) + 12 (a8: read perm+dbit, write rid+dbit)."""
+def formula_bytes(B: int, m: int):
+    """SURVEY 8(d) roofline bytes per key of mask + compress + k radix passes, for a full-width
+    LSD sort on the superset width m: B (a1) + (B + W) (a3) + k*2*(W+4) - 4 (a5) + W (a6),
+    W = 4*ceil(m/32), k = ceil(m/8). The build sorts by distinguishing prefixes (NEXT-1) and
+    moves fewer bytes than this; the formula is the contract's yardstick."""
     W = 4 * ((m + 31) // 32)
-    WD = 4 * ((d + 31) // 32)
     k = (m + 7) // 8
-    per_key = {
-        "a1_mask": B,
-        "a3_compress": B + W,
-        "a4_hist": W,
-        "a5_passes": (k * 2 * (W + 4) - 4) if k else 0,
-        "a6_adjacent": W,
-        "a7_repack": (W + WD) if d != m and d else 0,
-        "a8_bulkload": 12 if with_tree else 0,
-    }
-    pass_bytes = (2 * (W + 4) * n * k - 4 * n) / k if k else 0.0      # average per onesweep launch
-    return per_key, pass_bytes
+    return {"a1_mask": B, "a3_compress": B + W, "a5_passes": (k * 2 * (W + 4) - 4) if k else 0, "a6_adjacent": W}
 
 
 class ClockSampler:
@@ -132,14 +123,16 @@ def max_over_ranks(x: float, world: int, device) -> float:
 
 
 def traffic_from_profiles(cfg_name: str):
+    """ncu --set full dram__bytes_read+write of one profiled launch of the dominant kernel
+    (profiles/ncu_traffic.json), with that launch's algorithmic bytes for comparison."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
         e = d.get(cfg_name)
         if e:
-            return float(e["dram_bytes_per_launch"]), e.get("source")
-    return None, None
+            return float(e["dram_bytes_per_launch"]), e.get("source"), e.get("algorithmic_bytes_per_launch")
+    return None, None, None
 
 
 # ------------------------------------------------------------------------------------------
@@ -246,10 +239,13 @@ def main():
         builder(keys)
     torch.cuda.synchronize(device)
     m, d, passes = int(builder.out.sort_bits), int(builder.out.popcount), int(builder.out.passes)
+    rounds, refined = int(builder.out.rounds), int(builder.out.refined_keys)
 
-    # ---- timed region: K fused builds, inputs resident in HBM (1.6 GB > 126 MB L2)
+    # ---- timed region: K fused builds, inputs resident in HBM (keys > 126 MB L2 for cfg2-5)
     cks.set_timing(True)
     stage_acc = None
+    k_ms = k_bytes = 0.0
+    k_count = 0
     launches0 = cks.launches()
     barrier(world)
     torch.cuda.synchronize(device)
@@ -260,6 +256,10 @@ def main():
         builder(keys)
         st = cks.stage_ms()                                  # events on the library's stream
         stage_acc = st if stage_acc is None else [a + b for a, b in zip(stage_acc, st)]
+        kms, kby, kc = cks.kernel_stats()                    # the dominant kernel's own events
+        k_ms += kms
+        k_bytes += kby
+        k_count += kc
     ev1.record(stream)
     torch.cuda.synchronize(device)
     clk = clocks.stop()
@@ -269,17 +269,19 @@ def main():
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_max = max_over_ranks(ms, world, device)
     stages = [s / args.steps for s in stage_acc]
-    names = ["a1_mask", "a3_compress", "a4_hist", "a5_passes", "a6_adjacent", "a7_repack", "a8_bulkload", "total"]
+    names = ["a1_mask", "a3_compress", "a4_sort_setup", "a5_sort", "a6_exact_D", "a7_packed_D", "a8_bulkload",
+             "total"]
     stages_ms = dict(zip(names, [round(s, 4) for s in stages]))
 
-    # ---- roofline of the dominant kernel (the onesweep LSD pass)
+    # ---- roofline of the dominant kernel: the warp-specialised LSD downsweep (one launch per
+    # digit pass), algorithmic bytes = every stream of the pass read once and written once
     peak, peak_src = measured_peaks()
-    per_key, pass_bytes = algorithmic_bytes(n, B, m, d, 64)
-    pass_ms = stages_ms["a5_passes"] / passes if passes else None
-    achieved = pass_bytes / (pass_ms * 1e-3) / 1e9 if pass_ms else None
-    traffic, traffic_src = traffic_from_profiles(c["name"])
-    path_bytes = sum(per_key.values()) * n
-    path_gbs = path_bytes / (ms * 1e-3) / 1e9
+    achieved = (k_bytes / (k_ms * 1e-3) / 1e9) if k_ms > 0 else None
+    traffic, traffic_src, traffic_alg = traffic_from_profiles(c["name"])
+    fbytes = formula_bytes(B, m)
+    path_bytes = sum(fbytes.values()) * n
+    core_ms = sum(stages[i] for i in range(0, 5))            # mask .. exact D (no packed-D, no tree)
+    path_gbs = path_bytes / (core_ms * 1e-3) / 1e9
 
     # ---- e2e: same call with HOST buffers (H2D keys + D2H perm inside the timed region)
     e2e = None
@@ -309,15 +311,21 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": c["name"], "n": n, "key_bytes": B, "fanout": 64, "fill": 1.0,
                        "superset": "byteocc D+", "sort_bits": m, "d_bits": d, "lsd_passes": passes,
+                       "refine_rounds": rounds, "refined_keys": refined,
+                       "sort": "by distinguishing prefixes (NEXT-1)" if rounds else "single LSD sort",
                        "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (keys 1.6 GB vs 126 MB), no flush"},
+                       "l2": f"inputs larger than L2 (keys {n * B / 1e6:.0f} MB vs 126 MB), no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_onesweep (one LSD digit pass)", "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": pass_bytes, "avg_launch_ms": pass_ms,
-                         "traffic_source": traffic_src},
-            "path_roofline": {"algorithmic_bytes_per_key": per_key, "achieved_gbs": path_gbs,
-                              "frac_of_peak": path_gbs / peak, "frac_of_8tbs": path_gbs / 8000.0},
+                         "kernel": "k_downsweep_ws (warp-specialised LSD digit pass)", "peak_source": peak_src,
+                         "launches_per_step": k_count / args.steps if args.steps else None,
+                         "kernel_ms_per_step": k_ms / args.steps if args.steps else None,
+                         "algorithmic_bytes_per_launch": (k_bytes / k_count) if k_count else None,
+                         "traffic_source": traffic_src, "traffic_launch_algorithmic_bytes": traffic_alg},
+            "path_roofline": {"formula": "SURVEY 8(d): mask + compress + k full-width LSD passes + adjacency",
+                              "formula_bytes_per_key": fbytes, "mask_to_exact_D_ms": core_ms,
+                              "achieved_gbs": path_gbs, "frac_of_peak": path_gbs / peak,
+                              "frac_of_8tbs": path_gbs / 8000.0},
             "stages_ms": stages_ms,
             "cpu_baseline": cpu,
             "e2e": e2e,

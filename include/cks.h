@@ -80,6 +80,11 @@ int cks_ctx_set_timing(cks_ctx* ctx, int enable);
 int cks_ctx_stage_ms(cks_ctx* ctx, float* out, int max);
 /* Number of kernels libcks launched since the context was created. */
 uint64_t cks_ctx_launches(const cks_ctx* ctx);
+/* Dominant kernel of the last timed cks_build (the warp-specialised LSD downsweep, one
+ * launch per digit pass): summed CUDA-event time in ms on the context's stream, summed
+ * algorithmic bytes (every stream of the pass read once and written once) and the number
+ * of launches. Synchronises. Zeros when timing was off. */
+int cks_ctx_kernel_stats(cks_ctx* ctx, double* ms, double* bytes, uint32_t* count);
 const char* cks_strerror(int code);
 const char* cks_last_error(const cks_ctx* ctx);
 

@@ -56,7 +56,7 @@ class BuildOut(ctypes.Structure):
 
 
 EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing",
-           "cks_ctx_stage_ms", "cks_ctx_launches", "cks_strerror", "cks_last_error",
+           "cks_ctx_stage_ms", "cks_ctx_launches", "cks_ctx_kernel_stats", "cks_strerror", "cks_last_error",
            "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
            "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_build", "cks_build_host"]
 
@@ -78,6 +78,8 @@ def load_library(path: str | None = None):
     L.cks_ctx_stage_ms.argtypes = [p, ctypes.POINTER(f32), i32]
     L.cks_ctx_launches.argtypes = [p]
     L.cks_ctx_launches.restype = u64
+    L.cks_ctx_kernel_stats.argtypes = [p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(u32)]
     L.cks_strerror.argtypes = [i32]
     L.cks_strerror.restype = ctypes.c_char_p
     L.cks_last_error.argtypes = [p]
@@ -160,6 +162,14 @@ def stage_ms() -> list[float]:
     buf = (ctypes.c_float * 8)()
     k = L.cks_ctx_stage_ms(c, buf, 8)
     return [float(buf[i]) for i in range(k)]
+
+
+def kernel_stats() -> tuple[float, float, int]:
+    """(ms, algorithmic bytes, launches) of the dominant kernel in the last timed build."""
+    L, c = _context()
+    ms, by, cnt = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint32()
+    _check(L, c, L.cks_ctx_kernel_stats(c, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(cnt)))
+    return float(ms.value), float(by.value), int(cnt.value)
 
 
 def superset_mask(keys: torch.Tensor, kind: int = SUPERSET_BYTEOCC) -> np.ndarray:

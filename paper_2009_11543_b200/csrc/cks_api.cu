@@ -33,6 +33,12 @@ struct cks_ctx {
     cudaStream_t copy_stream = nullptr;
     cudaStream_t aux_stream = nullptr;   // partial tail tile of an LSD pass
     cudaEvent_t aux_ev[2] = {};
+    // dominant-kernel timing (cks_ctx_kernel_stats): event pairs around each warp-specialised
+    // downsweep of the last timed build, and their algorithmic bytes
+    static constexpr int kMaxKev = 128;
+    cudaEvent_t kev[2 * kMaxKev] = {};
+    double kbytes[kMaxKev] = {};
+    int nkev = 0;
     char err[512] = {0};
     uint64_t launches = 0;
     uint32_t epoch = 1;
@@ -194,7 +200,7 @@ uint32_t* first_pass_out(cks_ctx* ctx, uint32_t P) {
 int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_t np, uint32_t key_passes,
              uint64_t n, const uint32_t* in_rid, uint32_t rid_passes, uint32_t* final_planes,
              uint64_t final_pitch, uint32_t* final_rid, const uint32_t** sorted_view, uint64_t* sorted_pitch,
-             uint32_t digit0 = 0) {
+             uint32_t digit0 = 0, bool mark_stages = true) {
     if (digit0 > key_passes) digit0 = key_passes;
     const uint32_t Pfull = key_passes + (in_rid ? rid_passes : 0);
     const uint32_t P = Pfull - digit0;
@@ -245,7 +251,7 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
         ctx->launches += (uint64_t)hl;
         LAUNCH(launch_scan(as<uint32_t>(ctx->hist), Pfull, as<uint32_t>(ctx->base), ctx->stream));
     }
-    mark(ctx, ST_HIST);
+    if (mark_stages) mark(ctx, ST_HIST);
 
     const uint32_t* cur_p = in_planes;
     uint64_t cur_pitch = in_pitch;
@@ -298,7 +304,15 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
             aux.stream = ctx->aux_stream;
             aux.fork = ctx->aux_ev[0];
             aux.join = ctx->aux_ev[1];
+            const int ke = ctx->nkev;
+            if (ctx->timing && ke < cks_ctx::kMaxKev) {
+                aux.ws_begin = ctx->kev[2 * ke];
+                aux.ws_end = ctx->kev[2 * ke + 1];
+                ctx->kbytes[ke] = 0.0;
+                aux.ws_bytes = &ctx->kbytes[ke];
+            }
             CK(launch_lsd_pass(la, ctx->sms, ctx->stream, aux, &nl));
+            if (aux.ws_bytes && ctx->kbytes[ke] > 0.0) ctx->nkev++;
             ctx->launches += (uint64_t)nl;
             cur_p = out_p;
             cur_pitch = out_pitch;
@@ -414,7 +428,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         carried = as<uint32_t>(ctx->pd);
     }
     TRY(run_sort(ctx, pm + (uint64_t)(np - np0) * sp, sp, np0, 4 * np0, n, nullptr, 0, carried, sp, out->perm,
-                 &sorted0, &sp0, dig0));
+                 &sorted0, &sp0, dig0, false));
     LAUNCH(launch_ref_adj(np0 >= 2 ? sorted0 + (uint64_t)(np0 - 2) * sp0 : nullptr, sorted0 + (uint64_t)(np0 - 1) * sp0,
                           nullptr, nullptr, n, 0, moff, m, B, dbit, tie, dacc, true, ctx->sms, ctx->stream));
     out->rounds = 1;
@@ -492,7 +506,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         uint64_t svp = cp;
         out->passes += 8 + (segbits + 7) / 8 - d0;
         TRY(run_sort(ctx, as<uint32_t>(ctx->cmp), cp, 3, 8 + (segbits + 7) / 8, n2, as<uint32_t>(ctx->crid), 0,
-                     nullptr, 0, as<uint32_t>(ctx->crid2), &sv, &svp, d0));
+                     nullptr, 0, as<uint32_t>(ctx->crid2), &sv, &svp, d0, false));
         LAUNCH(launch_ref_put(out->perm, posB_, as<uint32_t>(ctx->crid2), n2, pm, sp, np, carried, ctx->sms,
                               ctx->stream));
         LAUNCH(launch_ref_adj(qlo >= 0 ? sv : nullptr, sv + svp, sv + 2 * svp, posB_, n2, 64 * r, moff, m, B, dbit,
@@ -722,6 +736,7 @@ int cks_ctx_create(int device, void* stream, cks_ctx** out) {
     bool ok = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
     if (ok) ok = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; i < 2 && ok; i++) ok = cudaEventCreateWithFlags(&ctx->aux_ev[i], cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < 2 * cks_ctx::kMaxKev && ok; i++) ok = cudaEventCreate(&ctx->kev[i]) == cudaSuccess;
     for (int i = 0; i < ST_N && ok; i++) ok = cudaEventCreate(&ctx->ev[i]) == cudaSuccess;
     for (int i = 0; i < 3 && ok; i++) ok = cudaEventCreateWithFlags(&ctx->plan_ev[i], cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < 2 && ok; i++) ok = cudaMallocHost(&ctx->h_plan[i], sizeof(GatherPlan)) == cudaSuccess;
@@ -764,6 +779,8 @@ int cks_ctx_destroy(cks_ctx* ctx) {
     if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
     for (int i = 0; i < 2; i++)
         if (ctx->aux_ev[i]) cudaEventDestroy(ctx->aux_ev[i]);
+    for (int i = 0; i < 2 * cks_ctx::kMaxKev; i++)
+        if (ctx->kev[i]) cudaEventDestroy(ctx->kev[i]);
     delete ctx;
     return CKS_OK;
 }
@@ -804,6 +821,23 @@ int cks_ctx_stage_ms(cks_ctx* ctx, float* out, int max) {
 }
 
 uint64_t cks_ctx_launches(const cks_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cks_ctx_kernel_stats(cks_ctx* ctx, double* ms, double* bytes, uint32_t* count) {
+    if (!ctx || !ms || !bytes || !count) return CKS_EINVAL;
+    *ms = 0.0;
+    *bytes = 0.0;
+    *count = 0;
+    if (!ctx->timed) return CKS_OK;
+    for (int i = 0; i < ctx->nkev; i++) {
+        CK(cudaEventSynchronize(ctx->kev[2 * i + 1]));
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, ctx->kev[2 * i], ctx->kev[2 * i + 1]));
+        *ms += t;
+        *bytes += ctx->kbytes[i];
+    }
+    *count = (uint32_t)ctx->nkev;
+    return CKS_OK;
+}
 
 const char* cks_strerror(int code) {
     switch (code) {
@@ -903,6 +937,7 @@ int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const u
     if (!out || !out->mask || (n && !out->perm)) return fail(ctx, CKS_EINVAL, "NULL output");
     CK(cudaSetDevice(ctx->device));
     ctx->timed = ctx->timing;
+    ctx->nkev = 0;
     mark(ctx, ST_BEGIN);
     return build_common(ctx, keys, n, B, prior, out, true);
 }
@@ -914,6 +949,7 @@ int cks_build_host(cks_ctx* ctx, const uint8_t* host_keys, uint64_t n, uint32_t 
     if (out->dbit || out->tree.node_cnt) return fail(ctx, CKS_EINVAL, "cks_build_host: dbit/tree must be NULL");
     CK(cudaSetDevice(ctx->device));
     ctx->timed = ctx->timing;
+    ctx->nkev = 0;
     mark(ctx, ST_BEGIN);
     const size_t bytes = (size_t)n * B;
     TRY(ensure(ctx, ctx->keys, bytes));

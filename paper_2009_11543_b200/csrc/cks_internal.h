@@ -109,6 +109,10 @@ struct LsdPassArgs {
 struct LsdAux {
     cudaStream_t stream = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    // timing of the dominant kernel (the warp-specialised downsweep): events recorded around
+    // it when non-null; *ws_bytes receives its algorithmic bytes (0 if it did not run)
+    cudaEvent_t ws_begin = nullptr, ws_end = nullptr;
+    double* ws_bytes = nullptr;
 };
 cudaError_t launch_lsd_pass(const LsdPassArgs& a, int sms, cudaStream_t st, const LsdAux& aux, int* launches);
 void lsd_sizes(uint64_t n, uint64_t* tiles, uint64_t* chunks);

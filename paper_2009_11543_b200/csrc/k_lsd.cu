@@ -704,7 +704,11 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
             cudaEventRecord(aux.join, aux.stream);
             nl++;
         }
+        if (aux.ws_begin) cudaEventRecord(aux.ws_begin, st);
         k_downsweep_ws<ITEMS><<<(unsigned)grid, kWsThreads, smem, st>>>(w, (uint32_t)nfull);
+        if (aux.ws_end) cudaEventRecord(aux.ws_end, st);
+        // algorithmic bytes: every loaded stream read once, every stream written once
+        if (aux.ws_bytes) *aux.ws_bytes = (double)nfull * TILE * 4.0 * (double)(streams + (int)a.nplanes + 1);
         nl++;
         if (tail && aux.stream) cudaStreamWaitEvent(st, aux.join, 0);
         if (!tail || aux.stream) { *launches = nl; return cudaGetLastError(); }

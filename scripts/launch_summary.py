@@ -15,8 +15,8 @@ for _, k, v in last:
     name = k.split('(')[0].replace('void ', '')[:48]
     a = agg.setdefault(name, [0, 0.0])
     a[0] += 1; a[1] += v
-print(f"last build: {len(last)} launches, {tot/1e3:.3f} ms (ncu serialised)")
+print(f"last build: {len(last)} launches, {tot/1e3:.1f} us (ncu serialised)")
 for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
-    print(f"  {k:50s} n={c:4d} {v/1e3:8.3f} ms  {v/tot*100:5.1f}%")
+    print(f"  {k:50s} n={c:4d} {v/1e3:9.1f} us  {v/tot*100:5.1f}%")
 if '-v' in sys.argv:
-    for _, k, v in last: print(f"    {k.split('(')[0][:60]:60s} {v/1e3:8.4f}")
+    for _, k, v in last: print(f"    {k.split('(')[0][:60]:60s} {v/1e3:9.2f} us")

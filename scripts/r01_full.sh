@@ -1,11 +1,10 @@
 # Round-1 GPU evidence: gpu tests, one bench line, launch list (ncu time only), one full capture.
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"
-tail -3 gpurun_out/pytest_gpu.log
+tail -1 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc $?"
 tail -1 gpurun_out/bench.json
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu1 rc $?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${K:-k_downsweep}" -s ${S:-20} -c 1 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc $?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${K:-k_downsweep_ws}" -s ${S:-20} -c 1 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc $?"
 echo done
