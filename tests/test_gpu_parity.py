@@ -301,3 +301,61 @@ def test_full_size_config(cfg):
     T = int(b.shape.total_nodes)
     rid = u32(b.tree["entry_rid"])[:T * 64]
     assert np.array_equal(rid[:keys.shape[0]], perm)          # fill 1.0: leaf slots in order == perm
+
+
+# ---- NEXT-1: sort by distinguishing prefixes (refinement rounds) -----------------------------
+
+def hier_keys(n, widths, seed, groups=(7, 40), dup_rows=600, carriers=True):
+    """Keys whose first bytes come from few patterns, so that the first 64 (and 128) bits of
+    the compressed key tie over long runs and the refinement has to run LSD rounds and finish
+    runs of every length; exact duplicates in blocks of 2..60 rows. `widths` = number of
+    distinct values per byte (256 = full byte; 2**b makes the byte contribute b mask bits)."""
+    rng = np.random.default_rng(seed)
+    B = len(widths)
+    w = np.asarray(widths)
+    keys = (rng.integers(0, 1 << 30, (n, B)) % w).astype(np.uint8)
+    a = rng.integers(0, groups[0], n)
+    pa = (rng.integers(0, 1 << 30, (groups[0], min(B, 10))) % w[:min(B, 10)]).astype(np.uint8)
+    keys[:, :min(B, 10)] = pa[a]
+    if B > 10:
+        hi = min(B, 20)
+        b = rng.integers(0, groups[1], n)
+        pb = (rng.integers(0, 1 << 30, (groups[1], hi - 10)) % w[10:hi]).astype(np.uint8)
+        sel = rng.random(n) < 0.8
+        keys[sel, 10:hi] = pb[b[sel]]
+    if carriers:                                    # every byte takes every allowed value once
+        m = min(n, int(w.max()))
+        keys[:m] = (np.arange(m)[:, None] % w[None, :]).astype(np.uint8)
+    src = rng.integers(0, n, dup_rows)
+    reps = rng.integers(1, 60, dup_rows)
+    dst = rng.permutation(n)[: int(reps.sum())]
+    keys[dst] = keys[np.repeat(src, reps)[: dst.size]]
+    return keys[rng.permutation(n)]
+
+
+@pytest.mark.parametrize("m", [65, 96, 97, 127, 128, 129, 192, 200, 256])
+def test_refine_widths(m):
+    widths = [256] * (m // 8) + ([1 << (m % 8)] if m % 8 else [])
+    keys = hier_keys(60_000, widths, seed=m)
+    r = cks.build(dev(keys))
+    assert r["sort_bits"] == m
+    check_build(keys, r)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_refine_long_runs(seed):
+    # 32-byte keys, D+ = 256 bits (four 64-bit chunks): runs of up to ~10k keys tie on
+    # chunk 0, thousands still tie on chunk 1; equal-key blocks of every length
+    keys = hier_keys(120_000, [256] * 32, seed=seed, groups=(3, 12), dup_rows=2000)
+    r = cks.build(dev(keys))
+    check_build(keys, r)
+
+
+def test_refine_runs_of_equal_keys():
+    # long runs of equal keys that stay tied to the last chunk (no chunk ever separates them)
+    rng = np.random.default_rng(11)
+    base = rng.integers(0, 256, (40, 24), dtype=np.uint8)
+    counts = np.array([1, 2, 3, 15, 16, 17, 63, 64, 65, 200, 4000, 9000] * 3 + [1, 1, 1, 1])
+    keys = np.repeat(base, counts, axis=0)
+    keys = keys[rng.permutation(keys.shape[0])]
+    check_build(keys, cks.build(dev(keys)))
