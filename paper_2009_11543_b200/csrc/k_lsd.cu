@@ -522,12 +522,21 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
         const uint32_t ltm = lt_mask();
         uint32_t* h = s_hist + warp * HW;
         const uint32_t hbase = smem_addr(h);
+        // global offsets of digit rt for a tile (upsweep output), loaded one tile ahead so the
+        // global-load latency is hidden behind the ranking of the current tile
+        uint32_t nc = 0, nt = 0;
+        auto fetch = [&](uint32_t j) {
+            if (rt < kRadix && j < my_tiles) {
+                const uint32_t tile = blockIdx.x + j * G;
+                nc = __ldg(a.chunk_tot + (uint64_t)(tile / a.chunk_tiles) * kRadix + rt);
+                nt = __ldg(a.tile_off + (uint64_t)tile * kRadix + rt);
+            }
+        };
+        fetch(0);
         for (uint32_t j = 0; j < my_tiles; j++) {
-            const uint32_t tile = blockIdx.x + j * G;
             const uint32_t buf = j & 1;
-            const uint32_t goff = rt < kRadix ? a.chunk_tot[(uint64_t)(tile / a.chunk_tiles) * kRadix + rt] +
-                                                    a.tile_off[(uint64_t)tile * kRadix + rt]
-                                              : 0u;
+            const uint32_t goff = nc + nt;
+            fetch(j + 1);
             const uint32_t* dslot = ring + (size_t)(j % kDigitSlots) * TILE;
 #pragma unroll
             for (int q = lane; q < HW; q += 32) h[q] = 0;
