@@ -49,7 +49,7 @@ struct cks_ctx {
     // scratch
     DevBuf occ, masks8, planeA, planeB, ridA, ridB, hist, base, status, counters, dacc, moff, dbit,
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
-        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, tie, keep, done, rcnt, rtot;   // NEXT-1
+        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, tie, keep, done, mlist, rcnt, rtot;   // NEXT-1
     int algo = -1;                    // LSD pass: 1 = reduce-then-scan (default), 0 = onesweep
                                       // (decoupled look-back; measured slower)
     size_t status_tiles = 0;
@@ -448,6 +448,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         TRY(ensure(ctx, ctx->runoff, sp * 4));
         TRY(ensure(ctx, ctx->keep, n + 16));
         TRY(ensure(ctx, ctx->done, n + 16));
+        TRY(ensure(ctx, ctx->mlist, sp * 4));
         TRY(ensure(ctx, ctx->rcnt, (size_t)(ref_tiles(n) + 1) * 8));
         TRY(ensure(ctx, ctx->rtot, 16));
     }
@@ -476,8 +477,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         // (2) finish short runs and runs of equal keys in place
         const int qtop = (int)np - 1 - 2 * (int)r;
         LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, posA_, segA_, as<uint32_t>(ctx->runoff), nseg, nn, out->perm,
-                                dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B, ctx->sms,
-                                ctx->stream));
+                                dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B,
+                                as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->rtot) + 2, ctx->sms, ctx->stream));
         // (3) the runs left for an LSD round
         LAUNCH(launch_ref_compact(as<uint8_t>(ctx->keep), nn, posA_, as<uint32_t>(ctx->rcnt), as<uint32_t>(ctx->rtot),
                                   posB_, segB_, nullptr, ctx->stream));
@@ -762,7 +763,7 @@ int cks_ctx_destroy(cks_ctx* ctx) {
                       &ctx->dbit, &ctx->rmin0, &ctx->rmin1, &ctx->plan[0], &ctx->plan[1], &ctx->plan[2],
                       &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total,
                       &ctx->pm, &ctx->pd, &ctx->cmp, &ctx->crid, &ctx->crid2, &ctx->posA, &ctx->posB,
-                      &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->tie, &ctx->keep, &ctx->done,
+                      &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->tie, &ctx->keep, &ctx->done, &ctx->mlist,
                       &ctx->rcnt, &ctx->rtot};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);

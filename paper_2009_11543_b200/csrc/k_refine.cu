@@ -17,6 +17,8 @@
 // Kernels: k_ref_adj (round adjacency: D_i, tie flags, D accumulation), k_ref_count /
 // k_ref_scan / k_ref_scatter (compaction of the tied runs into the next round's list),
 // k_ref_gather (chunk r of the listed rows), k_ref_put (sorted row ids back into place).
+#include <stdlib.h>
+
 #include "cks_internal.h"
 
 namespace cks {
@@ -206,12 +208,16 @@ k_ref_gather(const uint32_t* __restrict__ pm, uint64_t pitch, int qhi, int qlo, 
 // (duplicates). Every other run is flagged for the next LSD round (keep[k] = 1 for its
 // members but the first: the compaction's tie convention).
 constexpr uint32_t kLocal = 16;
-constexpr uint32_t kDupCheck = 64;
+constexpr uint32_t kCta = 2048;                  // medium runs: one CTA, bitonic sort in shared memory
+constexpr uint32_t kCtaWords = 8;                // ... if at most this many P_M planes remain (measured:
+                                                 // with 10 remaining planes, cfg4, gathering them by row
+                                                 // id costs more than leaving the runs to the LSD round)
 __global__ void __launch_bounds__(kRefThreads)
 k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* __restrict__ moff,
             const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
             uint32_t* __restrict__ perm, uint16_t* __restrict__ dbit, uint32_t* __restrict__ dacc,
-            uint8_t* __restrict__ done, uint32_t* __restrict__ carried, uint32_t nwords) {
+            uint8_t* __restrict__ done, uint32_t* __restrict__ carried, uint32_t nwords, uint32_t* __restrict__ mlist,
+            uint32_t* __restrict__ mcount, uint32_t cta_max) {
     __shared__ uint32_t s_bm[kMaxBits / 32];                         // D bits found by this block
     for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
     __syncthreads();
@@ -286,15 +292,93 @@ k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qt
                     if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
                 }
             }
+        } else if (L <= cta_max && qtop + 1 <= (int)kCtaWords) {
+            mlist[atomicAdd(mcount, 1u)] = (uint32_t)s;           // medium run: one CTA sorts it
         } else {
-            // a moderately long run of equal keys is finished too (row-id order = stable order)
-            bool dup = L <= kDupCheck;
-            const uint32_t r0 = perm[p0];
-            for (uint32_t j = 1; dup && j < L; j++) dup = cmp(r0, perm[p0 + j], nullptr) == 0;
-            done[s] = dup ? 1 : 0;
+            done[s] = 0;                                         // long run: next LSD round
             continue;
         }
         done[s] = 1;
+    }
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
+        if (s_bm[w]) atomicOr(&dacc[w], s_bm[w]);
+}
+
+// Medium runs (kLocal < L <= kCta): one CTA per run (grid-stride over the list made by
+// k_ref_local). The run's row ids and remaining P_M words (planes qtop .. 0, from the
+// carried sorted planes or by row id) are staged in shared memory and an index array is
+// bitonic-sorted by (words, row id) -- the stable order; then perm, the carried planes and
+// the D_i (first differing remaining bit) are written at the run's positions.
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_cta(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* __restrict__ moff,
+          const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
+          uint32_t* __restrict__ perm, uint16_t* __restrict__ dbit, uint32_t* __restrict__ dacc,
+          uint32_t* __restrict__ carried, uint32_t nwords, const uint32_t* __restrict__ mlist,
+          const uint32_t* __restrict__ mcount) {
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* s_rid = s_dyn;                                         // [kCta]
+    uint32_t* s_kw = s_rid + kCta;                                   // [Wr][kCta], word 0 = plane qtop
+    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_kw + (qtop + 1) * kCta);   // [kCta]
+    __shared__ uint32_t s_bm[kMaxBits / 32];
+    const uint32_t Wr = (uint32_t)qtop + 1;
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
+    const uint32_t cnt = *mcount;
+    for (uint32_t mi = blockIdx.x; mi < cnt; mi += gridDim.x) {
+        const uint32_t s = mlist[mi];
+        const uint32_t k0 = run_off[s];
+        const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
+        const uint32_t L = k1 - k0;
+        const uint32_t p0 = pos[k0];
+        uint32_t P2 = 1;
+        while (P2 < L) P2 <<= 1;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) {
+            const uint32_t row = perm[p0 + j];
+            s_rid[j] = row;
+            for (uint32_t q = 0; q < Wr; q++)
+                s_kw[q * kCta + j] = carried ? carried[(uint64_t)(qtop - (int)q) * pitch + p0 + j]
+                                             : __ldg(pm + (uint64_t)(qtop - (int)q) * pitch + row);
+        }
+        for (uint32_t j = threadIdx.x; j < P2; j += blockDim.x) s_idx[j] = (uint16_t)j;
+        __syncthreads();
+        auto less = [&](uint32_t a, uint32_t b) -> bool {            // padding (>= L) sorts last
+            if (a >= L || b >= L) return a < b;
+            for (uint32_t q = 0; q < Wr; q++) {
+                const uint32_t x = s_kw[q * kCta + a], y = s_kw[q * kCta + b];
+                if (x != y) return x < y;
+            }
+            return s_rid[a] < s_rid[b];
+        };
+        for (uint32_t size = 2; size <= P2; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = threadIdx.x; i < P2 / 2; i += blockDim.x) {
+                    const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const uint32_t a = s_idx[lo], b = s_idx[hi];
+                    if (less(b, a) == up) { s_idx[lo] = (uint16_t)b; s_idx[hi] = (uint16_t)a; }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) {
+            const uint32_t a = s_idx[j];
+            perm[p0 + j] = s_rid[a];
+            if (carried)
+                for (uint32_t q = 0; q < Wr; q++) carried[(uint64_t)(qtop - (int)q) * pitch + p0 + j] = s_kw[q * kCta + a];
+            if (j == 0) continue;
+            const uint32_t b = s_idx[j - 1];
+            for (uint32_t q = 0; q < Wr; q++) {
+                const uint32_t x = s_kw[q * kCta + a] ^ s_kw[q * kCta + b];
+                if (x) {
+                    const uint32_t d = moff[32u * (np - 1 - (uint32_t)(qtop - (int)q)) + (uint32_t)__clz(x)];
+                    dbit[p0 + j] = (uint16_t)d;
+                    const uint32_t bb = 0x80000000u >> (d & 31);
+                    if (!(s_bm[d >> 5] & bb)) atomicOr(&s_bm[d >> 5], bb);
+                    break;
+                }
+            }
+        }
     }
     __syncthreads();
     for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
@@ -334,6 +418,18 @@ static unsigned grid_of(uint64_t work, int sms) {
     return (unsigned)(g ? g : 1);
 }
 
+// longest run sorted by one CTA (env CKS_REF_CTA, default 2048, at most kCta)
+static uint32_t cta_max() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("CKS_REF_CTA");
+        v = e ? atoi(e) : (int)kCta;
+        if (v < 0) v = 0;
+        if (v > (int)kCta) v = (int)kCta;
+    }
+    return (uint32_t)v;
+}
+
 uint64_t ref_tiles(uint64_t nr) { return (nr + kRefTile - 1) / kRefTile; }
 
 cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_t* seg, const uint32_t* pos,
@@ -360,11 +456,24 @@ cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* 
 cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
                              const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
-                             uint32_t* carried, uint32_t B, int sms, cudaStream_t st) {
+                             uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* mcount, int sms,
+                             cudaStream_t st) {
     if (nseg == 0) return cudaSuccess;
     const uint32_t nwords = (8 * B + 31) / 32;
+    cudaMemsetAsync(mcount, 0, 4, st);
     k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn, perm,
-                                                            dbit, dacc, done, carried, nwords);
+                                                            dbit, dacc, done, carried, nwords, mlist, mcount,
+                                                            cta_max());
+    if (qtop + 1 <= (int)kCtaWords) {
+        const size_t smem = (size_t)kCta * 4 * (qtop + 2) + (size_t)kCta * 2;
+        static size_t configured = 0;
+        if (smem > configured) {
+            cudaFuncSetAttribute(k_ref_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured = smem;
+        }
+        k_ref_cta<<<(unsigned)(sms * 4), kRefThreads, smem, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn,
+                                                                  perm, dbit, dacc, carried, nwords, mlist, mcount);
+    }
     k_ref_keep<<<grid_of(nn, sms), kRefThreads, 0, st>>>(seg, run_off, done, nn, keep);
     return cudaGetLastError();
 }
