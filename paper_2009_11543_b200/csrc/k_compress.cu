@@ -12,6 +12,7 @@
 // Keys are staged through shared memory with coalesced 16-byte loads; each row is
 // padded to an odd number of 16-byte units so a thread's 16-byte reads of its own row
 // are bank-conflict free (8 lanes per phase hit 8 distinct 16-byte bank groups).
+#include <stdlib.h>
 #include <string.h>
 
 #include "cks_internal.h"
@@ -165,49 +166,69 @@ struct FixedPlan {
 };
 
 template <int B>
+__device__ __forceinline__ void load_key(const uint8_t* kp, uint32_t (&w)[B / 4]) {
+    if (B == 8) {
+        uint2 v = __ldg(reinterpret_cast<const uint2*>(kp));
+        w[0] = v.x;
+        w[1] = v.y;
+    } else {
+#pragma unroll
+        for (int u = 0; u < B / 16; u++) {
+            uint4 v = __ldg(reinterpret_cast<const uint4*>(kp) + u);
+            w[4 * u + 0] = v.x;
+            w[4 * u + 1] = v.y;
+            w[4 * u + 2] = v.z;
+            w[4 * u + 3] = v.w;
+        }
+    }
+}
+
+// KPT keys per thread per iteration, all loads issued before any gather: more bytes in
+// flight (the row-list variant's loads are random rows behind a dependent perm load).
+template <int B, int KPT, bool SKIP>
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_fixed(const uint8_t* __restrict__ keys, uint64_t n, const __grid_constant__ FixedPlan<B / 4> plan,
                  uint32_t* __restrict__ planes, uint64_t pitch, uint32_t lead, const uint32_t* __restrict__ rows) {
     constexpr int NW = B / 4;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t w[NW];
-        const uint8_t* kp = keys + (rows ? (uint64_t)__ldg(rows + i) : i) * B;
-        if (B == 8) {
-            uint2 v = __ldg(reinterpret_cast<const uint2*>(kp));
-            w[0] = v.x;
-            w[1] = v.y;
-        } else {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += T * KPT) {
+        uint32_t w[KPT][NW];
+        uint64_t r[KPT];
 #pragma unroll
-            for (int u = 0; u < B / 16; u++) {
-                uint4 v = __ldg(reinterpret_cast<const uint4*>(kp) + u);
-                w[4 * u + 0] = v.x;
-                w[4 * u + 1] = v.y;
-                w[4 * u + 2] = v.z;
-                w[4 * u + 3] = v.w;
-            }
+        for (int u = 0; u < KPT; u++) {
+            const uint64_t i = i0 + u * T;
+            r[u] = i < n ? (rows ? (uint64_t)__ldg(rows + i) : i) : 0;
         }
-        unsigned long long acc = 0;
-        uint32_t accbits = lead, q = 0;
 #pragma unroll
-        for (int k = NW - 1; k >= 0; k--) {                      // least significant end of P first
-            if (plan.mask[k] == 0) continue;
-            uint32_t x = bswap32(w[k]) & plan.mask[k];
+        for (int u = 0; u < KPT; u++)
+            if (i0 + u * T < n) load_key<B>(keys + r[u] * B, w[u]);
 #pragma unroll
-            for (int s = 0; s < 5; s++) {
-                uint32_t t = x & plan.mv[k][s];
-                x = (x ^ t) | (t >> (1u << s));
+        for (int u = 0; u < KPT; u++) {
+            const uint64_t i = i0 + u * T;
+            if (i >= n) break;
+            unsigned long long acc = 0;
+            uint32_t accbits = lead, q = 0;
+#pragma unroll
+            for (int k = NW - 1; k >= 0; k--) {                  // least significant end of P first
+                if (plan.mask[k] == 0) continue;
+                uint32_t x = bswap32(w[u][k]) & plan.mask[k];
+#pragma unroll
+                for (int s = 0; s < 5; s++) {
+                    if (SKIP && plan.mv[k][s] == 0) continue;    // uniform: steps this mask does not need
+                    uint32_t t = x & plan.mv[k][s];
+                    x = (x ^ t) | (t >> (1u << s));
+                }
+                acc |= (unsigned long long)x << accbits;
+                accbits += plan.cnt[k];
+                if (accbits >= 32) {
+                    planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
+                    acc >>= 32;
+                    accbits -= 32;
+                    q++;
+                }
             }
-            acc |= (unsigned long long)x << accbits;
-            accbits += plan.cnt[k];
-            if (accbits >= 32) {
-                planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
-                acc >>= 32;
-                accbits -= 32;
-                q++;
-            }
+            if (accbits) planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
         }
-        if (accbits) planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
     }
 }
 
@@ -222,7 +243,11 @@ static void launch_fixed(const uint8_t* keys, uint64_t n, const GatherPlan* hpla
         for (int k = 0; k < 5; k++) fp.mv[g.src][k] = g.mv[k];
         fp.cnt[g.src] = g.cnt;
     }
-    k_compress_fixed<B><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, lead, rows);
+    // rows: random key rows behind a dependent load -> 4 keys in flight per thread; in order:
+    // ALU-bound, one key per thread measured fastest (neither 2 keys per thread nor skipping
+    // the parallel-suffix steps a mask does not need paid off)
+    if (rows) k_compress_fixed<B, 4, false><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, lead, rows);
+    else k_compress_fixed<B, 1, false><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, lead, rows);
 }
 
 static int grid_for(uint64_t work, int per_sm, int sms) {
