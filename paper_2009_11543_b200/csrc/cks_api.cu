@@ -479,11 +479,17 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, posA_, segA_, as<uint32_t>(ctx->runoff), nseg, nn, out->perm,
                                 dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B,
                                 as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->rtot) + 2, ctx->sms, ctx->stream));
-        // (3) the runs left for an LSD round
-        LAUNCH(launch_ref_compact(as<uint8_t>(ctx->keep), nn, posA_, as<uint32_t>(ctx->rcnt), as<uint32_t>(ctx->rtot),
-                                  posB_, segB_, nullptr, ctx->stream));
+        // (3) the runs left for an LSD round (none: done)
+        CK(cudaMemcpyAsync(ctx->h_tot, as<uint32_t>(ctx->rtot) + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
         uint64_t n2 = 0, nseg2 = 0;
-        TRY(counts(&n2, &nseg2));
+        if (ctx->h_tot[1] > 0) {
+            LAUNCH(launch_ref_keep(segA_, as<uint32_t>(ctx->runoff), as<uint8_t>(ctx->done), nn, as<uint8_t>(ctx->keep),
+                                   ctx->sms, ctx->stream));
+            LAUNCH(launch_ref_compact(as<uint8_t>(ctx->keep), nn, posA_, as<uint32_t>(ctx->rcnt),
+                                      as<uint32_t>(ctx->rtot), posB_, segB_, nullptr, ctx->stream));
+            TRY(counts(&n2, &nseg2));
+        }
         if (log)
             fprintf(stderr, "[cks refine] round %u: %llu tied keys in %llu runs; %llu keys in %llu runs left for LSD\n",
                     r, (unsigned long long)nn, (unsigned long long)nseg, (unsigned long long)n2,

@@ -134,6 +134,8 @@ cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, in
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
                              uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* mcount, int sms,
                              cudaStream_t st);
+cudaError_t launch_ref_keep(const uint32_t* seg, const uint32_t* run_off, const uint8_t* done, uint64_t nn,
+                            uint8_t* keep, int sms, cudaStream_t st);
 cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, int qhi, int qlo, const uint32_t* pos,
                               const uint32_t* seg, const uint32_t* perm, uint64_t nr, uint32_t* out, uint64_t opitch,
                               uint32_t* orid, int sms, cudaStream_t st);

@@ -80,30 +80,29 @@ k_ref_adj(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, cons
 
 // Element k belongs to a tied run if it ties with its predecessor or its successor; it
 // starts a run if it does not tie with its predecessor.
-__device__ __forceinline__ void ref_flags(const uint8_t* tie, uint64_t nr, uint64_t k, uint32_t& member,
-                                          uint32_t& start) {
-    if (k >= nr) { member = start = 0; return; }
-    const uint32_t a = tie[k], b = k + 1 < nr ? tie[k + 1] : 0u;
-    member = a | b;
-    start = member & (a ^ 1u);
+
+// Tiles of kRefTile elements; warp w of a tile owns the contiguous elements
+// [w*32*kRefItems, (w+1)*32*kRefItems), walked 32 at a time (coalesced flag loads, ballots).
+__device__ __forceinline__ void ref_flags2(const uint8_t* tie, uint64_t nr, uint64_t k, bool& member, bool& start) {
+    const uint32_t a = k < nr ? tie[k] : 0u, b = k + 1 < nr ? tie[k + 1] : 0u;
+    member = (a | b) != 0;
+    start = member && !a;
 }
 
-// per tile of kRefTile elements: (members, run starts)
+// per tile: (members, run starts)
 __global__ void __launch_bounds__(kRefThreads)
 k_ref_count(const uint8_t* __restrict__ tie, uint64_t nr, uint32_t* __restrict__ cnt) {
     __shared__ uint32_t s_red[2][kRefThreads / 32];
-    const uint64_t k0 = (uint64_t)blockIdx.x * kRefTile + (uint64_t)threadIdx.x * kRefItems;
-    uint32_t cm = 0, cs = 0;
-#pragma unroll
-    for (int i = 0; i < kRefItems; i++) {
-        uint32_t mb, st;
-        ref_flags(tie, nr, k0 + i, mb, st);
-        cm += mb;
-        cs += st;
-    }
-    cm = __reduce_add_sync(0xffffffffu, cm);
-    cs = __reduce_add_sync(0xffffffffu, cs);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t k0 = (uint64_t)blockIdx.x * kRefTile + (uint64_t)warp * 32 * kRefItems + lane;
+    uint32_t cm = 0, cs = 0;
+#pragma unroll 4
+    for (int i = 0; i < kRefItems; i++) {
+        bool mb, st;
+        ref_flags2(tie, nr, k0 + 32 * i, mb, st);
+        cm += __popc(__ballot_sync(0xffffffffu, mb));
+        cs += __popc(__ballot_sync(0xffffffffu, st));
+    }
     if (lane == 0) { s_red[0][warp] = cm; s_red[1][warp] = cs; }
     __syncthreads();
     if (threadIdx.x < 2) {
@@ -151,37 +150,41 @@ k_ref_scan(uint32_t* __restrict__ cnt, uint32_t ntiles, uint32_t* __restrict__ t
     if (threadIdx.x < 2) tot[threadIdx.x] = s_carry[threadIdx.x];
 }
 
-// write the next round's list: global position and run index of every tied element
+// write the next round's list: global position and run index of every tied element (and the
+// list index of every run's first element)
 __global__ void __launch_bounds__(kRefThreads)
 k_ref_scatter(const uint8_t* __restrict__ tie, uint64_t nr, const uint32_t* __restrict__ pos,
               const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pos_next, uint32_t* __restrict__ seg_next,
               uint32_t* __restrict__ run_off) {
     __shared__ uint32_t s_w[2][kRefThreads / 32];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t k0 = (uint64_t)blockIdx.x * kRefTile + (uint64_t)threadIdx.x * kRefItems;
-    uint32_t mb[kRefItems], st[kRefItems], cm = 0, cs = 0;
-#pragma unroll
-    for (int i = 0; i < kRefItems; i++) {
-        ref_flags(tie, nr, k0 + i, mb[i], st[i]);
-        cm += mb[i];
-        cs += st[i];
+    const uint32_t ltm = (1u << lane) - 1u;
+    const uint64_t k0 = (uint64_t)blockIdx.x * kRefTile + (uint64_t)warp * 32 * kRefItems + lane;
+    uint32_t cm = 0, cs = 0;
+    for (int i = 0; i < kRefItems; i++) {                       // pass 1: this warp's counts
+        bool mb, st;
+        ref_flags2(tie, nr, k0 + 32 * i, mb, st);
+        cm += __popc(__ballot_sync(0xffffffffu, mb));
+        cs += __popc(__ballot_sync(0xffffffffu, st));
     }
-    const uint32_t em = warp_excl_scan(cm, lane), es = warp_excl_scan(cs, lane);
-    if (lane == 31) { s_w[0][warp] = em + cm; s_w[1][warp] = es + cs; }
+    if (lane == 0) { s_w[0][warp] = cm; s_w[1][warp] = cs; }
     __syncthreads();
-    uint32_t bm = cnt[2 * (uint64_t)blockIdx.x], bs = cnt[2 * (uint64_t)blockIdx.x + 1];
-    for (uint32_t w = 0; w < warp; w++) { bm += s_w[0][w]; bs += s_w[1][w]; }
-    uint32_t om = bm + em, os = bs + es;                    // os = run starts before this thread
-#pragma unroll
-    for (int i = 0; i < kRefItems; i++) {
-        os += st[i];
-        if (mb[i]) {
-            const uint64_t k = k0 + i;
-            pos_next[om] = pos ? pos[k] : (uint32_t)k;
-            seg_next[om] = os - 1;
-            if (st[i] && run_off) run_off[os - 1] = om;
-            om++;
+    uint32_t om = cnt[2 * (uint64_t)blockIdx.x], os = cnt[2 * (uint64_t)blockIdx.x + 1];
+    for (uint32_t w = 0; w < warp; w++) { om += s_w[0][w]; os += s_w[1][w]; }
+    for (int i = 0; i < kRefItems; i++) {                       // pass 2: write in element order
+        bool mb, st;
+        const uint64_t k = k0 + 32 * i;
+        ref_flags2(tie, nr, k, mb, st);
+        const uint32_t bm = __ballot_sync(0xffffffffu, mb), bs = __ballot_sync(0xffffffffu, st);
+        if (mb) {
+            const uint32_t o = om + __popc(bm & ltm);
+            const uint32_t sg = os + __popc(bs & (ltm | (1u << lane))) - 1;   // runs started so far
+            pos_next[o] = pos ? pos[k] : (uint32_t)k;
+            seg_next[o] = sg;
+            if (st && run_off) run_off[sg] = o;
         }
+        om += __popc(bm);
+        os += __popc(bs);
     }
 }
 
@@ -296,6 +299,7 @@ k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qt
             mlist[atomicAdd(mcount, 1u)] = (uint32_t)s;           // medium run: one CTA sorts it
         } else {
             done[s] = 0;                                         // long run: next LSD round
+            atomicAdd(mcount + 1, 1u);
             continue;
         }
         done[s] = 1;
@@ -458,9 +462,9 @@ cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, in
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
                              uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* mcount, int sms,
                              cudaStream_t st) {
-    if (nseg == 0) return cudaSuccess;
+    if (nseg == 0) return cudaMemsetAsync(mcount, 0, 8, st);
     const uint32_t nwords = (8 * B + 31) / 32;
-    cudaMemsetAsync(mcount, 0, 4, st);
+    cudaMemsetAsync(mcount, 0, 8, st);                           // medium runs, long runs
     k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn, perm,
                                                             dbit, dacc, done, carried, nwords, mlist, mcount,
                                                             cta_max());
@@ -474,6 +478,12 @@ cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, in
         k_ref_cta<<<(unsigned)(sms * 4), kRefThreads, smem, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn,
                                                                   perm, dbit, dacc, carried, nwords, mlist, mcount);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_keep(const uint32_t* seg, const uint32_t* run_off, const uint8_t* done, uint64_t nn,
+                            uint8_t* keep, int sms, cudaStream_t st) {
+    if (nn == 0) return cudaSuccess;
     k_ref_keep<<<grid_of(nn, sms), kRefThreads, 0, st>>>(seg, run_off, done, nn, keep);
     return cudaGetLastError();
 }
