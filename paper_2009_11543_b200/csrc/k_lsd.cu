@@ -402,11 +402,18 @@ k_downsweep(const LsdPassArgs a) {
 //                  coalesced runs, releasing each slot (`empty`) as they go.
 // So while the writers move tile j the rankers already work on tile j+1 and the producer
 // keeps the next loads in flight: the store stream never waits for a ranking phase.
-constexpr int kRW = 16;                          // ranker warps: ranking is latency-bound, so
-constexpr int kWW = 8;                           // it gets twice the warps of the writers
-constexpr int kWsWarps = kRW + kWW + 1;          // + 1 producer
-constexpr int kWsThreads = kWsWarps * 32;
-constexpr int kRT = kRW * 32;                    // ranker threads
+// Shapes (TILE keys, RW ranker warps, WW writer warps, CTAs per SM): ranking is
+// latency-bound, so rankers get twice the warps of the writers.
+//   WsShape<4096, 16, 8, 1>  one CTA of 800 threads per SM (default)
+//   WsShape<2048,  8, 4, 2>  two CTAs of 416 threads per SM (CKS_LSD_ITEMS=8)
+template <int TILE_, int RW_, int WW_, int MINB_>
+struct WsShape {
+    static constexpr int TILE = TILE_, RW = RW_, WW = WW_, MINB = MINB_;
+    static constexpr int RT = RW * 32, WT = WW * 32;            // ranker / writer threads
+    static constexpr int THREADS = (RW + WW + 1) * 32;          // + 1 producer warp
+    static constexpr int RI = TILE / RT, WI = TILE / WT;        // keys per ranker lane / slots per writer
+    static_assert(RT >= kRadix, "digit phase needs a thread per digit");
+};
 constexpr uint32_t kDigitSlots = 3;              // digit-word ring (ranked one tile ahead)
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
@@ -418,8 +425,10 @@ __device__ __forceinline__ void bar_init_n(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void bar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
-// exclusive scan over the kRT ranker threads (named barrier 1)
+// exclusive scan over the RW*32 ranker threads (named barrier 1)
+template <int RW>
 __device__ __forceinline__ uint32_t scan_rankers(uint32_t v, uint32_t* s_warp, uint32_t rt) {
+    constexpr int kRW = RW, kRT = RW * 32;
     const uint32_t lane = rt & 31, warp = rt >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -444,10 +453,10 @@ __device__ __forceinline__ uint32_t scan_rankers(uint32_t v, uint32_t* s_warp, u
     return r;
 }
 
-template <int ITEMS>
-__global__ void __launch_bounds__(kWsThreads, 1)
+template <class SH>
+__global__ void __launch_bounds__(SH::THREADS, SH::MINB)
 k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
-    constexpr int TILE = kSortThreads * ITEMS;
+    constexpr int TILE = SH::TILE, kRW = SH::RW, kWW = SH::WW, kRT = SH::RT, WI = SH::WI;
     constexpr int HW = kRadix + 8;
     extern __shared__ __align__(128) uint8_t s_dyn[];
     uint32_t* ring = reinterpret_cast<uint32_t*>(s_dyn);                                   // [R][TILE]
@@ -516,7 +525,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
 
     if (warp < kRW) {
         // ---------------- rankers: thread rt < 256 is digit rt in the per-digit phases
-        constexpr int RI = TILE / kRT;                           // keys per ranker lane
+        constexpr int RI = SH::RI;                               // keys per ranker lane
         const uint32_t rt = tid;
         const uint32_t wofs = warp * 32 * RI;
         const uint32_t ltm = lt_mask();
@@ -570,7 +579,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
 #pragma unroll
                     for (int k = 0; k < kRW; k++) { c[k] = s_hist[k * HW + rt]; total += c[k]; }
                 }
-                const uint32_t excl = scan_rankers(total, s_warp, rt);
+                const uint32_t excl = scan_rankers<kRW>(total, s_warp, rt);
                 if (rt < kRadix) {
                     uint32_t run = excl;
 #pragma unroll
@@ -590,7 +599,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
         return;
     }
 
-    // ---------------- writers: thread wt owns output slots r*256 + wt
+    // ---------------- writers: thread wt owns output slots r*WT + wt
     const uint32_t wt = tid - kRT;
     uint32_t y = 0;                                              // data item counter
     for (uint32_t j = 0; j < my_tiles; j++) {
@@ -598,18 +607,18 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
         const uint32_t buf = j & 1;
         bar_wait(&s_ranked[buf], (j >> 1) & 1u);
         const uint16_t* src = s_src + buf * TILE;
-        uint32_t from[ITEMS], dest[ITEMS];
+        uint32_t from[WI], dest[WI];
 #pragma unroll
-        for (int r = 0; r < ITEMS; r++) from[r] = src[r * kSortThreads + wt];
+        for (int r = 0; r < WI; r++) from[r] = src[r * SH::WT + wt];
         {
             const uint32_t slot = j % kDigitSlots;
             bar_wait(&s_full[slot], (j / kDigitSlots) & 1u);
             const uint8_t* sl = reinterpret_cast<const uint8_t*>(ring + (size_t)slot * TILE);
             uint32_t* out = dst_of(0);
 #pragma unroll
-            for (int r = 0; r < ITEMS; r++) {
+            for (int r = 0; r < WI; r++) {
                 const uint32_t w = *reinterpret_cast<const uint32_t*>(sl + from[r]);
-                dest[r] = (a.debug & 1) ? tile * (uint32_t)TILE + r * kSortThreads + wt : r * kSortThreads + wt + s_gb[buf][digit_of(w, sel)];
+                dest[r] = (a.debug & 1) ? tile * (uint32_t)TILE + r * SH::WT + wt : r * SH::WT + wt + s_gb[buf][digit_of(w, sel)];
                 out[dest[r]] = w;
             }
             __syncwarp();
@@ -620,7 +629,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
             if (k == S - 1 && implicit_rid) {
                 const uint32_t b32 = tile * (uint32_t)TILE;
 #pragma unroll
-                for (int r = 0; r < ITEMS; r++) out[dest[r]] = b32 + (from[r] >> 2);
+                for (int r = 0; r < WI; r++) out[dest[r]] = b32 + (from[r] >> 2);
                 continue;
             }
             const uint32_t slot = kDigitSlots + y % R;
@@ -628,7 +637,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
             y++;
             const uint8_t* sl = reinterpret_cast<const uint8_t*>(ring + (size_t)slot * TILE);
 #pragma unroll
-            for (int r = 0; r < ITEMS; r++) out[dest[r]] = *reinterpret_cast<const uint32_t*>(sl + from[r]);
+            for (int r = 0; r < WI; r++) out[dest[r]] = *reinterpret_cast<const uint32_t*>(sl + from[r]);
             __syncwarp();
             if (lane == 0) bar_arrive(&s_empty[slot]);
         }
@@ -679,8 +688,11 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
     int nl = 2;
     if (g_lsd_ws && a.tma && nfull > 0) {
         // warp-specialised kernel over the full tiles, one persistent CTA per SM
-        constexpr size_t fixed = (size_t)kRW * (kRadix + 8) * 4 + (size_t)2 * TILE * 2;
-        const int max_slots = (int)((200u * 1024u - fixed) / ((size_t)TILE * 4));
+        using SH = typename std::conditional<ITEMS == 8, WsShape<2048, 8, 4, 2>, WsShape<4096, 16, 8, 1>>::type;
+        static_assert(SH::TILE == TILE, "the upsweep's tile is the downsweep's tile");
+        constexpr size_t fixed = (size_t)SH::RW * (kRadix + 8) * 4 + (size_t)2 * TILE * 2;
+        const size_t budget = SH::MINB == 2 ? 100u * 1024u : 200u * 1024u;
+        const int max_slots = (int)((budget - fixed) / ((size_t)TILE * 4));
         int R = 2 * (streams - 1);                           // data ring: the non-digit streams
         if (R > max_slots - (int)kDigitSlots) R = max_slots - (int)kDigitSlots;
         if (R > 16) R = 16;
@@ -690,10 +702,11 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
         const size_t smem = (size_t)(kDigitSlots + R) * TILE * 4 + fixed;
         static size_t configured_ws = 0;
         if (smem > configured_ws) {
-            cudaFuncSetAttribute(k_downsweep_ws<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(k_downsweep_ws<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             configured_ws = smem;
         }
-        const uint64_t grid = nfull < (uint64_t)sms ? nfull : (uint64_t)sms;
+        const uint64_t gmax = (uint64_t)sms * SH::MINB;
+        const uint64_t grid = nfull < gmax ? nfull : gmax;
         const bool tail = nfull != tiles;
         if (tail && aux.stream) {
             // the partial last tile runs concurrently on the aux stream (its offsets are
@@ -714,7 +727,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
             nl++;
         }
         if (aux.ws_begin) cudaEventRecord(aux.ws_begin, st);
-        k_downsweep_ws<ITEMS><<<(unsigned)grid, kWsThreads, smem, st>>>(w, (uint32_t)nfull);
+        k_downsweep_ws<SH><<<(unsigned)grid, SH::THREADS, smem, st>>>(w, (uint32_t)nfull);
         if (aux.ws_end) cudaEventRecord(aux.ws_end, st);
         // algorithmic bytes: every loaded stream read once, every stream written once
         if (aux.ws_bytes) *aux.ws_bytes = (double)nfull * TILE * 4.0 * (double)(streams + (int)a.nplanes + 1);
