@@ -240,7 +240,7 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
         lsd_sizes(n, &lsd_tiles, &lsd_chunks);
         TRY(ensure(ctx, ctx->tile_off, (size_t)lsd_tiles * 256 * 4));
         TRY(ensure(ctx, ctx->chunk_tot, (size_t)lsd_chunks * 256 * 4));
-        TRY(ensure(ctx, ctx->total, 256 * 4));
+        TRY(ensure(ctx, ctx->total, 256 * 4, /*zero=*/true));    // then kept zero by every downsweep
     }
     if (ctx->algo == 0) {
         CK(cudaMemsetAsync(ctx->hist.p, 0, (size_t)Pfull * 256 * 4, ctx->stream));

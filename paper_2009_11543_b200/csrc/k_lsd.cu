@@ -50,6 +50,12 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
                      " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
     }
 }
+// Programmatic dependent launch: the kernels of a pass are launched with programmatic stream
+// serialisation, so a kernel's CTAs can be scheduled while its predecessor drains; each
+// waits here before touching what the predecessor wrote.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t lt_mask() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -101,6 +107,8 @@ k_upsweep(const LsdPassArgs a) {
     constexpr int TILE = kSortThreads * ITEMS;
     constexpr int V = ITEMS / 4;                              // uint4 loads per thread per tile
     __shared__ uint32_t bins[kW][kRadix];
+    pdl_wait();
+    pdl_trigger();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t n = a.n;
     const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
@@ -160,6 +168,8 @@ __global__ void __launch_bounds__(1024)
 k_chunk_scan(const LsdPassArgs a, uint32_t nchunks) {
     __shared__ uint32_t s_part[32][33];
     __shared__ uint32_t s_base[32];
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t d = blockIdx.x * 32 + lane;
     if (warp == 0) {                                         // bucket base of digit d
@@ -233,6 +243,7 @@ k_downsweep(const LsdPassArgs a) {
     const uint64_t n = a.n;
     const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
     const uint32_t G = gridDim.x;
+    if (blockIdx.x == 0 && tid < kRadix) a.total[tid] = 0;      // digit totals of the next pass's upsweep
     const int np = (int)a.nplanes, dp = a.digit_plane;
     const int S = np + 1;
     const bool implicit_rid = a.in_rid == nullptr;
@@ -494,6 +505,9 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
         bar_fence_init();
     }
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
+    if (blockIdx.x == 0 && tid < kRadix) a.total[tid] = 0;      // digit totals of the next pass's upsweep
 
     if (warp == kRW + kWW) {
         // ---------------- producer: digit words one tile ahead in their own 3-slot ring
@@ -675,14 +689,29 @@ void lsd_sizes(uint64_t n, uint64_t* tiles, uint64_t* chunks) {
     *chunks = (*tiles + g_lsd_chunk - 1) / g_lsd_chunk;
 }
 
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int ITEMS>
 static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAux& aux, int* launches) {
     constexpr int TILE = kSortThreads * ITEMS;
     const uint64_t tiles = (a.n + TILE - 1) / TILE;
     const uint64_t chunks = (tiles + a.chunk_tiles - 1) / a.chunk_tiles;
-    cudaMemsetAsync(a.total, 0, kRadix * 4, st);
-    k_upsweep<ITEMS><<<(unsigned)chunks, kSortThreads, 0, st>>>(a);
-    k_chunk_scan<<<kRadix / 32, 1024, 0, st>>>(a, (uint32_t)chunks);
+    // (a.total is zero: the previous pass's downsweep cleared it, or it was just allocated)
+    launch_pdl(k_upsweep<ITEMS>, dim3((unsigned)chunks), dim3(kSortThreads), 0, st, a);
+    launch_pdl(k_chunk_scan, dim3(kRadix / 32), dim3(1024), 0, st, a, (uint32_t)chunks);
     const int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
     const uint64_t nfull = a.n / TILE;
     int nl = 2;
@@ -727,7 +756,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
             nl++;
         }
         if (aux.ws_begin) cudaEventRecord(aux.ws_begin, st);
-        k_downsweep_ws<SH><<<(unsigned)grid, SH::THREADS, smem, st>>>(w, (uint32_t)nfull);
+        launch_pdl(k_downsweep_ws<SH>, dim3((unsigned)grid), dim3(SH::THREADS), smem, st, w, (uint32_t)nfull);
         if (aux.ws_end) cudaEventRecord(aux.ws_end, st);
         // algorithmic bytes: every loaded stream read once, every stream written once
         if (aux.ws_bytes) *aux.ws_bytes = (double)nfull * TILE * 4.0 * (double)(streams + (int)a.nplanes + 1);
