@@ -305,7 +305,8 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
             aux.fork = ctx->aux_ev[0];
             aux.join = ctx->aux_ev[1];
             const int ke = ctx->nkev;
-            if (ctx->timing && ke < cks_ctx::kMaxKev) {
+            static const bool no_kev = getenv("CKS_NO_KERNEL_EVENTS") != nullptr;   // experiments only
+            if (ctx->timing && !no_kev && ke < cks_ctx::kMaxKev) {
                 aux.ws_begin = ctx->kev[2 * ke];
                 aux.ws_end = ctx->kev[2 * ke + 1];
                 ctx->kbytes[ke] = 0.0;
