@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(kSortThreads)
 k_upsweep(const LsdPassArgs a) {
     constexpr int TILE = kSortThreads * ITEMS;
     constexpr int V = ITEMS / 4;                              // uint4 loads per thread per tile
-    __shared__ uint32_t bins[kW][kRadix];
+    // cumulative per-warp bins, one set per tile parity: tile t's counts are bins[t&1] now
+    // minus bins[t&1] two tiles ago, so no per-tile clearing and one barrier per tile
+    __shared__ uint32_t bins[2][kW][kRadix];
     pdl_wait();
     pdl_trigger();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -117,25 +119,30 @@ k_upsweep(const LsdPassArgs a) {
     const uint32_t* src = a.digit_plane >= 0 ? a.in_planes + (uint64_t)a.digit_plane * a.in_pitch : a.in_rid;
     const uint32_t sel = a.shift >> 3;
     const bool vec = src && ((uintptr_t)src % 16 == 0);
-    uint32_t* hb = bins[warp];
-    uint32_t running = 0;
-    uint4 w[V];
-    auto load = [&](uint32_t t) {                            // full, aligned tiles only
+#pragma unroll
+    for (int p = 0; p < 2; p++)
+#pragma unroll
+        for (int k = 0; k < kW; k++) bins[p][k][tid] = 0;
+    __syncthreads();
+    uint32_t running = 0, prev[2] = {0u, 0u};
+    uint4 w[2][V];                                            // tiles t+1 and t+2 in flight
+    auto load = [&](uint32_t t, auto b) {                      // full, aligned tiles only
         const uint4* s4 = reinterpret_cast<const uint4*>(src + (uint64_t)t * TILE);
 #pragma unroll
-        for (int v = 0; v < V; v++) w[v] = __ldg(s4 + v * kSortThreads + tid);
+        for (int v = 0; v < V; v++) w[decltype(b)::value][v] = __ldg(s4 + v * kSortThreads + tid);
     };
-    auto is_fast = [&](uint32_t t) { return vec && (uint64_t)(t + 1) * TILE <= n; };
-    if (t0 < t1 && is_fast(t0)) load(t0);
-    for (uint32_t t = t0; t < t1; t++) {
-#pragma unroll
-        for (int j = lane; j < kRadix; j += 32) hb[j] = 0;
-        __syncwarp();
+    auto is_fast = [&](uint32_t t) { return vec && t < t1 && (uint64_t)(t + 1) * TILE <= n; };
+    if (is_fast(t0)) load(t0, std::integral_constant<int, 0>{});
+    if (is_fast(t0 + 1)) load(t0 + 1, std::integral_constant<int, 1>{});
+    // one tile; P (the buffer / bin parity) is a compile-time constant so w stays in registers
+    auto tile_step = [&](auto pc, uint32_t t) {
+        constexpr int P = decltype(pc)::value;
+        uint32_t* hb = bins[P][warp];
         if (is_fast(t)) {
             uint4 c[V];
 #pragma unroll
-            for (int v = 0; v < V; v++) c[v] = w[v];
-            if (t + 1 < t1 && is_fast(t + 1)) load(t + 1);    // next tile's words in flight
+            for (int v = 0; v < V; v++) c[v] = w[P][v];
+            if (is_fast(t + 2)) load(t + 2, pc);              // two tiles ahead
 #pragma unroll
             for (int v = 0; v < V; v++) {
                 atomicAdd(&hb[digit_of(c[v].x, sel)], 1u);
@@ -149,15 +156,18 @@ k_upsweep(const LsdPassArgs a) {
                 const uint64_t idx = tb + (uint64_t)i * kSortThreads + tid;
                 if (idx < n) atomicAdd(&hb[digit_of(src ? __ldg(src + idx) : (uint32_t)idx, sel)], 1u);
             }
-            if (t + 1 < t1 && is_fast(t + 1)) load(t + 1);
         }
         __syncthreads();
-        uint32_t cnt = 0;
+        uint32_t cum = 0;
 #pragma unroll
-        for (int k = 0; k < kW; k++) cnt += bins[k][tid];
+        for (int k = 0; k < kW; k++) cum += bins[P][k][tid];
         a.tile_off[(uint64_t)t * kRadix + tid] = running;
-        running += cnt;
-        __syncthreads();
+        running += cum - prev[P];
+        prev[P] = cum;
+    };
+    for (uint32_t t = t0; t < t1; t += 2) {
+        tile_step(std::integral_constant<int, 0>{}, t);
+        if (t + 1 < t1) tile_step(std::integral_constant<int, 1>{}, t + 1);
     }
     a.chunk_tot[(uint64_t)blockIdx.x * kRadix + tid] = running;
     if (running) atomicAdd(&a.total[tid], running);
