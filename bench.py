@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full-key", action="store_true", help="skip the full-key comparison (NEXT-2)")
+    ap.add_argument("--full-key-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3                                     # contract: W >= 3
@@ -300,6 +302,39 @@ def main():
                "timing": "host wall clock around cks_build_host (it synchronises), max over ranks"}
         assert np.array_equal(r["mask"], builder.mask)
 
+    # ---- NEXT-2: the same pipeline on the FULL key (M = all 8B bits, one LSD sort over them),
+    # the GPU analog of the paper's full-key build, and the paper's Table 2/6 statistics
+    paper_stats = None
+    if not args.no_full_key:
+        rid_bits = max(1, (n - 1).bit_length())
+        full_sort_key = 8 * ((B + 7) // 8) + 8                         # Table 2: key words + 8 B record id
+        comp_sort_key = 8 * ((d + rid_bits + 63) // 64)
+        paper_stats = {"full_key_bits": 8 * B, "d_bits": d, "compression_ratio": (8 * B / d) if d else None,
+                       "record_id_bits": rid_bits, "full_sort_key_bytes": full_sort_key,
+                       "compressed_sort_key_bytes": comp_sort_key,
+                       "sort_key_ratio": full_sort_key / comp_sort_key if comp_sort_key else None,
+                       "definitions": "P:523-526 (Table 2), P:559-563; total ratio as Table 6 (P:689-706)"}
+        cks.set_sort_mode(cks.SORT_SINGLE)
+        allbits = np.full(B, 0xFF, np.uint8)
+        full = cks.Builder(n, B, device, fanout=64, fill=1.0)
+        full(keys, prior_mask=allbits)
+        torch.cuda.synchronize(device)
+        fs = max(1, min(args.steps, args.full_key_steps))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(fs):
+            full(keys, prior_mask=allbits)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        cks.set_sort_mode(cks.SORT_PREFIX_AUTO)
+        fms = e0.elapsed_time(e1) / fs
+        assert np.array_equal(full.mask, builder.mask)                  # same exact D either way
+        paper_stats.update({"full_key_ms_per_step": fms, "full_key_passes": int(full.out.passes),
+                            "compressed_ms_per_step": ms, "total_ratio": fms / ms, "full_key_steps": fs,
+                            "full_key_keys_per_s": n / (fms * 1e-3)})
+        del full
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, c["name"], min(args.cpu_sample, n))
@@ -327,6 +362,7 @@ def main():
                               "achieved_gbs": path_gbs, "frac_of_peak": path_gbs / peak,
                               "frac_of_8tbs": path_gbs / 8000.0},
             "stages_ms": stages_ms,
+            "paper_stats": paper_stats,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,

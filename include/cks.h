@@ -74,6 +74,15 @@ int cks_ctx_destroy(cks_ctx* ctx);
 int cks_ctx_set_stream(cks_ctx* ctx, void* stream);
 /* 1 = record per-stage CUDA events in cks_build (read with cks_ctx_stage_ms). */
 int cks_ctx_set_timing(cks_ctx* ctx, int enable);
+/* How cks_build / cks_distinction_mask sort (the result is the same):
+ *   CKS_SORT_SINGLE       one stable LSD sort over all m = |M| bits of P_M;
+ *   CKS_SORT_PREFIX_AUTO  by distinguishing prefixes (NEXT-1) when m > 64 (default);
+ *   CKS_SORT_PREFIX       by distinguishing prefixes whenever m > 0.
+ * The environment variable CKS_REFINE (0/1/2) sets the initial mode of new contexts. */
+#define CKS_SORT_SINGLE 0
+#define CKS_SORT_PREFIX_AUTO 1
+#define CKS_SORT_PREFIX 2
+int cks_ctx_set_sort_mode(cks_ctx* ctx, int mode);
 /* Stage times (ms) of the last timed cks_build: a1 mask, a3 compress, a4 histograms+scan,
  * a5 LSD passes, a6 adjacency, a7 repack, a8 bulk load, total. Synchronises. Returns the
  * count written (0 if timing was off). */

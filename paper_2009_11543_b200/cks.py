@@ -55,7 +55,7 @@ class BuildOut(ctypes.Structure):
                 ("rounds", ctypes.c_uint32), ("reserved0", ctypes.c_uint32), ("refined_keys", ctypes.c_uint64)]
 
 
-EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing",
+EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing", "cks_ctx_set_sort_mode",
            "cks_ctx_stage_ms", "cks_ctx_launches", "cks_ctx_kernel_stats", "cks_strerror", "cks_last_error",
            "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
            "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_build", "cks_build_host"]
@@ -75,6 +75,7 @@ def load_library(path: str | None = None):
     L.cks_ctx_destroy.argtypes = [p]
     L.cks_ctx_set_stream.argtypes = [p, p]
     L.cks_ctx_set_timing.argtypes = [p, i32]
+    L.cks_ctx_set_sort_mode.argtypes = [p, i32]
     L.cks_ctx_stage_ms.argtypes = [p, ctypes.POINTER(f32), i32]
     L.cks_ctx_launches.argtypes = [p]
     L.cks_ctx_launches.restype = u64
@@ -155,6 +156,15 @@ def launches() -> int:
 def set_timing(enable: bool):
     L, c = _context()
     L.cks_ctx_set_timing(c, 1 if enable else 0)
+
+
+SORT_SINGLE, SORT_PREFIX_AUTO, SORT_PREFIX = 0, 1, 2
+
+
+def set_sort_mode(mode: int, device: int | None = None):
+    """CKS_SORT_SINGLE / CKS_SORT_PREFIX_AUTO (default) / CKS_SORT_PREFIX for later builds."""
+    L, c = _context(device)
+    _check(L, c, L.cks_ctx_set_sort_mode(c, int(mode)))
 
 
 def stage_ms() -> list[float]:

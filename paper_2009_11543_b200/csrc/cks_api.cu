@@ -810,6 +810,12 @@ int cks_ctx_set_timing(cks_ctx* ctx, int enable) {
     return CKS_OK;
 }
 
+int cks_ctx_set_sort_mode(cks_ctx* ctx, int mode) {
+    if (!ctx || mode < CKS_SORT_SINGLE || mode > CKS_SORT_PREFIX) return CKS_EINVAL;
+    ctx->refine = mode;
+    return CKS_OK;
+}
+
 int cks_ctx_stage_ms(cks_ctx* ctx, float* out, int max) {
     if (!ctx || !out) return 0;
     if (!ctx->timed) return 0;

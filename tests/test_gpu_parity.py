@@ -359,3 +359,41 @@ def test_refine_runs_of_equal_keys():
     keys = np.repeat(base, counts, axis=0)
     keys = keys[rng.permutation(keys.shape[0])]
     check_build(keys, cks.build(dev(keys)))
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_sort_modes_agree(cfg):
+    # single full-width sort, auto and forced prefix refinement: the same (key, row id) order,
+    # D, D_i and sorted P_D (Theorem 2 and stability), all equal to the oracle
+    keys = cksgen.config(cfg, n=60_001)
+    d = dev(keys)
+    res = {}
+    try:
+        for mode in (cks.SORT_SINGLE, cks.SORT_PREFIX_AUTO, cks.SORT_PREFIX):
+            cks.set_sort_mode(mode)
+            res[mode] = cks.build(d)
+    finally:
+        cks.set_sort_mode(cks.SORT_PREFIX_AUTO)
+    check_build(keys, res[cks.SORT_PREFIX_AUTO])
+    for mode in (cks.SORT_SINGLE, cks.SORT_PREFIX):
+        assert np.array_equal(res[mode]["mask"], res[cks.SORT_PREFIX_AUTO]["mask"])
+        assert np.array_equal(u32(res[mode]["perm"]), u32(res[cks.SORT_PREFIX_AUTO]["perm"]))
+        assert np.array_equal(u16(res[mode]["dbit"]), u16(res[cks.SORT_PREFIX_AUTO]["dbit"]))
+        assert np.array_equal(u32(res[mode]["packed"]), u32(res[cks.SORT_PREFIX_AUTO]["packed"]))
+
+
+def test_full_key_build():
+    # NEXT-2: the full-key pipeline (M = every key bit) reaches the same exact D and order
+    keys = cksgen.config(3, n=40_000)
+    try:
+        cks.set_sort_mode(cks.SORT_SINGLE)
+        r = cks.build(dev(keys), prior_mask=np.full(keys.shape[1], 0xFF, np.uint8))
+    finally:
+        cks.set_sort_mode(cks.SORT_PREFIX_AUTO)
+    assert r["sort_bits"] == 8 * keys.shape[1]
+    check_build(keys, r)
+
+
+def test_sort_mode_rejects():
+    with pytest.raises(cks.CksError):
+        cks.set_sort_mode(7)
