@@ -242,6 +242,7 @@ def main():
     torch.cuda.synchronize(device)
     m, d, passes = int(builder.out.sort_bits), int(builder.out.popcount), int(builder.out.passes)
     rounds, refined = int(builder.out.rounds), int(builder.out.refined_keys)
+    round0_bits = int(builder.out.round0_bits)
 
     # ---- timed region: K fused builds, inputs resident in HBM (keys > 126 MB L2 for cfg2-5)
     cks.set_timing(True)
@@ -346,7 +347,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": c["name"], "n": n, "key_bytes": B, "fanout": 64, "fill": 1.0,
                        "superset": "byteocc D+", "sort_bits": m, "d_bits": d, "lsd_passes": passes,
-                       "refine_rounds": rounds, "refined_keys": refined,
+                       "refine_rounds": rounds, "refined_keys": refined, "round0_bits": round0_bits,
                        "sort": "by distinguishing prefixes (NEXT-1)" if rounds else "single LSD sort",
                        "parallelism": f"replicas{world}" if world > 1 else "single",
                        "l2": f"inputs larger than L2 (keys {n * B / 1e6:.0f} MB vs 126 MB), no flush"},

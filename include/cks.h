@@ -208,7 +208,7 @@ typedef struct {
     const uint32_t* packed;   /* VIEW (ctx-owned): sorted P_D planes; plane q at packed + q*packed_pitch */
     uint64_t packed_pitch;    /* plane stride of `packed` in u32 elements (>= n, padded for alignment) */
     uint32_t rounds;          /* prefix-refinement rounds run (0 = plain single sort) */
-    uint32_t reserved0;
+    uint32_t round0_bits;     /* width of the first refinement round (top bits of P_M) */
     uint64_t refined_keys;    /* keys re-sorted in rounds >= 1 (summed over rounds) */
 } cks_build_out;
 

@@ -52,7 +52,7 @@ class BuildOut(ctypes.Structure):
                 ("superset_kind", ctypes.c_int), ("popcount", ctypes.c_uint32),
                 ("sort_bits", ctypes.c_uint32), ("height", ctypes.c_uint32), ("passes", ctypes.c_uint32),
                 ("packed", ctypes.c_void_p), ("packed_pitch", ctypes.c_uint64),
-                ("rounds", ctypes.c_uint32), ("reserved0", ctypes.c_uint32), ("refined_keys", ctypes.c_uint64)]
+                ("rounds", ctypes.c_uint32), ("round0_bits", ctypes.c_uint32), ("refined_keys", ctypes.c_uint64)]
 
 
 EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing", "cks_ctx_set_sort_mode",

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "../../include/cks.h"
@@ -396,7 +397,7 @@ static void repack_words(const uint8_t* M, const uint8_t* D, uint32_t B, uint32_
 // exact D (out->mask) and P_D in sorted order (out->packed).
 int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* M, uint32_t m,
                  cks_build_out* out, uint16_t* dbit) {
-    const uint32_t np = (m + 31) / 32, nch = (np + 1) / 2, lead = 32 * np - m;
+    const uint32_t np = (m + 31) / 32, lead = 32 * np - m;
     const uint64_t sp = scratch_pitch(n);
     const uint32_t nwords = (8 * B + 31) / 32;
     // a3: P_M left-aligned (the first mask position is bit 31 of the top plane), so chunk r
@@ -405,6 +406,27 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     uint32_t* pm = as<uint32_t>(ctx->pm);
     TRY(run_compress(ctx, keys, n, B, M, pm, sp, lead));
     mark(ctx, ST_COMPRESS);
+    // width T of round 0: the narrowest multiple of 8 bits that separates a strided sample of
+    // the keys as well as the full 64-bit chunk does (fewer round-0 passes; whatever still ties
+    // is finished by the later rounds -- the result is exact for any T). CKS_ROUND0_BITS forces.
+    uint32_t T = 64;
+    {
+        static int forced = -2;
+        if (forced == -2) { const char* e = getenv("CKS_ROUND0_BITS"); forced = e ? atoi(e) : 0; }
+        if (forced > 0 && forced <= 64 && (forced & 7) == 0) {
+            T = (uint32_t)forced;
+        } else if (np >= 2 && n >= (1u << 16)) {
+            TRY(ensure(ctx, ctx->rtot, 64));
+            uint32_t* cnt = as<uint32_t>(ctx->rtot) + 4;
+            LAUNCH(launch_prefix_sample(pm + (uint64_t)(np - 1) * sp, pm + (uint64_t)(np - 2) * sp, n, 16384, cnt,
+                                        ctx->stream));
+            CK(cudaMemcpyAsync(ctx->h_tot, cnt, 32, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            for (uint32_t w = 0; w < 8; w++)
+                if (ctx->h_tot[w] == ctx->h_tot[7]) { T = 8 * (w + 1); break; }
+        }
+        if (T > m) T = (m + 7) & ~7u;
+    }
     mark(ctx, ST_HIST);
     TRY(upload_moff(ctx, M, B, m));
     TRY(ensure(ctx, ctx->dacc, (size_t)nwords * 4));
@@ -420,7 +442,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     // that reorder runs move its planes too).
     const bool carry = np == 3;
     const uint32_t np0 = carry ? 3 : (np >= 2 ? 2 : 1);
-    const uint32_t dig0 = carry ? 4 : (np <= 2 ? lead / 8 : 0);
+    // round 0 sorts the top T bits of chunk 0 (the digits below them are skipped)
+    const uint32_t dig0 = np <= 2 ? (lead / 8 > 4 * np0 - T / 8 ? lead / 8 : 4 * np0 - T / 8) : 4 * np0 - T / 8;
     const uint32_t* sorted0 = nullptr;
     uint64_t sp0 = sp;
     uint32_t* carried = nullptr;
@@ -431,7 +454,9 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     TRY(run_sort(ctx, pm + (uint64_t)(np - np0) * sp, sp, np0, 4 * np0, n, nullptr, 0, carried, sp, out->perm,
                  &sorted0, &sp0, dig0, false));
     LAUNCH(launch_ref_adj(np0 >= 2 ? sorted0 + (uint64_t)(np0 - 2) * sp0 : nullptr, sorted0 + (uint64_t)(np0 - 1) * sp0,
-                          nullptr, nullptr, n, 0, moff, m, B, dbit, tie, dacc, true, ctx->sms, ctx->stream));
+                          nullptr, nullptr, n, 0, moff, m, B, dbit, tie, dacc, true, ctx->sms, ctx->stream,
+                          ~0ull << (64 - T)));
+    out->round0_bits = T;
     out->rounds = 1;
     out->refined_keys = 0;
     out->passes = 4 * np0 - dig0;
@@ -439,7 +464,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     // comparing their remaining bits; the others are re-sorted by (run, chunk r).
     uint64_t nr = n;
     const uint32_t* pos = nullptr;                               // list of round r-1 (null: all keys)
-    if (nch > 1) {
+    if (T < m) {
         DevBuf* pb[3] = {&ctx->posA, &ctx->posB, &ctx->posC};
         DevBuf* sb[3] = {&ctx->segA, &ctx->segB, &ctx->segC};
         for (int i = 0; i < 3; i++) {
@@ -451,7 +476,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         TRY(ensure(ctx, ctx->done, n + 16));
         TRY(ensure(ctx, ctx->mlist, sp * 4));
         TRY(ensure(ctx, ctx->rcnt, (size_t)(ref_tiles(n) + 1) * 8));
-        TRY(ensure(ctx, ctx->rtot, 16));
+        TRY(ensure(ctx, ctx->rtot, 64));
     }
     auto counts = [&](uint64_t* a, uint64_t* b) -> int {
         CK(cudaMemcpyAsync(ctx->h_tot, ctx->rtot.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -462,7 +487,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     };
     const bool log = getenv("CKS_REFINE_LOG") != nullptr;
     int li = -1;                                                 // buffer of the current list
-    for (uint32_t r = 1; r < nch; r++) {
+    for (uint32_t r = 1; T + 64 * (r - 1) < m; r++) {
+        const uint32_t o = T + 64 * (r - 1);                     // first P_M bit of this round's chunk
         const int ai = li == 0 ? 1 : 0;                          // (1)'s output
         const int bi = li < 0 ? 1 : 3 - li - ai;                 // (3)'s output, the next list
         uint32_t* posA_ = as<uint32_t>(ai == 0 ? ctx->posA : ai == 1 ? ctx->posB : ctx->posC);
@@ -476,10 +502,11 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         TRY(counts(&nn, &nseg));
         if (nn == 0) break;
         // (2) finish short runs and runs of equal keys in place
-        const int qtop = (int)np - 1 - 2 * (int)r;
+        const int qtop = (int)np - 1 - (int)(o >> 5);            // plane holding bit o
         LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, posA_, segA_, as<uint32_t>(ctx->runoff), nseg, nn, out->perm,
                                 dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B,
-                                as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->rtot) + 2, ctx->sms, ctx->stream));
+                                as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->rtot) + 2, ctx->sms, ctx->stream,
+                                0xFFFFFFFFu >> (o & 31)));
         // (3) the runs left for an LSD round (none: done)
         CK(cudaMemcpyAsync(ctx->h_tot, as<uint32_t>(ctx->rtot) + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -499,17 +526,14 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         if (n2 == 0) break;
         out->rounds = r + 1;
         // (4) LSD round: the left runs by (run, chunk r)
-        const int qhi = (int)np - 1 - 2 * (int)r, qlo = (int)np - 2 - 2 * (int)r;
         const uint64_t cp = scratch_pitch(n2);
         TRY(ensure(ctx, ctx->cmp, (size_t)3 * cp * 4));
         TRY(ensure(ctx, ctx->crid, cp * 4));
         TRY(ensure(ctx, ctx->crid2, cp * 4));
-        LAUNCH(launch_ref_gather(pm, sp, qhi, qlo, posB_, segB_, out->perm, n2, as<uint32_t>(ctx->cmp), cp,
+        LAUNCH(launch_ref_gather(pm, sp, np, o, posB_, segB_, out->perm, n2, as<uint32_t>(ctx->cmp), cp,
                                  as<uint32_t>(ctx->crid), ctx->sms, ctx->stream));
         const uint32_t segbits = nseg2 > 1 ? 32u - (uint32_t)__builtin_clz((uint32_t)(nseg2 - 1)) : 0u;
-        uint32_t d0 = 0;
-        if (qlo < 0) d0 = 4 + lead / 8;                  // single-plane chunk: high word = plane 0
-        else if (qlo == 0) d0 = lead / 8;                // low word = plane 0 holds the padding
+        const uint32_t d0 = o + 64 > m ? (o + 64 - m) / 8 : 0;   // digits past the last mask bit are zero
         const uint32_t* sv = nullptr;
         uint64_t svp = cp;
         out->passes += 8 + (segbits + 7) / 8 - d0;
@@ -517,8 +541,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
                      nullptr, 0, as<uint32_t>(ctx->crid2), &sv, &svp, d0, false));
         LAUNCH(launch_ref_put(out->perm, posB_, as<uint32_t>(ctx->crid2), n2, pm, sp, np, carried, ctx->sms,
                               ctx->stream));
-        LAUNCH(launch_ref_adj(qlo >= 0 ? sv : nullptr, sv + svp, sv + 2 * svp, posB_, n2, 64 * r, moff, m, B, dbit,
-                              tie, dacc, false, ctx->sms, ctx->stream));
+        LAUNCH(launch_ref_adj(sv, sv + svp, sv + 2 * svp, posB_, n2, o, moff, m, B, dbit, tie, dacc, false, ctx->sms,
+                              ctx->stream));
         pos = posB_;
         nr = n2;
         li = bi;
@@ -538,10 +562,11 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     if (out->popcount > 0) {
         if (!carry) TRY(ensure(ctx, ctx->pd, (size_t)npd * sp * 4));
         uint32_t* pd = carry ? pm : as<uint32_t>(ctx->pd);       // (P_M in row order is no longer needed)
-        if ((nch == 1 || carry) && lead == 0 && same_mask(out->mask, M, B)) {
+        const bool single = T >= m;                               // round 0 sorted all of P_M
+        if ((single || carry) && lead == 0 && same_mask(out->mask, M, B)) {
             out->packed = sorted0;
             out->packed_pitch = sp0;
-        } else if (nch == 1 || carry) {
+        } else if (single || carry) {
             std::vector<uint32_t> sub(np, 0);
             repack_words(M, out->mask, B, m, lead, sub);
             TRY(claim_slot(ctx, 1));
@@ -635,6 +660,7 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     out->passes = k;
     out->rounds = 0;
     out->refined_keys = 0;
+    out->round0_bits = 0;
     uint16_t* dbit = out->dbit;
     if (!dbit && n) {
         TRY(ensure(ctx, ctx->dbit, n * 2));

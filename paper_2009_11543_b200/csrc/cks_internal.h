@@ -33,6 +33,10 @@ struct GatherPlan {
     GatherStep step[kMaxWords > kMaxPlanes ? kMaxWords : kMaxPlanes];
 };
 
+// Raise a kernel's dynamic shared-memory limit on the current device to at least `bytes`.
+// Never lowers it: one record per (device, kernel) shared by every launch site (cks_plan.cpp).
+cudaError_t raise_smem_limit(const void* kernel, size_t bytes);
+
 // Host-side planning (cks_plan.cpp).
 void plan_compress(const uint8_t* mask, uint32_t key_bytes, GatherPlan* plan);
 void plan_repack(const uint32_t* sub_words /* u32[np_in], bit b of word q = P_M bit 32q+b kept */,
@@ -43,6 +47,11 @@ cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32
                              int sms, cudaStream_t st);
 cudaError_t launch_occ_finalize(const uint32_t* occ, uint32_t B, uint64_t n, uint8_t* dplus,
                                 uint8_t* variant, cudaStream_t st);
+// First-round width of the refinement: sorts a strided sample of `samples` (power of two,
+// <= 16384) top-64-bit prefixes of P_M (planes hi / lo, lo may be NULL) in one CTA and writes
+// counts[w] = distinct prefixes of the top 8(w+1) bits, w = 0..7.
+cudaError_t launch_prefix_sample(const uint32_t* hi, const uint32_t* lo, uint64_t n, uint32_t samples,
+                                 uint32_t* counts, cudaStream_t st);
 // Planes are u32 SoA arrays: plane q of a packed array starts at ptr + q*pitch (pitch in
 // elements; user buffers have pitch n, library scratch pads the pitch to 32 elements so every
 // plane is 128-byte aligned for TMA).
@@ -126,17 +135,18 @@ cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
 uint64_t ref_tiles(uint64_t nr);
 cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_t* seg, const uint32_t* pos,
                            uint64_t nr, uint32_t cbase, const uint16_t* moff, uint32_t m, uint32_t B,
-                           uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st);
+                           uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st,
+                           unsigned long long cmask = ~0ull);
 cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* pos, uint32_t* cnt, uint32_t* tot,
                                uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, cudaStream_t st);
 cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
                              const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
                              uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* mcount, int sms,
-                             cudaStream_t st);
+                             cudaStream_t st, uint32_t fmask);
 cudaError_t launch_ref_keep(const uint32_t* seg, const uint32_t* run_off, const uint8_t* done, uint64_t nn,
                             uint8_t* keep, int sms, cudaStream_t st);
-cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, int qhi, int qlo, const uint32_t* pos,
+cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, uint32_t np, uint32_t o, const uint32_t* pos,
                               const uint32_t* seg, const uint32_t* perm, uint64_t nr, uint32_t* out, uint64_t opitch,
                               uint32_t* orid, int sms, cudaStream_t st);
 cudaError_t launch_ref_put(uint32_t* perm, const uint32_t* pos, const uint32_t* rid, uint64_t nr, const uint32_t* pm,

@@ -7,9 +7,26 @@
 // low popcount(mask) bits -- what PEXT does in hardware.
 #include <string.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "cks_internal.h"
 
 namespace cks {
+
+cudaError_t raise_smem_limit(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> limit;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    size_t& cur = limit[{dev, kernel}];
+    if (bytes <= cur) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
+}
 
 static void move_masks(uint32_t m, uint32_t mv[5]) {
     uint32_t mk = ~m << 1;                 // count unselected positions to the right

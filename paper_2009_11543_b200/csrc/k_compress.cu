@@ -275,8 +275,7 @@ cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const G
     if ((B & 15) == 0 && ((uintptr_t)keys & 15) == 0 && !rows) {
         uint32_t S16 = (B >> 4) | 1;
         size_t smem = (size_t)kCompressThreads * S16 * 16;
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_compress_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        raise_smem_limit((const void*)k_compress_tiled, smem);
         int per_sm = smem <= 24 * 1024 ? 8 : smem <= 48 * 1024 ? 4 : smem <= 100 * 1024 ? 2 : 1;
         k_compress_tiled<<<grid_for(n, per_sm, sms), kCompressThreads, smem, st>>>(keys, n, B, dplan, nsteps,
                                                                                    np, planes, pitch, lead);

@@ -739,11 +739,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
         LsdPassArgs w = a;
         w.slots = (uint32_t)R;
         const size_t smem = (size_t)(kDigitSlots + R) * TILE * 4 + fixed;
-        static size_t configured_ws = 0;
-        if (smem > configured_ws) {
-            cudaFuncSetAttribute(k_downsweep_ws<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured_ws = smem;
-        }
+        raise_smem_limit((const void*)k_downsweep_ws<SH>, smem);
         const uint64_t gmax = (uint64_t)sms * SH::MINB;
         const uint64_t grid = nfull < gmax ? nfull : gmax;
         const bool tail = nfull != tiles;
@@ -754,11 +750,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
             tl.tile_begin = (uint32_t)nfull;
             if ((int)tl.slots > 2 * streams) tl.slots = streams > 0 ? 2 * streams : 1;
             const size_t tsm = (size_t)tl.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 2;
-            static size_t configured_t = 0;
-            if (tsm > configured_t) {
-                cudaFuncSetAttribute(k_downsweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-                configured_t = tsm;
-            }
+            raise_smem_limit((const void*)k_downsweep<ITEMS>, tsm);
             cudaEventRecord(aux.fork, st);
             cudaStreamWaitEvent(aux.stream, aux.fork, 0);
             k_downsweep<ITEMS><<<1, kSortThreads, tsm, aux.stream>>>(tl);
@@ -777,11 +769,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
     }
     if ((int)a.slots > 2 * streams) a.slots = streams > 0 ? 2 * streams : 1;
     size_t smem = (size_t)a.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 2;
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaFuncSetAttribute(k_downsweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
+    raise_smem_limit((const void*)k_downsweep<ITEMS>, smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_downsweep<ITEMS>, kSortThreads, smem);
     if (per_sm < 1) per_sm = 1;

@@ -196,8 +196,7 @@ cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32
     } else {
         uint64_t want = (n + 255) / 256;
         int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_occupancy_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        raise_smem_limit((const void*)k_occupancy_generic, smem);
         k_occupancy_generic<<<grid, 256, smem, st>>>(keys, n, B, occ);
     }
     return cudaGetLastError();

@@ -40,12 +40,13 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane) {
 }  // namespace
 
 // Round adjacency over a sorted list of nr chunks (lo may be NULL: single-plane chunk;
-// seg NULL: one segment; pos NULL: element k sits at global position k).
+// seg NULL: one segment; pos NULL: element k sits at global position k). Only the chunk bits
+// in cmask are compared (round 0 sorts by the top T <= 64 bits).
 __global__ void __launch_bounds__(kRefThreads)
 k_ref_adj(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, const uint32_t* __restrict__ seg,
           const uint32_t* __restrict__ pos, uint64_t nr, uint32_t cbase, const uint16_t* __restrict__ moff,
           uint32_t m, uint32_t nwords, uint16_t* __restrict__ dbit, uint8_t* __restrict__ tie,
-          uint32_t* __restrict__ dacc, int round0) {
+          uint32_t* __restrict__ dacc, int round0, unsigned long long cmask) {
     extern __shared__ uint32_t s_dyn[];
     uint32_t* s_bm = s_dyn;                                          // [nwords]
     uint16_t* s_moff = reinterpret_cast<uint16_t*>(s_dyn + nwords);  // [m]
@@ -58,8 +59,8 @@ k_ref_adj(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, cons
         if (k == 0) {
             if (round0) dbit[g] = CKS_NONE_INTERNAL;
         } else if (!seg || seg[k] == seg[k - 1]) {
-            const unsigned long long x = ((unsigned long long)(hi[k] ^ hi[k - 1]) << 32) |
-                                         (lo ? (unsigned long long)(lo[k] ^ lo[k - 1]) : 0ull);
+            const unsigned long long x = (((unsigned long long)(hi[k] ^ hi[k - 1]) << 32) |
+                                          (lo ? (unsigned long long)(lo[k] ^ lo[k - 1]) : 0ull)) & cmask;
             if (x) {
                 const uint32_t d = s_moff[cbase + (uint32_t)__clzll((long long)x)];
                 dbit[g] = (uint16_t)d;
@@ -188,15 +189,25 @@ k_ref_scatter(const uint8_t* __restrict__ tie, uint64_t nr, const uint32_t* __re
     }
 }
 
-// chunk r (hi = plane qhi, lo = plane qlo or none) of the listed rows, plus run and row id
+// 64 bits of P_M starting at bit o (counted from its most significant bit; left-aligned planes)
+// of the listed rows -- hi = bits [o, o+32), lo = bits [o+32, o+64) -- plus run and row id
+__device__ __forceinline__ uint32_t pm_bits32(const uint32_t* pm, uint64_t pitch, uint32_t np, uint32_t o,
+                                              uint32_t row) {
+    const int q = (int)np - 1 - (int)(o >> 5);
+    const uint32_t sh = o & 31;
+    const uint32_t a = q >= 0 ? __ldg(pm + (uint64_t)q * pitch + row) : 0u;
+    const uint32_t b = (sh && q >= 1) ? __ldg(pm + (uint64_t)(q - 1) * pitch + row) : 0u;
+    return sh ? __funnelshift_l(b, a, sh) : a;
+}
+
 __global__ void __launch_bounds__(kRefThreads)
-k_ref_gather(const uint32_t* __restrict__ pm, uint64_t pitch, int qhi, int qlo, const uint32_t* __restrict__ pos,
+k_ref_gather(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, uint32_t o, const uint32_t* __restrict__ pos,
              const uint32_t* __restrict__ seg, const uint32_t* __restrict__ perm, uint64_t nr,
              uint32_t* __restrict__ out, uint64_t opitch, uint32_t* __restrict__ orid) {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t row = perm[pos[k]];
-        out[k] = qlo >= 0 ? __ldg(pm + (uint64_t)qlo * pitch + row) : 0u;
-        out[opitch + k] = __ldg(pm + (uint64_t)qhi * pitch + row);
+        out[k] = pm_bits32(pm, pitch, np, o + 32, row);
+        out[opitch + k] = pm_bits32(pm, pitch, np, o, row);
         out[2 * opitch + k] = seg[k];
         orid[k] = row;
     }
@@ -211,6 +222,7 @@ k_ref_gather(const uint32_t* __restrict__ pm, uint64_t pitch, int qhi, int qlo, 
 // (duplicates). Every other run is flagged for the next LSD round (keep[k] = 1 for its
 // members but the first: the compaction's tie convention).
 constexpr uint32_t kLocal = 16;
+constexpr int kCarryWords = 3;                   // remaining words held in registers (carried path)
 constexpr uint32_t kCta = 2048;                  // medium runs: one CTA, bitonic sort in shared memory
 constexpr uint32_t kCtaWords = 8;                // ... if at most this many P_M planes remain (measured:
                                                  // with 10 remaining planes, cfg4, gathering them by row
@@ -220,7 +232,7 @@ k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qt
             const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
             uint32_t* __restrict__ perm, uint16_t* __restrict__ dbit, uint32_t* __restrict__ dacc,
             uint8_t* __restrict__ done, uint32_t* __restrict__ carried, uint32_t nwords, uint32_t* __restrict__ mlist,
-            uint32_t* __restrict__ mcount, uint32_t cta_max) {
+            uint32_t* __restrict__ mcount, uint32_t cta_max, uint32_t fmask) {
     __shared__ uint32_t s_bm[kMaxBits / 32];                         // D bits found by this block
     for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
     __syncthreads();
@@ -236,7 +248,8 @@ k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qt
         // -1: a < b, 1: a > b, 0: equal remaining bits; *t = first differing compressed index
         auto cmp = [&](uint32_t a, uint32_t b, uint32_t* t) -> int {
             for (int q = qtop; q >= 0; q--) {
-                const uint32_t wa = __ldg(pm + (uint64_t)q * pitch + a), wb = __ldg(pm + (uint64_t)q * pitch + b);
+                const uint32_t mq = q == qtop ? fmask : 0xFFFFFFFFu;
+                const uint32_t wa = __ldg(pm + (uint64_t)q * pitch + a) & mq, wb = __ldg(pm + (uint64_t)q * pitch + b) & mq;
                 if (wa != wb) {
                     if (t) *t = 32u * (np - 1 - (uint32_t)q) + (uint32_t)__clz(wa ^ wb);
                     return wa < wb ? -1 : 1;
@@ -244,30 +257,57 @@ k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qt
             }
             return 0;
         };
-        if (carried && L <= kLocal) {
-            // P_M is carried in sorted order and the remainder is its plane 0 (qtop == 0): sort the
-            // run's (plane-0 word, row id) pairs read at its contiguous positions, no row gathers
-            uint32_t rows[kLocal], w[kLocal];
-            for (uint32_t j = 0; j < L; j++) { rows[j] = perm[p0 + j]; w[j] = carried[p0 + j]; }
+        if (carried && L <= kLocal && qtop < (int)kCarryWords) {
+            // P_M is carried in sorted order and at most kCarryWords planes remain: sort the run's
+            // (remaining words, row id) read at its contiguous positions, no row gathers
+            constexpr int CW = kCarryWords;
+            uint32_t rows[kLocal], w[kLocal][CW];
+            for (uint32_t j = 0; j < L; j++) {
+                rows[j] = perm[p0 + j];
+#pragma unroll
+                for (int c = 0; c < CW; c++)
+                    w[j][c] = c <= qtop ? carried[(uint64_t)(qtop - c) * pitch + p0 + j] & (c == 0 ? fmask : ~0u) : 0u;
+            }
+            auto lt = [&](const uint32_t* x, uint32_t rx, const uint32_t* y, uint32_t ry) -> bool {
+#pragma unroll
+                for (int c = 0; c < CW; c++)
+                    if (x[c] != y[c]) return x[c] < y[c];
+                return rx < ry;
+            };
             for (uint32_t j = 1; j < L; j++) {
-                const uint32_t x = rows[j], y = w[j];
+                uint32_t x[CW];
+#pragma unroll
+                for (int c = 0; c < CW; c++) x[c] = w[j][c];
+                const uint32_t rx = rows[j];
                 uint32_t i = j;
-                while (i > 0 && (w[i - 1] > y || (w[i - 1] == y && rows[i - 1] > x))) {
+                while (i > 0 && lt(x, rx, w[i - 1], rows[i - 1])) {
                     rows[i] = rows[i - 1];
-                    w[i] = w[i - 1];
+#pragma unroll
+                    for (int c = 0; c < CW; c++) w[i][c] = w[i - 1][c];
                     i--;
                 }
-                rows[i] = x;
-                w[i] = y;
+                rows[i] = rx;
+#pragma unroll
+                for (int c = 0; c < CW; c++) w[i][c] = x[c];
             }
             for (uint32_t j = 0; j < L; j++) {
                 perm[p0 + j] = rows[j];
-                carried[p0 + j] = w[j];
-                if (j == 0 || w[j] == w[j - 1]) continue;
-                const uint32_t d = moff[32u * (np - 1) + (uint32_t)__clz(w[j] ^ w[j - 1])];
-                dbit[p0 + j] = (uint16_t)d;
-                const uint32_t b = 0x80000000u >> (d & 31);
-                if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
+                for (int c = 0; c <= qtop; c++) {                 // (masked-off bits of word 0 tie: keep them)
+                    uint64_t at = (uint64_t)(qtop - c) * pitch + p0 + j;
+                    carried[at] = c == 0 ? (carried[at] & ~fmask) | w[j][0] : w[j][c];
+                }
+                if (j == 0) continue;
+#pragma unroll
+                for (int c = 0; c < CW; c++) {
+                    const uint32_t x = w[j][c] ^ w[j - 1][c];
+                    if (x) {
+                        const uint32_t d = moff[32u * (np - 1 - (uint32_t)(qtop - c)) + (uint32_t)__clz(x)];
+                        dbit[p0 + j] = (uint16_t)d;
+                        const uint32_t b = 0x80000000u >> (d & 31);
+                        if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
+                        break;
+                    }
+                }
             }
         } else if (L <= kLocal) {
             uint32_t rows[kLocal];
@@ -319,7 +359,7 @@ k_ref_cta(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop
           const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
           uint32_t* __restrict__ perm, uint16_t* __restrict__ dbit, uint32_t* __restrict__ dacc,
           uint32_t* __restrict__ carried, uint32_t nwords, const uint32_t* __restrict__ mlist,
-          const uint32_t* __restrict__ mcount) {
+          const uint32_t* __restrict__ mcount, uint32_t fmask) {
     extern __shared__ uint32_t s_dyn[];
     uint32_t* s_rid = s_dyn;                                         // [kCta]
     uint32_t* s_kw = s_rid + kCta;                                   // [Wr][kCta], word 0 = plane qtop
@@ -341,8 +381,9 @@ k_ref_cta(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop
             const uint32_t row = perm[p0 + j];
             s_rid[j] = row;
             for (uint32_t q = 0; q < Wr; q++)
-                s_kw[q * kCta + j] = carried ? carried[(uint64_t)(qtop - (int)q) * pitch + p0 + j]
-                                             : __ldg(pm + (uint64_t)(qtop - (int)q) * pitch + row);
+                s_kw[q * kCta + j] = (carried ? carried[(uint64_t)(qtop - (int)q) * pitch + p0 + j]
+                                              : __ldg(pm + (uint64_t)(qtop - (int)q) * pitch + row)) &
+                                     (q == 0 ? fmask : 0xFFFFFFFFu);
         }
         for (uint32_t j = threadIdx.x; j < P2; j += blockDim.x) s_idx[j] = (uint16_t)j;
         __syncthreads();
@@ -368,8 +409,12 @@ k_ref_cta(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop
         for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) {
             const uint32_t a = s_idx[j];
             perm[p0 + j] = s_rid[a];
-            if (carried)
-                for (uint32_t q = 0; q < Wr; q++) carried[(uint64_t)(qtop - (int)q) * pitch + p0 + j] = s_kw[q * kCta + a];
+            if (carried) {                                      // reorder the carried planes too
+                for (uint32_t q = 0; q < Wr; q++) {
+                    const uint64_t at = (uint64_t)(qtop - (int)q) * pitch + p0 + j;
+                    carried[at] = q == 0 ? (carried[at] & ~fmask) | s_kw[a] : s_kw[q * kCta + a];
+                }
+            }
             if (j == 0) continue;
             const uint32_t b = s_idx[j - 1];
             for (uint32_t q = 0; q < Wr; q++) {
@@ -438,12 +483,13 @@ uint64_t ref_tiles(uint64_t nr) { return (nr + kRefTile - 1) / kRefTile; }
 
 cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_t* seg, const uint32_t* pos,
                            uint64_t nr, uint32_t cbase, const uint16_t* moff, uint32_t m, uint32_t B,
-                           uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st) {
+                           uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st,
+                           unsigned long long cmask) {
     if (nr == 0) return cudaSuccess;
     const uint32_t nwords = (8 * B + 31) / 32;
     const size_t smem = (size_t)nwords * 4 + (size_t)m * 2 + 16;
     k_ref_adj<<<grid_of(nr, sms), kRefThreads, smem, st>>>(lo, hi, seg, pos, nr, cbase, moff, m, nwords, dbit, tie,
-                                                           dacc, round0 ? 1 : 0);
+                                                           dacc, round0 ? 1 : 0, cmask);
     return cudaGetLastError();
 }
 
@@ -461,22 +507,19 @@ cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, in
                              const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
                              uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* mcount, int sms,
-                             cudaStream_t st) {
+                             cudaStream_t st, uint32_t fmask) {
     if (nseg == 0) return cudaMemsetAsync(mcount, 0, 8, st);
     const uint32_t nwords = (8 * B + 31) / 32;
     cudaMemsetAsync(mcount, 0, 8, st);                           // medium runs, long runs
     k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn, perm,
                                                             dbit, dacc, done, carried, nwords, mlist, mcount,
-                                                            cta_max());
+                                                            cta_max(), fmask);
     if (qtop + 1 <= (int)kCtaWords) {
         const size_t smem = (size_t)kCta * 4 * (qtop + 2) + (size_t)kCta * 2;
-        static size_t configured = 0;
-        if (smem > configured) {
-            cudaFuncSetAttribute(k_ref_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured = smem;
-        }
+        raise_smem_limit((const void*)k_ref_cta, smem);
         k_ref_cta<<<(unsigned)(sms * 4), kRefThreads, smem, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn,
-                                                                  perm, dbit, dacc, carried, nwords, mlist, mcount);
+                                                                  perm, dbit, dacc, carried, nwords, mlist, mcount,
+                                                                  fmask);
     }
     return cudaGetLastError();
 }
@@ -488,11 +531,11 @@ cudaError_t launch_ref_keep(const uint32_t* seg, const uint32_t* run_off, const 
     return cudaGetLastError();
 }
 
-cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, int qhi, int qlo, const uint32_t* pos,
+cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, uint32_t np, uint32_t o, const uint32_t* pos,
                               const uint32_t* seg, const uint32_t* perm, uint64_t nr, uint32_t* out, uint64_t opitch,
                               uint32_t* orid, int sms, cudaStream_t st) {
     if (nr == 0) return cudaSuccess;
-    k_ref_gather<<<grid_of(nr, sms), kRefThreads, 0, st>>>(pm, pitch, qhi, qlo, pos, seg, perm, nr, out, opitch, orid);
+    k_ref_gather<<<grid_of(nr, sms), kRefThreads, 0, st>>>(pm, pitch, np, o, pos, seg, perm, nr, out, opitch, orid);
     return cudaGetLastError();
 }
 
@@ -500,6 +543,57 @@ cudaError_t launch_ref_put(uint32_t* perm, const uint32_t* pos, const uint32_t* 
                            uint64_t pitch, uint32_t np, uint32_t* carried, int sms, cudaStream_t st) {
     if (nr == 0) return cudaSuccess;
     k_ref_put<<<grid_of(nr, sms), kRefThreads, 0, st>>>(perm, pos, rid, nr, pm, pitch, np, carried);
+    return cudaGetLastError();
+}
+
+}  // namespace cks
+
+namespace cks {
+
+// One CTA: a strided sample of top-64-bit prefixes of P_M is bitonic-sorted in shared memory,
+// then the number of distinct prefixes of the top 8, 16, ..., 64 bits is counted.
+__global__ void __launch_bounds__(1024)
+k_prefix_sample(const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo, uint64_t n, uint32_t S,
+                uint32_t* __restrict__ counts) {
+    extern __shared__ unsigned long long s_v[];                     // [S]
+    __shared__ uint32_t s_cnt[8];
+    if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+    for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) {
+        const uint64_t row = (uint64_t)i * n / S;
+        s_v[i] = ((unsigned long long)hi[row] << 32) | (lo ? lo[row] : 0u);
+    }
+    __syncthreads();
+    for (uint32_t size = 2; size <= S; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < S / 2; i += blockDim.x) {
+                const uint32_t a = 2 * i - (i & (stride - 1)), b = a + stride;
+                const bool up = (a & size) == 0;
+                const unsigned long long x = s_v[a], y = s_v[b];
+                if ((x > y) == up) { s_v[a] = y; s_v[b] = x; }
+            }
+            __syncthreads();
+        }
+    }
+    uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) {
+        const unsigned long long d = i ? s_v[i] ^ s_v[i - 1] : ~0ull;
+#pragma unroll
+        for (int w = 0; w < 8; w++) c[w] += (d >> (56 - 8 * w)) != 0;   // differs in the top 8(w+1) bits
+    }
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        const uint32_t r = __reduce_add_sync(0xffffffffu, c[w]);
+        if ((threadIdx.x & 31) == 0 && r) atomicAdd(&s_cnt[w], r);
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) counts[threadIdx.x] = s_cnt[threadIdx.x];
+}
+
+cudaError_t launch_prefix_sample(const uint32_t* hi, const uint32_t* lo, uint64_t n, uint32_t samples,
+                                 uint32_t* counts, cudaStream_t st) {
+    const size_t smem = (size_t)samples * 8;
+    raise_smem_limit((const void*)k_prefix_sample, smem);
+    k_prefix_sample<<<1, 1024, smem, st>>>(hi, lo, n, samples, counts);
     return cudaGetLastError();
 }
 
