@@ -341,6 +341,8 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
 
 bool same_mask(const uint8_t* a, const uint8_t* b, uint32_t B) { return memcmp(a, b, B) == 0; }
 
+constexpr uint32_t kSampleKeys = 4096;           // keys sorted to choose the round-0 width
+
 // D-offset table of the sort mask: moff[t] = key position of the (t+1)-st mask bit.
 int upload_moff(cks_ctx* ctx, const uint8_t* sort_mask, uint32_t B, uint32_t m) {
     TRY(ensure(ctx, ctx->moff, (size_t)(m + 1) * 2));
@@ -404,29 +406,37 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     // is planes np-1-2r (high word) and np-2-2r (low word)
     TRY(ensure(ctx, ctx->pm, (size_t)np * sp * 4));
     uint32_t* pm = as<uint32_t>(ctx->pm);
-    TRY(run_compress(ctx, keys, n, B, M, pm, sp, lead));
-    mark(ctx, ST_COMPRESS);
-    // width T of round 0: the narrowest multiple of 8 bits that separates a strided sample of
-    // the keys as well as the full 64-bit chunk does (fewer round-0 passes; whatever still ties
-    // is finished by the later rounds -- the result is exact for any T). CKS_ROUND0_BITS forces.
-    uint32_t T = 64;
-    {
-        static int forced = -2;
-        if (forced == -2) { const char* e = getenv("CKS_ROUND0_BITS"); forced = e ? atoi(e) : 0; }
-        if (forced > 0 && forced <= 64 && (forced & 7) == 0) {
-            T = (uint32_t)forced;
-        } else if (np >= 2 && n >= (1u << 16)) {
-            TRY(ensure(ctx, ctx->rtot, 64));
-            uint32_t* cnt = as<uint32_t>(ctx->rtot) + 4;
-            LAUNCH(launch_prefix_sample(pm + (uint64_t)(np - 1) * sp, pm + (uint64_t)(np - 2) * sp, n, 16384, cnt,
-                                        ctx->stream));
-            CK(cudaMemcpyAsync(ctx->h_tot, cnt, 32, cudaMemcpyDeviceToHost, ctx->stream));
-            CK(cudaStreamSynchronize(ctx->stream));
-            for (uint32_t w = 0; w < 8; w++)
-                if (ctx->h_tot[w] == ctx->h_tot[7]) { T = 8 * (w + 1); break; }
-        }
-        if (T > m) T = (m + 7) & ~7u;
+    // a2 + a3, and the width T of round 0: the narrowest multiple of 8 bits that separates a
+    // strided sample of the keys as well as the full 64-bit chunk does (fewer round-0 passes;
+    // whatever still ties is finished by the later rounds -- the result is exact for any T).
+    // The sample is compressed and sorted on the side stream while the full compress runs.
+    // CKS_ROUND0_BITS forces T.
+    TRY(claim_slot(ctx, 0));
+    plan_compress(M, B, ctx->h_plan[0]);
+    GatherPlan* dplan;
+    TRY(upload_plan(ctx, 0, &dplan));
+    static int forced = -2;
+    if (forced == -2) { const char* e = getenv("CKS_ROUND0_BITS"); forced = e ? atoi(e) : 0; }
+    const bool sample = !(forced > 0 && forced <= 64 && (forced & 7) == 0) && np >= 2 && n >= (1u << 16);
+    TRY(ensure(ctx, ctx->rtot, 64));
+    uint32_t* scnt = as<uint32_t>(ctx->rtot) + 4;
+    if (sample) {
+        CK(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_ev[0], 0));
+        LAUNCH(launch_prefix_sample(keys, n, B, dplan, kSampleKeys, scnt, ctx->aux_stream));
+        CK(cudaMemcpyAsync(ctx->h_tot + 8, scnt, 32, cudaMemcpyDeviceToHost, ctx->aux_stream));
+        CK(cudaEventRecord(ctx->aux_ev[1], ctx->aux_stream));
     }
+    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, pm, sp, ctx->sms, ctx->stream, lead));
+    mark(ctx, ST_COMPRESS);
+    uint32_t T = forced > 0 && forced <= 64 && (forced & 7) == 0 ? (uint32_t)forced : 64;
+    if (sample) {
+        CK(cudaEventSynchronize(ctx->aux_ev[1]));
+        for (uint32_t w = 0; w < 8; w++)
+            if (ctx->h_tot[8 + w] == ctx->h_tot[15]) { T = 8 * (w + 1); break; }
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));   // (scnt is reused below)
+    }
+    if (T > m) T = (m + 7) & ~7u;
     mark(ctx, ST_HIST);
     TRY(upload_moff(ctx, M, B, m));
     TRY(ensure(ctx, ctx->dacc, (size_t)nwords * 4));

@@ -47,10 +47,10 @@ cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32
                              int sms, cudaStream_t st);
 cudaError_t launch_occ_finalize(const uint32_t* occ, uint32_t B, uint64_t n, uint8_t* dplus,
                                 uint8_t* variant, cudaStream_t st);
-// First-round width of the refinement: sorts a strided sample of `samples` (power of two,
-// <= 16384) top-64-bit prefixes of P_M (planes hi / lo, lo may be NULL) in one CTA and writes
-// counts[w] = distinct prefixes of the top 8(w+1) bits, w = 0..7.
-cudaError_t launch_prefix_sample(const uint32_t* hi, const uint32_t* lo, uint64_t n, uint32_t samples,
+// First-round width of the refinement: compresses a strided sample of `samples` keys (power
+// of two, <= 16384) with the compress plan, sorts their top-64-bit prefixes of P_M in one CTA
+// and writes counts[w] = distinct prefixes of the top 8(w+1) bits, w = 0..7.
+cudaError_t launch_prefix_sample(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* plan, uint32_t samples,
                                  uint32_t* counts, cudaStream_t st);
 // Planes are u32 SoA arrays: plane q of a packed array starts at ptr + q*pitch (pitch in
 // elements; user buffers have pitch n, library scratch pads the pitch to 32 elements so every

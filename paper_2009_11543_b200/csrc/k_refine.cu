@@ -550,17 +550,40 @@ cudaError_t launch_ref_put(uint32_t* perm, const uint32_t* pos, const uint32_t* 
 
 namespace cks {
 
-// One CTA: a strided sample of top-64-bit prefixes of P_M is bitonic-sorted in shared memory,
-// then the number of distinct prefixes of the top 8, 16, ..., 64 bits is counted.
+// One CTA: the top 64 bits of P_M of a strided sample of keys (compressed here with the
+// compress plan, most significant gather step first) are bitonic-sorted in shared memory,
+// then the number of distinct prefixes of the top 8, 16, ..., 64 bits is counted. Runs on a
+// side stream while the full compress runs.
 __global__ void __launch_bounds__(1024)
-k_prefix_sample(const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo, uint64_t n, uint32_t S,
-                uint32_t* __restrict__ counts) {
+k_prefix_sample(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const GatherPlan* __restrict__ plan,
+                uint32_t S, uint32_t* __restrict__ counts) {
     extern __shared__ unsigned long long s_v[];                     // [S]
     __shared__ uint32_t s_cnt[8];
     if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+    const uint32_t nsteps = plan->nsteps;
     for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) {
-        const uint64_t row = (uint64_t)i * n / S;
-        s_v[i] = ((unsigned long long)hi[row] << 32) | (lo ? lo[row] : 0u);
+        const uint8_t* k = keys + ((uint64_t)i * n / S) * B;
+        unsigned long long top = 0;
+        uint32_t got = 0;
+        for (int s = (int)nsteps - 1; s >= 0 && got < 64; s--) {
+            const GatherStep& g = plan->step[s];
+            uint32_t w = 0;
+            for (uint32_t b = 0; b < 4; b++) {
+                const uint32_t j = g.src * 4 + b;
+                w = (w << 8) | (j < B ? k[j] : 0u);
+            }
+            uint32_t x = w & g.mask;
+#pragma unroll
+            for (int q = 0; q < 5; q++) {
+                const uint32_t tq = x & g.mv[q];
+                x = (x ^ tq) | (tq >> (1u << q));
+            }
+            uint32_t c = g.cnt;
+            if (got + c > 64) { x >>= got + c - 64; c = 64 - got; }
+            top = (c == 64 ? 0ull : top << c) | x;
+            got += c;
+        }
+        s_v[i] = got ? top << (64 - got) : 0ull;
     }
     __syncthreads();
     for (uint32_t size = 2; size <= S; size <<= 1) {
@@ -589,11 +612,11 @@ k_prefix_sample(const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo
     if (threadIdx.x < 8) counts[threadIdx.x] = s_cnt[threadIdx.x];
 }
 
-cudaError_t launch_prefix_sample(const uint32_t* hi, const uint32_t* lo, uint64_t n, uint32_t samples,
+cudaError_t launch_prefix_sample(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* plan, uint32_t samples,
                                  uint32_t* counts, cudaStream_t st) {
     const size_t smem = (size_t)samples * 8;
     raise_smem_limit((const void*)k_prefix_sample, smem);
-    k_prefix_sample<<<1, 1024, smem, st>>>(hi, lo, n, samples, counts);
+    k_prefix_sample<<<1, 1024, smem, st>>>(keys, n, B, plan, samples, counts);
     return cudaGetLastError();
 }
 
