@@ -50,7 +50,7 @@ struct cks_ctx {
     // scratch
     DevBuf occ, masks8, planeA, planeB, ridA, ridB, hist, base, status, counters, dacc, moff, dbit,
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
-        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, tie, keep, done, mlist, rcnt, rtot;   // NEXT-1
+        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, tie, keep, done, mlist, wlist, rcnt, rtot;   // NEXT-1
     int algo = -1;                    // LSD pass: 1 = reduce-then-scan (default), 0 = onesweep
                                       // (decoupled look-back; measured slower)
     size_t status_tiles = 0;
@@ -485,6 +485,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         TRY(ensure(ctx, ctx->keep, n + 16));
         TRY(ensure(ctx, ctx->done, n + 16));
         TRY(ensure(ctx, ctx->mlist, sp * 4));
+        TRY(ensure(ctx, ctx->wlist, sp * 4));
         TRY(ensure(ctx, ctx->rcnt, (size_t)(ref_tiles(n) + 1) * 8));
         TRY(ensure(ctx, ctx->rtot, 64));
     }
@@ -515,10 +516,10 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         const int qtop = (int)np - 1 - (int)(o >> 5);            // plane holding bit o
         LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, posA_, segA_, as<uint32_t>(ctx->runoff), nseg, nn, out->perm,
                                 dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B,
-                                as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->rtot) + 2, ctx->sms, ctx->stream,
-                                0xFFFFFFFFu >> (o & 31)));
+                                as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->wlist), as<uint32_t>(ctx->rtot) + 12,
+                                ctx->sms, ctx->stream, 0xFFFFFFFFu >> (o & 31)));
         // (3) the runs left for an LSD round (none: done)
-        CK(cudaMemcpyAsync(ctx->h_tot, as<uint32_t>(ctx->rtot) + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_tot, as<uint32_t>(ctx->rtot) + 12, 8, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         uint64_t n2 = 0, nseg2 = 0;
         if (ctx->h_tot[1] > 0) {
@@ -807,6 +808,7 @@ int cks_ctx_destroy(cks_ctx* ctx) {
                       &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total,
                       &ctx->pm, &ctx->pd, &ctx->cmp, &ctx->crid, &ctx->crid2, &ctx->posA, &ctx->posB,
                       &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->tie, &ctx->keep, &ctx->done, &ctx->mlist,
+                      &ctx->wlist,
                       &ctx->rcnt, &ctx->rtot};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);

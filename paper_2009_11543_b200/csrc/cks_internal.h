@@ -142,7 +142,7 @@ cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* 
 cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
                              const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
-                             uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* mcount, int sms,
+                             uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* wlist, uint32_t* mcount, int sms,
                              cudaStream_t st, uint32_t fmask);
 cudaError_t launch_ref_keep(const uint32_t* seg, const uint32_t* run_off, const uint8_t* done, uint64_t nn,
                             uint8_t* keep, int sms, cudaStream_t st);

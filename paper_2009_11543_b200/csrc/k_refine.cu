@@ -213,136 +213,224 @@ k_ref_gather(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, uint3
     }
 }
 
-// Finish small tied runs in place (carried: P_M in sorted order at carried, planes of pitch
-// `pitch`; only used when the remaining bits are its plane 0). Thread per run s of the list (members run_off[s] ..
-// run_off[s+1]-1 at the contiguous global positions pos[run_off[s]] + j): a run of at most
-// kLocal keys is sorted by its remaining P_M bits (planes qtop .. 0; the earlier chunks tie)
-// with the row id as tie-break -- the stable order -- and its D_i are taken from the first
-// differing remaining bit. A longer run whose keys are all equal is already in row-id order
-// (duplicates). Every other run is flagged for the next LSD round (keep[k] = 1 for its
-// members but the first: the compaction's tie convention).
-constexpr uint32_t kLocal = 16;
-constexpr int kCarryWords = 3;                   // remaining words held in registers (carried path)
+// Finish tied runs in place. Every element's "remaining key" is its P_M words from plane qtop
+// down to 0 (the plane holding the first bit after the tied prefix; word qtop masked by fmask)
+// -- read from the carried sorted planes at the run's positions when P_M is carried, else
+// from P_M by row id -- and the run is sorted by (remaining key, row id): the stable order,
+// a total order. D_i of each new neighbour pair = first differing remaining bit.
+// By run length L:   L <= 4      k_ref_local, one thread, a 5-comparator network in registers
+//                                (P_M read by row and more than 4 planes left: insertion sort on
+//                                row ids with lazily read words, up to 16 keys);
+//                    L <= 32     k_ref_warp, one warp, bitonic network over shuffles;
+//                    L <= 2048   k_ref_cta, one CTA, bitonic sort in shared memory;
+//                    longer      next LSD round (`done` = 0).
+constexpr uint32_t kLocal = 4;
+constexpr uint32_t kWarpRun = 32;
+constexpr uint32_t kLazyRun = 16;                // pm path with more planes than registers
+constexpr int kRegWords = 4;                     // remaining words held in registers (thread / warp paths)
 constexpr uint32_t kCta = 2048;                  // medium runs: one CTA, bitonic sort in shared memory
 constexpr uint32_t kCtaWords = 8;                // ... if at most this many P_M planes remain (measured:
                                                  // with 10 remaining planes, cfg4, gathering them by row
                                                  // id costs more than leaving the runs to the LSD round)
+
+struct RunCtx {                                  // what every run finisher needs
+    const uint32_t* pm;
+    uint64_t pitch;
+    uint32_t np;
+    int qtop;
+    uint32_t fmask;
+    const uint16_t* moff;
+    uint32_t* perm;
+    uint16_t* dbit;
+    uint32_t* carried;
+};
+
+// remaining word c (0 = plane qtop) of the element at global position p with row id `row`
+__device__ __forceinline__ uint32_t rem_word(const RunCtx& R, int c, uint32_t p, uint32_t row) {
+    const int q = R.qtop - c;
+    const uint32_t v = R.carried ? R.carried[(uint64_t)q * R.pitch + p] : __ldg(R.pm + (uint64_t)q * R.pitch + row);
+    return c == 0 ? v & R.fmask : v;
+}
+// write back element (words w, row id) to position p; D_i against the previous element's words
+template <int W>
+__device__ __forceinline__ void put_elem(const RunCtx& R, uint32_t p, const uint32_t (&w)[W], uint32_t row,
+                                         const uint32_t* prev, uint32_t* s_bm) {
+    R.perm[p] = row;
+    if (R.carried)                                   // the carried planes follow their rows
+        for (int c = 0; c <= R.qtop && c < W; c++) {
+            const uint64_t at = (uint64_t)(R.qtop - c) * R.pitch + p;
+            R.carried[at] = c == 0 ? (R.carried[at] & ~R.fmask) | w[0] : w[c];
+        }
+    if (!prev) return;
+#pragma unroll
+    for (int c = 0; c < W; c++) {
+        const uint32_t x = w[c] ^ prev[c];
+        if (x) {
+            const uint32_t d = R.moff[32u * (R.np - 1 - (uint32_t)(R.qtop - c)) + (uint32_t)__clz(x)];
+            R.dbit[p] = (uint16_t)d;
+            const uint32_t b = 0x80000000u >> (d & 31);
+            if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
+            return;
+        }
+    }
+}
+
+template <int W>
+__device__ __forceinline__ bool key_less(const uint32_t (&a)[W], uint32_t ra, const uint32_t (&b)[W], uint32_t rb) {
+#pragma unroll
+    for (int c = 0; c < W; c++)
+        if (a[c] != b[c]) return a[c] < b[c];
+    return ra < rb;
+}
+
+// Thread per run: short runs (<= 4, registers only: a fixed network, static indices); longer
+// runs are routed to the warp list, the CTA list or the next LSD round.
 __global__ void __launch_bounds__(kRefThreads)
-k_ref_local(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* __restrict__ moff,
-            const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
-            uint32_t* __restrict__ perm, uint16_t* __restrict__ dbit, uint32_t* __restrict__ dacc,
-            uint8_t* __restrict__ done, uint32_t* __restrict__ carried, uint32_t nwords, uint32_t* __restrict__ mlist,
-            uint32_t* __restrict__ mcount, uint32_t cta_max, uint32_t fmask) {
+k_ref_local(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg,
+            uint64_t nn, uint32_t* __restrict__ dacc, uint8_t* __restrict__ done, uint32_t nwords,
+            uint32_t* __restrict__ mlist, uint32_t* __restrict__ wlist, uint32_t* __restrict__ mcount,
+            uint32_t cta_max) {
+    constexpr int W = kRegWords;
     __shared__ uint32_t s_bm[kMaxBits / 32];                         // D bits found by this block
     for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
     __syncthreads();
     const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t sweeps = (nseg + nthreads - 1) / nthreads;       // uniform trip count (block barrier below)
+    const int Wr = R.qtop + 1;
     for (uint64_t it = 0; it < sweeps; it++) {
         const uint64_t s = it * nthreads + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
         if (s >= nseg) continue;
         const uint32_t k0 = run_off[s];
         const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
         const uint32_t L = k1 - k0;
-        const uint32_t p0 = pos[k0];
-        // -1: a < b, 1: a > b, 0: equal remaining bits; *t = first differing compressed index
-        auto cmp = [&](uint32_t a, uint32_t b, uint32_t* t) -> int {
-            for (int q = qtop; q >= 0; q--) {
-                const uint32_t mq = q == qtop ? fmask : 0xFFFFFFFFu;
-                const uint32_t wa = __ldg(pm + (uint64_t)q * pitch + a) & mq, wb = __ldg(pm + (uint64_t)q * pitch + b) & mq;
-                if (wa != wb) {
-                    if (t) *t = 32u * (np - 1 - (uint32_t)q) + (uint32_t)__clz(wa ^ wb);
-                    return wa < wb ? -1 : 1;
+        uint8_t fin = 1;
+        if (L <= kLocal && Wr <= W) {
+            const uint32_t p0 = pos[k0];
+            uint32_t r[4], w[4][W];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                r[j] = 0xFFFFFFFFu;                                  // padding sorts last
+#pragma unroll
+                for (int c = 0; c < W; c++) w[j][c] = 0xFFFFFFFFu;
+                if ((uint32_t)j < L) {
+                    r[j] = R.perm[p0 + j];
+#pragma unroll
+                    for (int c = 0; c < W; c++) w[j][c] = c < Wr ? rem_word(R, c, p0 + j, r[j]) : 0u;
                 }
             }
-            return 0;
-        };
-        if (carried && L <= kLocal && qtop < (int)kCarryWords) {
-            // P_M is carried in sorted order and at most kCarryWords planes remain: sort the run's
-            // (remaining words, row id) read at its contiguous positions, no row gathers
-            constexpr int CW = kCarryWords;
-            uint32_t rows[kLocal], w[kLocal][CW];
-            for (uint32_t j = 0; j < L; j++) {
-                rows[j] = perm[p0 + j];
+            auto cswap = [&](int x, int y) {
+                if (key_less<W>(w[y], r[y], w[x], r[x])) {
+                    const uint32_t tr = r[x]; r[x] = r[y]; r[y] = tr;
 #pragma unroll
-                for (int c = 0; c < CW; c++)
-                    w[j][c] = c <= qtop ? carried[(uint64_t)(qtop - c) * pitch + p0 + j] & (c == 0 ? fmask : ~0u) : 0u;
-            }
-            auto lt = [&](const uint32_t* x, uint32_t rx, const uint32_t* y, uint32_t ry) -> bool {
-#pragma unroll
-                for (int c = 0; c < CW; c++)
-                    if (x[c] != y[c]) return x[c] < y[c];
-                return rx < ry;
+                    for (int c = 0; c < W; c++) { const uint32_t tw = w[x][c]; w[x][c] = w[y][c]; w[y][c] = tw; }
+                }
             };
-            for (uint32_t j = 1; j < L; j++) {
-                uint32_t x[CW];
+            cswap(0, 1); cswap(2, 3); cswap(0, 2); cswap(1, 3); cswap(1, 2);
 #pragma unroll
-                for (int c = 0; c < CW; c++) x[c] = w[j][c];
-                const uint32_t rx = rows[j];
-                uint32_t i = j;
-                while (i > 0 && lt(x, rx, w[i - 1], rows[i - 1])) {
-                    rows[i] = rows[i - 1];
-#pragma unroll
-                    for (int c = 0; c < CW; c++) w[i][c] = w[i - 1][c];
-                    i--;
-                }
-                rows[i] = rx;
-#pragma unroll
-                for (int c = 0; c < CW; c++) w[i][c] = x[c];
-            }
-            for (uint32_t j = 0; j < L; j++) {
-                perm[p0 + j] = rows[j];
-                for (int c = 0; c <= qtop; c++) {                 // (masked-off bits of word 0 tie: keep them)
-                    uint64_t at = (uint64_t)(qtop - c) * pitch + p0 + j;
-                    carried[at] = c == 0 ? (carried[at] & ~fmask) | w[j][0] : w[j][c];
-                }
-                if (j == 0) continue;
-#pragma unroll
-                for (int c = 0; c < CW; c++) {
-                    const uint32_t x = w[j][c] ^ w[j - 1][c];
-                    if (x) {
-                        const uint32_t d = moff[32u * (np - 1 - (uint32_t)(qtop - c)) + (uint32_t)__clz(x)];
-                        dbit[p0 + j] = (uint16_t)d;
-                        const uint32_t b = 0x80000000u >> (d & 31);
-                        if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
-                        break;
+            for (int j = 0; j < 4; j++)
+                if ((uint32_t)j < L) put_elem<W>(R, p0 + j, w[j], r[j], j ? w[j - 1] : nullptr, s_bm);
+        } else if (L <= kLazyRun && !R.carried && (Wr > W || L <= kLocal)) {
+            // more remaining planes than registers: an insertion sort on row ids, words read
+            // from P_M by row as the comparisons need them (most pairs differ in the first)
+            const uint32_t p0 = pos[k0];
+            auto cmp = [&](uint32_t a, uint32_t b, uint32_t* tt) -> int {
+                for (int c = 0; c < Wr; c++) {
+                    const uint32_t wa = rem_word(R, c, 0, a), wb = rem_word(R, c, 0, b);
+                    if (wa != wb) {
+                        if (tt) *tt = 32u * (R.np - 1 - (uint32_t)(R.qtop - c)) + (uint32_t)__clz(wa ^ wb);
+                        return wa < wb ? -1 : 1;
                     }
                 }
-            }
-        } else if (L <= kLocal) {
-            uint32_t rows[kLocal];
-#pragma unroll
-            for (uint32_t j = 0; j < kLocal; j++) rows[j] = j < L ? perm[p0 + j] : 0u;
-            for (uint32_t j = 1; j < L; j++) {                   // insertion sort, stable by row id
-                const uint32_t x = rows[j];
+                return 0;
+            };
+            uint32_t r[kLazyRun];
+            for (uint32_t j = 0; j < L; j++) r[j] = R.perm[p0 + j];
+            for (uint32_t j = 1; j < L; j++) {
+                const uint32_t x = r[j];
                 uint32_t i = j;
                 while (i > 0) {
-                    const int c = cmp(rows[i - 1], x, nullptr);
-                    if (c < 0 || (c == 0 && rows[i - 1] < x)) break;
-                    rows[i] = rows[i - 1];
+                    const int c = cmp(r[i - 1], x, nullptr);
+                    if (c < 0 || (c == 0 && r[i - 1] < x)) break;
+                    r[i] = r[i - 1];
                     i--;
                 }
-                rows[i] = x;
+                r[i] = x;
             }
             for (uint32_t j = 0; j < L; j++) {
-                perm[p0 + j] = rows[j];
-                if (j == 0) continue;
+                R.perm[p0 + j] = r[j];
                 uint32_t tt = 0;
-                if (cmp(rows[j - 1], rows[j], &tt) != 0) {
-                    const uint32_t d = moff[tt];
-                    dbit[p0 + j] = (uint16_t)d;
+                if (j && cmp(r[j - 1], r[j], &tt) != 0) {
+                    const uint32_t d = R.moff[tt];
+                    R.dbit[p0 + j] = (uint16_t)d;
                     const uint32_t b = 0x80000000u >> (d & 31);
                     if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
                 }
             }
-        } else if (L <= cta_max && qtop + 1 <= (int)kCtaWords) {
-            mlist[atomicAdd(mcount, 1u)] = (uint32_t)s;           // medium run: one CTA sorts it
+        } else if (L <= kWarpRun && Wr <= W) {
+            wlist[atomicAdd(mcount + 2, 1u)] = (uint32_t)s;
+        } else if (L <= cta_max && Wr <= (int)kCtaWords) {
+            mlist[atomicAdd(mcount, 1u)] = (uint32_t)s;
         } else {
-            done[s] = 0;                                         // long run: next LSD round
+            fin = 0;                                                 // long run: next LSD round
             atomicAdd(mcount + 1, 1u);
-            continue;
         }
-        done[s] = 1;
+        done[s] = fin;
+    }
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
+        if (s_bm[w]) atomicOr(&dacc[w], s_bm[w]);
+}
+
+// Warp per run (5..32 keys): lane j holds element j (padding sorts last); bitonic network by
+// shuffles; lane j writes the j-th smallest and its D_i against lane j-1's element.
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_warp(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg,
+           uint64_t nn, uint32_t* __restrict__ dacc, uint32_t nwords, const uint32_t* __restrict__ wlist,
+           const uint32_t* __restrict__ mcount) {
+    constexpr int W = kRegWords;
+    __shared__ uint32_t s_bm[kMaxBits / 32];
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t cnt = mcount[2];
+    const int Wr = R.qtop + 1;
+    const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
+    for (uint32_t wi = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); wi < cnt; wi += nwarps) {
+        const uint32_t s = wlist[wi];
+        const uint32_t k0 = run_off[s];
+        const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
+        const uint32_t L = k1 - k0;
+        const uint32_t p0 = pos[k0];
+        uint32_t r = 0xFFFFFFFFu, w[W];
+#pragma unroll
+        for (int c = 0; c < W; c++) w[c] = 0xFFFFFFFFu;
+        if (lane < L) {
+            r = R.perm[p0 + lane];
+#pragma unroll
+            for (int c = 0; c < W; c++) w[c] = c < Wr ? rem_word(R, c, p0 + lane, r) : 0u;
+        }
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                uint32_t ow[W];
+#pragma unroll
+                for (int c = 0; c < W; c++) ow[c] = __shfl_xor_sync(0xffffffffu, w[c], stride);
+                const uint32_t orr = __shfl_xor_sync(0xffffffffu, r, stride);
+                const bool lower = (lane & stride) == 0;             // this lane keeps the min if ascending
+                const bool up = (lane & size) == 0;
+                const bool other_less = key_less<W>(ow, orr, w, r);
+                if (other_less == (lower == up)) {
+                    r = orr;
+#pragma unroll
+                    for (int c = 0; c < W; c++) w[c] = ow[c];
+                }
+            }
+        }
+        uint32_t pw[W];
+#pragma unroll
+        for (int c = 0; c < W; c++) pw[c] = __shfl_up_sync(0xffffffffu, w[c], 1);
+        if (lane < L) put_elem<W>(R, p0 + lane, w, r, lane ? pw : nullptr, s_bm);
     }
     __syncthreads();
     for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
@@ -506,14 +594,18 @@ cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* 
 cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
                              const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
-                             uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* mcount, int sms,
+                             uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* wlist, uint32_t* mcount, int sms,
                              cudaStream_t st, uint32_t fmask) {
-    if (nseg == 0) return cudaMemsetAsync(mcount, 0, 8, st);
+    (void)seg;
+    (void)keep;
+    cudaMemsetAsync(mcount, 0, 12, st);                          // medium runs, long runs, warp runs
+    if (nseg == 0) return cudaGetLastError();
     const uint32_t nwords = (8 * B + 31) / 32;
-    cudaMemsetAsync(mcount, 0, 8, st);                           // medium runs, long runs
-    k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn, perm,
-                                                            dbit, dacc, done, carried, nwords, mlist, mcount,
-                                                            cta_max(), fmask);
+    RunCtx R{pm, pitch, np, qtop, fmask, moff, perm, dbit, carried};
+    k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(R, pos, run_off, nseg, nn, dacc, done, nwords, mlist,
+                                                            wlist, mcount, cta_max());
+    if (qtop + 1 <= kRegWords)
+        k_ref_warp<<<(unsigned)(sms * 8), kRefThreads, 0, st>>>(R, pos, run_off, nseg, nn, dacc, nwords, wlist, mcount);
     if (qtop + 1 <= (int)kCtaWords) {
         const size_t smem = (size_t)kCta * 4 * (qtop + 2) + (size_t)kCta * 2;
         raise_smem_limit((const void*)k_ref_cta, smem);
