@@ -406,9 +406,10 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     // is planes np-1-2r (high word) and np-2-2r (low word)
     TRY(ensure(ctx, ctx->pm, (size_t)np * sp * 4));
     uint32_t* pm = as<uint32_t>(ctx->pm);
-    // a2 + a3, and the width T of round 0: the narrowest multiple of 8 bits that separates a
-    // strided sample of the keys as well as the full 64-bit chunk does (fewer round-0 passes;
-    // whatever still ties is finished by the later rounds -- the result is exact for any T).
+    // a2 + a3, and the width T of round 0: 8 bits more than the narrowest multiple of 8 bits
+    // that separates a strided sample of the keys as well as the full 64-bit chunk does (fewer
+    // round-0 passes; whatever still ties is finished by the later rounds -- the result is
+    // exact for any T).
     // The sample is compressed and sorted on the side stream while the full compress runs.
     // CKS_ROUND0_BITS forces T.
     TRY(claim_slot(ctx, 0));
@@ -432,8 +433,10 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     uint32_t T = forced > 0 && forced <= 64 && (forced & 7) == 0 ? (uint32_t)forced : 64;
     if (sample) {
         CK(cudaEventSynchronize(ctx->aux_ev[1]));
+        // one byte of margin: a 4096-key sample misses the birthday collisions that tie millions
+        // of keys at the narrowest separating width (measured: cfg5 40 -> 48, cfg3 32 -> 40)
         for (uint32_t w = 0; w < 8; w++)
-            if (ctx->h_tot[8 + w] == ctx->h_tot[15]) { T = 8 * (w + 1); break; }
+            if (ctx->h_tot[8 + w] == ctx->h_tot[15]) { T = 8 * (w + 2) < 64 ? 8 * (w + 2) : 64; break; }
         CK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));   // (scnt is reused below)
     }
     if (T > m) T = (m + 7) & ~7u;
