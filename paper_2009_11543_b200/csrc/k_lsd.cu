@@ -331,8 +331,9 @@ k_downsweep(const LsdPassArgs a) {
                 peers[i] = match_bits<FULL ? 8 : 9>(dg[i]);
             }
             // the group's lowest lane (unique per label) reserves the group's places in the
-            // warp-private bin (predicated atomics, all issued before any result is used;
-            // shared atomics of one warp apply in issue order: stable), then broadcasts
+            // warp-private bin (predicated atomics, all issued before any result is used; a
+            // __syncwarp between items orders item i's reservations before item i+1's: stable),
+            // then broadcasts
             uint32_t old[ITEMS];
             const uint32_t hbase = smem_addr(h);
 #pragma unroll
@@ -343,6 +344,7 @@ k_downsweep(const LsdPassArgs a) {
                              : "=r"(old[i]) : "r"(lower), "r"(hbase + dg[i] * 4), "r"((uint32_t)__popc(peers[i]))
                              : "memory");
                 pos[i] = lower;
+                __syncwarp();                                    // item i's reservations before item i+1's
             }
 #pragma unroll
             for (int i = 0; i < ITEMS; i++) pos[i] += __shfl_sync(0xFFFFFFFFu, old[i], __ffs(peers[i]) - 1);
@@ -592,6 +594,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
                                  : "=r"(old[i]) : "r"(lower), "r"(hbase + dg[i] * 4), "r"((uint32_t)__popc(peers[i]))
                                  : "memory");
                     pos[i] = lower;
+                    __syncwarp();                                // item i's reservations before item i+1's
                 }
 #pragma unroll
                 for (int i = 0; i < RI; i++) pos[i] += __shfl_sync(0xFFFFFFFFu, old[i], __ffs(peers[i]) - 1);
