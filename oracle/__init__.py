@@ -57,6 +57,8 @@ def _load():
         L.orc_adjacent_compressed.argtypes = [p, u32, u64, p, u32, p, p]
         L.orc_bulkload.argtypes = [p, p, u64, u32, u32, p, u32, p, p, p, p, p]
         L.orc_bulkload.restype = u32
+        L.orc_paper_tree.argtypes = [p, u64, u32, p, p, u32, u32, u32, p]
+        L.orc_paper_tree.restype = u32
         _lib = L
     return _lib
 
@@ -211,6 +213,30 @@ def bulkload(perm, dbit, keys, fanout: int, fill: float = 1.0):
     assert h == len(lv)
     return dict(height=h, level_nodes=level_nodes[:h].copy(), node_cnt=node_cnt,
                 entry_rid=rid, entry_child=child, entry_dbit=edb, per=per)
+
+
+def paper_tree_levels(n: int, leaf_per: int, inner_per: int) -> list[int]:
+    """Nodes per level of the paper-format tree (leaves first)."""
+    if n == 0:
+        return []
+    lv = [(n + leaf_per - 1) // leaf_per]
+    while lv[-1] > 1:
+        lv.append((lv[-1] + inner_per - 1) // inner_per)
+    return lv
+
+
+def paper_tree(keys, perm, dbit, pk: int = 32, fill: float = 0.9):
+    """NEXT-3: node images u8[total][256] of the paper's index tree."""
+    k = _keys(keys)
+    n, B = k.shape
+    leaf_per, inner_per = int(np.floor(14 * fill)), int(np.floor(9 * fill))
+    lv = paper_tree_levels(n, leaf_per, inner_per)
+    nodes = np.zeros((max(1, sum(lv)), 256), np.uint8)
+    perm = np.ascontiguousarray(perm, dtype=np.uint32)
+    db = np.ascontiguousarray(dbit, dtype=np.uint16)
+    h = _load().orc_paper_tree(_ptr(k), n, B, _ptr(perm), _ptr(db), pk, leaf_per, inner_per, nodes.ctypes.data)
+    assert h == len(lv)
+    return dict(height=h, levels=lv, nodes=nodes[:sum(lv)], leaf_per=leaf_per, inner_per=inner_per)
 
 
 def first_build(keys, threads: int = 1):

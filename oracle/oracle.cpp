@@ -358,4 +358,104 @@ uint32_t orc_bulkload(const uint32_t* perm, const uint16_t* dbit, uint64_t n, ui
     return (uint32_t)lv.size();
 }
 
+
+/* ---- NEXT-3: the paper's index tree format (Sec. 4.2; Sec. 5.3) ----
+ *
+ * Node = 256 bytes. Leaf: 24-byte header, 8-byte next-node pointer, 14 entries of 16
+ * bytes ("(256-32)/16 = 14"); an entry is a partial key, a distinction bit position,
+ * an index key length and a record ID. Non-leaf: 24-byte header, 9 entries of 24
+ * bytes = partial key, distinction bit position, key length, child pointer, pointer
+ * to the highest key. Nodes are filled to floor(max fanout * fill).
+ * Byte layout (little-endian, R16):
+ *   header  u16 count | u16 level | u32 key_bytes | u64 highest key (record id) | u64 0
+ *   leaf    u64 next leaf (node index, all-ones for the last) | 14 x {u32 pk | u16 dbit |
+ *           u16 key_len | u64 record id}
+ *   inner   9 x {u32 pk | u16 dbit | u16 key_len | u64 child node index | u64 highest key}
+ * The partial key is the pk bits following the entry's distinction bit position D (P:335,
+ * reading C14: positions D+1 .. D+pk; positions past the key are 0); with no distinction bit
+ * (first key, equal keys) positions 0 .. pk-1 (reading R16). Bits are packed from bit 31 down.
+ * Non-leaf entry: highest key of the child's subtree, its D-bit against the previous entry's
+ * highest key at the same level, computed here directly on the full keys. Nodes are
+ * numbered leaves first, then each level up. Returns the height. */
+static uint32_t partial_key(const uint8_t* key, uint32_t B, int d, uint32_t pk) {
+    uint32_t v = 0;
+    uint32_t p0 = d < 0 ? 0u : (uint32_t)d + 1;
+    for (uint32_t j = 0; j < pk; j++) {
+        uint32_t p = p0 + j;
+        uint32_t bit = p < 8 * B ? (uint32_t)key_bit(key, p) : 0u;
+        v |= bit << (31 - j);
+    }
+    return v;
+}
+static void put16(uint8_t* o, uint16_t v) { memcpy(o, &v, 2); }
+static void put32(uint8_t* o, uint32_t v) { memcpy(o, &v, 4); }
+static void put64(uint8_t* o, uint64_t v) { memcpy(o, &v, 8); }
+
+uint32_t orc_paper_tree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
+                        uint32_t pk, uint32_t leaf_per, uint32_t inner_per, uint8_t* nodes) {
+    if (n == 0) return 0;
+    std::vector<uint64_t> lv;                         /* nodes per level */
+    std::vector<uint64_t> cover;                      /* sorted keys per node of each level */
+    uint64_t c = (n + leaf_per - 1) / leaf_per;
+    lv.push_back(c);
+    cover.push_back(leaf_per);
+    while (c > 1) {
+        c = (c + inner_per - 1) / inner_per;
+        lv.push_back(c);
+        cover.push_back(cover.back() * inner_per);
+    }
+    uint64_t total = 0;
+    for (uint64_t x : lv) total += x;
+    memset(nodes, 0, total * 256);
+    auto key = [&](uint64_t sorted_idx) { return keys + (uint64_t)perm[sorted_idx] * B; };
+    /* leaves */
+    for (uint64_t j = 0; j < lv[0]; j++) {
+        uint8_t* nd = nodes + j * 256;
+        uint64_t k0 = j * leaf_per, k1 = std::min(k0 + leaf_per, n);
+        put16(nd, (uint16_t)(k1 - k0));
+        put16(nd + 2, 0);
+        put32(nd + 4, B);
+        put64(nd + 8, perm[k1 - 1]);
+        put64(nd + 24, j + 1 < lv[0] ? j + 1 : ~0ull);
+        for (uint64_t k = k0; k < k1; k++) {
+            uint8_t* e = nd + 32 + (k - k0) * 16;
+            int d = dbit[k] == ORC_NONE ? -1 : (int)dbit[k];
+            put32(e, partial_key(key(k), B, d, pk));
+            put16(e + 4, dbit[k]);
+            put16(e + 6, (uint16_t)B);
+            put64(e + 8, perm[k]);
+        }
+    }
+    /* non-leaf levels */
+    uint64_t off = lv[0], below = 0;
+    for (size_t l = 1; l < lv.size(); l++) {
+        for (uint64_t j = 0; j < lv[l]; j++) {
+            uint8_t* nd = nodes + (off + j) * 256;
+            uint64_t c0 = j * inner_per, c1 = std::min(c0 + inner_per, lv[l - 1]);
+            uint64_t hi_last = std::min((c1) * cover[l - 1], n) - 1;
+            put16(nd, (uint16_t)(c1 - c0));
+            put16(nd + 2, (uint16_t)l);
+            put32(nd + 4, B);
+            put64(nd + 8, perm[hi_last]);
+            for (uint64_t ch = c0; ch < c1; ch++) {
+                uint8_t* e = nd + 24 + (ch - c0) * 24;
+                uint64_t hi = std::min((ch + 1) * cover[l - 1], n) - 1;      /* highest key of child ch */
+                int d = -1;
+                if (ch > 0) {
+                    uint64_t phi = ch * cover[l - 1] - 1;                       /* ... of child ch-1 */
+                    d = orc_dbit_pair(key(phi), key(hi), B);
+                }
+                put32(e, partial_key(key(hi), B, d, pk));
+                put16(e + 4, d < 0 ? (uint16_t)ORC_NONE : (uint16_t)d);
+                put16(e + 6, (uint16_t)B);
+                put64(e + 8, below + ch);
+                put64(e + 16, perm[hi]);
+            }
+        }
+        below = off;
+        off += lv[l];
+    }
+    return (uint32_t)lv.size();
+}
+
 }  /* extern "C" */

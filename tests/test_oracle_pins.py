@@ -339,3 +339,81 @@ def test_bulkload_structure(n, fanout, fill):
         assert edb[0] == oracle.NONE16
         off += nodes
         span *= per
+
+
+# ---- NEXT-3: the paper's index tree format (Sec. 4.2, Sec. 5.3) ---------------------------
+
+def le(nd, off, size):
+    return int.from_bytes(bytes(nd[off:off + size]), "little")
+
+
+def test_paper_tree_fig2_partial_key():
+    # "the partial key of key_1 when pk = 4 is 1010, because D_1 = 5"
+    perm = np.arange(6, dtype=np.uint32)                          # FIG2 rows are in sorted order
+    dbit, _ = oracle.adjacent_dbits(FIG2, perm)
+    t = oracle.paper_tree(FIG2, perm, dbit, pk=4, fill=0.9)
+    assert t["height"] == 1 and t["leaf_per"] == 12 and t["inner_per"] == 8   # floor(14*.9), floor(9*.9)
+    leaf = t["nodes"][0]
+    assert le(leaf, 0, 2) == 6 and le(leaf, 2, 2) == 0 and le(leaf, 8, 8) == 5
+    assert le(leaf, 24, 8) == (1 << 64) - 1                       # no next leaf
+    e1 = leaf[32 + 16:32 + 32]
+    assert le(e1, 0, 4) >> 28 == 0b1010
+    assert le(e1, 4, 2) == 5 and le(e1, 6, 2) == 2 and le(e1, 8, 8) == 1
+
+
+def ref_partial_key(key: bytes, d, pk):
+    """pk bits after position d (reading C14) via big-integer shifts."""
+    v = int.from_bytes(key, "big")
+    nb = 8 * len(key)
+    start = 0 if d is None else d + 1
+    out = 0
+    for j in range(pk):
+        p = start + j
+        out = (out << 1) | ((v >> (nb - 1 - p)) & 1 if p < nb else 0)
+    return out << (32 - pk)
+
+
+@pytest.mark.parametrize("n,fill,pk", [(1, 0.9, 32), (12, 0.9, 32), (13, 0.9, 16), (1000, 0.9, 32),
+                                      (20_000, 1.0, 24)])
+def test_paper_tree_structure(n, fill, pk):
+    keys = cksgen.config(3, n=n) if n > 1 else cksgen.uniform(1, 32, seed=3)
+    perm = oracle.sort_keys(keys)
+    dbit, _ = oracle.adjacent_dbits(keys, perm)
+    t = oracle.paper_tree(keys, perm, dbit, pk=pk, fill=fill)
+    lp, ip = t["leaf_per"], t["inner_per"]
+    # node counts: ceil(n / per) per level (P:500)
+    lv, c = [-(-n // lp)], -(-n // lp)
+    while c > 1:
+        c = -(-c // ip)
+        lv.append(c)
+    assert t["levels"] == lv
+    nodes = t["nodes"]
+    # leaves in order hold the sorted record ids; headers point at the highest key; next chain
+    rids = [le(nodes[j], 32 + 16 * e + 8, 8) for j in range(lv[0]) for e in range(le(nodes[j], 0, 2))]
+    assert rids == [int(x) for x in perm]
+    for j in range(lv[0]):
+        cnt = le(nodes[j], 0, 2)
+        assert le(nodes[j], 8, 8) == le(nodes[j], 32 + 16 * (cnt - 1) + 8, 8)
+        assert le(nodes[j], 24, 8) == (j + 1 if j + 1 < lv[0] else (1 << 64) - 1)
+    # partial keys against a big-integer re-derivation on sampled entries
+    rng = np.random.default_rng(n)
+    for k in rng.choice(n, min(n, 200), replace=False):
+        j, e = divmod(int(k), lp)
+        ent = nodes[j][32 + 16 * e: 48 + 16 * e]
+        d = None if dbit[k] == 0xFFFF else int(dbit[k])
+        assert le(ent, 0, 4) == ref_partial_key(bytes(keys[perm[k]]), d, pk)
+    # inner entries: child index, highest key, and the D-bit against the previous entry's
+    # highest key equals the minimum D_k over the child's keys (Lemma 1, P:180)
+    off, below, cover = lv[0], 0, lp
+    for l in range(1, len(lv)):
+        for j in range(lv[l]):
+            nd = nodes[off + j]
+            assert le(nd, 2, 2) == l
+            for e in range(le(nd, 0, 2)):
+                ch = j * ip + e
+                ent = nd[24 + 24 * e: 48 + 24 * e]
+                hi = min((ch + 1) * cover, n) - 1
+                assert le(ent, 8, 8) == below + ch and le(ent, 16, 8) == perm[hi]
+                want = 0xFFFF if ch == 0 else int(dbit[ch * cover: hi + 1].min())
+                assert le(ent, 4, 2) == want
+        below, off, cover = off, off + lv[l], cover * ip
