@@ -335,6 +335,21 @@ def main():
                             "compressed_ms_per_step": ms, "total_ratio": fms / ms, "full_key_steps": fs,
                             "full_key_keys_per_s": n / (fms * 1e-3)})
         del full
+        # NEXT-3: the paper's 256-byte-node index tree from this build's perm and D_i (pk = 32)
+        ps = cks.paper_tree_shape(n, 0.9)
+        nodes = torch.empty((int(ps.total_nodes), cks.PTREE_NODE_BYTES), dtype=torch.uint8, device=device)
+        cks.paper_tree(keys, builder.perm[:n], builder.dbit[:n], 32, 0.9, out=nodes)
+        e0.record(stream)
+        for _ in range(fs):
+            cks.paper_tree(keys, builder.perm[:n], builder.dbit[:n], 32, 0.9, out=nodes)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        pms = e0.elapsed_time(e1) / fs
+        paper_stats.update({"paper_tree_ms": pms, "paper_tree_nodes": int(ps.total_nodes),
+                            "paper_tree_height": int(ps.height),
+                            "paper_tree_note": "NEXT-3: 256-B nodes, leaf 12/14, inner 8/9 entries (fill 0.9), "
+                                               "pk 32 read from the key rows"})
+        del nodes
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

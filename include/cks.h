@@ -182,6 +182,33 @@ int cks_bulkload_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* 
 int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n,
                  uint32_t fanout, float fill, const cks_tree* out);
 
+/* ---- NEXT-3: the paper's index tree format (Sec. 4.2; Sec. 5.3) -------
+ * Nodes of 256 bytes, leaves first then each level up, numbered from 0; a node holds
+ * floor(max fanout * fill) entries (leaf max 14, non-leaf max 9; fill 0.9 -> 12 / 8). Little-
+ * endian layout:
+ *   header (24 B)  u16 count | u16 level (0 = leaf) | u32 key_bytes | u64 highest key (record
+ *                  id of the node's last key) | u64 0
+ *   leaf           u64 next leaf (node index, all ones for the last leaf) at byte 24, then 14
+ *                  entries of 16 B at 32 + 16 e: u32 partial key | u16 D_i | u16 key length |
+ *                  u64 record id
+ *   non-leaf       9 entries of 24 B at 24 + 24 e: u32 partial key | u16 D-bit | u16 key length
+ *                  | u64 child node index | u64 highest key (record id)
+ * Unused entries and bytes are 0. The partial key holds the pk_bits (<= 32) key bits at
+ * positions D+1 .. D+pk (reading C14; 0 past the key), packed from bit 31 down, where D
+ * is the entry's distinction bit position; with none (first key, equal keys) positions
+ * 0 .. pk-1. A non-leaf entry's D-bit is that of its child's highest key against the previous
+ * entry's highest key at the same level (CKS_DBIT_NONE for the first), equal to the
+ * minimum D_k over the child's keys (Lemma 1).
+ * cks_paper_tree_shape: host arithmetic; fanout = 14, per_node = leaf entries, reserved =
+ * non-leaf entries. cks_paper_tree: keys device u8[n][key_bytes]; perm / dbit from cks_build;
+ * nodes device u8[total_nodes][256]. Asynchronous. */
+#define CKS_PTREE_NODE_BYTES 256
+#define CKS_PTREE_LEAF_FANOUT 14
+#define CKS_PTREE_INNER_FANOUT 9
+int cks_paper_tree_shape(uint64_t n, float fill, cks_tree_shape* out);
+int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, const uint32_t* perm,
+                   const uint16_t* dbit, uint32_t pk_bits, float fill, uint8_t* nodes);
+
 /* ---- fused first build: a1 -> a2 -> a3 -> a4 -> a5 -> a6 -> a7 -> a8 -----------------------
  * The benchmarked step. The superset mask M (or prior_mask) is compressed once; the sort
  * runs by distinguishing prefixes ("sort by distinguishing prefixes",

@@ -58,7 +58,8 @@ class BuildOut(ctypes.Structure):
 EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing", "cks_ctx_set_sort_mode",
            "cks_ctx_stage_ms", "cks_ctx_launches", "cks_ctx_kernel_stats", "cks_strerror", "cks_last_error",
            "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
-           "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_build", "cks_build_host"]
+           "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_paper_tree_shape", "cks_paper_tree",
+           "cks_build", "cks_build_host"]
 
 
 def load_library(path: str | None = None):
@@ -92,6 +93,8 @@ def load_library(path: str | None = None):
     L.cks_adjacent_dbits.argtypes = [p, p, u32, u64, p, u32, p, ctypes.POINTER(u32), p]
     L.cks_bulkload_shape.argtypes = [u64, u32, f32, ctypes.POINTER(TreeShape)]
     L.cks_bulkload.argtypes = [p, p, p, u64, u32, f32, ctypes.POINTER(Tree)]
+    L.cks_paper_tree_shape.argtypes = [u64, f32, ctypes.POINTER(TreeShape)]
+    L.cks_paper_tree.argtypes = [p, p, u64, u32, p, p, u32, f32, p]
     L.cks_build.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     L.cks_build_host.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     for name in EXPORTS:
@@ -277,6 +280,31 @@ def bulkload(perm: torch.Tensor, dbit: torch.Tensor | None, fanout: int = 64, fi
     _check(L, c, L.cks_bulkload(c, _ptr(perm), _ptr(dbit), n, fanout, fill, ctypes.byref(tr)))
     t["shape"] = shape
     return t
+
+
+PTREE_NODE_BYTES = 256
+
+
+def paper_tree_shape(n: int, fill: float = 0.9) -> TreeShape:
+    """NEXT-3 tree shape: per_node = leaf entries, reserved = non-leaf entries."""
+    s = TreeShape()
+    rc = load_library().cks_paper_tree_shape(n, fill, ctypes.byref(s))
+    if rc != CKS_OK:
+        raise CksError(rc, "bad paper-tree shape")
+    return s
+
+
+def paper_tree(keys: torch.Tensor, perm: torch.Tensor, dbit: torch.Tensor, pk_bits: int = 32,
+               fill: float = 0.9, out: torch.Tensor | None = None) -> torch.Tensor:
+    """NEXT-3: the paper's 256-byte-node index tree (include/cks.h layout) as u8[total][256]."""
+    n, B = _keys(keys)
+    L, c = _context(keys.device.index)
+    s = paper_tree_shape(n, fill)
+    T = int(s.total_nodes)
+    if out is None:
+        out = torch.empty((max(T, 1), PTREE_NODE_BYTES), dtype=torch.uint8, device=keys.device)
+    _check(L, c, L.cks_paper_tree(c, _ptr(keys), n, B, _ptr(perm), _ptr(dbit), pk_bits, fill, _ptr(out)))
+    return out[:T]
 
 
 class Builder:

@@ -958,6 +958,53 @@ int cks_bulkload_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* 
     return tree_shape(n, fanout, fill, out);
 }
 
+int cks_paper_tree_shape(uint64_t n, float fill, cks_tree_shape* s) {
+    if (!s || !(fill > 0.f) || fill > 1.f) return CKS_EINVAL;
+    const uint32_t lp = (uint32_t)((double)CKS_PTREE_LEAF_FANOUT * (double)fill);
+    const uint32_t ip = (uint32_t)((double)CKS_PTREE_INNER_FANOUT * (double)fill);
+    if (lp < 2 || ip < 2) return CKS_EINVAL;
+    memset(s, 0, sizeof(*s));
+    s->n = n;
+    s->fanout = CKS_PTREE_LEAF_FANOUT;
+    s->per_node = lp;
+    s->reserved = ip;                                    // entries per non-leaf node
+    uint64_t c = n, off = 0, per = lp;
+    uint32_t h = 0;
+    while (c > 0) {
+        c = (c + per - 1) / per;
+        if (h >= CKS_MAX_LEVELS) return CKS_ERANGE;
+        s->level_nodes[h] = c;
+        s->level_offset[h] = off;
+        off += c;
+        h++;
+        per = ip;
+        if (c <= 1) break;
+    }
+    s->height = h;
+    s->total_nodes = off;
+    s->inner_nodes = h ? off - s->level_nodes[0] : 0;
+    return CKS_OK;
+}
+
+int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm,
+                   const uint16_t* dbit, uint32_t pk_bits, float fill, uint8_t* nodes) {
+    TRY(check_keys(ctx, keys, n, B));
+    if (pk_bits > 32) return fail(ctx, CKS_EINVAL, "pk_bits %u > 32", pk_bits);
+    if (n && (!perm || !dbit || !nodes)) return fail(ctx, CKS_EINVAL, "NULL perm, dbit or nodes with n > 0");
+    cks_tree_shape s;
+    const int rc = cks_paper_tree_shape(n, fill, &s);
+    if (rc != CKS_OK) return fail(ctx, rc, "bad paper-tree shape (fill %f)", (double)fill);
+    if (n == 0) return CKS_OK;
+    CK(cudaSetDevice(ctx->device));
+    TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
+    TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+    int nl = 0;
+    CK(launch_ptree(keys, n, B, perm, dbit, pk_bits, s.per_node, s.reserved, s.level_nodes, s.level_offset,
+                    s.height, nodes, as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl));
+    ctx->launches += (uint64_t)nl;
+    return CKS_OK;
+}
+
 int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
                  float fill, const cks_tree* out) {
     if (!ctx) return CKS_EINVAL;

@@ -168,4 +168,10 @@ cudaError_t launch_bulk_inner(const uint32_t* perm, const uint16_t* rmin_below, 
                               uint32_t* rid, uint16_t* edbit, uint32_t* child, uint64_t inner_off,
                               uint16_t* rmin, int sms, cudaStream_t st);
 
+// NEXT-3 paper-format index tree (k_ptree.cu)
+cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
+                         uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
+                         const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
+                         uint16_t* rmin_b, int sms, cudaStream_t st, int* launches);
+
 }  // namespace cks

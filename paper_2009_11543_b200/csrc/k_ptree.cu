@@ -1,0 +1,141 @@
+// k_ptree.cu -- NEXT-3: the paper's index tree format, built bottom-up from
+// the sorted row ids and the D_i (Sec. 4.2; Sec. 5.3).
+//
+// Node = 256 bytes. Leaf: 24-byte header, 8-byte next pointer, 14 entries of 16 bytes
+// {partial key, distinction bit position, key length, record id}; non-leaf: 24-byte
+// header, 9 entries of 24 bytes {partial key, distinction bit position, key length, child,
+// highest key}. Nodes hold floor(max fanout * fill) entries. The partial key
+// is the pk bits of the key following the entry's distinction bit position (reading
+// C14), read from the key row (option C(b) of P:491: dereference the record). A non-leaf
+// entry's distinction bit position is that of its child's highest key against the previous
+// entry's highest key = the minimum D_k over the child's keys (Lemma 1),
+// carried up the levels as per-node minima. Byte layout: DESIGN.md R16 / include/cks.h.
+#include "cks_internal.h"
+
+namespace cks {
+
+namespace {
+constexpr int kPtThreads = 128;
+
+// pk (<= 32) bits of the B-byte key starting at bit position p0 (bit 0 = MSB of byte 0),
+// left-aligned in a u32; positions past the key read as 0
+__device__ __forceinline__ uint32_t key_bits(const uint8_t* key, uint32_t B, uint32_t p0, uint32_t pk) {
+    if (pk == 0) return 0u;
+    unsigned long long w = 0;                                     // 40-bit window from byte p0/8
+    const uint32_t b0 = p0 >> 3;
+#pragma unroll
+    for (int i = 0; i < 5; i++) {
+        const uint32_t j = b0 + i;
+        w = (w << 8) | (j < B ? key[j] : 0u);
+    }
+    const uint32_t v = (uint32_t)(w >> (8 - (p0 & 7)));         // bits p0 .. p0+31 (window bits 0..31)
+    return pk >= 32 ? v : v & ~(0xFFFFFFFFu >> pk);
+}
+__device__ __forceinline__ uint32_t pk_of(const uint8_t* keys, uint32_t B, uint32_t rid, uint16_t d, uint32_t pk) {
+    return key_bits(keys + (uint64_t)rid * B, B, d == CKS_NONE_INTERNAL ? 0u : (uint32_t)d + 1, pk);
+}
+}  // namespace
+
+// thread per leaf node
+__global__ void __launch_bounds__(kPtThreads)
+k_ptree_leaves(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
+               const uint16_t* __restrict__ dbit, uint32_t pk, uint32_t per, uint64_t nleaves,
+               uint8_t* __restrict__ nodes, uint16_t* __restrict__ rmin) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nleaves; j += (uint64_t)gridDim.x * blockDim.x) {
+        uint4* nd = reinterpret_cast<uint4*>(nodes + j * 256);
+        const uint64_t k0 = j * per, k1 = min(k0 + per, n);
+        uint16_t mn = CKS_NONE_INTERNAL;
+        uint32_t last = 0;
+        for (uint32_t e = 0; e < 14; e++) {
+            const uint64_t k = k0 + e;
+            uint4 ent = make_uint4(0, 0, 0, 0);
+            if (k < k1) {
+                const uint32_t rid = perm[k];
+                const uint16_t d = dbit[k];
+                mn = d < mn ? d : mn;
+                last = rid;
+                ent = make_uint4(pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16), rid, 0u);
+            }
+            nd[2 + e] = ent;                                      // 32 + 16 e
+        }
+        // header {count, level 0, key bytes, highest key, 0} + next leaf
+        const unsigned long long next = j + 1 < nleaves ? j + 1 : ~0ull;
+        nd[0] = make_uint4((uint32_t)(k1 - k0), B, last, 0u);
+        nd[1] = make_uint4(0u, 0u, (uint32_t)next, (uint32_t)(next >> 32));
+        rmin[j] = mn;
+    }
+}
+
+// thread per node of level `level` (>= 1)
+__global__ void __launch_bounds__(kPtThreads)
+k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
+              uint32_t pk, uint32_t per, uint64_t nbelow, uint64_t cover_below, uint64_t below_off, uint64_t nnodes,
+              uint64_t node_off, uint32_t level, const uint16_t* __restrict__ rmin_below, uint16_t* __restrict__ rmin,
+              uint8_t* __restrict__ nodes) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnodes; j += (uint64_t)gridDim.x * blockDim.x) {
+        uint8_t* nd = nodes + (node_off + j) * 256;
+        uint2* w = reinterpret_cast<uint2*>(nd);
+        const uint64_t c0 = j * per, c1 = min(c0 + per, nbelow);
+        uint16_t mn = CKS_NONE_INTERNAL;
+        uint32_t last = 0;
+        for (uint32_t e = 0; e < 9; e++) {
+            const uint64_t ch = c0 + e;
+            uint2 a = make_uint2(0, 0), b = make_uint2(0, 0), c = make_uint2(0, 0);
+            if (ch < c1) {
+                const uint64_t hi = min((ch + 1) * cover_below, n) - 1;       // highest key of the child
+                const uint32_t rid = perm[hi];
+                const uint16_t rm = rmin_below[ch];
+                mn = rm < mn ? rm : mn;
+                const uint16_t d = ch == 0 ? (uint16_t)CKS_NONE_INTERNAL : rm;   // vs the previous entry
+                last = rid;
+                const unsigned long long child = below_off + ch;
+                a = make_uint2(pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16));
+                b = make_uint2((uint32_t)child, (uint32_t)(child >> 32));
+                c = make_uint2(rid, 0u);
+            }
+            w[3 + 3 * e] = a;                                     // 24 + 24 e
+            w[4 + 3 * e] = b;
+            w[5 + 3 * e] = c;
+        }
+        w[0] = make_uint2((uint32_t)(c1 - c0) | (level << 16), B);
+        w[1] = make_uint2(last, 0u);
+        w[2] = make_uint2(0u, 0u);
+        w[30] = make_uint2(0u, 0u);                               // bytes 240..255
+        w[31] = make_uint2(0u, 0u);
+        rmin[j] = mn;
+    }
+}
+
+static unsigned grid_pt(uint64_t work, int sms) {
+    uint64_t g = (work + kPtThreads - 1) / kPtThreads;
+    const uint64_t cap = (uint64_t)sms * 16;
+    if (g > cap) g = cap;
+    return (unsigned)(g ? g : 1);
+}
+
+cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
+                         uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
+                         const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
+                         uint16_t* rmin_b, int sms, cudaStream_t st, int* launches) {
+    *launches = 0;
+    if (n == 0 || height == 0) return cudaSuccess;
+    k_ptree_leaves<<<grid_pt(level_nodes[0], sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
+                                                                       level_nodes[0], nodes, rmin_a);
+    ++*launches;
+    uint64_t cover = leaf_per;
+    uint16_t* below = rmin_a;
+    uint16_t* cur = rmin_b;
+    for (uint32_t l = 1; l < height; l++) {
+        k_ptree_inner<<<grid_pt(level_nodes[l], sms), kPtThreads, 0, st>>>(
+            keys, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
+            level_offset[l], l, below, cur, nodes);
+        ++*launches;
+        cover *= inner_per;
+        uint16_t* t = below;
+        below = cur;
+        cur = t;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace cks

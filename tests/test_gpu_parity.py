@@ -397,3 +397,18 @@ def test_full_key_build():
 def test_sort_mode_rejects():
     with pytest.raises(cks.CksError):
         cks.set_sort_mode(7)
+
+
+# ---- NEXT-3: the paper's index tree format --------------------------------------------------
+
+@pytest.mark.parametrize("cfg,n,pk,fill", [(1, 13, 32, 0.9), (5, 4097, 32, 0.9), (3, 100_003, 32, 0.9),
+                                           (4, 60_000, 17, 0.9), (2, 77_777, 8, 1.0), (1, None, 32, 0.9)])
+def test_paper_tree_vs_oracle(cfg, n, pk, fill):
+    keys = cksgen.config(cfg, n=n)
+    d = dev(keys)
+    b = cks.Builder(keys.shape[0], keys.shape[1], d.device)
+    b(d)
+    nodes = cks.paper_tree(d, b.perm[:keys.shape[0]], b.dbit[:keys.shape[0]], pk_bits=pk, fill=fill)
+    ref = oracle.paper_tree(keys, u32(b.perm)[:keys.shape[0]], u16(b.dbit)[:keys.shape[0]], pk=pk, fill=fill)
+    assert nodes.shape[0] == sum(ref["levels"])
+    assert np.array_equal(nodes.cpu().numpy(), ref["nodes"])

@@ -81,3 +81,12 @@ def test_binding_has_no_cpu_fallback():
             src = open(os.path.join(pkg, f)).read()
             assert "import oracle" not in src and "from oracle" not in src, f
             assert "cksgen" not in src, f
+
+
+def test_paper_tree_shape_host():
+    # NEXT-3 tree shape: host arithmetic against the oracle's level counts (INDBTAB-sized)
+    from paper_2009_11543_b200 import cks
+    s = cks.paper_tree_shape(16_392_000, 0.9)
+    lv = oracle.paper_tree_levels(16_392_000, 12, 8)
+    assert s.height == len(lv) and [int(s.level_nodes[i]) for i in range(s.height)] == lv
+    assert s.per_node == 12 and s.reserved == 8 and int(s.total_nodes) == sum(lv)
