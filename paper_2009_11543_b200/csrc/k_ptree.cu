@@ -36,32 +36,38 @@ __device__ __forceinline__ uint32_t pk_of(const uint8_t* keys, uint32_t B, uint3
 }
 }  // namespace
 
-// thread per leaf node
+// leaves, thread per sorted key k (entry k % per of leaf k / per): the key-row reads of a
+// warp are independent (a thread per node would walk its entries serially)
 __global__ void __launch_bounds__(kPtThreads)
-k_ptree_leaves(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
-               const uint16_t* __restrict__ dbit, uint32_t pk, uint32_t per, uint64_t nleaves,
-               uint8_t* __restrict__ nodes, uint16_t* __restrict__ rmin) {
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nleaves; j += (uint64_t)gridDim.x * blockDim.x) {
+k_ptree_leaf_entries(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
+                     const uint16_t* __restrict__ dbit, uint32_t pk, uint32_t per, uint64_t nleaves,
+                     uint8_t* __restrict__ nodes) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = k / per;
+        const uint32_t e = (uint32_t)(k - j * per);
         uint4* nd = reinterpret_cast<uint4*>(nodes + j * 256);
+        const uint32_t rid = perm[k];
+        const uint16_t d = dbit[k];
+        nd[2 + e] = make_uint4(pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16), rid, 0u);   // 32 + 16 e
+        if (e == 0) {                                             // header, next leaf, unused entries
+            const uint64_t k1 = min(k + per, n);
+            const unsigned long long next = j + 1 < nleaves ? j + 1 : ~0ull;
+            nd[0] = make_uint4((uint32_t)(k1 - k), B, perm[k1 - 1], 0u);
+            nd[1] = make_uint4(0u, 0u, (uint32_t)next, (uint32_t)(next >> 32));
+            for (uint32_t u = (uint32_t)(k1 - k); u < 14; u++) nd[2 + u] = make_uint4(0, 0, 0, 0);
+        }
+    }
+}
+
+// per-leaf minimum of D_k over its keys (the D-bit of its highest key against the previous
+// leaf's, Lemma 1), thread per leaf
+__global__ void __launch_bounds__(kPtThreads)
+k_ptree_leaf_min(const uint16_t* __restrict__ dbit, uint64_t n, uint32_t per, uint64_t nleaves,
+                 uint16_t* __restrict__ rmin) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nleaves; j += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k0 = j * per, k1 = min(k0 + per, n);
         uint16_t mn = CKS_NONE_INTERNAL;
-        uint32_t last = 0;
-        for (uint32_t e = 0; e < 14; e++) {
-            const uint64_t k = k0 + e;
-            uint4 ent = make_uint4(0, 0, 0, 0);
-            if (k < k1) {
-                const uint32_t rid = perm[k];
-                const uint16_t d = dbit[k];
-                mn = d < mn ? d : mn;
-                last = rid;
-                ent = make_uint4(pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16), rid, 0u);
-            }
-            nd[2 + e] = ent;                                      // 32 + 16 e
-        }
-        // header {count, level 0, key bytes, highest key, 0} + next leaf
-        const unsigned long long next = j + 1 < nleaves ? j + 1 : ~0ull;
-        nd[0] = make_uint4((uint32_t)(k1 - k0), B, last, 0u);
-        nd[1] = make_uint4(0u, 0u, (uint32_t)next, (uint32_t)(next >> 32));
+        for (uint64_t k = k0; k < k1; k++) mn = dbit[k] < mn ? dbit[k] : mn;
         rmin[j] = mn;
     }
 }
@@ -108,7 +114,7 @@ k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const ui
 
 static unsigned grid_pt(uint64_t work, int sms) {
     uint64_t g = (work + kPtThreads - 1) / kPtThreads;
-    const uint64_t cap = (uint64_t)sms * 16;
+    const uint64_t cap = (uint64_t)sms * 32;
     if (g > cap) g = cap;
     return (unsigned)(g ? g : 1);
 }
@@ -119,9 +125,10 @@ cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint
                          uint16_t* rmin_b, int sms, cudaStream_t st, int* launches) {
     *launches = 0;
     if (n == 0 || height == 0) return cudaSuccess;
-    k_ptree_leaves<<<grid_pt(level_nodes[0], sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
-                                                                       level_nodes[0], nodes, rmin_a);
-    ++*launches;
+    k_ptree_leaf_entries<<<grid_pt(n, sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
+                                                                 level_nodes[0], nodes);
+    k_ptree_leaf_min<<<grid_pt(level_nodes[0], sms), kPtThreads, 0, st>>>(dbit, n, leaf_per, level_nodes[0], rmin_a);
+    *launches += 2;
     uint64_t cover = leaf_per;
     uint16_t* below = rmin_a;
     uint16_t* cur = rmin_b;
