@@ -50,7 +50,7 @@ struct cks_ctx {
     // scratch
     DevBuf occ, masks8, planeA, planeB, ridA, ridB, hist, base, status, counters, dacc, moff, dbit,
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
-        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, tie, keep, done, mlist, wlist, rcnt, rtot;   // NEXT-1
+        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, tie, keep, done, mlist, wlist, rcnt, rtot;   // NEXT-1
     int algo = -1;                    // LSD pass: 1 = reduce-then-scan (default), 0 = onesweep
                                       // (decoupled look-back; measured slower)
     size_t status_tiles = 0;
@@ -485,6 +485,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             TRY(ensure(ctx, *sb[i], sp * 4));
         }
         TRY(ensure(ctx, ctx->runoff, sp * 4));
+        TRY(ensure(ctx, ctx->runpos, sp * 4));
         TRY(ensure(ctx, ctx->keep, n + 16));
         TRY(ensure(ctx, ctx->done, n + 16));
         TRY(ensure(ctx, ctx->mlist, sp * 4));
@@ -511,13 +512,14 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         uint32_t* segB_ = as<uint32_t>(bi == 0 ? ctx->segA : bi == 1 ? ctx->segB : ctx->segC);
         // (1) the tied runs of the current list
         LAUNCH(launch_ref_compact(tie, nr, pos, as<uint32_t>(ctx->rcnt), as<uint32_t>(ctx->rtot), posA_, segA_,
-                                  as<uint32_t>(ctx->runoff), ctx->stream));
+                                  as<uint32_t>(ctx->runoff), as<uint32_t>(ctx->runpos), ctx->stream));
         uint64_t nn = 0, nseg = 0;
         TRY(counts(&nn, &nseg));
         if (nn == 0) break;
         // (2) finish short runs and runs of equal keys in place
         const int qtop = (int)np - 1 - (int)(o >> 5);            // plane holding bit o
-        LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, posA_, segA_, as<uint32_t>(ctx->runoff), nseg, nn, out->perm,
+        LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, as<uint32_t>(ctx->runpos), segA_, as<uint32_t>(ctx->runoff),
+                                nseg, nn, out->perm,
                                 dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B,
                                 as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->wlist), as<uint32_t>(ctx->rtot) + 12,
                                 ctx->sms, ctx->stream, 0xFFFFFFFFu >> (o & 31)));
@@ -529,7 +531,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             LAUNCH(launch_ref_keep(segA_, as<uint32_t>(ctx->runoff), as<uint8_t>(ctx->done), nn, as<uint8_t>(ctx->keep),
                                    ctx->sms, ctx->stream));
             LAUNCH(launch_ref_compact(as<uint8_t>(ctx->keep), nn, posA_, as<uint32_t>(ctx->rcnt),
-                                      as<uint32_t>(ctx->rtot), posB_, segB_, nullptr, ctx->stream));
+                                      as<uint32_t>(ctx->rtot), posB_, segB_, nullptr, nullptr, ctx->stream));
             TRY(counts(&n2, &nseg2));
         }
         if (log)
@@ -810,7 +812,7 @@ int cks_ctx_destroy(cks_ctx* ctx) {
                       &ctx->dbit, &ctx->rmin0, &ctx->rmin1, &ctx->plan[0], &ctx->plan[1], &ctx->plan[2],
                       &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total,
                       &ctx->pm, &ctx->pd, &ctx->cmp, &ctx->crid, &ctx->crid2, &ctx->posA, &ctx->posB,
-                      &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->tie, &ctx->keep, &ctx->done, &ctx->mlist,
+                      &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->runpos, &ctx->tie, &ctx->keep, &ctx->done, &ctx->mlist,
                       &ctx->wlist,
                       &ctx->rcnt, &ctx->rtot};
     for (DevBuf* b : bufs)

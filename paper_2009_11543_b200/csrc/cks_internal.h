@@ -137,10 +137,12 @@ cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_
                            uint64_t nr, uint32_t cbase, const uint16_t* moff, uint32_t m, uint32_t B,
                            uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st,
                            unsigned long long cmask = ~0ull);
+// run_off / run_pos (NULL: not needed): list index and global position of each run's first key
 cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* pos, uint32_t* cnt, uint32_t* tot,
-                               uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, cudaStream_t st);
+                               uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, uint32_t* run_pos,
+                               cudaStream_t st);
 cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
-                             const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
+                             const uint32_t* run_pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
                              uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* wlist, uint32_t* mcount, int sms,
                              cudaStream_t st, uint32_t fmask);

@@ -156,7 +156,7 @@ k_ref_scan(uint32_t* __restrict__ cnt, uint32_t ntiles, uint32_t* __restrict__ t
 __global__ void __launch_bounds__(kRefThreads)
 k_ref_scatter(const uint8_t* __restrict__ tie, uint64_t nr, const uint32_t* __restrict__ pos,
               const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pos_next, uint32_t* __restrict__ seg_next,
-              uint32_t* __restrict__ run_off) {
+              uint32_t* __restrict__ run_off, uint32_t* __restrict__ run_pos) {
     __shared__ uint32_t s_w[2][kRefThreads / 32];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ltm = (1u << lane) - 1u;
@@ -180,9 +180,13 @@ k_ref_scatter(const uint8_t* __restrict__ tie, uint64_t nr, const uint32_t* __re
         if (mb) {
             const uint32_t o = om + __popc(bm & ltm);
             const uint32_t sg = os + __popc(bs & (ltm | (1u << lane))) - 1;   // runs started so far
-            pos_next[o] = pos ? pos[k] : (uint32_t)k;
+            const uint32_t pk = pos ? pos[k] : (uint32_t)k;
+            pos_next[o] = pk;
             seg_next[o] = sg;
-            if (st && run_off) run_off[sg] = o;
+            if (st && run_off) {
+                run_off[sg] = o;
+                run_pos[sg] = pk;                                     // position of the run's first key
+            }
         }
         om += __popc(bm);
         os += __popc(bs);
@@ -286,7 +290,7 @@ __device__ __forceinline__ bool key_less(const uint32_t (&a)[W], uint32_t ra, co
 // Thread per run: short runs (<= 4, registers only: a fixed network, static indices); longer
 // runs are routed to the warp list, the CTA list or the next LSD round.
 __global__ void __launch_bounds__(kRefThreads)
-k_ref_local(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg,
+k_ref_local(RunCtx R, const uint32_t* __restrict__ run_pos, const uint32_t* __restrict__ run_off, uint64_t nseg,
             uint64_t nn, uint32_t* __restrict__ dacc, uint8_t* __restrict__ done, uint32_t nwords,
             uint32_t* __restrict__ mlist, uint32_t* __restrict__ wlist, uint32_t* __restrict__ mcount,
             uint32_t cta_max) {
@@ -303,9 +307,9 @@ k_ref_local(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restri
         const uint32_t k0 = run_off[s];
         const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
         const uint32_t L = k1 - k0;
+        const uint32_t p0 = run_pos[s];                               // position of the run's first key
         uint8_t fin = 1;
         if (L <= kLocal && Wr <= W) {
-            const uint32_t p0 = pos[k0];
             uint32_t r[4], w[4][W];
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -332,7 +336,6 @@ k_ref_local(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restri
         } else if (L <= kLazyRun && !R.carried && (Wr > W || L <= kLocal)) {
             // more remaining planes than registers: an insertion sort on row ids, words read
             // from P_M by row as the comparisons need them (most pairs differ in the first)
-            const uint32_t p0 = pos[k0];
             auto cmp = [&](uint32_t a, uint32_t b, uint32_t* tt) -> int {
                 for (int c = 0; c < Wr; c++) {
                     const uint32_t wa = rem_word(R, c, 0, a), wb = rem_word(R, c, 0, b);
@@ -384,7 +387,7 @@ k_ref_local(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restri
 // Warp per run (5..32 keys): lane j holds element j (padding sorts last); bitonic network by
 // shuffles; lane j writes the j-th smallest and its D_i against lane j-1's element.
 __global__ void __launch_bounds__(kRefThreads)
-k_ref_warp(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg,
+k_ref_warp(RunCtx R, const uint32_t* __restrict__ run_pos, const uint32_t* __restrict__ run_off, uint64_t nseg,
            uint64_t nn, uint32_t* __restrict__ dacc, uint32_t nwords, const uint32_t* __restrict__ wlist,
            const uint32_t* __restrict__ mcount) {
     constexpr int W = kRegWords;
@@ -400,7 +403,7 @@ k_ref_warp(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restric
         const uint32_t k0 = run_off[s];
         const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
         const uint32_t L = k1 - k0;
-        const uint32_t p0 = pos[k0];
+        const uint32_t p0 = run_pos[s];
         uint32_t r = 0xFFFFFFFFu, w[W];
 #pragma unroll
         for (int c = 0; c < W; c++) w[c] = 0xFFFFFFFFu;
@@ -444,7 +447,7 @@ k_ref_warp(RunCtx R, const uint32_t* __restrict__ pos, const uint32_t* __restric
 // the D_i (first differing remaining bit) are written at the run's positions.
 __global__ void __launch_bounds__(kRefThreads)
 k_ref_cta(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* __restrict__ moff,
-          const uint32_t* __restrict__ pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
+          const uint32_t* __restrict__ run_pos, const uint32_t* __restrict__ run_off, uint64_t nseg, uint64_t nn,
           uint32_t* __restrict__ perm, uint16_t* __restrict__ dbit, uint32_t* __restrict__ dacc,
           uint32_t* __restrict__ carried, uint32_t nwords, const uint32_t* __restrict__ mlist,
           const uint32_t* __restrict__ mcount, uint32_t fmask) {
@@ -461,7 +464,7 @@ k_ref_cta(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, int qtop
         const uint32_t k0 = run_off[s];
         const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
         const uint32_t L = k1 - k0;
-        const uint32_t p0 = pos[k0];
+        const uint32_t p0 = run_pos[s];
         uint32_t P2 = 1;
         while (P2 < L) P2 <<= 1;
         __syncthreads();
@@ -582,17 +585,18 @@ cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_
 }
 
 cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* pos, uint32_t* cnt, uint32_t* tot,
-                               uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, cudaStream_t st) {
+                               uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, uint32_t* run_pos,
+                               cudaStream_t st) {
     const uint64_t tiles = ref_tiles(nr);
     if (tiles == 0) return cudaMemsetAsync(tot, 0, 8, st);
     k_ref_count<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, cnt);
     k_ref_scan<<<1, 1024, 0, st>>>(cnt, (uint32_t)tiles, tot);
-    k_ref_scatter<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, pos, cnt, pos_next, seg_next, run_off);
+    k_ref_scatter<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, pos, cnt, pos_next, seg_next, run_off, run_pos);
     return cudaGetLastError();
 }
 
 cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
-                             const uint32_t* pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
+                             const uint32_t* run_pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,
                              uint32_t* carried, uint32_t B, uint32_t* mlist, uint32_t* wlist, uint32_t* mcount, int sms,
                              cudaStream_t st, uint32_t fmask) {
@@ -602,14 +606,14 @@ cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, in
     if (nseg == 0) return cudaGetLastError();
     const uint32_t nwords = (8 * B + 31) / 32;
     RunCtx R{pm, pitch, np, qtop, fmask, moff, perm, dbit, carried};
-    k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(R, pos, run_off, nseg, nn, dacc, done, nwords, mlist,
+    k_ref_local<<<grid_of(nseg, sms), kRefThreads, 0, st>>>(R, run_pos, run_off, nseg, nn, dacc, done, nwords, mlist,
                                                             wlist, mcount, cta_max());
     if (qtop + 1 <= kRegWords)
-        k_ref_warp<<<(unsigned)(sms * 8), kRefThreads, 0, st>>>(R, pos, run_off, nseg, nn, dacc, nwords, wlist, mcount);
+        k_ref_warp<<<(unsigned)(sms * 8), kRefThreads, 0, st>>>(R, run_pos, run_off, nseg, nn, dacc, nwords, wlist, mcount);
     if (qtop + 1 <= (int)kCtaWords) {
         const size_t smem = (size_t)kCta * 4 * (qtop + 2) + (size_t)kCta * 2;
         raise_smem_limit((const void*)k_ref_cta, smem);
-        k_ref_cta<<<(unsigned)(sms * 4), kRefThreads, smem, st>>>(pm, pitch, np, qtop, moff, pos, run_off, nseg, nn,
+        k_ref_cta<<<(unsigned)(sms * 4), kRefThreads, smem, st>>>(pm, pitch, np, qtop, moff, run_pos, run_off, nseg, nn,
                                                                   perm, dbit, dacc, carried, nwords, mlist, mcount,
                                                                   fmask);
     }
