@@ -42,18 +42,14 @@ struct cks_ctx {
     int nkev = 0;
     char err[512] = {0};
     uint64_t launches = 0;
-    uint32_t epoch = 1;
     bool timing = false;
     bool timed = false;
     cudaEvent_t ev[ST_N] = {};
     cudaEvent_t plan_ev[3] = {};      // guards the pinned staging slots
     // scratch
-    DevBuf occ, masks8, planeA, planeB, ridA, ridB, hist, base, status, counters, dacc, moff, dbit,
+    DevBuf occ, masks8, planeA, planeB, ridA, ridB, dacc, moff, dbit,
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
         pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, tie, keep, done, mlist, wlist, rcnt, rtot;   // NEXT-1
-    int algo = -1;                    // LSD pass: 1 = reduce-then-scan (default), 0 = onesweep
-                                      // (decoupled look-back; measured slower)
-    size_t status_tiles = 0;
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
     uint16_t* h_moff = nullptr;
@@ -222,36 +218,11 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
     TRY(ensure(ctx, ctx->planeB, pbytes));
     TRY(ensure(ctx, ctx->ridA, sp * 4));
     TRY(ensure(ctx, ctx->ridB, sp * 4));
-    TRY(ensure(ctx, ctx->hist, (size_t)Pfull * 256 * 4));
-    TRY(ensure(ctx, ctx->base, (size_t)Pfull * 256 * 4));
-    TRY(ensure(ctx, ctx->counters, (size_t)Pfull * 4));
-    if (ctx->algo < 0) {
-        const char* e = getenv("CKS_SORT_ALGO");
-        ctx->algo = e ? atoi(e) : 1;
-    }
-    if (ctx->algo == 0) {
-        const uint64_t tiles = onesweep_tiles(n);
-        if (ctx->status_tiles < tiles) {
-            TRY(ensure(ctx, ctx->status, (size_t)tiles * 256 * 8, /*zero=*/true));
-            ctx->status_tiles = ctx->status.cap / (256 * 8);
-        }
-    }
     uint64_t lsd_tiles = 0, lsd_chunks = 0;
-    if (ctx->algo != 0) {
-        lsd_sizes(n, &lsd_tiles, &lsd_chunks);
-        TRY(ensure(ctx, ctx->tile_off, (size_t)lsd_tiles * 256 * 4));
-        TRY(ensure(ctx, ctx->chunk_tot, (size_t)lsd_chunks * 256 * 4));
-        TRY(ensure(ctx, ctx->total, 256 * 4, /*zero=*/true));    // then kept zero by every downsweep
-    }
-    if (ctx->algo == 0) {
-        CK(cudaMemsetAsync(ctx->hist.p, 0, (size_t)Pfull * 256 * 4, ctx->stream));
-        CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)Pfull * 4, ctx->stream));
-        int hl = 0;
-        CK(launch_hist(in_planes, in_pitch, n, key_passes, in_rid, rid_passes, as<uint32_t>(ctx->hist), ctx->sms,
-                       ctx->stream, &hl));
-        ctx->launches += (uint64_t)hl;
-        LAUNCH(launch_scan(as<uint32_t>(ctx->hist), Pfull, as<uint32_t>(ctx->base), ctx->stream));
-    }
+    lsd_sizes(n, &lsd_tiles, &lsd_chunks);
+    TRY(ensure(ctx, ctx->tile_off, (size_t)lsd_tiles * 256 * 4));
+    TRY(ensure(ctx, ctx->chunk_tot, (size_t)lsd_chunks * 256 * 4));
+    TRY(ensure(ctx, ctx->total, 256 * 4, /*zero=*/true));        // then kept zero by every downsweep
     if (mark_stages) mark(ctx, ST_HIST);
 
     const uint32_t* cur_p = in_planes;
@@ -263,73 +234,43 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
         uint32_t* out_p = odd ? as<uint32_t>(ctx->planeA) : (last && final_planes ? final_planes : as<uint32_t>(ctx->planeB));
         uint64_t out_pitch = (last && final_planes && !odd) ? final_pitch : sp;
         uint32_t* out_r = last ? final_rid : (odd ? as<uint32_t>(ctx->ridA) : as<uint32_t>(ctx->ridB));
-        OnesweepArgs a;
-        memset(&a, 0, sizeof(a));
-        a.in_planes = cur_p;
-        a.out_planes = out_p;
-        a.in_rid = cur_r;
-        a.out_rid = out_r;
-        a.n = n;
-        a.in_pitch = cur_pitch;
-        a.out_pitch = out_pitch;
-        a.nplanes = np;
-        uint32_t hist_index;
+        LsdPassArgs la;
+        memset(&la, 0, sizeof(la));
+        la.in_planes = cur_p;
+        la.out_planes = out_p;
+        la.in_rid = cur_r;
+        la.out_rid = out_r;
+        la.n = n;
+        la.in_pitch = cur_pitch;
+        la.out_pitch = out_pitch;
+        la.nplanes = np;
         if (in_rid && t < rid_passes) {                  // row-id digits first (least significant)
-            a.digit_plane = -1;
-            a.shift = 8 * t;
-            hist_index = key_passes + t;
+            la.digit_plane = -1;
+            la.shift = 8 * t;
         } else {
-            uint32_t p = (in_rid ? t - rid_passes : t) + digit0;
-            a.digit_plane = (int32_t)(p >> 2);
-            a.shift = 8 * (p & 3);
-            hist_index = p;
+            const uint32_t p = (in_rid ? t - rid_passes : t) + digit0;
+            la.digit_plane = (int32_t)(p >> 2);
+            la.shift = 8 * (p & 3);
         }
-        if (ctx->algo != 0) {
-            LsdPassArgs la;
-            memset(&la, 0, sizeof(la));
-            la.in_planes = cur_p;
-            la.out_planes = out_p;
-            la.in_rid = cur_r;
-            la.out_rid = out_r;
-            la.n = n;
-            la.in_pitch = cur_pitch;
-            la.out_pitch = out_pitch;
-            la.nplanes = np;
-            la.digit_plane = a.digit_plane;
-            la.shift = a.shift;
-            la.tile_off = as<uint32_t>(ctx->tile_off);
-            la.chunk_tot = as<uint32_t>(ctx->chunk_tot);
-            la.total = as<uint32_t>(ctx->total);
-            int nl = 0;
-            LsdAux aux;
-            aux.stream = ctx->aux_stream;
-            aux.fork = ctx->aux_ev[0];
-            aux.join = ctx->aux_ev[1];
-            const int ke = ctx->nkev;
-            static const bool no_kev = getenv("CKS_NO_KERNEL_EVENTS") != nullptr;   // experiments only
-            if (ctx->timing && !no_kev && ke < cks_ctx::kMaxKev) {
-                aux.ws_begin = ctx->kev[2 * ke];
-                aux.ws_end = ctx->kev[2 * ke + 1];
-                ctx->kbytes[ke] = 0.0;
-                aux.ws_bytes = &ctx->kbytes[ke];
-            }
-            CK(launch_lsd_pass(la, ctx->sms, ctx->stream, aux, &nl));
-            if (aux.ws_bytes && ctx->kbytes[ke] > 0.0) ctx->nkev++;
-            ctx->launches += (uint64_t)nl;
-            cur_p = out_p;
-            cur_pitch = out_pitch;
-            cur_r = out_r;
-            continue;
+        la.tile_off = as<uint32_t>(ctx->tile_off);
+        la.chunk_tot = as<uint32_t>(ctx->chunk_tot);
+        la.total = as<uint32_t>(ctx->total);
+        LsdAux aux;
+        aux.stream = ctx->aux_stream;
+        aux.fork = ctx->aux_ev[0];
+        aux.join = ctx->aux_ev[1];
+        const int ke = ctx->nkev;
+        static const bool no_kev = getenv("CKS_NO_KERNEL_EVENTS") != nullptr;   // experiments only
+        if (ctx->timing && !no_kev && ke < cks_ctx::kMaxKev) {
+            aux.ws_begin = ctx->kev[2 * ke];
+            aux.ws_end = ctx->kev[2 * ke + 1];
+            ctx->kbytes[ke] = 0.0;
+            aux.ws_bytes = &ctx->kbytes[ke];
         }
-        a.bucket_base = as<uint32_t>(ctx->base) + (size_t)hist_index * 256;
-        a.tile_counter = as<uint32_t>(ctx->counters) + t;
-        a.status = as<unsigned long long>(ctx->status);
-        if (ctx->epoch >= 0x7FFFFFF0u) {                 // flag namespace exhausted: reset
-            CK(cudaMemsetAsync(ctx->status.p, 0, ctx->status.cap, ctx->stream));
-            ctx->epoch = 1;
-        }
-        a.epoch = ctx->epoch++;
-        LAUNCH(launch_onesweep(a, ctx->stream));
+        int nl = 0;
+        CK(launch_lsd_pass(la, ctx->sms, ctx->stream, aux, &nl));
+        if (aux.ws_bytes && ctx->kbytes[ke] > 0.0) ctx->nkev++;
+        ctx->launches += (uint64_t)nl;
         cur_p = out_p;
         cur_pitch = out_pitch;
         cur_r = out_r;
@@ -808,7 +749,7 @@ int cks_ctx_destroy(cks_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->occ, &ctx->masks8, &ctx->planeA, &ctx->planeB, &ctx->ridA, &ctx->ridB,
-                      &ctx->hist, &ctx->base, &ctx->status, &ctx->counters, &ctx->dacc, &ctx->moff,
+                      &ctx->dacc, &ctx->moff,
                       &ctx->dbit, &ctx->rmin0, &ctx->rmin1, &ctx->plan[0], &ctx->plan[1], &ctx->plan[2],
                       &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total,
                       &ctx->pm, &ctx->pd, &ctx->cmp, &ctx->crid, &ctx->crid2, &ctx->posA, &ctx->posB,

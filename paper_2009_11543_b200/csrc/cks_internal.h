@@ -63,36 +63,6 @@ cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const G
 cudaError_t launch_repack(const uint32_t* in_planes, uint64_t in_pitch, uint64_t n, const GatherPlan* dplan,
                           uint32_t nsteps, uint32_t out_planes, uint32_t* out, uint64_t out_pitch, int sms,
                           cudaStream_t st);
-// histograms of all LSD digits: digit p = bits [8p, 8p+8) of P (p < key_passes) followed
-// by, if rid != NULL, the row-id digits (rid_passes of them) at indices key_passes+.
-cudaError_t launch_hist(const uint32_t* planes, uint64_t pitch, uint64_t n, uint32_t key_passes,
-                        const uint32_t* rid, uint32_t rid_passes, uint32_t* hist, int sms,
-                        cudaStream_t st, int* launches);
-cudaError_t launch_scan(const uint32_t* hist, uint32_t passes, uint32_t* base, cudaStream_t st);
-
-struct OnesweepArgs {
-    const uint32_t* in_planes;   // plane q at in_planes + q*in_pitch
-    uint32_t* out_planes;        // plane q at out_planes + q*out_pitch
-    const uint32_t* in_rid;      // NULL = implicit row id (input index)
-    uint32_t* out_rid;
-    uint64_t n;
-    uint64_t in_pitch;
-    uint64_t out_pitch;
-    uint32_t nplanes;            // planes carried
-    int32_t digit_plane;         // plane holding the digit; -1 = digit taken from the row id
-    uint32_t shift;              // digit = (word >> shift) & 0xFF
-    const uint32_t* bucket_base; // u32[256] global exclusive bases of this pass
-    uint32_t* tile_counter;      // zeroed before the pass
-    unsigned long long* status;  // u64[num_tiles][256] look-back words
-    uint32_t epoch;              // flag namespace of this pass
-    uint32_t slots;              // shared-memory stream slots (set by the launcher)
-    uint32_t tma;                // 1 = inputs aligned for 1-D bulk copies (set by the launcher)
-    uint32_t debug;              // timing experiments only (CKS_OS_DEBUG): bit0 skip look-back, bit1 skip streams > 0
-};
-cudaError_t launch_onesweep(const OnesweepArgs& a, cudaStream_t st);
-uint64_t onesweep_tiles(uint64_t n);
-uint64_t onesweep_tile_keys();
-
 // Reduce-then-scan LSD pass (k_lsd.cu): upsweep -> chunk scan -> persistent downsweep.
 struct LsdPassArgs {
     const uint32_t* in_planes;
