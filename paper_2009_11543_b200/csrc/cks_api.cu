@@ -49,7 +49,7 @@ struct cks_ctx {
     // scratch
     DevBuf occ, masks8, planeA, planeB, ridA, ridB, dacc, moff, dbit,
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
-        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, tie, keep, done, mlist, wlist, rcnt, rtot;   // NEXT-1
+        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, runoff2, runpos2, tie, keep, done, mlist, wlist, rcnt, rtot;   // NEXT-1
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
     uint16_t* h_moff = nullptr;
@@ -427,6 +427,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         }
         TRY(ensure(ctx, ctx->runoff, sp * 4));
         TRY(ensure(ctx, ctx->runpos, sp * 4));
+        TRY(ensure(ctx, ctx->runoff2, sp * 4));
+        TRY(ensure(ctx, ctx->runpos2, sp * 4));
         TRY(ensure(ctx, ctx->keep, n + 16));
         TRY(ensure(ctx, ctx->done, n + 16));
         TRY(ensure(ctx, ctx->mlist, sp * 4));
@@ -464,38 +466,48 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
                                 dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B,
                                 as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->wlist), as<uint32_t>(ctx->rtot) + 12,
                                 ctx->sms, ctx->stream, 0xFFFFFFFFu >> (o & 31)));
-        // (3) the runs left for an LSD round (none: done)
-        CK(cudaMemcpyAsync(ctx->h_tot, as<uint32_t>(ctx->rtot) + 12, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        // (3) the runs left for a round on the next 64 bits (none: done)
+        CK(cudaMemcpyAsync(ctx->h_tot, as<uint32_t>(ctx->rtot) + 12, 16, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        const uint32_t maxlong = ctx->h_tot[3];
         uint64_t n2 = 0, nseg2 = 0;
         if (ctx->h_tot[1] > 0) {
             LAUNCH(launch_ref_keep(segA_, as<uint32_t>(ctx->runoff), as<uint8_t>(ctx->done), nn, as<uint8_t>(ctx->keep),
                                    ctx->sms, ctx->stream));
             LAUNCH(launch_ref_compact(as<uint8_t>(ctx->keep), nn, posA_, as<uint32_t>(ctx->rcnt),
-                                      as<uint32_t>(ctx->rtot), posB_, segB_, nullptr, nullptr, ctx->stream));
+                                      as<uint32_t>(ctx->rtot), posB_, segB_, as<uint32_t>(ctx->runoff2),
+                                      as<uint32_t>(ctx->runpos2), ctx->stream));
             TRY(counts(&n2, &nseg2));
         }
         if (log)
-            fprintf(stderr, "[cks refine] round %u: %llu tied keys in %llu runs; %llu keys in %llu runs left for LSD\n",
-                    r, (unsigned long long)nn, (unsigned long long)nseg, (unsigned long long)n2,
-                    (unsigned long long)nseg2);
+            fprintf(stderr, "[cks refine] round %u: %llu tied keys in %llu runs; %llu keys in %llu runs (longest %u) "
+                    "left for the next chunk\n", r, (unsigned long long)nn, (unsigned long long)nseg,
+                    (unsigned long long)n2, (unsigned long long)nseg2, maxlong);
         out->refined_keys += nn;
         if (n2 == 0) break;
         out->rounds = r + 1;
-        // (4) LSD round: the left runs by (run, chunk r)
+        // (4) the left runs by (run, 64-bit chunk at o): one CTA per run when every run fits,
+        // else an LSD round over the compact list
         const uint64_t cp = scratch_pitch(n2);
         TRY(ensure(ctx, ctx->cmp, (size_t)3 * cp * 4));
         TRY(ensure(ctx, ctx->crid, cp * 4));
         TRY(ensure(ctx, ctx->crid2, cp * 4));
-        LAUNCH(launch_ref_gather(pm, sp, np, o, posB_, segB_, out->perm, n2, as<uint32_t>(ctx->cmp), cp,
-                                 as<uint32_t>(ctx->crid), ctx->sms, ctx->stream));
-        const uint32_t segbits = nseg2 > 1 ? 32u - (uint32_t)__builtin_clz((uint32_t)(nseg2 - 1)) : 0u;
-        const uint32_t d0 = o + 64 > m ? (o + 64 - m) / 8 : 0;   // digits past the last mask bit are zero
         const uint32_t* sv = nullptr;
         uint64_t svp = cp;
-        out->passes += 8 + (segbits + 7) / 8 - d0;
-        TRY(run_sort(ctx, as<uint32_t>(ctx->cmp), cp, 3, 8 + (segbits + 7) / 8, n2, as<uint32_t>(ctx->crid), 0,
-                     nullptr, 0, as<uint32_t>(ctx->crid2), &sv, &svp, d0, false));
+        if (maxlong <= kChunkCtaKeys) {
+            LAUNCH(launch_ref_cta_chunk(pm, sp, np, o, out->perm, as<uint32_t>(ctx->runoff2), as<uint32_t>(ctx->runpos2),
+                                        nseg2, n2, as<uint32_t>(ctx->cmp), cp, as<uint32_t>(ctx->crid2), ctx->sms,
+                                        ctx->stream));
+            sv = as<uint32_t>(ctx->cmp);
+        } else {
+            LAUNCH(launch_ref_gather(pm, sp, np, o, posB_, segB_, out->perm, n2, as<uint32_t>(ctx->cmp), cp,
+                                     as<uint32_t>(ctx->crid), ctx->sms, ctx->stream));
+            const uint32_t segbits = nseg2 > 1 ? 32u - (uint32_t)__builtin_clz((uint32_t)(nseg2 - 1)) : 0u;
+            const uint32_t d0 = o + 64 > m ? (o + 64 - m) / 8 : 0;   // digits past the last mask bit are zero
+            out->passes += 8 + (segbits + 7) / 8 - d0;
+            TRY(run_sort(ctx, as<uint32_t>(ctx->cmp), cp, 3, 8 + (segbits + 7) / 8, n2, as<uint32_t>(ctx->crid), 0,
+                         nullptr, 0, as<uint32_t>(ctx->crid2), &sv, &svp, d0, false));
+        }
         LAUNCH(launch_ref_put(out->perm, posB_, as<uint32_t>(ctx->crid2), n2, pm, sp, np, carried, ctx->sms,
                               ctx->stream));
         LAUNCH(launch_ref_adj(sv, sv + svp, sv + 2 * svp, posB_, n2, o, moff, m, B, dbit, tie, dacc, false, ctx->sms,
@@ -753,7 +765,8 @@ int cks_ctx_destroy(cks_ctx* ctx) {
                       &ctx->dbit, &ctx->rmin0, &ctx->rmin1, &ctx->plan[0], &ctx->plan[1], &ctx->plan[2],
                       &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total,
                       &ctx->pm, &ctx->pd, &ctx->cmp, &ctx->crid, &ctx->crid2, &ctx->posA, &ctx->posB,
-                      &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->runpos, &ctx->tie, &ctx->keep, &ctx->done, &ctx->mlist,
+                      &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->runpos, &ctx->runoff2, &ctx->runpos2,
+                      &ctx->tie, &ctx->keep, &ctx->done, &ctx->mlist,
                       &ctx->wlist,
                       &ctx->rcnt, &ctx->rtot};
     for (DevBuf* b : bufs)

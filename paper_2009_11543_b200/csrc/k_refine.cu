@@ -374,8 +374,9 @@ k_ref_local(RunCtx R, const uint32_t* __restrict__ run_pos, const uint32_t* __re
         } else if (L <= cta_max && Wr <= (int)kCtaWords) {
             mlist[atomicAdd(mcount, 1u)] = (uint32_t)s;
         } else {
-            fin = 0;                                                 // long run: next LSD round
+            fin = 0;                                                 // long run: next round
             atomicAdd(mcount + 1, 1u);
+            atomicMax(mcount + 3, L);
         }
         done[s] = fin;
     }
@@ -536,6 +537,64 @@ k_ref_keep(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ run_of
     }
 }
 
+// A refinement round without LSD passes, when every long run fits a CTA: CTA per run (of the
+// list made by the second compaction, runs in list order), its members' 64-bit chunk at bit o
+// (from P_M by row id) and row ids staged in shared memory and bitonic-sorted by (chunk, row
+// id) -- the stable order, as the (run, chunk) LSD round would produce -- then written in the
+// LSD round's output format (compact planes lo, hi, run; sorted row ids) at the run's list range.
+constexpr uint32_t kChunkCta = kChunkCtaKeys;
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_cta_chunk(const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, uint32_t o,
+                const uint32_t* __restrict__ perm, const uint32_t* __restrict__ run_off,
+                const uint32_t* __restrict__ run_pos, uint64_t nseg, uint64_t nn, uint32_t* __restrict__ out,
+                uint64_t opitch, uint32_t* __restrict__ orid) {
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* s_hi = s_dyn;                                          // [kChunkCta]
+    uint32_t* s_lo = s_hi + kChunkCta;
+    uint32_t* s_row = s_lo + kChunkCta;
+    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_row + kChunkCta);
+    for (uint64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+        const uint32_t k0 = run_off[s];
+        const uint32_t k1 = s + 1 < nseg ? run_off[s + 1] : (uint32_t)nn;
+        const uint32_t L = k1 - k0, p0 = run_pos[s];
+        uint32_t P2 = 1;
+        while (P2 < L) P2 <<= 1;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) {
+            const uint32_t row = perm[p0 + j];
+            s_row[j] = row;
+            s_hi[j] = pm_bits32(pm, pitch, np, o, row);
+            s_lo[j] = pm_bits32(pm, pitch, np, o + 32, row);
+        }
+        for (uint32_t j = threadIdx.x; j < P2; j += blockDim.x) s_idx[j] = (uint16_t)j;
+        __syncthreads();
+        auto less = [&](uint32_t a, uint32_t b) -> bool {            // padding (>= L) sorts last
+            if (a >= L || b >= L) return a < b;
+            if (s_hi[a] != s_hi[b]) return s_hi[a] < s_hi[b];
+            if (s_lo[a] != s_lo[b]) return s_lo[a] < s_lo[b];
+            return s_row[a] < s_row[b];
+        };
+        for (uint32_t size = 2; size <= P2; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = threadIdx.x; i < P2 / 2; i += blockDim.x) {
+                    const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const uint32_t a = s_idx[lo], b = s_idx[hi];
+                    if (less(b, a) == up) { s_idx[lo] = (uint16_t)b; s_idx[hi] = (uint16_t)a; }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) {
+            const uint32_t a = s_idx[j];
+            out[k0 + j] = s_lo[a];
+            out[opitch + k0 + j] = s_hi[a];
+            out[2 * opitch + k0 + j] = (uint32_t)s;
+            orid[k0 + j] = s_row[a];
+        }
+    }
+}
+
 // sorted row ids back to their run's positions (and, when P_M is carried in sorted order,
 // its planes for those rows)
 __global__ void __launch_bounds__(kRefThreads)
@@ -602,7 +661,7 @@ cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, in
                              cudaStream_t st, uint32_t fmask) {
     (void)seg;
     (void)keep;
-    cudaMemsetAsync(mcount, 0, 12, st);                          // medium runs, long runs, warp runs
+    cudaMemsetAsync(mcount, 0, 16, st);                          // medium, long, warp runs; longest long run
     if (nseg == 0) return cudaGetLastError();
     const uint32_t nwords = (8 * B + 31) / 32;
     RunCtx R{pm, pitch, np, qtop, fmask, moff, perm, dbit, carried};
@@ -632,6 +691,18 @@ cudaError_t launch_ref_gather(const uint32_t* pm, uint64_t pitch, uint32_t np, u
                               uint32_t* orid, int sms, cudaStream_t st) {
     if (nr == 0) return cudaSuccess;
     k_ref_gather<<<grid_of(nr, sms), kRefThreads, 0, st>>>(pm, pitch, np, o, pos, seg, perm, nr, out, opitch, orid);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_cta_chunk(const uint32_t* pm, uint64_t pitch, uint32_t np, uint32_t o, const uint32_t* perm,
+                                 const uint32_t* run_off, const uint32_t* run_pos, uint64_t nseg, uint64_t nn,
+                                 uint32_t* out, uint64_t opitch, uint32_t* orid, int sms, cudaStream_t st) {
+    if (nseg == 0) return cudaSuccess;
+    const uint64_t g = nseg < (uint64_t)sms * 4 ? nseg : (uint64_t)sms * 4;
+    const size_t smem = (size_t)kChunkCta * 14;
+    raise_smem_limit((const void*)k_ref_cta_chunk, smem);
+    k_ref_cta_chunk<<<(unsigned)g, kRefThreads, smem, st>>>(pm, pitch, np, o, perm, run_off, run_pos, nseg, nn, out,
+                                                            opitch, orid);
     return cudaGetLastError();
 }
 

@@ -412,3 +412,13 @@ def test_paper_tree_vs_oracle(cfg, n, pk, fill):
     ref = oracle.paper_tree(keys, u32(b.perm)[:keys.shape[0]], u16(b.dbit)[:keys.shape[0]], pk=pk, fill=fill)
     assert nodes.shape[0] == sum(ref["levels"])
     assert np.array_equal(nodes.cpu().numpy(), ref["nodes"])
+
+
+@pytest.mark.parametrize("seed", [4, 5])
+def test_refine_chunk_cta_rounds(seed):
+    # 64-byte keys (D+ = 512 bits: more remaining planes than the CTA tier takes), runs of
+    # ~1.5k keys tied on the first 80 bits: the long runs fit a CTA, so the next rounds sort
+    # them by one CTA each instead of LSD passes (k_ref_cta_chunk)
+    keys = hier_keys(60_000, [256] * 64, seed=seed, groups=(40, 7), dup_rows=300)
+    r = cks.build(dev(keys))
+    check_build(keys, r)
