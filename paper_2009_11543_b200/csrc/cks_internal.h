@@ -39,6 +39,7 @@ cudaError_t raise_smem_limit(const void* kernel, size_t bytes);
 
 // Host-side planning (cks_plan.cpp).
 void plan_compress(const uint8_t* mask, uint32_t key_bytes, GatherPlan* plan);
+void move_masks_left(uint32_t mask, uint32_t mv[5]);
 void plan_repack(const uint32_t* sub_words /* u32[np_in], bit b of word q = P_M bit 32q+b kept */,
                  uint32_t np_in, GatherPlan* plan);
 

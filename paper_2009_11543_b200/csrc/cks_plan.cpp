@@ -43,6 +43,20 @@ static void move_masks(uint32_t m, uint32_t mv[5]) {
     }
 }
 
+// mirror image: the selected bits end left-aligned (top popcount(m) bits), each step moving
+// bits LEFT by 2^k, so a step is x + (x & mv) * (2^(2^k) - 1) -- one multiply-add
+static uint32_t rev32(uint32_t x) {
+    uint32_t r = 0;
+    for (int i = 0; i < 32; i++) r |= ((x >> i) & 1u) << (31 - i);
+    return r;
+}
+
+void move_masks_left(uint32_t m, uint32_t mv[5]) {
+    uint32_t r[5];
+    move_masks(rev32(m), r);
+    for (int k = 0; k < 5; k++) mv[k] = rev32(r[k]);
+}
+
 static void add_step(GatherPlan* plan, uint32_t src, uint32_t mask) {
     GatherStep& s = plan->step[plan->nsteps++];
     s.src = src;

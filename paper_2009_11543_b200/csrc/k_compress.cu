@@ -183,12 +183,24 @@ __device__ __forceinline__ void load_key(const uint8_t* kp, uint32_t (&w)[B / 4]
     }
 }
 
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
 // KPT keys per thread per iteration, all loads issued before any gather: more bytes in
 // flight (the row-list variant's loads are random rows behind a dependent perm load).
-template <int B, int KPT, bool SKIP>
+// The gather runs mirrored (move_masks_left): each field ends left-aligned in its word and
+// a step is one multiply-add, x + (x & mv) * (2^(2^s) - 1) (the moved bits land on zeros,
+// so the add is the OR of the shifted bits), which runs on the FMA pipe and halves the
+// integer-ALU work that bounds this kernel; the fields are appended from the most
+// significant end of P down, plane np-1 first, after `toppad` zero bits.
+template <int B, int KPT>
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_fixed(const uint8_t* __restrict__ keys, uint64_t n, const __grid_constant__ FixedPlan<B / 4> plan,
-                 uint32_t* __restrict__ planes, uint64_t pitch, uint32_t lead, const uint32_t* __restrict__ rows) {
+                 uint32_t* __restrict__ planes, uint64_t pitch, uint32_t np, uint32_t toppad,
+                 const uint32_t* __restrict__ rows) {
     constexpr int NW = B / 4;
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += T * KPT) {
@@ -206,48 +218,44 @@ k_compress_fixed(const uint8_t* __restrict__ keys, uint64_t n, const __grid_cons
         for (int u = 0; u < KPT; u++) {
             const uint64_t i = i0 + u * T;
             if (i >= n) break;
-            unsigned long long acc = 0;
-            uint32_t accbits = lead, q = 0;
+            unsigned long long acc = 0;                          // pending bits, left-aligned
+            uint32_t accbits = toppad, q = np - 1;
 #pragma unroll
-            for (int k = NW - 1; k >= 0; k--) {                  // least significant end of P first
+            for (int k = 0; k < NW; k++) {                       // most significant end of P first
                 if (plan.mask[k] == 0) continue;
                 uint32_t x = bswap32(w[u][k]) & plan.mask[k];
 #pragma unroll
-                for (int s = 0; s < 5; s++) {
-                    if (SKIP && plan.mv[k][s] == 0) continue;    // uniform: steps this mask does not need
-                    uint32_t t = x & plan.mv[k][s];
-                    x = (x ^ t) | (t >> (1u << s));
-                }
-                acc |= (unsigned long long)x << accbits;
+                for (int s = 0; s < 5; s++) x = mad_u32(x & plan.mv[k][s], (1u << (1u << s)) - 1u, x);
+                acc |= ((unsigned long long)x << 32) >> accbits;
                 accbits += plan.cnt[k];
                 if (accbits >= 32) {
-                    planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
-                    acc >>= 32;
+                    planes[(uint64_t)q * pitch + i] = (uint32_t)(acc >> 32);
+                    acc <<= 32;
                     accbits -= 32;
-                    q++;
+                    q--;
                 }
             }
-            if (accbits) planes[(uint64_t)q * pitch + i] = (uint32_t)acc;
+            if (accbits) planes[(uint64_t)q * pitch + i] = (uint32_t)(acc >> 32);
         }
     }
 }
 
 template <int B>
 static void launch_fixed(const uint8_t* keys, uint64_t n, const GatherPlan* hplan, uint32_t* planes, uint64_t pitch,
-                         uint32_t lead, const uint32_t* rows, int grid, cudaStream_t st) {
+                         uint32_t np, uint32_t lead, const uint32_t* rows, int grid, cudaStream_t st) {
     FixedPlan<B / 4> fp;
     memset(&fp, 0, sizeof(fp));
     for (uint32_t s = 0; s < hplan->nsteps; s++) {
         const GatherStep& g = hplan->step[s];
         fp.mask[g.src] = g.mask;
-        for (int k = 0; k < 5; k++) fp.mv[g.src][k] = g.mv[k];
+        move_masks_left(g.mask, fp.mv[g.src]);
         fp.cnt[g.src] = g.cnt;
     }
+    const uint32_t toppad = np * 32 - hplan->out_bits - lead;
     // rows: random key rows behind a dependent load -> 4 keys in flight per thread; in order:
-    // ALU-bound, one key per thread measured fastest (neither 2 keys per thread nor skipping
-    // the parallel-suffix steps a mask does not need paid off)
-    if (rows) k_compress_fixed<B, 4, false><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, lead, rows);
-    else k_compress_fixed<B, 1, false><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, lead, rows);
+    // ALU-bound, one key per thread measured fastest
+    if (rows) k_compress_fixed<B, 4><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, np, toppad, rows);
+    else k_compress_fixed<B, 1><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, np, toppad, rows);
 }
 
 static int grid_for(uint64_t work, int per_sm, int sms) {
@@ -265,10 +273,10 @@ cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const G
     if (((uintptr_t)keys & 15) == 0 && (B == 8 || B == 16 || B == 32 || B == 64)) {
         int grid = grid_for(n, 8, sms);
         switch (B) {
-            case 8: launch_fixed<8>(keys, n, hplan, planes, pitch, lead, rows, grid, st); break;
-            case 16: launch_fixed<16>(keys, n, hplan, planes, pitch, lead, rows, grid, st); break;
-            case 32: launch_fixed<32>(keys, n, hplan, planes, pitch, lead, rows, grid, st); break;
-            default: launch_fixed<64>(keys, n, hplan, planes, pitch, lead, rows, grid, st); break;
+            case 8: launch_fixed<8>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st); break;
+            case 16: launch_fixed<16>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st); break;
+            case 32: launch_fixed<32>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st); break;
+            default: launch_fixed<64>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st); break;
         }
         return cudaGetLastError();
     }
