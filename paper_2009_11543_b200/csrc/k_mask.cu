@@ -120,14 +120,33 @@ __global__ void k_occ_finalize(const uint32_t* __restrict__ occ, uint32_t B, uin
     }
 }
 
-// Specialised path for a compile-time key width B in {8, 16, 32, 64} (16-byte aligned keys).
+// Specialised paths for a compile-time key width B in {8, 16} (chunk per thread, below) and
+// {32, 64} (key per thread, k_occupancy_rows), 16-byte aligned keys.
 // Occupancy is kept as one flag BYTE per (position, value) in shared memory, so marking a
 // byte is a plain store of 1 -- no load, no test, no atomic (every writer stores the same
 // value): extract the byte (PRMT), add it to the position's row, store. Rows are padded by 4
-// bytes so positions 16 apart (the two halves of a warp when B = 32) use different banks.
+// bytes so that rows start in different banks.
 // Each thread keeps U 16-byte chunks in flight. The flags are folded into the u32 bitsets
 // at the end.
 constexpr int kRowBytes = 260;
+
+// fold: thread per (position, word): 32 flags -> one u32
+template <int B>
+__device__ __forceinline__ void fold_flags(const uint8_t* flag, uint32_t* __restrict__ occ_g) {
+    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) {
+        const uint8_t* f = flag + (i >> 3) * kRowBytes + (i & 7) * 32;
+        uint32_t bits = 0;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+            uint32_t q = *reinterpret_cast<const uint32_t*>(f + k);
+            bits |= ((q & 0xFF) ? 1u : 0u) << k;
+            bits |= ((q & 0xFF00) ? 1u : 0u) << (k + 1);
+            bits |= ((q & 0xFF0000) ? 1u : 0u) << (k + 2);
+            bits |= ((q & 0xFF000000) ? 1u : 0u) << (k + 3);
+        }
+        if (bits) atomicOr(&occ_g[i], bits);
+    }
+}
 
 template <int B>
 __global__ void __launch_bounds__(256) k_occupancy_bytes(const uint8_t* __restrict__ keys, uint64_t nchunks,
@@ -157,20 +176,47 @@ __global__ void __launch_bounds__(256) k_occupancy_bytes(const uint8_t* __restri
         }
     }
     __syncthreads();
-    // fold: thread per (position, word): 32 flags -> one u32
-    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) {
-        const uint8_t* f = flag + (i >> 3) * kRowBytes + (i & 7) * 32;
-        uint32_t bits = 0;
+    fold_flags<B>(flag, occ_g);
+}
+
+// B in {32, 64}: thread per key. In the chunk-per-thread kernel above the lanes of a warp
+// hold chunks of B/16 different byte positions, so one store instruction hits B/16 flag rows
+// at the same value offsets -- B/16-way bank conflicts on text keys, whose bytes span few
+// banks. Here every lane of a store instruction marks the same position j of its own key:
+// one row, values in distinct words (or the same word), conflict-free. The key's 16-byte
+// loads are L1-allocating so the lanes' 64-byte-strided loads fetch each sector once.
+template <int B>
+__global__ void __launch_bounds__(256) k_occupancy_rows(const uint8_t* __restrict__ keys, uint64_t n,
+                                                        uint32_t* __restrict__ occ_g) {
+    __shared__ __align__(16) uint8_t flag[B * kRowBytes];
+    for (uint32_t i = threadIdx.x; i < B * kRowBytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(flag)[i] = 0;
+    __syncthreads();
+    constexpr int U = B / 16;                                 // 16-byte units per key
+    constexpr int KPT = 64 / B;                               // keys in flight per thread
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += KPT * stride) {
+        int4 v[KPT][U];
 #pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-            uint32_t q = *reinterpret_cast<const uint32_t*>(f + k);
-            bits |= ((q & 0xFF) ? 1u : 0u) << k;
-            bits |= ((q & 0xFF00) ? 1u : 0u) << (k + 1);
-            bits |= ((q & 0xFF0000) ? 1u : 0u) << (k + 2);
-            bits |= ((q & 0xFF000000) ? 1u : 0u) << (k + 3);
+        for (int k = 0; k < KPT; k++)
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                v[k][u] = i + k * stride < n ? __ldg(reinterpret_cast<const int4*>(keys + (i + k * stride) * B) + u)
+                                             : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int k = 0; k < KPT; k++) {
+            if (i + k * stride >= n) break;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t w[4] = {(uint32_t)v[k][u].x, (uint32_t)v[k][u].y, (uint32_t)v[k][u].z,
+                                       (uint32_t)v[k][u].w};
+#pragma unroll
+                for (int b = 0; b < 16; b++)
+                    flag[(16 * u + b) * kRowBytes + __byte_perm(w[b >> 2], 0, 0x4440 + (b & 3))] = 1;
+            }
         }
-        if (bits) atomicOr(&occ_g[i], bits);
     }
+    __syncthreads();
+    fold_flags<B>(flag, occ_g);
 }
 
 cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32_t* occ,
@@ -178,15 +224,18 @@ cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32
     size_t smem = (size_t)B * 9 * sizeof(uint32_t);
     bool pow2 = (B & (B - 1)) == 0;
     bool aligned = ((uintptr_t)keys & 15) == 0;
-    if (aligned && (B == 8 || B == 16 || B == 32 || B == 64) && ((n * B) & 15) == 0) {
+    if (aligned && (B == 32 || B == 64)) {
+        uint64_t want = (n + 255) / 256;
+        int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
+        if (B == 32) k_occupancy_rows<32><<<grid, 256, 0, st>>>(keys, n, occ);
+        else k_occupancy_rows<64><<<grid, 256, 0, st>>>(keys, n, occ);
+    } else if (aligned && (B == 8 || B == 16) && ((n * B) & 15) == 0) {
         uint64_t nchunks = (n * B) >> 4;
         uint64_t want = (nchunks + 255) / 256;
         int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
         switch (B) {
             case 8: k_occupancy_bytes<8><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
-            case 16: k_occupancy_bytes<16><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
-            case 32: k_occupancy_bytes<32><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
-            default: k_occupancy_bytes<64><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
+            default: k_occupancy_bytes<16><<<grid, 256, 0, st>>>(keys, nchunks, occ); break;
         }
     } else if (pow2 && aligned) {
         uint64_t nchunks = (n * B) >> 4;
