@@ -374,10 +374,17 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     uint32_t T = forced > 0 && forced <= 64 && (forced & 7) == 0 ? (uint32_t)forced : 64;
     if (sample) {
         CK(cudaEventSynchronize(ctx->aux_ev[1]));
-        // one byte of margin: a 4096-key sample misses the birthday collisions that tie millions
-        // of keys at the narrowest separating width (measured: cfg5 40 -> 48, cfg3 32 -> 40)
+        // one byte of margin when P_M is read back by row id: a 4096-key sample misses the birthday
+        // collisions that tie millions of keys at the narrowest separating width, and finishing
+        // those by row is dearer than a pass (measured: cfg3 32 -> 40). With P_M carried (np == 3)
+        // the tile kernel finishes short ties from the sorted planes for less than a pass costs
+        // (measured, cfg5: T = 40 3.65 ms, 48 3.89 ms)
+        const uint32_t margin = np == 3 ? 0u : 1u;
         for (uint32_t w = 0; w < 8; w++)
-            if (ctx->h_tot[8 + w] == ctx->h_tot[15]) { T = 8 * (w + 2) < 64 ? 8 * (w + 2) : 64; break; }
+            if (ctx->h_tot[8 + w] == ctx->h_tot[15]) {
+                T = 8 * (w + 1 + margin) < 64 ? 8 * (w + 1 + margin) : 64;
+                break;
+            }
         CK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));   // (scnt is reused below)
     }
     if (T > m) T = (m + 7) & ~7u;
@@ -407,9 +414,19 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     }
     TRY(run_sort(ctx, pm + (uint64_t)(np - np0) * sp, sp, np0, 4 * np0, n, nullptr, 0, carried, sp, out->perm,
                  &sorted0, &sp0, dig0, false));
-    LAUNCH(launch_ref_adj(np0 >= 2 ? sorted0 + (uint64_t)(np0 - 2) * sp0 : nullptr, sorted0 + (uint64_t)(np0 - 1) * sp0,
-                          nullptr, nullptr, n, 0, moff, m, B, dbit, tie, dacc, true, ctx->sms, ctx->stream,
-                          ~0ull << (64 - T)));
+    // round-0 adjacency; when rounds follow, fused with finishing the short runs inside a tile
+    static const bool no_tile = getenv("CKS_NO_TILE_RUNS") != nullptr;   // experiments only
+    const uint32_t* lo0 = np0 >= 2 ? sorted0 + (uint64_t)(np0 - 2) * sp0 : nullptr;
+    const uint32_t* hi0 = sorted0 + (uint64_t)(np0 - 1) * sp0;
+    TRY(ensure(ctx, ctx->rtot, 64));
+    CK(cudaMemsetAsync(as<uint32_t>(ctx->rtot) + 2, 0, 4, ctx->stream));
+    if (T < m && carry && !no_tile)       // (P_M by row id: the compaction + k_ref_local path measured faster)
+        LAUNCH(launch_ref_tile(pm, sp, np, (int)np - 1 - (int)(T >> 5), 0xFFFFFFFFu >> (T & 31), moff, out->perm, dbit,
+                               carried, lo0, hi0, sp0, n, ~0ull << (64 - T), B, tie, dacc, as<uint32_t>(ctx->rtot) + 2,
+                               ctx->sms, ctx->stream));
+    else
+        LAUNCH(launch_ref_adj(lo0, hi0, nullptr, nullptr, n, 0, moff, m, B, dbit, tie, dacc, true, ctx->sms,
+                              ctx->stream, ~0ull << (64 - T)));
     out->round0_bits = T;
     out->rounds = 1;
     out->refined_keys = 0;
@@ -437,10 +454,14 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         TRY(ensure(ctx, ctx->rtot, 64));
     }
     auto counts = [&](uint64_t* a, uint64_t* b) -> int {
-        CK(cudaMemcpyAsync(ctx->h_tot, ctx->rtot.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_tot, ctx->rtot.p, 12, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         *a = ctx->h_tot[0];
         *b = ctx->h_tot[1];
+        if (ctx->h_tot[2]) {                                     // keys finished by the tile kernel
+            out->refined_keys += ctx->h_tot[2];
+            CK(cudaMemsetAsync(as<uint32_t>(ctx->rtot) + 2, 0, 4, ctx->stream));
+        }
         return CKS_OK;
     };
     const bool log = getenv("CKS_REFINE_LOG") != nullptr;

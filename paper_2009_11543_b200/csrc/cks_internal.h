@@ -104,6 +104,10 @@ cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
 
 // NEXT-1 prefix refinement (k_refine.cu)
 uint64_t ref_tiles(uint64_t nr);
+cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, uint32_t fmask,
+                            const uint16_t* moff, uint32_t* perm, uint16_t* dbit, uint32_t* carried, const uint32_t* lo,
+                            const uint32_t* hi, uint64_t hpitch, uint64_t n, unsigned long long cmask, uint32_t B,
+                            uint8_t* tie, uint32_t* dacc, uint32_t* handled, int sms, cudaStream_t st);
 cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_t* seg, const uint32_t* pos,
                            uint64_t nr, uint32_t cbase, const uint16_t* moff, uint32_t m, uint32_t B,
                            uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st,

@@ -84,8 +84,21 @@ k_ref_adj(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, cons
 
 // Tiles of kRefTile elements; warp w of a tile owns the contiguous elements
 // [w*32*kRefItems, (w+1)*32*kRefItems), walked 32 at a time (coalesced flag loads, ballots).
-__device__ __forceinline__ void ref_flags2(const uint8_t* tie, uint64_t nr, uint64_t k, bool& member, bool& start) {
-    const uint32_t a = k < nr ? tie[k] : 0u, b = k + 1 < nr ? tie[k + 1] : 0u;
+// the tile's kRefTile + 1 flags staged in shared memory with 16-byte loads (zero past nr)
+__device__ __forceinline__ void stage_flags(const uint8_t* __restrict__ tie, uint64_t nr, uint64_t base, uint8_t* s_f) {
+    const uint64_t k = base + 16 * (uint64_t)threadIdx.x;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (k + 16 <= nr && ((reinterpret_cast<uintptr_t>(tie) & 15) == 0)) {
+        v = *reinterpret_cast<const uint4*>(tie + k);
+    } else {
+        uint8_t* b = reinterpret_cast<uint8_t*>(&v);
+        for (int j = 0; j < 16; j++) b[j] = k + j < nr ? tie[k + j] : 0;
+    }
+    reinterpret_cast<uint4*>(s_f)[threadIdx.x] = v;
+    if (threadIdx.x == 0) s_f[kRefTile] = base + kRefTile < nr ? tie[base + kRefTile] : 0;
+}
+__device__ __forceinline__ void ref_flags_s(const uint8_t* s_f, uint32_t k, bool& member, bool& start) {
+    const uint32_t a = s_f[k], b = s_f[k + 1];
     member = (a | b) != 0;
     start = member && !a;
 }
@@ -94,13 +107,16 @@ __device__ __forceinline__ void ref_flags2(const uint8_t* tie, uint64_t nr, uint
 __global__ void __launch_bounds__(kRefThreads)
 k_ref_count(const uint8_t* __restrict__ tie, uint64_t nr, uint32_t* __restrict__ cnt) {
     __shared__ uint32_t s_red[2][kRefThreads / 32];
+    __shared__ __align__(16) uint8_t s_f[kRefTile + 16];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t k0 = (uint64_t)blockIdx.x * kRefTile + (uint64_t)warp * 32 * kRefItems + lane;
+    stage_flags(tie, nr, (uint64_t)blockIdx.x * kRefTile, s_f);
+    __syncthreads();
+    const uint32_t k0 = warp * 32 * kRefItems + lane;
     uint32_t cm = 0, cs = 0;
 #pragma unroll 4
     for (int i = 0; i < kRefItems; i++) {
         bool mb, st;
-        ref_flags2(tie, nr, k0 + 32 * i, mb, st);
+        ref_flags_s(s_f, k0 + 32 * i, mb, st);
         cm += __popc(__ballot_sync(0xffffffffu, mb));
         cs += __popc(__ballot_sync(0xffffffffu, st));
     }
@@ -158,13 +174,18 @@ k_ref_scatter(const uint8_t* __restrict__ tie, uint64_t nr, const uint32_t* __re
               const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pos_next, uint32_t* __restrict__ seg_next,
               uint32_t* __restrict__ run_off, uint32_t* __restrict__ run_pos) {
     __shared__ uint32_t s_w[2][kRefThreads / 32];
+    __shared__ __align__(16) uint8_t s_f[kRefTile + 16];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ltm = (1u << lane) - 1u;
-    const uint64_t k0 = (uint64_t)blockIdx.x * kRefTile + (uint64_t)warp * 32 * kRefItems + lane;
+    const uint64_t base = (uint64_t)blockIdx.x * kRefTile;
+    stage_flags(tie, nr, base, s_f);
+    __syncthreads();
+    const uint32_t l0 = warp * 32 * kRefItems + lane;
+    const uint64_t k0 = base + l0;
     uint32_t cm = 0, cs = 0;
     for (int i = 0; i < kRefItems; i++) {                       // pass 1: this warp's counts
         bool mb, st;
-        ref_flags2(tie, nr, k0 + 32 * i, mb, st);
+        ref_flags_s(s_f, l0 + 32 * i, mb, st);
         cm += __popc(__ballot_sync(0xffffffffu, mb));
         cs += __popc(__ballot_sync(0xffffffffu, st));
     }
@@ -175,7 +196,7 @@ k_ref_scatter(const uint8_t* __restrict__ tie, uint64_t nr, const uint32_t* __re
     for (int i = 0; i < kRefItems; i++) {                       // pass 2: write in element order
         bool mb, st;
         const uint64_t k = k0 + 32 * i;
-        ref_flags2(tie, nr, k, mb, st);
+        ref_flags_s(s_f, l0 + 32 * i, mb, st);
         const uint32_t bm = __ballot_sync(0xffffffffu, mb), bs = __ballot_sync(0xffffffffu, st);
         if (mb) {
             const uint32_t o = om + __popc(bm & ltm);
@@ -285,6 +306,310 @@ __device__ __forceinline__ bool key_less(const uint32_t (&a)[W], uint32_t ra, co
     for (int c = 0; c < W; c++)
         if (a[c] != b[c]) return a[c] < b[c];
     return ra < rb;
+}
+
+// Round-0 adjacency fused with finishing the short runs that lie inside one tile of the
+// sorted order (most runs, when round 0 leaves many small ties). Tile of kTileKeys positions
+// per CTA iteration:
+//   1. tie flags / adjacency D_i of every position from the top T bits (as k_ref_adj, round 0);
+//   2. runs that start and end inside the tile and have at most kTileRun keys are "handled":
+//      each member ranks itself in its run by (remaining P_M words, row id) -- the same total
+//      order as k_ref_local -- reading the words from the carried planes (kept in shared
+//      memory) or from P_M by row id;
+//   3. the handled runs are written back in sorted order (row ids, carried planes, D_i of every
+//      member after the first) and their tie flags cleared, so the compaction that follows
+//      sees only the runs left (crossing a tile edge, longer, or too many remaining words).
+// A member's top T bits equal its run's, so a neighbouring tile reading this tile's edge
+// position for its own adjacency sees the same masked bits before or after the rewrite.
+constexpr int kTileKeys = 2048;
+constexpr int kTileItems = kTileKeys / kRefThreads;     // consecutive positions per thread (8)
+constexpr uint32_t kTileRun = 8;
+
+// 8 consecutive u32 (positions p0..p0+7, p0 % 8 == 0) -- two 16-byte accesses when the whole
+// group is in range and `vec` (16-byte aligned arrays), else element by element
+__device__ __forceinline__ void ld8(const uint32_t* a, uint64_t p0, uint64_t n, bool vec, uint32_t (&v)[kTileItems]) {
+    if (vec && p0 + kTileItems <= n) {
+        const uint4 x = *reinterpret_cast<const uint4*>(a + p0), y = *reinterpret_cast<const uint4*>(a + p0 + 4);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kTileItems; j++) v[j] = p0 + j < n ? a[p0 + j] : 0u;
+    }
+}
+__device__ __forceinline__ void st8(uint32_t* a, uint64_t p0, uint64_t n, bool vec, const uint32_t (&v)[kTileItems]) {
+    if (vec && p0 + kTileItems <= n) {
+        *reinterpret_cast<uint4*>(a + p0) = make_uint4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<uint4*>(a + p0 + 4) = make_uint4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kTileItems; j++)
+            if (p0 + j < n) a[p0 + j] = v[j];
+    }
+}
+
+__device__ __forceinline__ uint32_t tpad(uint32_t i) { return i + (i >> 5); }   // thread-of-8 layout, conflict-free
+constexpr int kTilePad = kTileKeys + kTileKeys / 32;
+
+constexpr size_t tile_smem_bytes(int wc) {
+    return (size_t)kTilePad * 8 + (size_t)wc * kTilePad * 4 + (size_t)kTilePad * 4 + (size_t)kTileKeys * 4 +
+           (size_t)kTilePad * 2;
+}
+
+// WC: remaining words (= qtop + 1, 1..3), all carried in sorted order. (A variant reading
+// them from P_M by row id for wider keys measured slower than the compaction + k_ref_local
+// path, which those keys keep.) Thread t owns the 8 consecutive positions [8t, 8t+8) of the tile;
+// run bounds come from two block scans (last run start at or before a position, first run
+// start after it), so a member needs no walk over the tie flags.
+template <int WC>
+__global__ void __launch_bounds__(kRefThreads, 3)
+k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigned long long cmask, uint32_t nwords,
+           bool vec, uint8_t* __restrict__ tie, uint32_t* __restrict__ dacc, uint32_t* __restrict__ handled) {
+    static_assert(WC >= 1 && WC <= 3, "carried remaining words");
+    constexpr int NWS = WC;
+    constexpr int NWARP = kRefThreads / 32;
+    __shared__ uint32_t s_bm[kMaxBits / 32];
+    extern __shared__ __align__(16) unsigned char s_tiledyn[];            // tile_smem_bytes(WC)
+    unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_tiledyn);   // members: words 0 (masked), 1
+    uint32_t (*s_w)[kTilePad] = reinterpret_cast<uint32_t (*)[kTilePad]>(s_key + kTilePad);   // carried words
+    uint32_t* s_row = s_w[NWS];                                           // [kTilePad] row ids
+    uint32_t* s_mem = s_row + kTilePad;                  // members: tile index | run start << 11 | length << 22
+    uint16_t* s_at = reinterpret_cast<uint16_t*>(s_mem + kTileKeys);     // run-order position -> tile index
+    __shared__ unsigned long long s_last[kRefThreads];
+    __shared__ int s_wmax[NWARP], s_wmin[NWARP], s_wcnt[NWARP];
+    __shared__ uint32_t s_cnt, s_tnext;
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
+    if (threadIdx.x == 0) s_cnt = 0;
+    const int Wr = R.qtop + 1;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
+    auto top = [&](uint64_t k) -> unsigned long long {
+        return (((unsigned long long)hi[k] << 32) | (lo ? (unsigned long long)lo[k] : 0ull)) & cmask;
+    };
+    auto word = [&](int c, uint32_t i) -> uint32_t {      // remaining word c of tile element i
+        return c == 0 ? s_w[0][tpad(i)] & R.fmask : s_w[c < NWS ? c : 0][tpad(i)];
+    };
+    // remaining key of element i for ordering: words 0 (masked) and 1 in s_key; word 2 (WC == 3)
+    // only where s_key ties
+    auto key_less = [&](uint32_t k, uint32_t i, unsigned long long ki, uint32_t ri) -> bool {
+        const unsigned long long kk = s_key[tpad(k)];
+        if (kk != ki) return kk < ki;
+        if (WC == 3) {
+            const uint32_t a2 = s_w[NWS - 1][tpad(k)], b2 = s_w[NWS - 1][tpad(i)];
+            if (a2 != b2) return a2 < b2;
+        }
+        return s_row[tpad(k)] < ri;
+    };
+    auto mark_d = [&](uint32_t d) {
+        const uint32_t b = 0x80000000u >> (d & 31);
+        if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
+    };
+    const uint32_t i0 = threadIdx.x * kTileItems;
+    __syncthreads();
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t t0 = tile * kTileKeys;
+        const uint32_t tn = (uint32_t)(n - t0 < (uint64_t)kTileKeys ? n - t0 : (uint64_t)kTileKeys);
+        const uint64_t p0 = t0 + i0;
+        // A. loads: top bits, row ids, carried words
+        uint32_t vh[kTileItems], vl[kTileItems], vr[kTileItems];
+        ld8(hi, p0, n, vec, vh);
+        if (lo) ld8(lo, p0, n, vec, vl);
+        ld8(R.perm, p0, n, vec, vr);
+        unsigned long long tk[kTileItems];
+#pragma unroll
+        for (int j = 0; j < kTileItems; j++) {
+            tk[j] = (((unsigned long long)vh[j] << 32) | (lo ? (unsigned long long)vl[j] : 0ull)) & cmask;
+            s_row[tpad(i0 + j)] = vr[j];
+        }
+        {
+#pragma unroll
+            for (int c = 0; c < NWS; c++) {
+                uint32_t vw[kTileItems];
+                ld8(R.carried + (uint64_t)(R.qtop - c) * R.pitch, p0, n, vec, vw);
+#pragma unroll
+                for (int j = 0; j < kTileItems; j++) s_w[c][tpad(i0 + j)] = vw[j];
+            }
+        }
+        s_last[threadIdx.x] = tk[kTileItems - 1];
+        if (threadIdx.x == 0) s_tnext = (t0 + tn < n && top(t0 + tn) == top(t0 + tn - 1)) ? 1u : 0u;
+        const unsigned long long left = (threadIdx.x == 0 && t0 > 0) ? top(t0 - 1) : 0ull;
+        __syncthreads();
+        // B. tie flags, adjacency D_i, run starts (positions past n count as starts)
+        unsigned long long prev = threadIdx.x ? s_last[threadIdx.x - 1] : left;
+        uint32_t tb = 0;                                  // bit j: position i0+j ties with its predecessor
+        uint16_t odb[kTileItems];
+        uint32_t dz = 0;                                  // bit j: position i0+j has an adjacency D_i
+#pragma unroll
+        for (int j = 0; j < kTileItems; j++) {
+            const uint64_t p = p0 + j;
+            odb[j] = CKS_NONE_INTERNAL;
+            if (p > 0 && p < n) {
+                const unsigned long long x = tk[j] ^ prev;
+                if (x) {
+                    odb[j] = __ldg(R.moff + (uint32_t)__clzll((long long)x));
+                    dz |= 1u << j;
+                } else {
+                    tb |= 1u << j;
+                }
+            }
+            prev = tk[j];
+        }
+        {                                                 // D accumulation: the 8 tests first, then atomics
+            uint32_t seen[kTileItems];
+#pragma unroll
+            for (int j = 0; j < kTileItems; j++) seen[j] = (dz >> j & 1) ? s_bm[odb[j] >> 5] : ~0u;
+#pragma unroll
+            for (int j = 0; j < kTileItems; j++) {
+                const uint32_t b = 0x80000000u >> (odb[j] & 31);
+                if (!(seen[j] & b)) atomicOr(&s_bm[odb[j] >> 5], b);
+            }
+        }
+        const uint32_t sb = ~tb & 0xFFu;                  // run starts
+        int lst = sb ? (int)(i0 + 31 - __clz(sb)) : -1;  // last start in this thread
+        int fst = sb ? (int)(i0 + __ffs(sb) - 1) : kTileKeys + 1;   // first start
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, lst, o), z = __shfl_down_sync(0xffffffffu, fst, o);
+            if (lane >= (uint32_t)o) lst = max(lst, y);
+            if (lane + o < 32) fst = min(fst, z);
+        }
+        if (lane == 31) s_wmax[warp] = lst;
+        if (lane == 0) s_wmin[warp] = fst;
+        int inA = __shfl_up_sync(0xffffffffu, lst, 1), outE = __shfl_down_sync(0xffffffffu, fst, 1);
+        if (lane == 0) inA = -1;
+        if (lane == 31) outE = kTileKeys + 1;
+        __syncthreads();
+        for (uint32_t w = 0; w < warp; w++) inA = max(inA, s_wmax[w]);
+        for (uint32_t w = warp + 1; w < NWARP; w++) outE = min(outE, s_wmin[w]);
+        // C. handled members: the run [a, e) lies in the tile, 2 <= e - a <= kTileRun
+        uint32_t hm = 0;
+        int ra[kTileItems], re[kTileItems];
+        {
+            int a = inA;
+#pragma unroll
+            for (int j = 0; j < kTileItems; j++) {
+                if (sb >> j & 1) a = (int)(i0 + j);
+                ra[j] = a;
+            }
+            int e = outE;
+#pragma unroll
+            for (int j = kTileItems - 1; j >= 0; j--) {
+                re[j] = e;
+                if (sb >> j & 1) e = (int)(i0 + j);
+            }
+        }
+        const bool ok_words = Wr == WC;
+#pragma unroll
+        for (int j = 0; j < kTileItems; j++) {
+            int e = re[j] > (int)tn ? (int)tn : re[j];
+            const bool closed = e < (int)tn || !s_tnext;
+            if (ok_words && ra[j] >= 0 && closed && e - ra[j] >= 2 && e - ra[j] <= (int)kTileRun) {
+                hm |= 1u << j;
+                re[j] = e;
+                const uint32_t w0 = s_w[0][tpad(i0 + j)], w1 = WC >= 2 ? s_w[1][tpad(i0 + j)] : 0u;
+                s_key[tpad(i0 + j)] = ((unsigned long long)(w0 & R.fmask) << 32) | w1;
+            }
+        }
+        // member list: block exclusive scan of the per-thread member counts
+        const uint32_t mc = (uint32_t)__popc(hm);
+        uint32_t mo = mc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, mo, o);
+            if (lane >= (uint32_t)o) mo += y;
+        }
+        if (lane == 31) s_wcnt[warp] = (int)mo;
+        mo -= mc;
+        __syncthreads();
+        uint32_t nmem = 0;
+        for (uint32_t w = 0; w < NWARP; w++) {
+            if (w < warp) mo += (uint32_t)s_wcnt[w];
+            nmem += (uint32_t)s_wcnt[w];
+        }
+        if (nmem == 0) {                                  // nothing to reorder: flags and D_i only
+            uint32_t ot[2] = {0, 0};
+#pragma unroll
+            for (int j = 0; j < kTileItems; j++) ot[j >> 2] |= (tb >> j & 1u) << (8 * (j & 3));
+            if (vec && p0 + kTileItems <= n) {
+                *reinterpret_cast<uint2*>(tie + p0) = make_uint2(ot[0], ot[1]);
+                *reinterpret_cast<uint4*>(R.dbit + p0) = make_uint4(
+                    (tb & 1 ? 0xFFFFu : odb[0]) | ((uint32_t)(tb & 2 ? 0xFFFFu : odb[1]) << 16),
+                    (tb & 4 ? 0xFFFFu : odb[2]) | ((uint32_t)(tb & 8 ? 0xFFFFu : odb[3]) << 16),
+                    (tb & 16 ? 0xFFFFu : odb[4]) | ((uint32_t)(tb & 32 ? 0xFFFFu : odb[5]) << 16),
+                    (tb & 64 ? 0xFFFFu : odb[6]) | ((uint32_t)(tb & 128 ? 0xFFFFu : odb[7]) << 16));
+            } else {
+                for (int j = 0; j < kTileItems; j++)
+                    if (p0 + j < n) { tie[p0 + j] = (uint8_t)(tb >> j & 1); R.dbit[p0 + j] = odb[j]; }
+            }
+            __syncthreads();
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < kTileItems; j++)
+            if (hm >> j & 1) s_mem[mo++] = (i0 + j) | ((uint32_t)ra[j] << 11) | ((uint32_t)(re[j] - ra[j]) << 22);
+        __syncthreads();
+        // D. rank of each member in its run by (remaining words, row id), member per thread
+        for (uint32_t u = threadIdx.x; u < nmem; u += blockDim.x) {
+            const uint32_t v = s_mem[u];
+            const uint32_t i = v & 0x7FFu, a = (v >> 11) & 0x7FFu, L = v >> 22;
+            const unsigned long long ki = s_key[tpad(i)];
+            const uint32_t ri = s_row[tpad(i)];
+            uint32_t r = 0;
+            for (uint32_t k = a; k < a + L; k++) r += key_less(k, i, ki, ri) ? 1u : 0u;   // (k == i: false)
+            s_at[tpad(a + r)] = (uint16_t)i;
+        }
+        if (threadIdx.x == 0) s_cnt += nmem;
+        __syncthreads();
+        // E. write back this thread's positions in run order
+        uint32_t orow[kTileItems], ot[2] = {0, 0};
+        uint32_t ow[NWS][kTileItems];
+#pragma unroll
+        for (int j = 0; j < kTileItems; j++) {
+            const uint32_t dd = i0 + j;
+            uint32_t src = dd;
+            uint32_t t = tb >> j & 1u;
+            uint16_t db = t ? (uint16_t)CKS_NONE_INTERNAL : odb[j];
+            if (hm >> j & 1) {
+                src = s_at[tpad(dd)];
+                if (t) {                                  // after the run's first position
+                    const uint32_t pj = s_at[tpad(dd - 1)];
+                    const unsigned long long x = s_key[tpad(pj)] ^ s_key[tpad(src)];
+                    const uint32_t b0 = 32u * (R.np - 1 - (uint32_t)R.qtop);   // P_M bit of word 0's MSB
+                    int fd = x ? (int)(b0 + (uint32_t)__clzll((long long)x)) : -1;
+                    if (fd < 0)
+                        for (int c = 2; c < Wr; c++) {
+                            const uint32_t y = word(c, pj) ^ word(c, src);
+                            if (y) { fd = (int)(b0 + 32u * (uint32_t)c + (uint32_t)__clz(y)); break; }
+                        }
+                    if (fd >= 0) {
+                        db = __ldg(R.moff + fd);
+                        mark_d(db);
+                    }
+                }
+                t = 0;
+            }
+            orow[j] = s_row[tpad(src)];
+            odb[j] = db;
+            ot[j >> 2] |= t << (8 * (j & 3));
+#pragma unroll
+            for (int c = 0; c < NWS; c++) ow[c][j] = s_w[c][tpad(src)];
+        }
+        st8(R.perm, p0, n, vec, orow);
+#pragma unroll
+        for (int c = 0; c < NWS; c++) st8(R.carried + (uint64_t)(R.qtop - c) * R.pitch, p0, n, vec, ow[c]);
+        if (vec && p0 + kTileItems <= n) {
+            *reinterpret_cast<uint2*>(tie + p0) = make_uint2(ot[0], ot[1]);
+            *reinterpret_cast<uint4*>(R.dbit + p0) =
+                make_uint4(odb[0] | ((uint32_t)odb[1] << 16), odb[2] | ((uint32_t)odb[3] << 16),
+                           odb[4] | ((uint32_t)odb[5] << 16), odb[6] | ((uint32_t)odb[7] << 16));
+        } else {
+            for (int j = 0; j < kTileItems; j++)
+                if (p0 + j < n) { tie[p0 + j] = (uint8_t)(ot[j >> 2] >> (8 * (j & 3))); R.dbit[p0 + j] = odb[j]; }
+        }
+        __syncthreads();
+    }
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
+        if (s_bm[w]) atomicOr(&dacc[w], s_bm[w]);
+    if (threadIdx.x == 0 && s_cnt) atomicAdd(handled, s_cnt);
 }
 
 // Thread per run: short runs (<= 4, registers only: a fixed network, static indices); longer
@@ -640,6 +965,37 @@ cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_
     const size_t smem = (size_t)nwords * 4 + (size_t)m * 2 + 16;
     k_ref_adj<<<grid_of(nr, sms), kRefThreads, smem, st>>>(lo, hi, seg, pos, nr, cbase, moff, m, nwords, dbit, tie,
                                                            dacc, round0 ? 1 : 0, cmask);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, uint32_t fmask,
+                            const uint16_t* moff, uint32_t* perm, uint16_t* dbit, uint32_t* carried, const uint32_t* lo,
+                            const uint32_t* hi, uint64_t hpitch, uint64_t n, unsigned long long cmask, uint32_t B,
+                            uint8_t* tie, uint32_t* dacc, uint32_t* handled, int sms, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const uint32_t nwords = (8 * B + 31) / 32;
+    RunCtx R{pm, pitch, np, qtop, fmask, moff, perm, dbit, carried};
+    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
+    const uint64_t cap = (uint64_t)sms * 3;                      // resident CTAs (__launch_bounds__(256, 3))
+    const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    const bool vec = al(perm) && al(dbit) && al(hi) && (!lo || al(lo)) && (hpitch & 3) == 0 && (pitch & 3) == 0 &&
+                     (!carried || al(carried));
+    if (!carried) return cudaErrorInvalidValue;
+    const int wc = qtop + 1;
+#define CKS_TILE_CASE(W)                                                                                        \
+    case W:                                                                                                     \
+        raise_smem_limit((const void*)k_ref_tile<W>, tile_smem_bytes(W));                                       \
+        k_ref_tile<W><<<grid, kRefThreads, tile_smem_bytes(W), st>>>(R, lo, hi, n, cmask, nwords, vec, tie, dacc, \
+                                                                     handled);                                  \
+        break;
+    switch (wc) {
+        CKS_TILE_CASE(1)
+        CKS_TILE_CASE(2)
+        CKS_TILE_CASE(3)
+        default: return cudaErrorInvalidValue;
+    }
+#undef CKS_TILE_CASE
     return cudaGetLastError();
 }
 

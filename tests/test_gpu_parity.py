@@ -422,3 +422,37 @@ def test_refine_chunk_cta_rounds(seed):
     keys = hier_keys(60_000, [256] * 64, seed=seed, groups=(40, 7), dup_rows=300)
     r = cks.build(dev(keys))
     check_build(keys, r)
+
+
+_FORCED_T_SCRIPT = r"""
+import sys, numpy as np, torch
+from paper_2009_11543_b200 import cks
+keys = np.load(sys.argv[1])
+r = cks.build(torch.from_numpy(keys).cuda(), tree=False)
+np.savez(sys.argv[2], mask=r["mask"], popcount=r["popcount"], sort_bits=r["sort_bits"],
+         perm=r["perm"].cpu().numpy(), dbit=r["dbit"].cpu().numpy(), packed=r["packed"].cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("T", [8, 16, 24, 40, 56, 64])
+@pytest.mark.parametrize("m", [72, 92])
+def test_refine_forced_round0_width(T, m, tmp_path):
+    # P_M of three planes is carried through round 0 and the short ties inside a tile are
+    # finished from the sorted planes (k_ref_tile): T < 32 leaves 3 remaining words, T < 64 2,
+    # T = 64 1. CKS_ROUND0_BITS is read once per process, hence the subprocess.
+    import os
+    import subprocess
+    import sys
+    widths = [256] * (m // 8) + ([1 << (m % 8)] if m % 8 else [])
+    keys = hier_keys(70_001, widths, seed=T + m, groups=(5, 30), dup_rows=900)
+    kp, rp = tmp_path / "keys.npy", tmp_path / "r.npz"
+    np.save(kp, keys)
+    env = dict(os.environ, CKS_ROUND0_BITS=str(T))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", _FORCED_T_SCRIPT, str(kp), str(rp)], env=env, cwd=root, check=True,
+                   timeout=300)
+    z = np.load(rp)
+    assert int(z["sort_bits"]) == m
+    r = dict(mask=z["mask"], popcount=int(z["popcount"]), perm=torch.from_numpy(z["perm"]),
+             dbit=torch.from_numpy(z["dbit"]), packed=torch.from_numpy(z["packed"]), tree=None)
+    check_build(keys, r)
