@@ -367,7 +367,7 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
     static_assert(WC >= 1 && WC <= 3, "carried remaining words");
     constexpr int NWS = WC;
     constexpr int NWARP = kRefThreads / 32;
-    __shared__ uint32_t s_bm[kMaxBits / 32];
+    __shared__ uint32_t s_pm[3];                         // D of the CTA as P_M bit indices
     extern __shared__ __align__(16) unsigned char s_tiledyn[];            // tile_smem_bytes(WC)
     unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_tiledyn);   // members: words 0 (masked), 1
     uint32_t (*s_w)[kTilePad] = reinterpret_cast<uint32_t (*)[kTilePad]>(s_key + kTilePad);   // carried words
@@ -377,7 +377,7 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
     __shared__ unsigned long long s_last[kRefThreads];
     __shared__ int s_wmax[NWARP], s_wmin[NWARP], s_wcnt[NWARP];
     __shared__ uint32_t s_cnt, s_tnext;
-    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0;
+    if (threadIdx.x < 3) s_pm[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_cnt = 0;
     const int Wr = R.qtop + 1;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -399,9 +399,14 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
         }
         return s_row[tpad(k)] < ri;
     };
-    auto mark_d = [&](uint32_t d) {
-        const uint32_t b = 0x80000000u >> (d & 31);
-        if (!(s_bm[d >> 5] & b)) atomicOr(&s_bm[d >> 5], b);
+    // D found by this thread, as P_M bit indices (m <= 96: three words in registers), mapped
+    // to key bits through moff once per CTA at the end
+    uint32_t dm0 = 0, dm1 = 0, dm2 = 0;
+    auto mark_pm = [&](uint32_t i) {
+        const uint32_t w = i >> 5, bit = 1u << (i & 31);
+        dm0 |= w == 0 ? bit : 0u;
+        dm1 |= w == 1 ? bit : 0u;
+        dm2 |= w == 2 ? bit : 0u;
     };
     const uint32_t i0 = threadIdx.x * kTileItems;
     __syncthreads();
@@ -437,7 +442,6 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
         unsigned long long prev = threadIdx.x ? s_last[threadIdx.x - 1] : left;
         uint32_t tb = 0;                                  // bit j: position i0+j ties with its predecessor
         uint16_t odb[kTileItems];
-        uint32_t dz = 0;                                  // bit j: position i0+j has an adjacency D_i
 #pragma unroll
         for (int j = 0; j < kTileItems; j++) {
             const uint64_t p = p0 + j;
@@ -445,23 +449,14 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
             if (p > 0 && p < n) {
                 const unsigned long long x = tk[j] ^ prev;
                 if (x) {
-                    odb[j] = __ldg(R.moff + (uint32_t)__clzll((long long)x));
-                    dz |= 1u << j;
+                    const uint32_t pmb = (uint32_t)__clzll((long long)x);
+                    odb[j] = __ldg(R.moff + pmb);
+                    mark_pm(pmb);
                 } else {
                     tb |= 1u << j;
                 }
             }
             prev = tk[j];
-        }
-        {                                                 // D accumulation: the 8 tests first, then atomics
-            uint32_t seen[kTileItems];
-#pragma unroll
-            for (int j = 0; j < kTileItems; j++) seen[j] = (dz >> j & 1) ? s_bm[odb[j] >> 5] : ~0u;
-#pragma unroll
-            for (int j = 0; j < kTileItems; j++) {
-                const uint32_t b = 0x80000000u >> (odb[j] & 31);
-                if (!(seen[j] & b)) atomicOr(&s_bm[odb[j] >> 5], b);
-            }
         }
         const uint32_t sb = ~tb & 0xFFu;                  // run starts
         int lst = sb ? (int)(i0 + 31 - __clz(sb)) : -1;  // last start in this thread
@@ -509,8 +504,13 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
                 s_key[tpad(i0 + j)] = ((unsigned long long)(w0 & R.fmask) << 32) | w1;
             }
         }
-        // member list: block exclusive scan of the per-thread member counts
-        const uint32_t mc = (uint32_t)__popc(hm);
+        // member list, pair members first: block exclusive scan of the per-thread counts
+        // (pairs in the low 16 bits, longer runs' members in the high)
+        uint32_t h2 = 0;
+#pragma unroll
+        for (int j = 0; j < kTileItems; j++)
+            if ((hm >> j & 1) && re[j] - ra[j] == 2) h2 |= 1u << j;
+        const uint32_t mc = (uint32_t)__popc(h2) | ((uint32_t)__popc(hm & ~h2) << 16);
         uint32_t mo = mc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -520,11 +520,12 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
         if (lane == 31) s_wcnt[warp] = (int)mo;
         mo -= mc;
         __syncthreads();
-        uint32_t nmem = 0;
+        uint32_t tot = 0;
         for (uint32_t w = 0; w < NWARP; w++) {
             if (w < warp) mo += (uint32_t)s_wcnt[w];
-            nmem += (uint32_t)s_wcnt[w];
+            tot += (uint32_t)s_wcnt[w];
         }
+        const uint32_t npair = tot & 0xFFFFu, nmem = npair + (tot >> 16);
         if (nmem == 0) {                                  // nothing to reorder: flags and D_i only
             uint32_t ot[2] = {0, 0};
 #pragma unroll
@@ -543,59 +544,77 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
             __syncthreads();
             continue;
         }
+        {
+            uint32_t o2 = mo & 0xFFFFu, ox = npair + (mo >> 16);
 #pragma unroll
-        for (int j = 0; j < kTileItems; j++)
-            if (hm >> j & 1) s_mem[mo++] = (i0 + j) | ((uint32_t)ra[j] << 11) | ((uint32_t)(re[j] - ra[j]) << 22);
+            for (int j = 0; j < kTileItems; j++)
+                if (hm >> j & 1)
+                    s_mem[(h2 >> j & 1) ? o2++ : ox++] =
+                        (i0 + j) | ((uint32_t)ra[j] << 11) | ((uint32_t)(re[j] - ra[j]) << 22);
+        }
         __syncthreads();
-        // D. rank of each member in its run by (remaining words, row id), member per thread
+        // D. rank of each member in its run by (remaining words, row id), member per thread;
+        // pairs (most runs) with one comparison, in warps of their own
         for (uint32_t u = threadIdx.x; u < nmem; u += blockDim.x) {
             const uint32_t v = s_mem[u];
             const uint32_t i = v & 0x7FFu, a = (v >> 11) & 0x7FFu, L = v >> 22;
             const unsigned long long ki = s_key[tpad(i)];
             const uint32_t ri = s_row[tpad(i)];
             uint32_t r = 0;
-            for (uint32_t k = a; k < a + L; k++) r += key_less(k, i, ki, ri) ? 1u : 0u;   // (k == i: false)
+            if (u < npair) r = key_less(i == a ? a + 1 : a, i, ki, ri) ? 1u : 0u;
+            else
+                for (uint32_t k = a; k < a + L; k++) r += key_less(k, i, ki, ri) ? 1u : 0u;   // (k == i: false)
             s_at[tpad(a + r)] = (uint16_t)i;
         }
         if (threadIdx.x == 0) s_cnt += nmem;
         __syncthreads();
-        // E. write back this thread's positions in run order
-        uint32_t orow[kTileItems], ot[2] = {0, 0};
-        uint32_t ow[NWS][kTileItems];
+        // E. write back: D_i and tie flags of every position; row ids and carried words only
+        // where this thread's positions were reordered (whole 32-byte groups, else untouched)
+        uint32_t ot[2] = {0, 0};
+        if (!hm) {
 #pragma unroll
-        for (int j = 0; j < kTileItems; j++) {
-            const uint32_t dd = i0 + j;
-            uint32_t src = dd;
-            uint32_t t = tb >> j & 1u;
-            uint16_t db = t ? (uint16_t)CKS_NONE_INTERNAL : odb[j];
-            if (hm >> j & 1) {
-                src = s_at[tpad(dd)];
-                if (t) {                                  // after the run's first position
-                    const uint32_t pj = s_at[tpad(dd - 1)];
-                    const unsigned long long x = s_key[tpad(pj)] ^ s_key[tpad(src)];
-                    const uint32_t b0 = 32u * (R.np - 1 - (uint32_t)R.qtop);   // P_M bit of word 0's MSB
-                    int fd = x ? (int)(b0 + (uint32_t)__clzll((long long)x)) : -1;
-                    if (fd < 0)
-                        for (int c = 2; c < Wr; c++) {
-                            const uint32_t y = word(c, pj) ^ word(c, src);
-                            if (y) { fd = (int)(b0 + 32u * (uint32_t)c + (uint32_t)__clz(y)); break; }
-                        }
-                    if (fd >= 0) {
-                        db = __ldg(R.moff + fd);
-                        mark_d(db);
-                    }
-                }
-                t = 0;
+            for (int j = 0; j < kTileItems; j++) {
+                ot[j >> 2] |= (tb >> j & 1u) << (8 * (j & 3));
+                if (tb >> j & 1) odb[j] = CKS_NONE_INTERNAL;
             }
-            orow[j] = s_row[tpad(src)];
-            odb[j] = db;
-            ot[j >> 2] |= t << (8 * (j & 3));
+        } else {
+            uint32_t orow[kTileItems];
+            uint32_t ow[NWS][kTileItems];
 #pragma unroll
-            for (int c = 0; c < NWS; c++) ow[c][j] = s_w[c][tpad(src)];
+            for (int j = 0; j < kTileItems; j++) {
+                const uint32_t dd = i0 + j;
+                uint32_t src = dd;
+                uint32_t t = tb >> j & 1u;
+                uint16_t db = t ? (uint16_t)CKS_NONE_INTERNAL : odb[j];
+                if (hm >> j & 1) {
+                    src = s_at[tpad(dd)];
+                    if (t) {                                  // after the run's first position
+                        const uint32_t pj = s_at[tpad(dd - 1)];
+                        const unsigned long long x = s_key[tpad(pj)] ^ s_key[tpad(src)];
+                        const uint32_t b0 = 32u * (R.np - 1 - (uint32_t)R.qtop);   // P_M bit of word 0's MSB
+                        int fd = x ? (int)(b0 + (uint32_t)__clzll((long long)x)) : -1;
+                        if (fd < 0)
+                            for (int c = 2; c < Wr; c++) {
+                                const uint32_t y = word(c, pj) ^ word(c, src);
+                                if (y) { fd = (int)(b0 + 32u * (uint32_t)c + (uint32_t)__clz(y)); break; }
+                            }
+                        if (fd >= 0) {
+                            db = __ldg(R.moff + fd);
+                            mark_pm((uint32_t)fd);
+                        }
+                    }
+                    t = 0;
+                }
+                orow[j] = s_row[tpad(src)];
+                odb[j] = db;
+                ot[j >> 2] |= t << (8 * (j & 3));
+#pragma unroll
+                for (int c = 0; c < NWS; c++) ow[c][j] = s_w[c][tpad(src)];
+            }
+            st8(R.perm, p0, n, vec, orow);
+#pragma unroll
+            for (int c = 0; c < NWS; c++) st8(R.carried + (uint64_t)(R.qtop - c) * R.pitch, p0, n, vec, ow[c]);
         }
-        st8(R.perm, p0, n, vec, orow);
-#pragma unroll
-        for (int c = 0; c < NWS; c++) st8(R.carried + (uint64_t)(R.qtop - c) * R.pitch, p0, n, vec, ow[c]);
         if (vec && p0 + kTileItems <= n) {
             *reinterpret_cast<uint2*>(tie + p0) = make_uint2(ot[0], ot[1]);
             *reinterpret_cast<uint4*>(R.dbit + p0) =
@@ -607,8 +626,22 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
         }
         __syncthreads();
     }
-    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
-        if (s_bm[w]) atomicOr(&dacc[w], s_bm[w]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dm0 |= __shfl_xor_sync(0xffffffffu, dm0, o);
+        dm1 |= __shfl_xor_sync(0xffffffffu, dm1, o);
+        dm2 |= __shfl_xor_sync(0xffffffffu, dm2, o);
+    }
+    if (lane == 0) {
+        atomicOr(&s_pm[0], dm0);
+        atomicOr(&s_pm[1], dm1);
+        atomicOr(&s_pm[2], dm2);
+    }
+    __syncthreads();
+    if (threadIdx.x < 96 && (s_pm[threadIdx.x >> 5] >> (threadIdx.x & 31) & 1u)) {
+        const uint32_t d = __ldg(R.moff + threadIdx.x);
+        atomicOr(&dacc[d >> 5], 0x80000000u >> (d & 31));
+    }
     if (threadIdx.x == 0 && s_cnt) atomicAdd(handled, s_cnt);
 }
 
