@@ -142,6 +142,43 @@ int cks_adjacent_dbits(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t pac
                        uint64_t n, const uint8_t* sort_mask, uint32_t key_bytes,
                        uint8_t* mask_out, uint32_t* popcount_out, uint16_t* dbit_out);
 
+/* ---- NEXT-4: the sharded path -------------------------------------------
+ * One process per GPU holds a shard of the key column; the pieces below are the per-shard
+ * steps between the exchanges (the orchestration and the collectives are the caller's:
+ * paper_2009_11543_b200/shard.py).
+ *
+ * cks_occupancy: a1's per-byte occupancy of this shard's keys -- bit (v & 31) of word
+ * occ_out[j*8 + (v>>5)] set when byte value v occurs at byte position j (the set whose D-bits
+ * form D+). occ_out: device u32[key_bytes*8], overwritten. Asynchronous. The union
+ * over shards (bitwise OR; NCCL has no OR reduction, so: all-gather + cks_occupancy_mask)
+ * is the occupancy of the whole column. */
+int cks_occupancy(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, uint32_t* occ_out);
+
+/* cks_occupancy_mask: the superset mask of the union of `nocc` occupancies (device
+ * u32[nocc][key_bytes*8], e.g. the all-gathered shard occupancies), n_total = keys over all
+ * shards: kind CKS_SUPERSET_BYTEOCC -> D+ (as cks_superset_mask), CKS_SUPERSET_VARIANT -> V.
+ * mask_out: host u8[key_bytes]; popcount_out: host, may be NULL. Synchronises. */
+int cks_occupancy_mask(cks_ctx* ctx, const uint32_t* occ, uint32_t nocc, uint32_t key_bytes, uint64_t n_total,
+                       int kind, uint8_t* mask_out, uint32_t* popcount_out);
+
+/* cks_rank_sorted: for each query q (device u32[nq][np+1]: P's plane words 0..np-1 --
+ * plane 0 least significant, as cks_compress -- then a row id) the number of elements of
+ * a sorted (P, row id) sequence that are smaller than it (lower bound in the order of
+ * Theorem 2 with the row-id tie-break). sorted_packed: device u32[np][n] (np =
+ * ceil(packed_bits/32)), sorted_rid: device u32[n]; element i's row id is
+ * rid_base + sorted_rid[i] (compared in 64 bits). ranks_out: device u64[nq].
+ * Used to cut a locally sorted shard at the global splitters. Asynchronous. */
+int cks_rank_sorted(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t packed_bits, uint64_t n,
+                    const uint32_t* sorted_rid, uint64_t rid_base, const uint32_t* queries, uint32_t nq,
+                    uint64_t* ranks_out);
+
+/* cks_repack: P_D from P_M for D a subset of M (a7): packed_in device
+ * u32[ceil(|M|/32)][n], packed_out device u32[ceil(|D|/32)][n], both right-aligned as
+ * cks_compress, same element order. in_mask = M, out_mask = D: host u8[key_bytes].
+ * Asynchronous (CKS_EINVAL if D is not a subset of M). */
+int cks_repack(cks_ctx* ctx, const uint32_t* packed_in, const uint8_t* in_mask, const uint8_t* out_mask,
+               uint32_t key_bytes, uint64_t n, uint32_t* packed_out);
+
 /* ---- a8: bottom-up bulk load (Sec. 5.3) -----------------------------------------
  * Nodes have `fanout` slots filled with per_node = floor(fanout*fill) entries.
  * Level 0 = leaves; levels are concatenated leaves first (level_offset[l]).

@@ -59,7 +59,7 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_ctx_stage_ms", "cks_ctx_launches", "cks_ctx_kernel_stats", "cks_strerror", "cks_last_error",
            "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
            "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_paper_tree_shape", "cks_paper_tree",
-           "cks_build", "cks_build_host"]
+           "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack"]
 
 
 def load_library(path: str | None = None):
@@ -97,6 +97,10 @@ def load_library(path: str | None = None):
     L.cks_paper_tree.argtypes = [p, p, u64, u32, p, p, u32, f32, p]
     L.cks_build.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     L.cks_build_host.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
+    L.cks_occupancy.argtypes = [p, p, u64, u32, p]
+    L.cks_occupancy_mask.argtypes = [p, p, u32, u32, u64, i32, p, ctypes.POINTER(u32)]
+    L.cks_rank_sorted.argtypes = [p, p, u32, u64, p, u64, p, u32, p]
+    L.cks_repack.argtypes = [p, p, p, p, u32, u64, p]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or i32
     _lib = L
@@ -104,21 +108,33 @@ def load_library(path: str | None = None):
 
 
 def _context(device: int | None = None):
+    """The calling thread's context on `device` (one per (device, thread): a context owns
+    scratch that its calls reuse, so threads driving one device each get their own)."""
     L = load_library()
     if not torch.cuda.is_available():
         raise RuntimeError("libcks needs a CUDA device (no CPU fallback)")
     dev = torch.cuda.current_device() if device is None else device
+    key = (dev, threading.get_ident())
     with _lock:
-        c = _ctx.get(dev)
+        c = _ctx.get(key)
         if c is None:
             c = ctypes.c_void_p()
             stream = torch.cuda.current_stream(dev).cuda_stream
             rc = L.cks_ctx_create(dev, ctypes.c_void_p(stream), ctypes.byref(c))
             if rc != CKS_OK:
                 raise CksError(rc, L.cks_strerror(rc).decode())
-            _ctx[dev] = c
+            _ctx[key] = c
     L.cks_ctx_set_stream(c, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
     return L, c
+
+
+def release_thread_contexts():
+    """Destroy the calling thread's contexts (and their scratch)."""
+    L = load_library()
+    tid = threading.get_ident()
+    with _lock:
+        for key in [k for k in _ctx if k[1] == tid]:
+            L.cks_ctx_destroy(_ctx.pop(key))
 
 
 def _check(L, c, rc):
@@ -244,6 +260,56 @@ def adjacent_dbits(sorted_packed: torch.Tensor, bits: int, sort_mask, want_dbit:
     _check(L, c, L.cks_adjacent_dbits(c, _ptr(sorted_packed) if sorted_packed.numel() else None, bits, n,
                                       sm.ctypes.data, B, mask.ctypes.data, ctypes.byref(pc), _ptr(dbit)))
     return mask, dbit
+
+
+# ---- NEXT-4: per-shard steps of the sharded path (shard.py drives them) -------------------
+
+def occupancy(keys: torch.Tensor) -> torch.Tensor:
+    """int32[B*8] (u32 bit patterns): per-byte occupancy of these keys (cks_occupancy)."""
+    n, B = _keys(keys)
+    L, c = _context(keys.device.index)
+    occ = torch.empty(B * 8, dtype=torch.int32, device=keys.device)
+    _check(L, c, L.cks_occupancy(c, _ptr(keys), n, B, _ptr(occ)))
+    return occ
+
+
+def occupancy_mask(occs: torch.Tensor, n_total: int, kind: int = SUPERSET_BYTEOCC) -> np.ndarray:
+    """Superset mask [B] of the union of stacked occupancies int32[G, B*8] (cks_occupancy_mask)."""
+    if occs.dtype != torch.int32 or occs.dim() != 2 or occs.shape[1] % 8 or not occs.is_contiguous():
+        raise ValueError("occs must be contiguous int32 [G, B*8]")
+    G, B = occs.shape[0], occs.shape[1] // 8
+    L, c = _context(occs.device.index)
+    mask = np.zeros(B, np.uint8)
+    pc = ctypes.c_uint32()
+    _check(L, c, L.cks_occupancy_mask(c, _ptr(occs), G, B, n_total, kind, mask.ctypes.data, ctypes.byref(pc)))
+    return mask
+
+
+def rank_sorted(sorted_packed: torch.Tensor, bits: int, sorted_rid: torch.Tensor, rid_base: int,
+                queries: torch.Tensor) -> torch.Tensor:
+    """int64[nq]: lower-bound ranks of (P, row id) queries int32[nq, np+1] in a sorted shard."""
+    n = sorted_packed.shape[1]
+    nq = queries.shape[0]
+    if queries.dtype != torch.int32 or not queries.is_contiguous() or queries.shape[1] != nplanes(bits) + 1:
+        raise ValueError("queries must be contiguous int32 [nq, ceil(bits/32)+1]")
+    L, c = _context(sorted_packed.device.index)
+    ranks = torch.empty(nq, dtype=torch.int64, device=sorted_packed.device)
+    _check(L, c, L.cks_rank_sorted(c, _ptr(sorted_packed) if sorted_packed.numel() else None, bits, n,
+                                   _ptr(sorted_rid), rid_base, _ptr(queries) if nq else None, nq,
+                                   _ptr(ranks) if nq else None))
+    return ranks
+
+
+def repack(packed: torch.Tensor, in_mask, out_mask) -> torch.Tensor:
+    """P_out (int32[ceil(|out|/32), n]) from P_in for out_mask a subset of in_mask (cks_repack)."""
+    im = np.ascontiguousarray(np.asarray(in_mask, dtype=np.uint8))
+    om = np.ascontiguousarray(np.asarray(out_mask, dtype=np.uint8))
+    n = packed.shape[1]
+    L, c = _context(packed.device.index)
+    out = torch.empty((nplanes(popcount(om)), n), dtype=torch.int32, device=packed.device)
+    _check(L, c, L.cks_repack(c, _ptr(packed) if packed.numel() else None, im.ctypes.data, om.ctypes.data, im.size, n,
+                              _ptr(out) if out.numel() else None))
+    return out
 
 
 def bulkload_shape(n: int, fanout: int, fill: float = 1.0) -> TreeShape:

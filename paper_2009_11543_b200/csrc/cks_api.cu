@@ -895,6 +895,64 @@ int cks_superset_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B,
     return CKS_OK;
 }
 
+int cks_occupancy(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, uint32_t* occ_out) {
+    TRY(check_keys(ctx, keys, n, B));
+    if (!occ_out) return fail(ctx, CKS_EINVAL, "occ_out is NULL");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemsetAsync(occ_out, 0, (size_t)B * 8 * 4, ctx->stream));
+    if (n) LAUNCH(launch_occupancy(keys, n, B, occ_out, ctx->sms, ctx->stream));
+    return CKS_OK;
+}
+
+int cks_occupancy_mask(cks_ctx* ctx, const uint32_t* occ, uint32_t nocc, uint32_t B, uint64_t n_total, int kind,
+                       uint8_t* mask_out, uint32_t* popcount_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (B < 1 || B > CKS_MAX_KEY_BYTES) return fail(ctx, CKS_EINVAL, "key_bytes %u not in [1,512]", B);
+    if (!occ || nocc == 0 || !mask_out) return fail(ctx, CKS_EINVAL, "NULL occupancy or mask, or nocc = 0");
+    CK(cudaSetDevice(ctx->device));
+    TRY(ensure(ctx, ctx->occ, (size_t)B * 8 * 4));
+    LAUNCH(launch_occ_union(occ, nocc, B * 8, as<uint32_t>(ctx->occ), ctx->stream));
+    uint32_t m = 0;
+    TRY(run_superset(ctx, nullptr, n_total, B, kind, mask_out, &m, /*keys_ready=*/false));
+    if (popcount_out) *popcount_out = m;
+    return CKS_OK;
+}
+
+int cks_rank_sorted(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bits, uint64_t n, const uint32_t* sorted_rid,
+                    uint64_t rid_base, const uint32_t* queries, uint32_t nq, uint64_t* ranks_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (bits > kMaxBits) return fail(ctx, CKS_EINVAL, "packed_bits %u > %u", bits, kMaxBits);
+    if (nq && (!queries || !ranks_out)) return fail(ctx, CKS_EINVAL, "NULL queries or ranks_out");
+    if (n && nq && (!sorted_rid || (bits && !sorted_packed))) return fail(ctx, CKS_EINVAL, "NULL sorted input");
+    CK(cudaSetDevice(ctx->device));
+    LAUNCH(launch_rank_sorted(sorted_packed, (bits + 31) / 32, n, sorted_rid, rid_base, queries, nq,
+                              reinterpret_cast<unsigned long long*>(ranks_out), ctx->stream));
+    return CKS_OK;
+}
+
+int cks_repack(cks_ctx* ctx, const uint32_t* packed_in, const uint8_t* in_mask, const uint8_t* out_mask, uint32_t B,
+               uint64_t n, uint32_t* packed_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (B < 1 || B > CKS_MAX_KEY_BYTES) return fail(ctx, CKS_EINVAL, "key_bytes %u not in [1,512]", B);
+    if (!in_mask || !out_mask) return fail(ctx, CKS_EINVAL, "mask pointer is NULL");
+    for (uint32_t j = 0; j < B; j++)
+        if (out_mask[j] & ~in_mask[j]) return fail(ctx, CKS_EINVAL, "out_mask is not a subset of in_mask (byte %u)", j);
+    const uint32_t m = popcount_mask(in_mask, B), d = popcount_mask(out_mask, B);
+    if (n == 0 || d == 0) return CKS_OK;
+    if (!packed_in || !packed_out) return fail(ctx, CKS_EINVAL, "NULL packed buffer");
+    CK(cudaSetDevice(ctx->device));
+    const uint32_t np = (m + 31) / 32;
+    std::vector<uint32_t> sub(np, 0);
+    repack_words(in_mask, out_mask, B, m, 0, sub);
+    TRY(claim_slot(ctx, 1));
+    plan_repack(sub.data(), np, ctx->h_plan[1]);
+    GatherPlan* dplan;
+    TRY(upload_plan(ctx, 1, &dplan));
+    LAUNCH(launch_repack(packed_in, n, n, dplan, ctx->h_plan[1]->nsteps, (d + 31) / 32, packed_out, n, ctx->sms,
+                         ctx->stream));
+    return CKS_OK;
+}
+
 int cks_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* mask,
                  uint32_t* packed_out) {
     TRY(check_keys(ctx, keys, n, B));

@@ -104,6 +104,9 @@ cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
 
 // NEXT-1 prefix refinement (k_refine.cu)
 uint64_t ref_tiles(uint64_t nr);
+cudaError_t launch_occ_union(const uint32_t* occ, uint32_t nocc, uint32_t words, uint32_t* out, cudaStream_t st);
+cudaError_t launch_rank_sorted(const uint32_t* planes, uint32_t np, uint64_t n, const uint32_t* rid, uint64_t rid_base,
+                               const uint32_t* q, uint32_t nq, unsigned long long* ranks, cudaStream_t st);
 cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, uint32_t fmask,
                             const uint16_t* moff, uint32_t* perm, uint16_t* dbit, uint32_t* carried, const uint32_t* lo,
                             const uint32_t* hi, uint64_t hpitch, uint64_t n, unsigned long long cmask, uint32_t B,

@@ -1,0 +1,273 @@
+"""NEXT-4: the sharded first build.
+
+One rank per GPU holds a contiguous shard of the key column (rank r: global row ids
+off_r .. off_r + n_r - 1). The method shards with one exchange step:
+
+  a1  per-shard byte occupancy -> all-gather -> union -> D+ (cks_occupancy[_mask]); NCCL has
+      no bitwise-OR reduction, so the union is taken on the gathered occupancies;
+  a3  compress the shard by D+ (row-parallel, no exchange);
+  a5  local sort of (P, row id); a regular sample of every sorted shard -> all-gather ->
+      G-1 splitters in the (P, row id) order (total: duplicates split by row id), cut every
+      sorted shard at the splitters (cks_rank_sorted) -> ONE all-to-all of (P, row id) ->
+      sort the received pairs by (P, row id): rank r now holds the r-th slice of the global
+      order (the paper's range partition);
+  a6  adjacency over the slice plus the pair across each slice boundary (the previous
+      non-empty slice's last key is all-gathered), D = OR of the slices' D (all-gather);
+  a7  P_D of the slice by repacking P_{D+} (cks_repack);
+  a8  rank 0 bulk-loads the gathered order (the thin tail; per-shard subtrees with a merged
+      top, are the next step).
+
+Every per-shard step is a libcks kernel (`CudaOps`); this module only moves data between
+ranks. `Comm` implementations: `TorchComm` (torch.distributed: NCCL between GPUs, gloo for
+the CPU tests) and `ThreadComm` (G ranks as threads of one process on one device -- no
+kernel waits on another rank; used to run the sharded path on one GPU).
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from . import cks
+
+NONE = 0xFFFF
+
+
+# ---- communicators -----------------------------------------------------------------------
+
+class TorchComm:
+    """Collectives over a torch.distributed process group (NCCL: CUDA tensors; gloo: the
+    tensors are staged through host memory)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        self.cpu = dist.get_backend(group) == "gloo"
+
+    def _dev(self, t):
+        return t.cpu() if self.cpu else t
+
+    def allgather(self, t: torch.Tensor) -> list[torch.Tensor]:
+        x = self._dev(t.contiguous())
+        out = [torch.empty_like(x) for _ in range(self.size)]
+        self.dist.all_gather(out, x, group=self.group)
+        return [o.to(t.device) for o in out]
+
+    def alltoallv(self, t: torch.Tensor, send_counts: list[int]) -> torch.Tensor:
+        """Rows [sum(send_counts[:d]), +send_counts[d]) of t go to rank d; returns the rows
+        received, source rank order."""
+        x = self._dev(t.contiguous())
+        sc = torch.tensor(send_counts, dtype=torch.int64)
+        rc = torch.empty_like(sc)
+        sc_d, rc_d = (sc, rc) if self.cpu else (sc.to(t.device), rc.to(t.device))
+        self.dist.all_to_all_single(rc_d, sc_d, group=self.group)
+        recv_counts = [int(v) for v in rc_d.tolist()]
+        out = torch.empty((sum(recv_counts),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        self.dist.all_to_all_single(out, x, recv_counts, send_counts, group=self.group)
+        return out.to(t.device)
+
+
+class ThreadComm:
+    """G ranks as threads of one process (each thread: its own CUDA stream and libcks
+    context). A collective synchronises the caller's stream, publishes its tensor, and
+    waits at a barrier for the others."""
+
+    class _Shared:
+        def __init__(self, size):
+            self.size = size
+            self.barrier = threading.Barrier(size)
+            self.slots = [None] * size
+
+    def __init__(self, shared, rank):
+        self.sh, self.rank, self.size = shared, rank, shared.size
+
+    @classmethod
+    def group(cls, size: int) -> list["ThreadComm"]:
+        sh = cls._Shared(size)
+        return [cls(sh, r) for r in range(size)]
+
+    def _publish(self, obj):
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+        self.sh.slots[self.rank] = obj
+        self.sh.barrier.wait()
+
+    def allgather(self, t: torch.Tensor) -> list[torch.Tensor]:
+        self._publish(t.contiguous())
+        out = [s.clone() for s in self.sh.slots]
+        self.sh.barrier.wait()
+        return out
+
+    def alltoallv(self, t: torch.Tensor, send_counts: list[int]) -> torch.Tensor:
+        self._publish(list(torch.split(t.contiguous(), send_counts, dim=0)))
+        out = torch.cat([self.sh.slots[s][self.rank] for s in range(self.size)], dim=0).clone()
+        self.sh.barrier.wait()
+        return out
+
+    @staticmethod
+    def run(size: int, fn, *args_per_rank):
+        """Run fn(comm, *args_per_rank[r]) for every rank r in its own thread; results by rank."""
+        comms = ThreadComm.group(size)
+        res, err = [None] * size, []
+
+        def body(r):
+            try:
+                dev = torch.cuda.current_device() if torch.cuda.is_available() else None
+                if dev is not None:
+                    with torch.cuda.stream(torch.cuda.Stream(dev)):
+                        res[r] = fn(comms[r], *[a[r] for a in args_per_rank])
+                        torch.cuda.current_stream().synchronize()
+                    cks.release_thread_contexts()
+                else:
+                    res[r] = fn(comms[r], *[a[r] for a in args_per_rank])
+            except BaseException as e:          # unblock the others, re-raise below
+                err.append(e)
+                comms[r].sh.barrier.abort()
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(size)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if err:
+            raise err[0]
+        return res
+
+
+# ---- per-shard steps -------------------------------------------------------------------------
+
+class CudaOps:
+    """The per-shard steps as libcks kernels (the product path; no CPU fallback)."""
+    occupancy = staticmethod(cks.occupancy)
+    occupancy_mask = staticmethod(cks.occupancy_mask)
+    compress = staticmethod(cks.compress)
+    rank_sorted = staticmethod(cks.rank_sorted)
+    repack = staticmethod(cks.repack)
+
+    @staticmethod
+    def sort(planes, bits, row_ids=None):
+        return cks.sort(planes, bits, row_ids, want_sorted=True)
+
+    @staticmethod
+    def adjacent(sorted_planes, bits, sort_mask):
+        return cks.adjacent_dbits(sorted_planes, bits, sort_mask, want_dbit=True)
+
+    @staticmethod
+    def bulkload(perm, dbit, fanout, fill):
+        return cks.bulkload(perm, dbit, fanout, fill)
+
+
+# ---- host logic ----------------------------------------------------------------------------
+
+def pick_splitters(samples: np.ndarray, size: int) -> np.ndarray:
+    """G-1 splitters from the gathered regular samples (u32 rows: P plane words 0..np-1, then
+    the row id), in the (P, row id) order: the samples at ranks i*S/G, i = 1..G-1."""
+    s = np.asarray(samples, dtype=np.uint32).reshape(-1, samples.shape[-1])
+    if size <= 1 or s.shape[0] == 0:
+        return np.zeros((0, s.shape[1]), np.uint32)
+    npl = s.shape[1] - 1
+    order = np.lexsort([s[:, npl]] + [s[:, w] for w in range(npl)])   # last key primary: top plane
+    srt = s[order]
+    return np.ascontiguousarray(srt[[(i * srt.shape[0]) // size for i in range(1, size)]])
+
+
+def regular_sample(count: int, per_rank: int) -> np.ndarray:
+    """Positions of a regular sample of `per_rank` elements of a sorted shard of `count`."""
+    s = min(per_rank, count)
+    return ((2 * np.arange(s, dtype=np.int64) + 1) * count) // (2 * s) if s else np.zeros(0, np.int64)
+
+
+def _as_i32(x: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.uint32)).view(np.int32)
+
+
+# ---- the sharded first build -------------------------------------------------------------------
+
+def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int = 256, fanout: int = 64,
+                  fill: float = 1.0, tree: bool = True, superset_kind: int = cks.SUPERSET_BYTEOCC) -> dict:
+    """This rank's slice of the global first build. Returns dict(mask = exact D (same on all
+    ranks), popcount, sort_mask = D+, sort_bits, perm = global row ids of the slice in order,
+    dbit = D_i of the slice (against the global predecessor), packed = P_D of the slice,
+    offset = global position of the slice's first key, n_total, send_counts, tree (rank 0))."""
+    G, r = comm.size, comm.rank
+    dev = keys.device
+    n, B = int(keys.shape[0]), int(keys.shape[1])
+    ns = [int(t.item()) for t in comm.allgather(torch.tensor([n], dtype=torch.int64, device=dev))]
+    off, N = sum(ns[:r]), sum(ns)
+    if N >= 1 << 32:
+        raise ValueError("n_total >= 2^32 (u32 row ids)")
+
+    # a1: D+ of the whole column from the union of the shard occupancies
+    occ = ops.occupancy(keys)
+    M = ops.occupancy_mask(torch.stack(comm.allgather(occ)), N, superset_kind)
+    m = cks.popcount(M)
+    npl = cks.nplanes(m)
+
+    # a3 + local a5
+    P = ops.compress(keys, M)
+    perm_l, S = ops.sort(P, m, None)                              # local indices, sorted planes
+    rid_g = perm_l + off if n else perm_l                         # global row ids (u32 patterns)
+
+    # splitters from a regular sample of every sorted shard
+    pos = torch.from_numpy(regular_sample(n, samples_per_rank)).to(dev)
+    samp = torch.zeros((samples_per_rank, npl + 1), dtype=torch.int32, device=dev)
+    if pos.numel():
+        samp[:pos.numel(), :npl] = S[:, pos].t()
+        samp[:pos.numel(), npl] = rid_g[pos]
+    cnt = torch.tensor([pos.numel()], dtype=torch.int64, device=dev)
+    counts = [int(c.item()) for c in comm.allgather(cnt)]
+    rows = [t[:c].cpu().numpy().view(np.uint32) for t, c in zip(comm.allgather(samp), counts)]
+    spl = pick_splitters(np.concatenate(rows) if rows else np.zeros((0, npl + 1), np.uint32), G)
+    q = torch.from_numpy(_as_i32(spl)).to(dev).reshape(-1, npl + 1)
+    cuts = ops.rank_sorted(S, m, perm_l, off, q).cpu().tolist() if G > 1 else []
+    bounds = [0] + [int(c) for c in cuts] + [n]
+    send_counts = [bounds[i + 1] - bounds[i] for i in range(G)]
+
+    # the one exchange: (P, row id) rows to the rank owning their slice
+    rowsP = torch.cat([S.t(), rid_g.view(-1, 1)], dim=1) if n else torch.zeros((0, npl + 1), dtype=torch.int32,
+                                                                                  device=dev)
+    recv = comm.alltoallv(rowsP, send_counts)
+    R = recv[:, :npl].t().contiguous()
+    rids = recv[:, npl].contiguous()
+    nr = int(recv.shape[0])
+    perm, S2 = ops.sort(R, m, rids)                               # (P, row id) order: perm = global row ids
+
+    # a6: the slice plus the pair across its left boundary
+    last = torch.zeros(npl + 1, dtype=torch.int32, device=dev)
+    if nr:
+        last[0] = 1
+        last[1:] = S2[:, nr - 1]
+    lasts = comm.allgather(last)
+    prev = next((lasts[k][1:] for k in range(r - 1, -1, -1) if int(lasts[k][0].item())), None)
+    if prev is not None and nr:
+        Dl, dbit = ops.adjacent(torch.cat([prev.view(-1, 1), S2], dim=1).contiguous(), m, M)
+        dbit = dbit[1:]
+    else:
+        Dl, dbit = ops.adjacent(S2, m, M)
+    D = np.bitwise_or.reduce(np.stack([t.cpu().numpy() for t in comm.allgather(
+        torch.from_numpy(np.ascontiguousarray(Dl)).to(dev))]), axis=0).astype(np.uint8)
+
+    # a7: P_D of the slice
+    packed = ops.repack(S2, M, D) if not np.array_equal(D, M) else S2
+
+    nrs = [int(t.item()) for t in comm.allgather(torch.tensor([nr], dtype=torch.int64, device=dev))]
+    out = dict(mask=D, popcount=cks.popcount(D), sort_mask=M, sort_bits=m, perm=perm, dbit=dbit, packed=packed,
+               offset=sum(nrs[:r]), n_total=N, send_counts=send_counts, tree=None)
+
+    # a8: rank 0 bulk-loads the gathered order
+    if tree and N:
+        mx = max(nrs)
+        pad = torch.zeros((mx, 2), dtype=torch.int32, device=dev)
+        if nr:
+            pad[:nr, 0] = perm
+            pad[:nr, 1] = dbit.to(torch.int32)
+        allp = comm.allgather(pad)
+        if r == 0:
+            gp = torch.cat([t[:c, 0] for t, c in zip(allp, nrs)]).contiguous()
+            gd = torch.cat([t[:c, 1] for t, c in zip(allp, nrs)]).to(torch.int16).contiguous()
+            out["tree"] = ops.bulkload(gp, gd, fanout, fill)
+    return out
