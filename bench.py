@@ -188,6 +188,70 @@ def run_reference(args, world, rank):
 
 # ------------------------------------------------------------------------------------------
 
+def run_sharded(args, world, rank, local):
+    """--sharded (NEXT-4): every rank holds a full-size shard of the config (rank r: generator
+    seed + r; rank 0's shard is the single-GPU workload) and the ranks build ONE index over the
+    union (shard.build_sharded: occupancy all-gather, splitters, one all-to-all of (P, row id),
+    boundary pairs, OR of D, rank-0 bulk load). Weak scaling: n keys per GPU."""
+    import numpy as np
+    import torch
+
+    import cksgen
+    from paper_2009_11543_b200 import cks, shard
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    c = cksgen.CONFIGS[args.config]
+    n, B = c["n"], c["B"]
+    host = torch.empty((n, B), dtype=torch.uint8, pin_memory=True)
+    cksgen.config(args.config, seed=c["seed"] + rank, out=host.numpy())
+    keys = host.to(device)
+    comm = shard.TorchComm() if world > 1 else shard.ThreadComm.group(1)[0]
+    stream = torch.cuda.current_stream(device)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    for _ in range(args.warmup):
+        out = shard.build_sharded(keys, comm)
+    torch.cuda.synchronize(device)
+    cks.set_timing(True)
+    k_ms = k_bytes = 0.0
+    launches0 = cks.launches()
+    barrier(world)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        out = shard.build_sharded(keys, comm)
+        kms, kby, _ = cks.kernel_stats()
+        k_ms += kms
+        k_bytes += kby
+    ev1.record(stream)
+    torch.cuda.synchronize(device)
+    clk = clocks.stop()
+    barrier(world)
+    gpu_launches = cks.launches() - launches0
+    cks.set_timing(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_max = max_over_ranks(ms, world, device)
+    peak, peak_src = measured_peaks()
+    achieved = (k_bytes / (k_ms * 1e-3) / 1e9) if k_ms > 0 else None
+    slice_max = max_over_ranks(float(out["perm"].numel()), world, device)
+    if rank == 0:
+        line = {"metric": METRIC, "value": n * world / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": {"workload": c["name"], "n_per_rank": n, "n_total": n * world, "key_bytes": B,
+                           "fanout": 64, "sort_bits": int(out["sort_bits"]), "d_bits": int(out["popcount"]),
+                           "parallelism": f"sharded: range partition over {world} rank(s), one all-to-all",
+                           "largest_slice": int(slice_max), "l2": "inputs larger than L2, no flush"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": (achieved / peak) if (achieved and peak) else None, "traffic": None,
+                             "kernel": "k_downsweep_ws (warp-specialised LSD digit pass)", "peak_source": peak_src},
+                "cpu_baseline": None, "e2e": None, "gpu_launches": gpu_launches, "clocks": clk}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,11 +267,20 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-full-key", action="store_true", help="skip the full-key comparison (NEXT-2)")
     ap.add_argument("--full-key-steps", type=int, default=3)
+    ap.add_argument("--sharded", action="store_true",
+                    help="NEXT-4: one global build over all ranks' shards (range partition + all-to-all) "
+                         "instead of one independent build per rank")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3                                     # contract: W >= 3
 
     world, rank, local = dist_setup(args)
+    if args.sharded and args.impl == "ours":
+        run_sharded(args, world, rank, local)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, world, rank)
         if world > 1:

@@ -172,6 +172,17 @@ int cks_rank_sorted(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t packed
                     const uint32_t* sorted_rid, uint64_t rid_base, const uint32_t* queries, uint32_t nq,
                     uint64_t* ranks_out);
 
+/* cks_partition: stable partition of a shard's (P, row id) pairs by G-1 splitters (device
+ * u32[G-1][np+1], the query layout of cks_rank_sorted, ascending): element i (row id
+ * rid_base + i) goes to part d = the number of splitters <= (P_i, rid_base + i). Outputs, in
+ * part order and within a part in input order: packed_out device u32[np][n], rid_out device
+ * u32[n] (the row ids), counts_out device u64[G] (elements per part). One destination pass
+ * plus one LSD digit pass on the part index (G <= 256). Since the parts keep the input
+ * order, a receiver that concatenates the parts sent to it in source-rank order holds them in
+ * row-id order, and a stable sort on P alone yields the (P, row id) order. Asynchronous. */
+int cks_partition(cks_ctx* ctx, const uint32_t* packed, uint32_t packed_bits, uint64_t n, const uint32_t* splitters,
+                  uint32_t parts, uint64_t rid_base, uint32_t* packed_out, uint32_t* rid_out, uint64_t* counts_out);
+
 /* cks_repack: P_D from P_M for D a subset of M (a7): packed_in device
  * u32[ceil(|M|/32)][n], packed_out device u32[ceil(|D|/32)][n], both right-aligned as
  * cks_compress, same element order. in_mask = M, out_mask = D: host u8[key_bytes].

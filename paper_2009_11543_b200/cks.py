@@ -59,7 +59,8 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_ctx_stage_ms", "cks_ctx_launches", "cks_ctx_kernel_stats", "cks_strerror", "cks_last_error",
            "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
            "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_paper_tree_shape", "cks_paper_tree",
-           "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack"]
+           "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
+           "cks_partition"]
 
 
 def load_library(path: str | None = None):
@@ -101,6 +102,7 @@ def load_library(path: str | None = None):
     L.cks_occupancy_mask.argtypes = [p, p, u32, u32, u64, i32, p, ctypes.POINTER(u32)]
     L.cks_rank_sorted.argtypes = [p, p, u32, u64, p, u64, p, u32, p]
     L.cks_repack.argtypes = [p, p, p, p, u32, u64, p]
+    L.cks_partition.argtypes = [p, p, u32, u64, p, u32, u64, p, p, p]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or i32
     _lib = L
@@ -298,6 +300,24 @@ def rank_sorted(sorted_packed: torch.Tensor, bits: int, sorted_rid: torch.Tensor
                                    _ptr(sorted_rid), rid_base, _ptr(queries) if nq else None, nq,
                                    _ptr(ranks) if nq else None))
     return ranks
+
+
+def partition(packed: torch.Tensor, bits: int, splitters: torch.Tensor, parts: int, rid_base: int):
+    """(packed int32[np, n], row ids int32[n], counts int64[parts]): stable partition of the
+    (P, rid_base + i) pairs by parts-1 splitters int32[parts-1, np+1] (cks_partition)."""
+    n = packed.shape[1]
+    if packed.dtype != torch.int32 or not packed.is_contiguous() or packed.shape[0] != nplanes(bits):
+        raise ValueError("packed must be contiguous int32 [ceil(bits/32), n]")
+    if splitters.dtype != torch.int32 or not splitters.is_contiguous() or splitters.shape[0] != parts - 1:
+        raise ValueError("splitters must be contiguous int32 [parts-1, ceil(bits/32)+1]")
+    L, c = _context(packed.device.index)
+    out = torch.empty_like(packed)
+    rid = torch.empty(n, dtype=torch.int32, device=packed.device)
+    counts = torch.empty(parts, dtype=torch.int64, device=packed.device)
+    _check(L, c, L.cks_partition(c, _ptr(packed) if packed.numel() else None, bits, n,
+                                 _ptr(splitters) if splitters.numel() else None, parts, rid_base,
+                                 _ptr(out) if out.numel() else None, _ptr(rid) if n else None, _ptr(counts)))
+    return out, rid, counts
 
 
 def repack(packed: torch.Tensor, in_mask, out_mask) -> torch.Tensor:

@@ -49,7 +49,8 @@ struct cks_ctx {
     // scratch
     DevBuf occ, masks8, planeA, planeB, ridA, ridB, dacc, moff, dbit,
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
-        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, runoff2, runpos2, tie, keep, done, mlist, wlist, rcnt, rtot;   // NEXT-1
+        pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, runoff2, runpos2, tie, keep, done, mlist, wlist, rcnt, rtot,   // NEXT-1
+        part_in, part_out;                                                 // NEXT-4
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
     uint16_t* h_moff = nullptr;
@@ -927,6 +928,43 @@ int cks_rank_sorted(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bits, 
     CK(cudaSetDevice(ctx->device));
     LAUNCH(launch_rank_sorted(sorted_packed, (bits + 31) / 32, n, sorted_rid, rid_base, queries, nq,
                               reinterpret_cast<unsigned long long*>(ranks_out), ctx->stream));
+    return CKS_OK;
+}
+
+int cks_partition(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t n, const uint32_t* splitters,
+                  uint32_t parts, uint64_t rid_base, uint32_t* packed_out, uint32_t* rid_out, uint64_t* counts_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (bits > kMaxBits) return fail(ctx, CKS_EINVAL, "packed_bits %u > %u", bits, kMaxBits);
+    if (parts < 1 || parts > 256) return fail(ctx, CKS_EINVAL, "parts %u not in [1, 256]", parts);
+    if (n >= (1ull << 32) || rid_base + n > (1ull << 32)) return fail(ctx, CKS_ERANGE, "row ids exceed u32");
+    if (!counts_out || (parts > 1 && !splitters)) return fail(ctx, CKS_EINVAL, "NULL splitters or counts_out");
+    if (n && (!rid_out || (bits && (!packed || !packed_out)))) return fail(ctx, CKS_EINVAL, "NULL buffer with n > 0");
+    CK(cudaSetDevice(ctx->device));
+    const uint32_t np = (bits + 31) / 32;
+    if (parts == 1 || n == 0) {                                   // one part: the input order
+        const unsigned long long cnt = n;
+        CK(cudaMemsetAsync(counts_out, 0, (size_t)parts * 8, ctx->stream));
+        CK(cudaMemcpyAsync(counts_out, &cnt, 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));                   // (&cnt is on the stack)
+        if (n && np) CK(cudaMemcpyAsync(packed_out, packed, (size_t)np * n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (n) {
+            LAUNCH(launch_iota(rid_out, n, ctx->stream));
+            LAUNCH(launch_add_base(rid_out, n, (uint32_t)rid_base, ctx->sms, ctx->stream));
+        }
+        return CKS_OK;
+    }
+    // [part index, P planes] -> one LSD pass on the part index's low byte (stable)
+    const uint64_t sp = scratch_pitch(n);
+    TRY(ensure(ctx, ctx->part_in, (size_t)(np + 1) * sp * 4));
+    TRY(ensure(ctx, ctx->part_out, (size_t)(np + 1) * sp * 4));
+    uint32_t* in = as<uint32_t>(ctx->part_in);
+    uint32_t* out = as<uint32_t>(ctx->part_out);
+    LAUNCH(launch_part_dest(packed, np, n, n, splitters, parts - 1, rid_base, in,
+                            reinterpret_cast<unsigned long long*>(counts_out), ctx->sms, ctx->stream));
+    if (np) CK(cudaMemcpy2DAsync(in + sp, sp * 4, packed, n * 4, n * 4, np, cudaMemcpyDeviceToDevice, ctx->stream));
+    TRY(run_sort(ctx, in, sp, np + 1, 1, n, nullptr, 0, out, sp, rid_out, nullptr, nullptr, 0, false));
+    if (np) CK(cudaMemcpy2DAsync(packed_out, n * 4, out + sp, sp * 4, n * 4, np, cudaMemcpyDeviceToDevice, ctx->stream));
+    LAUNCH(launch_add_base(rid_out, n, (uint32_t)rid_base, ctx->sms, ctx->stream));
     return CKS_OK;
 }
 

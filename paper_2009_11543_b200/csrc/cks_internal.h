@@ -104,6 +104,10 @@ cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
 
 // NEXT-1 prefix refinement (k_refine.cu)
 uint64_t ref_tiles(uint64_t nr);
+cudaError_t launch_part_dest(const uint32_t* planes, uint32_t np, uint64_t n, uint64_t pitch, const uint32_t* spl,
+                             uint32_t nspl, uint64_t rid_base, uint32_t* dest, unsigned long long* counts, int sms,
+                             cudaStream_t st);
+cudaError_t launch_add_base(uint32_t* a, uint64_t n, uint32_t base, int sms, cudaStream_t st);
 cudaError_t launch_occ_union(const uint32_t* occ, uint32_t nocc, uint32_t words, uint32_t* out, cudaStream_t st);
 cudaError_t launch_rank_sorted(const uint32_t* planes, uint32_t np, uint64_t n, const uint32_t* rid, uint64_t rid_base,
                                const uint32_t* q, uint32_t nq, unsigned long long* ranks, cudaStream_t st);

@@ -41,6 +41,67 @@ __global__ void k_rank_sorted(const uint32_t* __restrict__ planes, uint32_t np, 
     ranks[t] = lo;
 }
 
+// part of every element: the number of splitters (in shared memory) <= (P_i, rid_base + i);
+// per-part counts
+__global__ void __launch_bounds__(256)
+k_part_dest(const uint32_t* __restrict__ planes, uint32_t np, uint64_t n, uint64_t pitch,
+            const uint32_t* __restrict__ spl, uint32_t nspl, uint64_t rid_base, uint32_t* __restrict__ dest,
+            unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t s_sp[];                     // [nspl][np+1], then counts [nspl+1]
+    uint32_t* s_cnt = s_sp + nspl * (np + 1);
+    for (uint32_t i = threadIdx.x; i < nspl * (np + 1); i += blockDim.x) s_sp[i] = spl[i];
+    for (uint32_t i = threadIdx.x; i <= nspl; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = nspl;                        // first splitter > element
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            const uint32_t* sk = s_sp + mid * (np + 1);
+            int c = 0;                                     // sign of splitter - element
+            for (int w = (int)np - 1; w >= 0 && c == 0; w--) {
+                const uint32_t a = sk[w], b = planes[(uint64_t)w * pitch + i];
+                c = a < b ? -1 : a > b ? 1 : 0;
+            }
+            if (c == 0) {
+                const uint64_t a = sk[np], b = rid_base + i;
+                c = a < b ? -1 : a > b ? 1 : 0;
+            }
+            if (c <= 0) lo = mid + 1;
+            else hi = mid;
+        }
+        dest[i] = lo;
+        atomicAdd(&s_cnt[lo], 1u);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i <= nspl; i += blockDim.x)
+        if (s_cnt[i]) atomicAdd(&counts[i], (unsigned long long)s_cnt[i]);
+}
+
+__global__ void k_add_base(uint32_t* __restrict__ a, uint64_t n, uint32_t base) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] += base;
+}
+
+cudaError_t launch_part_dest(const uint32_t* planes, uint32_t np, uint64_t n, uint64_t pitch, const uint32_t* spl,
+                             uint32_t nspl, uint64_t rid_base, uint32_t* dest, unsigned long long* counts, int sms,
+                             cudaStream_t st) {
+    cudaMemsetAsync(counts, 0, (size_t)(nspl + 1) * 8, st);
+    if (n == 0) return cudaGetLastError();
+    const size_t smem = ((size_t)nspl * (np + 1) + nspl + 1) * 4;
+    uint64_t g = (n + 255) / 256;
+    if (g > (uint64_t)sms * 8) g = (uint64_t)sms * 8;
+    k_part_dest<<<(unsigned)g, 256, smem, st>>>(planes, np, n, pitch, spl, nspl, rid_base, dest, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add_base(uint32_t* a, uint64_t n, uint32_t base, int sms, cudaStream_t st) {
+    if (n == 0 || base == 0) return cudaSuccess;
+    uint64_t g = (n + 255) / 256;
+    if (g > (uint64_t)sms * 8) g = (uint64_t)sms * 8;
+    k_add_base<<<(unsigned)g, 256, 0, st>>>(a, n, base);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_occ_union(const uint32_t* occ, uint32_t nocc, uint32_t words, uint32_t* out, cudaStream_t st) {
     k_occ_union<<<(words + 255) / 256 ? (words + 255) / 256 : 1, 256, 0, st>>>(occ, nocc, words, out);
     return cudaGetLastError();

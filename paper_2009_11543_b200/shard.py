@@ -6,11 +6,12 @@ off_r .. off_r + n_r - 1). The method shards with one exchange step (SURVEY 8(e)
   a1  per-shard byte occupancy -> all-gather -> union -> D+ (cks_occupancy[_mask]); NCCL has
       no bitwise-OR reduction, so the union is taken on the gathered occupancies;
   a3  compress the shard by D+ (row-parallel, no exchange);
-  a5  local sort of (P, row id); a regular sample of every sorted shard -> all-gather ->
-      G-1 splitters in the (P, row id) order (total: duplicates split by row id), cut every
-      sorted shard at the splitters (cks_rank_sorted) -> ONE all-to-all of (P, row id) ->
-      sort the received pairs by (P, row id): rank r now holds the r-th slice of the global
-      order (the paper's range partition, P:842-843, P:870-879);
+  a5  a regular sample of every shard -> all-gather -> G-1 splitters in the (P, row id)
+      order (total: duplicates split by row id); every shard is partitioned by them, stably
+      (cks_partition: one destination pass + one digit pass) -> ONE all-to-all of
+      (P, row id); the received parts, concatenated in source-rank order, are in row-id
+      order, so one stable sort on P alone orders them by (P, row id): rank r now holds the
+      r-th slice of the global order (the paper's range partition, P:842-843, P:870-879);
   a6  adjacency over the slice plus the pair across each slice boundary (the previous
       non-empty slice's last key is all-gathered), D = OR of the slices' D (all-gather);
   a7  P_D of the slice by repacking P_{D+} (cks_repack);
@@ -145,7 +146,7 @@ class CudaOps:
     occupancy = staticmethod(cks.occupancy)
     occupancy_mask = staticmethod(cks.occupancy_mask)
     compress = staticmethod(cks.compress)
-    rank_sorted = staticmethod(cks.rank_sorted)
+    partition = staticmethod(cks.partition)
     repack = staticmethod(cks.repack)
 
     @staticmethod
@@ -200,6 +201,12 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
     off, N = sum(ns[:r]), sum(ns)
     if N >= 1 << 32:
         raise ValueError("n_total >= 2^32 (u32 row ids)")
+    if N == 0:
+        e = torch.zeros(0, dtype=torch.int32, device=dev)
+        z = np.zeros(B, np.uint8)
+        return dict(mask=z, popcount=0, sort_mask=z, sort_bits=0, perm=e, dbit=e.to(torch.int16),
+                    packed=torch.zeros((0, 0), dtype=torch.int32, device=dev), offset=0, n_total=0,
+                    send_counts=[0] * G, tree=None)
 
     # a1: D+ of the whole column from the union of the shard occupancies
     occ = ops.occupancy(keys)
@@ -207,34 +214,31 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
     m = cks.popcount(M)
     npl = cks.nplanes(m)
 
-    # a3 + local a5
+    # a3
     P = ops.compress(keys, M)
-    perm_l, S = ops.sort(P, m, None)                              # local indices, sorted planes
-    rid_g = perm_l + off if n else perm_l                         # global row ids (u32 patterns)
 
-    # splitters from a regular sample of every sorted shard
+    # splitters from a regular sample of every shard
     pos = torch.from_numpy(regular_sample(n, samples_per_rank)).to(dev)
     samp = torch.zeros((samples_per_rank, npl + 1), dtype=torch.int32, device=dev)
     if pos.numel():
-        samp[:pos.numel(), :npl] = S[:, pos].t()
-        samp[:pos.numel(), npl] = rid_g[pos]
+        samp[:pos.numel(), :npl] = P[:, pos].t()
+        samp[:pos.numel(), npl] = (pos + off).to(torch.int32)
     cnt = torch.tensor([pos.numel()], dtype=torch.int64, device=dev)
     counts = [int(c.item()) for c in comm.allgather(cnt)]
     rows = [t[:c].cpu().numpy().view(np.uint32) for t, c in zip(comm.allgather(samp), counts)]
     spl = pick_splitters(np.concatenate(rows) if rows else np.zeros((0, npl + 1), np.uint32), G)
     q = torch.from_numpy(_as_i32(spl)).to(dev).reshape(-1, npl + 1)
-    cuts = ops.rank_sorted(S, m, perm_l, off, q).cpu().tolist() if G > 1 else []
-    bounds = [0] + [int(c) for c in cuts] + [n]
-    send_counts = [bounds[i + 1] - bounds[i] for i in range(G)]
 
-    # the one exchange: (P, row id) rows to the rank owning their slice
-    rowsP = torch.cat([S.t(), rid_g.view(-1, 1)], dim=1) if n else torch.zeros((0, npl + 1), dtype=torch.int32,
-                                                                                  device=dev)
+    # a5: stable partition, the one exchange, one stable sort on P
+    Pp, ridp, pc = ops.partition(P, m, q, G, off)
+    send_counts = [int(v) for v in pc.cpu().tolist()]
+    rowsP = torch.cat([Pp.t(), ridp.view(-1, 1)], dim=1)
     recv = comm.alltoallv(rowsP, send_counts)
     R = recv[:, :npl].t().contiguous()
     rids = recv[:, npl].contiguous()
     nr = int(recv.shape[0])
-    perm, S2 = ops.sort(R, m, rids)                               # (P, row id) order: perm = global row ids
+    order, S2 = ops.sort(R, m, None)                              # stable: received order = row-id order
+    perm = rids[order.long()] if nr else rids                     # global row ids in (P, row id) order
 
     # a6: the slice plus the pair across its left boundary
     last = torch.zeros(npl + 1, dtype=torch.int32, device=dev)

@@ -108,6 +108,24 @@ class OracleOps:
             out.append(int(lt.sum()))
         return torch.tensor(out, dtype=torch.int64)
 
+    def partition(self, planes, bits, splitters, parts, rid_base):
+        p = _u32(planes).reshape(planes.shape)
+        npl, n = p.shape
+        q = _u32(splitters).reshape(splitters.shape)
+        rid = np.arange(n, dtype=np.int64) + rid_base
+        dest = np.zeros(n, np.int64)
+        for row in q:                                     # count the splitters <= element
+            gt = np.zeros(n, bool)
+            eq = np.ones(n, bool)
+            for w in range(npl - 1, -1, -1):
+                gt |= eq & (row[w] > p[w])
+                eq &= p[w] == row[w]
+            gt |= eq & (int(row[npl]) > rid)
+            dest += ~gt
+        order = np.argsort(dest, kind="stable")
+        return (_i32(p[:, order]), _i32(rid[order].astype(np.uint32)),
+                torch.tensor(np.bincount(dest, minlength=parts), dtype=torch.int64))
+
     def adjacent(self, sorted_planes, bits, sort_mask):
         dbit, mask = oracle.adjacent_compressed(_u32(sorted_planes).reshape(sorted_planes.shape), bits, sort_mask)
         return mask, torch.from_numpy(dbit.view(np.int16).copy())

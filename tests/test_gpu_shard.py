@@ -53,3 +53,32 @@ def test_sharded_duplicates_and_equal_keys():
 def test_sharded_fanout_fill():
     keys = cksgen.config(3, n=50_000)
     check_slices(keys, run(keys, [20_000, 30_000], fanout=14, fill=0.9), fanout=14, fill=0.9)
+
+
+@pytest.mark.parametrize("bits,parts", [(23, 3), (96, 4), (200, 2), (0, 3)])
+def test_partition_and_rank_vs_oracle_ops(bits, parts):
+    # the two splitter primitives against the numpy reference of tests/shard_oracle_ops.py
+    from shard_oracle_ops import OracleOps
+    from paper_2009_11543_b200 import cks
+    rng = np.random.default_rng(bits + parts)
+    n, npl = 30_011, cks.nplanes(bits)
+    P = rng.integers(0, 1 << 32, (npl, n), dtype=np.uint64).astype(np.uint32)
+    if npl:
+        P[npl - 1] &= np.uint32((1 << (bits - 32 * (npl - 1))) - 1) if bits % 32 else np.uint32(0xFFFFFFFF)
+        P[:, ::7] = P[:, :1]                                    # duplicates of the first key
+    spl_rows = np.sort(rng.choice(n, parts - 1, replace=False))
+    spl = np.concatenate([P[:, spl_rows].T, (spl_rows + 1000).astype(np.uint32)[:, None]], axis=1)
+    from paper_2009_11543_b200 import shard as sh
+    spl = sh.pick_splitters(spl, parts) if parts > 1 else spl   # (P, row id) order
+    Pt = torch.from_numpy(P.view(np.int32)).cuda()
+    q = torch.from_numpy(np.ascontiguousarray(spl).view(np.int32)).cuda()
+    ops = OracleOps(None)
+    got = cks.partition(Pt, bits, q, parts, 1000)
+    exp = ops.partition(torch.from_numpy(P.view(np.int32)), bits, torch.from_numpy(np.ascontiguousarray(spl).view(np.int32)),
+                        parts, 1000)
+    for g, e in zip(got, exp):
+        assert np.array_equal(g.cpu().numpy(), e.numpy())
+    perm, S = cks.sort(Pt, bits, None, want_sorted=True)
+    r = cks.rank_sorted(S, bits, perm, 1000, q)
+    re_ = ops.rank_sorted(S.cpu(), bits, perm.cpu(), 1000, q.cpu())
+    assert np.array_equal(r.cpu().numpy(), re_.numpy())
