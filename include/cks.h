@@ -183,6 +183,19 @@ int cks_rank_sorted(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t packed
 int cks_partition(cks_ctx* ctx, const uint32_t* packed, uint32_t packed_bits, uint64_t n, const uint32_t* splitters,
                   uint32_t parts, uint64_t rid_base, uint32_t* packed_out, uint32_t* rid_out, uint64_t* counts_out);
 
+/* cks_sort_prefix: the first build's sort (a4-a6, by distinguishing prefixes as cks_build,
+ * SURVEY 8(f) NEXT-1) on GIVEN compressed keys instead of key rows: packed = P_M, device
+ * u32[ceil(m/32)][n] right-aligned as cks_compress, input order; sort_mask = M (host
+ * u8[key_bytes], m = its popcount). Outputs: perm_out device u32[n] = input indices in
+ * (P, index) order; dbit_out device u16[n] (D_i, first = CKS_DBIT_NONE); mask_out host
+ * u8[key_bytes] = exact D of this sequence (a subset of M); popcount_out (may be NULL);
+ * packed_out device u32[ceil(|D|/32)][n] = P_D in sorted order, or NULL to skip it. Used
+ * after the sharded path's exchange (the received pairs are in row-id order, so the index
+ * order is the row-id order). Synchronises. */
+int cks_sort_prefix(cks_ctx* ctx, const uint32_t* packed, const uint8_t* sort_mask, uint32_t key_bytes, uint64_t n,
+                    uint32_t* perm_out, uint16_t* dbit_out, uint8_t* mask_out, uint32_t* popcount_out,
+                    uint32_t* packed_out);
+
 /* cks_repack: P_D from P_M for D a subset of M (a7): packed_in device
  * u32[ceil(|M|/32)][n], packed_out device u32[ceil(|D|/32)][n], both right-aligned as
  * cks_compress, same element order. in_mask = M, out_mask = D: host u8[key_bytes].

@@ -60,7 +60,7 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
            "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_paper_tree_shape", "cks_paper_tree",
            "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
-           "cks_partition"]
+           "cks_partition", "cks_sort_prefix"]
 
 
 def load_library(path: str | None = None):
@@ -103,6 +103,7 @@ def load_library(path: str | None = None):
     L.cks_rank_sorted.argtypes = [p, p, u32, u64, p, u64, p, u32, p]
     L.cks_repack.argtypes = [p, p, p, p, u32, u64, p]
     L.cks_partition.argtypes = [p, p, u32, u64, p, u32, u64, p, p, p]
+    L.cks_sort_prefix.argtypes = [p, p, p, u32, u64, p, p, p, ctypes.POINTER(u32), p]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or i32
     _lib = L
@@ -318,6 +319,32 @@ def partition(packed: torch.Tensor, bits: int, splitters: torch.Tensor, parts: i
                                  _ptr(splitters) if splitters.numel() else None, parts, rid_base,
                                  _ptr(out) if out.numel() else None, _ptr(rid) if n else None, _ptr(counts)))
     return out, rid, counts
+
+
+def sort_prefix(packed: torch.Tensor, sort_mask, want_packed: bool = False):
+    """(order int32[n], dbit int16[n], exact D [B], P_D int32[.., n] or None): the first build's
+    sort by distinguishing prefixes on given P_M planes int32[ceil(m/32), n] (cks_sort_prefix)."""
+    sm = np.ascontiguousarray(np.asarray(sort_mask, dtype=np.uint8))
+    B = sm.size
+    n = packed.shape[1]
+    if packed.dtype != torch.int32 or not packed.is_contiguous() or packed.shape[0] != nplanes(popcount(sm)):
+        raise ValueError("packed must be contiguous int32 [ceil(m/32), n]")
+    L, c = _context(packed.device.index)
+    order = torch.empty(n, dtype=torch.int32, device=packed.device)
+    dbit = torch.empty(n, dtype=torch.int16, device=packed.device)
+    mask = np.zeros(B, np.uint8)
+    pc = ctypes.c_uint32()
+    out = None
+    if want_packed:
+        out = torch.empty((0, n), dtype=torch.int32, device=packed.device)
+    # P_D's width is known only after the sort: size it for |M| planes, trim after
+    buf = torch.empty((packed.shape[0], n), dtype=torch.int32, device=packed.device) if want_packed else None
+    _check(L, c, L.cks_sort_prefix(c, _ptr(packed) if packed.numel() else None, sm.ctypes.data, B, n,
+                                   _ptr(order) if n else None, _ptr(dbit) if n else None, mask.ctypes.data,
+                                   ctypes.byref(pc), _ptr(buf) if buf is not None and buf.numel() else None))
+    if want_packed:
+        out = buf[:nplanes(int(pc.value))]
+    return order, dbit, mask, out
 
 
 def repack(packed: torch.Tensor, in_mask, out_mask) -> torch.Tensor:

@@ -57,6 +57,7 @@ struct cks_ctx {
     uint32_t* h_small = nullptr;      // 4 KiB: masks, dacc words
     uint32_t* h_tot = nullptr;        // refinement: (members, runs) of the next round
     int refine = -1;                  // first build by distinguishing prefixes (NEXT-1)
+    bool skip_packed = false;         // cks_sort_prefix without packed_out: no a7
 };
 
 namespace {
@@ -339,8 +340,9 @@ static void repack_words(const uint8_t* M, const uint8_t* D, uint32_t B, uint32_
 
 // NEXT-1: first build by distinguishing prefixes (k_refine.cu). Outputs perm, dbit, the
 // exact D (out->mask) and P_D in sorted order (out->packed).
+// keys == NULL: P_M is given instead (planes_in, right-aligned u32[np][n] as cks_compress).
 int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* M, uint32_t m,
-                 cks_build_out* out, uint16_t* dbit) {
+                 cks_build_out* out, uint16_t* dbit, const uint32_t* planes_in = nullptr) {
     const uint32_t np = (m + 31) / 32, lead = 32 * np - m;
     const uint64_t sp = scratch_pitch(n);
     const uint32_t nwords = (8 * B + 31) / 32;
@@ -354,23 +356,36 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     // exact for any T).
     // The sample is compressed and sorted on the side stream while the full compress runs.
     // CKS_ROUND0_BITS forces T.
-    TRY(claim_slot(ctx, 0));
-    plan_compress(M, B, ctx->h_plan[0]);
-    GatherPlan* dplan;
-    TRY(upload_plan(ctx, 0, &dplan));
+    GatherPlan* dplan = nullptr;
+    if (!planes_in) {
+        TRY(claim_slot(ctx, 0));
+        plan_compress(M, B, ctx->h_plan[0]);
+        TRY(upload_plan(ctx, 0, &dplan));
+    }
     static int forced = -2;
     if (forced == -2) { const char* e = getenv("CKS_ROUND0_BITS"); forced = e ? atoi(e) : 0; }
     const bool sample = !(forced > 0 && forced <= 64 && (forced & 7) == 0) && np >= 2 && n >= (1u << 16);
     TRY(ensure(ctx, ctx->rtot, 64));
     uint32_t* scnt = as<uint32_t>(ctx->rtot) + 4;
-    if (sample) {
-        CK(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
-        CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_ev[0], 0));
-        LAUNCH(launch_prefix_sample(keys, n, B, dplan, kSampleKeys, scnt, ctx->aux_stream));
-        CK(cudaMemcpyAsync(ctx->h_tot + 8, scnt, 32, cudaMemcpyDeviceToHost, ctx->aux_stream));
-        CK(cudaEventRecord(ctx->aux_ev[1], ctx->aux_stream));
+    if (planes_in) {                                             // given P_M: left-align it, then sample
+        LAUNCH(launch_align_left(planes_in, n, np, n, lead, pm, sp, ctx->sms, ctx->stream));
+        if (sample) {
+            CK(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_ev[0], 0));
+            LAUNCH(launch_prefix_sample(nullptr, n, B, nullptr, kSampleKeys, scnt, ctx->aux_stream, pm, np, sp));
+            CK(cudaMemcpyAsync(ctx->h_tot + 8, scnt, 32, cudaMemcpyDeviceToHost, ctx->aux_stream));
+            CK(cudaEventRecord(ctx->aux_ev[1], ctx->aux_stream));
+        }
+    } else {
+        if (sample) {
+            CK(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_ev[0], 0));
+            LAUNCH(launch_prefix_sample(keys, n, B, dplan, kSampleKeys, scnt, ctx->aux_stream));
+            CK(cudaMemcpyAsync(ctx->h_tot + 8, scnt, 32, cudaMemcpyDeviceToHost, ctx->aux_stream));
+            CK(cudaEventRecord(ctx->aux_ev[1], ctx->aux_stream));
+        }
+        LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, pm, sp, ctx->sms, ctx->stream, lead));
     }
-    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, pm, sp, ctx->sms, ctx->stream, lead));
     mark(ctx, ST_COMPRESS);
     uint32_t T = forced > 0 && forced <= 64 && (forced & 7) == 0 ? (uint32_t)forced : 64;
     if (sample) {
@@ -550,7 +565,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     const uint32_t npd = (out->popcount + 31) / 32;
     out->packed = nullptr;
     out->packed_pitch = sp;
-    if (out->popcount > 0) {
+    if (out->popcount > 0 && !ctx->skip_packed) {
         if (!carry) TRY(ensure(ctx, ctx->pd, (size_t)npd * sp * 4));
         uint32_t* pd = carry ? pm : as<uint32_t>(ctx->pd);       // (P_M in row order is no longer needed)
         const bool single = T >= m;                               // round 0 sorted all of P_M
@@ -566,8 +581,18 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             TRY(upload_plan(ctx, 1, &dplan));
             LAUNCH(launch_repack(sorted0, sp0, n, dplan, ctx->h_plan[1]->nsteps, npd, pd, sp, ctx->sms, ctx->stream));
             out->packed = pd;
-        } else {
+        } else if (keys) {
             TRY(run_compress(ctx, keys, n, B, out->mask, pd, sp, 0, out->perm));
+            out->packed = pd;
+        } else {                                                  // given P_M (row order): gather + repack
+            std::vector<uint32_t> sub(np, 0);
+            repack_words(M, out->mask, B, m, lead, sub);
+            TRY(claim_slot(ctx, 1));
+            plan_repack(sub.data(), np, ctx->h_plan[1]);
+            GatherPlan* dplan;
+            TRY(upload_plan(ctx, 1, &dplan));
+            LAUNCH(launch_repack(pm, sp, n, dplan, ctx->h_plan[1]->nsteps, npd, pd, sp, ctx->sms, ctx->stream,
+                                 out->perm));
             out->packed = pd;
         }
     }
@@ -644,8 +669,9 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
 }
 
 // Everything after the sort mask is known: a3 .. a8 on device keys.
+// keys == NULL: P_M is given (planes_in, right-aligned u32[np][n]) -- cks_sort_prefix.
 int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* M,
-                    uint32_t m, cks_build_out* out, bool check_superset) {
+                    uint32_t m, cks_build_out* out, bool check_superset, const uint32_t* planes_in = nullptr) {
     const uint32_t np = (m + 31) / 32, k = (m + 7) / 8;
     out->sort_bits = m;
     out->passes = k;
@@ -664,7 +690,7 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     // 1 = auto: by prefixes whenever P_M is wider than one 64-bit chunk (m > 64); for m <= 64
     // round 0 would be the whole sort anyway
     if (n && m && (ctx->refine == 2 || (ctx->refine == 1 && m > 64))) {
-        TRY(build_refine(ctx, keys, n, B, M, m, out, dbit));
+        TRY(build_refine(ctx, keys, n, B, M, m, out, dbit, planes_in));
         out->height = 0;
         if (out->tree.node_cnt) {
             cks_tree tr = out->tree;
@@ -681,12 +707,18 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     uint32_t* cbuf = k ? (first_pass_out(ctx, k) == as<uint32_t>(ctx->planeA) ? as<uint32_t>(ctx->planeB)
                                                                               : as<uint32_t>(ctx->planeA))
                        : as<uint32_t>(ctx->planeB);
-    TRY(run_compress(ctx, keys, n, B, M, cbuf, sp));
+    uint64_t cpitch = sp;
+    if (planes_in) {                                              // given P_M: sort it in place of a compress
+        cbuf = const_cast<uint32_t*>(planes_in);                  // (read only: the first pass writes elsewhere)
+        cpitch = n;
+    } else {
+        TRY(run_compress(ctx, keys, n, B, M, cbuf, sp));
+    }
     mark(ctx, ST_COMPRESS);
     // a4 + a5
     const uint32_t* sorted = nullptr;
     uint64_t spitch = sp;
-    TRY(run_sort(ctx, cbuf, sp, np, k, n, nullptr, 0, nullptr, 0, out->perm, &sorted, &spitch));
+    TRY(run_sort(ctx, cbuf, cpitch, np, k, n, nullptr, 0, nullptr, 0, out->perm, &sorted, &spitch));
     mark(ctx, ST_SORT);
     // a6
     TRY(run_adjacent(ctx, sorted, spitch, m, n, M, B, out->mask, dbit));
@@ -699,7 +731,7 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     // a7: repack P_M -> P_D
     out->packed = sorted;
     out->packed_pitch = spitch;
-    if (!same_mask(out->mask, M, B) && out->popcount > 0) {
+    if (!same_mask(out->mask, M, B) && out->popcount > 0 && !ctx->skip_packed) {
         std::vector<uint32_t> sub(np, 0);
         repack_words(M, out->mask, B, m, 0, sub);
         TRY(claim_slot(ctx, 1));
@@ -965,6 +997,43 @@ int cks_partition(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t 
     TRY(run_sort(ctx, in, sp, np + 1, 1, n, nullptr, 0, out, sp, rid_out, nullptr, nullptr, 0, false));
     if (np) CK(cudaMemcpy2DAsync(packed_out, n * 4, out + sp, sp * 4, n * 4, np, cudaMemcpyDeviceToDevice, ctx->stream));
     LAUNCH(launch_add_base(rid_out, n, (uint32_t)rid_base, ctx->sms, ctx->stream));
+    return CKS_OK;
+}
+
+int cks_sort_prefix(cks_ctx* ctx, const uint32_t* packed, const uint8_t* sort_mask, uint32_t B, uint64_t n,
+                    uint32_t* perm_out, uint16_t* dbit_out, uint8_t* mask_out, uint32_t* popcount_out,
+                    uint32_t* packed_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (B < 1 || B > CKS_MAX_KEY_BYTES) return fail(ctx, CKS_EINVAL, "key_bytes %u not in [1,512]", B);
+    if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
+    if (!sort_mask || !mask_out) return fail(ctx, CKS_EINVAL, "mask pointer is NULL");
+    const uint32_t m = popcount_mask(sort_mask, B);
+    if (n && (!perm_out || !dbit_out || (m && !packed))) return fail(ctx, CKS_EINVAL, "NULL buffer with n > 0");
+    CK(cudaSetDevice(ctx->device));
+    ctx->timed = ctx->timing;
+    ctx->nkev = 0;
+    mark(ctx, ST_BEGIN);
+    cks_build_out o;
+    memset(&o, 0, sizeof(o));
+    o.mask = mask_out;
+    o.perm = perm_out;
+    o.dbit = dbit_out;
+    o.fanout = 64;
+    o.fill = 1.f;
+    if (n == 0) {
+        memset(mask_out, 0, B);
+        if (popcount_out) *popcount_out = 0;
+        return CKS_OK;
+    }
+    ctx->skip_packed = packed_out == nullptr;
+    const int rc = build_from_mask(ctx, nullptr, n, B, sort_mask, m, &o, false, packed);
+    ctx->skip_packed = false;
+    TRY(rc);
+    if (popcount_out) *popcount_out = o.popcount;
+    if (packed_out && o.popcount && o.packed)
+        CK(cudaMemcpy2DAsync(packed_out, n * 4, o.packed, o.packed_pitch * 4, n * 4, (o.popcount + 31) / 32,
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return CKS_OK;
 }
 

@@ -52,7 +52,8 @@ cudaError_t launch_occ_finalize(const uint32_t* occ, uint32_t B, uint64_t n, uin
 // of two, <= 16384) with the compress plan, sorts their top-64-bit prefixes of P_M in one CTA
 // and writes counts[w] = distinct prefixes of the top 8(w+1) bits, w = 0..7.
 cudaError_t launch_prefix_sample(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* plan, uint32_t samples,
-                                 uint32_t* counts, cudaStream_t st);
+                                 uint32_t* counts, cudaStream_t st, const uint32_t* pm = nullptr,
+                                 uint32_t np = 0, uint64_t pitch = 0);
 // Planes are u32 SoA arrays: plane q of a packed array starts at ptr + q*pitch (pitch in
 // elements; user buffers have pitch n, library scratch pads the pitch to 32 elements so every
 // plane is 128-byte aligned for TMA).
@@ -63,7 +64,7 @@ cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const G
                             int sms, cudaStream_t st, uint32_t lead = 0, const uint32_t* rows = nullptr);
 cudaError_t launch_repack(const uint32_t* in_planes, uint64_t in_pitch, uint64_t n, const GatherPlan* dplan,
                           uint32_t nsteps, uint32_t out_planes, uint32_t* out, uint64_t out_pitch, int sms,
-                          cudaStream_t st);
+                          cudaStream_t st, const uint32_t* rows = nullptr);
 // Reduce-then-scan LSD pass (k_lsd.cu): upsweep -> chunk scan -> persistent downsweep.
 struct LsdPassArgs {
     const uint32_t* in_planes;
@@ -107,6 +108,8 @@ uint64_t ref_tiles(uint64_t nr);
 cudaError_t launch_part_dest(const uint32_t* planes, uint32_t np, uint64_t n, uint64_t pitch, const uint32_t* spl,
                              uint32_t nspl, uint64_t rid_base, uint32_t* dest, unsigned long long* counts, int sms,
                              cudaStream_t st);
+cudaError_t launch_align_left(const uint32_t* in, uint64_t in_pitch, uint32_t np, uint64_t n, uint32_t lead,
+                              uint32_t* out, uint64_t out_pitch, int sms, cudaStream_t st);
 cudaError_t launch_add_base(uint32_t* a, uint64_t n, uint32_t base, int sms, cudaStream_t st);
 cudaError_t launch_occ_union(const uint32_t* occ, uint32_t nocc, uint32_t words, uint32_t* out, cudaStream_t st);
 cudaError_t launch_rank_sorted(const uint32_t* planes, uint32_t np, uint64_t n, const uint32_t* rid, uint64_t rid_base,

@@ -130,7 +130,7 @@ k_compress_generic(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B,
 // gathered by the sub-mask of P_M bits that are exact-D positions.
 __global__ void __launch_bounds__(kCompressThreads)
 k_repack(const uint32_t* __restrict__ in, uint64_t in_pitch, uint64_t n, const GatherPlan* __restrict__ plan,
-         uint32_t nsteps, uint32_t np, uint32_t* __restrict__ out, uint64_t out_pitch) {
+         uint32_t nsteps, uint32_t np, uint32_t* __restrict__ out, uint64_t out_pitch, const uint32_t* __restrict__ rows) {
     __shared__ GatherStep s_step[kMaxPlanes];
     for (uint32_t s = threadIdx.x; s < nsteps; s += blockDim.x) s_step[s] = plan->step[s];
     __syncthreads();
@@ -140,7 +140,7 @@ k_repack(const uint32_t* __restrict__ in, uint64_t in_pitch, uint64_t n, const G
         uint32_t accbits = 0, q = 0;
         for (uint32_t s = 0; s < nsteps; s++) {
             const GatherStep& g = s_step[s];
-            uint32_t x = gather_word(in[(uint64_t)g.src * in_pitch + i], g);
+            uint32_t x = gather_word(in[(uint64_t)g.src * in_pitch + (rows ? (uint64_t)rows[i] : i)], g);
             acc |= (unsigned long long)x << accbits;
             accbits += g.cnt;
             if (accbits >= 32) {
@@ -296,10 +296,10 @@ cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const G
 
 cudaError_t launch_repack(const uint32_t* in, uint64_t in_pitch, uint64_t n, const GatherPlan* dplan,
                           uint32_t nsteps, uint32_t np, uint32_t* out, uint64_t out_pitch, int sms,
-                          cudaStream_t st) {
+                          cudaStream_t st, const uint32_t* rows) {
     if (n == 0 || np == 0) return cudaSuccess;
     k_repack<<<grid_for(n, 8, sms), kCompressThreads, 0, st>>>(in, in_pitch, n, dplan, nsteps, np, out,
-                                                               out_pitch);
+                                                               out_pitch, rows);
     return cudaGetLastError();
 }
 

@@ -1112,12 +1112,18 @@ namespace cks {
 // side stream while the full compress runs.
 __global__ void __launch_bounds__(1024)
 k_prefix_sample(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const GatherPlan* __restrict__ plan,
-                uint32_t S, uint32_t* __restrict__ counts) {
+                uint32_t S, uint32_t* __restrict__ counts, const uint32_t* __restrict__ pm, uint32_t np, uint64_t pitch) {
     extern __shared__ unsigned long long s_v[];                     // [S]
     __shared__ uint32_t s_cnt[8];
     if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
-    const uint32_t nsteps = plan->nsteps;
+    const uint32_t nsteps = pm ? 0u : plan->nsteps;
     for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) {
+        if (pm) {                                                     // left-aligned P_M given
+            const uint64_t r = (uint64_t)i * n / S;
+            s_v[i] = ((unsigned long long)pm[(uint64_t)(np - 1) * pitch + r] << 32) |
+                     (np >= 2 ? pm[(uint64_t)(np - 2) * pitch + r] : 0u);
+            continue;
+        }
         const uint8_t* k = keys + ((uint64_t)i * n / S) * B;
         unsigned long long top = 0;
         uint32_t got = 0;
@@ -1169,10 +1175,10 @@ k_prefix_sample(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const 
 }
 
 cudaError_t launch_prefix_sample(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* plan, uint32_t samples,
-                                 uint32_t* counts, cudaStream_t st) {
+                                 uint32_t* counts, cudaStream_t st, const uint32_t* pm, uint32_t np, uint64_t pitch) {
     const size_t smem = (size_t)samples * 8;
     raise_smem_limit((const void*)k_prefix_sample, smem);
-    k_prefix_sample<<<1, 1024, smem, st>>>(keys, n, B, plan, samples, counts);
+    k_prefix_sample<<<1, 1024, smem, st>>>(keys, n, B, plan, samples, counts, pm, np, pitch);
     return cudaGetLastError();
 }
 

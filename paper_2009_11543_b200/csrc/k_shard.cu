@@ -77,6 +77,20 @@ k_part_dest(const uint32_t* __restrict__ planes, uint32_t np, uint64_t n, uint64
         if (s_cnt[i]) atomicAdd(&counts[i], (unsigned long long)s_cnt[i]);
 }
 
+// right-aligned planes (cks_compress layout) -> left-aligned by `lead` bits (the refinement's
+// P_M layout): out[q] = in[q] << lead | in[q-1] >> (32 - lead)
+__global__ void k_align_left(const uint32_t* __restrict__ in, uint64_t in_pitch, uint32_t np, uint64_t n,
+                             uint32_t lead, uint32_t* __restrict__ out, uint64_t out_pitch) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lower = 0;
+        for (uint32_t q = 0; q < np; q++) {
+            const uint32_t v = in[(uint64_t)q * in_pitch + i];
+            out[(uint64_t)q * out_pitch + i] = lead ? (v << lead) | (lower >> (32 - lead)) : v;
+            lower = v;
+        }
+    }
+}
+
 __global__ void k_add_base(uint32_t* __restrict__ a, uint64_t n, uint32_t base) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         a[i] += base;
@@ -91,6 +105,15 @@ cudaError_t launch_part_dest(const uint32_t* planes, uint32_t np, uint64_t n, ui
     uint64_t g = (n + 255) / 256;
     if (g > (uint64_t)sms * 8) g = (uint64_t)sms * 8;
     k_part_dest<<<(unsigned)g, 256, smem, st>>>(planes, np, n, pitch, spl, nspl, rid_base, dest, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_align_left(const uint32_t* in, uint64_t in_pitch, uint32_t np, uint64_t n, uint32_t lead,
+                              uint32_t* out, uint64_t out_pitch, int sms, cudaStream_t st) {
+    if (n == 0 || np == 0) return cudaSuccess;
+    uint64_t g = (n + 255) / 256;
+    if (g > (uint64_t)sms * 8) g = (uint64_t)sms * 8;
+    k_align_left<<<(unsigned)g, 256, 0, st>>>(in, in_pitch, np, n, lead, out, out_pitch);
     return cudaGetLastError();
 }
 

@@ -148,6 +148,7 @@ class CudaOps:
     compress = staticmethod(cks.compress)
     partition = staticmethod(cks.partition)
     repack = staticmethod(cks.repack)
+    sort_prefix = staticmethod(cks.sort_prefix)
 
     @staticmethod
     def sort(planes, bits, row_ids=None):
@@ -232,38 +233,46 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
     # a5: stable partition, the one exchange, one stable sort on P
     Pp, ridp, pc = ops.partition(P, m, q, G, off)
     send_counts = [int(v) for v in pc.cpu().tolist()]
-    rowsP = torch.cat([Pp.t(), ridp.view(-1, 1)], dim=1)
-    recv = comm.alltoallv(rowsP, send_counts)
-    R = recv[:, :npl].t().contiguous()
-    rids = recv[:, npl].contiguous()
-    nr = int(recv.shape[0])
-    order, S2 = ops.sort(R, m, None)                              # stable: received order = row-id order
-    perm = rids[order.long()] if nr else rids                     # global row ids in (P, row id) order
+    rids = comm.alltoallv(ridp, send_counts)                     # per plane: no transposes
+    R = torch.stack([comm.alltoallv(Pp[q], send_counts) for q in range(npl)]) if npl else \
+        torch.zeros((0, rids.shape[0]), dtype=torch.int32, device=dev)
+    nr = int(rids.shape[0])
+    # sort by distinguishing prefixes (stable: the received order is the row-id order), D_i
+    order, dbit, Dl, PDl = ops.sort_prefix(R, M, want_packed=True)
+    ol = order.long()
+    perm = rids[ol] if nr else rids                               # global row ids in (P, row id) order
 
-    # a6: the slice plus the pair across its left boundary
+    # a6 across the slice boundary: the previous non-empty slice's last key vs this first key
     last = torch.zeros(npl + 1, dtype=torch.int32, device=dev)
     if nr:
         last[0] = 1
-        last[1:] = S2[:, nr - 1]
+        last[1:] = R[:, ol[nr - 1]]
     lasts = comm.allgather(last)
     prev = next((lasts[k][1:] for k in range(r - 1, -1, -1) if int(lasts[k][0].item())), None)
+    Dl0, Db = Dl, None
     if prev is not None and nr:
-        Dl, dbit = ops.adjacent(torch.cat([prev.view(-1, 1), S2], dim=1).contiguous(), m, M)
-        dbit = dbit[1:]
-    else:
-        Dl, dbit = ops.adjacent(S2, m, M)
+        pair = torch.stack([prev, R[:, ol[0]]], dim=1).contiguous()
+        Db, db = ops.adjacent(pair, m, M)
+        dbit[0] = db[1]
+        Dl = Dl | Db
     D = np.bitwise_or.reduce(np.stack([t.cpu().numpy() for t in comm.allgather(
         torch.from_numpy(np.ascontiguousarray(Dl)).to(dev))]), axis=0).astype(np.uint8)
 
-    # a7: P_D of the slice
-    packed = ops.repack(S2, M, D) if not np.array_equal(D, M) else S2
+    # a7: P_D of the slice for the global D (the sort's own P_D when no other slice added bits)
+    if PDl is not None and np.array_equal(D, Dl0):
+        packed = PDl
+    else:
+        S2 = R[:, ol].contiguous() if nr else R
+        packed = ops.repack(S2, M, D) if not np.array_equal(D, M) else S2
 
     nrs = [int(t.item()) for t in comm.allgather(torch.tensor([nr], dtype=torch.int64, device=dev))]
     out = dict(mask=D, popcount=cks.popcount(D), sort_mask=M, sort_bits=m, perm=perm, dbit=dbit, packed=packed,
                offset=sum(nrs[:r]), n_total=N, send_counts=send_counts, tree=None)
 
     # a8: rank 0 bulk-loads the gathered order
-    if tree and N:
+    if tree and N and G == 1:
+        out["tree"] = ops.bulkload(perm, dbit, fanout, fill)
+    elif tree and N:
         mx = max(nrs)
         pad = torch.zeros((mx, 2), dtype=torch.int32, device=dev)
         if nr:

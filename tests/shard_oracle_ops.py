@@ -108,6 +108,13 @@ class OracleOps:
             out.append(int(lt.sum()))
         return torch.tensor(out, dtype=torch.int64)
 
+    def sort_prefix(self, planes, sort_mask, want_packed=False):
+        p = _u32(planes).reshape(planes.shape)
+        m = oracle.popcount(sort_mask)
+        order = oracle.sort_packed(p)                          # (P, index) order
+        dbit, mask = oracle.adjacent_compressed(p[:, order.astype(np.int64)], m, sort_mask)
+        return _i32(order), torch.from_numpy(dbit.view(np.int16).copy()), mask, None
+
     def partition(self, planes, bits, splitters, parts, rid_base):
         p = _u32(planes).reshape(planes.shape)
         npl, n = p.shape

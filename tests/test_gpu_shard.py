@@ -82,3 +82,22 @@ def test_partition_and_rank_vs_oracle_ops(bits, parts):
     r = cks.rank_sorted(S, bits, perm, 1000, q)
     re_ = ops.rank_sorted(S.cpu(), bits, perm.cpu(), 1000, q.cpu())
     assert np.array_equal(r.cpu().numpy(), re_.numpy())
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_sort_prefix_on_given_planes(cfg):
+    # cks_sort_prefix: the first build's sort from P_{D+} instead of key rows
+    import oracle
+    from paper_2009_11543_b200 import cks
+    keys = cksgen.config(cfg, n=150_001)
+    kd = torch.from_numpy(keys).cuda()
+    M = cks.superset_mask(kd)
+    P = cks.compress(kd, M)
+    order, dbit, D, PD = cks.sort_prefix(P, M, want_packed=True)
+    ref = oracle.first_build(keys)
+    assert np.array_equal(order.cpu().numpy().view(np.uint32), ref["perm"])
+    assert np.array_equal(dbit.cpu().numpy().view(np.uint16), ref["dbit"])
+    assert np.array_equal(D, ref["mask"])
+    assert np.array_equal(PD.cpu().numpy().view(np.uint32), ref["planes"][:, ref["perm"]])
+    o2, d2, D2, none = cks.sort_prefix(P, M)                  # without P_D
+    assert none is None and np.array_equal(o2.cpu().numpy(), order.cpu().numpy()) and np.array_equal(D2, D)
