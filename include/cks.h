@@ -270,6 +270,34 @@ int cks_paper_tree_shape(uint64_t n, float fill, cks_tree_shape* out);
 int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, const uint32_t* perm,
                    const uint16_t* dbit, uint32_t pk_bits, float fill, uint8_t* nodes);
 
+/* ---- P:502 block-parallel bulk load (the sharded path's a8, NEXT-4) ----------------------
+ * "n sort keys are divided into p blocks ... thread i constructs a subtree consisting of all
+ * sort keys in the i-th block. ... we remove the root nodes of the subtrees, and build the
+ * top layers of the whole tree by linking the children of the root nodes".
+ *
+ * cks_bulkload_block: levels 0 .. levels-1 (levels = 0: all) of the subtree over one block:
+ * perm / dbit = the block's slice of the global sorted order (D_i against the GLOBAL
+ * predecessor). Layout and entries as cks_bulkload over the block's own shape, except that
+ * with first_global = 0 (a block after the first) the first entry of every inner level takes
+ * its child's minimum D_k like every other entry (its predecessor lives in the previous
+ * block). top_min_out: device u16[nodes of the top built level] = minimum D_k under each of
+ * those nodes (input of the merge), or NULL. height_out: levels built. Asynchronous. */
+int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
+                       float fill, int first_global, uint32_t levels, cks_tree* out, uint16_t* top_min_out,
+                       uint32_t* height_out);
+
+/* cks_bulkload_top: the merged top over nchild child nodes = the blocks' top built levels
+ * concatenated in block order (child_rid: device u32[nchild], row id of each child's highest
+ * key; child_min: device u16[nchild], minimum D_k under each child). The first level above
+ * them has ceil(nchild/per) nodes whose entries are the children (entry_child = index into
+ * the child list; entry D-bit = child_min, CKS_DBIT_NONE for the first child), then upward
+ * to one root as cks_bulkload. Node ids start at 0 on that first level; arrays sized for
+ * cks_bulkload_shape(nchild, fanout, fill).total_nodes nodes (entry_child for all of them);
+ * nchild <= 1 builds nothing (the one child is the root). height_out: levels built.
+ * Asynchronous. */
+int cks_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* child_min, uint64_t nchild,
+                     uint32_t fanout, float fill, cks_tree* out, uint32_t* height_out);
+
 /* ---- fused first build: a1 -> a2 -> a3 -> a4 -> a5 -> a6 -> a7 -> a8 -----------------------
  * The benchmarked step. The superset mask M (or prior_mask) is compressed once; the sort
  * runs by distinguishing prefixes ("sort by distinguishing prefixes",

@@ -57,6 +57,8 @@ def _load():
         L.orc_adjacent_compressed.argtypes = [p, u32, u64, p, u32, p, p]
         L.orc_bulkload.argtypes = [p, p, u64, u32, u32, p, u32, p, p, p, p, p]
         L.orc_bulkload.restype = u32
+        L.orc_bulkload_blocks.argtypes = [p, p, u64, p, u32, u32, u32, p, u32, p, p, p, p, p]
+        L.orc_bulkload_blocks.restype = u32
         L.orc_paper_tree.argtypes = [p, u64, u32, p, p, u32, u32, u32, p]
         L.orc_paper_tree.restype = u32
         _lib = L
@@ -213,6 +215,29 @@ def bulkload(perm, dbit, keys, fanout: int, fill: float = 1.0):
     assert h == len(lv)
     return dict(height=h, level_nodes=level_nodes[:h].copy(), node_cnt=node_cnt,
                 entry_rid=rid, entry_child=child, entry_dbit=edb, per=per)
+
+
+def bulkload_blocks(perm, dbit, keys, block_n, fanout: int, fill: float = 1.0):
+    """P:502 block-parallel construction (orc_bulkload_blocks): dict as bulkload()."""
+    k = _keys(keys)
+    n, B = k.shape
+    per = int(np.floor(fanout * fill))
+    bn = np.ascontiguousarray(np.asarray(block_n, dtype=np.uint64))
+    assert int(bn.sum()) == n
+    # node count bound: every block's levels + the top (at most n leaves + n inner overall)
+    cap = max(1, 2 * n + 2 * len(bn) + 8)
+    level_nodes = np.zeros(64, np.uint64)
+    node_cnt = np.zeros(cap, np.uint32)
+    rid = np.zeros((cap, fanout), np.uint32)
+    child = np.zeros((cap, fanout), np.uint32)
+    edb = np.zeros((cap, fanout), np.uint16)
+    perm = np.ascontiguousarray(perm, dtype=np.uint32)
+    db = None if dbit is None else np.ascontiguousarray(dbit, dtype=np.uint16)
+    h = _load().orc_bulkload_blocks(_ptr(perm), _ptr(db), n, bn.ctypes.data, bn.size, fanout, per, _ptr(k), B,
+                                    level_nodes.ctypes.data, _ptr(node_cnt), _ptr(rid), _ptr(child), _ptr(edb))
+    total = int(level_nodes[:h].sum())
+    return dict(height=h, level_nodes=level_nodes[:h].copy(), node_cnt=node_cnt[:total],
+                entry_rid=rid[:total], entry_child=child[:total], entry_dbit=edb[:total], per=per)
 
 
 def paper_tree_levels(n: int, leaf_per: int, inner_per: int) -> list[int]:

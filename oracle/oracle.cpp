@@ -308,6 +308,122 @@ void orc_adjacent_compressed(const uint32_t* sorted_planes, uint32_t m, uint64_t
  *                         at this level, highest key of c) computed DIRECTLY on
  *                         the full keys; 0xFFFF for c = 0 / equal.
  * Empty slots: rid/child 0xFFFFFFFF, dbit 0xFFFF. Returns the height (levels). */
+/* Block-parallel index construction (Sec. 5.3): "n sort keys are divided into p
+ * blocks ... Thread i constructs a subtree consisting of all sort keys in the i-th block.
+ * When all the subtrees are constructed, they are merged into one tree ... we remove the root
+ * nodes of the subtrees, and build the top layers of the whole tree by linking the children
+ * of the root nodes of the subtrees."
+ * blocks: consecutive ranges of the sorted order of sizes block_n[0..nblocks) (empty blocks
+ * contribute nothing). Each block's subtree is the bottom-up bulk load of its keys (per
+ * entries a node). The root's children are at level h-2 of a subtree of height h; blocks of
+ * unequal heights (not in the paper, whose blocks are equal) keep their levels up to
+ * l* = max(0, min_b h_b - 2), so every leaf stays at the same depth (reading R17). Level
+ * l <= l* of the whole tree = the blocks' level-l nodes in block order; above l*, nodes of
+ * per consecutive nodes up to one root. Entries as orc_bulkload: a leaf entry is a key
+ * (row id, D_i); an inner entry is a child node (row id of its highest key, global child
+ * node id, D-bit of its highest key against the highest key of the previous node of that
+ * level -- across block borders -- computed from the keys; none for a level's first).
+ * Output layout as orc_bulkload (levels concatenated, leaves first). Returns the height. */
+uint32_t orc_bulkload_blocks(const uint32_t* perm, const uint16_t* dbit, uint64_t n, const uint64_t* block_n,
+                             uint32_t nblocks, uint32_t fanout, uint32_t per, const uint8_t* keys, uint32_t B,
+                             uint64_t* level_nodes_out, uint32_t* node_cnt, uint32_t* entry_rid,
+                             uint32_t* entry_child, uint16_t* entry_dbit) {
+    struct Node { uint64_t lo, hi; std::vector<uint64_t> ent; };  /* key range; entries (keys or child ids in level) */
+    std::vector<std::vector<std::vector<Node>>> sub;             /* [block][level][node] */
+    uint64_t start = 0;
+    for (uint32_t b = 0; b < nblocks; b++) {
+        const uint64_t nb = block_n[b];
+        if (nb == 0) continue;
+        std::vector<std::vector<Node>> lv(1);
+        for (uint64_t x = start; x < start + nb; x += per) {    /* leaves of per keys */
+            Node nd;
+            nd.lo = x;
+            nd.hi = std::min(x + per, start + nb) - 1;
+            for (uint64_t k = nd.lo; k <= nd.hi; k++) nd.ent.push_back(k);
+            lv[0].push_back(nd);
+        }
+        while (lv.back().size() > 1) {                          /* up to the subtree's root */
+            const std::vector<Node>& below = lv.back();
+            std::vector<Node> up;
+            for (uint64_t j = 0; j < below.size(); j += per) {
+                Node nd;
+                const uint64_t j1 = std::min<uint64_t>(j + per, below.size());
+                nd.lo = below[j].lo;
+                nd.hi = below[j1 - 1].hi;
+                for (uint64_t c = j; c < j1; c++) nd.ent.push_back(c);
+                up.push_back(nd);
+            }
+            lv.push_back(up);
+        }
+        sub.push_back(lv);
+        start += nb;
+    }
+    if (sub.empty()) return 0;
+    size_t hmin = sub[0].size();
+    for (auto& t : sub) hmin = std::min(hmin, t.size());
+    const size_t lstar = hmin >= 2 ? hmin - 2 : 0;               /* the roots' children (equal heights) */
+    /* the whole tree's levels 0..lstar: the blocks' levels concatenated; child ids rebased */
+    std::vector<std::vector<Node>> all(lstar + 1);
+    for (size_t l = 0; l <= lstar; l++) {
+        uint64_t rebase = 0;                                     /* nodes of level l-1 in earlier blocks */
+        for (size_t b = 0; b < sub.size(); b++) {
+            for (const Node& nd : sub[b][l]) {
+                Node c = nd;
+                if (l > 0)
+                    for (auto& e : c.ent) e += rebase;
+                all[l].push_back(c);
+            }
+            if (l > 0) rebase += sub[b][l - 1].size();
+        }
+    }
+    while (all.back().size() > 1) {                             /* the top layers */
+        const std::vector<Node>& below = all.back();
+        std::vector<Node> up;
+        for (uint64_t j = 0; j < below.size(); j += per) {
+            Node nd;
+            const uint64_t j1 = std::min<uint64_t>(j + per, below.size());
+            nd.lo = below[j].lo;
+            nd.hi = below[j1 - 1].hi;
+            for (uint64_t c = j; c < j1; c++) nd.ent.push_back(c);
+            up.push_back(nd);
+        }
+        all.push_back(up);
+    }
+    uint64_t off = 0;
+    for (size_t l = 0; l < all.size(); l++) {
+        level_nodes_out[l] = all[l].size();
+        const uint64_t below_off = l ? off - all[l - 1].size() : 0;
+        for (uint64_t j = 0; j < all[l].size(); j++) {
+            const Node& nd = all[l][j];
+            const uint64_t node = off + j;
+            node_cnt[node] = (uint32_t)nd.ent.size();
+            for (uint32_t e = 0; e < fanout; e++) {
+                const uint64_t slot = node * fanout + e;
+                entry_rid[slot] = 0xFFFFFFFFu;
+                entry_child[slot] = 0xFFFFFFFFu;
+                entry_dbit[slot] = ORC_NONE;
+                if (e >= nd.ent.size()) continue;
+                const uint64_t x = nd.ent[e];
+                if (l == 0) {
+                    entry_rid[slot] = perm[x];
+                    entry_dbit[slot] = dbit ? dbit[x] : (uint16_t)ORC_NONE;
+                } else {
+                    const Node& c = all[l - 1][x];
+                    entry_rid[slot] = perm[c.hi];
+                    entry_child[slot] = (uint32_t)(below_off + x);
+                    if (x > 0) {
+                        const Node& pv = all[l - 1][x - 1];
+                        int d = orc_dbit_pair(keys + (uint64_t)perm[pv.hi] * B, keys + (uint64_t)perm[c.hi] * B, B);
+                        entry_dbit[slot] = d < 0 ? (uint16_t)ORC_NONE : (uint16_t)d;
+                    }
+                }
+            }
+        }
+        off += all[l].size();
+    }
+    return (uint32_t)all.size();
+}
+
 uint32_t orc_bulkload(const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
                       uint32_t per, const uint8_t* keys, uint32_t B,
                       uint64_t* level_nodes_out, uint32_t* node_cnt, uint32_t* entry_rid,

@@ -60,7 +60,7 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
            "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_paper_tree_shape", "cks_paper_tree",
            "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
-           "cks_partition", "cks_sort_prefix"]
+           "cks_partition", "cks_sort_prefix", "cks_bulkload_block", "cks_bulkload_top"]
 
 
 def load_library(path: str | None = None):
@@ -104,6 +104,8 @@ def load_library(path: str | None = None):
     L.cks_repack.argtypes = [p, p, p, p, u32, u64, p]
     L.cks_partition.argtypes = [p, p, u32, u64, p, u32, u64, p, p, p]
     L.cks_sort_prefix.argtypes = [p, p, p, u32, u64, p, p, p, ctypes.POINTER(u32), p]
+    L.cks_bulkload_block.argtypes = [p, p, p, u64, u32, f32, i32, u32, ctypes.POINTER(Tree), p, ctypes.POINTER(u32)]
+    L.cks_bulkload_top.argtypes = [p, p, p, u64, u32, f32, ctypes.POINTER(Tree), ctypes.POINTER(u32)]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or i32
     _lib = L
@@ -392,6 +394,45 @@ def bulkload(perm: torch.Tensor, dbit: torch.Tensor | None, fanout: int = 64, fi
     tr = _tree_struct(t)
     _check(L, c, L.cks_bulkload(c, _ptr(perm), _ptr(dbit), n, fanout, fill, ctypes.byref(tr)))
     t["shape"] = shape
+    return t
+
+
+def bulkload_block(perm: torch.Tensor, dbit: torch.Tensor, fanout: int, fill: float, first_global: bool,
+                   levels: int = 0) -> dict:
+    """P:502 subtree over one block (cks_bulkload_block): tree dict of the block's levels
+    0..levels-1 plus "top_min" (minimum D_k under each node of the top built level) and
+    "height" (levels built)."""
+    n = perm.numel()
+    L, c = _context(perm.device.index)
+    shape = bulkload_shape(n, fanout, fill)
+    t = alloc_tree(shape, perm.device, with_dbit=True, with_child=True)
+    tr = _tree_struct(t)
+    H = min(levels, int(shape.height)) if levels else int(shape.height)
+    top_min = torch.empty(max(1, int(shape.level_nodes[H - 1]) if H else 1), dtype=torch.int16, device=perm.device)
+    h = ctypes.c_uint32()
+    _check(L, c, L.cks_bulkload_block(c, _ptr(perm) if n else None, _ptr(dbit) if n else None, n, fanout, fill,
+                                      1 if first_global else 0, levels, ctypes.byref(tr),
+                                      _ptr(top_min) if n else None, ctypes.byref(h)))
+    t["shape"], t["height"], t["top_min"] = shape, int(h.value), top_min
+    return t
+
+
+def bulkload_top(child_rid: torch.Tensor, child_min: torch.Tensor, fanout: int, fill: float) -> dict:
+    """P:502 merged top over the blocks' top nodes (cks_bulkload_top)."""
+    nc = child_rid.numel()
+    L, c = _context(child_rid.device.index)
+    shape = bulkload_shape(nc, fanout, fill)
+    T = int(shape.total_nodes) if nc > 1 else 0
+    f = fanout
+    t = dict(node_cnt=torch.empty(max(T, 1), dtype=torch.int32, device=child_rid.device),
+             entry_rid=torch.empty(max(T * f, 1), dtype=torch.int32, device=child_rid.device),
+             entry_dbit=torch.empty(max(T * f, 1), dtype=torch.int16, device=child_rid.device),
+             entry_child=torch.empty(max(T * f, 1), dtype=torch.int32, device=child_rid.device))
+    tr = _tree_struct(t)
+    h = ctypes.c_uint32()
+    _check(L, c, L.cks_bulkload_top(c, _ptr(child_rid) if nc else None, _ptr(child_min) if nc else None, nc, fanout,
+                                    fill, ctypes.byref(tr), ctypes.byref(h)))
+    t["height"], t["nodes"] = int(h.value), T
     return t
 
 

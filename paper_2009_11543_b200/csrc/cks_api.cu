@@ -627,15 +627,21 @@ int tree_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* s) {
 }
 
 // a8
+// first_global: the order's first entry is the global first (its levels' first entries get
+// CKS_DBIT_NONE); otherwise (a later block) every inner entry takes its child's minimum.
+// levels: build levels 0..levels-1 only (0 = all); top_min: minima of the top built level.
 int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
-                 float fill, const cks_tree* t, uint32_t* height) {
+                 float fill, const cks_tree* t, uint32_t* height, bool first_global = true, uint32_t levels = 0,
+                 uint16_t* top_min = nullptr) {
     cks_tree_shape s;
     int rc = tree_shape(n, fanout, fill, &s);
     if (rc != CKS_OK) return fail(ctx, rc, "bad bulk-load shape (fanout %u, fill %f)", fanout, (double)fill);
-    if (height) *height = s.height;
+    const uint32_t H = (levels == 0 || levels > s.height) ? s.height : levels;
+    if (height) *height = H;
     if (n == 0) return CKS_OK;
     if (!t || !t->node_cnt || !t->entry_rid) return fail(ctx, CKS_EINVAL, "tree arrays are NULL");
     if (t->entry_dbit && !dbit) return fail(ctx, CKS_EINVAL, "entry_dbit requested without dbit");
+    if (top_min && !dbit) return fail(ctx, CKS_EINVAL, "top_min requested without dbit");
     const uint32_t per = s.per_node;
     BulkLevel L{};
     L.entries = n;
@@ -643,7 +649,7 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
     L.node_off = 0;
     L.span = 1;
     // per-node minima of D_k (rmin) ping-pong between two scratch buffers, level by level
-    const bool mins = dbit && s.height > 1;
+    const bool mins = dbit && (H > 1 || top_min);
     if (mins) {
         TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
         TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
@@ -652,7 +658,7 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
                               mins ? as<uint16_t>(ctx->rmin0) : nullptr, ctx->sms, ctx->stream));
     const uint16_t* rbelow = mins ? as<uint16_t>(ctx->rmin0) : nullptr;
     uint64_t span = per;
-    for (uint32_t l = 1; l < s.height; l++) {
+    for (uint32_t l = 1; l < H; l++) {
         BulkLevel I{};
         I.entries = s.level_nodes[l - 1];
         I.nodes = s.level_nodes[l];
@@ -661,8 +667,45 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
         I.span = span;
         uint16_t* rout = mins ? ((l & 1) ? as<uint16_t>(ctx->rmin1) : as<uint16_t>(ctx->rmin0)) : nullptr;
         LAUNCH(launch_bulk_inner(perm, rbelow, I, n, fanout, per, t->node_cnt, t->entry_rid, t->entry_dbit,
-                                 t->entry_child, s.level_offset[1], rout, ctx->sms, ctx->stream));
+                                 t->entry_child, s.level_offset[1], rout, ctx->sms, ctx->stream, first_global));
         rbelow = rout;
+        span *= per;
+    }
+    if (top_min)
+        CK(cudaMemcpyAsync(top_min, rbelow, (size_t)s.level_nodes[H - 1] * 2, cudaMemcpyDeviceToDevice, ctx->stream));
+    return CKS_OK;
+}
+
+// P:502 merge: the levels above nchild child nodes (highest row id + minimum D_k of each);
+// node ids start at 0 on the first built level.
+int run_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* child_min, uint64_t nchild,
+                     uint32_t fanout, float fill, const cks_tree* t, uint32_t* height) {
+    cks_tree_shape s;
+    int rc = tree_shape(nchild, fanout, fill, &s);
+    if (rc != CKS_OK) return fail(ctx, rc, "bad bulk-load shape (fanout %u, fill %f)", fanout, (double)fill);
+    const uint32_t H = nchild > 1 ? s.height : 0;                 // levels over the children (one child: none)
+    if (height) *height = H;
+    if (nchild == 0) return CKS_OK;
+    if (!t || !t->node_cnt || !t->entry_rid) return fail(ctx, CKS_EINVAL, "tree arrays are NULL");
+    const uint32_t per = s.per_node;
+    TRY(ensure(ctx, ctx->rmin0, (size_t)nchild * 2 + 16));
+    TRY(ensure(ctx, ctx->rmin1, (size_t)nchild * 2 + 16));
+    const uint16_t* rbelow = child_min;
+    uint64_t span = 1, entries = nchild, below_off = 0, off = 0;
+    for (uint32_t l = 0; l < H; l++) {
+        BulkLevel I{};
+        I.entries = entries;
+        I.nodes = (entries + per - 1) / per;
+        I.node_off = off;
+        I.below_off = below_off;
+        I.span = span;
+        uint16_t* rout = (l & 1) ? as<uint16_t>(ctx->rmin1) : as<uint16_t>(ctx->rmin0);
+        LAUNCH(launch_bulk_inner(child_rid, rbelow, I, nchild, fanout, per, t->node_cnt, t->entry_rid, t->entry_dbit,
+                                 t->entry_child, 0, rout, ctx->sms, ctx->stream, true));
+        rbelow = rout;
+        below_off = I.node_off;
+        off += I.nodes;
+        entries = I.nodes;
         span *= per;
     }
     return CKS_OK;
@@ -1034,6 +1077,29 @@ int cks_sort_prefix(cks_ctx* ctx, const uint32_t* packed, const uint8_t* sort_ma
         CK(cudaMemcpy2DAsync(packed_out, n * 4, o.packed, o.packed_pitch * 4, n * 4, (o.popcount + 31) / 32,
                              cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    return CKS_OK;
+}
+
+int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout, float fill,
+                       int first_global, uint32_t levels, cks_tree* out, uint16_t* top_min_out, uint32_t* height_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
+    if (n && !perm) return fail(ctx, CKS_EINVAL, "perm is NULL");
+    CK(cudaSetDevice(ctx->device));
+    uint32_t h = 0;
+    TRY(run_bulkload(ctx, perm, dbit, n, fanout, fill, out, &h, first_global != 0, levels, top_min_out));
+    if (height_out) *height_out = h;
+    return CKS_OK;
+}
+
+int cks_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* child_min, uint64_t nchild,
+                     uint32_t fanout, float fill, cks_tree* out, uint32_t* height_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (nchild && (!child_rid || !child_min)) return fail(ctx, CKS_EINVAL, "NULL child arrays");
+    CK(cudaSetDevice(ctx->device));
+    uint32_t h = 0;
+    TRY(run_bulkload_top(ctx, child_rid, child_min, nchild, fanout, fill, out, &h));
+    if (height_out) *height_out = h;
     return CKS_OK;
 }
 

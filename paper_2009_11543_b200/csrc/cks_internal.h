@@ -158,7 +158,7 @@ cudaError_t launch_bulk_leaves(const uint32_t* perm, const uint16_t* dbit, const
 cudaError_t launch_bulk_inner(const uint32_t* perm, const uint16_t* rmin_below, const BulkLevel& L,
                               uint64_t n, uint32_t fanout, uint32_t per, uint32_t* node_cnt,
                               uint32_t* rid, uint16_t* edbit, uint32_t* child, uint64_t inner_off,
-                              uint16_t* rmin, int sms, cudaStream_t st);
+                              uint16_t* rmin, int sms, cudaStream_t st, bool first_none = true);
 
 // NEXT-3 paper-format index tree (k_ptree.cu)
 cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(256)
 k_bulk_inner(const uint32_t* __restrict__ perm, const uint16_t* __restrict__ rmin_below, BulkLevel L,
              uint64_t n, uint32_t fanout, uint32_t per, uint32_t* __restrict__ node_cnt,
              uint32_t* __restrict__ rid, uint16_t* __restrict__ edbit, uint32_t* __restrict__ child,
-             uint64_t inner_off, uint16_t* __restrict__ rmin) {
+             uint64_t inner_off, uint16_t* __restrict__ rmin, int first_none) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < L.nodes; j += nwarps) {
@@ -264,7 +264,7 @@ k_bulk_inner(const uint32_t* __restrict__ perm, const uint16_t* __restrict__ rmi
                 if (rmin_below) {
                     uint32_t v = rmin_below[x];
                     mn = min(mn, v);
-                    if (edbit) edbit[gs] = x == 0 ? (uint16_t)CKS_NONE_INTERNAL : (uint16_t)v;
+                    if (edbit) edbit[gs] = (x == 0 && first_none) ? (uint16_t)CKS_NONE_INTERNAL : (uint16_t)v;
                 }
             } else {
                 rid[gs] = 0xFFFFFFFFu;
@@ -362,9 +362,9 @@ cudaError_t launch_bulk_leaves(const uint32_t* perm, const uint16_t* dbit, const
 cudaError_t launch_bulk_inner(const uint32_t* perm, const uint16_t* rmin_below, const BulkLevel& L,
                               uint64_t n, uint32_t fanout, uint32_t per, uint32_t* node_cnt,
                               uint32_t* rid, uint16_t* edbit, uint32_t* child, uint64_t inner_off,
-                              uint16_t* rmin, int sms, cudaStream_t st) {
+                              uint16_t* rmin, int sms, cudaStream_t st, bool first_none) {
     k_bulk_inner<<<grid_warps(L.nodes, sms), 256, 0, st>>>(perm, rmin_below, L, n, fanout, per, node_cnt, rid,
-                                                           edbit, child, inner_off, rmin);
+                                                           edbit, child, inner_off, rmin, first_none ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -15,8 +15,9 @@ off_r .. off_r + n_r - 1). The method shards with one exchange step (SURVEY 8(e)
   a6  adjacency over the slice plus the pair across each slice boundary (the previous
       non-empty slice's last key is all-gathered), D = OR of the slices' D (all-gather);
   a7  P_D of the slice by repacking P_{D+} (cks_repack);
-  a8  rank 0 bulk-loads the gathered order (the thin tail; per-shard subtrees with a merged
-      top, are the next step).
+  a8  P:502: every rank bulk-loads a subtree over its slice (cks_bulkload_block), the
+      subtrees' roots are removed and rank 0 builds the top layers over the roots' children
+      (cks_bulkload_top); the tree stays distributed (assemble_tree joins it on the host).
 
 Every per-shard step is a libcks kernel (`CudaOps`); this module only moves data between
 ranks. `Comm` implementations: `TorchComm` (torch.distributed: NCCL between GPUs, gloo for
@@ -158,9 +159,8 @@ class CudaOps:
     def adjacent(sorted_planes, bits, sort_mask):
         return cks.adjacent_dbits(sorted_planes, bits, sort_mask, want_dbit=True)
 
-    @staticmethod
-    def bulkload(perm, dbit, fanout, fill):
-        return cks.bulkload(perm, dbit, fanout, fill)
+    bulkload_block = staticmethod(cks.bulkload_block)
+    bulkload_top = staticmethod(cks.bulkload_top)
 
 
 # ---- host logic ----------------------------------------------------------------------------
@@ -181,6 +181,75 @@ def regular_sample(count: int, per_rank: int) -> np.ndarray:
     """Positions of a regular sample of `per_rank` elements of a sorted shard of `count`."""
     s = min(per_rank, count)
     return ((2 * np.arange(s, dtype=np.int64) + 1) * count) // (2 * s) if s else np.zeros(0, np.int64)
+
+
+def _height(n: int, per: int) -> int:
+    """Levels of the bottom-up bulk load of n keys, per entries a node (0 for n = 0)."""
+    h, c = 0, n
+    while c > 0:
+        c = (c + per - 1) // per
+        h += 1
+        if c == 1:
+            break
+    return h
+
+
+def assemble_tree(outs: list[dict]) -> dict:
+    """Host-side join of the distributed P:502 tree (every rank's out["tree"], rank order) into
+    one node array set, levels concatenated leaves first (the layout of cks_bulkload):
+    node_cnt [T], entry_rid / entry_child [T, fanout] (u32), entry_dbit [T, fanout] (u16)."""
+    t0 = outs[0]["tree"]
+    f, lstar = t0["fanout"], t0["lstar"]
+    per = int(f * t0["fill"])
+    subs = [o["tree"]["sub"] for o in outs]
+    loc = [[int(s["shape"].level_nodes[l]) for l in range(lstar + 1)] if s is not None else [0] * (lstar + 1)
+           for s in subs]
+    top = t0["top"]
+    top_lv = []
+    c = sum(t0["children"])
+    while c > 1:
+        c = (c + per - 1) // per
+        top_lv.append(c)
+    lv = [sum(x[l] for x in loc) for l in range(lstar + 1)] + top_lv
+    goff = np.cumsum([0] + lv)
+    T = int(goff[-1])
+    node_cnt = np.zeros(T, np.uint32)
+    rid = np.full((T, f), 0xFFFFFFFF, np.uint32)
+    child = np.full((T, f), 0xFFFFFFFF, np.uint32)
+    edb = np.full((T, f), 0xFFFF, np.uint16)
+
+    def host(t, a, b, dt):
+        return t[a:b].cpu().numpy().view(dt)
+
+    for l in range(lstar + 1):
+        before = before_below = 0                        # this level's / the level below's nodes of earlier ranks
+        for s, x in zip(subs, loc):
+            if s is not None and x[l]:
+                sh = s["shape"]
+                lo, k = int(sh.level_offset[l]), x[l]
+                g = int(goff[l]) + before
+                node_cnt[g:g + k] = host(s["node_cnt"], lo, lo + k, np.uint32)
+                rid[g:g + k] = host(s["entry_rid"], lo * f, (lo + k) * f, np.uint32).reshape(k, f)
+                edb[g:g + k] = host(s["entry_dbit"], lo * f, (lo + k) * f, np.uint16).reshape(k, f)
+                if l > 0:
+                    io = lo - int(sh.level_nodes[0])
+                    ch = host(s["entry_child"], io * f, (io + k) * f, np.uint32).reshape(k, f).astype(np.int64)
+                    base = int(goff[l - 1]) + before_below - int(sh.level_offset[l - 1])
+                    child[g:g + k] = np.where(ch != 0xFFFFFFFF, ch + base, 0xFFFFFFFF).astype(np.uint32)
+            before += x[l]
+            before_below += x[l - 1] if l > 0 else 0
+    if top is not None:
+        k = sum(top_lv)
+        g = int(goff[lstar + 1])
+        node_cnt[g:g + k] = host(top["node_cnt"], 0, k, np.uint32)
+        rid[g:g + k] = host(top["entry_rid"], 0, k * f, np.uint32).reshape(k, f)
+        edb[g:g + k] = host(top["entry_dbit"], 0, k * f, np.uint16).reshape(k, f)
+        ch = host(top["entry_child"], 0, k * f, np.uint32).reshape(k, f).astype(np.int64)
+        base = np.full((k, 1), g, np.int64)
+        base[:top_lv[0]] = int(goff[lstar])              # the first top level indexes the child list
+        child[g:g + k] = np.where(ch != 0xFFFFFFFF, ch + base, 0xFFFFFFFF).astype(np.uint32)
+    return dict(height=len(lv), level_nodes=np.array(lv, np.uint64), node_cnt=node_cnt, entry_rid=rid,
+                entry_child=child, entry_dbit=edb)
 
 
 def _as_i32(x: np.ndarray) -> np.ndarray:
@@ -269,18 +338,29 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
     out = dict(mask=D, popcount=cks.popcount(D), sort_mask=M, sort_bits=m, perm=perm, dbit=dbit, packed=packed,
                offset=sum(nrs[:r]), n_total=N, send_counts=send_counts, tree=None)
 
-    # a8: rank 0 bulk-loads the gathered order
-    if tree and N and G == 1:
-        out["tree"] = ops.bulkload(perm, dbit, fanout, fill)
-    elif tree and N:
-        mx = max(nrs)
-        pad = torch.zeros((mx, 2), dtype=torch.int32, device=dev)
+    # a8: a subtree per slice; the roots removed; the top layers over their children
+    if tree and N:
+        per = int(fanout * fill)
+        hs = [int(t.item()) for t in comm.allgather(torch.tensor([_height(nr, per)], dtype=torch.int64, device=dev))]
+        hmin = min(h for h in hs if h > 0)
+        lstar = max(0, hmin - 2)
+        first_rank = next(k for k in range(G) if nrs[k] > 0)
+        sub, cnt = None, 0
         if nr:
-            pad[:nr, 0] = perm
-            pad[:nr, 1] = dbit.to(torch.int32)
-        allp = comm.allgather(pad)
-        if r == 0:
-            gp = torch.cat([t[:c, 0] for t, c in zip(allp, nrs)]).contiguous()
-            gd = torch.cat([t[:c, 1] for t, c in zip(allp, nrs)]).to(torch.int16).contiguous()
-            out["tree"] = ops.bulkload(gp, gd, fanout, fill)
+            sub = ops.bulkload_block(perm, dbit, fanout, fill, r == first_rank, lstar + 1)
+            cnt = int(sub["shape"].level_nodes[lstar])
+        span = per ** (lstar + 1)
+        hi = torch.clamp(torch.arange(1, cnt + 1, device=dev, dtype=torch.int64) * span, max=nr) - 1
+        cnts = [int(t.item()) for t in comm.allgather(torch.tensor([cnt], dtype=torch.int64, device=dev))]
+        pad = torch.zeros((max(1, max(cnts)), 2), dtype=torch.int32, device=dev)
+        if cnt:
+            pad[:cnt, 0] = perm[hi]
+            pad[:cnt, 1] = sub["top_min"][:cnt].to(torch.int32)
+        allc = comm.allgather(pad)
+        top = None
+        if r == 0 and sum(cnts) > 1:
+            crid = torch.cat([t[:c, 0] for t, c in zip(allc, cnts)]).contiguous()
+            cmin = torch.cat([t[:c, 1] for t, c in zip(allc, cnts)]).to(torch.int16).contiguous()
+            top = ops.bulkload_top(crid, cmin, fanout, fill)
+        out["tree"] = dict(sub=sub, lstar=lstar, children=cnts, top=top, fanout=fanout, fill=fill, sizes=nrs)
     return out

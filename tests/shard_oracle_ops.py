@@ -2,6 +2,8 @@
 the oracle (sort, compress, adjacency, bulk load) and plain numpy (occupancy bitsets, lower
 bounds, bit repack), so that the sharded orchestration and its collectives can run under
 gloo without a GPU. Only tests import this module."""
+from types import SimpleNamespace
+
 import numpy as np
 import torch
 
@@ -144,8 +146,60 @@ class OracleOps:
         keep = [t for t in range(m) if (int(out_mask[pos[t] >> 3]) >> (7 - (int(pos[t]) & 7))) & 1]
         return _i32(bits_to_planes(bits[:, keep]))
 
-    def bulkload(self, perm, dbit, fanout, fill):
-        return oracle.bulkload(_u32(perm), dbit.cpu().numpy().view(np.uint16), self.all_keys, fanout, fill)
+    def bulkload_block(self, perm, dbit, fanout, fill, first_global, levels):
+        """Range-minimum bulk load of one block (numpy; the independent check of the result is
+        oracle.bulkload_blocks, which takes the D-bits from the keys)."""
+        p = _u32(perm)
+        d = dbit.cpu().numpy().view(np.uint16).astype(np.int64)
+        per = int(fanout * fill)
+        lv = oracle.tree_levels(p.size, per)[:levels]
+        return self._levels(p, d, lv, fanout, per, first_global, leaves=True)
+
+    def bulkload_top(self, child_rid, child_min, fanout, fill):
+        p = _u32(child_rid)
+        d = child_min.cpu().numpy().view(np.uint16).astype(np.int64)
+        per = int(fanout * fill)
+        lv = oracle.tree_levels(p.size, per) if p.size > 1 else []
+        t = self._levels(p, d, lv, fanout, per, True, leaves=False)
+        t["height"] = len(lv)
+        return t
+
+    @staticmethod
+    def _levels(p, d, lv, f, per, first_global, leaves):
+        n = p.size
+        T = int(sum(lv))
+        off = np.cumsum([0] + list(lv))
+        cnt = np.zeros(max(T, 1), np.uint32)
+        rid = np.full(max(T, 1) * f, 0xFFFFFFFF, np.uint32)
+        edb = np.full(max(T, 1) * f, 0xFFFF, np.uint16)
+        inner0 = lv[0] if leaves and lv else 0
+        child = np.full(max(T - inner0, 1) * f, 0xFFFFFFFF, np.uint32)
+        rmin, span = d, 1
+        for l, nodes in enumerate(lv):
+            ents = n if l == 0 else lv[l - 1]
+            leaf = leaves and l == 0
+            out_min = np.zeros(nodes, np.int64)
+            for j in range(nodes):
+                xs = range(j * per, min((j + 1) * per, ents))
+                node = off[l] + j
+                cnt[node] = len(xs)
+                for e, x in enumerate(xs):
+                    s = node * f + e
+                    hi = min((x + 1) * span, n) - 1
+                    rid[s] = p[hi]
+                    if leaf:
+                        edb[s] = d[x]
+                    else:
+                        edb[s] = 0xFFFF if (x == 0 and first_global) else rmin[x]
+                        below = off[l - 1] if (leaves and l > 0) else (0 if l == 0 else off[l - 1])
+                        child[(node - inner0) * f + e] = below + x
+                out_min[j] = min(rmin[x] for x in xs)
+            rmin = out_min
+            span *= per
+        i32 = lambda a: torch.from_numpy(a.view(np.int32).copy())
+        return dict(shape=SimpleNamespace(level_nodes=list(lv), level_offset=list(off[:-1])), node_cnt=i32(cnt),
+                    entry_rid=i32(rid), entry_dbit=torch.from_numpy(edb.view(np.int16).copy()), entry_child=i32(child),
+                    top_min=torch.from_numpy(rmin.astype(np.uint16).view(np.int16).copy()))
 
 
 def check_slices(keys, outs, fanout=64, fill=1.0):
@@ -162,11 +216,12 @@ def check_slices(keys, outs, fanout=64, fill=1.0):
     if ref["m"]:
         packed = np.concatenate([o["packed"].cpu().numpy().view(np.uint32) for o in outs], axis=1)
         assert np.array_equal(packed, ref["planes"][:, ref["perm"]])
-    t = outs[0]["tree"]
-    if keys.shape[0]:
-        exp = oracle.bulkload(ref["perm"], ref["dbit"], keys, fanout, fill)
-        T = exp["entry_rid"].size
-        rid = t["entry_rid"].cpu().numpy() if torch.is_tensor(t["entry_rid"]) else t["entry_rid"]
-        db = t["entry_dbit"].cpu().numpy() if torch.is_tensor(t["entry_dbit"]) else t["entry_dbit"]
-        assert np.array_equal(rid.reshape(-1).view(np.uint32)[:T], exp["entry_rid"].ravel())
-        assert np.array_equal(db.reshape(-1).view(np.uint16)[:T], exp["entry_dbit"].ravel())
+    if keys.shape[0] and outs[0].get("tree") is not None:
+        from paper_2009_11543_b200 import shard
+        got = shard.assemble_tree(outs)
+        sizes = [o["perm"].numel() for o in outs]
+        exp = oracle.bulkload_blocks(ref["perm"], ref["dbit"], keys, sizes, fanout, fill)
+        assert got["height"] == exp["height"]
+        assert np.array_equal(got["level_nodes"], exp["level_nodes"])
+        for k in ("node_cnt", "entry_rid", "entry_child", "entry_dbit"):
+            assert np.array_equal(got[k], exp[k]), k

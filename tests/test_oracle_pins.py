@@ -417,3 +417,81 @@ def test_paper_tree_structure(n, fill, pk):
                 want = 0xFFFF if ch == 0 else int(dbit[ch * cover: hi + 1].min())
                 assert le(ent, 4, 2) == want
         below, off, cover = off, off + lv[l], cover * ip
+
+
+# ---- P:502 block-parallel construction (orc_bulkload_blocks, NEXT-4's a8) ------------------------
+
+def _subtree_ranges(t, n):
+    """(lo, hi) sorted-index range under every node, from the leaf counts upward."""
+    lv = [int(x) for x in t["level_nodes"]]
+    off = np.cumsum([0] + lv)
+    lo = np.zeros(off[-1], np.int64)
+    hi = np.zeros(off[-1], np.int64)
+    pos = 0
+    for j in range(lv[0]):
+        c = int(t["node_cnt"][j])
+        lo[j], hi[j] = pos, pos + c - 1
+        pos += c
+    assert pos == n
+    for l in range(1, len(lv)):
+        for j in range(lv[l]):
+            node = off[l] + j
+            ch = t["entry_child"][node][: int(t["node_cnt"][node])].astype(np.int64)
+            lo[node], hi[node] = lo[ch[0]], hi[ch[-1]]
+    return lo, hi
+
+
+@pytest.mark.parametrize("n,fanout", [(1, 8), (7, 8), (64, 8), (5000, 8), (3001, 16)])
+def test_bulkload_blocks_one_block_is_bulkload(n, fanout):
+    keys = cksgen.config(3, n=n)
+    ref = oracle.first_build(keys)
+    a = oracle.bulkload(ref["perm"], ref["dbit"], keys, fanout, 1.0)
+    b = oracle.bulkload_blocks(ref["perm"], ref["dbit"], keys, [n], fanout, 1.0)
+    assert a["height"] == b["height"]
+    for k in ("node_cnt", "entry_rid", "entry_child", "entry_dbit"):
+        assert np.array_equal(a[k], b[k])
+
+
+@pytest.mark.parametrize("blocks", [[64, 64, 64], [512, 512], [64] * 9])
+def test_bulkload_blocks_complete_subtrees_equal_global(blocks):
+    # blocks of per^k keys: complete subtrees; removing their roots and linking the roots'
+    # children (P:502) gives exactly the global bottom-up bulk load
+    n = sum(blocks)
+    keys = cksgen.config(5, n=n)
+    ref = oracle.first_build(keys)
+    a = oracle.bulkload(ref["perm"], ref["dbit"], keys, 8, 1.0)
+    b = oracle.bulkload_blocks(ref["perm"], ref["dbit"], keys, blocks, 8, 1.0)
+    for k in ("node_cnt", "entry_rid", "entry_child", "entry_dbit"):
+        assert np.array_equal(a[k], b[k])
+
+
+@pytest.mark.parametrize("blocks", [[100, 0, 37, 900], [1, 1, 1], [4000, 10], [333] * 7])
+def test_bulkload_blocks_invariants(blocks):
+    n = sum(blocks)
+    keys = cksgen.config(1, n=n)
+    ref = oracle.first_build(keys)
+    per = 8
+    t = oracle.bulkload_blocks(ref["perm"], ref["dbit"], keys, blocks, per, 1.0)
+    lv = [int(x) for x in t["level_nodes"]]
+    assert lv[-1] == 1 and all(1 <= c <= per for c in t["node_cnt"])
+    leaves = np.concatenate([t["entry_rid"][j][: int(t["node_cnt"][j])] for j in range(lv[0])])
+    assert np.array_equal(leaves, ref["perm"])                     # every key once, in order
+    nz = [b for b in blocks if b]
+    # leaves never straddle a block border (each block is built on its own, P:502)
+    borders = set(np.cumsum(nz)[:-1].tolist())
+    lo, hi = _subtree_ranges(t, n)
+    assert all(not (lo[j] < b <= hi[j]) for j in range(lv[0]) for b in borders)
+    off = np.cumsum([0] + lv)
+    for l in range(1, len(lv)):
+        first = True
+        for j in range(lv[l]):
+            node = off[l] + j
+            for e in range(int(t["node_cnt"][node])):
+                c = int(t["entry_child"][node][e])
+                assert t["entry_rid"][node][e] == ref["perm"][hi[c]]     # highest key of the child (P:356)
+                d = int(t["entry_dbit"][node][e])
+                if first:
+                    assert d == 0xFFFF
+                    first = False
+                else:                                                   # Lemma 1 (P:180) across borders
+                    assert d == int(ref["dbit"][lo[c]: hi[c] + 1].min())

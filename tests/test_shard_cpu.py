@@ -91,9 +91,7 @@ def _worker(rank, world, port, keys, sizes, q):
         k = torch.from_numpy(np.ascontiguousarray(keys[a:a + sizes[rank]]))
         o = sh.build_sharded(k, sh.TorchComm(), ops=Ops(keys), samples_per_rank=32)
         q.put((rank, dict(perm=o["perm"].numpy(), dbit=o["dbit"].numpy(), mask=o["mask"], offset=o["offset"],
-                          packed=o["packed"].numpy(), send=o["send_counts"],
-                          tree=None if o["tree"] is None else {k2: v for k2, v in o["tree"].items()
-                                                               if k2 in ("entry_rid", "entry_dbit")})))
+                          packed=o["packed"].numpy(), send=o["send_counts"], tree=o["tree"])))
     finally:
         dist.destroy_process_group()
 
