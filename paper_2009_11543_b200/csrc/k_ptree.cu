@@ -34,6 +34,25 @@ __device__ __forceinline__ uint32_t key_bits(const uint8_t* key, uint32_t B, uin
 __device__ __forceinline__ uint32_t pk_of(const uint8_t* keys, uint32_t B, uint32_t rid, uint16_t d, uint32_t pk) {
     return key_bits(keys + (uint64_t)rid * B, B, d == CKS_NONE_INTERNAL ? 0u : (uint32_t)d + 1, pk);
 }
+// the same with the 40-bit window read as two aligned 8-byte words (key rows 8-byte aligned,
+// B % 8 == 0): one sector per key instead of five byte loads
+__device__ __forceinline__ unsigned long long bswap64(unsigned long long x) {
+    const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+    return ((unsigned long long)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+}
+__device__ __forceinline__ uint32_t pk_of8(const uint8_t* keys, uint32_t B, uint32_t rid, uint16_t d, uint32_t pk) {
+    if (pk == 0) return 0u;
+    const uint32_t p0 = d == CKS_NONE_INTERNAL ? 0u : (uint32_t)d + 1;
+    const uint32_t w0 = (p0 >> 6);                                  // 8-byte word holding bit p0
+    if (8 * w0 >= B) return 0u;
+    const unsigned long long* row = reinterpret_cast<const unsigned long long*>(keys + (uint64_t)rid * B);
+    const unsigned long long a = bswap64(__ldg(row + w0));           // big-endian: bit 0 = MSB
+    const unsigned long long b = 8 * (w0 + 1) < B ? bswap64(__ldg(row + w0 + 1)) : 0ull;
+    const uint32_t sh = p0 & 63;
+    const unsigned long long v = sh ? (a << sh) | (b >> (64 - sh)) : a;
+    const uint32_t top = (uint32_t)(v >> 32);
+    return pk >= 32 ? top : top & ~(0xFFFFFFFFu >> pk);
+}
 }  // namespace
 
 // leaves, thread per sorted key k (entry k % per of leaf k / per): the key-row reads of a
@@ -41,20 +60,36 @@ __device__ __forceinline__ uint32_t pk_of(const uint8_t* keys, uint32_t B, uint3
 __global__ void __launch_bounds__(kPtThreads)
 k_ptree_leaf_entries(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
                      const uint16_t* __restrict__ dbit, uint32_t pk, uint32_t per, uint64_t nleaves,
-                     uint8_t* __restrict__ nodes) {
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t j = k / per;
-        const uint32_t e = (uint32_t)(k - j * per);
-        uint4* nd = reinterpret_cast<uint4*>(nodes + j * 256);
-        const uint32_t rid = perm[k];
-        const uint16_t d = dbit[k];
-        nd[2 + e] = make_uint4(pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16), rid, 0u);   // 32 + 16 e
-        if (e == 0) {                                             // header, next leaf, unused entries
-            const uint64_t k1 = min(k + per, n);
-            const unsigned long long next = j + 1 < nleaves ? j + 1 : ~0ull;
-            nd[0] = make_uint4((uint32_t)(k1 - k), B, perm[k1 - 1], 0u);
-            nd[1] = make_uint4(0u, 0u, (uint32_t)next, (uint32_t)(next >> 32));
-            for (uint32_t u = (uint32_t)(k1 - k); u < 14; u++) nd[2 + u] = make_uint4(0, 0, 0, 0);
+                     uint8_t* __restrict__ nodes, int words8) {
+    constexpr int U = 4;                                          // keys in flight per thread
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < n; k0 += U * T) {
+        uint32_t rid[U], pkv[U];
+        uint16_t d[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint64_t k = k0 + u * T;
+            rid[u] = k < n ? perm[k] : 0u;
+            d[u] = k < n ? dbit[k] : (uint16_t)CKS_NONE_INTERNAL;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            pkv[u] = k0 + u * T < n ? (words8 ? pk_of8(keys, B, rid[u], d[u], pk) : pk_of(keys, B, rid[u], d[u], pk)) : 0u;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint64_t k = k0 + u * T;
+            if (k >= n) break;
+            const uint64_t j = k / per;
+            const uint32_t e = (uint32_t)(k - j * per);
+            uint4* nd = reinterpret_cast<uint4*>(nodes + j * 256);
+            nd[2 + e] = make_uint4(pkv[u], (uint32_t)d[u] | (B << 16), rid[u], 0u);   // 32 + 16 e
+            if (e == 0) {                                         // header, next leaf, unused entries
+                const uint64_t k1 = min(k + per, n);
+                const unsigned long long next = j + 1 < nleaves ? j + 1 : ~0ull;
+                nd[0] = make_uint4((uint32_t)(k1 - k), B, perm[k1 - 1], 0u);
+                nd[1] = make_uint4(0u, 0u, (uint32_t)next, (uint32_t)(next >> 32));
+                for (uint32_t v = (uint32_t)(k1 - k); v < 14; v++) nd[2 + v] = make_uint4(0, 0, 0, 0);
+            }
         }
     }
 }
@@ -77,7 +112,7 @@ __global__ void __launch_bounds__(kPtThreads)
 k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
               uint32_t pk, uint32_t per, uint64_t nbelow, uint64_t cover_below, uint64_t below_off, uint64_t nnodes,
               uint64_t node_off, uint32_t level, const uint16_t* __restrict__ rmin_below, uint16_t* __restrict__ rmin,
-              uint8_t* __restrict__ nodes) {
+              uint8_t* __restrict__ nodes, int words8) {
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnodes; j += (uint64_t)gridDim.x * blockDim.x) {
         uint8_t* nd = nodes + (node_off + j) * 256;
         uint2* w = reinterpret_cast<uint2*>(nd);
@@ -95,7 +130,7 @@ k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const ui
                 const uint16_t d = ch == 0 ? (uint16_t)CKS_NONE_INTERNAL : rm;   // vs the previous entry
                 last = rid;
                 const unsigned long long child = below_off + ch;
-                a = make_uint2(pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16));
+                a = make_uint2(words8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16));
                 b = make_uint2((uint32_t)child, (uint32_t)(child >> 32));
                 c = make_uint2(rid, 0u);
             }
@@ -125,8 +160,9 @@ cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint
                          uint16_t* rmin_b, int sms, cudaStream_t st, int* launches) {
     *launches = 0;
     if (n == 0 || height == 0) return cudaSuccess;
+    const int words8 = (B % 8 == 0 && ((uintptr_t)keys & 7) == 0) ? 1 : 0;
     k_ptree_leaf_entries<<<grid_pt(n, sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
-                                                                 level_nodes[0], nodes);
+                                                                 level_nodes[0], nodes, words8);
     k_ptree_leaf_min<<<grid_pt(level_nodes[0], sms), kPtThreads, 0, st>>>(dbit, n, leaf_per, level_nodes[0], rmin_a);
     *launches += 2;
     uint64_t cover = leaf_per;
@@ -135,7 +171,7 @@ cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint
     for (uint32_t l = 1; l < height; l++) {
         k_ptree_inner<<<grid_pt(level_nodes[l], sms), kPtThreads, 0, st>>>(
             keys, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
-            level_offset[l], l, below, cur, nodes);
+            level_offset[l], l, below, cur, nodes, words8);
         ++*launches;
         cover *= inner_per;
         uint16_t* t = below;
