@@ -35,7 +35,8 @@ __device__ __forceinline__ uint32_t pk_of(const uint8_t* keys, uint32_t B, uint3
     return key_bits(keys + (uint64_t)rid * B, B, d == CKS_NONE_INTERNAL ? 0u : (uint32_t)d + 1, pk);
 }
 // the same with the 40-bit window read as two aligned 8-byte words (key rows 8-byte aligned,
-// B % 8 == 0): one sector per key instead of five byte loads
+// B % 8 == 0). A random row costs ~128 bytes of HBM traffic whichever way it is loaded
+// (ncu: cached, L2-only, one or two requests; cudaLimitMaxL2FetchGranularity has no effect)
 __device__ __forceinline__ unsigned long long bswap64(unsigned long long x) {
     const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
     return ((unsigned long long)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
@@ -57,10 +58,11 @@ __device__ __forceinline__ uint32_t pk_of8(const uint8_t* keys, uint32_t B, uint
 
 // leaves, thread per sorted key k (entry k % per of leaf k / per): the key-row reads of a
 // warp are independent (a thread per node would walk its entries serially)
+template <bool W8>
 __global__ void __launch_bounds__(kPtThreads)
 k_ptree_leaf_entries(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
                      const uint16_t* __restrict__ dbit, uint32_t pk, uint32_t per, uint64_t nleaves,
-                     uint8_t* __restrict__ nodes, int words8) {
+                     uint8_t* __restrict__ nodes) {
     constexpr int U = 4;                                          // keys in flight per thread
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < n; k0 += U * T) {
@@ -74,7 +76,7 @@ k_ptree_leaf_entries(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, c
         }
 #pragma unroll
         for (int u = 0; u < U; u++)
-            pkv[u] = k0 + u * T < n ? (words8 ? pk_of8(keys, B, rid[u], d[u], pk) : pk_of(keys, B, rid[u], d[u], pk)) : 0u;
+            pkv[u] = k0 + u * T < n ? (W8 ? pk_of8(keys, B, rid[u], d[u], pk) : pk_of(keys, B, rid[u], d[u], pk)) : 0u;
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint64_t k = k0 + u * T;
@@ -108,11 +110,12 @@ k_ptree_leaf_min(const uint16_t* __restrict__ dbit, uint64_t n, uint32_t per, ui
 }
 
 // thread per node of level `level` (>= 1)
+template <bool W8>
 __global__ void __launch_bounds__(kPtThreads)
 k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
               uint32_t pk, uint32_t per, uint64_t nbelow, uint64_t cover_below, uint64_t below_off, uint64_t nnodes,
               uint64_t node_off, uint32_t level, const uint16_t* __restrict__ rmin_below, uint16_t* __restrict__ rmin,
-              uint8_t* __restrict__ nodes, int words8) {
+              uint8_t* __restrict__ nodes) {
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnodes; j += (uint64_t)gridDim.x * blockDim.x) {
         uint8_t* nd = nodes + (node_off + j) * 256;
         uint2* w = reinterpret_cast<uint2*>(nd);
@@ -130,7 +133,7 @@ k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const ui
                 const uint16_t d = ch == 0 ? (uint16_t)CKS_NONE_INTERNAL : rm;   // vs the previous entry
                 last = rid;
                 const unsigned long long child = below_off + ch;
-                a = make_uint2(words8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16));
+                a = make_uint2(W8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16));
                 b = make_uint2((uint32_t)child, (uint32_t)(child >> 32));
                 c = make_uint2(rid, 0u);
             }
@@ -160,18 +163,27 @@ cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint
                          uint16_t* rmin_b, int sms, cudaStream_t st, int* launches) {
     *launches = 0;
     if (n == 0 || height == 0) return cudaSuccess;
-    const int words8 = (B % 8 == 0 && ((uintptr_t)keys & 7) == 0) ? 1 : 0;
-    k_ptree_leaf_entries<<<grid_pt(n, sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
-                                                                 level_nodes[0], nodes, words8);
+    const bool w8 = B % 8 == 0 && ((uintptr_t)keys & 7) == 0;    // (one path per instantiation)
+    if (w8)
+        k_ptree_leaf_entries<true><<<grid_pt(n, sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
+                                                                           level_nodes[0], nodes);
+    else
+        k_ptree_leaf_entries<false><<<grid_pt(n, sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
+                                                                            level_nodes[0], nodes);
     k_ptree_leaf_min<<<grid_pt(level_nodes[0], sms), kPtThreads, 0, st>>>(dbit, n, leaf_per, level_nodes[0], rmin_a);
     *launches += 2;
     uint64_t cover = leaf_per;
     uint16_t* below = rmin_a;
     uint16_t* cur = rmin_b;
     for (uint32_t l = 1; l < height; l++) {
-        k_ptree_inner<<<grid_pt(level_nodes[l], sms), kPtThreads, 0, st>>>(
-            keys, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
-            level_offset[l], l, below, cur, nodes, words8);
+        if (w8)
+            k_ptree_inner<true><<<grid_pt(level_nodes[l], sms), kPtThreads, 0, st>>>(
+                keys, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
+                level_offset[l], l, below, cur, nodes);
+        else
+            k_ptree_inner<false><<<grid_pt(level_nodes[l], sms), kPtThreads, 0, st>>>(
+                keys, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
+                level_offset[l], l, below, cur, nodes);
         ++*launches;
         cover *= inner_per;
         uint16_t* t = below;

@@ -6,10 +6,11 @@ from paper_2009_11543_b200 import cks
 keys = torch.from_numpy(cksgen.config(5)).cuda()
 b = cks.build(keys, tree=False)
 perm, dbit = b["perm"], b["dbit"]
-for _ in range(2): cks.paper_tree(keys, perm, dbit)
+PK = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+for _ in range(2): cks.paper_tree(keys, perm, dbit, PK)
 torch.cuda.synchronize()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(5): cks.paper_tree(keys, perm, dbit)
+for _ in range(5): cks.paper_tree(keys, perm, dbit, PK)
 e1.record(); torch.cuda.synchronize()
 print("paper_tree ms", e0.elapsed_time(e1) / 5)
