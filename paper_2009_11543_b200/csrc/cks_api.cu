@@ -50,7 +50,8 @@ struct cks_ctx {
     DevBuf occ, masks8, planeA, planeB, ridA, ridB, dacc, moff, dbit,
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
         pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, runoff2, runpos2, tie, keep, done, mlist, wlist, rcnt, rtot,   // NEXT-1
-        part_in, part_out;                                                 // NEXT-4
+        part_in, part_out,                                                 // NEXT-4
+        anyt;                                                              // k_ref_tile: tiles with ties left
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
     uint16_t* h_moff = nullptr;
@@ -436,10 +437,14 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     const uint32_t* hi0 = sorted0 + (uint64_t)(np0 - 1) * sp0;
     TRY(ensure(ctx, ctx->rtot, 64));
     CK(cudaMemsetAsync(as<uint32_t>(ctx->rtot) + 2, 0, 4, ctx->stream));
-    if (T < m && carry && !no_tile)       // (P_M by row id: the compaction + k_ref_local path measured faster)
+    const bool tiled = T < m && carry && !no_tile;   // (P_M by row id: the compaction + k_ref_local path measured faster)
+    if (tiled) {
+        TRY(ensure(ctx, ctx->anyt, ref_tiles(n) + 16));
+        CK(cudaMemsetAsync(ctx->anyt.p, 0, ref_tiles(n) + 16, ctx->stream));
         LAUNCH(launch_ref_tile(pm, sp, np, (int)np - 1 - (int)(T >> 5), 0xFFFFFFFFu >> (T & 31), moff, out->perm, dbit,
                                carried, lo0, hi0, sp0, n, ~0ull << (64 - T), B, tie, dacc, as<uint32_t>(ctx->rtot) + 2,
-                               ctx->sms, ctx->stream));
+                               ctx->sms, ctx->stream, as<uint8_t>(ctx->anyt)));
+    }
     else
         LAUNCH(launch_ref_adj(lo0, hi0, nullptr, nullptr, n, 0, moff, m, B, dbit, tie, dacc, true, ctx->sms,
                               ctx->stream, ~0ull << (64 - T)));
@@ -492,7 +497,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         uint32_t* segB_ = as<uint32_t>(bi == 0 ? ctx->segA : bi == 1 ? ctx->segB : ctx->segC);
         // (1) the tied runs of the current list
         LAUNCH(launch_ref_compact(tie, nr, pos, as<uint32_t>(ctx->rcnt), as<uint32_t>(ctx->rtot), posA_, segA_,
-                                  as<uint32_t>(ctx->runoff), as<uint32_t>(ctx->runpos), ctx->stream));
+                                  as<uint32_t>(ctx->runoff), as<uint32_t>(ctx->runpos), ctx->stream,
+                                  r == 1 && tiled ? as<uint8_t>(ctx->anyt) : nullptr));
         uint64_t nn = 0, nseg = 0;
         TRY(counts(&nn, &nseg));
         if (nn == 0) break;

@@ -117,7 +117,7 @@ cudaError_t launch_rank_sorted(const uint32_t* planes, uint32_t np, uint64_t n, 
 cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, uint32_t fmask,
                             const uint16_t* moff, uint32_t* perm, uint16_t* dbit, uint32_t* carried, const uint32_t* lo,
                             const uint32_t* hi, uint64_t hpitch, uint64_t n, unsigned long long cmask, uint32_t B,
-                            uint8_t* tie, uint32_t* dacc, uint32_t* handled, int sms, cudaStream_t st);
+                            uint8_t* tie, uint32_t* dacc, uint32_t* handled, int sms, cudaStream_t st, uint8_t* any);
 cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_t* seg, const uint32_t* pos,
                            uint64_t nr, uint32_t cbase, const uint16_t* moff, uint32_t m, uint32_t B,
                            uint16_t* dbit, uint8_t* tie, uint32_t* dacc, bool round0, int sms, cudaStream_t st,
@@ -125,7 +125,7 @@ cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_
 // run_off / run_pos (NULL: not needed): list index and global position of each run's first key
 cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* pos, uint32_t* cnt, uint32_t* tot,
                                uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, uint32_t* run_pos,
-                               cudaStream_t st);
+                               cudaStream_t st, const uint8_t* any = nullptr);
 cudaError_t launch_ref_local(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, const uint16_t* moff,
                              const uint32_t* run_pos, const uint32_t* seg, const uint32_t* run_off, uint64_t nseg,
                              uint64_t nn, uint32_t* perm, uint16_t* dbit, uint32_t* dacc, uint8_t* done, uint8_t* keep,

@@ -105,10 +105,14 @@ __device__ __forceinline__ void ref_flags_s(const uint8_t* s_f, uint32_t k, bool
 
 // per tile: (members, run starts)
 __global__ void __launch_bounds__(kRefThreads)
-k_ref_count(const uint8_t* __restrict__ tie, uint64_t nr, uint32_t* __restrict__ cnt) {
+k_ref_count(const uint8_t* __restrict__ tie, uint64_t nr, uint32_t* __restrict__ cnt, const uint8_t* __restrict__ any) {
     __shared__ uint32_t s_red[2][kRefThreads / 32];
     __shared__ __align__(16) uint8_t s_f[kRefTile + 16];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (any && !any[blockIdx.x]) {                        // no tie flag in this tile (nor the next's first)
+        if (threadIdx.x < 2) cnt[2 * (uint64_t)blockIdx.x + threadIdx.x] = 0;
+        return;
+    }
     stage_flags(tie, nr, (uint64_t)blockIdx.x * kRefTile, s_f);
     __syncthreads();
     const uint32_t k0 = warp * 32 * kRefItems + lane;
@@ -172,9 +176,10 @@ k_ref_scan(uint32_t* __restrict__ cnt, uint32_t ntiles, uint32_t* __restrict__ t
 __global__ void __launch_bounds__(kRefThreads)
 k_ref_scatter(const uint8_t* __restrict__ tie, uint64_t nr, const uint32_t* __restrict__ pos,
               const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pos_next, uint32_t* __restrict__ seg_next,
-              uint32_t* __restrict__ run_off, uint32_t* __restrict__ run_pos) {
+              uint32_t* __restrict__ run_off, uint32_t* __restrict__ run_pos, const uint8_t* __restrict__ any) {
     __shared__ uint32_t s_w[2][kRefThreads / 32];
     __shared__ __align__(16) uint8_t s_f[kRefTile + 16];
+    if (any && !any[blockIdx.x]) return;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ltm = (1u << lane) - 1u;
     const uint64_t base = (uint64_t)blockIdx.x * kRefTile;
@@ -363,7 +368,8 @@ constexpr size_t tile_smem_bytes(int wc) {
 template <int WC>
 __global__ void __launch_bounds__(kRefThreads, 3)
 k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigned long long cmask, uint32_t nwords,
-           bool vec, uint8_t* __restrict__ tie, uint32_t* __restrict__ dacc, uint32_t* __restrict__ handled) {
+           bool vec, uint8_t* __restrict__ tie, uint32_t* __restrict__ dacc, uint32_t* __restrict__ handled,
+           uint8_t* __restrict__ any) {
     static_assert(WC >= 1 && WC <= 3, "carried remaining words");
     constexpr int NWS = WC;
     constexpr int NWARP = kRefThreads / 32;
@@ -409,11 +415,21 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
         dm2 |= w == 2 ? bit : 0u;
     };
     const uint32_t i0 = threadIdx.x * kTileItems;
+    uint64_t p0 = 0;
+    // tie flags left in the compaction tile of position p0 (for k_ref_count / k_ref_scatter to
+    // skip tie-free tiles); a flag at a compaction tile's first position also concerns the
+    // tile before (its last key may start that run)
+    auto mark_any = [&](uint32_t tied, uint32_t first) {
+        if (!any || !tied) return;
+        const uint64_t c = p0 / kRefTile;
+        any[c] = 1;
+        if (first && c && p0 % kRefTile == 0) any[c - 1] = 1;
+    };
     __syncthreads();
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t t0 = tile * kTileKeys;
         const uint32_t tn = (uint32_t)(n - t0 < (uint64_t)kTileKeys ? n - t0 : (uint64_t)kTileKeys);
-        const uint64_t p0 = t0 + i0;
+        p0 = t0 + i0;
         // A. loads: top bits, row ids, carried words
         uint32_t vh[kTileItems], vl[kTileItems], vr[kTileItems];
         ld8(hi, p0, n, vec, vh);
@@ -541,6 +557,7 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
                 for (int j = 0; j < kTileItems; j++)
                     if (p0 + j < n) { tie[p0 + j] = (uint8_t)(tb >> j & 1); R.dbit[p0 + j] = odb[j]; }
             }
+            mark_any(ot[0] | ot[1], ot[0] & 0xFFu);
             __syncthreads();
             continue;
         }
@@ -624,6 +641,7 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
             for (int j = 0; j < kTileItems; j++)
                 if (p0 + j < n) { tie[p0 + j] = (uint8_t)(ot[j >> 2] >> (8 * (j & 3))); R.dbit[p0 + j] = odb[j]; }
         }
+        mark_any(ot[0] | ot[1], ot[0] & 0xFFu);
         __syncthreads();
     }
 #pragma unroll
@@ -1004,7 +1022,7 @@ cudaError_t launch_ref_adj(const uint32_t* lo, const uint32_t* hi, const uint32_
 cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int qtop, uint32_t fmask,
                             const uint16_t* moff, uint32_t* perm, uint16_t* dbit, uint32_t* carried, const uint32_t* lo,
                             const uint32_t* hi, uint64_t hpitch, uint64_t n, unsigned long long cmask, uint32_t B,
-                            uint8_t* tie, uint32_t* dacc, uint32_t* handled, int sms, cudaStream_t st) {
+                            uint8_t* tie, uint32_t* dacc, uint32_t* handled, int sms, cudaStream_t st, uint8_t* any) {
     if (n == 0) return cudaSuccess;
     const uint32_t nwords = (8 * B + 31) / 32;
     RunCtx R{pm, pitch, np, qtop, fmask, moff, perm, dbit, carried};
@@ -1020,7 +1038,7 @@ cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int
     case W:                                                                                                     \
         raise_smem_limit((const void*)k_ref_tile<W>, tile_smem_bytes(W));                                       \
         k_ref_tile<W><<<grid, kRefThreads, tile_smem_bytes(W), st>>>(R, lo, hi, n, cmask, nwords, vec, tie, dacc, \
-                                                                     handled);                                  \
+                                                                     handled, any);                             \
         break;
     switch (wc) {
         CKS_TILE_CASE(1)
@@ -1034,12 +1052,13 @@ cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int
 
 cudaError_t launch_ref_compact(const uint8_t* tie, uint64_t nr, const uint32_t* pos, uint32_t* cnt, uint32_t* tot,
                                uint32_t* pos_next, uint32_t* seg_next, uint32_t* run_off, uint32_t* run_pos,
-                               cudaStream_t st) {
+                               cudaStream_t st, const uint8_t* any) {
     const uint64_t tiles = ref_tiles(nr);
     if (tiles == 0) return cudaMemsetAsync(tot, 0, 8, st);
-    k_ref_count<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, cnt);
+    k_ref_count<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, cnt, any);
     k_ref_scan<<<1, 1024, 0, st>>>(cnt, (uint32_t)tiles, tot);
-    k_ref_scatter<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, pos, cnt, pos_next, seg_next, run_off, run_pos);
+    k_ref_scatter<<<(unsigned)tiles, kRefThreads, 0, st>>>(tie, nr, pos, cnt, pos_next, seg_next, run_off, run_pos,
+                                                           any);
     return cudaGetLastError();
 }
 
