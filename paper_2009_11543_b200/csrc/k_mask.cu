@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) k_occupancy_rows(const uint8_t* __restric
     for (uint32_t i = threadIdx.x; i < B * kRowBytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(flag)[i] = 0;
     __syncthreads();
     constexpr int U = B / 16;                                 // 16-byte units per key
-    constexpr int KPT = 64 / B;                               // keys in flight per thread
+    constexpr int KPT = 128 / B;                              // keys in flight per thread
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += KPT * stride) {
         int4 v[KPT][U];
