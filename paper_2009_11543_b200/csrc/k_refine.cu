@@ -2,21 +2,27 @@
 //
 // The paper builds from compressed keys and notes that sorting needs only the bits that
 // distinguish neighbours ("sort by distinguishing prefixes"; Theorem 2).
-// The first build here sorts on 64-bit chunks of the superset-compressed key P_M, most
-// significant chunk first:
-//   round 0  LSD-sort all keys by chunk 0 (k_lsd.cu), carrying only that chunk + row id;
-//   round r  the keys whose chunks 0..r-1 tie with a neighbour ("runs") are gathered into a
-//            compact list (chunk r of P_M by row id, run index), LSD-sorted by (run, chunk r)
-//            -- stable, so ties keep row-id order -- and written back into their run's
-//            positions, which are contiguous in the global order.
+// The first build here sorts on chunks of the superset-compressed key P_M, most significant
+// first:
+//   round 0  LSD-sort all keys by the top T <= 64 bits (k_lsd.cu; T from a sample), carrying
+//            that chunk + row id (and all of P_M when it has three planes);
+//   round r  the keys whose prefix ties with a neighbour ("runs") are finished by comparing
+//            their remaining bits when the run is short (k_ref_tile in-tile after round 0
+//            with P_M carried; k_ref_local / k_ref_warp / k_ref_cta from the compacted list),
+//            and the long runs are re-sorted by (run, next 64 bits): one CTA per run when
+//            every run fits (k_ref_cta_chunk), else a compact list (chunk of P_M by row id,
+//            run index) LSD-sorted by (run, chunk) -- stable, so ties keep row-id order --
+//            and written back into their run's positions, contiguous in the global order.
 // A pair of neighbours is separated in the first round whose chunk differs; its D-bit
 // is the first differing bit of that chunk, mapped through the M-offset table
 // (P:479): D_i = moff[64 r + clz64(chunk_i XOR chunk_{i-1})]. Pairs equal in every chunk
 // are duplicates (D_i = none, reading R3). The union of the D_i is the exact D.
 //
-// Kernels: k_ref_adj (round adjacency: D_i, tie flags, D accumulation), k_ref_count /
-// k_ref_scan / k_ref_scatter (compaction of the tied runs into the next round's list),
-// k_ref_gather (chunk r of the listed rows), k_ref_put (sorted row ids back into place).
+// Kernels: k_ref_adj (round adjacency: D_i, tie flags, D accumulation), k_ref_tile (round-0
+// adjacency fused with the in-tile short runs), k_ref_count / k_ref_scan / k_ref_scatter
+// (compaction of the tied runs into the next round's list), k_ref_local / k_ref_warp /
+// k_ref_cta (short and medium runs), k_ref_keep, k_ref_cta_chunk, k_ref_gather (chunk r of
+// the listed rows), k_ref_put (sorted row ids back into place), k_prefix_sample (T).
 #include <stdlib.h>
 
 #include "cks_internal.h"
