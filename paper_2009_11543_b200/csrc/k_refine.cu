@@ -375,7 +375,7 @@ template <int WC>
 __global__ void __launch_bounds__(kRefThreads, 3)
 k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigned long long cmask, uint32_t nwords,
            bool vec, uint8_t* __restrict__ tie, uint32_t* __restrict__ dacc, uint32_t* __restrict__ handled,
-           uint8_t* __restrict__ any) {
+           uint8_t* __restrict__ any, bool alias) {
     static_assert(WC >= 1 && WC <= 3, "carried remaining words");
     constexpr int NWS = WC;
     constexpr int NWARP = kRefThreads / 32;
@@ -450,8 +450,16 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
         {
 #pragma unroll
             for (int c = 0; c < NWS; c++) {
+                // plane qtop-c: with the chunk planes carried (hi = plane 2, lo = plane 1) the
+                // words of planes 2 and 1 are already in registers
+                const int q = WC - 1 - c;
+                if (alias && (q == 2 || q == 1)) {
+#pragma unroll
+                    for (int j = 0; j < kTileItems; j++) s_w[c][tpad(i0 + j)] = q == 2 ? vh[j] : vl[j];
+                    continue;
+                }
                 uint32_t vw[kTileItems];
-                ld8(R.carried + (uint64_t)(R.qtop - c) * R.pitch, p0, n, vec, vw);
+                ld8(R.carried + (uint64_t)q * R.pitch, p0, n, vec, vw);
 #pragma unroll
                 for (int j = 0; j < kTileItems; j++) s_w[c][tpad(i0 + j)] = vw[j];
             }
@@ -1040,11 +1048,12 @@ cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int
                      (!carried || al(carried));
     if (!carried) return cudaErrorInvalidValue;
     const int wc = qtop + 1;
+    const bool alias = np == 3 && lo == carried + pitch && hi == carried + 2 * pitch;
 #define CKS_TILE_CASE(W)                                                                                        \
     case W:                                                                                                     \
         raise_smem_limit((const void*)k_ref_tile<W>, tile_smem_bytes(W));                                       \
         k_ref_tile<W><<<grid, kRefThreads, tile_smem_bytes(W), st>>>(R, lo, hi, n, cmask, nwords, vec, tie, dacc, \
-                                                                     handled, any);                             \
+                                                                     handled, any, alias);                      \
         break;
     switch (wc) {
         CKS_TILE_CASE(1)
