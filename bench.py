@@ -138,20 +138,52 @@ def traffic_from_profiles(cfg_name: str):
 # ------------------------------------------------------------------------------------------
 # CPU oracle (cpu_baseline and --impl reference): the oracle as it stands, all host cores
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_stages(keys, threads: int) -> dict:
+    """The oracle's first build by stage (SURVEY 8(d) oracle timing): (i) exact D = full-key
+    sort + adjacency, (ii) compress, (iii) compressed sort; plus the bulk load."""
+    import oracle
+    t0 = time.perf_counter()
+    perm = oracle.sort_keys(keys, threads=threads)
+    dbit, mask = oracle.adjacent_dbits(keys, perm)
+    t1 = time.perf_counter()
+    planes = oracle.compress(keys, mask)
+    t2 = time.perf_counter()
+    oracle.sort_packed(planes, threads=threads)
+    t3 = time.perf_counter()
+    oracle.bulkload(perm, dbit, keys, 64, 1.0)
+    t4 = time.perf_counter()
+    return {"exact_D_s": round(t1 - t0, 3), "compress_s": round(t2 - t1, 3), "compressed_sort_s": round(t3 - t2, 3),
+            "bulkload_s": round(t4 - t3, 3), "total_s": round(t4 - t0, 3)}
+
+
 def cpu_baseline(cfg: int, cfg_name: str, sample_n: int):
     import oracle
     threads = oracle.threads_default()
     import cksgen
     keys = cksgen.config(cfg, n=sample_n)
-    t0 = time.perf_counter()
-    ref = oracle.first_build(keys, threads=threads)
-    dt = time.perf_counter() - t0
-    t = oracle.bulkload(ref["perm"], ref["dbit"], keys, 64, 1.0)        # noqa: F841
-    dt_total = time.perf_counter() - t0
+    st = oracle_stages(keys, threads)                       # all cores: __gnu_parallel::sort (P:148)
+    dt_total = st["total_s"]
+    one_n = max(1, sample_n // 8)                           # one core (std::sort) on an eighth
+    st1 = oracle_stages(keys[:one_n], 1)
     return {"value": sample_n / dt_total, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"first {sample_n:,} keys of {cfg_name} (same generator), oracle first build "
                       f"(parallel full-key sort + adjacency + bit-loop compress + packed sort) + bulk load, "
-                      f"{dt_total:.1f} s", "seconds": round(dt_total, 3)}
+                      f"{dt_total:.1f} s", "seconds": round(dt_total, 3),
+            "cores_affinity": len(os.sched_getaffinity(0)), "cpu_model": cpu_model(), "stages": st,
+            "rebuild_keys_per_s": sample_n / (st["compress_s"] + st["compressed_sort_s"] + st["bulkload_s"]),
+            "one_core": {"sample": f"first {one_n:,} keys", "stages": st1,
+                         "value": one_n / st1["total_s"] if st1["total_s"] else None}}
 
 
 def run_reference(args, world, rank):
@@ -266,6 +298,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-full-key", action="store_true", help="skip the full-key comparison (NEXT-2)")
+    ap.add_argument("--no-rebuild", action="store_true", help="skip the rebuild timing (prior mask = D)")
     ap.add_argument("--full-key-steps", type=int, default=3)
     ap.add_argument("--sharded", action="store_true",
                     help="NEXT-4: one global build over all ranks' shards (range partition + all-to-all) "
@@ -365,6 +398,28 @@ def main():
     core_ms = sum(stages[i] for i in range(0, 5))            # mask .. exact D (no packed-D, no tree)
     path_gbs = path_bytes / (core_ms * 1e-3) / 1e9
 
+    # ---- rebuild: the same column rebuilt with the previous exact D as the sort
+    # mask (no superset pass; m = |D|) -- SURVEY 8(d)'s rebuild roofline column
+    rebuild = None
+    if not args.no_rebuild:
+        rb = cks.Builder(n, B, device, fanout=64, fill=1.0)
+        dmask = builder.mask.copy()
+        rb(keys, prior_mask=dmask)
+        torch.cuda.synchronize(device)
+        rs = max(1, min(args.steps, 20))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(rs):
+            rb(keys, prior_mask=dmask)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        rms = max_over_ranks(e0.elapsed_time(e1) / rs, world, device)
+        assert np.array_equal(rb.mask, dmask)
+        rebuild = {"ms_per_step": rms, "value": n * world / (rms * 1e-3), "unit": UNIT, "sort_bits": int(rb.out.sort_bits),
+                   "steps": rs, "formula_bytes_per_key": sum(formula_bytes(B, int(rb.out.sort_bits)).values()) - B}
+        del rb
+
     # ---- e2e: same call with HOST buffers (H2D keys + D2H perm inside the timed region)
     e2e = None
     if not args.no_e2e:
@@ -458,7 +513,7 @@ def main():
                               "achieved_gbs": path_gbs, "frac_of_peak": path_gbs / peak,
                               "frac_of_8tbs": path_gbs / 8000.0},
             "stages_ms": stages_ms,
-            "paper_stats": paper_stats,
+            "paper_stats": paper_stats, "rebuild": rebuild,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
