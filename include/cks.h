@@ -341,6 +341,15 @@ int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
 int cks_build_host(cks_ctx* ctx, const uint8_t* host_keys, uint64_t n, uint32_t key_bytes,
                    const uint8_t* prior_mask, cks_build_out* out);
 
+/* cks_build_host_batch: `count` fused builds of HOST key columns (pinned u8[n][key_bytes]
+ * each, host_keys[i]), pipelined: column i+1 is copied to the device (copy stream) while
+ * column i builds and column i-1's permutation returns (a second copy stream), so the two PCIe
+ * directions and the build overlap; two device key buffers and two permutation buffers are
+ * context-owned. outs[i] as cks_build_host (mask, perm = host u32[n]; dbit and tree NULL);
+ * outs[i].packed is NULL on return. Synchronises at the end. */
+int cks_build_host_batch(cks_ctx* ctx, const uint8_t* const* host_keys, uint32_t count, uint64_t n,
+                         uint32_t key_bytes, const uint8_t* prior_mask, cks_build_out* outs);
+
 #ifdef __cplusplus
 }
 #endif

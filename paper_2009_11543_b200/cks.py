@@ -60,7 +60,8 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_superset_mask", "cks_distinction_mask", "cks_compress", "cks_sort",
            "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_paper_tree_shape", "cks_paper_tree",
            "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
-           "cks_partition", "cks_sort_prefix", "cks_bulkload_block", "cks_bulkload_top"]
+           "cks_partition", "cks_sort_prefix", "cks_bulkload_block", "cks_bulkload_top",
+           "cks_build_host_batch"]
 
 
 def load_library(path: str | None = None):
@@ -106,6 +107,7 @@ def load_library(path: str | None = None):
     L.cks_sort_prefix.argtypes = [p, p, p, u32, u64, p, p, p, ctypes.POINTER(u32), p]
     L.cks_bulkload_block.argtypes = [p, p, p, u64, u32, f32, i32, u32, ctypes.POINTER(Tree), p, ctypes.POINTER(u32)]
     L.cks_bulkload_top.argtypes = [p, p, p, u64, u32, f32, ctypes.POINTER(Tree), ctypes.POINTER(u32)]
+    L.cks_build_host_batch.argtypes = [p, p, u32, u64, u32, p, p]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or i32
     _lib = L
@@ -518,6 +520,33 @@ def build(keys: torch.Tensor, prior_mask=None, fanout: int = 64, fill: float = 1
     return dict(mask=b.mask.copy(), popcount=int(o.popcount), sort_bits=int(o.sort_bits), passes=int(o.passes),
                 perm=b.perm[:n], dbit=b.dbit[:n] if b.dbit is not None else None, packed=b.packed(),
                 tree=b.tree, shape=b.shape, height=int(o.height))
+
+
+def build_host_batch(columns: list, prior_mask=None, superset_kind: int = SUPERSET_BYTEOCC,
+                     perms: list | None = None, device: int | None = None) -> list[dict]:
+    """Pipelined fused builds of several HOST key columns (numpy uint8 [n, B] each, same shape,
+    ideally pinned): copies, builds and result copies overlap (cks_build_host_batch)."""
+    cols = [np.ascontiguousarray(c) for c in columns]
+    if not cols:
+        return []
+    n, B = cols[0].shape
+    if any(c.dtype != np.uint8 or c.shape != (n, B) for c in cols):
+        raise ValueError("columns must be uint8 [n, B] of one shape")
+    L, c = _context(device)
+    k = len(cols)
+    masks = [np.zeros(B, np.uint8) for _ in range(k)]
+    perms = perms if perms is not None else [np.empty(n, np.uint32) for _ in range(k)]
+    outs = (BuildOut * k)()
+    for i in range(k):
+        outs[i].mask = masks[i].ctypes.data
+        outs[i].perm = perms[i].ctypes.data
+        outs[i].superset_kind = superset_kind
+        outs[i].fanout, outs[i].fill = 64, 1.0
+    ptrs = (ctypes.c_void_p * k)(*[x.ctypes.data if n else None for x in cols])
+    pm = None if prior_mask is None else _host_mask(prior_mask, B)
+    _check(L, c, L.cks_build_host_batch(c, ptrs, k, n, B, None if pm is None else pm.ctypes.data, outs))
+    return [dict(mask=masks[i], popcount=int(outs[i].popcount), sort_bits=int(outs[i].sort_bits), perm=perms[i])
+            for i in range(k)]
 
 
 def build_host(host_keys: np.ndarray, prior_mask=None, superset_kind: int = SUPERSET_BYTEOCC,

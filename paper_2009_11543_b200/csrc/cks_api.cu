@@ -32,6 +32,8 @@ struct cks_ctx {
     int sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t d2h_stream = nullptr;    // cks_build_host_batch: results back while the next copies in
+    cudaEvent_t bev[6] = {};              // cks_build_host_batch: keys in / build done / perm out, x2
     cudaStream_t aux_stream = nullptr;   // partial tail tile of an LSD pass
     cudaEvent_t aux_ev[2] = {};
     // dominant-kernel timing (cks_ctx_kernel_stats): event pairs around each warp-specialised
@@ -51,7 +53,8 @@ struct cks_ctx {
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
         pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, runoff2, runpos2, tie, keep, done, mlist, wlist, rcnt, rtot,   // NEXT-1
         part_in, part_out,                                                 // NEXT-4
-        anyt;                                                              // k_ref_tile: tiles with ties left
+        anyt,                                                              // k_ref_tile: tiles with ties left
+        keys2, perm2;                                                      // cks_build_host_batch: 2nd buffers
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
     uint16_t* h_moff = nullptr;
@@ -840,6 +843,8 @@ int cks_ctx_create(int device, void* stream, cks_ctx** out) {
     }
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     bool ok = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+    if (ok) ok = cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; i < 6 && ok; i++) ok = cudaEventCreateWithFlags(&ctx->bev[i], cudaEventDisableTiming) == cudaSuccess;
     if (ok) ok = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; i < 2 && ok; i++) ok = cudaEventCreateWithFlags(&ctx->aux_ev[i], cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < 2 * cks_ctx::kMaxKev && ok; i++) ok = cudaEventCreate(&ctx->kev[i]) == cudaSuccess;
@@ -884,6 +889,9 @@ int cks_ctx_destroy(cks_ctx* ctx) {
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+    for (int i = 0; i < 6; i++)
+        if (ctx->bev[i]) cudaEventDestroy(ctx->bev[i]);
     if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
     for (int i = 0; i < 2; i++)
         if (ctx->aux_ev[i]) cudaEventDestroy(ctx->aux_ev[i]);
@@ -1309,6 +1317,63 @@ int cks_build_host(cks_ctx* ctx, const uint8_t* host_keys, uint64_t n, uint32_t 
     if (rc != CKS_OK) return rc;
     o.perm = host_perm;
     *out = o;
+    return CKS_OK;
+}
+
+int cks_build_host_batch(cks_ctx* ctx, const uint8_t* const* host_keys, uint32_t count, uint64_t n, uint32_t B,
+                         const uint8_t* prior, cks_build_out* outs) {
+    if (!ctx) return CKS_EINVAL;
+    if (count == 0) return CKS_OK;
+    if (!host_keys || !outs) return fail(ctx, CKS_EINVAL, "NULL host_keys or outs");
+    for (uint32_t i = 0; i < count; i++) {
+        TRY(check_keys(ctx, host_keys[i], n, B));
+        if (!outs[i].mask || (n && !outs[i].perm)) return fail(ctx, CKS_EINVAL, "NULL output (column %u)", i);
+        if (outs[i].dbit || outs[i].tree.node_cnt) return fail(ctx, CKS_EINVAL, "batch: dbit/tree must be NULL");
+    }
+    CK(cudaSetDevice(ctx->device));
+    const size_t bytes = (size_t)n * B;
+    TRY(ensure(ctx, ctx->keys, bytes));
+    TRY(ensure(ctx, ctx->keys2, bytes));
+    TRY(ensure(ctx, ctx->perm_scratch, n * 4 + 16));
+    TRY(ensure(ctx, ctx->perm2, n * 4 + 16));
+    uint8_t* kb[2] = {as<uint8_t>(ctx->keys), as<uint8_t>(ctx->keys2)};
+    uint32_t* pb[2] = {as<uint32_t>(ctx->perm_scratch), as<uint32_t>(ctx->perm2)};
+    cudaEvent_t* in_ev = ctx->bev;          // [2] keys of column i in kb[i & 1]
+    cudaEvent_t* done_ev = ctx->bev + 2;    // [2] build of the column in buffer b finished
+    cudaEvent_t* out_ev = ctx->bev + 4;     // [2] perm of buffer b copied out
+    // the copy of column i+1 runs (copy stream) while column i builds (library stream) and
+    // column i-1's permutation goes back (d2h stream): H2D and D2H use both PCIe directions
+    auto copy_in = [&](uint32_t i) -> int {
+        const int b = (int)(i & 1);
+        if (i >= 2) CK(cudaStreamWaitEvent(ctx->copy_stream, done_ev[b], 0));    // kb[b] free
+        if (bytes) CK(cudaMemcpyAsync(kb[b], host_keys[i], bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+        CK(cudaEventRecord(in_ev[b], ctx->copy_stream));
+        return CKS_OK;
+    };
+    TRY(copy_in(0));
+    for (uint32_t i = 0; i < count; i++) {
+        const int b = (int)(i & 1);
+        if (i + 1 < count) TRY(copy_in(i + 1));
+        CK(cudaStreamWaitEvent(ctx->stream, in_ev[b], 0));
+        if (i >= 2) CK(cudaStreamWaitEvent(ctx->stream, out_ev[b], 0));             // pb[b] free
+        ctx->timed = ctx->timing;
+        ctx->nkev = 0;
+        mark(ctx, ST_BEGIN);
+        cks_build_out o = outs[i];
+        o.perm = pb[b];
+        TRY(build_common(ctx, kb[b], n, B, prior, &o, /*keys_ready_for_mask=*/true));
+        CK(cudaEventRecord(done_ev[b], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->d2h_stream, done_ev[b], 0));
+        if (n) CK(cudaMemcpyAsync(outs[i].perm, pb[b], n * 4, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+        CK(cudaEventRecord(out_ev[b], ctx->d2h_stream));
+        uint32_t* host_perm = outs[i].perm;
+        outs[i] = o;
+        outs[i].perm = host_perm;
+        outs[i].packed = nullptr;                  // (device views of a reused buffer: not returned)
+    }
+    CK(cudaStreamSynchronize(ctx->d2h_stream));
+    CK(cudaStreamSynchronize(ctx->copy_stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return CKS_OK;
 }
 

@@ -456,3 +456,15 @@ def test_refine_forced_round0_width(T, m, tmp_path):
     r = dict(mask=z["mask"], popcount=int(z["popcount"]), perm=torch.from_numpy(z["perm"]),
              dbit=torch.from_numpy(z["dbit"]), packed=torch.from_numpy(z["packed"]), tree=None)
     check_build(keys, r)
+
+
+def test_build_host_batch_pipelined():
+    # cks_build_host_batch: three different columns through the double-buffered pipeline
+    cols = [cksgen.config(5, n=150_001, seed=s) for s in (11, 12, 13)]
+    rs = cks.build_host_batch(cols)
+    for keys, r in zip(cols, rs):
+        ref = oracle.first_build(keys)
+        assert np.array_equal(r["mask"], ref["mask"])
+        assert np.array_equal(r["perm"], ref["perm"])
+    one = cks.build_host_batch(cols[:1])                       # a batch of one
+    assert np.array_equal(one[0]["perm"], rs[0]["perm"])
