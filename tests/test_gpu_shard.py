@@ -2,6 +2,8 @@
 kernels, G ranks run as threads on cuda:0 (each with its own stream and context; no kernel
 waits on another rank), slices concatenated and compared with the oracle's single build bit
 for bit: permutation, D_i, exact D, P_D and the bulk-loaded tree."""
+import os
+
 import numpy as np
 import pytest
 
@@ -101,3 +103,41 @@ def test_sort_prefix_on_given_planes(cfg):
     assert np.array_equal(PD.cpu().numpy().view(np.uint32), ref["planes"][:, ref["perm"]])
     o2, d2, D2, none = cks.sort_prefix(P, M)                  # without P_D
     assert none is None and np.array_equal(o2.cpu().numpy(), order.cpu().numpy()) and np.array_equal(D2, D)
+
+
+_NCCL_SCRIPT = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+import cksgen
+from paper_2009_11543_b200 import shard
+dist.init_process_group("nccl", rank=0, world_size=1)
+torch.cuda.set_device(0)
+keys = cksgen.config(5, n=100_003)
+o = shard.build_sharded(torch.from_numpy(keys).cuda(), shard.TorchComm())
+np.savez(sys.argv[1], perm=o["perm"].cpu().numpy(), dbit=o["dbit"].cpu().numpy(), mask=o["mask"],
+         packed=o["packed"].cpu().numpy())
+dist.destroy_process_group()
+"""
+
+
+def test_sharded_over_nccl_world1(tmp_path):
+    # the TorchComm path on NCCL collectives (one rank: all_gather / all_to_all_single of itself)
+    import socket
+    import subprocess
+    import sys
+    import oracle
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    out = tmp_path / "r.npz"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", _NCCL_SCRIPT, str(out)], env=env, cwd=root, check=True, timeout=300)
+    z = np.load(out)
+    keys = cksgen.config(5, n=100_003)
+    ref = oracle.first_build(keys)
+    assert np.array_equal(z["perm"].view(np.uint32), ref["perm"])
+    assert np.array_equal(z["dbit"].view(np.uint16), ref["dbit"])
+    assert np.array_equal(z["mask"], ref["mask"])
+    assert np.array_equal(z["packed"].view(np.uint32), ref["planes"][:, ref["perm"]])
