@@ -141,3 +141,17 @@ def test_sharded_over_nccl_world1(tmp_path):
     assert np.array_equal(z["dbit"].view(np.uint16), ref["dbit"])
     assert np.array_equal(z["mask"], ref["mask"])
     assert np.array_equal(z["packed"].view(np.uint32), ref["planes"][:, ref["perm"]])
+
+
+def test_sharded_variant_superset():
+    # the union of occupancies also yields V (cks_occupancy_mask, CKS_SUPERSET_VARIANT)
+    from paper_2009_11543_b200 import cks
+    keys = cksgen.config(3, n=60_000)
+    outs = run(keys, [30_000, 30_000], superset_kind=cks.SUPERSET_VARIANT)
+    assert outs[0]["sort_bits"] == int(np.unpackbits(oracle_variant(keys)).sum())
+    check_slices(keys, outs)
+
+
+def oracle_variant(keys):
+    import oracle
+    return oracle.variant_bitmap(keys)
