@@ -468,3 +468,25 @@ def test_build_host_batch_pipelined():
         assert np.array_equal(r["perm"], ref["perm"])
     one = cks.build_host_batch(cols[:1])                       # a batch of one
     assert np.array_equal(one[0]["perm"], rs[0]["perm"])
+
+
+@pytest.mark.parametrize("B", [5, 13, 24, 100, 255])
+def test_build_odd_widths(B):
+    # the fused build on key widths off the specialised paths (generic occupancy / compress),
+    # past the sample threshold (n >= 65536) and with duplicate rows
+    rng = np.random.default_rng(B)
+    n = 70_001
+    keys = rng.integers(0, 256, (n, B), dtype=np.uint8)
+    keys[:, : min(B, 3)] = rng.integers(0, 4, (n, min(B, 3)), dtype=np.uint8)      # shared prefixes
+    dup = rng.integers(0, n, 2000)
+    keys[rng.integers(0, n, 2000)] = keys[dup]
+    check_build(keys, cks.build(dev(keys)))
+
+
+def test_build_unaligned_keys():
+    # a key column that starts 3 bytes into its buffer (no 16-byte vector paths)
+    keys = cksgen.config(3, n=50_001)
+    buf = torch.zeros(keys.size + 3, dtype=torch.uint8, device="cuda")
+    view = buf[3:].view(keys.shape[0], keys.shape[1])
+    view.copy_(dev(keys))
+    check_build(keys, cks.build(view))
