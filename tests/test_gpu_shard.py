@@ -155,3 +155,11 @@ def test_sharded_variant_superset():
 def oracle_variant(keys):
     import oracle
     return oracle.variant_bitmap(keys)
+
+
+def test_sharded_odd_width():
+    rng = np.random.default_rng(13)
+    keys = rng.integers(0, 256, (40_001, 13), dtype=np.uint8)
+    keys[:, :2] = rng.integers(0, 3, (40_001, 2), dtype=np.uint8)
+    keys[rng.integers(0, 40_001, 500)] = keys[rng.integers(0, 40_001, 500)]
+    check_slices(keys, run(keys, [10_000, 20_001, 10_000]))
