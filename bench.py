@@ -7,9 +7,10 @@ a4 histograms -> a5 LSD passes -> a6 adjacency (exact D) -> a7 repack -> a8 bulk
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
-N > 1 runs under torchrun (one process per GPU): replicas only -- each rank builds its own
-copy of the workload (the sort does not shard without an exchange step),
-weak scaling, value = all keys processed / max-over-ranks time. Rank 0 prints one JSON line.
+N > 1 runs under torchrun (one process per GPU) as the sharded build (NEXT-4, DESIGN.md
+Sec. 7): every rank holds a full-size shard and the ranks build ONE index over the union with
+one all-to-all exchange; weak scaling, value = all keys / max-over-ranks time. `--replicas`
+runs independent per-rank builds instead. Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -269,6 +270,28 @@ def run_sharded(args, world, rank, local):
     peak, peak_src = measured_peaks()
     achieved = (k_bytes / (k_ms * 1e-3) / 1e9) if k_ms > 0 else None
     slice_max = max_over_ranks(float(out["perm"].numel()), world, device)
+    # e2e through the same public call: every step copies this rank's shard in from pinned host
+    # memory and its slice of the permutation back out (host wall clock, max over ranks)
+    e2e = None
+    if not args.no_e2e:
+        steps_e = max(1, args.e2e_steps)
+        perm_h = torch.empty(n + n // 2 + 1024, dtype=torch.int32, pin_memory=True)
+        barrier(world)
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(steps_e):
+            keys.copy_(host, non_blocking=True)
+            o = shard.build_sharded(keys, comm)
+            k = int(o["perm"].numel())
+            perm_h[:k].copy_(o["perm"], non_blocking=True)
+            torch.cuda.synchronize(device)
+            d2h = k * 4 + B
+        dt = max_over_ranks((time.perf_counter() - t0) / steps_e, world, device)
+        e2e = {"value": n * world / dt, "unit": UNIT, "h2d_bytes_per_step": n * B, "d2h_bytes_per_step": d2h,
+               "ms_per_step": dt * 1e3, "steps": steps_e,
+               "timing": "host wall clock per step (H2D of the rank's shard, sharded build, D2H of its slice), "
+                         "max over ranks; byte counts are rank 0's"}
     if rank == 0:
         line = {"metric": METRIC, "value": n * world / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -280,7 +303,7 @@ def run_sharded(args, world, rank, local):
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": (achieved / peak) if (achieved and peak) else None, "traffic": None,
                              "kernel": "k_downsweep_ws (warp-specialised LSD digit pass)", "peak_source": peak_src},
-                "cpu_baseline": None, "e2e": None, "gpu_launches": gpu_launches, "clocks": clk}
+                "cpu_baseline": None, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk}
         print(json.dumps(line), flush=True)
 
 
@@ -302,12 +325,16 @@ def main():
     ap.add_argument("--full-key-steps", type=int, default=3)
     ap.add_argument("--sharded", action="store_true",
                     help="NEXT-4: one global build over all ranks' shards (range partition + all-to-all) "
-                         "instead of one independent build per rank")
+                         "instead of one independent build per rank (the default when N > 1)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent per-rank builds (no exchange) instead of the sharded build")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3                                     # contract: W >= 3
 
     world, rank, local = dist_setup(args)
+    if world > 1 and not args.replicas:
+        args.sharded = True
     if args.sharded and args.impl == "ours":
         run_sharded(args, world, rank, local)
         if world > 1:
@@ -365,9 +392,11 @@ def main():
     # so the other builds run back to back as a user's would
     every = max(1, args.steps // 10)
     sampled = 0
+    pbytes = []
     for i in range(args.steps):
         builder(keys)
         if (i + 1) % every == 0:
+            pbytes.append(cks.path_bytes())
             st = cks.stage_ms()                              # events on the library's stream
             stage_acc = st if stage_acc is None else [a + b for a, b in zip(stage_acc, st)]
             kms, kby, kc = cks.kernel_stats()                # the dominant kernel's own events
@@ -397,6 +426,9 @@ def main():
     path_bytes = sum(fbytes.values()) * n
     core_ms = sum(stages[i] for i in range(0, 5))            # mask .. exact D (no packed-D, no tree)
     path_gbs = path_bytes / (core_ms * 1e-3) / 1e9
+    # the work actually run: algorithmic bytes of every kernel of a build (cks_ctx_path_bytes)
+    actual_bytes = statistics.median(pbytes) if pbytes else None
+    total_ms = stages[7]
 
     # ---- rebuild: the same column rebuilt with the previous exact D as the sort
     # mask (no superset pass; m = |D|) -- SURVEY 8(d)'s rebuild roofline column
@@ -404,8 +436,18 @@ def main():
     if not args.no_rebuild:
         rb = cks.Builder(n, B, device, fanout=64, fill=1.0)
         dmask = builder.mask.copy()
-        rb(keys, prior_mask=dmask)
+        rb(keys, prior_mask=dmask)                          # (default: checked against the rows)
         torch.cuda.synchronize(device)
+        vs = max(1, min(args.steps, 10))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(vs):
+            rb(keys, prior_mask=dmask)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        vms = max_over_ranks(e0.elapsed_time(e1) / vs, world, device)
+        cks.set_verify(cks.VERIFY_OFF)                       # the paper's rebuild: no order check
         rs = max(1, min(args.steps, 20))
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -415,8 +457,11 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(device)
         rms = max_over_ranks(e0.elapsed_time(e1) / rs, world, device)
+        cks.set_verify(cks.VERIFY_PRIOR)
         assert np.array_equal(rb.mask, dmask)
-        rebuild = {"ms_per_step": rms, "value": n * world / (rms * 1e-3), "unit": UNIT, "sort_bits": int(rb.out.sort_bits),
+        rebuild = {"ms_per_step": rms, "verified_ms_per_step": vms,
+                   "note": "ms_per_step: the paper's rebuild (P:405-411), order check off; verified: with the "
+                           "default order check of a prior mask against the key rows (cks_ctx_set_verify)", "value": n * world / (rms * 1e-3), "unit": UNIT, "sort_bits": int(rb.out.sort_bits),
                    "steps": rs, "formula_bytes_per_key": sum(formula_bytes(B, int(rb.out.sort_bits)).values()) - B}
         del rb
 
@@ -455,26 +500,40 @@ def main():
                        "compressed_sort_key_bytes": comp_sort_key,
                        "sort_key_ratio": full_sort_key / comp_sort_key if comp_sort_key else None,
                        "definitions": "P:523-526 (Table 2), P:559-563; total ratio as Table 6 (P:689-706)"}
-        cks.set_sort_mode(cks.SORT_SINGLE)
         allbits = np.full(B, 0xFF, np.uint8)
-        full = cks.Builder(n, B, device, fanout=64, fill=1.0)
-        full(keys, prior_mask=allbits)
-        torch.cuda.synchronize(device)
         fs = max(1, min(args.steps, args.full_key_steps))
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(fs):
-            full(keys, prior_mask=allbits)
-        e1.record(stream)
-        torch.cuda.synchronize(device)
+        cks.set_verify(cks.VERIFY_OFF)                 # (all key bits: a superset by definition)
+
+        def timed_build(bld, prior, mode):
+            cks.set_sort_mode(mode)
+            bld(keys, prior_mask=prior)
+            torch.cuda.synchronize(device)
+            e0.record(stream)
+            for _ in range(fs):
+                bld(keys, prior_mask=prior)
+            e1.record(stream)
+            torch.cuda.synchronize(device)
+            return e0.elapsed_time(e1) / fs, int(bld.out.passes)
+        full = cks.Builder(n, B, device, fanout=64, fill=1.0)
+        comp = cks.Builder(n, B, device, fanout=64, fill=1.0)
+        # Table 6 compares the SAME sort on full and on compressed keys: both legs
+        # run each sort mode; the full-key leg sorts M = every key bit, the compressed one M = D+
+        f_single, fp_single = timed_build(full, allbits, cks.SORT_SINGLE)
+        c_single, cp_single = timed_build(comp, None, cks.SORT_SINGLE)
+        f_prefix, fp_prefix = timed_build(full, allbits, cks.SORT_PREFIX)
         cks.set_sort_mode(cks.SORT_PREFIX_AUTO)
-        fms = e0.elapsed_time(e1) / fs
-        assert np.array_equal(full.mask, builder.mask)                  # same exact D either way
-        paper_stats.update({"full_key_ms_per_step": fms, "full_key_passes": int(full.out.passes),
-                            "compressed_ms_per_step": ms, "total_ratio": fms / ms, "full_key_steps": fs,
-                            "full_key_keys_per_s": n / (fms * 1e-3)})
-        del full
+        cks.set_verify(cks.VERIFY_PRIOR)
+        assert np.array_equal(full.mask, builder.mask) and np.array_equal(comp.mask, builder.mask)
+        paper_stats.update({
+            "single_sort": {"full_key_ms": f_single, "full_key_passes": fp_single, "compressed_ms": c_single,
+                            "compressed_passes": cp_single, "total_ratio": f_single / c_single},
+            "by_prefixes": {"full_key_ms": f_prefix, "full_key_passes": fp_prefix, "compressed_ms": ms,
+                            "compressed_passes": passes, "total_ratio": f_prefix / ms},
+            "total_ratio_note": "Table 6 (P:689-706): the same sort on full keys (M = all key bits) and on "
+                                "compressed keys (M = D+), per sort mode; steps per leg: %d" % fs})
+        del full, comp
         # NEXT-3: the paper's 256-byte-node index tree from this build's perm and D_i (pk = 32)
         ps = cks.paper_tree_shape(n, 0.9)
         nodes = torch.empty((int(ps.total_nodes), cks.PTREE_NODE_BYTES), dtype=torch.uint8, device=device)
@@ -514,10 +573,18 @@ def main():
                          "sampled_steps": sampled,
                          "algorithmic_bytes_per_launch": (k_bytes / k_count) if k_count else None,
                          "traffic_source": traffic_src, "traffic_launch_algorithmic_bytes": traffic_alg},
-            "path_roofline": {"formula": "SURVEY 8(d): mask + compress + k full-width LSD passes + adjacency",
-                              "formula_bytes_per_key": fbytes, "mask_to_exact_D_ms": core_ms,
-                              "achieved_gbs": path_gbs, "frac_of_peak": path_gbs / peak,
-                              "frac_of_8tbs": path_gbs / 8000.0},
+            "path_roofline": {
+                "actual_bytes_per_key": actual_bytes / n if actual_bytes else None,
+                "actual_gbs": actual_bytes / (total_ms * 1e-3) / 1e9 if actual_bytes else None,
+                "actual_frac_of_peak": actual_bytes / (total_ms * 1e-3) / 1e9 / peak if actual_bytes else None,
+                "actual_note": "sum of the algorithmic bytes of every kernel one build launched "
+                               "(cks_ctx_path_bytes; DESIGN.md Sec. 6) / the whole build's time (a1..a8)",
+                "effective_formula": "SURVEY 8(d): mask + compress + k full-width LSD passes + adjacency; the "
+                                     "build sorts by distinguishing prefixes and moves fewer bytes, so this is an "
+                                     "effective speed-up over a full-width sort, not a roofline fraction",
+                "formula_bytes_per_key": fbytes, "mask_to_exact_D_ms": core_ms,
+                "effective_gbs": path_gbs, "effective_frac_of_peak": path_gbs / peak,
+                "effective_frac_of_8tbs": path_gbs / 8000.0},
             "stages_ms": stages_ms,
             "paper_stats": paper_stats, "rebuild": rebuild,
             "cpu_baseline": cpu,

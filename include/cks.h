@@ -31,9 +31,14 @@
  *              CKS_EINVAL  null pointer with n > 0, key_bytes not in [1, 512],
  *                          fanout < 2, fill not in (0, 1], floor(fanout*fill) < 2,
  *                          bits > 8*512, unknown kind;
- *              CKS_ERANGE  n >= 2^32 (row ids are u32), or a prior mask that is not
- *                          a superset of the true distinction bits (detected when
- *                          the sorted order contradicts it);
+ *              CKS_ERANGE  n >= 2^32 (row ids are u32); or, from cks_build /
+ *                          cks_build_host[_batch] / cks_distinction_mask with the order
+ *                          check on (cks_ctx_set_verify; by default whenever a prior mask
+ *                          is passed), a sort mask that is not a superset of the true
+ *                          distinction bits: Theorem 2 then does not hold and
+ *                          the check finds an adjacent pair of the returned order out of
+ *                          (key, row id) order. With the check off such a mask yields a
+ *                          wrong permutation without an error;
  *              CKS_ENOMEM  scratch allocation failed;
  *              CKS_ECUDA   a CUDA runtime error (text in cks_last_error).
  *            Duplicated keys are NOT an error (reading R3). n = 0 is a valid no-op.
@@ -77,12 +82,28 @@ int cks_ctx_set_timing(cks_ctx* ctx, int enable);
 /* How cks_build / cks_distinction_mask sort (the result is the same):
  *   CKS_SORT_SINGLE       one stable LSD sort over all m = |M| bits of P_M;
  *   CKS_SORT_PREFIX_AUTO  by distinguishing prefixes (NEXT-1) when m > 64 (default);
- *   CKS_SORT_PREFIX       by distinguishing prefixes whenever m > 0.
- * The environment variable CKS_REFINE (0/1/2) sets the initial mode of new contexts. */
+ *   CKS_SORT_PREFIX       by distinguishing prefixes whenever m > 0. */
 #define CKS_SORT_SINGLE 0
 #define CKS_SORT_PREFIX_AUTO 1
 #define CKS_SORT_PREFIX 2
 int cks_ctx_set_sort_mode(cks_ctx* ctx, int mode);
+/* Width T of the first refinement round: 0 = chosen from a sample
+ * (default), else a multiple of 8 in [8, 64]. The result does not depend on T (CKS_EINVAL
+ * otherwise). */
+int cks_ctx_set_round0_bits(cks_ctx* ctx, uint32_t bits);
+/* Order check of cks_build / cks_build_host[_batch] / cks_distinction_mask results against the
+ * key rows (one random row gather per key; returns CKS_ERANGE on a pair out of order, see
+ * ERRORS). The paper's rebuild extracts with the current D-bitmap, which is only
+ * correct while it contains every distinction bit; the check is complete because
+ * the (key, row id) order is total and a sequence is sorted iff every adjacent pair is.
+ *   CKS_VERIFY_OFF     never;
+ *   CKS_VERIFY_PRIOR   when the caller passes a prior mask (default; the library's own
+ *                      superset masks contain D by construction, reading R2);
+ *   CKS_VERIFY_ALWAYS  every build. */
+#define CKS_VERIFY_OFF 0
+#define CKS_VERIFY_PRIOR 1
+#define CKS_VERIFY_ALWAYS 2
+int cks_ctx_set_verify(cks_ctx* ctx, int mode);
 /* Stage times (ms) of the last timed cks_build: a1 mask, a3 compress, a4 histograms+scan,
  * a5 LSD passes, a6 adjacency, a7 repack, a8 bulk load, total. Synchronises. Returns the
  * count written (0 if timing was off). */
@@ -94,6 +115,12 @@ uint64_t cks_ctx_launches(const cks_ctx* ctx);
  * algorithmic bytes (every stream of the pass read once and written once) and the number
  * of launches. Synchronises. Zeros when timing was off. */
 int cks_ctx_kernel_stats(cks_ctx* ctx, double* ms, double* bytes, uint32_t* count);
+/* Algorithmic bytes of the last cks_build / cks_build_host / cks_sort_prefix on this context:
+ * the sum over every kernel it launched of the bytes that kernel must read and write at least
+ * (each input stream read once, each output written once; DESIGN.md Sec. 6 lists the per-kernel
+ * formulas). With the build's time this is the whole path's roofline, on the work actually
+ * run (not on a formula for a full-width sort). Host-side, no synchronisation. */
+int cks_ctx_path_bytes(const cks_ctx* ctx, double* bytes);
 const char* cks_strerror(int code);
 const char* cks_last_error(const cks_ctx* ctx);
 
@@ -109,7 +136,8 @@ int cks_superset_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t ke
 /* ---- exact D (first build; rebuild recompute) ------------------------
  * Exact distinction bits D = {D_1..D_{n}} over the sorted order (Theorem 1).
  * Runs: superset mask (or `prior_mask`, host u8[key_bytes], which MUST be a superset of
- * D, e.g. the previous D-bitmap) -> compress -> ONE stable sort -> adjacency.
+ * D, e.g. the previous D-bitmap; checked by default, CKS_ERANGE when it is not, see
+ * cks_ctx_set_verify) -> compress -> ONE stable sort -> adjacency.
  * If perm_out (device u32[n]) is non-NULL it receives the permutation of that same sort.
  * mask_out: host u8[key_bytes]; popcount_out: host, may be NULL. Synchronises. */
 int cks_distinction_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
@@ -236,12 +264,12 @@ typedef struct {
 } cks_tree;
 
 /* Host-only arithmetic; no context needed. */
-int cks_bulkload_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* out);
+int cks_bulkload_shape(uint64_t n, uint32_t fanout, double fill, cks_tree_shape* out);
 
 /* perm: device u32[n] (sorted row ids); dbit: device u16[n] D_i or NULL (then leaf and
  * inner D-bits are not produced: entry_dbit must be NULL too). Asynchronous. */
 int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n,
-                 uint32_t fanout, float fill, const cks_tree* out);
+                 uint32_t fanout, double fill, const cks_tree* out);
 
 /* ---- NEXT-3: the paper's index tree format (Sec. 4.2; Sec. 5.3) -------
  * Nodes of 256 bytes, leaves first then each level up, numbered from 0; a node holds
@@ -266,9 +294,9 @@ int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
 #define CKS_PTREE_NODE_BYTES 256
 #define CKS_PTREE_LEAF_FANOUT 14
 #define CKS_PTREE_INNER_FANOUT 9
-int cks_paper_tree_shape(uint64_t n, float fill, cks_tree_shape* out);
+int cks_paper_tree_shape(uint64_t n, double fill, cks_tree_shape* out);
 int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, const uint32_t* perm,
-                   const uint16_t* dbit, uint32_t pk_bits, float fill, uint8_t* nodes);
+                   const uint16_t* dbit, uint32_t pk_bits, double fill, uint8_t* nodes);
 
 /* ---- P:502 block-parallel bulk load (the sharded path's a8, NEXT-4) ----------------------
  * "n sort keys are divided into p blocks ... thread i constructs a subtree consisting of all
@@ -283,7 +311,7 @@ int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_b
  * block). top_min_out: device u16[nodes of the top built level] = minimum D_k under each of
  * those nodes (input of the merge), or NULL. height_out: levels built. Asynchronous. */
 int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
-                       float fill, int first_global, uint32_t levels, cks_tree* out, uint16_t* top_min_out,
+                       double fill, int first_global, uint32_t levels, cks_tree* out, uint16_t* top_min_out,
                        uint32_t* height_out);
 
 /* cks_bulkload_top: the merged top over nchild child nodes = the blocks' top built levels
@@ -296,7 +324,7 @@ int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit,
  * nchild <= 1 builds nothing (the one child is the root). height_out: levels built.
  * Asynchronous. */
 int cks_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* child_min, uint64_t nchild,
-                     uint32_t fanout, float fill, cks_tree* out, uint32_t* height_out);
+                     uint32_t fanout, double fill, cks_tree* out, uint32_t* height_out);
 
 /* ---- fused first build: a1 -> a2 -> a3 -> a4 -> a5 -> a6 -> a7 -> a8 -----------------------
  * The benchmarked step. The superset mask M (or prior_mask) is compressed once; the sort
@@ -305,8 +333,9 @@ int cks_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* ch
  * with a neighbour are re-sorted by (run, next 64 bits), round after round. A pair's D-bit
  * comes from the round that separates it, so the exact D and the D_i fall out of the sort;
  * P_D in sorted order is then compressed from the key rows (or repacked from the sorted
- * chunk when one chunk held all of P_M); bulk load. Environment CKS_REFINE=0 selects the
- * plain single sort over all m bits (one adjacency pass, repack skipped when M = D). */
+ * chunk when one chunk held all of P_M); bulk load. cks_ctx_set_sort_mode(CKS_SORT_SINGLE)
+ * selects the plain single sort over all m bits (one adjacency pass, repack skipped when
+ * M = D). */
 typedef struct {
     /* inputs (caller-owned buffers) */
     uint8_t* mask;            /* host u8[key_bytes]: receives exact D */
@@ -314,7 +343,7 @@ typedef struct {
     uint16_t* dbit;           /* device u16[n] or NULL (library scratch is used) */
     cks_tree tree;            /* device arrays, or node_cnt == NULL to skip the bulk load */
     uint32_t fanout;          /* bulk load fanout (>= 2) */
-    float fill;               /* bulk load fill in (0, 1] */
+    double fill;               /* bulk load fill in (0, 1] */
     int superset_kind;        /* CKS_SUPERSET_BYTEOCC (default) or CKS_SUPERSET_VARIANT */
     /* outputs */
     uint32_t popcount;        /* |D| */
@@ -329,8 +358,11 @@ typedef struct {
 } cks_build_out;
 
 /* keys: device u8[n][key_bytes]; prior_mask: host u8[key_bytes] superset or NULL.
+ * A prior mask must contain every distinction bit of THIS column (e.g. the D-bitmap of the
+ * last build when no key was inserted since); with the default order check a mask
+ * that does not returns CKS_ERANGE (see cks_ctx_set_verify).
  * Synchronises: after the superset mask, once per refinement round (to size the next
- * round) and after the exact D is known. */
+ * round), after the exact D is known, and after the order check when it runs. */
 int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
               const uint8_t* prior_mask, cks_build_out* out);
 

@@ -48,7 +48,7 @@ class Tree(ctypes.Structure):
 
 class BuildOut(ctypes.Structure):
     _fields_ = [("mask", ctypes.c_void_p), ("perm", ctypes.c_void_p), ("dbit", ctypes.c_void_p),
-                ("tree", Tree), ("fanout", ctypes.c_uint32), ("fill", ctypes.c_float),
+                ("tree", Tree), ("fanout", ctypes.c_uint32), ("fill", ctypes.c_double),
                 ("superset_kind", ctypes.c_int), ("popcount", ctypes.c_uint32),
                 ("sort_bits", ctypes.c_uint32), ("height", ctypes.c_uint32), ("passes", ctypes.c_uint32),
                 ("packed", ctypes.c_void_p), ("packed_pitch", ctypes.c_uint64),
@@ -61,7 +61,8 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_adjacent_dbits", "cks_bulkload_shape", "cks_bulkload", "cks_paper_tree_shape", "cks_paper_tree",
            "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
            "cks_partition", "cks_sort_prefix", "cks_bulkload_block", "cks_bulkload_top",
-           "cks_build_host_batch"]
+           "cks_build_host_batch", "cks_ctx_set_round0_bits", "cks_ctx_set_verify",
+           "cks_ctx_path_bytes"]
 
 
 def load_library(path: str | None = None):
@@ -73,12 +74,16 @@ def load_library(path: str | None = None):
     if not os.path.exists(path):
         raise RuntimeError(f"libcks.so not found at {path}; build it with `python __graft_entry__.py build`")
     L = ctypes.CDLL(path)
-    p, u64, u32, i32, f32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_float
+    p, u64, u32, i32, f32, f64 = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_float,
+                                  ctypes.c_double)
     L.cks_ctx_create.argtypes = [i32, p, ctypes.POINTER(p)]
     L.cks_ctx_destroy.argtypes = [p]
     L.cks_ctx_set_stream.argtypes = [p, p]
     L.cks_ctx_set_timing.argtypes = [p, i32]
     L.cks_ctx_set_sort_mode.argtypes = [p, i32]
+    L.cks_ctx_set_round0_bits.argtypes = [p, u32]
+    L.cks_ctx_set_verify.argtypes = [p, i32]
+    L.cks_ctx_path_bytes.argtypes = [p, ctypes.POINTER(ctypes.c_double)]
     L.cks_ctx_stage_ms.argtypes = [p, ctypes.POINTER(f32), i32]
     L.cks_ctx_launches.argtypes = [p]
     L.cks_ctx_launches.restype = u64
@@ -93,10 +98,10 @@ def load_library(path: str | None = None):
     L.cks_compress.argtypes = [p, p, u64, u32, p, p]
     L.cks_sort.argtypes = [p, p, u32, u64, p, p, p]
     L.cks_adjacent_dbits.argtypes = [p, p, u32, u64, p, u32, p, ctypes.POINTER(u32), p]
-    L.cks_bulkload_shape.argtypes = [u64, u32, f32, ctypes.POINTER(TreeShape)]
-    L.cks_bulkload.argtypes = [p, p, p, u64, u32, f32, ctypes.POINTER(Tree)]
-    L.cks_paper_tree_shape.argtypes = [u64, f32, ctypes.POINTER(TreeShape)]
-    L.cks_paper_tree.argtypes = [p, p, u64, u32, p, p, u32, f32, p]
+    L.cks_bulkload_shape.argtypes = [u64, u32, f64, ctypes.POINTER(TreeShape)]
+    L.cks_bulkload.argtypes = [p, p, p, u64, u32, f64, ctypes.POINTER(Tree)]
+    L.cks_paper_tree_shape.argtypes = [u64, f64, ctypes.POINTER(TreeShape)]
+    L.cks_paper_tree.argtypes = [p, p, u64, u32, p, p, u32, f64, p]
     L.cks_build.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     L.cks_build_host.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     L.cks_occupancy.argtypes = [p, p, u64, u32, p]
@@ -105,8 +110,8 @@ def load_library(path: str | None = None):
     L.cks_repack.argtypes = [p, p, p, p, u32, u64, p]
     L.cks_partition.argtypes = [p, p, u32, u64, p, u32, u64, p, p, p]
     L.cks_sort_prefix.argtypes = [p, p, p, u32, u64, p, p, p, ctypes.POINTER(u32), p]
-    L.cks_bulkload_block.argtypes = [p, p, p, u64, u32, f32, i32, u32, ctypes.POINTER(Tree), p, ctypes.POINTER(u32)]
-    L.cks_bulkload_top.argtypes = [p, p, p, u64, u32, f32, ctypes.POINTER(Tree), ctypes.POINTER(u32)]
+    L.cks_bulkload_block.argtypes = [p, p, p, u64, u32, f64, i32, u32, ctypes.POINTER(Tree), p, ctypes.POINTER(u32)]
+    L.cks_bulkload_top.argtypes = [p, p, p, u64, u32, f64, ctypes.POINTER(Tree), ctypes.POINTER(u32)]
     L.cks_build_host_batch.argtypes = [p, p, u32, u64, u32, p, p]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or i32
@@ -193,6 +198,21 @@ def set_sort_mode(mode: int, device: int | None = None):
     _check(L, c, L.cks_ctx_set_sort_mode(c, int(mode)))
 
 
+def set_round0_bits(bits: int, device: int | None = None):
+    """Width of refinement round 0 for later builds (0 = sampled; else a multiple of 8 <= 64)."""
+    L, c = _context(device)
+    _check(L, c, L.cks_ctx_set_round0_bits(c, int(bits)))
+
+
+VERIFY_OFF, VERIFY_PRIOR, VERIFY_ALWAYS = 0, 1, 2
+
+
+def set_verify(mode: int, device: int | None = None):
+    """Order check of later builds against the key rows (cks_ctx_set_verify)."""
+    L, c = _context(device)
+    _check(L, c, L.cks_ctx_set_verify(c, int(mode)))
+
+
 def stage_ms() -> list[float]:
     L, c = _context()
     buf = (ctypes.c_float * 8)()
@@ -206,6 +226,14 @@ def kernel_stats() -> tuple[float, float, int]:
     ms, by, cnt = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint32()
     _check(L, c, L.cks_ctx_kernel_stats(c, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(cnt)))
     return float(ms.value), float(by.value), int(cnt.value)
+
+
+def path_bytes() -> float:
+    """Algorithmic bytes of every kernel of the last build on this thread's context."""
+    L, c = _context()
+    b = ctypes.c_double()
+    _check(L, c, L.cks_ctx_path_bytes(c, ctypes.byref(b)))
+    return float(b.value)
 
 
 def superset_mask(keys: torch.Tensor, kind: int = SUPERSET_BYTEOCC) -> np.ndarray:

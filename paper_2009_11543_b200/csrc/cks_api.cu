@@ -54,13 +54,18 @@ struct cks_ctx {
         pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, runoff2, runpos2, tie, keep, done, mlist, wlist, rcnt, rtot,   // NEXT-1
         part_in, part_out,                                                 // NEXT-4
         anyt,                                                              // k_ref_tile: tiles with ties left
+        vbad,                                                              // k_verify_order result
         keys2, perm2;                                                      // cks_build_host_batch: 2nd buffers
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
     uint16_t* h_moff = nullptr;
     uint32_t* h_small = nullptr;      // 4 KiB: masks, dacc words
     uint32_t* h_tot = nullptr;        // refinement: (members, runs) of the next round
-    int refine = -1;                  // first build by distinguishing prefixes (NEXT-1)
+    int refine = CKS_SORT_PREFIX_AUTO; // first build by distinguishing prefixes (NEXT-1)
+    uint32_t round0_bits = 0;         // forced width of refinement round 0 (0 = sampled)
+    int verify = CKS_VERIFY_PRIOR;    // order check of the result against the key rows
+    bool verify_now = false;          // ... for the build in progress
+    double path_bytes = 0.0;          // algorithmic bytes of every kernel of the last build
     bool skip_packed = false;         // cks_sort_prefix without packed_out: no a7
 };
 
@@ -89,6 +94,9 @@ int fail(cks_ctx* c, int code, const char* fmt, ...) {
         ctx->launches++;    \
         CK(expr);           \
     } while (0)
+
+// algorithmic bytes of a launch (what it must read + write at least), summed per build
+#define BYTES(x) (ctx->path_bytes += (double)(x))
 
 #define TRY(expr)                   \
     do {                            \
@@ -161,6 +169,7 @@ int run_superset(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, int 
     if (keys_ready) {
         CK(cudaMemsetAsync(ctx->occ.p, 0, (size_t)B * 8 * 4, ctx->stream));
         if (n) LAUNCH(launch_occupancy(keys, n, B, as<uint32_t>(ctx->occ), ctx->sms, ctx->stream));
+        BYTES((double)n * B);
     }
     LAUNCH(launch_occ_finalize(as<uint32_t>(ctx->occ), B, n, as<uint8_t>(ctx->masks8),
                                as<uint8_t>(ctx->masks8) + B, ctx->stream));
@@ -185,6 +194,7 @@ int run_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     GatherPlan* dplan;
     TRY(upload_plan(ctx, 0, &dplan));
     LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, planes, pitch, ctx->sms, ctx->stream, lead, rows));
+    BYTES((double)n * (B + 4.0 * np + (rows ? 4.0 : 0.0)));
     return CKS_OK;
 }
 
@@ -266,8 +276,7 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
         aux.fork = ctx->aux_ev[0];
         aux.join = ctx->aux_ev[1];
         const int ke = ctx->nkev;
-        static const bool no_kev = getenv("CKS_NO_KERNEL_EVENTS") != nullptr;   // experiments only
-        if (ctx->timing && !no_kev && ke < cks_ctx::kMaxKev) {
+        if (ctx->timing && !knobs().no_kernel_events && ke < cks_ctx::kMaxKev) {
             aux.ws_begin = ctx->kev[2 * ke];
             aux.ws_end = ctx->kev[2 * ke + 1];
             ctx->kbytes[ke] = 0.0;
@@ -275,6 +284,8 @@ int run_sort(cks_ctx* ctx, const uint32_t* in_planes, uint64_t in_pitch, uint32_
         }
         int nl = 0;
         CK(launch_lsd_pass(la, ctx->sms, ctx->stream, aux, &nl));
+        // upsweep reads the digit word; the downsweep reads every loaded stream and writes all
+        BYTES(4.0 * n * (1 + (np + (cur_r ? 1 : 0)) + (np + 1)));
         if (aux.ws_bytes && ctx->kbytes[ke] > 0.0) ctx->nkev++;
         ctx->launches += (uint64_t)nl;
         cur_p = out_p;
@@ -321,6 +332,7 @@ int run_adjacent(cks_ctx* ctx, const uint32_t* sorted, uint64_t pitch, uint32_t 
     TRY(upload_moff(ctx, sort_mask, B, m));
     CK(cudaMemsetAsync(ctx->dacc.p, 0, (size_t)nwords * 4, ctx->stream));
     if (n && m) {
+        BYTES((double)n * (4.0 * ((m + 31) / 32) + (dbit ? 2.0 : 0.0)));
         LAUNCH(launch_adjacent(sorted, pitch, n, m, as<uint16_t>(ctx->moff), B, dbit, as<uint32_t>(ctx->dacc),
                                ctx->sms, ctx->stream));
     } else if (n && dbit) {
@@ -359,15 +371,14 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     // round-0 passes; whatever still ties is finished by the later rounds -- the result is
     // exact for any T).
     // The sample is compressed and sorted on the side stream while the full compress runs.
-    // CKS_ROUND0_BITS forces T.
+    // cks_ctx_set_round0_bits forces T.
     GatherPlan* dplan = nullptr;
     if (!planes_in) {
         TRY(claim_slot(ctx, 0));
         plan_compress(M, B, ctx->h_plan[0]);
         TRY(upload_plan(ctx, 0, &dplan));
     }
-    static int forced = -2;
-    if (forced == -2) { const char* e = getenv("CKS_ROUND0_BITS"); forced = e ? atoi(e) : 0; }
+    const int forced = (int)ctx->round0_bits;
     const bool sample = !(forced > 0 && forced <= 64 && (forced & 7) == 0) && np >= 2 && n >= (1u << 16);
     TRY(ensure(ctx, ctx->rtot, 64));
     uint32_t* scnt = as<uint32_t>(ctx->rtot) + 4;
@@ -435,7 +446,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     TRY(run_sort(ctx, pm + (uint64_t)(np - np0) * sp, sp, np0, 4 * np0, n, nullptr, 0, carried, sp, out->perm,
                  &sorted0, &sp0, dig0, false));
     // round-0 adjacency; when rounds follow, fused with finishing the short runs inside a tile
-    static const bool no_tile = getenv("CKS_NO_TILE_RUNS") != nullptr;   // experiments only
+    const bool no_tile = knobs().no_tile_runs;   // (experiments build only)
     const uint32_t* lo0 = np0 >= 2 ? sorted0 + (uint64_t)(np0 - 2) * sp0 : nullptr;
     const uint32_t* hi0 = sorted0 + (uint64_t)(np0 - 1) * sp0;
     TRY(ensure(ctx, ctx->rtot, 64));
@@ -444,13 +455,18 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     if (tiled) {
         TRY(ensure(ctx, ctx->anyt, ref_tiles(n) + 16));
         CK(cudaMemsetAsync(ctx->anyt.p, 0, ref_tiles(n) + 16, ctx->stream));
+        // reads the chunk (hi, lo), row ids and the carried words below the chunk; writes tie
+        // flags and D_i (the reordered members' row ids and words are counted after the round)
+        // (np == 3: chunk = planes 2, 1; the remaining words below the chunk add plane 0)
+        BYTES((double)n * (8.0 + 4.0 + 4.0 + 3.0));
         LAUNCH(launch_ref_tile(pm, sp, np, (int)np - 1 - (int)(T >> 5), 0xFFFFFFFFu >> (T & 31), moff, out->perm, dbit,
                                carried, lo0, hi0, sp0, n, ~0ull << (64 - T), B, tie, dacc, as<uint32_t>(ctx->rtot) + 2,
                                ctx->sms, ctx->stream, as<uint8_t>(ctx->anyt)));
-    }
-    else
+    } else {
         LAUNCH(launch_ref_adj(lo0, hi0, nullptr, nullptr, n, 0, moff, m, B, dbit, tie, dacc, true, ctx->sms,
                               ctx->stream, ~0ull << (64 - T)));
+        BYTES((double)n * (4.0 * (np0 >= 2 ? 2 : 1) + 3.0));
+    }
     out->round0_bits = T;
     out->rounds = 1;
     out->refined_keys = 0;
@@ -484,11 +500,12 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         *b = ctx->h_tot[1];
         if (ctx->h_tot[2]) {                                     // keys finished by the tile kernel
             out->refined_keys += ctx->h_tot[2];
+            BYTES((double)ctx->h_tot[2] * (4.0 + 4.0 * (double)((int)np - (int)(T >> 5))));   // row ids + words
             CK(cudaMemsetAsync(as<uint32_t>(ctx->rtot) + 2, 0, 4, ctx->stream));
         }
         return CKS_OK;
     };
-    const bool log = getenv("CKS_REFINE_LOG") != nullptr;
+    const bool log = knobs().refine_log;          // (experiments build only)
     int li = -1;                                                 // buffer of the current list
     for (uint32_t r = 1; T + 64 * (r - 1) < m; r++) {
         const uint32_t o = T + 64 * (r - 1);                     // first P_M bit of this round's chunk
@@ -504,6 +521,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
                                   r == 1 && tiled ? as<uint8_t>(ctx->anyt) : nullptr));
         uint64_t nn = 0, nseg = 0;
         TRY(counts(&nn, &nseg));
+        BYTES((double)nr * (1.0 + (pos ? 4.0 : 0.0)) + (double)nn * 8.0 + (double)nseg * 8.0);
         if (nn == 0) break;
         // (2) finish short runs and runs of equal keys in place
         const int qtop = (int)np - 1 - (int)(o >> 5);            // plane holding bit o
@@ -512,6 +530,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
                                 dbit, dacc, as<uint8_t>(ctx->done), as<uint8_t>(ctx->keep), carried, B,
                                 as<uint32_t>(ctx->mlist), as<uint32_t>(ctx->wlist), as<uint32_t>(ctx->rtot) + 12,
                                 ctx->sms, ctx->stream, 0xFFFFFFFFu >> (o & 31)));
+        BYTES((double)nseg * 8.0 + (double)nn * (4.0 + 4.0 * (double)(qtop + 1) + 2.0 + 1.0));
         // (3) the runs left for a round on the next 64 bits (none: done)
         CK(cudaMemcpyAsync(ctx->h_tot, as<uint32_t>(ctx->rtot) + 12, 16, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -524,6 +543,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
                                       as<uint32_t>(ctx->rtot), posB_, segB_, as<uint32_t>(ctx->runoff2),
                                       as<uint32_t>(ctx->runpos2), ctx->stream));
             TRY(counts(&n2, &nseg2));
+            BYTES((double)nn * 2.0 + (double)n2 * 8.0 + (double)nseg2 * 8.0);
         }
         if (log)
             fprintf(stderr, "[cks refine] round %u: %llu tied keys in %llu runs; %llu keys in %llu runs (longest %u) "
@@ -545,9 +565,11 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
                                         nseg2, n2, as<uint32_t>(ctx->cmp), cp, as<uint32_t>(ctx->crid2), ctx->sms,
                                         ctx->stream));
             sv = as<uint32_t>(ctx->cmp);
+            BYTES((double)nseg2 * 8.0 + (double)n2 * (4.0 + 8.0 + 12.0 + 4.0));   // row, chunk by row -> chunk, row
         } else {
             LAUNCH(launch_ref_gather(pm, sp, np, o, posB_, segB_, out->perm, n2, as<uint32_t>(ctx->cmp), cp,
                                      as<uint32_t>(ctx->crid), ctx->sms, ctx->stream));
+            BYTES((double)n2 * (8.0 + 4.0 + 8.0 + 12.0 + 4.0));  // pos, seg, row, chunk by row -> list
             const uint32_t segbits = nseg2 > 1 ? 32u - (uint32_t)__builtin_clz((uint32_t)(nseg2 - 1)) : 0u;
             const uint32_t d0 = o + 64 > m ? (o + 64 - m) / 8 : 0;   // digits past the last mask bit are zero
             out->passes += 8 + (segbits + 7) / 8 - d0;
@@ -556,6 +578,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         }
         LAUNCH(launch_ref_put(out->perm, posB_, as<uint32_t>(ctx->crid2), n2, pm, sp, np, carried, ctx->sms,
                               ctx->stream));
+        BYTES((double)n2 * (8.0 + 4.0 + (carried ? 8.0 * np : 0.0)) + (double)n2 * (12.0 + 4.0 + 3.0));  // put + adj
         LAUNCH(launch_ref_adj(sv, sv + svp, sv + 2 * svp, posB_, n2, o, moff, m, B, dbit, tie, dacc, false, ctx->sms,
                               ctx->stream));
         pos = posB_;
@@ -565,9 +588,6 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     mark(ctx, ST_SORT);
     TRY(read_dacc(ctx, B, out->mask));
     out->popcount = popcount_mask(out->mask, B);
-    for (uint32_t j = 0; j < B; j++)
-        if (out->mask[j] & ~M[j])
-            return fail(ctx, CKS_ERANGE, "adjacency produced a bit outside the sort mask (byte %u)", j);
     mark(ctx, ST_ADJ);
     // a7: P_D in sorted order -- from the sorted chunk when one chunk held all of P_M,
     // otherwise compressed again from the key rows in sorted order
@@ -589,6 +609,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             GatherPlan* dplan;
             TRY(upload_plan(ctx, 1, &dplan));
             LAUNCH(launch_repack(sorted0, sp0, n, dplan, ctx->h_plan[1]->nsteps, npd, pd, sp, ctx->sms, ctx->stream));
+            BYTES((double)n * 4.0 * (np + npd));
             out->packed = pd;
         } else if (keys) {
             TRY(run_compress(ctx, keys, n, B, out->mask, pd, sp, 0, out->perm));
@@ -602,6 +623,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             TRY(upload_plan(ctx, 1, &dplan));
             LAUNCH(launch_repack(pm, sp, n, dplan, ctx->h_plan[1]->nsteps, npd, pd, sp, ctx->sms, ctx->stream,
                                  out->perm));
+            BYTES((double)n * 4.0 * (1 + np + npd));
             out->packed = pd;
         }
     }
@@ -609,7 +631,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     return CKS_OK;
 }
 
-int tree_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* s) {
+int tree_shape(uint64_t n, uint32_t fanout, double fill, cks_tree_shape* s) {
     if (!s || fanout < 2 || !(fill > 0.f) || fill > 1.f) return CKS_EINVAL;
     uint32_t per = (uint32_t)((double)fanout * (double)fill);
     if (per < 2) return CKS_EINVAL;
@@ -640,7 +662,7 @@ int tree_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* s) {
 // CKS_DBIT_NONE); otherwise (a later block) every inner entry takes its child's minimum.
 // levels: build levels 0..levels-1 only (0 = all); top_min: minima of the top built level.
 int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
-                 float fill, const cks_tree* t, uint32_t* height, bool first_global = true, uint32_t levels = 0,
+                 double fill, const cks_tree* t, uint32_t* height, bool first_global = true, uint32_t levels = 0,
                  uint16_t* top_min = nullptr) {
     cks_tree_shape s;
     int rc = tree_shape(n, fanout, fill, &s);
@@ -663,6 +685,7 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
         TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
         TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
     }
+    BYTES((double)n * (8.0 + (dbit ? 2.0 + (t->entry_dbit ? 2.0 : 0.0) : 0.0)) + (double)s.level_nodes[0] * 4.0);
     LAUNCH(launch_bulk_leaves(perm, dbit, L, fanout, per, t->node_cnt, t->entry_rid, t->entry_dbit,
                               mins ? as<uint16_t>(ctx->rmin0) : nullptr, ctx->sms, ctx->stream));
     const uint16_t* rbelow = mins ? as<uint16_t>(ctx->rmin0) : nullptr;
@@ -688,7 +711,7 @@ int run_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
 // P:502 merge: the levels above nchild child nodes (highest row id + minimum D_k of each);
 // node ids start at 0 on the first built level.
 int run_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* child_min, uint64_t nchild,
-                     uint32_t fanout, float fill, const cks_tree* t, uint32_t* height) {
+                     uint32_t fanout, double fill, const cks_tree* t, uint32_t* height) {
     cks_tree_shape s;
     int rc = tree_shape(nchild, fanout, fill, &s);
     if (rc != CKS_OK) return fail(ctx, rc, "bad bulk-load shape (fanout %u, fill %f)", fanout, (double)fill);
@@ -720,10 +743,30 @@ int run_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* ch
     return CKS_OK;
 }
 
+// The order check (k_verify.cu) of the permutation just computed, when this build asks for it
+// (ctx->verify_now): CKS_ERANGE if the sort mask was not a superset of the distinction bits.
+int verify_if(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const cks_build_out* out) {
+    if (!ctx->verify_now || !keys || n < 2) return CKS_OK;
+    TRY(ensure(ctx, ctx->vbad, 16));
+    LAUNCH(launch_verify_order(keys, B, out->perm, n, as<unsigned long long>(ctx->vbad), ctx->sms, ctx->stream));
+    BYTES((double)n * (4.0 + B));
+    CK(cudaEventSynchronize(ctx->plan_ev[2]));
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->vbad.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    unsigned long long bad;
+    memcpy(&bad, ctx->h_small, 8);
+    if (bad != ~0ull)
+        return fail(ctx, CKS_ERANGE,
+                    "the sort mask is not a superset of the distinction bits: sorted positions %llu and %llu are "
+                    "out of (key, row id) order (Theorem 2 needs every D-bit in the mask, P:222-238)",
+                    bad - 1, bad);
+    return CKS_OK;
+}
+
 // Everything after the sort mask is known: a3 .. a8 on device keys.
 // keys == NULL: P_M is given (planes_in, right-aligned u32[np][n]) -- cks_sort_prefix.
 int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* M,
-                    uint32_t m, cks_build_out* out, bool check_superset, const uint32_t* planes_in = nullptr) {
+                    uint32_t m, cks_build_out* out, const uint32_t* planes_in = nullptr) {
     const uint32_t np = (m + 31) / 32, k = (m + 7) / 8;
     out->sort_bits = m;
     out->passes = k;
@@ -735,14 +778,11 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
         TRY(ensure(ctx, ctx->dbit, n * 2));
         dbit = as<uint16_t>(ctx->dbit);
     }
-    if (ctx->refine < 0) {
-        const char* e = getenv("CKS_REFINE");
-        ctx->refine = e ? atoi(e) : 1;
-    }
     // 1 = auto: by prefixes whenever P_M is wider than one 64-bit chunk (m > 64); for m <= 64
     // round 0 would be the whole sort anyway
     if (n && m && (ctx->refine == 2 || (ctx->refine == 1 && m > 64))) {
         TRY(build_refine(ctx, keys, n, B, M, m, out, dbit, planes_in));
+        TRY(verify_if(ctx, keys, n, B, out));
         out->height = 0;
         if (out->tree.node_cnt) {
             cks_tree tr = out->tree;
@@ -775,10 +815,6 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     // a6
     TRY(run_adjacent(ctx, sorted, spitch, m, n, M, B, out->mask, dbit));
     out->popcount = popcount_mask(out->mask, B);
-    for (uint32_t j = 0; j < B; j++)
-        if (out->mask[j] & ~M[j])
-            return fail(ctx, CKS_ERANGE, "adjacency produced a bit outside the sort mask (byte %u)", j);
-    (void)check_superset;
     mark(ctx, ST_ADJ);
     // a7: repack P_M -> P_D
     out->packed = sorted;
@@ -791,6 +827,7 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
         GatherPlan* dplan;
         TRY(upload_plan(ctx, 1, &dplan));
         uint32_t* dst = (sorted == as<uint32_t>(ctx->planeA)) ? as<uint32_t>(ctx->planeB) : as<uint32_t>(ctx->planeA);
+        BYTES((double)n * 4.0 * (np + (out->popcount + 31) / 32));
         LAUNCH(launch_repack(sorted, spitch, n, dplan, ctx->h_plan[1]->nsteps, (out->popcount + 31) / 32, dst, sp,
                              ctx->sms, ctx->stream));
         out->packed = dst;
@@ -799,6 +836,7 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
         out->packed = nullptr;
     }
     mark(ctx, ST_REPACK);
+    TRY(verify_if(ctx, keys, n, B, out));
     // a8
     out->height = 0;
     if (out->tree.node_cnt) {
@@ -821,7 +859,10 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask));
     }
     mark(ctx, ST_MASK);
-    return build_from_mask(ctx, keys, n, B, M.data(), m, out, prior != nullptr);
+    ctx->verify_now = keys && (ctx->verify == CKS_VERIFY_ALWAYS || (ctx->verify == CKS_VERIFY_PRIOR && prior));
+    const int rc = build_from_mask(ctx, keys, n, B, M.data(), m, out);
+    ctx->verify_now = false;
+    return rc;
 }
 
 }  // namespace
@@ -876,7 +917,8 @@ int cks_ctx_destroy(cks_ctx* ctx) {
                       &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->runpos, &ctx->runoff2, &ctx->runpos2,
                       &ctx->tie, &ctx->keep, &ctx->done, &ctx->mlist,
                       &ctx->wlist,
-                      &ctx->rcnt, &ctx->rtot};
+                      &ctx->rcnt, &ctx->rtot, &ctx->part_in, &ctx->part_out, &ctx->anyt, &ctx->vbad,
+                      &ctx->keys2, &ctx->perm2};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int i = 0; i < ST_N; i++)
@@ -924,6 +966,18 @@ int cks_ctx_set_sort_mode(cks_ctx* ctx, int mode) {
     return CKS_OK;
 }
 
+int cks_ctx_set_round0_bits(cks_ctx* ctx, uint32_t bits) {
+    if (!ctx || bits > 64 || (bits & 7)) return CKS_EINVAL;
+    ctx->round0_bits = bits;
+    return CKS_OK;
+}
+
+int cks_ctx_set_verify(cks_ctx* ctx, int mode) {
+    if (!ctx || mode < CKS_VERIFY_OFF || mode > CKS_VERIFY_ALWAYS) return CKS_EINVAL;
+    ctx->verify = mode;
+    return CKS_OK;
+}
+
 int cks_ctx_stage_ms(cks_ctx* ctx, float* out, int max) {
     if (!ctx || !out) return 0;
     if (!ctx->timed) return 0;
@@ -958,6 +1012,12 @@ int cks_ctx_kernel_stats(cks_ctx* ctx, double* ms, double* bytes, uint32_t* coun
         *bytes += ctx->kbytes[i];
     }
     *count = (uint32_t)ctx->nkev;
+    return CKS_OK;
+}
+
+int cks_ctx_path_bytes(const cks_ctx* ctx, double* bytes) {
+    if (!ctx || !bytes) return CKS_EINVAL;
+    *bytes = ctx->path_bytes;
     return CKS_OK;
 }
 
@@ -1069,6 +1129,7 @@ int cks_sort_prefix(cks_ctx* ctx, const uint32_t* packed, const uint8_t* sort_ma
     CK(cudaSetDevice(ctx->device));
     ctx->timed = ctx->timing;
     ctx->nkev = 0;
+    ctx->path_bytes = 0.0;
     mark(ctx, ST_BEGIN);
     cks_build_out o;
     memset(&o, 0, sizeof(o));
@@ -1083,7 +1144,7 @@ int cks_sort_prefix(cks_ctx* ctx, const uint32_t* packed, const uint8_t* sort_ma
         return CKS_OK;
     }
     ctx->skip_packed = packed_out == nullptr;
-    const int rc = build_from_mask(ctx, nullptr, n, B, sort_mask, m, &o, false, packed);
+    const int rc = build_from_mask(ctx, nullptr, n, B, sort_mask, m, &o, packed);
     ctx->skip_packed = false;
     TRY(rc);
     if (popcount_out) *popcount_out = o.popcount;
@@ -1094,7 +1155,7 @@ int cks_sort_prefix(cks_ctx* ctx, const uint32_t* packed, const uint8_t* sort_ma
     return CKS_OK;
 }
 
-int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout, float fill,
+int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout, double fill,
                        int first_global, uint32_t levels, cks_tree* out, uint16_t* top_min_out, uint32_t* height_out) {
     if (!ctx) return CKS_EINVAL;
     if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
@@ -1107,7 +1168,7 @@ int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit,
 }
 
 int cks_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* child_min, uint64_t nchild,
-                     uint32_t fanout, float fill, cks_tree* out, uint32_t* height_out) {
+                     uint32_t fanout, double fill, cks_tree* out, uint32_t* height_out) {
     if (!ctx) return CKS_EINVAL;
     if (nchild && (!child_rid || !child_min)) return fail(ctx, CKS_EINVAL, "NULL child arrays");
     CK(cudaSetDevice(ctx->device));
@@ -1176,11 +1237,11 @@ int cks_adjacent_dbits(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bit
     return CKS_OK;
 }
 
-int cks_bulkload_shape(uint64_t n, uint32_t fanout, float fill, cks_tree_shape* out) {
+int cks_bulkload_shape(uint64_t n, uint32_t fanout, double fill, cks_tree_shape* out) {
     return tree_shape(n, fanout, fill, out);
 }
 
-int cks_paper_tree_shape(uint64_t n, float fill, cks_tree_shape* s) {
+int cks_paper_tree_shape(uint64_t n, double fill, cks_tree_shape* s) {
     if (!s || !(fill > 0.f) || fill > 1.f) return CKS_EINVAL;
     const uint32_t lp = (uint32_t)((double)CKS_PTREE_LEAF_FANOUT * (double)fill);
     const uint32_t ip = (uint32_t)((double)CKS_PTREE_INNER_FANOUT * (double)fill);
@@ -1209,7 +1270,7 @@ int cks_paper_tree_shape(uint64_t n, float fill, cks_tree_shape* s) {
 }
 
 int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm,
-                   const uint16_t* dbit, uint32_t pk_bits, float fill, uint8_t* nodes) {
+                   const uint16_t* dbit, uint32_t pk_bits, double fill, uint8_t* nodes) {
     TRY(check_keys(ctx, keys, n, B));
     if (pk_bits > 32) return fail(ctx, CKS_EINVAL, "pk_bits %u > 32", pk_bits);
     if (n && (!perm || !dbit || !nodes)) return fail(ctx, CKS_EINVAL, "NULL perm, dbit or nodes with n > 0");
@@ -1228,7 +1289,7 @@ int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, co
 }
 
 int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
-                 float fill, const cks_tree* out) {
+                 double fill, const cks_tree* out) {
     if (!ctx) return CKS_EINVAL;
     if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
     if (n && !perm) return fail(ctx, CKS_EINVAL, "perm is NULL");
@@ -1262,6 +1323,7 @@ int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const u
     CK(cudaSetDevice(ctx->device));
     ctx->timed = ctx->timing;
     ctx->nkev = 0;
+    ctx->path_bytes = 0.0;
     mark(ctx, ST_BEGIN);
     return build_common(ctx, keys, n, B, prior, out, true);
 }
@@ -1274,6 +1336,7 @@ int cks_build_host(cks_ctx* ctx, const uint8_t* host_keys, uint64_t n, uint32_t 
     CK(cudaSetDevice(ctx->device));
     ctx->timed = ctx->timing;
     ctx->nkev = 0;
+    ctx->path_bytes = 0.0;
     mark(ctx, ST_BEGIN);
     const size_t bytes = (size_t)n * B;
     TRY(ensure(ctx, ctx->keys, bytes));
@@ -1358,6 +1421,7 @@ int cks_build_host_batch(cks_ctx* ctx, const uint8_t* const* host_keys, uint32_t
         if (i >= 2) CK(cudaStreamWaitEvent(ctx->stream, out_ev[b], 0));             // pb[b] free
         ctx->timed = ctx->timing;
         ctx->nkev = 0;
+        ctx->path_bytes = 0.0;
         mark(ctx, ST_BEGIN);
         cks_build_out o = outs[i];
         o.perm = pb[b];

@@ -37,6 +37,25 @@ struct GatherPlan {
 // Never lowers it: one record per (device, kernel) shared by every launch site (cks_plan.cpp).
 cudaError_t raise_smem_limit(const void* kernel, size_t bytes);
 
+// Tuning knobs (cks_plan.cpp). Fixed defaults in the product build: the library reads no
+// environment. Built with -DCKS_EXPERIMENTS=1 (CKS_EXPERIMENTS=1 python -m
+// paper_2009_11543_b200._build) the timing-experiment variables CKS_LSD_ITEMS / _SLOTS /
+// _CHUNK / _WS / _DEBUG (the last makes results WRONG), CKS_REF_CTA, CKS_NO_TILE_RUNS,
+// CKS_NO_KERNEL_EVENTS and CKS_REFINE_LOG override them. Initialised once (std::call_once),
+// read-only afterwards, so concurrent host threads see one consistent set.
+struct Knobs {
+    int lsd_items = 16;        // keys per thread of the LSD tile (8 or 16)
+    int lsd_slots = 4;         // ring slots of the non-specialised downsweep
+    int lsd_chunk = 0;         // tiles per upsweep CTA (0 = by size)
+    int lsd_ws = 1;            // warp-specialised downsweep on full tiles
+    int lsd_debug = 0;         // timing-only modes with wrong results (experiments build only)
+    int ref_cta = 2048;        // longest run one CTA sorts in the refinement
+    bool no_tile_runs = false; // round-0 adjacency without in-tile run finishing
+    bool no_kernel_events = false;
+    bool refine_log = false;
+};
+const Knobs& knobs();
+
 // Host-side planning (cks_plan.cpp).
 void plan_compress(const uint8_t* mask, uint32_t key_bytes, GatherPlan* plan);
 void move_masks_left(uint32_t mask, uint32_t mv[5]);
@@ -102,6 +121,10 @@ cudaError_t launch_adjacent(const uint32_t* planes, uint64_t pitch, uint64_t n, 
                             uint32_t B, uint16_t* dbit_out, uint32_t* dacc /* u32[ceil(8B/32)] */,
                             int sms, cudaStream_t st);
 cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
+// Order check (k_verify.cu): *first_bad = smallest sorted position i >= 1 whose pair
+// (perm[i-1], perm[i]) is not in (key, row id) order, or all ones when there is none.
+cudaError_t launch_verify_order(const uint8_t* keys, uint32_t B, const uint32_t* perm, uint64_t n,
+                                unsigned long long* first_bad, int sms, cudaStream_t st);
 
 // NEXT-1 prefix refinement (k_refine.cu)
 uint64_t ref_tiles(uint64_t nr);

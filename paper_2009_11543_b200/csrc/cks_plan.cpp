@@ -5,6 +5,7 @@
 // have an odd number of unselected positions (in units of 2^k) below them move right by
 // 2^k. Applying the five steps to (x & mask) leaves the selected bits, in order, in the
 // low popcount(mask) bits -- what PEXT does in hardware.
+#include <stdlib.h>
 #include <string.h>
 
 #include <map>
@@ -14,6 +15,35 @@
 #include "cks_internal.h"
 
 namespace cks {
+
+const Knobs& knobs() {
+    static Knobs k;
+    static std::once_flag once;
+    std::call_once(once, [] {
+#if defined(CKS_EXPERIMENTS) && CKS_EXPERIMENTS
+        auto env = [](const char* name, int def) {
+            const char* e = getenv(name);
+            return e ? atoi(e) : def;
+        };
+        k.lsd_items = env("CKS_LSD_ITEMS", 16);
+        if (k.lsd_items != 8 && k.lsd_items != 16) k.lsd_items = 16;
+        k.lsd_slots = env("CKS_LSD_SLOTS", 4);
+        if (k.lsd_slots < 1) k.lsd_slots = 1;
+        if (k.lsd_slots > 16) k.lsd_slots = 16;
+        k.lsd_chunk = env("CKS_LSD_CHUNK", 0);
+        if (k.lsd_chunk < 0) k.lsd_chunk = 0;
+        k.lsd_ws = env("CKS_LSD_WS", 1);
+        k.lsd_debug = env("CKS_LSD_DEBUG", 0);
+        k.ref_cta = env("CKS_REF_CTA", 2048);
+        if (k.ref_cta < 0) k.ref_cta = 0;
+        if (k.ref_cta > 2048) k.ref_cta = 2048;
+        k.no_tile_runs = getenv("CKS_NO_TILE_RUNS") != nullptr;
+        k.no_kernel_events = getenv("CKS_NO_KERNEL_EVENTS") != nullptr;
+        k.refine_log = getenv("CKS_REFINE_LOG") != nullptr;
+#endif
+    });
+    return k;
+}
 
 cudaError_t raise_smem_limit(const void* kernel, size_t bytes) {
     static std::mutex mu;

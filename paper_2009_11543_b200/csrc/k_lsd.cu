@@ -31,6 +31,12 @@ namespace cks {
 namespace {
 
 constexpr int kW = kSortThreads / 32;
+// timing-only debug modes of the downsweep (wrong results): compiled in only with CKS_EXPERIMENTS
+#if defined(CKS_EXPERIMENTS) && CKS_EXPERIMENTS
+constexpr bool kLsdDebug = true;
+#else
+constexpr bool kLsdDebug = false;
+#endif
 
 // Programmatic dependent launch: the kernels of a pass are launched with programmatic stream
 // serialisation, so a kernel's CTAs can be scheduled while its predecessor drains; each
@@ -601,7 +607,8 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
             uint16_t* src = s_src + buf * TILE;
 #pragma unroll
             for (int i = 0; i < RI; i++)
-                src[(a.debug & 2) ? wofs + i * 32 + lane : pos[i] + h[dg[i]]] = (uint16_t)((wofs + i * 32 + lane) * 4);
+                src[(kLsdDebug && (a.debug & 2)) ? wofs + i * 32 + lane : pos[i] + h[dg[i]]] =
+                    (uint16_t)((wofs + i * 32 + lane) * 4);
             __syncwarp();
             if (lane == 0) bar_arrive(&s_ranked[buf]);
         }
@@ -627,7 +634,8 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
 #pragma unroll
             for (int r = 0; r < WI; r++) {
                 const uint32_t w = *reinterpret_cast<const uint32_t*>(sl + from[r]);
-                dest[r] = (a.debug & 1) ? tile * (uint32_t)TILE + r * SH::WT + wt : r * SH::WT + wt + s_gb[buf][digit_of(w, sel)];
+                dest[r] = (kLsdDebug && (a.debug & 1)) ? tile * (uint32_t)TILE + r * SH::WT + wt
+                                                       : r * SH::WT + wt + s_gb[buf][digit_of(w, sel)];
                 out[dest[r]] = w;
             }
             __syncwarp();
@@ -655,35 +663,14 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
 
 // ---- launch ---------------------------------------------------------------------------------
 
-static int g_lsd_items = 0, g_lsd_slots = 0, g_lsd_chunk = 0, g_lsd_ws = 1;
-
-static void lsd_config() {
-    if (g_lsd_items) return;
-    const char* e = getenv("CKS_LSD_ITEMS");
-    g_lsd_items = e ? atoi(e) : 16;
-    if (g_lsd_items != 8 && g_lsd_items != 16) g_lsd_items = 16;
-    const char* s = getenv("CKS_LSD_SLOTS");
-    g_lsd_slots = s ? atoi(s) : 4;
-    if (g_lsd_slots < 1) g_lsd_slots = 1;
-    if (g_lsd_slots > 16) g_lsd_slots = 16;
-    const char* c = getenv("CKS_LSD_CHUNK");
-    g_lsd_chunk = c ? atoi(c) : 0;                       // 0: by size (chunk_for)
-    const char* w = getenv("CKS_LSD_WS");
-    g_lsd_ws = w ? atoi(w) : 1;
-    if (g_lsd_chunk < 0) g_lsd_chunk = 0;
-}
-
 // tiles per upsweep CTA: 32 for the largest lists (measured cfg5, 12.2 k tiles: 3.64 -> 3.60 ms),
 // 16 below 8192 tiles (cfg3/cfg4 and the refinement's lists lose parallelism with 32)
 static uint32_t chunk_for(uint64_t tiles) {
-    if (g_lsd_chunk > 0) return (uint32_t)g_lsd_chunk;
+    if (knobs().lsd_chunk > 0) return (uint32_t)knobs().lsd_chunk;
     return tiles >= 8192 ? 32u : 16u;
 }
 
-uint64_t lsd_tile_keys() {
-    lsd_config();
-    return (uint64_t)kSortThreads * g_lsd_items;
-}
+uint64_t lsd_tile_keys() { return (uint64_t)kSortThreads * knobs().lsd_items; }
 
 void lsd_sizes(uint64_t n, uint64_t* tiles, uint64_t* chunks) {
     uint64_t t = lsd_tile_keys();
@@ -718,7 +705,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
     const int streams = (int)a.nplanes + 1 - (a.in_rid == nullptr ? 1 : 0);
     const uint64_t nfull = a.n / TILE;
     int nl = 2;
-    if (g_lsd_ws && a.tma && nfull > 0) {
+    if (knobs().lsd_ws && a.tma && nfull > 0) {
         // warp-specialised kernel over the full tiles, one persistent CTA per SM
         using SH = typename std::conditional<ITEMS == 8, WsShape<2048, 8, 4, 2>, WsShape<4096, 16, 8, 1>>::type;
         static_assert(SH::TILE == TILE, "the upsweep's tile is the downsweep's tile");
@@ -777,16 +764,14 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
 cudaError_t launch_lsd_pass(const LsdPassArgs& args, int sms, cudaStream_t st, const LsdAux& aux, int* launches) {
     *launches = 0;
     if (args.n == 0) return cudaSuccess;
-    lsd_config();
+    const Knobs& kn = knobs();
     LsdPassArgs a = args;
-    a.slots = (uint32_t)g_lsd_slots;
-    a.chunk_tiles = chunk_for((a.n + (uint64_t)kSortThreads * g_lsd_items - 1) / ((uint64_t)kSortThreads * g_lsd_items));
-    static int dbg = -1;
-    if (dbg < 0) { const char* e = getenv("CKS_LSD_DEBUG"); dbg = e ? atoi(e) : 0; }
-    a.debug = (uint32_t)dbg;
+    a.slots = (uint32_t)kn.lsd_slots;
+    a.chunk_tiles = chunk_for((a.n + lsd_tile_keys() - 1) / lsd_tile_keys());
+    a.debug = (uint32_t)kn.lsd_debug;
     a.tma = ((uintptr_t)a.in_planes % 16 == 0) && (a.in_pitch % 4 == 0) &&
             (a.in_rid == nullptr || (uintptr_t)a.in_rid % 16 == 0);
-    return g_lsd_items == 8 ? lsd_pass<8>(a, sms, st, aux, launches) : lsd_pass<16>(a, sms, st, aux, launches);
+    return kn.lsd_items == 8 ? lsd_pass<8>(a, sms, st, aux, launches) : lsd_pass<16>(a, sms, st, aux, launches);
 }
 
 }  // namespace cks

@@ -1007,16 +1007,10 @@ static unsigned grid_of(uint64_t work, int sms) {
     return (unsigned)(g ? g : 1);
 }
 
-// longest run sorted by one CTA (env CKS_REF_CTA, default 2048, at most kCta)
+// longest run sorted by one CTA (knob ref_cta, default 2048 = kCta)
 static uint32_t cta_max() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("CKS_REF_CTA");
-        v = e ? atoi(e) : (int)kCta;
-        if (v < 0) v = 0;
-        if (v > (int)kCta) v = (int)kCta;
-    }
-    return (uint32_t)v;
+    const int v = knobs().ref_cta;
+    return (uint32_t)(v < (int)kCta ? v : (int)kCta);
 }
 
 uint64_t ref_tiles(uint64_t nr) { return (nr + kRefTile - 1) / kRefTile; }

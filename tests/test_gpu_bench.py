@@ -45,6 +45,21 @@ def test_bench_line_contract():
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
 
 
+def test_bench_line_paths_and_ratios():
+    d = run_bench("--config", "5", "--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
+                  "--full-key-steps", "1")
+    pr = d["path_roofline"]
+    # the whole path on the work actually run: between the dominant kernel's bytes and the
+    # full-width formula's
+    assert 0 < pr["actual_bytes_per_key"] < sum(pr["formula_bytes_per_key"].values())
+    assert 0 < pr["actual_frac_of_peak"] < 1.0
+    ps = d["paper_stats"]
+    for mode in ("single_sort", "by_prefixes"):
+        assert ps[mode]["total_ratio"] > 1.0 and ps[mode]["full_key_passes"] > ps[mode]["compressed_passes"]
+    assert d["rebuild"]["verified_ms_per_step"] >= d["rebuild"]["ms_per_step"] * 0.9
+
+
 def test_bench_sharded_line():
-    d = run_bench("--config", "2", "--steps", "3", "--warmup", "3", "--sharded")
+    d = run_bench("--config", "2", "--steps", "3", "--warmup", "3", "--sharded", "--e2e-steps", "1")
     assert d["value"] > 0 and d["config"]["n_total"] == d["config"]["n_per_rank"] and d["gpu_launches"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 16_000_000 * 8

@@ -142,7 +142,7 @@ def test_adjacent_dbits_vs_oracle(cfg):
 
 @pytest.mark.parametrize("n,fanout,fill", [(1, 64, 1.0), (64, 64, 1.0), (65, 64, 1.0), (4097, 64, 1.0),
                                            (300_000, 64, 1.0), (50_000, 14, 0.9), (20_000, 9, 0.9),
-                                           (1000, 2, 1.0)])
+                                           (1000, 2, 1.0), (30_001, 10, 0.9), (9_999, 100, 0.9)])
 def test_bulkload_vs_oracle(n, fanout, fill):
     keys = cksgen.config(5, n=n)
     perm = oracle.sort_keys(keys)
@@ -216,6 +216,66 @@ def test_rebuild_with_prior_mask():
     sub = keys[::3].copy()
     r2 = cks.build(dev(sub), prior_mask=ref["mask"])
     check_build(sub, r2)
+
+
+def _dropped_masks(keys, count):
+    """(mask = exact D minus one bit, whether the oracle's order on P_mask differs from the
+    full-key order) for up to `count` bits of D: Theorem 2 needs every D-bit."""
+    ref = oracle.first_build(keys)
+    out = []
+    for p in sorted(positions(ref["mask"]))[:count]:
+        m = ref["mask"].copy()
+        m[p >> 3] &= ~np.uint8(0x80 >> (p & 7))
+        wrong = not np.array_equal(oracle.sort_packed(oracle.compress(keys, m)), ref["perm"])
+        out.append((m, wrong))
+    return ref, out
+
+
+@pytest.mark.parametrize("cfg,n", [(3, 40_000), (5, 60_000), (1, 30_000)])
+def test_prior_mask_not_superset_is_detected(cfg, n):
+    # a stale D-bitmap (one distinction bit missing, as after an insert) must not return a
+    # wrong permutation silently: the order check reports CKS_ERANGE exactly when the
+    # compressed order differs from the full-key order (decided by the oracle)
+    keys = cksgen.config(cfg, n=n)
+    ref, cases = _dropped_masks(keys, 12)
+    assert any(w for _, w in cases), "no dropped bit changes the order: the test has no teeth"
+    d = dev(keys)
+    for m, wrong in cases:
+        if wrong:
+            with pytest.raises(cks.CksError) as ei:
+                cks.build(d, prior_mask=m)
+            assert ei.value.code == cks.CKS_ERANGE
+            with pytest.raises(cks.CksError) as ei:
+                cks.distinction_mask(d, prior_mask=m)
+            assert ei.value.code == cks.CKS_ERANGE
+        else:
+            r = cks.build(d, prior_mask=m)
+            assert np.array_equal(u32(r["perm"]), ref["perm"])
+    m_bad = next(m for m, w in cases if w)
+    with pytest.raises(cks.CksError) as ei:
+        cks.build_host(keys, prior_mask=m_bad)
+    assert ei.value.code == cks.CKS_ERANGE
+    # with the check off the library returns the compressed order as is (documented)
+    cks.set_verify(cks.VERIFY_OFF)
+    try:
+        r = cks.build(d, prior_mask=m_bad)
+        assert not np.array_equal(u32(r["perm"]), ref["perm"])
+    finally:
+        cks.set_verify(cks.VERIFY_PRIOR)
+
+
+def test_verify_always_passes_valid_builds():
+    keys = cksgen.config(4, n=50_000)
+    cks.set_verify(cks.VERIFY_ALWAYS)
+    try:
+        check_build(keys, cks.build(dev(keys)))
+        ref = oracle.first_build(keys)
+        check_build(keys, cks.build(dev(keys), prior_mask=ref["mask"]))
+    finally:
+        cks.set_verify(cks.VERIFY_PRIOR)
+    for bad in (-1, 3):
+        with pytest.raises(cks.CksError):
+            cks.set_verify(bad)
 
 
 @pytest.mark.parametrize("maker", ["empty", "one", "two_equal", "two", "all_equal", "all16", "consecutive",
@@ -424,38 +484,27 @@ def test_refine_chunk_cta_rounds(seed):
     check_build(keys, r)
 
 
-_FORCED_T_SCRIPT = r"""
-import sys, numpy as np, torch
-from paper_2009_11543_b200 import cks
-keys = np.load(sys.argv[1])
-r = cks.build(torch.from_numpy(keys).cuda(), tree=False)
-np.savez(sys.argv[2], mask=r["mask"], popcount=r["popcount"], sort_bits=r["sort_bits"],
-         perm=r["perm"].cpu().numpy(), dbit=r["dbit"].cpu().numpy(), packed=r["packed"].cpu().numpy())
-"""
-
-
 @pytest.mark.parametrize("T", [8, 16, 24, 40, 56, 64])
 @pytest.mark.parametrize("m", [72, 92])
-def test_refine_forced_round0_width(T, m, tmp_path):
+def test_refine_forced_round0_width(T, m):
     # P_M of three planes is carried through round 0 and the short ties inside a tile are
     # finished from the sorted planes (k_ref_tile): T < 32 leaves 3 remaining words, T < 64 2,
-    # T = 64 1. CKS_ROUND0_BITS is read once per process, hence the subprocess.
-    import os
-    import subprocess
-    import sys
+    # T = 64 1. cks_ctx_set_round0_bits forces T; the result must not depend on it.
     widths = [256] * (m // 8) + ([1 << (m % 8)] if m % 8 else [])
     keys = hier_keys(70_001, widths, seed=T + m, groups=(5, 30), dup_rows=900)
-    kp, rp = tmp_path / "keys.npy", tmp_path / "r.npz"
-    np.save(kp, keys)
-    env = dict(os.environ, CKS_ROUND0_BITS=str(T))
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    subprocess.run([sys.executable, "-c", _FORCED_T_SCRIPT, str(kp), str(rp)], env=env, cwd=root, check=True,
-                   timeout=300)
-    z = np.load(rp)
-    assert int(z["sort_bits"]) == m
-    r = dict(mask=z["mask"], popcount=int(z["popcount"]), perm=torch.from_numpy(z["perm"]),
-             dbit=torch.from_numpy(z["dbit"]), packed=torch.from_numpy(z["packed"]), tree=None)
+    cks.set_round0_bits(T)
+    try:
+        r = cks.build(torch.from_numpy(keys).cuda(), tree=False)
+    finally:
+        cks.set_round0_bits(0)
+    assert int(r["sort_bits"]) == m
     check_build(keys, r)
+
+
+def test_round0_bits_rejects_bad_width():
+    for bad in (4, 65, 72, 12):
+        with pytest.raises(cks.CksError):
+            cks.set_round0_bits(bad)
 
 
 def test_build_host_batch_pipelined():

@@ -52,9 +52,10 @@ def test_sharded_duplicates_and_equal_keys():
     check_slices(eq, run(eq, [3000, 3000, 3000]))
 
 
-def test_sharded_fanout_fill():
+@pytest.mark.parametrize("fanout,fill", [(14, 0.9), (10, 0.9), (100, 0.9)])
+def test_sharded_fanout_fill(fanout, fill):
     keys = cksgen.config(3, n=50_000)
-    check_slices(keys, run(keys, [20_000, 30_000], fanout=14, fill=0.9), fanout=14, fill=0.9)
+    check_slices(keys, run(keys, [20_000, 30_000], fanout=fanout, fill=fill), fanout=fanout, fill=fill)
 
 
 @pytest.mark.parametrize("bits,parts", [(23, 3), (96, 4), (200, 2), (0, 3)])

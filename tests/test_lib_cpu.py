@@ -47,7 +47,8 @@ def test_sm100a_cubin(lib):
 
 
 @pytest.mark.parametrize("n,fanout,fill", [(0, 64, 1.0), (1, 64, 1.0), (64, 64, 1.0), (65, 64, 1.0),
-                                           (50_000_000, 64, 1.0), (16_392_000, 14, 0.9), (12345, 9, 0.9)])
+                                           (50_000_000, 64, 1.0), (16_392_000, 14, 0.9), (12345, 9, 0.9),
+                                           (1000, 10, 0.9), (5000, 50, 0.9), (5000, 100, 0.9), (777, 7, 0.3)])
 def test_tree_shape_closed_form(n, fanout, fill):
     from paper_2009_11543_b200 import cks
     s = cks.bulkload_shape(n, fanout, fill)
@@ -56,6 +57,14 @@ def test_tree_shape_closed_form(n, fanout, fill):
     assert s.height == len(lv) and s.per_node == per
     assert [int(s.level_nodes[i]) for i in range(s.height)] == lv
     assert int(s.total_nodes) == sum(lv)
+
+
+def test_fill_is_double():
+    # fill crosses the ABI as a double, so the library's entries per node agree with any
+    # caller computing floor(fanout * fill) in double precision (10 x 0.9 = 9, not 8)
+    from paper_2009_11543_b200 import cks
+    for fanout, fill, per in [(10, 0.9, 9), (50, 0.9, 45), (100, 0.9, 90), (14, 0.9, 12), (9, 0.9, 8)]:
+        assert cks.bulkload_shape(100, fanout, fill).per_node == per
 
 
 @pytest.mark.parametrize("fanout,fill", [(1, 1.0), (64, 0.0), (64, 1.5), (2, 0.9)])
@@ -90,3 +99,17 @@ def test_paper_tree_shape_host():
     lv = oracle.paper_tree_levels(16_392_000, 12, 8)
     assert s.height == len(lv) and [int(s.level_nodes[i]) for i in range(s.height)] == lv
     assert s.per_node == 12 and s.reserved == 8 and int(s.total_nodes) == sum(lv)
+
+
+def test_product_build_reads_no_environment(lib):
+    # the timing-experiment knobs (one of them makes results wrong) exist only in a build
+    # with -DCKS_EXPERIMENTS=1; the product library must not contain their names
+    from paper_2009_11543_b200 import _build
+    if os.environ.get("CKS_EXPERIMENTS") == "1":
+        pytest.skip("experiments build")
+    blob = open(_build.SO, "rb").read()
+    for name in (b"CKS_LSD_DEBUG", b"CKS_LSD_ITEMS", b"CKS_REF_CTA", b"CKS_NO_TILE_RUNS", b"CKS_REFINE",
+                 b"CKS_ROUND0_BITS"):
+        assert name not in blob, name
+    out = subprocess.run(["nm", "-D", _build.SO], capture_output=True, text=True).stdout
+    assert " getenv" not in out
