@@ -10,6 +10,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 SO = os.path.join(LIBDIR, "libcks.so")
+# checked build (-DCKS_CHECKED=1): device bounds assertions, poisoned scratch, canary bands;
+# the pool has no compute-sanitizer, so tests/sanitize_cases.py runs against this one
+SO_CHECKED = os.path.join(LIBDIR, "libcks_checked.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC_FLAGS = [
@@ -24,27 +27,29 @@ def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
-def stale() -> bool:
-    if not os.path.exists(SO):
+def stale(so: str = SO) -> bool:
+    if not os.path.exists(so):
         return True
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "cks.h")]
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return SO
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    so = SO_CHECKED if checked else SO
+    if not force and not stale(so):
+        return so
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(LIBDIR, "obj_checked" if checked else "obj")
+    flags = extra_flags() + (["-DCKS_CHECKED=1"] if checked else [])
     os.makedirs(objdir, exist_ok=True)
     # one nvcc per translation unit, in parallel, then one link
     jobs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = ["nvcc", *NVCC_FLAGS, *extra_flags(), "-c", "-o", obj, src]
+        cmd = ["nvcc", *NVCC_FLAGS, *flags, "-c", "-o", obj, src]
         jobs.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
-    log = os.path.join(LIBDIR, "build.log")
+    log = os.path.join(LIBDIR, "build_checked.log" if checked else "build.log")
     failed = []
     with open(log, "w") as f:
         for cmd, obj, pr in jobs:
@@ -56,13 +61,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(err)
         if failed:
             raise RuntimeError(f"nvcc failed (see {log}):\n{failed[0][-4000:]}")
-        cmd = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", SO,
+        cmd = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", so,
                *[o for _, o, _ in jobs], "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed (see {log}):\n{r.stderr[-4000:]}")
-    return SO
+    return so
 
 
 def extra_flags() -> list[str]:

@@ -104,6 +104,14 @@ int fail(cks_ctx* c, int code, const char* fmt, ...) {
         if (r_ != CKS_OK) return r_; \
     } while (0)
 
+#if defined(CKS_CHECKED) && CKS_CHECKED
+#define CKS_CHECKED_BUILD 1
+constexpr size_t kGuardBytes = 4096;
+constexpr int kPoison = 0xA5, kCanary = 0x5A;
+#else
+#define CKS_CHECKED_BUILD 0
+#endif
+
 int ensure(cks_ctx* ctx, DevBuf& b, size_t bytes, bool zero = false) {
     if (bytes == 0) bytes = 16;
     if (b.cap >= bytes) return CKS_OK;
@@ -113,19 +121,60 @@ int ensure(cks_ctx* ctx, DevBuf& b, size_t bytes, bool zero = false) {
         b.p = nullptr;
         b.cap = 0;
     }
+#if CKS_CHECKED_BUILD
+    // checked build: no headroom, a canary band after the buffer and poisoned contents, so a
+    // write past the end or a read of never-written scratch changes a result (check_guards)
+    size_t cap = bytes;
+    cudaError_t e = cudaMalloc(&b.p, cap + kGuardBytes);
+#else
     size_t cap = bytes + bytes / 8;                          // a little headroom
     cudaError_t e = cudaMalloc(&b.p, cap);
+#endif
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(ctx, CKS_ENOMEM, "cudaMalloc(%zu): %s", cap, cudaGetErrorString(e));
     }
     b.cap = cap;
+#if CKS_CHECKED_BUILD
+    CK(cudaMemsetAsync(b.p, kPoison, cap, ctx->stream));
+    CK(cudaMemsetAsync((uint8_t*)b.p + cap, kCanary, kGuardBytes, ctx->stream));
+#endif
     if (zero) CK(cudaMemsetAsync(b.p, 0, cap, ctx->stream));
     return CKS_OK;
 }
 
 template <class T>
 T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
+
+// every scratch buffer of a context
+#define CKS_SCRATCH_LIST(c)                                                                                      \
+    {&c->occ, &c->masks8, &c->planeA, &c->planeB, &c->ridA, &c->ridB, &c->dacc, &c->moff, &c->dbit, &c->rmin0, \
+     &c->rmin1, &c->plan[0], &c->plan[1], &c->plan[2], &c->keys, &c->perm_scratch, &c->tile_off, &c->chunk_tot, \
+     &c->total, &c->pm, &c->pd, &c->cmp, &c->crid, &c->crid2, &c->posA, &c->posB, &c->posC, &c->segA, &c->segB,   \
+     &c->segC, &c->runoff, &c->runpos, &c->runoff2, &c->runpos2, &c->tie, &c->keep, &c->done, &c->mlist,         \
+     &c->wlist, &c->rcnt, &c->rtot, &c->part_in, &c->part_out, &c->anyt, &c->vbad, &c->keys2, &c->perm2}
+
+// checked build: the canary band after every scratch buffer must be intact after a call
+// (synchronises); no-op otherwise
+int check_guards(cks_ctx* ctx) {
+#if CKS_CHECKED_BUILD
+    CK(cudaStreamSynchronize(ctx->stream));
+    static thread_local uint8_t host[kGuardBytes];
+    DevBuf* bufs[] = CKS_SCRATCH_LIST(ctx);
+    for (size_t i = 0; i < sizeof(bufs) / sizeof(bufs[0]); i++) {
+        DevBuf* b = bufs[i];
+        if (!b->p) continue;
+        CK(cudaMemcpy(host, (uint8_t*)b->p + b->cap, kGuardBytes, cudaMemcpyDeviceToHost));
+        for (size_t j = 0; j < kGuardBytes; j++)
+            if (host[j] != (uint8_t)kCanary)
+                return fail(ctx, CKS_ECUDA, "checked build: write past scratch buffer #%zu (cap %zu) at +%zu", i,
+                            b->cap, j);
+    }
+#else
+    (void)ctx;
+#endif
+    return CKS_OK;
+}
 
 uint32_t popcount_mask(const uint8_t* m, uint32_t B) {
     uint32_t c = 0;
@@ -862,7 +911,8 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     ctx->verify_now = keys && (ctx->verify == CKS_VERIFY_ALWAYS || (ctx->verify == CKS_VERIFY_PRIOR && prior));
     const int rc = build_from_mask(ctx, keys, n, B, M.data(), m, out);
     ctx->verify_now = false;
-    return rc;
+    TRY(rc);
+    return check_guards(ctx);
 }
 
 }  // namespace
@@ -909,16 +959,7 @@ int cks_ctx_destroy(cks_ctx* ctx) {
     if (!ctx) return CKS_EINVAL;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    DevBuf* bufs[] = {&ctx->occ, &ctx->masks8, &ctx->planeA, &ctx->planeB, &ctx->ridA, &ctx->ridB,
-                      &ctx->dacc, &ctx->moff,
-                      &ctx->dbit, &ctx->rmin0, &ctx->rmin1, &ctx->plan[0], &ctx->plan[1], &ctx->plan[2],
-                      &ctx->keys, &ctx->perm_scratch, &ctx->tile_off, &ctx->chunk_tot, &ctx->total,
-                      &ctx->pm, &ctx->pd, &ctx->cmp, &ctx->crid, &ctx->crid2, &ctx->posA, &ctx->posB,
-                      &ctx->posC, &ctx->segA, &ctx->segB, &ctx->segC, &ctx->runoff, &ctx->runpos, &ctx->runoff2, &ctx->runpos2,
-                      &ctx->tie, &ctx->keep, &ctx->done, &ctx->mlist,
-                      &ctx->wlist,
-                      &ctx->rcnt, &ctx->rtot, &ctx->part_in, &ctx->part_out, &ctx->anyt, &ctx->vbad,
-                      &ctx->keys2, &ctx->perm2};
+    DevBuf* bufs[] = CKS_SCRATCH_LIST(ctx);
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int i = 0; i < ST_N; i++)
@@ -1065,7 +1106,7 @@ int cks_occupancy_mask(cks_ctx* ctx, const uint32_t* occ, uint32_t nocc, uint32_
     uint32_t m = 0;
     TRY(run_superset(ctx, nullptr, n_total, B, kind, mask_out, &m, /*keys_ready=*/false));
     if (popcount_out) *popcount_out = m;
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_rank_sorted(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bits, uint64_t n, const uint32_t* sorted_rid,
@@ -1077,7 +1118,7 @@ int cks_rank_sorted(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bits, 
     CK(cudaSetDevice(ctx->device));
     LAUNCH(launch_rank_sorted(sorted_packed, (bits + 31) / 32, n, sorted_rid, rid_base, queries, nq,
                               reinterpret_cast<unsigned long long*>(ranks_out), ctx->stream));
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_partition(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t n, const uint32_t* splitters,
@@ -1114,7 +1155,7 @@ int cks_partition(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t 
     TRY(run_sort(ctx, in, sp, np + 1, 1, n, nullptr, 0, out, sp, rid_out, nullptr, nullptr, 0, false));
     if (np) CK(cudaMemcpy2DAsync(packed_out, n * 4, out + sp, sp * 4, n * 4, np, cudaMemcpyDeviceToDevice, ctx->stream));
     LAUNCH(launch_add_base(rid_out, n, (uint32_t)rid_base, ctx->sms, ctx->stream));
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_sort_prefix(cks_ctx* ctx, const uint32_t* packed, const uint8_t* sort_mask, uint32_t B, uint64_t n,
@@ -1152,7 +1193,7 @@ int cks_sort_prefix(cks_ctx* ctx, const uint32_t* packed, const uint8_t* sort_ma
         CK(cudaMemcpy2DAsync(packed_out, n * 4, o.packed, o.packed_pitch * 4, n * 4, (o.popcount + 31) / 32,
                              cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout, double fill,
@@ -1164,7 +1205,7 @@ int cks_bulkload_block(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit,
     uint32_t h = 0;
     TRY(run_bulkload(ctx, perm, dbit, n, fanout, fill, out, &h, first_global != 0, levels, top_min_out));
     if (height_out) *height_out = h;
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* child_min, uint64_t nchild,
@@ -1175,7 +1216,7 @@ int cks_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* ch
     uint32_t h = 0;
     TRY(run_bulkload_top(ctx, child_rid, child_min, nchild, fanout, fill, out, &h));
     if (height_out) *height_out = h;
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_repack(cks_ctx* ctx, const uint32_t* packed_in, const uint8_t* in_mask, const uint8_t* out_mask, uint32_t B,
@@ -1198,7 +1239,7 @@ int cks_repack(cks_ctx* ctx, const uint32_t* packed_in, const uint8_t* in_mask, 
     TRY(upload_plan(ctx, 1, &dplan));
     LAUNCH(launch_repack(packed_in, n, n, dplan, ctx->h_plan[1]->nsteps, (d + 31) / 32, packed_out, n, ctx->sms,
                          ctx->stream));
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* mask,
@@ -1208,7 +1249,8 @@ int cks_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     uint32_t m = popcount_mask(mask, B);
     if (n && m && !packed_out) return fail(ctx, CKS_EINVAL, "packed_out is NULL");
     CK(cudaSetDevice(ctx->device));
-    return run_compress(ctx, keys, n, B, mask, packed_out, n);
+    TRY(run_compress(ctx, keys, n, B, mask, packed_out, n));
+    return check_guards(ctx);
 }
 
 int cks_sort(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t n, const uint32_t* row_ids,
@@ -1220,7 +1262,7 @@ int cks_sort(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t n, co
     CK(cudaSetDevice(ctx->device));
     const uint32_t np = (bits + 31) / 32, k = (bits + 7) / 8;
     TRY(run_sort(ctx, packed, n, np, k, n, row_ids, 4, sorted_packed_out, n, perm_out, nullptr, nullptr));
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_adjacent_dbits(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bits, uint64_t n,
@@ -1234,7 +1276,7 @@ int cks_adjacent_dbits(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t bit
     CK(cudaSetDevice(ctx->device));
     TRY(run_adjacent(ctx, sorted_packed, n, bits, n, sort_mask, B, mask_out, dbit_out));
     if (popcount_out) *popcount_out = popcount_mask(mask_out, B);
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_bulkload_shape(uint64_t n, uint32_t fanout, double fill, cks_tree_shape* out) {
@@ -1285,7 +1327,7 @@ int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, co
     CK(launch_ptree(keys, n, B, perm, dbit, pk_bits, s.per_node, s.reserved, s.level_nodes, s.level_offset,
                     s.height, nodes, as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl));
     ctx->launches += (uint64_t)nl;
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint64_t n, uint32_t fanout,
@@ -1294,7 +1336,8 @@ int cks_bulkload(cks_ctx* ctx, const uint32_t* perm, const uint16_t* dbit, uint6
     if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
     if (n && !perm) return fail(ctx, CKS_EINVAL, "perm is NULL");
     CK(cudaSetDevice(ctx->device));
-    return run_bulkload(ctx, perm, dbit, n, fanout, fill, out, nullptr);
+    TRY(run_bulkload(ctx, perm, dbit, n, fanout, fill, out, nullptr));
+    return check_guards(ctx);
 }
 
 int cks_distinction_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* prior,
@@ -1313,7 +1356,7 @@ int cks_distinction_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t
     }
     TRY(build_common(ctx, keys, n, B, prior, &o, true));
     if (popcount_out) *popcount_out = o.popcount;
-    return CKS_OK;
+    return check_guards(ctx);
 }
 
 int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* prior,

@@ -6,6 +6,16 @@
 
 #define CKS_NONE_INTERNAL 0xFFFFu
 
+// Checked build (-DCKS_CHECKED=1, lib/libcks_checked.so; the pool has no compute-sanitizer):
+// device-side bounds assertions at the computed-index stores, poisoned scratch and canary
+// bands after every scratch buffer (cks_api.cu). The product build compiles them out.
+#if defined(CKS_CHECKED) && CKS_CHECKED
+#include <assert.h>
+#define CKS_DCHECK(c) assert(c)
+#else
+#define CKS_DCHECK(c) ((void)0)
+#endif
+
 namespace cks {
 
 constexpr uint32_t kMaxKeyBytes = 512;

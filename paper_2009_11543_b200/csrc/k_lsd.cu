@@ -371,6 +371,7 @@ k_downsweep(const LsdPassArgs a) {
                     from[r] = s_src[s];
                     const uint32_t w = *reinterpret_cast<const uint32_t*>(slot + from[r]);
                     dest[r] = s + s_gb[digit_of(w, sel)];
+                    CKS_DCHECK(dest[r] < n);
                     out[dest[r]] = w;
                 }
             }
@@ -606,9 +607,11 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
             named_sync(1, kRT);
             uint16_t* src = s_src + buf * TILE;
 #pragma unroll
-            for (int i = 0; i < RI; i++)
+            for (int i = 0; i < RI; i++) {
+                CKS_DCHECK(pos[i] + h[dg[i]] < (uint32_t)TILE);
                 src[(kLsdDebug && (a.debug & 2)) ? wofs + i * 32 + lane : pos[i] + h[dg[i]]] =
                     (uint16_t)((wofs + i * 32 + lane) * 4);
+            }
             __syncwarp();
             if (lane == 0) bar_arrive(&s_ranked[buf]);
         }
@@ -636,6 +639,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
                 const uint32_t w = *reinterpret_cast<const uint32_t*>(sl + from[r]);
                 dest[r] = (kLsdDebug && (a.debug & 1)) ? tile * (uint32_t)TILE + r * SH::WT + wt
                                                        : r * SH::WT + wt + s_gb[buf][digit_of(w, sel)];
+                CKS_DCHECK(dest[r] < a.n);
                 out[dest[r]] = w;
             }
             __syncwarp();

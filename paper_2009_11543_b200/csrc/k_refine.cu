@@ -291,6 +291,7 @@ __device__ __forceinline__ uint32_t rem_word(const RunCtx& R, int c, uint32_t p,
 template <int W>
 __device__ __forceinline__ void put_elem(const RunCtx& R, uint32_t p, const uint32_t (&w)[W], uint32_t row,
                                          const uint32_t* prev, uint32_t* s_bm) {
+    CKS_DCHECK(p < R.pitch && row < R.pitch);
     R.perm[p] = row;
     if (R.carried)                                   // the carried planes follow their rows
         for (int c = 0; c <= R.qtop && c < W; c++) {
@@ -595,6 +596,7 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
             if (u < npair) r = key_less(i == a ? a + 1 : a, i, ki, ri) ? 1u : 0u;
             else
                 for (uint32_t k = a; k < a + L; k++) r += key_less(k, i, ki, ri) ? 1u : 0u;   // (k == i: false)
+            CKS_DCHECK(r < L && a + L <= (uint32_t)kTileKeys);
             s_at[tpad(a + r)] = (uint16_t)i;
         }
         if (threadIdx.x == 0) s_cnt += nmem;
@@ -619,6 +621,7 @@ k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigne
                 uint16_t db = t ? (uint16_t)CKS_NONE_INTERNAL : odb[j];
                 if (hm >> j & 1) {
                     src = s_at[tpad(dd)];
+                    CKS_DCHECK(src < (uint32_t)kTileKeys && src >= (uint32_t)ra[j] && src < (uint32_t)re[j]);
                     if (t) {                                  // after the run's first position
                         const uint32_t pj = s_at[tpad(dd - 1)];
                         const unsigned long long x = s_key[tpad(pj)] ^ s_key[tpad(src)];
@@ -992,6 +995,7 @@ k_ref_put(uint32_t* __restrict__ perm, const uint32_t* __restrict__ pos, const u
           const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, uint32_t* __restrict__ carried) {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = pos[k], r = rid[k];
+        CKS_DCHECK(p < pitch && r < pitch);
         perm[p] = r;
         if (carried)
             for (uint32_t q = 0; q < np; q++) carried[(uint64_t)q * pitch + p] = __ldg(pm + (uint64_t)q * pitch + r);

@@ -1,4 +1,6 @@
-"""Small builds for compute-sanitizer (scripts/sanitize.sh): every kernel family of the path
+"""Small builds for the checked library (lib/libcks_checked.so: device bounds assertions,
+poisoned scratch, canary bands after every scratch buffer; this pool has no compute-sanitizer)
+and, where available, compute-sanitizer (scripts/sanitize.sh): every kernel family of the path
 runs at least once -- cfg1 (plain LSD sort, 16-B keys), cfg5 and cfg3 samples (refinement,
 k_ref_tile, compaction, short-run finishers), cfg4 (LSD refinement rounds), the edge sets
 (empty, one key, all equal, odd widths, unaligned keys), the order check and its negative
@@ -18,7 +20,26 @@ import torch  # noqa: E402
 
 import cksgen  # noqa: E402
 import oracle  # noqa: E402
-from paper_2009_11543_b200 import cks  # noqa: E402
+from paper_2009_11543_b200 import _build, cks  # noqa: E402
+
+CANARY = 0x3C3C3C3C
+
+
+def guarded_build(keys_d, prior=None):
+    """cks_build into caller buffers with a canary tail: the library must write exactly n
+    entries of perm and dbit (and the tree arrays they size)."""
+    n, B = keys_d.shape
+    b = cks.Builder(n, B, keys_d.device)
+    big_p = torch.full((n + 4096,), CANARY, dtype=torch.int32, device=keys_d.device)
+    big_d = torch.full((n + 4096,), 0x3C3C, dtype=torch.int16, device=keys_d.device)
+    b.perm, b.dbit = big_p[:max(n, 1)], big_d[:max(n, 1)]
+    b.out.perm, b.out.dbit = big_p.data_ptr(), big_d.data_ptr()
+    b(keys_d, prior)
+    torch.cuda.synchronize()
+    assert bool((big_p[n:] == CANARY).all()), "perm written past n"
+    assert bool((big_d[n:] == 0x3C3C).all()), "dbit written past n"
+    o = b.out
+    return dict(mask=b.mask.copy(), popcount=int(o.popcount), perm=big_p[:n], dbit=big_d[:n], packed=b.packed())
 
 
 def u32(t):
@@ -42,7 +63,7 @@ def main(quick: bool):
              ("empty", np.zeros((0, 16), np.uint8)), ("one", cksgen.config(1, n=1)),
              ("all_equal", cksgen.all_equal(5000, 24, 3)), ("odd13", cksgen.uniform(9001, 13, 5, 20000))]
     for name, keys in cases:
-        r = cks.build(torch.from_numpy(np.ascontiguousarray(keys)).cuda())
+        r = guarded_build(torch.from_numpy(np.ascontiguousarray(keys)).cuda())
         torch.cuda.synchronize()
         check(keys, r)
         print("ok", name, keys.shape, flush=True)
@@ -87,4 +108,11 @@ def main(quick: bool):
 
 
 if __name__ == "__main__":
-    main(len(sys.argv) > 1 and sys.argv[1] == "quick")
+    args = sys.argv[1:]
+    if "product" not in args:                          # default: the checked library
+        if not os.path.exists(_build.SO_CHECKED):
+            _build.build(checked=True)
+        cks.load_library(_build.SO_CHECKED)
+        print("library:", _build.SO_CHECKED, flush=True)
+    main("quick" in args)
+    print("all cases ok", flush=True)

@@ -322,6 +322,28 @@ def test_build_repeatable_and_stream():
     assert np.array_equal(a["mask"], b["mask"])
 
 
+@pytest.mark.parametrize("cfg,n", [(5, 2_000_003), (3, 1_500_001)])
+def test_repeated_builds_under_contention(cfg, n):
+    # race stress (the pool has no racecheck): the warp-specialised pass hands tiles between
+    # producer, rankers and writers through mbarriers, and k_ref_tile works in shared memory;
+    # 12 builds with a matmul stream competing for the SMs must all equal the oracle
+    keys = cksgen.config(cfg, n=n)
+    ref = oracle.first_build(keys, threads=oracle.threads_default())
+    d = dev(keys)
+    side = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    for i in range(12):
+        if i % 2:
+            with torch.cuda.stream(side):
+                for _ in range(4):
+                    a = (a @ a).clamp_(-1, 1)
+        r = cks.build(d, tree=False)
+        assert np.array_equal(u32(r["perm"]), ref["perm"]), i
+        assert np.array_equal(u16(r["dbit"]), ref["dbit"]), i
+        assert np.array_equal(r["mask"], ref["mask"]), i
+    torch.cuda.synchronize()
+
+
 # ---- full-size configs (the launch configuration bench.py times) ----------------------------
 
 def verify_sorted_perm(keys, perm):
@@ -539,3 +561,16 @@ def test_build_unaligned_keys():
     view = buf[3:].view(keys.shape[0], keys.shape[1])
     view.copy_(dev(keys))
     check_build(keys, cks.build(view))
+
+
+def test_checked_library_cases():
+    # the bounds-checked build (device asserts at computed-index stores, poisoned scratch,
+    # canary bands) over every kernel family; a failed assert or canary is a non-zero exit
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "sanitize_cases.py"), "quick"], cwd=root,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "libcks_checked.so" in r.stdout and "all cases ok" in r.stdout
