@@ -18,6 +18,10 @@
  *   cfg3  n x 32 B title-like NUL-padded strings (lognormal length, Zipf first char)
  *   cfg4  n x 64 B URL-like NUL-padded strings (200 Zipf hosts + random path)
  *   cfg5  n x 32 B ACGT 32-mers from a 4n-base sequence with 10% copied repeats
+ *   Zipf(s,n,m)  the paper's sensitivity-analysis family (Sec. 6.4):
+ *         n-byte keys; in every 8-byte word the first m bytes hold one fixed ASCII
+ *         character and the other 8-m bytes lower-case letters drawn from Zipf(s, 26)
+ *         (rank 1 = 'a', ..., rank 26 = 'z'); 10 M keys in the paper
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -210,6 +214,22 @@ int cksgen_genome(uint64_t seed, uint64_t n, uint32_t B, uint8_t* out) {
         memcpy(out + (uint64_t)i * B, seq + st, B);
     }
     free(seq);
+    return 0;
+}
+
+/* Zipf(s, B, m): every 8-byte word of a key = m copies of `fixed`, then
+ * 8 - m letters 'a' + (rank - 1) with rank ~ Zipf(s, 26); a trailing partial word likewise */
+int cksgen_zipf(uint64_t seed, uint64_t n, uint32_t B, double s, uint32_t m, uint8_t fixed, uint8_t* out) {
+    if ((!out && n) || B == 0 || m > 8 || !(s > 0.0)) return -1;
+    double cdf[26];
+    zipf_cdf(s, 26, cdf);
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < (int64_t)n; i++) {
+        rowrng r = { draw(seed, 30, (uint64_t)i) };
+        uint8_t* row = out + (uint64_t)i * B;
+        for (uint32_t j = 0; j < B; j++)
+            row[j] = (j % 8) < m ? fixed : (uint8_t)('a' + zipf_pick(cdf, 26, rr_unif(&r)));
+    }
     return 0;
 }
 
