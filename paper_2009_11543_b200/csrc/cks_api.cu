@@ -53,7 +53,7 @@ struct cks_ctx {
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
         pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, runoff2, runpos2, tie, keep, done, mlist, wlist, rcnt, rtot,   // NEXT-1
         part_in, part_out,                                                 // NEXT-4
-        anyt,                                                              // k_ref_tile: tiles with ties left
+        anyt,                                                              // k_ref_reg: compaction tiles with ties left
         vbad,                                                              // k_verify_order result
         keys2, perm2;                                                      // cks_build_host_batch: 2nd buffers
     // pinned host staging

@@ -7,7 +7,7 @@
 //   round 0  LSD-sort all keys by the top T <= 64 bits (k_lsd.cu; T from a sample), carrying
 //            that chunk + row id (and all of P_M when it has three planes);
 //   round r  the keys whose prefix ties with a neighbour ("runs") are finished by comparing
-//            their remaining bits when the run is short (k_ref_tile in-tile after round 0
+//            their remaining bits when the run is short (k_ref_reg in registers after round 0
 //            with P_M carried; k_ref_local / k_ref_warp / k_ref_cta from the compacted list),
 //            and the long runs are re-sorted by (run, next 64 bits): one CTA per run when
 //            every run fits (k_ref_cta_chunk), else a compact list (chunk of P_M by row id,
@@ -18,12 +18,14 @@
 // (P:479): D_i = moff[64 r + clz64(chunk_i XOR chunk_{i-1})]. Pairs equal in every chunk
 // are duplicates (D_i = none, reading R3). The union of the D_i is the exact D.
 //
-// Kernels: k_ref_adj (round adjacency: D_i, tie flags, D accumulation), k_ref_tile (round-0
+// Kernels: k_ref_adj (round adjacency: D_i, tie flags, D accumulation), k_ref_reg (round-0
 // adjacency fused with the in-tile short runs), k_ref_count / k_ref_scan / k_ref_scatter
 // (compaction of the tied runs into the next round's list), k_ref_local / k_ref_warp /
 // k_ref_cta (short and medium runs), k_ref_keep, k_ref_cta_chunk, k_ref_gather (chunk r of
 // the listed rows), k_ref_put (sorted row ids back into place), k_prefix_sample (T).
 #include <stdlib.h>
+
+#include <type_traits>
 
 #include "cks_internal.h"
 
@@ -320,22 +322,9 @@ __device__ __forceinline__ bool key_less(const uint32_t (&a)[W], uint32_t ra, co
     return ra < rb;
 }
 
-// Round-0 adjacency fused with finishing the short runs that lie inside one tile of the
-// sorted order (most runs, when round 0 leaves many small ties). Tile of kTileKeys positions
-// per CTA iteration:
-//   1. tie flags / adjacency D_i of every position from the top T bits (as k_ref_adj, round 0);
-//   2. runs that start and end inside the tile and have at most kTileRun keys are "handled":
-//      each member ranks itself in its run by (remaining P_M words, row id) -- the same total
-//      order as k_ref_local -- reading the words from the carried planes (kept in shared
-//      memory) or from P_M by row id;
-//   3. the handled runs are written back in sorted order (row ids, carried planes, D_i of every
-//      member after the first) and their tie flags cleared, so the compaction that follows
-//      sees only the runs left (crossing a tile edge, longer, or too many remaining words).
-// A member's top T bits equal its run's, so a neighbouring tile reading this tile's edge
-// position for its own adjacency sees the same masked bits before or after the rewrite.
+// Positions handled per CTA / per thread by the round-0 finisher (k_ref_reg).
 constexpr int kTileKeys = 2048;
 constexpr int kTileItems = kTileKeys / kRefThreads;     // consecutive positions per thread (8)
-constexpr uint32_t kTileRun = 8;
 
 // 8 consecutive u32 (positions p0..p0+7, p0 % 8 == 0) -- two 16-byte accesses when the whole
 // group is in range and `vec` (16-byte aligned arrays), else element by element
@@ -359,318 +348,310 @@ __device__ __forceinline__ void st8(uint32_t* a, uint64_t p0, uint64_t n, bool v
     }
 }
 
-__device__ __forceinline__ uint32_t tpad(uint32_t i) { return i + (i >> 5); }   // thread-of-8 layout, conflict-free
-constexpr int kTilePad = kTileKeys + kTileKeys / 32;
-
-constexpr size_t tile_smem_bytes(int wc) {
-    return (size_t)kTilePad * 8 + (size_t)wc * kTilePad * 4 + (size_t)kTilePad * 4 + (size_t)kTileKeys * 4 +
-           (size_t)kTilePad * 2;
+// Round-0 adjacency fused with finishing the short runs one thread holds (registers only; it
+// replaces a shared-memory tile kernel with block scans and a member list, 0.65 -> 0.48 ms on
+// cfg5 -- DESIGN.md Sec. 6.2). Thread = 8 consecutive
+// sorted positions, CTA = 2048:
+//   1. tie flag of every position against its predecessor on the top T bits, D_i of the others
+//      (moff of the first differing P_M bit);
+//   2. tied runs that lie inside the thread's 8 positions are sorted in registers by (remaining
+//      P_M words, row id) -- the stable order -- with an odd-even transposition network whose
+//      comparator (j, j+1) is enabled only when j+1 ties with j inside such a run;
+//   3. runs of exactly two keys across two neighbouring lanes take one compare-exchange over
+//      shuffles;
+//   4. the members' D_i (first differing remaining bit, none for equal keys) are written and
+//      their tie flags cleared. Runs crossing a thread boundary with 3+ keys, or a warp
+//      boundary, keep their tie flags for the compaction that follows (round 1: k_ref_local /
+//      k_ref_warp / k_ref_cta), as do runs longer than a thread.
+// Remaining key of a position (WC = qtop + 1 words, planes qtop .. 0 of the carried sorted P_M,
+// word 0 masked by fmask): WC 1: k = w0; WC 2: k = w0:w1; WC 3: k = w0:w1, x = w2.
+template <int WC>
+__device__ __forceinline__ bool rk_less(unsigned long long ka, uint32_t xa, uint32_t ra, unsigned long long kb,
+                                        uint32_t xb, uint32_t rb) {
+    if (ka != kb) return ka < kb;
+    if (WC == 3 && xa != xb) return xa < xb;
+    return ra < rb;
 }
 
-// WC: remaining words (= qtop + 1, 1..3), all carried in sorted order. (A variant reading
-// them from P_M by row id for wider keys measured slower than the compaction + k_ref_local
-// path, which those keys keep.) Thread t owns the 8 consecutive positions [8t, 8t+8) of the tile;
-// run bounds come from two block scans (last run start at or before a position, first run
-// start after it), so a member needs no walk over the tie flags.
 template <int WC>
 __global__ void __launch_bounds__(kRefThreads, 3)
-k_ref_tile(RunCtx R, const uint32_t* lo, const uint32_t* hi, uint64_t n, unsigned long long cmask, uint32_t nwords,
-           bool vec, uint8_t* __restrict__ tie, uint32_t* __restrict__ dacc, uint32_t* __restrict__ handled,
-           uint8_t* __restrict__ any, bool alias) {
+k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, uint64_t n,
+          unsigned long long cmask, bool vec, uint8_t* __restrict__ tie, uint32_t* __restrict__ dacc,
+          uint32_t* __restrict__ handled, uint8_t* __restrict__ any) {
     static_assert(WC >= 1 && WC <= 3, "carried remaining words");
-    constexpr int NWS = WC;
-    constexpr int NWARP = kRefThreads / 32;
-    __shared__ uint32_t s_pm[3];                         // D of the CTA as P_M bit indices
-    extern __shared__ __align__(16) unsigned char s_tiledyn[];            // tile_smem_bytes(WC)
-    unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_tiledyn);   // members: words 0 (masked), 1
-    uint32_t (*s_w)[kTilePad] = reinterpret_cast<uint32_t (*)[kTilePad]>(s_key + kTilePad);   // carried words
-    uint32_t* s_row = s_w[NWS];                                           // [kTilePad] row ids
-    uint32_t* s_mem = s_row + kTilePad;                  // members: tile index | run start << 11 | length << 22
-    uint16_t* s_at = reinterpret_cast<uint16_t*>(s_mem + kTileKeys);     // run-order position -> tile index
-    __shared__ unsigned long long s_last[kRefThreads];
-    __shared__ int s_wmax[NWARP], s_wmin[NWARP], s_wcnt[NWARP];
-    __shared__ uint32_t s_cnt, s_tnext;
+    constexpr int I = kTileItems;                                 // 8 positions per thread
+    __shared__ uint32_t s_pm[3];                                  // D of the CTA as P_M bit indices
+    __shared__ uint32_t s_cnt;
     if (threadIdx.x < 3) s_pm[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_cnt = 0;
-    const int Wr = R.qtop + 1;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
-    auto top = [&](uint64_t k) -> unsigned long long {
-        return (((unsigned long long)hi[k] << 32) | (lo ? (unsigned long long)lo[k] : 0ull)) & cmask;
-    };
-    auto word = [&](int c, uint32_t i) -> uint32_t {      // remaining word c of tile element i
-        return c == 0 ? s_w[0][tpad(i)] & R.fmask : s_w[c < NWS ? c : 0][tpad(i)];
-    };
-    // remaining key of element i for ordering: words 0 (masked) and 1 in s_key; word 2 (WC == 3)
-    // only where s_key ties
-    auto key_less = [&](uint32_t k, uint32_t i, unsigned long long ki, uint32_t ri) -> bool {
-        const unsigned long long kk = s_key[tpad(k)];
-        if (kk != ki) return kk < ki;
-        if (WC == 3) {
-            const uint32_t a2 = s_w[NWS - 1][tpad(k)], b2 = s_w[NWS - 1][tpad(i)];
-            if (a2 != b2) return a2 < b2;
-        }
-        return s_row[tpad(k)] < ri;
-    };
-    // D found by this thread, as P_M bit indices (m <= 96: three words in registers), mapped
-    // to key bits through moff once per CTA at the end
-    uint32_t dm0 = 0, dm1 = 0, dm2 = 0;
-    auto mark_pm = [&](uint32_t i) {
-        const uint32_t w = i >> 5, bit = 1u << (i & 31);
-        dm0 |= w == 0 ? bit : 0u;
-        dm1 |= w == 1 ? bit : 0u;
-        dm2 |= w == 2 ? bit : 0u;
-    };
-    const uint32_t i0 = threadIdx.x * kTileItems;
-    uint64_t p0 = 0;
-    // tie flags left in the compaction tile of position p0 (for k_ref_count / k_ref_scatter to
-    // skip tie-free tiles); a flag at a compaction tile's first position also concerns the
-    // tile before (its last key may start that run)
-    auto mark_any = [&](uint32_t tied, uint32_t first) {
-        if (!any || !tied) return;
-        const uint64_t c = p0 / kRefTile;
-        any[c] = 1;
-        if (first && c && p0 % kRefTile == 0) any[c - 1] = 1;
-    };
     __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    // persistent CTAs: D and the counts are reduced once per CTA, not per tile (one global atomic
+    // per D-bit per CTA)
+    unsigned long long dlo = 0;
+    uint32_t dhi = 0, hm = 0;
+    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t t0 = tile * kTileKeys;
-        const uint32_t tn = (uint32_t)(n - t0 < (uint64_t)kTileKeys ? n - t0 : (uint64_t)kTileKeys);
-        p0 = t0 + i0;
-        // A. loads: top bits, row ids, carried words
-        uint32_t vh[kTileItems], vl[kTileItems], vr[kTileItems];
+        const uint64_t p0 = (tile * kRefThreads + threadIdx.x) * I;
+        auto top = [&](uint64_t k) -> unsigned long long {
+            return (((unsigned long long)__ldg(hi + k) << 32) | (unsigned long long)__ldg(lo + k)) & cmask;
+        };
+        // A. loads: chunk words (hi = plane 2, lo = plane 1 of the carried planes), row ids, plane 0
+        uint32_t vh[I], vl[I], vr[I], v0[I];
         ld8(hi, p0, n, vec, vh);
-        if (lo) ld8(lo, p0, n, vec, vl);
+        ld8(lo, p0, n, vec, vl);
         ld8(R.perm, p0, n, vec, vr);
-        unsigned long long tk[kTileItems];
-#pragma unroll
-        for (int j = 0; j < kTileItems; j++) {
-            tk[j] = (((unsigned long long)vh[j] << 32) | (lo ? (unsigned long long)vl[j] : 0ull)) & cmask;
-            s_row[tpad(i0 + j)] = vr[j];
-        }
-        {
-#pragma unroll
-            for (int c = 0; c < NWS; c++) {
-                // plane qtop-c: with the chunk planes carried (hi = plane 2, lo = plane 1) the
-                // words of planes 2 and 1 are already in registers
-                const int q = WC - 1 - c;
-                if (alias && (q == 2 || q == 1)) {
-#pragma unroll
-                    for (int j = 0; j < kTileItems; j++) s_w[c][tpad(i0 + j)] = q == 2 ? vh[j] : vl[j];
-                    continue;
-                }
-                uint32_t vw[kTileItems];
-                ld8(R.carried + (uint64_t)q * R.pitch, p0, n, vec, vw);
-#pragma unroll
-                for (int j = 0; j < kTileItems; j++) s_w[c][tpad(i0 + j)] = vw[j];
-            }
-        }
-        s_last[threadIdx.x] = tk[kTileItems - 1];
-        if (threadIdx.x == 0) s_tnext = (t0 + tn < n && top(t0 + tn) == top(t0 + tn - 1)) ? 1u : 0u;
-        const unsigned long long left = (threadIdx.x == 0 && t0 > 0) ? top(t0 - 1) : 0ull;
-        __syncthreads();
-        // B. tie flags, adjacency D_i, run starts (positions past n count as starts)
-        unsigned long long prev = threadIdx.x ? s_last[threadIdx.x - 1] : left;
-        uint32_t tb = 0;                                  // bit j: position i0+j ties with its predecessor
-        uint16_t odb[kTileItems];
-#pragma unroll
-        for (int j = 0; j < kTileItems; j++) {
-            const uint64_t p = p0 + j;
+        if (WC >= 1) ld8(R.carried, p0, n, vec, v0);                  // plane 0
+        const uint32_t vm = p0 >= n ? 0u : (p0 + I <= n ? 0xFFu : (1u << (uint32_t)(n - p0)) - 1u);
+        unsigned long long tk[I];
+    #pragma unroll
+        for (int j = 0; j < I; j++) tk[j] = (((unsigned long long)vh[j] << 32) | vl[j]) & cmask;
+        // neighbours across the thread: the previous position's top bits, the next's tie
+        unsigned long long tprev = __shfl_up_sync(0xffffffffu, tk[I - 1], 1);
+        if (lane == 0 && p0 > 0 && p0 - 1 < n) tprev = top(p0 - 1);
+        // B. tie bits (position j ties with j-1) and D_i of the others from the top T bits
+        uint32_t tb = 0;
+        uint16_t odb[I];
+    #pragma unroll
+        for (int j = 0; j < I; j++) {
+            const unsigned long long pv = j ? tk[j - 1] : tprev;
             odb[j] = CKS_NONE_INTERNAL;
-            if (p > 0 && p < n) {
-                const unsigned long long x = tk[j] ^ prev;
+            if ((vm >> j & 1) && p0 + j > 0) {
+                const unsigned long long x = tk[j] ^ pv;
                 if (x) {
-                    const uint32_t pmb = (uint32_t)__clzll((long long)x);
+                    const uint32_t pmb = (uint32_t)__clzll((long long)x);   // < T <= 64
                     odb[j] = __ldg(R.moff + pmb);
-                    mark_pm(pmb);
+                    dlo |= 1ull << pmb;
                 } else {
                     tb |= 1u << j;
                 }
             }
-            prev = tk[j];
         }
-        const uint32_t sb = ~tb & 0xFFu;                  // run starts
-        int lst = sb ? (int)(i0 + 31 - __clz(sb)) : -1;  // last start in this thread
-        int fst = sb ? (int)(i0 + __ffs(sb) - 1) : kTileKeys + 1;   // first start
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, lst, o), z = __shfl_down_sync(0xffffffffu, fst, o);
-            if (lane >= (uint32_t)o) lst = max(lst, y);
-            if (lane + o < 32) fst = min(fst, z);
+        const uint32_t tbn = __shfl_down_sync(0xffffffffu, tb, 1);      // next lane's tie bits
+        bool tie_next = lane < 31 ? (tbn & 1u) != 0 : false;
+        if (lane == 31 && (vm >> (I - 1) & 1) && p0 + I < n) tie_next = top(p0 + I) == tk[I - 1];
+        // C. runs inside the thread: links L (bit j: j ties with j-1, j >= 1); runs open to the left
+        // (position 0 ties with the previous lane) or right (the next lane's first position ties
+        // with position 7) are not finished here
+        const uint32_t L = tb & 0xFEu;
+        uint32_t hl = L;
+        if (tb & 1u) {                                                // run through position 0
+            const uint32_t e = (uint32_t)__ffs(~(L | 1u)) - 1u;       // first position after it
+            hl &= ~(((1u << e) - 1u) & ~1u);
         }
-        if (lane == 31) s_wmax[warp] = lst;
-        if (lane == 0) s_wmin[warp] = fst;
-        int inA = __shfl_up_sync(0xffffffffu, lst, 1), outE = __shfl_down_sync(0xffffffffu, fst, 1);
-        if (lane == 0) inA = -1;
-        if (lane == 31) outE = kTileKeys + 1;
-        __syncthreads();
-        for (uint32_t w = 0; w < warp; w++) inA = max(inA, s_wmax[w]);
-        for (uint32_t w = warp + 1; w < NWARP; w++) outE = min(outE, s_wmin[w]);
-        // C. handled members: the run [a, e) lies in the tile, 2 <= e - a <= kTileRun
-        uint32_t hm = 0;
-        int ra[kTileItems], re[kTileItems];
+        if (tie_next) {                                               // run through position 7
+            const uint32_t s = 31u - (uint32_t)__clz(~L & 0xFFu);     // its first position
+            hl &= ~(0xFFu & ~((2u << s) - 1u));
+        }
+        // remaining keys (plane q of position j: q = 2 -> vh, 1 -> vl, 0 -> v0; q compile-time)
+    #define CKS_PV(q, j) ((q) == 2 ? vh[j] : (q) == 1 ? vl[j] : v0[j])
+        unsigned long long key[I];
+        uint32_t kx[I], topw[I];                                      // topw: word 0's chunk bits (equal in a run)
+    #pragma unroll
+        for (int j = 0; j < I; j++) {
+            const uint32_t w = CKS_PV(WC - 1, j);                     // plane qtop = WC - 1
+            topw[j] = w & ~R.fmask;
+            const uint32_t w0 = w & R.fmask;
+            if (WC == 1) key[j] = w0;
+            else key[j] = ((unsigned long long)w0 << 32) | CKS_PV(WC - 2, j);
+    #undef CKS_PV
+            kx[j] = WC == 3 ? v0[j] : 0u;
+        }
+        // D. odd-even transposition network over the handled runs: L phases sort runs of up to L
+        // keys, so the warp runs as many phases as its longest handled run (mostly 2-4), each
+        // comparator a branch-free select
+        bool changed = false;
+        uint32_t runmax = 0;                                          // longest handled run (keys)
         {
-            int a = inA;
-#pragma unroll
-            for (int j = 0; j < kTileItems; j++) {
-                if (sb >> j & 1) a = (int)(i0 + j);
-                ra[j] = a;
+            uint32_t h = hl, len = 1;
+    #pragma unroll
+            for (int j = 1; j < I; j++) {
+                len = (h >> j & 1u) ? len + 1 : 1u;
+                runmax = len > runmax ? len : runmax;
             }
-            int e = outE;
-#pragma unroll
-            for (int j = kTileItems - 1; j >= 0; j--) {
-                re[j] = e;
-                if (sb >> j & 1) e = (int)(i0 + j);
+            if (!hl) runmax = 0;
+        }
+        const uint32_t phases = __reduce_max_sync(0xffffffffu, runmax);
+        auto cex = [&](int j) {
+            const bool sw = (hl >> (j + 1) & 1u) && rk_less<WC>(key[j + 1], kx[j + 1], vr[j + 1], key[j], kx[j], vr[j]);
+            const unsigned long long ka = key[j], kb = key[j + 1];
+            key[j] = sw ? kb : ka;
+            key[j + 1] = sw ? ka : kb;
+            if (WC == 3) {
+                const uint32_t xa = kx[j], xb = kx[j + 1];
+                kx[j] = sw ? xb : xa;
+                kx[j + 1] = sw ? xa : xb;
+            }
+            const uint32_t ra = vr[j], rb = vr[j + 1];
+            vr[j] = sw ? rb : ra;
+            vr[j + 1] = sw ? ra : rb;
+            changed |= sw;
+        };
+        for (uint32_t ph = 0; ph < phases; ph += 2) {
+    #pragma unroll
+            for (int j = 0; j + 1 < I; j += 2) cex(j);
+            if (ph + 1 < phases) {
+    #pragma unroll
+                for (int j = 1; j + 1 < I; j += 2) cex(j);
             }
         }
-        const bool ok_words = Wr == WC;
-#pragma unroll
-        for (int j = 0; j < kTileItems; j++) {
-            int e = re[j] > (int)tn ? (int)tn : re[j];
-            const bool closed = e < (int)tn || !s_tnext;
-            if (ok_words && ra[j] >= 0 && closed && e - ra[j] >= 2 && e - ra[j] <= (int)kTileRun) {
-                hm |= 1u << j;
-                re[j] = e;
-                const uint32_t w0 = s_w[0][tpad(i0 + j)], w1 = WC >= 2 ? s_w[1][tpad(i0 + j)] : 0u;
-                s_key[tpad(i0 + j)] = ((unsigned long long)(w0 & R.fmask) << 32) | w1;
-            }
-        }
-        // member list, pair members first: block exclusive scan of the per-thread counts
-        // (pairs in the low 16 bits, longer runs' members in the high)
-        uint32_t h2 = 0;
-#pragma unroll
-        for (int j = 0; j < kTileItems; j++)
-            if ((hm >> j & 1) && re[j] - ra[j] == 2) h2 |= 1u << j;
-        const uint32_t mc = (uint32_t)__popc(h2) | ((uint32_t)__popc(hm & ~h2) << 16);
-        uint32_t mo = mc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, mo, o);
-            if (lane >= (uint32_t)o) mo += y;
-        }
-        if (lane == 31) s_wcnt[warp] = (int)mo;
-        mo -= mc;
-        __syncthreads();
-        uint32_t tot = 0;
-        for (uint32_t w = 0; w < NWARP; w++) {
-            if (w < warp) mo += (uint32_t)s_wcnt[w];
-            tot += (uint32_t)s_wcnt[w];
-        }
-        const uint32_t npair = tot & 0xFFFFu, nmem = npair + (tot >> 16);
-        if (nmem == 0) {                                  // nothing to reorder: flags and D_i only
-            uint32_t ot[2] = {0, 0};
-#pragma unroll
-            for (int j = 0; j < kTileItems; j++) ot[j >> 2] |= (tb >> j & 1u) << (8 * (j & 3));
-            if (vec && p0 + kTileItems <= n) {
-                *reinterpret_cast<uint2*>(tie + p0) = make_uint2(ot[0], ot[1]);
-                *reinterpret_cast<uint4*>(R.dbit + p0) = make_uint4(
-                    (tb & 1 ? 0xFFFFu : odb[0]) | ((uint32_t)(tb & 2 ? 0xFFFFu : odb[1]) << 16),
-                    (tb & 4 ? 0xFFFFu : odb[2]) | ((uint32_t)(tb & 8 ? 0xFFFFu : odb[3]) << 16),
-                    (tb & 16 ? 0xFFFFu : odb[4]) | ((uint32_t)(tb & 32 ? 0xFFFFu : odb[5]) << 16),
-                    (tb & 64 ? 0xFFFFu : odb[6]) | ((uint32_t)(tb & 128 ? 0xFFFFu : odb[7]) << 16));
-            } else {
-                for (int j = 0; j < kTileItems; j++)
-                    if (p0 + j < n) { tie[p0 + j] = (uint8_t)(tb >> j & 1); R.dbit[p0 + j] = odb[j]; }
-            }
-            mark_any(ot[0] | ot[1], ot[0] & 0xFFu);
-            __syncthreads();
-            continue;
-        }
-        {
-            uint32_t o2 = mo & 0xFFFFu, ox = npair + (mo >> 16);
-#pragma unroll
-            for (int j = 0; j < kTileItems; j++)
-                if (hm >> j & 1)
-                    s_mem[(h2 >> j & 1) ? o2++ : ox++] =
-                        (i0 + j) | ((uint32_t)ra[j] << 11) | ((uint32_t)(re[j] - ra[j]) << 22);
-        }
-        __syncthreads();
-        // D. rank of each member in its run by (remaining words, row id), member per thread;
-        // pairs (most runs) with one comparison, in warps of their own
-        for (uint32_t u = threadIdx.x; u < nmem; u += blockDim.x) {
-            const uint32_t v = s_mem[u];
-            const uint32_t i = v & 0x7FFu, a = (v >> 11) & 0x7FFu, L = v >> 22;
-            const unsigned long long ki = s_key[tpad(i)];
-            const uint32_t ri = s_row[tpad(i)];
-            uint32_t r = 0;
-            if (u < npair) r = key_less(i == a ? a + 1 : a, i, ki, ri) ? 1u : 0u;
-            else
-                for (uint32_t k = a; k < a + L; k++) r += key_less(k, i, ki, ri) ? 1u : 0u;   // (k == i: false)
-            CKS_DCHECK(r < L && a + L <= (uint32_t)kTileKeys);
-            s_at[tpad(a + r)] = (uint16_t)i;
-        }
-        if (threadIdx.x == 0) s_cnt += nmem;
-        __syncthreads();
-        // E. write back: D_i and tie flags of every position; row ids and carried words only
-        // where this thread's positions were reordered (whole 32-byte groups, else untouched)
-        uint32_t ot[2] = {0, 0};
-        if (!hm) {
-#pragma unroll
-            for (int j = 0; j < kTileItems; j++) {
-                ot[j >> 2] |= (tb >> j & 1u) << (8 * (j & 3));
-                if (tb >> j & 1) odb[j] = CKS_NONE_INTERNAL;
-            }
-        } else {
-            uint32_t orow[kTileItems];
-            uint32_t ow[NWS][kTileItems];
-#pragma unroll
-            for (int j = 0; j < kTileItems; j++) {
-                const uint32_t dd = i0 + j;
-                uint32_t src = dd;
-                uint32_t t = tb >> j & 1u;
-                uint16_t db = t ? (uint16_t)CKS_NONE_INTERNAL : odb[j];
-                if (hm >> j & 1) {
-                    src = s_at[tpad(dd)];
-                    CKS_DCHECK(src < (uint32_t)kTileKeys && src >= (uint32_t)ra[j] && src < (uint32_t)re[j]);
-                    if (t) {                                  // after the run's first position
-                        const uint32_t pj = s_at[tpad(dd - 1)];
-                        const unsigned long long x = s_key[tpad(pj)] ^ s_key[tpad(src)];
-                        const uint32_t b0 = 32u * (R.np - 1 - (uint32_t)R.qtop);   // P_M bit of word 0's MSB
-                        int fd = x ? (int)(b0 + (uint32_t)__clzll((long long)x)) : -1;
-                        if (fd < 0)
-                            for (int c = 2; c < Wr; c++) {
-                                const uint32_t y = word(c, pj) ^ word(c, src);
-                                if (y) { fd = (int)(b0 + 32u * (uint32_t)c + (uint32_t)__clz(y)); break; }
-                            }
-                        if (fd >= 0) {
-                            db = __ldg(R.moff + fd);
-                            mark_pm((uint32_t)fd);
-                        }
-                    }
-                    t = 0;
+        // E. D_i of the handled runs' members after their first
+    #pragma unroll
+        for (int j = 1; j < I; j++) {
+            if (hl >> j & 1u) {
+                const unsigned long long x = key[j] ^ key[j - 1];
+                const uint32_t b0 = 32u * (R.np - (uint32_t)WC);
+                int fd = -1;
+                if (x) fd = (int)(b0 + (uint32_t)__clzll((long long)x) - (WC == 1 ? 32u : 0u));
+                else if (WC == 3 && (kx[j] ^ kx[j - 1])) fd = (int)(b0 + 64u + (uint32_t)__clz(kx[j] ^ kx[j - 1]));
+                odb[j] = CKS_NONE_INTERNAL;
+                if (fd >= 0) {
+                    odb[j] = __ldg(R.moff + fd);
+                    if (fd < 64) dlo |= 1ull << fd; else dhi |= 1u << (fd - 64);
                 }
-                orow[j] = s_row[tpad(src)];
-                odb[j] = db;
-                ot[j >> 2] |= t << (8 * (j & 3));
-#pragma unroll
-                for (int c = 0; c < NWS; c++) ow[c][j] = s_w[c][tpad(src)];
             }
-            st8(R.perm, p0, n, vec, orow);
-#pragma unroll
-            for (int c = 0; c < NWS; c++) st8(R.carried + (uint64_t)(R.qtop - c) * R.pitch, p0, n, vec, ow[c]);
         }
-        if (vec && p0 + kTileItems <= n) {
+        // E2. runs across two lanes: a second network over the window [4, 12) of lane t (its
+        // positions 4..7 and lane t+1's 0..3), for the run holding window positions 3 and 4 when
+        // it lies inside the window (runs of up to 5 keys always do); not across warps
+        const uint32_t wl = ((tb >> 4) | (tbn << 4)) & 0xFFu;       // bit i: window i ties with i-1
+        uint32_t hl2 = 0;
+        if (lane < 31 && (wl >> 4 & 1u) && (wl & 0x0Fu) != 0x0Fu) {
+            const uint32_t a = 31u - (uint32_t)__clz(~wl & 0x0Fu);       // the run's first window position
+            const uint32_t hz = ~wl & 0xE0u;
+            const uint32_t e = hz ? (uint32_t)__ffs(hz) - 1u : 8u;       // first window position after it
+            if (e < 8u || !(tbn >> 4 & 1u)) hl2 = ((1u << e) - 1u) & ~((2u << a) - 1u);
+        }
+        // the window's positions 0..3 are key[4..7] (in place); 4..7 the next lane's 0..3 (nk)
+        unsigned long long nk[4];
+        uint32_t nx[4], nr[4];
+        uint16_t nd[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            nk[j] = __shfl_down_sync(0xffffffffu, key[j], 1);
+            nx[j] = WC == 3 ? __shfl_down_sync(0xffffffffu, kx[j], 1) : 0u;
+            nr[j] = __shfl_down_sync(0xffffffffu, vr[j], 1);
+            nd[j] = (uint16_t)__shfl_down_sync(0xffffffffu, (uint32_t)odb[j], 1);
+        }
+#define CKS_WK(j) (*((j) < 4 ? &key[4 + (j)] : &nk[(j) - 4]))
+#define CKS_WX(j) (*((j) < 4 ? &kx[4 + (j)] : &nx[(j) - 4]))
+#define CKS_WR(j) (*((j) < 4 ? &vr[4 + (j)] : &nr[(j) - 4]))
+#define CKS_WD(j) (*((j) < 4 ? &odb[4 + (j)] : &nd[(j) - 4]))
+        const uint32_t phases2 = __reduce_max_sync(0xffffffffu, hl2 ? (uint32_t)__popc(hl2) + 1u : 0u);
+        bool wchanged = false;
+        auto wcex = [&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            const bool sw = (hl2 >> (j + 1) & 1u) &&
+                            rk_less<WC>(CKS_WK(j + 1), CKS_WX(j + 1), CKS_WR(j + 1), CKS_WK(j), CKS_WX(j), CKS_WR(j));
+            const unsigned long long ka = CKS_WK(j), kb = CKS_WK(j + 1);
+            CKS_WK(j) = sw ? kb : ka;
+            CKS_WK(j + 1) = sw ? ka : kb;
+            if (WC == 3) {
+                const uint32_t xa = CKS_WX(j), xb = CKS_WX(j + 1);
+                CKS_WX(j) = sw ? xb : xa;
+                CKS_WX(j + 1) = sw ? xa : xb;
+            }
+            const uint32_t ra = CKS_WR(j), rb = CKS_WR(j + 1);
+            CKS_WR(j) = sw ? rb : ra;
+            CKS_WR(j + 1) = sw ? ra : rb;
+            wchanged |= sw;
+        };
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, 1>;
+        using I2 = std::integral_constant<int, 2>;
+        using I3 = std::integral_constant<int, 3>;
+        using I4 = std::integral_constant<int, 4>;
+        using I5 = std::integral_constant<int, 5>;
+        using I6 = std::integral_constant<int, 6>;
+        for (uint32_t ph = 0; ph < phases2; ph += 2) {
+            wcex(I0{}); wcex(I2{}); wcex(I4{}); wcex(I6{});
+            if (ph + 1 < phases2) { wcex(I1{}); wcex(I3{}); wcex(I5{}); }
+        }
+        auto wdi = [&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            if (hl2 >> j & 1u) {
+                const unsigned long long x = CKS_WK(j) ^ CKS_WK(j - 1);
+                const uint32_t b0 = 32u * (R.np - (uint32_t)WC);
+                int fd = -1;
+                if (x) fd = (int)(b0 + (uint32_t)__clzll((long long)x) - (WC == 1 ? 32u : 0u));
+                else if (WC == 3 && (CKS_WX(j) ^ CKS_WX(j - 1)))
+                    fd = (int)(b0 + 64u + (uint32_t)__clz(CKS_WX(j) ^ CKS_WX(j - 1)));
+                CKS_WD(j) = CKS_NONE_INTERNAL;
+                if (fd >= 0) {
+                    CKS_WD(j) = __ldg(R.moff + fd);
+                    if (fd < 64) dlo |= 1ull << fd; else dhi |= 1u << (fd - 64);
+                }
+            }
+        };
+        wdi(I1{}); wdi(I2{}); wdi(I3{}); wdi(I4{}); wdi(I5{}); wdi(I6{}); wdi(std::integral_constant<int, 7>{});
+#undef CKS_WK
+#undef CKS_WX
+#undef CKS_WR
+#undef CKS_WD
+        changed |= wchanged;                                      // (the run always holds window position 3)
+        const uint32_t hl2p = __shfl_up_sync(0xffffffffu, hl2, 1);   // the previous lane's window
+        const bool chp = __shfl_up_sync(0xffffffffu, (uint32_t)wchanged, 1) != 0u;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const unsigned long long k2 = __shfl_up_sync(0xffffffffu, nk[j], 1);
+            const uint32_t x2 = WC == 3 ? __shfl_up_sync(0xffffffffu, nx[j], 1) : 0u;
+            const uint32_t r2 = __shfl_up_sync(0xffffffffu, nr[j], 1);
+            const uint16_t d2 = (uint16_t)__shfl_up_sync(0xffffffffu, (uint32_t)nd[j], 1);
+            if (lane > 0 && hl2p) { key[j] = k2; kx[j] = x2; vr[j] = r2; odb[j] = d2; }
+        }
+        if (lane > 0 && hl2p && chp) changed = true;
+        // F. write back: tie flags of the unfinished runs only, D_i, and the reordered groups
+        const uint32_t tout = tb & ~hl & ~((hl2 & 0x0Eu) << 4) & ~(lane > 0 ? (hl2p >> 4) & 0x0Fu : 0u);
+        if (changed) {
+            st8(R.perm, p0, n, vec, vr);
+            uint32_t ow[I];
+    #pragma unroll
+            for (int c = 0; c < WC; c++) {
+                const int q = WC - 1 - c;                                 // plane of remaining word c
+    #pragma unroll
+                for (int j = 0; j < I; j++) {
+                    (void)q;
+                    if (c == 0) ow[j] = topw[j] | (uint32_t)(WC == 1 ? key[j] : key[j] >> 32);
+                    else if (c == 1) ow[j] = (uint32_t)key[j];
+                    else ow[j] = kx[j];
+                }
+                st8(R.carried + (uint64_t)q * R.pitch, p0, n, vec, ow);
+            }
+        }
+        uint32_t ot[2] = {0, 0};
+    #pragma unroll
+        for (int j = 0; j < I; j++) {
+            ot[j >> 2] |= (tout >> j & 1u) << (8 * (j & 3));
+            if (tout >> j & 1u) odb[j] = CKS_NONE_INTERNAL;
+        }
+        if (vec && p0 + I <= n) {
             *reinterpret_cast<uint2*>(tie + p0) = make_uint2(ot[0], ot[1]);
             *reinterpret_cast<uint4*>(R.dbit + p0) =
                 make_uint4(odb[0] | ((uint32_t)odb[1] << 16), odb[2] | ((uint32_t)odb[3] << 16),
                            odb[4] | ((uint32_t)odb[5] << 16), odb[6] | ((uint32_t)odb[7] << 16));
         } else {
-            for (int j = 0; j < kTileItems; j++)
-                if (p0 + j < n) { tie[p0 + j] = (uint8_t)(ot[j >> 2] >> (8 * (j & 3))); R.dbit[p0 + j] = odb[j]; }
+            for (int j = 0; j < I; j++)
+                if (p0 + j < n) { tie[p0 + j] = (uint8_t)(tout >> j & 1u); R.dbit[p0 + j] = odb[j]; }
         }
-        mark_any(ot[0] | ot[1], ot[0] & 0xFFu);
-        __syncthreads();
+        if (any && tout) {                                            // compaction tiles with ties left
+            const uint64_t c = p0 / kRefTile;
+            any[c] = 1;
+            if ((tout & 1u) && c && p0 % kRefTile == 0) any[c - 1] = 1;
+        }
+        hm += (uint32_t)__popc(hl | (hl >> 1)) + (uint32_t)__popc(hl2 | (hl2 >> 1));
     }
+    // G. counts and D
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        dm0 |= __shfl_xor_sync(0xffffffffu, dm0, o);
-        dm1 |= __shfl_xor_sync(0xffffffffu, dm1, o);
-        dm2 |= __shfl_xor_sync(0xffffffffu, dm2, o);
+        dlo |= __shfl_xor_sync(0xffffffffu, dlo, o);
+        dhi |= __shfl_xor_sync(0xffffffffu, dhi, o);
+        hm += __shfl_xor_sync(0xffffffffu, hm, o);
     }
     if (lane == 0) {
-        atomicOr(&s_pm[0], dm0);
-        atomicOr(&s_pm[1], dm1);
-        atomicOr(&s_pm[2], dm2);
+        atomicOr(&s_pm[0], (uint32_t)dlo);
+        atomicOr(&s_pm[1], (uint32_t)(dlo >> 32));
+        atomicOr(&s_pm[2], dhi);
+        atomicAdd(&s_cnt, hm);
     }
     __syncthreads();
     if (threadIdx.x < 96 && (s_pm[threadIdx.x >> 5] >> (threadIdx.x & 31) & 1u)) {
@@ -1047,11 +1028,15 @@ cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int
     if (!carried) return cudaErrorInvalidValue;
     const int wc = qtop + 1;
     const bool alias = np == 3 && lo == carried + pitch && hi == carried + 2 * pitch;
+    if (!alias) return cudaErrorInvalidValue;                    // (chunk = carried planes 2, 1)
+    (void)nwords;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ref_reg<2>, kRefThreads, 0);
+    const uint64_t tiles = (n + kTileKeys - 1) / kTileKeys, gmax = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
+    const unsigned rgrid = (unsigned)(tiles < gmax ? tiles : gmax);
 #define CKS_TILE_CASE(W)                                                                                        \
     case W:                                                                                                     \
-        raise_smem_limit((const void*)k_ref_tile<W>, tile_smem_bytes(W));                                       \
-        k_ref_tile<W><<<grid, kRefThreads, tile_smem_bytes(W), st>>>(R, lo, hi, n, cmask, nwords, vec, tie, dacc, \
-                                                                     handled, any, alias);                      \
+        k_ref_reg<W><<<rgrid, kRefThreads, 0, st>>>(R, lo, hi, n, cmask, vec, tie, dacc, handled, any);        \
         break;
     switch (wc) {
         CKS_TILE_CASE(1)
