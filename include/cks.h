@@ -298,6 +298,22 @@ int cks_paper_tree_shape(uint64_t n, double fill, cks_tree_shape* out);
 int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, const uint32_t* perm,
                    const uint16_t* dbit, uint32_t pk_bits, double fill, uint8_t* nodes);
 
+/* cks_paper_tree_ds: the same nodes (byte for byte), with every partial-key bit taken from the
+ * source P:484-496 names instead of the key row:
+ *   A  positions in packed_mask: from the sorted compressed planes (sorted_packed: device
+ *      u32[ceil(|packed_mask|/32)][packed_pitch], right-aligned as cks_compress, in sorted order --
+ *      e.g. cks_build_out.packed / packed_pitch with packed_mask = the exact D);
+ *   B  invariant positions (0 in `variant`): from the reference key value (ref_key);
+ *   C  the other variant positions: C(b), from the key row (keys; may be NULL when every variant
+ *      position is in packed_mask, CKS_EINVAL otherwise), read only by entries whose window
+ *      holds such a position.
+ * variant / ref_key: host u8[key_bytes], the DS-metadata of the column (cks_build_out.variant /
+ * ref_key). Asynchronous. */
+int cks_paper_tree_ds(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, const uint32_t* perm,
+                      const uint16_t* dbit, const uint32_t* sorted_packed, uint64_t packed_pitch,
+                      const uint8_t* packed_mask, const uint8_t* variant, const uint8_t* ref_key, uint32_t pk_bits,
+                      double fill, uint8_t* nodes);
+
 /* ---- P:502 block-parallel bulk load (the sharded path's a8, NEXT-4) ----------------------
  * "n sort keys are divided into p blocks ... thread i constructs a subtree consisting of all
  * sort keys in the i-th block. ... we remove the root nodes of the subtrees, and build the
@@ -355,6 +371,22 @@ typedef struct {
     uint32_t rounds;          /* prefix-refinement rounds run (0 = plain single sort) */
     uint32_t round0_bits;     /* width of the first refinement round (top bits of P_M) */
     uint64_t refined_keys;    /* keys re-sorted in rounds >= 1 (summed over rounds) */
+    /* DS-metadata recompute at (re)build time, optional:  */
+    uint8_t* variant;         /* host u8[key_bytes] or NULL: receives the variant bitmap V =
+                                 OR over the keys of key XOR reference key; a first build
+                                 takes it from the superset pass, a rebuild (prior mask) runs one
+                                 more pass over the keys for it */
+    uint8_t* ref_key;         /* host u8[key_bytes] or NULL: receives the reference key value,
+                                 the key of row 0 ("an arbitrary index key") */
+    /* NEXT-3, optional: the paper-format index tree (cks_paper_tree's layout) built by the same
+     * call from the sorted order, with partial keys from the sources of P:484-496: A the
+     * compressed key, B the reference key for invariant bits, C(a) the variant bits outside the
+     * sort mask that some partial key needs, compressed into one more plane that rides through
+     * the sort with P_M (when P_M has three planes and they fit one plane), else C(b) the key
+     * rows. cks_paper_tree_shape(n, ptree_fill) gives the node count. */
+    uint8_t* ptree_nodes;     /* device u8[total_nodes][256] or NULL (no paper tree) */
+    uint32_t ptree_pk;        /* partial key bits (<= 32) */
+    double ptree_fill;        /* fill factor in (0, 1] */
 } cks_build_out;
 
 /* keys: device u8[n][key_bytes]; prior_mask: host u8[key_bytes] superset or NULL.

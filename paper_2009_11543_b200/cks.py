@@ -52,7 +52,9 @@ class BuildOut(ctypes.Structure):
                 ("superset_kind", ctypes.c_int), ("popcount", ctypes.c_uint32),
                 ("sort_bits", ctypes.c_uint32), ("height", ctypes.c_uint32), ("passes", ctypes.c_uint32),
                 ("packed", ctypes.c_void_p), ("packed_pitch", ctypes.c_uint64),
-                ("rounds", ctypes.c_uint32), ("round0_bits", ctypes.c_uint32), ("refined_keys", ctypes.c_uint64)]
+                ("rounds", ctypes.c_uint32), ("round0_bits", ctypes.c_uint32), ("refined_keys", ctypes.c_uint64),
+                ("variant", ctypes.c_void_p), ("ref_key", ctypes.c_void_p),
+                ("ptree_nodes", ctypes.c_void_p), ("ptree_pk", ctypes.c_uint32), ("ptree_fill", ctypes.c_double)]
 
 
 EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing", "cks_ctx_set_sort_mode",
@@ -62,7 +64,7 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
            "cks_partition", "cks_sort_prefix", "cks_bulkload_block", "cks_bulkload_top",
            "cks_build_host_batch", "cks_ctx_set_round0_bits", "cks_ctx_set_verify",
-           "cks_ctx_path_bytes"]
+           "cks_ctx_path_bytes", "cks_paper_tree_ds"]
 
 
 def load_library(path: str | None = None):
@@ -102,6 +104,7 @@ def load_library(path: str | None = None):
     L.cks_bulkload.argtypes = [p, p, p, u64, u32, f64, ctypes.POINTER(Tree)]
     L.cks_paper_tree_shape.argtypes = [u64, f64, ctypes.POINTER(TreeShape)]
     L.cks_paper_tree.argtypes = [p, p, u64, u32, p, p, u32, f64, p]
+    L.cks_paper_tree_ds.argtypes = [p, p, u64, u32, p, p, p, u64, p, p, p, u32, f64, p]
     L.cks_build.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     L.cks_build_host.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     L.cks_occupancy.argtypes = [p, p, u64, u32, p]
@@ -491,13 +494,35 @@ def paper_tree(keys: torch.Tensor, perm: torch.Tensor, dbit: torch.Tensor, pk_bi
     return out[:T]
 
 
+def paper_tree_ds(keys: torch.Tensor | None, n: int, B: int, perm: torch.Tensor, dbit: torch.Tensor,
+                  packed: torch.Tensor | None, packed_pitch: int, packed_mask, variant, ref_key, pk_bits: int = 32,
+                  fill: float = 0.9, out: torch.Tensor | None = None) -> torch.Tensor:
+    """NEXT-3 tree with partial keys from the DS-metadata sources (cks_paper_tree_ds): packed =
+    the sorted compressed planes (int32 [.., >= n], row pitch packed_pitch) of packed_mask."""
+    dev = perm.device
+    L, c = _context(dev.index)
+    s = paper_tree_shape(n, fill)
+    T = int(s.total_nodes)
+    if out is None:
+        out = torch.empty((max(T, 1), PTREE_NODE_BYTES), dtype=torch.uint8, device=dev)
+    xm, vm, rk = _host_mask(packed_mask, B), _host_mask(variant, B), _host_mask(ref_key, B)
+    _check(L, c, L.cks_paper_tree_ds(c, _ptr(keys), n, B, _ptr(perm), _ptr(dbit),
+                                     _ptr(packed) if packed is not None and packed.numel() else None, packed_pitch,
+                                     xm.ctypes.data, vm.ctypes.data, rk.ctypes.data, pk_bits, fill, _ptr(out)))
+    return out[:T]
+
+
 class Builder:
     """Preallocated fused first build (cks_build) for repeated steps on one key shape."""
 
     def __init__(self, n: int, B: int, device, fanout: int = 64, fill: float = 1.0,
-                 superset_kind: int = SUPERSET_BYTEOCC, tree: bool = True, dbit: bool = True):
+                 superset_kind: int = SUPERSET_BYTEOCC, tree: bool = True, dbit: bool = True,
+                 ds_metadata: bool = False, paper_tree_pk: int | None = None, paper_tree_fill: float = 0.9):
         self.n, self.B = n, B
         self.mask = np.zeros(B, np.uint8)
+        # DS-metadata (P:359-372): variant bitmap and reference key, recomputed by the build
+        self.variant = np.zeros(B, np.uint8) if ds_metadata else None
+        self.ref_key = np.zeros(B, np.uint8) if ds_metadata else None
         self.perm = torch.empty(max(n, 1), dtype=torch.int32, device=device)
         self.dbit = torch.empty(max(n, 1), dtype=torch.int16, device=device) if dbit else None
         self.shape = bulkload_shape(n, fanout, fill)
@@ -511,6 +536,19 @@ class Builder:
         self.out.fanout = fanout
         self.out.fill = fill
         self.out.superset_kind = superset_kind
+        if ds_metadata:
+            self.out.variant = self.variant.ctypes.data
+            self.out.ref_key = self.ref_key.ctypes.data
+        # NEXT-3: the paper-format tree built by the same call (partial keys from A/B/C(a))
+        self.ptree = None
+        if paper_tree_pk is not None:
+            ps = paper_tree_shape(n, paper_tree_fill)
+            self.ptree = torch.empty((max(int(ps.total_nodes), 1), PTREE_NODE_BYTES), dtype=torch.uint8,
+                                     device=device)
+            self.ptree_nodes = int(ps.total_nodes)
+            self.out.ptree_nodes = self.ptree.data_ptr()
+            self.out.ptree_pk = paper_tree_pk
+            self.out.ptree_fill = paper_tree_fill
 
     def __call__(self, keys: torch.Tensor, prior_mask=None) -> "Builder":
         n, B = _keys(keys)
@@ -540,14 +578,21 @@ def raw_view(ptr: int, numel: int, device) -> torch.Tensor:
 
 
 def build(keys: torch.Tensor, prior_mask=None, fanout: int = 64, fill: float = 1.0,
-          superset_kind: int = SUPERSET_BYTEOCC, tree: bool = True) -> dict:
+          superset_kind: int = SUPERSET_BYTEOCC, tree: bool = True, ds_metadata: bool = False,
+          paper_tree_pk: int | None = None, paper_tree_fill: float = 0.9) -> dict:
     n, B = _keys(keys)
-    b = Builder(n, B, keys.device, fanout, fill, superset_kind, tree)
+    b = Builder(n, B, keys.device, fanout, fill, superset_kind, tree, ds_metadata=ds_metadata,
+                paper_tree_pk=paper_tree_pk, paper_tree_fill=paper_tree_fill)
     b(keys, prior_mask)
     o = b.out
-    return dict(mask=b.mask.copy(), popcount=int(o.popcount), sort_bits=int(o.sort_bits), passes=int(o.passes),
-                perm=b.perm[:n], dbit=b.dbit[:n] if b.dbit is not None else None, packed=b.packed(),
-                tree=b.tree, shape=b.shape, height=int(o.height))
+    r = dict(mask=b.mask.copy(), popcount=int(o.popcount), sort_bits=int(o.sort_bits), passes=int(o.passes),
+             perm=b.perm[:n], dbit=b.dbit[:n] if b.dbit is not None else None, packed=b.packed(),
+             tree=b.tree, shape=b.shape, height=int(o.height))
+    if ds_metadata:
+        r.update(variant=b.variant.copy(), ref_key=b.ref_key.copy())
+    if b.ptree is not None:
+        r["paper_tree"] = b.ptree[:b.ptree_nodes]
+    return r
 
 
 def build_host_batch(columns: list, prior_mask=None, superset_kind: int = SUPERSET_BYTEOCC,

@@ -55,9 +55,10 @@ struct cks_ctx {
         part_in, part_out,                                                 // NEXT-4
         anyt,                                                              // k_ref_reg: compaction tiles with ties left
         vbad,                                                              // k_verify_order result
+        ptab,                                                              // cks_paper_tree_ds tables
         keys2, perm2;                                                      // cks_build_host_batch: 2nd buffers
     // pinned host staging
-    GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: unused
+    GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: partial-key bits (P_E)
     uint16_t* h_moff = nullptr;
     uint32_t* h_small = nullptr;      // 4 KiB: masks, dacc words
     uint32_t* h_tot = nullptr;        // refinement: (members, runs) of the next round
@@ -66,6 +67,9 @@ struct cks_ctx {
     int verify = CKS_VERIFY_PRIOR;    // order check of the result against the key rows
     bool verify_now = false;          // ... for the build in progress
     double path_bytes = 0.0;          // algorithmic bytes of every kernel of the last build
+    std::vector<uint8_t> pt_E;        // fused paper tree: partial-key bits appended to P_M (C(a))
+    bool pt_on = false;
+    uint32_t pt_npe = 0;              // planes actually appended by the last build_refine
     bool skip_packed = false;         // cks_sort_prefix without packed_out: no a7
 };
 
@@ -152,7 +156,8 @@ T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
      &c->rmin1, &c->plan[0], &c->plan[1], &c->plan[2], &c->keys, &c->perm_scratch, &c->tile_off, &c->chunk_tot, \
      &c->total, &c->pm, &c->pd, &c->cmp, &c->crid, &c->crid2, &c->posA, &c->posB, &c->posC, &c->segA, &c->segB,   \
      &c->segC, &c->runoff, &c->runpos, &c->runoff2, &c->runpos2, &c->tie, &c->keep, &c->done, &c->mlist,         \
-     &c->wlist, &c->rcnt, &c->rtot, &c->part_in, &c->part_out, &c->anyt, &c->vbad, &c->keys2, &c->perm2}
+     &c->wlist, &c->rcnt, &c->rtot, &c->part_in, &c->part_out, &c->anyt, &c->vbad, &c->keys2, &c->perm2,     \
+     &c->ptab}
 
 // checked build: the canary band after every scratch buffer must be intact after a call
 // (synchronises); no-op otherwise
@@ -210,7 +215,7 @@ int claim_slot(cks_ctx* ctx, int slot) {
 
 // a1: superset mask into host `mask_out`; returns popcount via *m.
 int run_superset(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, int kind,
-                 uint8_t* mask_out, uint32_t* m, bool keys_ready = true) {
+                 uint8_t* mask_out, uint32_t* m, bool keys_ready = true, uint8_t* variant_out = nullptr) {
     if (kind != CKS_SUPERSET_VARIANT && kind != CKS_SUPERSET_BYTEOCC)
         return fail(ctx, CKS_EINVAL, "unknown superset kind %d", kind);
     TRY(ensure(ctx, ctx->occ, (size_t)B * 8 * 4));
@@ -227,6 +232,7 @@ int run_superset(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, int 
     CK(cudaStreamSynchronize(ctx->stream));
     const uint8_t* src = reinterpret_cast<const uint8_t*>(ctx->h_small) + (kind == CKS_SUPERSET_BYTEOCC ? 0 : B);
     memcpy(mask_out, src, B);
+    if (variant_out) memcpy(variant_out, reinterpret_cast<const uint8_t*>(ctx->h_small) + B, B);
     *m = popcount_mask(mask_out, B);
     return CKS_OK;
 }
@@ -406,9 +412,14 @@ static void repack_words(const uint8_t* M, const uint8_t* D, uint32_t B, uint32_
 // NEXT-1: first build by distinguishing prefixes (k_refine.cu). Outputs perm, dbit, the
 // exact D (out->mask) and P_D in sorted order (out->packed).
 // keys == NULL: P_M is given instead (planes_in, right-aligned u32[np][n] as cks_compress).
+// E != NULL (P_M of three planes, keys given): the partial-key bits E (C(a) of P:492) are
+// compressed into one more plane appended below P_M and ride through the sort with it.
 int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* M, uint32_t m,
-                 cks_build_out* out, uint16_t* dbit, const uint32_t* planes_in = nullptr) {
-    const uint32_t np = (m + 31) / 32, lead = 32 * np - m;
+                 cks_build_out* out, uint16_t* dbit, const uint32_t* planes_in = nullptr, const uint8_t* E = nullptr) {
+    const uint32_t npm = (m + 31) / 32, lead = 32 * npm - m;
+    const uint32_t npe = (E && keys && !planes_in && npm == 3) ? 1u : 0u;   // appended planes (P_E)
+    const uint32_t np = npm + npe;                               // planes sorted / carried
+    ctx->pt_npe = npe;
     const uint64_t sp = scratch_pitch(n);
     const uint32_t nwords = (8 * B + 31) / 32;
     // a3: P_M left-aligned (the first mask position is bit 31 of the top plane), so chunk r
@@ -428,7 +439,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         TRY(upload_plan(ctx, 0, &dplan));
     }
     const int forced = (int)ctx->round0_bits;
-    const bool sample = !(forced > 0 && forced <= 64 && (forced & 7) == 0) && np >= 2 && n >= (1u << 16);
+    const bool sample = !(forced > 0 && forced <= 64 && (forced & 7) == 0) && npm >= 2 && n >= (1u << 16);
     TRY(ensure(ctx, ctx->rtot, 64));
     uint32_t* scnt = as<uint32_t>(ctx->rtot) + 4;
     if (planes_in) {                                             // given P_M: left-align it, then sample
@@ -448,7 +459,17 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             CK(cudaMemcpyAsync(ctx->h_tot + 8, scnt, 32, cudaMemcpyDeviceToHost, ctx->aux_stream));
             CK(cudaEventRecord(ctx->aux_ev[1], ctx->aux_stream));
         }
-        LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, pm, sp, ctx->sms, ctx->stream, lead));
+        LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], npm, pm + (uint64_t)npe * sp, sp, ctx->sms,
+                               ctx->stream, lead));
+        if (npe) {                                               // P_E, left-aligned in plane 0
+            TRY(claim_slot(ctx, 2));
+            plan_compress(E, B, ctx->h_plan[2]);
+            GatherPlan* eplan;
+            TRY(upload_plan(ctx, 2, &eplan));
+            const uint32_t me = ctx->h_plan[2]->out_bits;
+            LAUNCH(launch_compress(keys, n, B, eplan, ctx->h_plan[2], 1, pm, sp, ctx->sms, ctx->stream, 32 - me));
+            BYTES((double)n * (B + 4.0));
+        }
     }
     mark(ctx, ST_COMPRESS);
     uint32_t T = forced > 0 && forced <= 64 && (forced & 7) == 0 ? (uint32_t)forced : 64;
@@ -459,7 +480,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         // those by row is dearer than a pass (measured: cfg3 32 -> 40). With P_M carried (np == 3)
         // the tile kernel finishes short ties from the sorted planes for less than a pass costs
         // (measured, cfg5: T = 40 3.65 ms, 48 3.89 ms)
-        const uint32_t margin = np == 3 ? 0u : 1u;
+        const uint32_t margin = npm == 3 ? 0u : 1u;
         for (uint32_t w = 0; w < 8; w++)
             if (ctx->h_tot[8 + w] == ctx->h_tot[15]) {
                 T = 8 * (w + 1 + margin) < 64 ? 8 * (w + 1 + margin) : 64;
@@ -481,8 +502,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     // round-0 passes (4 more bytes per key per pass), which is cheaper than gathering the key
     // rows again at the end: P_M then comes out in sorted order (and stays so: the rounds
     // that reorder runs move its planes too).
-    const bool carry = np == 3;
-    const uint32_t np0 = carry ? 3 : (np >= 2 ? 2 : 1);
+    const bool carry = npm == 3;
+    const uint32_t np0 = carry ? np : (np >= 2 ? 2 : 1);
     // round 0 sorts the top T bits of chunk 0 (the digits below them are skipped)
     const uint32_t dig0 = np <= 2 ? (lead / 8 > 4 * np0 - T / 8 ? lead / 8 : 4 * np0 - T / 8) : 4 * np0 - T / 8;
     const uint32_t* sorted0 = nullptr;
@@ -500,7 +521,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     const uint32_t* hi0 = sorted0 + (uint64_t)(np0 - 1) * sp0;
     TRY(ensure(ctx, ctx->rtot, 64));
     CK(cudaMemsetAsync(as<uint32_t>(ctx->rtot) + 2, 0, 4, ctx->stream));
-    const bool tiled = T < m && carry && !no_tile;   // (P_M by row id: the compaction + k_ref_local path measured faster)
+    const bool tiled = T < m && carry && !no_tile && (int)np - (int)(T >> 5) <= 3;   // (P_M by row id: the compaction + k_ref_local path measured faster)
     if (tiled) {
         TRY(ensure(ctx, ctx->anyt, ref_tiles(n) + 16));
         CK(cudaMemsetAsync(ctx->anyt.p, 0, ref_tiles(n) + 16, ctx->stream));
@@ -647,12 +668,12 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         if (!carry) TRY(ensure(ctx, ctx->pd, (size_t)npd * sp * 4));
         uint32_t* pd = carry ? pm : as<uint32_t>(ctx->pd);       // (P_M in row order is no longer needed)
         const bool single = T >= m;                               // round 0 sorted all of P_M
-        if ((single || carry) && lead == 0 && same_mask(out->mask, M, B)) {
+        if ((single || carry) && lead == 0 && npe == 0 && same_mask(out->mask, M, B)) {
             out->packed = sorted0;
             out->packed_pitch = sp0;
         } else if (single || carry) {
             std::vector<uint32_t> sub(np, 0);
-            repack_words(M, out->mask, B, m, lead, sub);
+            repack_words(M, out->mask, B, m, lead + 32 * npe, sub);
             TRY(claim_slot(ctx, 1));
             plan_repack(sub.data(), np, ctx->h_plan[1]);
             GatherPlan* dplan;
@@ -830,7 +851,7 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     // 1 = auto: by prefixes whenever P_M is wider than one 64-bit chunk (m > 64); for m <= 64
     // round 0 would be the whole sort anyway
     if (n && m && (ctx->refine == 2 || (ctx->refine == 1 && m > 64))) {
-        TRY(build_refine(ctx, keys, n, B, M, m, out, dbit, planes_in));
+        TRY(build_refine(ctx, keys, n, B, M, m, out, dbit, planes_in, ctx->pt_on ? ctx->pt_E.data() : nullptr));
         TRY(verify_if(ctx, keys, n, B, out));
         out->height = 0;
         if (out->tree.node_cnt) {
@@ -896,6 +917,52 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     return CKS_OK;
 }
 
+// NEXT-3 tree with the paper's partial-key sources: segments X (mask X, first bit gx
+// from the MSB of the np sorted planes) and Y (mask Y or NULL, first bit gy) give source A,
+// `ref` source B (invariant = 0 in V), the key rows C(b) for the other variant positions.
+int run_ptree_ds(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
+                 const uint32_t* planes, uint64_t pitch, uint32_t np, const uint8_t* X, uint32_t gx, const uint8_t* Y,
+                 uint32_t gy, const uint8_t* V, const uint8_t* ref, uint32_t pk, double fill, uint8_t* nodes) {
+    bool need_rows = false;
+    for (uint32_t j = 0; j < B; j++) need_rows |= (V[j] & ~X[j] & ~(Y ? Y[j] : 0)) != 0;
+    if (n && (!perm || !dbit || !nodes || (need_rows && !keys)))
+        return fail(ctx, CKS_EINVAL, "NULL perm, dbit, nodes, or keys (variant bits outside the planes)");
+    cks_tree_shape s;
+    const int rc = cks_paper_tree_shape(n, fill, &s);
+    if (rc != CKS_OK) return fail(ctx, rc, "bad paper-tree shape (fill %f)", fill);
+    if (n == 0) return CKS_OK;
+    TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
+    TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+    // tables (k_ptree.cu PkDs): rows of S = B + 8 bytes (8 zero bytes after each, so a 40-bit
+    // window never needs a bound check) for X, Y, V and the reference key, then the u16 rank of
+    // each byte's first X / Y position
+    const size_t S = (size_t)B + 8, tb = 4 * S + 4 * (size_t)B;
+    TRY(ensure(ctx, ctx->ptab, tb + 16));
+    CK(cudaEventSynchronize(ctx->plan_ev[2]));
+    uint8_t* h = reinterpret_cast<uint8_t*>(ctx->h_small);
+    memset(h, 0, tb);
+    memcpy(h, X, B);
+    if (Y) memcpy(h + S, Y, B);
+    memcpy(h + 2 * S, V, B);
+    memcpy(h + 3 * S, ref, B);
+    uint16_t rx = 0, ry = 0;
+    for (uint32_t j = 0; j < B; j++) {
+        memcpy(h + 4 * S + 2 * j, &rx, 2);
+        memcpy(h + 4 * S + 2 * (size_t)B + 2 * j, &ry, 2);
+        rx = (uint16_t)(rx + __builtin_popcount(X[j]));
+        ry = (uint16_t)(ry + (Y ? __builtin_popcount(Y[j]) : 0));
+    }
+    CK(cudaMemcpyAsync(ctx->ptab.p, h, tb, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->plan_ev[2], ctx->stream));
+    PtreeDs ds{planes, pitch, np, gx, gy, as<uint8_t>(ctx->ptab)};
+    int nl = 0;
+    CK(launch_ptree(keys, n, B, perm, dbit, pk, s.per_node, s.reserved, s.level_nodes, s.level_offset, s.height, nodes,
+                    as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl, &ds));
+    ctx->launches += (uint64_t)nl;
+    BYTES((double)n * (4.0 * np + 4.0 + 2.0) + (double)s.total_nodes * 256.0);
+    return CKS_OK;
+}
+
 int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* prior,
                  cks_build_out* out, bool keys_ready_for_mask) {
     std::vector<uint8_t> M(B, 0);
@@ -903,15 +970,80 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     if (prior) {
         memcpy(M.data(), prior, B);
         m = popcount_mask(M.data(), B);
+        if (out->variant) {
+            // rebuild: the new variant bitmap needs one pass over the keys (P:413 step 3)
+            std::vector<uint8_t> tmp(B);
+            uint32_t mt = 0;
+            TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_VARIANT, tmp.data(), &mt, true, out->variant));
+        }
     } else {
         int kind = out->superset_kind;
-        TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask));
+        TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask, out->variant));
+    }
+    if (out->ref_key) {                                  // the reference key (row 0's key)
+        if (n) {
+            CK(cudaEventSynchronize(ctx->plan_ev[2]));
+            CK(cudaMemcpyAsync(ctx->h_small, keys, B, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            memcpy(out->ref_key, ctx->h_small, B);
+        } else {
+            memset(out->ref_key, 0, B);
+        }
+    }
+    // NEXT-3 fused paper tree: DS-metadata V and the reference key, and the partial-key bits that
+    // are variant but not in M (E, P:492 C(a)) -- appended to P_M when P_M is carried (3 planes)
+    const bool ptree = out->ptree_nodes != nullptr && n > 0;
+    std::vector<uint8_t> V(B, 0), ref(B, 0);
+    ctx->pt_on = false;
+    ctx->pt_npe = 0;
+    if (ptree) {
+        if (out->ptree_pk > 32) return fail(ctx, CKS_EINVAL, "ptree_pk %u > 32", out->ptree_pk);
+        if (out->variant) {
+            memcpy(V.data(), out->variant, B);
+        } else {
+            uint32_t mt = 0;
+            std::vector<uint8_t> tmp(B);
+            TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_VARIANT, tmp.data(), &mt, true, V.data()));
+        }
+        CK(cudaEventSynchronize(ctx->plan_ev[2]));
+        CK(cudaMemcpyAsync(ctx->h_small, keys, B, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        memcpy(ref.data(), ctx->h_small, B);
+        // E = variant positions outside M inside some window [q+1, q+pk] (q in M) or [0, pk)
+        const uint32_t pk = out->ptree_pk, nb = 8 * B;
+        std::vector<uint8_t> win(nb + 1, 0);
+        int last = -1;                                           // last M position at or before p
+        ctx->pt_E.assign(B, 0);
+        uint32_t ne = 0;
+        for (uint32_t p = 0; p < nb; p++) {
+            const bool inM = (M[p >> 3] >> (7 - (p & 7))) & 1, inV = (V[p >> 3] >> (7 - (p & 7))) & 1;
+            const bool inwin = p < pk || (last >= 0 && p <= (uint32_t)last + pk);
+            if (inV && !inM && inwin) { ctx->pt_E[p >> 3] |= (uint8_t)(0x80u >> (p & 7)); ne++; }
+            if (inM) last = (int)p;
+        }
+        ctx->pt_on = ne > 0 && ne <= 32;
     }
     mark(ctx, ST_MASK);
     ctx->verify_now = keys && (ctx->verify == CKS_VERIFY_ALWAYS || (ctx->verify == CKS_VERIFY_PRIOR && prior));
     const int rc = build_from_mask(ctx, keys, n, B, M.data(), m, out);
     ctx->verify_now = false;
+    ctx->pt_on = false;
     TRY(rc);
+    if (ptree) {
+        const uint16_t* db = out->dbit ? out->dbit : as<uint16_t>(ctx->dbit);
+        if (ctx->pt_npe) {                                       // A from the carried P_M | P_E, B, no rows
+            const uint32_t npm = (m + 31) / 32;
+            TRY(run_ptree_ds(ctx, keys, n, B, out->perm, db, as<uint32_t>(ctx->pd), scratch_pitch(n), npm + 1,
+                             M.data(), 0, ctx->pt_E.data(), 32 * npm, V.data(), ref.data(), out->ptree_pk,
+                             out->ptree_fill, out->ptree_nodes));
+        } else {                                                 // A from P_D, B, C(b) from the rows
+            const uint32_t npd = (out->popcount + 31) / 32;
+            TRY(run_ptree_ds(ctx, keys, n, B, out->perm, db, out->packed, out->packed_pitch, npd, out->mask,
+                             32 * npd - out->popcount, nullptr, 0, V.data(), ref.data(), out->ptree_pk,
+                             out->ptree_fill, out->ptree_nodes));
+        }
+        mark(ctx, ST_BULK);
+    }
     return check_guards(ctx);
 }
 
@@ -941,7 +1073,7 @@ int cks_ctx_create(int device, void* stream, cks_ctx** out) {
     for (int i = 0; i < 2 * cks_ctx::kMaxKev && ok; i++) ok = cudaEventCreate(&ctx->kev[i]) == cudaSuccess;
     for (int i = 0; i < ST_N && ok; i++) ok = cudaEventCreate(&ctx->ev[i]) == cudaSuccess;
     for (int i = 0; i < 3 && ok; i++) ok = cudaEventCreateWithFlags(&ctx->plan_ev[i], cudaEventDisableTiming) == cudaSuccess;
-    for (int i = 0; i < 2 && ok; i++) ok = cudaMallocHost(&ctx->h_plan[i], sizeof(GatherPlan)) == cudaSuccess;
+    for (int i = 0; i < 3 && ok; i++) ok = cudaMallocHost(&ctx->h_plan[i], sizeof(GatherPlan)) == cudaSuccess;
     if (ok) ok = cudaMallocHost(&ctx->h_moff, kMaxBits * 2) == cudaSuccess;
     if (ok) ok = cudaMallocHost(&ctx->h_small, 8192) == cudaSuccess;
     if (ok) ok = cudaMallocHost(&ctx->h_tot, 64) == cudaSuccess;
@@ -966,7 +1098,7 @@ int cks_ctx_destroy(cks_ctx* ctx) {
         if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
     for (int i = 0; i < 3; i++)
         if (ctx->plan_ev[i]) cudaEventDestroy(ctx->plan_ev[i]);
-    for (int i = 0; i < 2; i++)
+    for (int i = 0; i < 3; i++)
         if (ctx->h_plan[i]) cudaFreeHost(ctx->h_plan[i]);
     if (ctx->h_moff) cudaFreeHost(ctx->h_moff);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
@@ -1327,6 +1459,24 @@ int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, co
     CK(launch_ptree(keys, n, B, perm, dbit, pk_bits, s.per_node, s.reserved, s.level_nodes, s.level_offset,
                     s.height, nodes, as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl));
     ctx->launches += (uint64_t)nl;
+    return check_guards(ctx);
+}
+
+int cks_paper_tree_ds(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm,
+                      const uint16_t* dbit, const uint32_t* sorted_packed, uint64_t packed_pitch,
+                      const uint8_t* packed_mask, const uint8_t* variant, const uint8_t* ref_key, uint32_t pk_bits,
+                      double fill, uint8_t* nodes) {
+    if (!ctx) return CKS_EINVAL;
+    if (B < 1 || B > CKS_MAX_KEY_BYTES) return fail(ctx, CKS_EINVAL, "key_bytes %u not in [1,512]", B);
+    if (n >= (1ull << 32)) return fail(ctx, CKS_ERANGE, "n >= 2^32");
+    if (pk_bits > 32) return fail(ctx, CKS_EINVAL, "pk_bits %u > 32", pk_bits);
+    if (!packed_mask || !variant || !ref_key) return fail(ctx, CKS_EINVAL, "NULL DS-metadata mask or key");
+    const uint32_t mx = popcount_mask(packed_mask, B);
+    if (n && mx && (!sorted_packed || packed_pitch < n)) return fail(ctx, CKS_EINVAL, "NULL planes or pitch < n");
+    CK(cudaSetDevice(ctx->device));
+    const uint32_t np = (mx + 31) / 32;
+    TRY(run_ptree_ds(ctx, keys, n, B, perm, dbit, sorted_packed, packed_pitch, np, packed_mask, 32 * np - mx, nullptr,
+                     0, variant, ref_key, pk_bits, fill, nodes));
     return check_guards(ctx);
 }
 

@@ -193,10 +193,19 @@ cudaError_t launch_bulk_inner(const uint32_t* perm, const uint16_t* rmin_below, 
                               uint32_t* rid, uint16_t* edbit, uint32_t* child, uint64_t inner_off,
                               uint16_t* rmin, int sms, cudaStream_t st, bool first_none = true);
 
-// NEXT-3 paper-format index tree (k_ptree.cu)
+// NEXT-3 paper-format index tree (k_ptree.cu). ds == NULL: partial keys from the key rows;
+// else from the DS-metadata sources (sorted compressed planes, reference key, rows only for
+// variant positions outside the planes' mask).
+struct PtreeDs {
+    const uint32_t* planes;    // sorted compressed planes: segment X (mask X) then Y (mask Y)
+    uint64_t pitch;
+    uint32_t np;
+    uint32_t gx, gy;           // first bit of X / Y counted from the MSB of the np planes
+    const uint8_t* tab;        // device tables: X, Y, variant, ref bytes; u16 byte ranks of X, Y
+};
 cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
                          uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
                          const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
-                         uint16_t* rmin_b, int sms, cudaStream_t st, int* launches);
+                         uint16_t* rmin_b, int sms, cudaStream_t st, int* launches, const PtreeDs* ds = nullptr);
 
 }  // namespace cks

@@ -56,11 +56,87 @@ __device__ __forceinline__ uint32_t pk_of8(const uint8_t* keys, uint32_t B, uint
 }
 }  // namespace
 
+// Where a partial key's bits come from.
+//   PkRows  every bit from the key row (C(b): dereference the record) -- any caller.
+//   PkDs    A: from the sorted compressed planes the build produced (positions of `xmask`,
+//           compressed index = rank in xmask), B: invariant positions (0 in the variant bitmap)
+//           from the reference key, C(b): the remaining variant positions from the key row,
+//           read only when the entry's window holds one.
+struct PkRows {
+    const uint8_t* keys;
+    uint32_t B;
+    bool w8;
+    __device__ __forceinline__ uint32_t get(uint64_t /*k*/, uint32_t rid, uint16_t d, uint32_t pk) const {
+        return w8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk);
+    }
+};
+
+struct PkDs {
+    const uint8_t* keys;                 // rows for C(b) (may be NULL when V is inside X u Y)
+    uint32_t B;
+    bool w8;
+    const uint32_t* planes;              // sorted compressed planes, plane np-1 most significant
+    uint64_t pitch;
+    uint32_t np;
+    uint32_t gx, gy;                     // bit (from the MSB of the np planes) of segment X's / Y's
+                                         // first compressed bit; X then Y (Y may be empty)
+    const uint8_t* tab;                  // device: 4 byte rows of S = B + 8 bytes (the last 8 zero):
+                                         // X mask, Y mask, variant, ref key; then u16 ranks of
+                                         // byte j's first X / Y bit at 4S + 2j / 4S + 2B + 2j
+    __device__ __forceinline__ uint32_t S() const { return B + 8u; }
+    // 32 mask/key bits of table row `row` from bit p0 (MSB-first, p0 < 8B; zero past the key)
+    __device__ __forceinline__ uint32_t win(uint32_t row, uint32_t p0) const {
+        const uint8_t* b = tab + row * S() + (p0 >> 3);
+        unsigned long long w = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) w = (w << 8) | (uint32_t)b[i];
+        return (uint32_t)(w >> (8 - (p0 & 7)));
+    }
+    // c (<= 32) bits of the planes from bit g (counted from the MSB), left-aligned
+    __device__ __forceinline__ uint32_t field(uint64_t k, uint32_t g, uint32_t c) const {
+        if (c == 0) return 0u;
+        const int q = (int)np - 1 - (int)(g >> 5);
+        CKS_DCHECK(q >= 0 && q < (int)np && k < pitch);
+        const uint32_t a = __ldg(planes + (uint64_t)q * pitch + k);
+        const uint32_t b = q >= 1 ? __ldg(planes + (uint64_t)(q - 1) * pitch + k) : 0u;
+        const uint32_t v = (g & 31) ? __funnelshift_l(b, a, g & 31) : a;
+        return c >= 32 ? v : v & ~(0xFFFFFFFFu >> c);
+    }
+    // A: the window's bits of segment `row` (0 = X, 1 = Y), deposited at their positions w
+    __device__ __forceinline__ uint32_t seg_bits(uint64_t k, uint32_t p0, uint32_t w, uint32_t row, uint32_t g0) const {
+        const uint32_t j0 = p0 >> 3;
+        const uint8_t* rk = tab + 4 * S() + 2 * row * B + 2 * j0;
+        const uint32_t r = ((uint32_t)rk[0] | ((uint32_t)rk[1] << 8)) +
+                           (uint32_t)__popc((uint32_t)tab[row * S() + j0] >> (8 - (p0 & 7)));
+        uint32_t f = field(k, g0 + r, (uint32_t)__popc(w)), m = w, out = 0;
+        while (m) {
+            const uint32_t hb = 0x80000000u >> __clz(m);
+            if (f & 0x80000000u) out |= hb;
+            f <<= 1;
+            m &= ~hb;
+        }
+        return out;
+    }
+    __device__ __forceinline__ uint32_t get(uint64_t k, uint32_t rid, uint16_t d, uint32_t pk) const {
+        if (pk == 0) return 0u;
+        const uint32_t p0 = d == CKS_NONE_INTERNAL ? 0u : (uint32_t)d + 1;
+        if (p0 >= 8 * B) return 0u;
+        const uint32_t pkm = pk >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> pk);
+        const uint32_t wx = win(0, p0) & pkm, wy = win(1, p0) & pkm, wv = win(2, p0) & pkm;
+        uint32_t out = win(3, p0) & ~wv & pkm;                     // B: invariant bits
+        if (wx) out |= seg_bits(k, p0, wx, 0, gx);                 // A
+        if (wy) out |= seg_bits(k, p0, wy, 1, gy);
+        const uint32_t wc = wv & ~wx & ~wy;                        // C(b): variant, not compressed
+        if (wc) out |= (w8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk)) & wc;
+        return out;
+    }
+};
+
 // leaves, thread per sorted key k (entry k % per of leaf k / per): the key-row reads of a
 // warp are independent (a thread per node would walk its entries serially)
-template <bool W8>
+template <class Src>
 __global__ void __launch_bounds__(kPtThreads)
-k_ptree_leaf_entries(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
+k_ptree_leaf_entries(const Src src, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
                      const uint16_t* __restrict__ dbit, uint32_t pk, uint32_t per, uint64_t nleaves,
                      uint8_t* __restrict__ nodes) {
     constexpr int U = 4;                                          // keys in flight per thread
@@ -76,7 +152,7 @@ k_ptree_leaf_entries(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, c
         }
 #pragma unroll
         for (int u = 0; u < U; u++)
-            pkv[u] = k0 + u * T < n ? (W8 ? pk_of8(keys, B, rid[u], d[u], pk) : pk_of(keys, B, rid[u], d[u], pk)) : 0u;
+            pkv[u] = k0 + u * T < n ? src.get(k0 + u * T, rid[u], d[u], pk) : 0u;
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint64_t k = k0 + u * T;
@@ -110,9 +186,9 @@ k_ptree_leaf_min(const uint16_t* __restrict__ dbit, uint64_t n, uint32_t per, ui
 }
 
 // thread per node of level `level` (>= 1)
-template <bool W8>
+template <class Src>
 __global__ void __launch_bounds__(kPtThreads)
-k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
+k_ptree_inner(const Src src, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
               uint32_t pk, uint32_t per, uint64_t nbelow, uint64_t cover_below, uint64_t below_off, uint64_t nnodes,
               uint64_t node_off, uint32_t level, const uint16_t* __restrict__ rmin_below, uint16_t* __restrict__ rmin,
               uint8_t* __restrict__ nodes) {
@@ -120,20 +196,25 @@ k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const ui
         uint8_t* nd = nodes + (node_off + j) * 256;
         uint2* w = reinterpret_cast<uint2*>(nd);
         const uint64_t c0 = j * per, c1 = min(c0 + per, nbelow);
+        const uint32_t cnt = (uint32_t)(c1 - c0);
         uint16_t mn = CKS_NONE_INTERNAL;
         uint32_t last = 0;
-        for (uint32_t e = 0; e < 9; e++) {
-            const uint64_t ch = c0 + e;
+        for (uint32_t e = 0; e < 9u; e++) {
             uint2 a = make_uint2(0, 0), b = make_uint2(0, 0), c = make_uint2(0, 0);
-            if (ch < c1) {
-                const uint64_t hi = min((ch + 1) * cover_below, n) - 1;       // highest key of the child
-                const uint32_t rid = perm[hi];
-                const uint16_t rm = rmin_below[ch];
+            if (e < cnt) {
+                const uint64_t ch = c0 + e;
+                uint64_t hk = (ch + 1) * cover_below;                    // one past the child's highest key
+                if (hk > n) hk = n;
+                const uint64_t hi = hk - 1;
+                CKS_DCHECK(hi < n && ch < nbelow);
+                const uint32_t rid = __ldg(perm + hi);
+                const uint16_t rm = __ldg(rmin_below + ch);
                 mn = rm < mn ? rm : mn;
                 const uint16_t d = ch == 0 ? (uint16_t)CKS_NONE_INTERNAL : rm;   // vs the previous entry
                 last = rid;
                 const unsigned long long child = below_off + ch;
-                a = make_uint2(W8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk), (uint32_t)d | (B << 16));
+                const uint32_t pkv = src.get(hi, rid, d, pk);
+                a = make_uint2(pkv, (uint32_t)d | (B << 16));
                 b = make_uint2((uint32_t)child, (uint32_t)(child >> 32));
                 c = make_uint2(rid, 0u);
             }
@@ -141,7 +222,7 @@ k_ptree_inner(const uint8_t* __restrict__ keys, uint64_t n, uint32_t B, const ui
             w[4 + 3 * e] = b;
             w[5 + 3 * e] = c;
         }
-        w[0] = make_uint2((uint32_t)(c1 - c0) | (level << 16), B);
+        w[0] = make_uint2(cnt | (level << 16), B);
         w[1] = make_uint2(last, 0u);
         w[2] = make_uint2(0u, 0u);
         w[30] = make_uint2(0u, 0u);                               // bytes 240..255
@@ -157,33 +238,24 @@ static unsigned grid_pt(uint64_t work, int sms) {
     return (unsigned)(g ? g : 1);
 }
 
-cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
-                         uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
-                         const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
-                         uint16_t* rmin_b, int sms, cudaStream_t st, int* launches) {
+template <class Src>
+static cudaError_t run_ptree(const Src& src, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
+                             uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
+                             const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
+                             uint16_t* rmin_b, int sms, cudaStream_t st, int* launches) {
     *launches = 0;
     if (n == 0 || height == 0) return cudaSuccess;
-    const bool w8 = B % 8 == 0 && ((uintptr_t)keys & 7) == 0;    // (one path per instantiation)
-    if (w8)
-        k_ptree_leaf_entries<true><<<grid_pt(n, sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
-                                                                           level_nodes[0], nodes);
-    else
-        k_ptree_leaf_entries<false><<<grid_pt(n, sms), kPtThreads, 0, st>>>(keys, n, B, perm, dbit, pk, leaf_per,
-                                                                            level_nodes[0], nodes);
+    k_ptree_leaf_entries<Src><<<grid_pt(n, sms), kPtThreads, 0, st>>>(src, n, B, perm, dbit, pk, leaf_per,
+                                                                      level_nodes[0], nodes);
     k_ptree_leaf_min<<<grid_pt(level_nodes[0], sms), kPtThreads, 0, st>>>(dbit, n, leaf_per, level_nodes[0], rmin_a);
     *launches += 2;
     uint64_t cover = leaf_per;
     uint16_t* below = rmin_a;
     uint16_t* cur = rmin_b;
     for (uint32_t l = 1; l < height; l++) {
-        if (w8)
-            k_ptree_inner<true><<<grid_pt(level_nodes[l], sms), kPtThreads, 0, st>>>(
-                keys, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
-                level_offset[l], l, below, cur, nodes);
-        else
-            k_ptree_inner<false><<<grid_pt(level_nodes[l], sms), kPtThreads, 0, st>>>(
-                keys, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
-                level_offset[l], l, below, cur, nodes);
+        k_ptree_inner<Src><<<(unsigned)((level_nodes[l] + 31) / 32), 32, 0, st>>>(
+            src, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
+            level_offset[l], l, below, cur, nodes);
         ++*launches;
         cover *= inner_per;
         uint16_t* t = below;
@@ -191,6 +263,21 @@ cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint
         cur = t;
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
+                         uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
+                         const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
+                         uint16_t* rmin_b, int sms, cudaStream_t st, int* launches, const PtreeDs* ds) {
+    const bool w8 = B % 8 == 0 && ((uintptr_t)keys & 7) == 0;
+    if (ds) {
+        PkDs src{keys, B, w8, ds->planes, ds->pitch, ds->np, ds->gx, ds->gy, ds->tab};
+        return run_ptree(src, n, B, perm, dbit, pk, leaf_per, inner_per, level_nodes, level_offset, height, nodes,
+                         rmin_a, rmin_b, sms, st, launches);
+    }
+    PkRows src{keys, B, w8};
+    return run_ptree(src, n, B, perm, dbit, pk, leaf_per, inner_per, level_nodes, level_offset, height, nodes, rmin_a,
+                     rmin_b, sms, st, launches);
 }
 
 }  // namespace cks

@@ -373,12 +373,12 @@ __device__ __forceinline__ bool rk_less(unsigned long long ka, uint32_t xa, uint
     return ra < rb;
 }
 
-template <int WC>
+template <int WC, int NP>
 __global__ void __launch_bounds__(kRefThreads, 3)
 k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, uint64_t n,
           unsigned long long cmask, bool vec, uint8_t* __restrict__ tie, uint32_t* __restrict__ dacc,
           uint32_t* __restrict__ handled, uint8_t* __restrict__ any) {
-    static_assert(WC >= 1 && WC <= 3, "carried remaining words");
+    static_assert(WC >= 1 && WC <= 3 && (NP == 3 || NP == 4) && WC <= NP, "carried remaining words");
     constexpr int I = kTileItems;                                 // 8 positions per thread
     __shared__ uint32_t s_pm[3];                                  // D of the CTA as P_M bit indices
     __shared__ uint32_t s_cnt;
@@ -396,12 +396,18 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
         auto top = [&](uint64_t k) -> unsigned long long {
             return (((unsigned long long)__ldg(hi + k) << 32) | (unsigned long long)__ldg(lo + k)) & cmask;
         };
-        // A. loads: chunk words (hi = plane 2, lo = plane 1 of the carried planes), row ids, plane 0
-        uint32_t vh[I], vl[I], vr[I], v0[I];
+        // A. loads: chunk words (hi = plane NP-1, lo = plane NP-2 of the carried planes), row
+        // ids, the planes below the chunk (0, and 1 when NP = 4)
+        uint32_t vh[I], vl[I], vr[I], v0[I], v1[I];
         ld8(hi, p0, n, vec, vh);
         ld8(lo, p0, n, vec, vl);
         ld8(R.perm, p0, n, vec, vr);
-        if (WC >= 1) ld8(R.carried, p0, n, vec, v0);                  // plane 0
+        ld8(R.carried, p0, n, vec, v0);                               // plane 0
+        if (NP == 4) ld8(R.carried + R.pitch, p0, n, vec, v1);        // plane 1
+        else {
+#pragma unroll
+            for (int j = 0; j < I; j++) v1[j] = 0u;
+        }
         const uint32_t vm = p0 >= n ? 0u : (p0 + I <= n ? 0xFFu : (1u << (uint32_t)(n - p0)) - 1u);
         unsigned long long tk[I];
     #pragma unroll
@@ -443,8 +449,9 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
             const uint32_t s = 31u - (uint32_t)__clz(~L & 0xFFu);     // its first position
             hl &= ~(0xFFu & ~((2u << s) - 1u));
         }
-        // remaining keys (plane q of position j: q = 2 -> vh, 1 -> vl, 0 -> v0; q compile-time)
-    #define CKS_PV(q, j) ((q) == 2 ? vh[j] : (q) == 1 ? vl[j] : v0[j])
+        // remaining keys (plane q of position j, q compile-time: NP-1 -> vh, NP-2 -> vl, 1 -> v1, 0 -> v0)
+    #define CKS_PV(q, j) ((q) == NP - 1 ? vh[j] : (q) == NP - 2 ? vl[j] : (q) == 1 ? v1[j] : v0[j])
+    #define CKS_PV2(q, j) ((q) == NP - 1 ? vh[j] : (q) == NP - 2 ? vl[j] : (q) == 1 ? v1[j] : v0[j])
         unsigned long long key[I];
         uint32_t kx[I], topw[I];                                      // topw: word 0's chunk bits (equal in a run)
     #pragma unroll
@@ -455,8 +462,9 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
             if (WC == 1) key[j] = w0;
             else key[j] = ((unsigned long long)w0 << 32) | CKS_PV(WC - 2, j);
     #undef CKS_PV
-            kx[j] = WC == 3 ? v0[j] : 0u;
+            kx[j] = WC == 3 ? CKS_PV2(0, j) : 0u;
         }
+    #undef CKS_PV2
         // D. odd-even transposition network over the handled runs: L phases sort runs of up to L
         // keys, so the warp runs as many phases as its longest handled run (mostly 2-4), each
         // comparator a branch-free select
@@ -1019,24 +1027,23 @@ cudaError_t launch_ref_tile(const uint32_t* pm, uint64_t pitch, uint32_t np, int
     if (n == 0) return cudaSuccess;
     const uint32_t nwords = (8 * B + 31) / 32;
     RunCtx R{pm, pitch, np, qtop, fmask, moff, perm, dbit, carried};
-    const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
-    const uint64_t cap = 1ull << 31;                             // a tile per CTA (measured: 1% faster than 3 per SM persistent)
-    const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     const bool vec = al(perm) && al(dbit) && al(hi) && (!lo || al(lo)) && (hpitch & 3) == 0 && (pitch & 3) == 0 &&
                      (!carried || al(carried));
     if (!carried) return cudaErrorInvalidValue;
     const int wc = qtop + 1;
-    const bool alias = np == 3 && lo == carried + pitch && hi == carried + 2 * pitch;
+    const bool alias = (np == 3 || np == 4) && lo == carried + (np - 2) * pitch && hi == carried + (np - 1) * pitch;
     if (!alias) return cudaErrorInvalidValue;                    // (chunk = carried planes 2, 1)
     (void)nwords;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ref_reg<2>, kRefThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ref_reg<2, 3>, kRefThreads, 0);
     const uint64_t tiles = (n + kTileKeys - 1) / kTileKeys, gmax = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
     const unsigned rgrid = (unsigned)(tiles < gmax ? tiles : gmax);
 #define CKS_TILE_CASE(W)                                                                                        \
     case W:                                                                                                     \
-        k_ref_reg<W><<<rgrid, kRefThreads, 0, st>>>(R, lo, hi, n, cmask, vec, tie, dacc, handled, any);        \
+        if (np == 4) k_ref_reg<W < 3 ? W : 3, 4><<<rgrid, kRefThreads, 0, st>>>(R, lo, hi, n, cmask, vec, tie,   \
+                                                                                dacc, handled, any);           \
+        else k_ref_reg<W, 3><<<rgrid, kRefThreads, 0, st>>>(R, lo, hi, n, cmask, vec, tie, dacc, handled, any); \
         break;
     switch (wc) {
         CKS_TILE_CASE(1)

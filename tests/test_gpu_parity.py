@@ -496,6 +496,95 @@ def test_paper_tree_vs_oracle(cfg, n, pk, fill):
     assert np.array_equal(nodes.cpu().numpy(), ref["nodes"])
 
 
+@pytest.mark.parametrize("cfg,n", [(1, 30_001), (3, 80_000), (5, 90_001), (2, 50_000)])
+def test_ds_metadata_first_build_and_rebuild(cfg, n):
+    # DS-metadata recompute: the variant bitmap V and the reference key come out of
+    # the first build (from its superset pass) and of a rebuild (one more pass over the keys)
+    keys = cksgen.config(cfg, n=n)
+    d = dev(keys)
+    V = oracle.variant_bitmap(keys)
+    r = cks.build(d, ds_metadata=True)
+    assert np.array_equal(r["variant"], V) and np.array_equal(r["ref_key"], keys[0])
+    r2 = cks.build(d, prior_mask=r["mask"], ds_metadata=True)
+    assert np.array_equal(r2["variant"], V) and np.array_equal(r2["ref_key"], keys[0])
+    check_build(keys, r2)
+    # D is a subset of V: every distinction bit varies
+    assert positions(r["mask"]) <= positions(V)
+
+
+@pytest.mark.parametrize("cfg,n,pk,fill", [(1, 13, 32, 0.9), (5, 40_963, 32, 0.9), (3, 100_003, 32, 0.9),
+                                           (4, 60_000, 17, 0.9), (2, 77_777, 8, 1.0), (1, None, 32, 0.9),
+                                           (5, 1, 32, 0.9), (3, 5000, 1, 0.5)])
+def test_paper_tree_ds_sources_vs_oracle(cfg, n, pk, fill):
+    # NEXT-3 partial keys from the paper's sources: A = the sorted compressed key
+    # (P_D from the build), B = the reference key for invariant bits, C(b) = the key row only
+    # for variant bits outside D. The node images must equal the oracle's (bits from the rows)
+    keys = cksgen.config(cfg, n=n)
+    N, B = keys.shape
+    d = dev(keys)
+    r = cks.build(d, ds_metadata=True)
+    perm, dbit = r["perm"], r["dbit"]
+    nodes = cks.paper_tree_ds(d, N, B, perm, dbit, r["packed"], N, r["mask"], r["variant"], r["ref_key"], pk, fill)
+    ref = oracle.paper_tree(keys, u32(perm), u16(dbit), pk=pk, fill=fill)
+    assert np.array_equal(nodes.cpu().numpy(), ref["nodes"])
+    # with every variant bit in the planes' mask no row is read: keys may be NULL
+    if positions(r["variant"]) <= positions(r["mask"]):
+        nodes2 = cks.paper_tree_ds(None, N, B, perm, dbit, r["packed"], N, r["mask"], r["variant"], r["ref_key"],
+                                   pk, fill)
+        assert np.array_equal(nodes2.cpu().numpy(), ref["nodes"])
+    elif N:
+        with pytest.raises(cks.CksError):
+            cks.paper_tree_ds(None, N, B, perm, dbit, r["packed"], N, r["mask"], r["variant"], r["ref_key"], pk, fill)
+
+
+@pytest.mark.parametrize("cfg,n,pk,fill,ds", [(5, 120_001, 32, 0.9, False), (5, 70_001, 17, 1.0, True),
+                                              (3, 90_000, 32, 0.9, True), (4, 50_000, 32, 0.9, False),
+                                              (1, None, 24, 0.9, False), (2, 40_000, 32, 0.9, True)])
+def test_build_fused_paper_tree(cfg, n, pk, fill, ds):
+    # cks_build with ptree_nodes: the paper-format tree from the same call. With P_M carried
+    # (cfg5) the variant bits outside the sort mask that partial keys need ride through the sort
+    # as one more plane (C(a)); the build's own outputs must not change
+    keys = cksgen.config(cfg, n=n)
+    r = cks.build(dev(keys), paper_tree_pk=pk, paper_tree_fill=fill, ds_metadata=ds)
+    check_build(keys, r)
+    ref = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=pk, fill=fill)
+    assert np.array_equal(r["paper_tree"].cpu().numpy(), ref["nodes"])
+
+
+@pytest.mark.parametrize("T", [24, 40, 64])
+def test_fused_paper_tree_forced_round0(T):
+    # the appended plane through every round-0 width (T < 32 leaves 4 remaining words: the
+    # compaction path; T = 40 / 64 the register finisher with 4 planes)
+    keys = cksgen.config(5, n=66_000)
+    cks.set_round0_bits(T)
+    try:
+        r = cks.build(dev(keys), paper_tree_pk=32)
+    finally:
+        cks.set_round0_bits(0)
+    check_build(keys, r)
+    ref = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
+    assert np.array_equal(r["paper_tree"].cpu().numpy(), ref["nodes"])
+
+
+def test_paper_tree_ds_all_variant_bits_compressed():
+    # the packed mask = V (a rebuild sorted by the variant bitmap): partial keys need no rows
+    keys = cksgen.config(3, n=60_000)
+    N, B = keys.shape
+    d = dev(keys)
+    V = oracle.variant_bitmap(keys)
+    r = cks.build(d, prior_mask=V, ds_metadata=True)
+    cks.set_sort_mode(cks.SORT_SINGLE)
+    try:
+        rv = cks.build(d, prior_mask=V)
+    finally:
+        cks.set_sort_mode(cks.SORT_PREFIX_AUTO)
+    planes = cks.compress(d, V)                                   # P_V in row order ...
+    sorted_pv = planes[:, rv["perm"].long()].contiguous()         # ... in sorted order
+    nodes = cks.paper_tree_ds(None, N, B, rv["perm"], rv["dbit"], sorted_pv, N, V, V, r["ref_key"], 32, 0.9)
+    ref = oracle.paper_tree(keys, u32(rv["perm"]), u16(rv["dbit"]), pk=32, fill=0.9)
+    assert np.array_equal(nodes.cpu().numpy(), ref["nodes"])
+
+
 @pytest.mark.parametrize("seed", [4, 5])
 def test_refine_chunk_cta_rounds(seed):
     # 64-byte keys (D+ = 512 bits: more remaining planes than the CTA tier takes), runs of
