@@ -539,20 +539,47 @@ def main():
                                 "mask = every key bit) and on compressed keys (prior mask = the exact D-bitmap, "
                                 "the paper's extract + sort + build), per sort mode; steps per leg: %d" % fs})
         del full, comp
-        # NEXT-3: the paper's 256-byte-node index tree from this build's perm and D_i (pk = 32)
+        # NEXT-3: the paper's 256-byte-node index tree (pk = 32, fill 0.9), three ways:
+        #   rows   cks_paper_tree: every partial-key bit from the key row (C(b), random row reads)
+        #   ds     cks_paper_tree_ds: A from the sorted P_D, B from the reference key, C(b) rows only
+        #          for variant bits outside D
+        #   fused  cks_build with ptree_nodes: the bits partial keys need outside the sort mask ride
+        #          through the sort as one more plane (C(a)); reported as the build's extra time
         ps = cks.paper_tree_shape(n, 0.9)
         nodes = torch.empty((int(ps.total_nodes), cks.PTREE_NODE_BYTES), dtype=torch.uint8, device=device)
-        cks.paper_tree(keys, builder.perm[:n], builder.dbit[:n], 32, 0.9, out=nodes)
-        e0.record(stream)
-        for _ in range(fs):
-            cks.paper_tree(keys, builder.perm[:n], builder.dbit[:n], 32, 0.9, out=nodes)
-        e1.record(stream)
-        torch.cuda.synchronize(device)
-        pms = e0.elapsed_time(e1) / fs
-        paper_stats.update({"paper_tree_ms": pms, "paper_tree_nodes": int(ps.total_nodes),
-                            "paper_tree_height": int(ps.height),
-                            "paper_tree_note": "NEXT-3: 256-B nodes, leaf 12/14, inner 8/9 entries (fill 0.9), "
-                                               "pk 32 read from the key rows"})
+
+        def timed(fn):
+            fn()
+            torch.cuda.synchronize(device)
+            e0.record(stream)
+            for _ in range(fs):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize(device)
+            return e0.elapsed_time(e1) / fs
+        pms = timed(lambda: cks.paper_tree(keys, builder.perm[:n], builder.dbit[:n], 32, 0.9, out=nodes))
+        dsb = cks.Builder(n, B, device, fanout=64, fill=1.0, ds_metadata=True)
+        dsb(keys)
+        pk_planes = dsb.packed()
+        dms = timed(lambda: cks.paper_tree_ds(keys, n, B, dsb.perm[:n], dsb.dbit[:n], pk_planes, pk_planes.stride(0),
+                                              dsb.mask, dsb.variant, dsb.ref_key, 32, 0.9, out=nodes))
+        same_ds = bool(torch.equal(nodes, cks.paper_tree(keys, dsb.perm[:n], dsb.dbit[:n], 32, 0.9)))
+        del dsb, pk_planes
+        fused = {}
+        for name, src in (("rows", cks.PTREE_ROWS), ("ds", cks.PTREE_DS), ("carry", cks.PTREE_CARRY)):
+            fb = cks.Builder(n, B, device, fanout=64, fill=1.0, paper_tree_pk=32, paper_tree_fill=0.9,
+                             paper_tree_source=src)
+            fms = timed(lambda: fb(keys))
+            fused[name] = {"build_with_tree_ms": fms, "tree_extra_ms": fms - ms,
+                           "equals_rows_tree": bool(torch.equal(fb.ptree[:fb.ptree_nodes], nodes))}
+            del fb
+        paper_stats.update({"paper_tree_ms": pms, "paper_tree_ds_ms": dms, "fused_build_with_tree": fused,
+                            "paper_tree_nodes": int(ps.total_nodes),
+                            "paper_tree_height": int(ps.height), "ds_tree_equals_rows_tree": same_ds,
+                            "paper_tree_note": "NEXT-3: 256-B nodes, leaf 12/14, inner 8/9 entries (fill 0.9), pk 32; "
+                                               "paper_tree_ms: bits from the key rows (C(b)); paper_tree_ds_ms: A "
+                                               "from P_D + B + C(b) where needed; fused: C(a), the needed variant "
+                                               "bits carried through the sort (P:484-496)"})
         del nodes
 
     cpu = None

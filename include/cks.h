@@ -378,16 +378,27 @@ typedef struct {
                                  more pass over the keys for it */
     uint8_t* ref_key;         /* host u8[key_bytes] or NULL: receives the reference key value,
                                  the key of row 0 ("an arbitrary index key") */
-    /* NEXT-3, optional: the paper-format index tree (cks_paper_tree's layout) built by the same
-     * call from the sorted order, with partial keys from the sources of P:484-496: A the
-     * compressed key, B the reference key for invariant bits, C(a) the variant bits outside the
-     * sort mask that some partial key needs, compressed into one more plane that rides through
-     * the sort with P_M (when P_M has three planes and they fit one plane), else C(b) the key
-     * rows. cks_paper_tree_shape(n, ptree_fill) gives the node count. */
+    /* NEXT-3, optional: the paper-format index tree (cks_paper_tree's layout, identical bytes)
+     * built by the same call from the sorted order; partial-key bits from the sources of
+     * P:484-496 chosen by ptree_source:
+     *   CKS_PTREE_ROWS   C(b): every bit from the key row (random row reads; measured fastest
+     *                    on cfg5, DESIGN.md Sec. 6.3 -- the default);
+     *   CKS_PTREE_DS     A from the sorted P_D, B from the reference key for invariant bits, C(b)
+     *                    rows only for the variant bits outside D;
+     *   CKS_PTREE_CARRY  as DS, with C(a): the variant bits outside the sort mask that some
+     *                    partial key needs are compressed into one more plane that rides through
+     *                    the sort with P_M (when P_M has three planes and they fit one plane), so
+     *                    the tree reads no rows.
+     * cks_paper_tree_shape(n, ptree_fill) gives the node count. */
     uint8_t* ptree_nodes;     /* device u8[total_nodes][256] or NULL (no paper tree) */
     uint32_t ptree_pk;        /* partial key bits (<= 32) */
+    uint32_t ptree_source;    /* CKS_PTREE_ROWS (0) / CKS_PTREE_DS (1) / CKS_PTREE_CARRY (2) */
     double ptree_fill;        /* fill factor in (0, 1] */
 } cks_build_out;
+
+#define CKS_PTREE_ROWS 0
+#define CKS_PTREE_DS 1
+#define CKS_PTREE_CARRY 2
 
 /* keys: device u8[n][key_bytes]; prior_mask: host u8[key_bytes] superset or NULL.
  * A prior mask must contain every distinction bit of THIS column (e.g. the D-bitmap of the

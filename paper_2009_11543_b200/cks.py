@@ -54,7 +54,11 @@ class BuildOut(ctypes.Structure):
                 ("packed", ctypes.c_void_p), ("packed_pitch", ctypes.c_uint64),
                 ("rounds", ctypes.c_uint32), ("round0_bits", ctypes.c_uint32), ("refined_keys", ctypes.c_uint64),
                 ("variant", ctypes.c_void_p), ("ref_key", ctypes.c_void_p),
-                ("ptree_nodes", ctypes.c_void_p), ("ptree_pk", ctypes.c_uint32), ("ptree_fill", ctypes.c_double)]
+                ("ptree_nodes", ctypes.c_void_p), ("ptree_pk", ctypes.c_uint32), ("ptree_source", ctypes.c_uint32),
+                ("ptree_fill", ctypes.c_double)]
+
+
+PTREE_ROWS, PTREE_DS, PTREE_CARRY = 0, 1, 2
 
 
 EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing", "cks_ctx_set_sort_mode",
@@ -517,7 +521,8 @@ class Builder:
 
     def __init__(self, n: int, B: int, device, fanout: int = 64, fill: float = 1.0,
                  superset_kind: int = SUPERSET_BYTEOCC, tree: bool = True, dbit: bool = True,
-                 ds_metadata: bool = False, paper_tree_pk: int | None = None, paper_tree_fill: float = 0.9):
+                 ds_metadata: bool = False, paper_tree_pk: int | None = None, paper_tree_fill: float = 0.9,
+                 paper_tree_source: int = 0):
         self.n, self.B = n, B
         self.mask = np.zeros(B, np.uint8)
         # DS-metadata: variant bitmap and reference key, recomputed by the build
@@ -549,6 +554,7 @@ class Builder:
             self.out.ptree_nodes = self.ptree.data_ptr()
             self.out.ptree_pk = paper_tree_pk
             self.out.ptree_fill = paper_tree_fill
+            self.out.ptree_source = paper_tree_source
 
     def __call__(self, keys: torch.Tensor, prior_mask=None) -> "Builder":
         n, B = _keys(keys)
@@ -579,10 +585,10 @@ def raw_view(ptr: int, numel: int, device) -> torch.Tensor:
 
 def build(keys: torch.Tensor, prior_mask=None, fanout: int = 64, fill: float = 1.0,
           superset_kind: int = SUPERSET_BYTEOCC, tree: bool = True, ds_metadata: bool = False,
-          paper_tree_pk: int | None = None, paper_tree_fill: float = 0.9) -> dict:
+          paper_tree_pk: int | None = None, paper_tree_fill: float = 0.9, paper_tree_source: int = 0) -> dict:
     n, B = _keys(keys)
     b = Builder(n, B, keys.device, fanout, fill, superset_kind, tree, ds_metadata=ds_metadata,
-                paper_tree_pk=paper_tree_pk, paper_tree_fill=paper_tree_fill)
+                paper_tree_pk=paper_tree_pk, paper_tree_fill=paper_tree_fill, paper_tree_source=paper_tree_source)
     b(keys, prior_mask)
     o = b.out
     r = dict(mask=b.mask.copy(), popcount=int(o.popcount), sort_bits=int(o.sort_bits), passes=int(o.passes),

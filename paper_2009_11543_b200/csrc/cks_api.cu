@@ -70,6 +70,8 @@ struct cks_ctx {
     std::vector<uint8_t> pt_E;        // fused paper tree: partial-key bits appended to P_M (C(a))
     bool pt_on = false;
     uint32_t pt_npe = 0;              // planes actually appended by the last build_refine
+    PtreeEnt* h_ptab = nullptr;       // pinned staging of the paper tree's per-window table
+    cudaEvent_t ptab_ev = nullptr;
     bool skip_packed = false;         // cks_sort_prefix without packed_out: no a7
 };
 
@@ -668,8 +670,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         if (!carry) TRY(ensure(ctx, ctx->pd, (size_t)npd * sp * 4));
         uint32_t* pd = carry ? pm : as<uint32_t>(ctx->pd);       // (P_M in row order is no longer needed)
         const bool single = T >= m;                               // round 0 sorted all of P_M
-        if ((single || carry) && lead == 0 && npe == 0 && same_mask(out->mask, M, B)) {
-            out->packed = sorted0;
+        if ((single || carry) && lead == 0 && same_mask(out->mask, M, B)) {
+            out->packed = sorted0 + (uint64_t)npe * sp0;           // (P_M's planes above the appended P_E)
             out->packed_pitch = sp0;
         } else if (single || carry) {
             std::vector<uint32_t> sub(np, 0);
@@ -933,28 +935,35 @@ int run_ptree_ds(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     if (n == 0) return CKS_OK;
     TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
     TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
-    // tables (k_ptree.cu PkDs): rows of S = B + 8 bytes (8 zero bytes after each, so a 40-bit
-    // window never needs a bound check) for X, Y, V and the reference key, then the u16 rank of
-    // each byte's first X / Y position
-    const size_t S = (size_t)B + 8, tb = 4 * S + 4 * (size_t)B;
-    TRY(ensure(ctx, ctx->ptab, tb + 16));
-    CK(cudaEventSynchronize(ctx->plan_ev[2]));
-    uint8_t* h = reinterpret_cast<uint8_t*>(ctx->h_small);
-    memset(h, 0, tb);
-    memcpy(h, X, B);
-    if (Y) memcpy(h + S, Y, B);
-    memcpy(h + 2 * S, V, B);
-    memcpy(h + 3 * S, ref, B);
-    uint16_t rx = 0, ry = 0;
-    for (uint32_t j = 0; j < B; j++) {
-        memcpy(h + 4 * S + 2 * j, &rx, 2);
-        memcpy(h + 4 * S + 2 * (size_t)B + 2 * j, &ry, 2);
-        rx = (uint16_t)(rx + __builtin_popcount(X[j]));
-        ry = (uint16_t)(ry + (Y ? __builtin_popcount(Y[j]) : 0));
+    // per-window-start table (k_ptree.cu PkDs): for p0 = 0 .. 8B, the pk-bit window's X / Y /
+    // invariant / row positions and the ranks of its first position in X and Y
+    const uint32_t nb = 8 * B, nent = nb + 1;
+    TRY(ensure(ctx, ctx->ptab, (size_t)nent * sizeof(PtreeEnt) + 16));
+    if (!ctx->h_ptab) {
+        CK(cudaMallocHost(&ctx->h_ptab, (size_t)(8 * CKS_MAX_KEY_BYTES + 1) * sizeof(PtreeEnt)));
+        CK(cudaEventRecord(ctx->ptab_ev, ctx->stream));
     }
-    CK(cudaMemcpyAsync(ctx->ptab.p, h, tb, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaEventRecord(ctx->plan_ev[2], ctx->stream));
-    PtreeDs ds{planes, pitch, np, gx, gy, as<uint8_t>(ctx->ptab)};
+    CK(cudaEventSynchronize(ctx->ptab_ev));                     // the previous upload is done
+    auto bit = [&](const uint8_t* m, uint32_t p) -> uint32_t {
+        return (m && p < nb) ? (uint32_t)(m[p >> 3] >> (7 - (p & 7))) & 1u : 0u;
+    };
+    uint32_t rx = 0, ry = 0;
+    for (uint32_t p0 = 0; p0 < nent; p0++) {
+        PtreeEnt& e = ctx->h_ptab[p0];
+        e = PtreeEnt{0, 0, 0, 0, rx, ry};
+        for (uint32_t i = 0; i < pk && p0 + i < nb; i++) {
+            const uint32_t p = p0 + i, b = 0x80000000u >> i;
+            if (bit(X, p)) e.wx |= b;
+            else if (bit(Y, p)) e.wy |= b;
+            else if (bit(V, p)) e.wc |= b;
+            else if (bit(ref, p)) e.refb |= b;
+        }
+        rx += bit(X, p0);
+        ry += bit(Y, p0);
+    }
+    CK(cudaMemcpyAsync(ctx->ptab.p, ctx->h_ptab, (size_t)nent * sizeof(PtreeEnt), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->ptab_ev, ctx->stream));
+    PtreeDs ds{planes, pitch, np, gx, gy, as<PtreeEnt>(ctx->ptab)};
     int nl = 0;
     CK(launch_ptree(keys, n, B, perm, dbit, pk, s.per_node, s.reserved, s.level_nodes, s.level_offset, s.height, nodes,
                     as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl, &ds));
@@ -965,21 +974,24 @@ int run_ptree_ds(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
 
 int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* prior,
                  cks_build_out* out, bool keys_ready_for_mask) {
-    std::vector<uint8_t> M(B, 0);
+    std::vector<uint8_t> M(B, 0), V(B, 0);
     uint32_t m = 0;
+    const bool ptree = out->ptree_nodes != nullptr && n > 0;
+    const bool want_v = out->variant || ptree;
     if (prior) {
         memcpy(M.data(), prior, B);
         m = popcount_mask(M.data(), B);
-        if (out->variant) {
+        if (want_v) {
             // rebuild: the new variant bitmap needs one pass over the keys (P:413 step 3)
             std::vector<uint8_t> tmp(B);
             uint32_t mt = 0;
-            TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_VARIANT, tmp.data(), &mt, true, out->variant));
+            TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_VARIANT, tmp.data(), &mt, true, V.data()));
         }
     } else {
         int kind = out->superset_kind;
-        TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask, out->variant));
+        TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask, V.data()));
     }
+    if (out->variant) memcpy(out->variant, V.data(), B);
     if (out->ref_key) {                                  // the reference key (row 0's key)
         if (n) {
             CK(cudaEventSynchronize(ctx->plan_ev[2]));
@@ -992,19 +1004,13 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     }
     // NEXT-3 fused paper tree: DS-metadata V and the reference key, and the partial-key bits that
     // are variant but not in M (E, P:492 C(a)) -- appended to P_M when P_M is carried (3 planes)
-    const bool ptree = out->ptree_nodes != nullptr && n > 0;
-    std::vector<uint8_t> V(B, 0), ref(B, 0);
+    std::vector<uint8_t> ref(B, 0);
     ctx->pt_on = false;
     ctx->pt_npe = 0;
     if (ptree) {
         if (out->ptree_pk > 32) return fail(ctx, CKS_EINVAL, "ptree_pk %u > 32", out->ptree_pk);
-        if (out->variant) {
-            memcpy(V.data(), out->variant, B);
-        } else {
-            uint32_t mt = 0;
-            std::vector<uint8_t> tmp(B);
-            TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_VARIANT, tmp.data(), &mt, true, V.data()));
-        }
+        if (out->ptree_source > CKS_PTREE_CARRY)
+            return fail(ctx, CKS_EINVAL, "unknown ptree_source %u", out->ptree_source);
         CK(cudaEventSynchronize(ctx->plan_ev[2]));
         CK(cudaMemcpyAsync(ctx->h_small, keys, B, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -1021,7 +1027,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             if (inV && !inM && inwin) { ctx->pt_E[p >> 3] |= (uint8_t)(0x80u >> (p & 7)); ne++; }
             if (inM) last = (int)p;
         }
-        ctx->pt_on = ne > 0 && ne <= 32;
+        ctx->pt_on = out->ptree_source == CKS_PTREE_CARRY && ne > 0 && ne <= 32;
     }
     mark(ctx, ST_MASK);
     ctx->verify_now = keys && (ctx->verify == CKS_VERIFY_ALWAYS || (ctx->verify == CKS_VERIFY_PRIOR && prior));
@@ -1031,7 +1037,18 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     TRY(rc);
     if (ptree) {
         const uint16_t* db = out->dbit ? out->dbit : as<uint16_t>(ctx->dbit);
-        if (ctx->pt_npe) {                                       // A from the carried P_M | P_E, B, no rows
+        if (out->ptree_source == CKS_PTREE_ROWS) {                // C(b) for every bit
+            cks_tree_shape s;
+            TRY(cks_paper_tree_shape(n, out->ptree_fill, &s) == CKS_OK ? CKS_OK
+                    : fail(ctx, CKS_EINVAL, "bad paper-tree fill %f", out->ptree_fill));
+            TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
+            TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+            int nl = 0;
+            CK(launch_ptree(keys, n, B, out->perm, db, out->ptree_pk, s.per_node, s.reserved, s.level_nodes,
+                            s.level_offset, s.height, out->ptree_nodes, as<uint16_t>(ctx->rmin0),
+                            as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl));
+            ctx->launches += (uint64_t)nl;
+        } else if (ctx->pt_npe) {                                       // A from the carried P_M | P_E, B, no rows
             const uint32_t npm = (m + 31) / 32;
             TRY(run_ptree_ds(ctx, keys, n, B, out->perm, db, as<uint32_t>(ctx->pd), scratch_pitch(n), npm + 1,
                              M.data(), 0, ctx->pt_E.data(), 32 * npm, V.data(), ref.data(), out->ptree_pk,
@@ -1077,6 +1094,7 @@ int cks_ctx_create(int device, void* stream, cks_ctx** out) {
     if (ok) ok = cudaMallocHost(&ctx->h_moff, kMaxBits * 2) == cudaSuccess;
     if (ok) ok = cudaMallocHost(&ctx->h_small, 8192) == cudaSuccess;
     if (ok) ok = cudaMallocHost(&ctx->h_tot, 64) == cudaSuccess;
+    if (ok) ok = cudaEventCreateWithFlags(&ctx->ptab_ev, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < 3 && ok; i++) ok = cudaEventRecord(ctx->plan_ev[i], ctx->stream) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -1103,6 +1121,8 @@ int cks_ctx_destroy(cks_ctx* ctx) {
     if (ctx->h_moff) cudaFreeHost(ctx->h_moff);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
+    if (ctx->h_ptab) cudaFreeHost(ctx->h_ptab);
+    if (ctx->ptab_ev) cudaEventDestroy(ctx->ptab_ev);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
     for (int i = 0; i < 6; i++)

@@ -196,12 +196,18 @@ cudaError_t launch_bulk_inner(const uint32_t* perm, const uint16_t* rmin_below, 
 // NEXT-3 paper-format index tree (k_ptree.cu). ds == NULL: partial keys from the key rows;
 // else from the DS-metadata sources (sorted compressed planes, reference key, rows only for
 // variant positions outside the planes' mask).
+// Per window start p0 (= D + 1, 0 for none; 8B + 1 entries): the pk-bit window's positions in X
+// and in Y, its invariant bits taken from the reference key, the variant positions in neither
+// (read from the rows), and the rank in X / Y of the window's first position.
+struct PtreeEnt {
+    uint32_t wx, wy, refb, wc, rx, ry;
+};
 struct PtreeDs {
     const uint32_t* planes;    // sorted compressed planes: segment X (mask X) then Y (mask Y)
     uint64_t pitch;
     uint32_t np;
     uint32_t gx, gy;           // first bit of X / Y counted from the MSB of the np planes
-    const uint8_t* tab;        // device tables: X, Y, variant, ref bytes; u16 byte ranks of X, Y
+    const PtreeEnt* ent;       // device table, 8B + 1 entries
 };
 cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
                          uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,

@@ -66,8 +66,14 @@ struct PkRows {
     const uint8_t* keys;
     uint32_t B;
     bool w8;
-    __device__ __forceinline__ uint32_t get(uint64_t /*k*/, uint32_t rid, uint16_t d, uint32_t pk) const {
+    __device__ __forceinline__ void pre(uint64_t, uint32_t (&)[4]) const {}
+    __device__ __forceinline__ uint32_t get(uint64_t /*k*/, uint32_t rid, uint16_t d, uint32_t pk,
+                                            const uint32_t (&)[4]) const {
         return w8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk);
+    }
+    __device__ __forceinline__ uint32_t get(uint64_t k, uint32_t rid, uint16_t d, uint32_t pk) const {
+        const uint32_t w[4] = {0, 0, 0, 0};
+        return get(k, rid, d, pk, w);
     }
 };
 
@@ -80,35 +86,29 @@ struct PkDs {
     uint32_t np;
     uint32_t gx, gy;                     // bit (from the MSB of the np planes) of segment X's / Y's
                                          // first compressed bit; X then Y (Y may be empty)
-    const uint8_t* tab;                  // device: 4 byte rows of S = B + 8 bytes (the last 8 zero):
-                                         // X mask, Y mask, variant, ref key; then u16 ranks of
-                                         // byte j's first X / Y bit at 4S + 2j / 4S + 2B + 2j
-    __device__ __forceinline__ uint32_t S() const { return B + 8u; }
-    // 32 mask/key bits of table row `row` from bit p0 (MSB-first, p0 < 8B; zero past the key)
-    __device__ __forceinline__ uint32_t win(uint32_t row, uint32_t p0) const {
-        const uint8_t* b = tab + row * S() + (p0 >> 3);
-        unsigned long long w = 0;
+    const PtreeEnt* ent;                 // per window start p0 = D + 1 (0 for none), 8B + 1 entries
+    // the plane words of sorted position k loaded ahead (np <= 4): the loads do not wait for the
+    // per-window table lookup
+    __device__ __forceinline__ void pre(uint64_t k, uint32_t (&w)[4]) const {
 #pragma unroll
-        for (int i = 0; i < 5; i++) w = (w << 8) | (uint32_t)b[i];
-        return (uint32_t)(w >> (8 - (p0 & 7)));
+        for (int q = 0; q < 4; q++) w[q] = (np <= 4 && q < (int)np) ? __ldg(planes + (uint64_t)q * pitch + k) : 0u;
+    }
+    __device__ __forceinline__ static uint32_t pick(const uint32_t (&w)[4], int q) {
+        return q == 0 ? w[0] : q == 1 ? w[1] : q == 2 ? w[2] : w[3];
     }
     // c (<= 32) bits of the planes from bit g (counted from the MSB), left-aligned
-    __device__ __forceinline__ uint32_t field(uint64_t k, uint32_t g, uint32_t c) const {
-        if (c == 0) return 0u;
+    __device__ __forceinline__ uint32_t field(uint64_t k, uint32_t g, uint32_t c, const uint32_t (&w)[4]) const {
         const int q = (int)np - 1 - (int)(g >> 5);
         CKS_DCHECK(q >= 0 && q < (int)np && k < pitch);
-        const uint32_t a = __ldg(planes + (uint64_t)q * pitch + k);
-        const uint32_t b = q >= 1 ? __ldg(planes + (uint64_t)(q - 1) * pitch + k) : 0u;
+        const bool reg = np <= 4;
+        const uint32_t a = reg ? pick(w, q) : __ldg(planes + (uint64_t)q * pitch + k);
+        const uint32_t b = q >= 1 ? (reg ? pick(w, q - 1) : __ldg(planes + (uint64_t)(q - 1) * pitch + k)) : 0u;
         const uint32_t v = (g & 31) ? __funnelshift_l(b, a, g & 31) : a;
         return c >= 32 ? v : v & ~(0xFFFFFFFFu >> c);
     }
-    // A: the window's bits of segment `row` (0 = X, 1 = Y), deposited at their positions w
-    __device__ __forceinline__ uint32_t seg_bits(uint64_t k, uint32_t p0, uint32_t w, uint32_t row, uint32_t g0) const {
-        const uint32_t j0 = p0 >> 3;
-        const uint8_t* rk = tab + 4 * S() + 2 * row * B + 2 * j0;
-        const uint32_t r = ((uint32_t)rk[0] | ((uint32_t)rk[1] << 8)) +
-                           (uint32_t)__popc((uint32_t)tab[row * S() + j0] >> (8 - (p0 & 7)));
-        uint32_t f = field(k, g0 + r, (uint32_t)__popc(w)), m = w, out = 0;
+    // the left-aligned field's bits deposited, in order, at the set bits of m (software PDEP)
+    __device__ __forceinline__ static uint32_t deposit(uint32_t f, uint32_t m) {
+        uint32_t out = 0;
         while (m) {
             const uint32_t hb = 0x80000000u >> __clz(m);
             if (f & 0x80000000u) out |= hb;
@@ -118,16 +118,21 @@ struct PkDs {
         return out;
     }
     __device__ __forceinline__ uint32_t get(uint64_t k, uint32_t rid, uint16_t d, uint32_t pk) const {
-        if (pk == 0) return 0u;
-        const uint32_t p0 = d == CKS_NONE_INTERNAL ? 0u : (uint32_t)d + 1;
-        if (p0 >= 8 * B) return 0u;
-        const uint32_t pkm = pk >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> pk);
-        const uint32_t wx = win(0, p0) & pkm, wy = win(1, p0) & pkm, wv = win(2, p0) & pkm;
-        uint32_t out = win(3, p0) & ~wv & pkm;                     // B: invariant bits
-        if (wx) out |= seg_bits(k, p0, wx, 0, gx);                 // A
-        if (wy) out |= seg_bits(k, p0, wy, 1, gy);
-        const uint32_t wc = wv & ~wx & ~wy;                        // C(b): variant, not compressed
-        if (wc) out |= (w8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk)) & wc;
+        uint32_t w[4];
+        pre(k, w);
+        return get(k, rid, d, pk, w);
+    }
+    __device__ __forceinline__ uint32_t get(uint64_t k, uint32_t rid, uint16_t d, uint32_t pk,
+                                            const uint32_t (&w)[4]) const {
+        const uint32_t p0 = d == CKS_NONE_INTERNAL ? 0u : min((uint32_t)d + 1, 8 * B);
+        const uint2 e0 = __ldg(reinterpret_cast<const uint2*>(ent + p0));
+        const uint2 e1 = __ldg(reinterpret_cast<const uint2*>(ent + p0) + 1);
+        const uint2 e2 = __ldg(reinterpret_cast<const uint2*>(ent + p0) + 2);
+        // e0 = (wx, wy), e1 = (ref bits, wc), e2 = (rank x, rank y) -- all within the pk bits
+        uint32_t out = e1.x;                                       // B: invariant bits
+        if (e0.x) out |= deposit(field(k, gx + e2.x, (uint32_t)__popc(e0.x), w), e0.x);   // A
+        if (e0.y) out |= deposit(field(k, gy + e2.y, (uint32_t)__popc(e0.y), w), e0.y);
+        if (e1.y) out |= (w8 ? pk_of8(keys, B, rid, d, pk) : pk_of(keys, B, rid, d, pk)) & e1.y;   // C(b)
         return out;
     }
 };
@@ -142,17 +147,18 @@ k_ptree_leaf_entries(const Src src, uint64_t n, uint32_t B, const uint32_t* __re
     constexpr int U = 4;                                          // keys in flight per thread
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < n; k0 += U * T) {
-        uint32_t rid[U], pkv[U];
+        uint32_t rid[U], pkv[U], pw[U][4];
         uint16_t d[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint64_t k = k0 + u * T;
             rid[u] = k < n ? perm[k] : 0u;
             d[u] = k < n ? dbit[k] : (uint16_t)CKS_NONE_INTERNAL;
+            if (k < n) src.pre(k, pw[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; u++)
-            pkv[u] = k0 + u * T < n ? src.get(k0 + u * T, rid[u], d[u], pk) : 0u;
+            pkv[u] = k0 + u * T < n ? src.get(k0 + u * T, rid[u], d[u], pk, pw[u]) : 0u;
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint64_t k = k0 + u * T;
@@ -271,7 +277,7 @@ cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint
                          uint16_t* rmin_b, int sms, cudaStream_t st, int* launches, const PtreeDs* ds) {
     const bool w8 = B % 8 == 0 && ((uintptr_t)keys & 7) == 0;
     if (ds) {
-        PkDs src{keys, B, w8, ds->planes, ds->pitch, ds->np, ds->gx, ds->gy, ds->tab};
+        PkDs src{keys, B, w8, ds->planes, ds->pitch, ds->np, ds->gx, ds->gy, ds->ent};
         return run_ptree(src, n, B, perm, dbit, pk, leaf_per, inner_per, level_nodes, level_offset, height, nodes,
                          rmin_a, rmin_b, sms, st, launches);
     }

@@ -537,15 +537,17 @@ def test_paper_tree_ds_sources_vs_oracle(cfg, n, pk, fill):
             cks.paper_tree_ds(None, N, B, perm, dbit, r["packed"], N, r["mask"], r["variant"], r["ref_key"], pk, fill)
 
 
+@pytest.mark.parametrize("src", [cks.PTREE_ROWS, cks.PTREE_DS, cks.PTREE_CARRY])
 @pytest.mark.parametrize("cfg,n,pk,fill,ds", [(5, 120_001, 32, 0.9, False), (5, 70_001, 17, 1.0, True),
                                               (3, 90_000, 32, 0.9, True), (4, 50_000, 32, 0.9, False),
                                               (1, None, 24, 0.9, False), (2, 40_000, 32, 0.9, True)])
-def test_build_fused_paper_tree(cfg, n, pk, fill, ds):
-    # cks_build with ptree_nodes: the paper-format tree from the same call. With P_M carried
-    # (cfg5) the variant bits outside the sort mask that partial keys need ride through the sort
-    # as one more plane (C(a)); the build's own outputs must not change
+def test_build_fused_paper_tree(cfg, n, pk, fill, ds, src):
+    # cks_build with ptree_nodes: the paper-format tree from the same call, from each of the
+    # paper's partial-key sources. With CARRY on cfg5 the variant bits outside the sort mask that
+    # partial keys need ride through the sort as one more plane (C(a)); the build's own outputs
+    # must not change
     keys = cksgen.config(cfg, n=n)
-    r = cks.build(dev(keys), paper_tree_pk=pk, paper_tree_fill=fill, ds_metadata=ds)
+    r = cks.build(dev(keys), paper_tree_pk=pk, paper_tree_fill=fill, ds_metadata=ds, paper_tree_source=src)
     check_build(keys, r)
     ref = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=pk, fill=fill)
     assert np.array_equal(r["paper_tree"].cpu().numpy(), ref["nodes"])
@@ -558,7 +560,7 @@ def test_fused_paper_tree_forced_round0(T):
     keys = cksgen.config(5, n=66_000)
     cks.set_round0_bits(T)
     try:
-        r = cks.build(dev(keys), paper_tree_pk=32)
+        r = cks.build(dev(keys), paper_tree_pk=32, paper_tree_source=cks.PTREE_CARRY)
     finally:
         cks.set_round0_bits(0)
     check_build(keys, r)
