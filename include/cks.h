@@ -211,6 +211,23 @@ int cks_rank_sorted(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t packed
 int cks_partition(cks_ctx* ctx, const uint32_t* packed, uint32_t packed_bits, uint64_t n, const uint32_t* splitters,
                   uint32_t parts, uint64_t rid_base, uint32_t* packed_out, uint32_t* rid_out, uint64_t* counts_out);
 
+/* The fused partition-and-send (NEXT-4): the partition of cks_partition with
+ * every part written straight into its receiver's buffer by the digit pass itself, instead of a
+ * local partition followed by an all-to-all.
+ * cks_partition_count: part of every element and the per-part counts (counts_out device
+ * u64[parts]); keeps the partition input in the context for the send. The caller all-gathers
+ * the counts (G x G), sizes the receive buffers and computes where its part starts in each.
+ * cks_partition_send: the one stable digit pass on the part index of the last count on this
+ * context; part d's planes go to dst_planes[d] + q * dst_pitch[d] (plane q, u32 elements from
+ * this sender's start in receiver d's buffer) and its global row ids (rid_base + i) to
+ * dst_rid[d]. dst_planes / dst_pitch / dst_rid are HOST arrays [parts] of DEVICE addresses:
+ * peer pointers when the receiver is another GPU (cudaIpc / P2P; NVLink stores), plain device
+ * pointers when it is on this one. Asynchronous; the receiver may read after the sender's
+ * stream completes (the caller's barrier). */
+int cks_partition_count(cks_ctx* ctx, const uint32_t* packed, uint32_t packed_bits, uint64_t n,
+                        const uint32_t* splitters, uint32_t parts, uint64_t rid_base, uint64_t* counts_out);
+int cks_partition_send(cks_ctx* ctx, uint32_t* const* dst_planes, const uint64_t* dst_pitch, uint32_t* const* dst_rid);
+
 /* cks_sort_prefix: the first build's sort (a4-a6, by distinguishing prefixes as cks_build,
  * SURVEY 8(f) NEXT-1) on GIVEN compressed keys instead of key rows: packed = P_M, device
  * u32[ceil(m/32)][n] right-aligned as cks_compress, input order; sort_mask = M (host

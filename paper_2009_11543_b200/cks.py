@@ -68,7 +68,7 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
            "cks_partition", "cks_sort_prefix", "cks_bulkload_block", "cks_bulkload_top",
            "cks_build_host_batch", "cks_ctx_set_round0_bits", "cks_ctx_set_verify",
-           "cks_ctx_path_bytes", "cks_paper_tree_ds"]
+           "cks_ctx_path_bytes", "cks_paper_tree_ds", "cks_partition_count", "cks_partition_send"]
 
 
 def load_library(path: str | None = None):
@@ -116,6 +116,8 @@ def load_library(path: str | None = None):
     L.cks_rank_sorted.argtypes = [p, p, u32, u64, p, u64, p, u32, p]
     L.cks_repack.argtypes = [p, p, p, p, u32, u64, p]
     L.cks_partition.argtypes = [p, p, u32, u64, p, u32, u64, p, p, p]
+    L.cks_partition_count.argtypes = [p, p, u32, u64, p, u32, u64, p]
+    L.cks_partition_send.argtypes = [p, p, p, p]
     L.cks_sort_prefix.argtypes = [p, p, p, u32, u64, p, p, p, ctypes.POINTER(u32), p]
     L.cks_bulkload_block.argtypes = [p, p, p, u64, u32, f64, i32, u32, ctypes.POINTER(Tree), p, ctypes.POINTER(u32)]
     L.cks_bulkload_top.argtypes = [p, p, p, u64, u32, f64, ctypes.POINTER(Tree), ctypes.POINTER(u32)]
@@ -358,6 +360,33 @@ def partition(packed: torch.Tensor, bits: int, splitters: torch.Tensor, parts: i
                                  _ptr(splitters) if splitters.numel() else None, parts, rid_base,
                                  _ptr(out) if out.numel() else None, _ptr(rid) if n else None, _ptr(counts)))
     return out, rid, counts
+
+
+def partition_count(packed: torch.Tensor, bits: int, splitters: torch.Tensor, parts: int, rid_base: int):
+    """int64[parts]: elements per part of the stable partition by parts-1 splitters (the first
+    half of the fused partition-and-send, cks_partition_count)."""
+    n = packed.shape[1]
+    if packed.dtype != torch.int32 or not packed.is_contiguous() or packed.shape[0] != nplanes(bits):
+        raise ValueError("packed must be contiguous int32 [ceil(bits/32), n]")
+    if splitters.dtype != torch.int32 or not splitters.is_contiguous() or splitters.shape[0] != parts - 1:
+        raise ValueError("splitters must be contiguous int32 [parts-1, ceil(bits/32)+1]")
+    L, c = _context(packed.device.index)
+    counts = torch.empty(parts, dtype=torch.int64, device=packed.device)
+    _check(L, c, L.cks_partition_count(c, _ptr(packed) if packed.numel() else None, bits, n,
+                                       _ptr(splitters) if splitters.numel() else None, parts, rid_base,
+                                       _ptr(counts)))
+    return counts
+
+
+def partition_send(dst_planes: list, dst_pitch: list, dst_rid: list, device: int | None = None):
+    """Second half (cks_partition_send): write every part of the last partition_count on this
+    thread's context straight into its receiver's buffers (device addresses, element units:
+    dst_planes[d] + q * dst_pitch[d] is plane q of part d's destination)."""
+    L, c = _context(device)
+    k = len(dst_rid)
+    P = ctypes.c_void_p * k
+    pit = (ctypes.c_uint64 * k)(*[int(x) for x in dst_pitch])
+    _check(L, c, L.cks_partition_send(c, P(*dst_planes), pit, P(*dst_rid)))
 
 
 def sort_prefix(packed: torch.Tensor, sort_mask, want_packed: bool = False):

@@ -56,6 +56,7 @@ struct cks_ctx {
         anyt,                                                              // k_ref_reg: compaction tiles with ties left
         vbad,                                                              // k_verify_order result
         ptab,                                                              // cks_paper_tree_ds tables
+        part_ptrs,                                                         // cks_partition_send pointer table
         keys2, perm2;                                                      // cks_build_host_batch: 2nd buffers
     // pinned host staging
     GatherPlan* h_plan[3] = {};       // 0: compress, 1: repack, 2: partial-key bits (P_E)
@@ -71,6 +72,8 @@ struct cks_ctx {
     bool pt_on = false;
     uint32_t pt_npe = 0;              // planes actually appended by the last build_refine
     PtreeEnt* h_ptab = nullptr;       // pinned staging of the paper tree's per-window table
+    uint64_t ps_n = 0, ps_rid_base = 0; // cks_partition_count -> cks_partition_send state
+    uint32_t ps_np = 0, ps_parts = 0;
     cudaEvent_t ptab_ev = nullptr;
     bool skip_packed = false;         // cks_sort_prefix without packed_out: no a7
 };
@@ -159,7 +162,7 @@ T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
      &c->total, &c->pm, &c->pd, &c->cmp, &c->crid, &c->crid2, &c->posA, &c->posB, &c->posC, &c->segA, &c->segB,   \
      &c->segC, &c->runoff, &c->runpos, &c->runoff2, &c->runpos2, &c->tie, &c->keep, &c->done, &c->mlist,         \
      &c->wlist, &c->rcnt, &c->rtot, &c->part_in, &c->part_out, &c->anyt, &c->vbad, &c->keys2, &c->perm2,     \
-     &c->ptab}
+     &c->ptab, &c->part_ptrs}
 
 // checked build: the canary band after every scratch buffer must be intact after a call
 // (synchronises); no-op otherwise
@@ -426,8 +429,14 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     const uint32_t nwords = (8 * B + 31) / 32;
     // a3: P_M left-aligned (the first mask position is bit 31 of the top plane), so chunk r
     // is planes np-1-2r (high word) and np-2-2r (low word)
-    TRY(ensure(ctx, ctx->pm, (size_t)np * sp * 4));
-    uint32_t* pm = as<uint32_t>(ctx->pm);
+    // given P_M that is already left-aligned with the scratch pitch (m a multiple of 32, n of 32;
+    // e.g. the sharded path's received planes): sorted from where it is, read only
+    const bool pm_given = planes_in && lead == 0 && sp == n && ((uintptr_t)planes_in & 15) == 0;
+    uint32_t* pm = pm_given ? const_cast<uint32_t*>(planes_in) : nullptr;
+    if (!pm_given) {
+        TRY(ensure(ctx, ctx->pm, (size_t)np * sp * 4));
+        pm = as<uint32_t>(ctx->pm);
+    }
     // a2 + a3, and the width T of round 0: 8 bits more than the narrowest multiple of 8 bits
     // that separates a strided sample of the keys as well as the full 64-bit chunk does (fewer
     // round-0 passes; whatever still ties is finished by the later rounds -- the result is
@@ -445,7 +454,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     TRY(ensure(ctx, ctx->rtot, 64));
     uint32_t* scnt = as<uint32_t>(ctx->rtot) + 4;
     if (planes_in) {                                             // given P_M: left-align it, then sample
-        LAUNCH(launch_align_left(planes_in, n, np, n, lead, pm, sp, ctx->sms, ctx->stream));
+        if (!pm_given) LAUNCH(launch_align_left(planes_in, n, np, n, lead, pm, sp, ctx->sms, ctx->stream));
         if (sample) {
             CK(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
             CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_ev[0], 0));
@@ -669,6 +678,10 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     if (out->popcount > 0 && !ctx->skip_packed) {
         if (!carry) TRY(ensure(ctx, ctx->pd, (size_t)npd * sp * 4));
         uint32_t* pd = carry ? pm : as<uint32_t>(ctx->pd);       // (P_M in row order is no longer needed)
+        if (carry && pm_given) {                                  // (the caller's planes are read only)
+            TRY(ensure(ctx, ctx->pm, (size_t)np * sp * 4));
+            pd = as<uint32_t>(ctx->pm);
+        }
         const bool single = T >= m;                               // round 0 sorted all of P_M
         if ((single || carry) && lead == 0 && same_mask(out->mask, M, B)) {
             out->packed = sorted0 + (uint64_t)npe * sp0;           // (P_M's planes above the appended P_E)
@@ -1307,6 +1320,92 @@ int cks_partition(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t 
     TRY(run_sort(ctx, in, sp, np + 1, 1, n, nullptr, 0, out, sp, rid_out, nullptr, nullptr, 0, false));
     if (np) CK(cudaMemcpy2DAsync(packed_out, n * 4, out + sp, sp * 4, n * 4, np, cudaMemcpyDeviceToDevice, ctx->stream));
     LAUNCH(launch_add_base(rid_out, n, (uint32_t)rid_base, ctx->sms, ctx->stream));
+    return check_guards(ctx);
+}
+
+int cks_partition_count(cks_ctx* ctx, const uint32_t* packed, uint32_t bits, uint64_t n, const uint32_t* splitters,
+                        uint32_t parts, uint64_t rid_base, uint64_t* counts_out) {
+    if (!ctx) return CKS_EINVAL;
+    if (bits > kMaxBits) return fail(ctx, CKS_EINVAL, "packed_bits %u > %u", bits, kMaxBits);
+    if (parts < 1 || parts > 256) return fail(ctx, CKS_EINVAL, "parts %u not in [1, 256]", parts);
+    if (n >= (1ull << 32) || rid_base + n > (1ull << 32)) return fail(ctx, CKS_ERANGE, "row ids exceed u32");
+    if (!counts_out || (parts > 1 && !splitters) || (n && bits && !packed))
+        return fail(ctx, CKS_EINVAL, "NULL splitters, counts_out or packed");
+    CK(cudaSetDevice(ctx->device));
+    const uint32_t np = (bits + 31) / 32;
+    const uint64_t sp = scratch_pitch(n);
+    TRY(ensure(ctx, ctx->part_in, (size_t)(np + 1) * sp * 4));
+    uint32_t* in = as<uint32_t>(ctx->part_in);
+    CK(cudaMemsetAsync(counts_out, 0, (size_t)parts * 8, ctx->stream));
+    if (n) {
+        if (parts > 1) {
+            LAUNCH(launch_part_dest(packed, np, n, n, splitters, parts - 1, rid_base, in,
+                                    reinterpret_cast<unsigned long long*>(counts_out), ctx->sms, ctx->stream));
+        } else {
+            CK(cudaMemsetAsync(in, 0, n * 4, ctx->stream));
+            const unsigned long long cnt = n;
+            CK(cudaMemcpyAsync(counts_out, &cnt, 8, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));                   // (&cnt is on the stack)
+        }
+        if (np) CK(cudaMemcpy2DAsync(in + sp, sp * 4, packed, n * 4, n * 4, np, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    ctx->ps_n = n;
+    ctx->ps_np = np;
+    ctx->ps_parts = parts;
+    ctx->ps_rid_base = rid_base;
+    return check_guards(ctx);
+}
+
+int cks_partition_send(cks_ctx* ctx, uint32_t* const* dst_planes, const uint64_t* dst_pitch, uint32_t* const* dst_rid) {
+    if (!ctx) return CKS_EINVAL;
+    const uint32_t parts = ctx->ps_parts, np = ctx->ps_np;
+    const uint64_t n = ctx->ps_n;
+    if (parts == 0) return fail(ctx, CKS_EINVAL, "cks_partition_send without cks_partition_count");
+    if (!dst_rid || (np && (!dst_planes || !dst_pitch))) return fail(ctx, CKS_EINVAL, "NULL destination tables");
+    CK(cudaSetDevice(ctx->device));
+    ctx->ps_parts = 0;
+    if (n == 0) return CKS_OK;
+    // pointer table: stream k = 1..np is plane k-1, stream np+1 the row id; 256 parts per stream
+    const size_t ptab = (size_t)(np + 1) * 256;
+    TRY(ensure(ctx, ctx->part_ptrs, ptab * sizeof(uint32_t*) + 256 * 4 + 16));
+    std::vector<uint32_t*> h(ptab, nullptr);
+    for (uint32_t d = 0; d < parts; d++) {
+        for (uint32_t q = 0; q < np; q++) h[(size_t)q * 256 + d] = dst_planes[d] + q * dst_pitch[d];
+        h[(size_t)np * 256 + d] = dst_rid[d];
+    }
+    CK(cudaMemcpyAsync(ctx->part_ptrs.p, h.data(), ptab * sizeof(uint32_t*), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));                       // (h is on the stack)
+    const uint64_t sp = scratch_pitch(n);
+    uint64_t lsd_tiles = 0, lsd_chunks = 0;
+    lsd_sizes(n, &lsd_tiles, &lsd_chunks);
+    TRY(ensure(ctx, ctx->tile_off, (size_t)lsd_tiles * 256 * 4));
+    TRY(ensure(ctx, ctx->chunk_tot, (size_t)lsd_chunks * 256 * 4));
+    TRY(ensure(ctx, ctx->total, 256 * 4, /*zero=*/true));
+    LsdPassArgs la;
+    memset(&la, 0, sizeof(la));
+    la.in_planes = as<uint32_t>(ctx->part_in);
+    la.out_planes = as<uint32_t>(ctx->part_in);                  // (not written: every stream is scattered)
+    la.out_rid = as<uint32_t>(ctx->part_in);
+    la.n = n;
+    la.in_pitch = sp;
+    la.out_pitch = sp;
+    la.nplanes = np + 1;
+    la.digit_plane = 0;
+    la.shift = 0;
+    la.tile_off = as<uint32_t>(ctx->tile_off);
+    la.chunk_tot = as<uint32_t>(ctx->chunk_tot);
+    la.total = as<uint32_t>(ctx->total);
+    la.rid_add = (uint32_t)ctx->ps_rid_base;
+    la.part_dst = as<uint32_t* const>(ctx->part_ptrs);
+    la.bbase = reinterpret_cast<uint32_t*>(as<uint8_t>(ctx->part_ptrs) + ptab * sizeof(uint32_t*));
+    LsdAux aux;
+    aux.stream = ctx->aux_stream;
+    aux.fork = ctx->aux_ev[0];
+    aux.join = ctx->aux_ev[1];
+    int nl = 0;
+    CK(launch_lsd_pass(la, ctx->sms, ctx->stream, aux, &nl));
+    ctx->launches += (uint64_t)nl;
+    BYTES((double)n * 4.0 * (1 + (np + 1) + (np + 1)));
     return check_guards(ctx);
 }
 

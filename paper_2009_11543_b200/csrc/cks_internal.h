@@ -114,6 +114,11 @@ struct LsdPassArgs {
     uint32_t tma;                // set by the launcher
     uint32_t tile_begin;         // first tile this launch covers (set by the launcher)
     uint32_t debug;              // timing experiments only (CKS_LSD_DEBUG); results are wrong when set
+    uint32_t rid_add;            // added to implicit row ids as they are written
+    // scatter-to-parts (fused partition-and-send, k_lsd.cu SCATTER): stream k >= 1 of an element
+    // of part d is written to part_dst[(k-1)*256 + d][its position - bbase[d]]; NULL = off
+    uint32_t* const* part_dst;
+    uint32_t* bbase;             // u32[256] bucket bases, written by the chunk scan when non-NULL
 };
 // optional side stream for the partial last tile (runs concurrently with the full tiles)
 struct LsdAux {

@@ -180,6 +180,7 @@ k_chunk_scan(const LsdPassArgs a, uint32_t nchunks) {
             if (lane >= o) x += y;
         }
         s_base[lane] = run + x - a.total[d];
+        if (a.bbase) a.bbase[d] = s_base[lane];              // (scatter-to-parts passes)
     }
     const uint32_t per = (nchunks + 31) / 32;
     const uint32_t c0 = warp * per, c1 = min(c0 + per, nchunks);
@@ -224,7 +225,15 @@ __device__ __forceinline__ uint32_t match_bits(uint32_t d) {
     return peers;
 }
 
-template <int ITEMS>
+// SCATTER (the fused partition-and-send of the sharded path): stream 0 (the part index) is not
+// written, and every other stream k of an element of part d goes to
+// part_dst[(k-1)*256 + d][position - bucket base of d] -- each part straight into its receiver's
+// buffer (a peer device pointer over NVLink when the receiver is another GPU).
+__device__ __forceinline__ uint32_t* part_out(const LsdPassArgs& a, int k, uint32_t d, uint32_t pos) {
+    return a.part_dst[(uint32_t)(k - 1) * 256u + d] + (pos - a.bbase[d]);
+}
+
+template <int ITEMS, bool SCATTER>
 __global__ void __launch_bounds__(kSortThreads, ITEMS == 8 ? 3 : 2)
 k_downsweep(const LsdPassArgs a) {
     constexpr int TILE = kSortThreads * ITEMS;
@@ -358,7 +367,7 @@ k_downsweep(const LsdPassArgs a) {
         for (int i = 0; i < ITEMS; i++)
             if (FULL || dg[i] < 0x100u) s_src[pos[i] + h[dg[i]]] = (uint16_t)((wofs + i * 32 + lane) * 4);
         __syncthreads();
-        uint32_t from[ITEMS], dest[ITEMS];
+        uint32_t from[ITEMS], dest[ITEMS], dd[ITEMS];
         // ---- stream 0 (the digit word): gather in digit order; the gathered word's digit
         // gives the slot's global destination (consecutive slots share digits: no conflicts)
         {
@@ -370,9 +379,10 @@ k_downsweep(const LsdPassArgs a) {
                 if (FULL || s < tile_n) {
                     from[r] = s_src[s];
                     const uint32_t w = *reinterpret_cast<const uint32_t*>(slot + from[r]);
-                    dest[r] = s + s_gb[digit_of(w, sel)];
+                    dd[r] = digit_of(w, sel);
+                    dest[r] = s + s_gb[dd[r]];
                     CKS_DCHECK(dest[r] < n);
-                    out[dest[r]] = w;
+                    if (!SCATTER) out[dest[r]] = w;
                 }
             }
             __syncthreads();
@@ -382,17 +392,22 @@ k_downsweep(const LsdPassArgs a) {
         for (int k = 1; k < S; k++) {
             uint32_t* out = dst_of(k);
             if (k == S - 1 && implicit_rid) {
-                const uint32_t b32 = (uint32_t)base;
+                const uint32_t b32 = (uint32_t)base + a.rid_add;
 #pragma unroll
                 for (int r = 0; r < ITEMS; r++)
-                    if (FULL || r * kSortThreads + tid < tile_n) out[dest[r]] = b32 + (from[r] >> 2);
+                    if (FULL || r * kSortThreads + tid < tile_n) {
+                        uint32_t* o = SCATTER ? part_out(a, k, dd[r], dest[r]) : out + dest[r];
+                        *o = b32 + (from[r] >> 2);
+                    }
                 continue;
             }
             const uint8_t* slot = reinterpret_cast<const uint8_t*>(acquire(k));
 #pragma unroll
             for (int r = 0; r < ITEMS; r++)
-                if (FULL || r * kSortThreads + tid < tile_n)
-                    out[dest[r]] = *reinterpret_cast<const uint32_t*>(slot + from[r]);
+                if (FULL || r * kSortThreads + tid < tile_n) {
+                    uint32_t* o = SCATTER ? part_out(a, k, dd[r], dest[r]) : out + dest[r];
+                    *o = *reinterpret_cast<const uint32_t*>(slot + from[r]);
+                }
             __syncthreads();
             release();
         }
@@ -465,7 +480,7 @@ __device__ __forceinline__ uint32_t scan_rankers(uint32_t v, uint32_t* s_warp, u
     return r;
 }
 
-template <class SH>
+template <class SH, bool SCATTER>
 __global__ void __launch_bounds__(SH::THREADS, SH::MINB)
 k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
     constexpr int TILE = SH::TILE, kRW = SH::RW, kWW = SH::WW, kRT = SH::RT, WI = SH::WI;
@@ -627,6 +642,7 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
         bar_wait(&s_ranked[buf], (j >> 1) & 1u);
         const uint16_t* src = s_src + buf * TILE;
         uint32_t from[WI], dest[WI];
+        uint8_t dd[SCATTER ? WI : 1];                           // SCATTER: the slot's part
 #pragma unroll
         for (int r = 0; r < WI; r++) from[r] = src[r * SH::WT + wt];
         {
@@ -637,10 +653,16 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
 #pragma unroll
             for (int r = 0; r < WI; r++) {
                 const uint32_t w = *reinterpret_cast<const uint32_t*>(sl + from[r]);
+                const uint32_t dg = digit_of(w, sel);
                 dest[r] = (kLsdDebug && (a.debug & 1)) ? tile * (uint32_t)TILE + r * SH::WT + wt
-                                                       : r * SH::WT + wt + s_gb[buf][digit_of(w, sel)];
+                                                       : r * SH::WT + wt + s_gb[buf][dg];
                 CKS_DCHECK(dest[r] < a.n);
-                out[dest[r]] = w;
+                if (SCATTER) {
+                    dd[r] = (uint8_t)dg;
+                    dest[r] -= a.bbase[dg];                      // position inside the part
+                } else {
+                    out[dest[r]] = w;
+                }
             }
             __syncwarp();
             if (lane == 0) { bar_arrive(&s_written[buf]); bar_arrive(&s_empty[slot]); }
@@ -648,9 +670,13 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
         for (int k = 1; k < S; k++) {
             uint32_t* out = dst_of(k);
             if (k == S - 1 && implicit_rid) {
-                const uint32_t b32 = tile * (uint32_t)TILE;
+                const uint32_t b32 = tile * (uint32_t)TILE + a.rid_add;
 #pragma unroll
-                for (int r = 0; r < WI; r++) out[dest[r]] = b32 + (from[r] >> 2);
+                for (int r = 0; r < WI; r++) {
+                    uint32_t* o = SCATTER ? a.part_dst[(uint32_t)(k - 1) * 256u + dd[SCATTER ? r : 0]] + dest[r]
+                                          : out + dest[r];
+                    *o = b32 + (from[r] >> 2);
+                }
                 continue;
             }
             const uint32_t slot = kDigitSlots + y % R;
@@ -658,7 +684,11 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
             y++;
             const uint8_t* sl = reinterpret_cast<const uint8_t*>(ring + (size_t)slot * TILE);
 #pragma unroll
-            for (int r = 0; r < WI; r++) out[dest[r]] = *reinterpret_cast<const uint32_t*>(sl + from[r]);
+            for (int r = 0; r < WI; r++) {
+                uint32_t* o = SCATTER ? a.part_dst[(uint32_t)(k - 1) * 256u + dd[SCATTER ? r : 0]] + dest[r]
+                                      : out + dest[r];
+                *o = *reinterpret_cast<const uint32_t*>(sl + from[r]);
+            }
             __syncwarp();
             if (lane == 0) bar_arrive(&s_empty[slot]);
         }
@@ -698,7 +728,7 @@ static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
     cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
-template <int ITEMS>
+template <int ITEMS, bool SCATTER>
 static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAux& aux, int* launches) {
     constexpr int TILE = kSortThreads * ITEMS;
     const uint64_t tiles = (a.n + TILE - 1) / TILE;
@@ -723,7 +753,7 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
         LsdPassArgs w = a;
         w.slots = (uint32_t)R;
         const size_t smem = (size_t)(kDigitSlots + R) * TILE * 4 + fixed;
-        raise_smem_limit((const void*)k_downsweep_ws<SH>, smem);
+        raise_smem_limit((const void*)k_downsweep_ws<SH, SCATTER>, smem);
         const uint64_t gmax = (uint64_t)sms * SH::MINB;
         const uint64_t grid = nfull < gmax ? nfull : gmax;
         const bool tail = nfull != tiles;
@@ -734,15 +764,15 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
             tl.tile_begin = (uint32_t)nfull;
             if ((int)tl.slots > 2 * streams) tl.slots = streams > 0 ? 2 * streams : 1;
             const size_t tsm = (size_t)tl.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 2;
-            raise_smem_limit((const void*)k_downsweep<ITEMS>, tsm);
+            raise_smem_limit((const void*)k_downsweep<ITEMS, SCATTER>, tsm);
             cudaEventRecord(aux.fork, st);
             cudaStreamWaitEvent(aux.stream, aux.fork, 0);
-            k_downsweep<ITEMS><<<1, kSortThreads, tsm, aux.stream>>>(tl);
+            k_downsweep<ITEMS, SCATTER><<<1, kSortThreads, tsm, aux.stream>>>(tl);
             cudaEventRecord(aux.join, aux.stream);
             nl++;
         }
         if (aux.ws_begin) cudaEventRecord(aux.ws_begin, st);
-        launch_pdl(k_downsweep_ws<SH>, dim3((unsigned)grid), dim3(SH::THREADS), smem, st, w, (uint32_t)nfull);
+        launch_pdl(k_downsweep_ws<SH, SCATTER>, dim3((unsigned)grid), dim3(SH::THREADS), smem, st, w, (uint32_t)nfull);
         if (aux.ws_end) cudaEventRecord(aux.ws_end, st);
         // algorithmic bytes: every loaded stream read once, every stream written once
         if (aux.ws_bytes) *aux.ws_bytes = (double)nfull * TILE * 4.0 * (double)(streams + (int)a.nplanes + 1);
@@ -753,13 +783,13 @@ static cudaError_t lsd_pass(LsdPassArgs a, int sms, cudaStream_t st, const LsdAu
     }
     if ((int)a.slots > 2 * streams) a.slots = streams > 0 ? 2 * streams : 1;
     size_t smem = (size_t)a.slots * TILE * 4 + kW * (kRadix + 8) * 4 + (size_t)TILE * 2;
-    raise_smem_limit((const void*)k_downsweep<ITEMS>, smem);
+    raise_smem_limit((const void*)k_downsweep<ITEMS, SCATTER>, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_downsweep<ITEMS>, kSortThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_downsweep<ITEMS, SCATTER>, kSortThreads, smem);
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)sms * per_sm;
     if (grid > tiles - a.tile_begin) grid = tiles - a.tile_begin;
-    k_downsweep<ITEMS><<<(unsigned)grid, kSortThreads, smem, st>>>(a);
+    k_downsweep<ITEMS, SCATTER><<<(unsigned)grid, kSortThreads, smem, st>>>(a);
     nl++;
     *launches = nl;
     return cudaGetLastError();
@@ -775,7 +805,13 @@ cudaError_t launch_lsd_pass(const LsdPassArgs& args, int sms, cudaStream_t st, c
     a.debug = (uint32_t)kn.lsd_debug;
     a.tma = ((uintptr_t)a.in_planes % 16 == 0) && (a.in_pitch % 4 == 0) &&
             (a.in_rid == nullptr || (uintptr_t)a.in_rid % 16 == 0);
-    return kn.lsd_items == 8 ? lsd_pass<8>(a, sms, st, aux, launches) : lsd_pass<16>(a, sms, st, aux, launches);
+    if (a.part_dst) {
+        if (a.in_rid || a.digit_plane != 0) return cudaErrorInvalidValue;   // (the partition pass only)
+        return kn.lsd_items == 8 ? lsd_pass<8, true>(a, sms, st, aux, launches)
+                                 : lsd_pass<16, true>(a, sms, st, aux, launches);
+    }
+    return kn.lsd_items == 8 ? lsd_pass<8, false>(a, sms, st, aux, launches)
+                             : lsd_pass<16, false>(a, sms, st, aux, launches);
 }
 
 }  // namespace cks

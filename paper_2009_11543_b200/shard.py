@@ -40,7 +40,9 @@ NONE = 0xFFFF
 
 class TorchComm:
     """Collectives over a torch.distributed process group (NCCL: CUDA tensors; gloo: the
-    tensors are staged through host memory)."""
+    tensors are staged through host memory). No peer pointers: the exchange is an NCCL
+    all-to-all (the baseline of DESIGN.md Sec. 7)."""
+    peer_access = False
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -59,15 +61,17 @@ class TorchComm:
         self.dist.all_gather(out, x, group=self.group)
         return [o.to(t.device) for o in out]
 
-    def alltoallv(self, t: torch.Tensor, send_counts: list[int]) -> torch.Tensor:
+    def alltoallv(self, t: torch.Tensor, send_counts: list[int], recv_counts: list[int] | None = None) -> torch.Tensor:
         """Rows [sum(send_counts[:d]), +send_counts[d]) of t go to rank d; returns the rows
-        received, source rank order."""
+        received, source rank order. recv_counts (known from the all-gathered count matrix)
+        saves the count exchange."""
         x = self._dev(t.contiguous())
-        sc = torch.tensor(send_counts, dtype=torch.int64)
-        rc = torch.empty_like(sc)
-        sc_d, rc_d = (sc, rc) if self.cpu else (sc.to(t.device), rc.to(t.device))
-        self.dist.all_to_all_single(rc_d, sc_d, group=self.group)
-        recv_counts = [int(v) for v in rc_d.tolist()]
+        if recv_counts is None:
+            sc = torch.tensor(send_counts, dtype=torch.int64)
+            rc = torch.empty_like(sc)
+            sc_d, rc_d = (sc, rc) if self.cpu else (sc.to(t.device), rc.to(t.device))
+            self.dist.all_to_all_single(rc_d, sc_d, group=self.group)
+            recv_counts = [int(v) for v in rc_d.tolist()]
         out = torch.empty((sum(recv_counts),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         self.dist.all_to_all_single(out, x, recv_counts, send_counts, group=self.group)
         return out.to(t.device)
@@ -83,6 +87,8 @@ class ThreadComm:
             self.size = size
             self.barrier = threading.Barrier(size)
             self.slots = [None] * size
+
+    peer_access = True                   # all ranks on one device: a rank may write another's buffers
 
     def __init__(self, shared, rank):
         self.sh, self.rank, self.size = shared, rank, shared.size
@@ -104,7 +110,16 @@ class ThreadComm:
         self.sh.barrier.wait()
         return out
 
-    def alltoallv(self, t: torch.Tensor, send_counts: list[int]) -> torch.Tensor:
+    def allgather_obj(self, obj) -> list:
+        self._publish(obj)
+        out = list(self.sh.slots)
+        self.sh.barrier.wait()
+        return out
+
+    def barrier(self):
+        self.allgather_obj(None)
+
+    def alltoallv(self, t: torch.Tensor, send_counts: list[int], recv_counts: list[int] | None = None) -> torch.Tensor:
         self._publish(list(torch.split(t.contiguous(), send_counts, dim=0)))
         out = torch.cat([self.sh.slots[s][self.rank] for s in range(self.size)], dim=0).clone()
         self.sh.barrier.wait()
@@ -148,6 +163,8 @@ class CudaOps:
     occupancy_mask = staticmethod(cks.occupancy_mask)
     compress = staticmethod(cks.compress)
     partition = staticmethod(cks.partition)
+    partition_count = staticmethod(cks.partition_count)
+    partition_send = staticmethod(cks.partition_send)
     repack = staticmethod(cks.repack)
     sort_prefix = staticmethod(cks.sort_prefix)
 
@@ -258,8 +275,34 @@ def _as_i32(x: np.ndarray) -> np.ndarray:
 
 # ---- the sharded first build -------------------------------------------------------------------
 
+def _exchange_fused(comm, ops, P, m, q, off, npl, dev):
+    """The fused partition-and-send: the count pass, one all-gather of the
+    G x G count matrix, receive buffers sized from its column, their addresses published, and
+    ONE digit pass that writes every part straight into its receiver's buffer (peer device
+    memory), then a barrier. Returns (received P planes, received row ids, send counts)."""
+    G, r = comm.size, comm.rank
+    n = int(P.shape[1])
+    pc = ops.partition_count(P, m, q, G, off)
+    cm = torch.stack(comm.allgather(pc)).cpu().numpy()          # cm[s][d]: elements s sends to d
+    nr = int(cm[:, r].sum())
+    R = torch.empty((npl, nr), dtype=torch.int32, device=dev)
+    rids = torch.empty(nr, dtype=torch.int32, device=dev)
+    peers = comm.allgather_obj((R.data_ptr(), rids.data_ptr(), nr))
+    dst_planes, dst_pitch, dst_rid = [], [], []
+    for d in range(G):
+        pr, rr, pitch = peers[d]
+        at = int(cm[:r, d].sum())                                # this sender's start at receiver d
+        dst_planes.append(pr + 4 * at if npl else 0)
+        dst_pitch.append(pitch)
+        dst_rid.append(rr + 4 * at)
+    ops.partition_send(dst_planes, dst_pitch, dst_rid, dev.index)
+    comm.barrier()                                               # every sender's stream has completed
+    return R, rids, [int(v) for v in cm[r]]
+
+
 def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int = 256, fanout: int = 64,
-                  fill: float = 1.0, tree: bool = True, superset_kind: int = cks.SUPERSET_BYTEOCC) -> dict:
+                  fill: float = 1.0, tree: bool = True, superset_kind: int = cks.SUPERSET_BYTEOCC,
+                  fused: bool | None = None) -> dict:
     """This rank's slice of the global first build. Returns dict(mask = exact D (same on all
     ranks), popcount, sort_mask = D+, sort_bits, perm = global row ids of the slice in order,
     dbit = D_i of the slice (against the global predecessor), packed = P_D of the slice,
@@ -267,7 +310,7 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
     G, r = comm.size, comm.rank
     dev = keys.device
     n, B = int(keys.shape[0]), int(keys.shape[1])
-    ns = [int(t.item()) for t in comm.allgather(torch.tensor([n], dtype=torch.int64, device=dev))]
+    ns = [n] if G == 1 else [int(t.item()) for t in comm.allgather(torch.tensor([n], dtype=torch.int64, device=dev))]
     off, N = sum(ns[:r]), sum(ns)
     if N >= 1 << 32:
         raise ValueError("n_total >= 2^32 (u32 row ids)")
@@ -280,68 +323,89 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
 
     # a1: D+ of the whole column from the union of the shard occupancies
     occ = ops.occupancy(keys)
-    M = ops.occupancy_mask(torch.stack(comm.allgather(occ)), N, superset_kind)
+    M = ops.occupancy_mask(occ[None] if G == 1 else torch.stack(comm.allgather(occ)), N, superset_kind)
     m = cks.popcount(M)
     npl = cks.nplanes(m)
 
     # a3
     P = ops.compress(keys, M)
 
-    # splitters from a regular sample of every shard
-    pos = torch.from_numpy(regular_sample(n, samples_per_rank)).to(dev)
-    samp = torch.zeros((samples_per_rank, npl + 1), dtype=torch.int32, device=dev)
-    if pos.numel():
-        samp[:pos.numel(), :npl] = P[:, pos].t()
-        samp[:pos.numel(), npl] = (pos + off).to(torch.int32)
-    cnt = torch.tensor([pos.numel()], dtype=torch.int64, device=dev)
-    counts = [int(c.item()) for c in comm.allgather(cnt)]
-    rows = [t[:c].cpu().numpy().view(np.uint32) for t, c in zip(comm.allgather(samp), counts)]
-    spl = pick_splitters(np.concatenate(rows) if rows else np.zeros((0, npl + 1), np.uint32), G)
-    q = torch.from_numpy(_as_i32(spl)).to(dev).reshape(-1, npl + 1)
+    # splitters from a regular sample of every shard (none with one shard)
+    q = None
+    if G > 1:
+        pos = torch.from_numpy(regular_sample(n, samples_per_rank)).to(dev)
+        samp = torch.zeros((samples_per_rank, npl + 1), dtype=torch.int32, device=dev)
+        if pos.numel():
+            samp[:pos.numel(), :npl] = P[:, pos].t()
+            samp[:pos.numel(), npl] = (pos + off).to(torch.int32)
+        cnt = torch.tensor([pos.numel()], dtype=torch.int64, device=dev)
+        counts = [int(c.item()) for c in comm.allgather(cnt)]
+        rows = [t[:c].cpu().numpy().view(np.uint32) for t, c in zip(comm.allgather(samp), counts)]
+        spl = pick_splitters(np.concatenate(rows) if rows else np.zeros((0, npl + 1), np.uint32), G)
+        q = torch.from_numpy(_as_i32(spl)).to(dev).reshape(-1, npl + 1)
 
     # a5: stable partition, the one exchange, one stable sort on P
-    Pp, ridp, pc = ops.partition(P, m, q, G, off)
-    send_counts = [int(v) for v in pc.cpu().tolist()]
-    rids = comm.alltoallv(ridp, send_counts)                     # per plane: no transposes
-    R = torch.stack([comm.alltoallv(Pp[q], send_counts) for q in range(npl)]) if npl else \
-        torch.zeros((0, rids.shape[0]), dtype=torch.int32, device=dev)
-    nr = int(rids.shape[0])
+    if fused is None:
+        fused = getattr(comm, "peer_access", False) and hasattr(ops, "partition_count")
+    if G == 1:                                                   # one part: the input order
+        R, send_counts, rids = P, [n], None
+    elif fused:
+        R, rids, send_counts = _exchange_fused(comm, ops, P, m, q, off, npl, dev)
+    else:
+        Pp, ridp, pc = ops.partition(P, m, q, G, off)
+        # the G x G count matrix in one collective: send counts (row r) and receive counts
+        # (column r) without a second exchange
+        cm = torch.stack(comm.allgather(pc)).cpu().numpy()
+        send_counts = [int(v) for v in cm[r]]
+        recv_counts = [int(v) for v in cm[:, r]]
+        rids = comm.alltoallv(ridp, send_counts, recv_counts)    # per plane: no transposes
+        R = torch.stack([comm.alltoallv(Pp[q], send_counts, recv_counts) for q in range(npl)]) if npl else \
+            torch.zeros((0, rids.shape[0]), dtype=torch.int32, device=dev)
+    nr = int(R.shape[1]) if rids is None else int(rids.shape[0])
     # sort by distinguishing prefixes (stable: the received order is the row-id order), D_i
     order, dbit, Dl, PDl = ops.sort_prefix(R, M, want_packed=True)
-    ol = order.long()
-    perm = rids[ol] if nr else rids                               # global row ids in (P, row id) order
+    if rids is None:                                             # one rank: row id = off + index
+        perm = order + off if off else order
+        ol = None
+    else:
+        ol = order.long()
+        perm = rids[ol] if nr else rids                           # global row ids in (P, row id) order
 
     # a6 across the slice boundary: the previous non-empty slice's last key vs this first key
-    last = torch.zeros(npl + 1, dtype=torch.int32, device=dev)
-    if nr:
-        last[0] = 1
-        last[1:] = R[:, ol[nr - 1]]
-    lasts = comm.allgather(last)
-    prev = next((lasts[k][1:] for k in range(r - 1, -1, -1) if int(lasts[k][0].item())), None)
-    Dl0, Db = Dl, None
-    if prev is not None and nr:
-        pair = torch.stack([prev, R[:, ol[0]]], dim=1).contiguous()
-        Db, db = ops.adjacent(pair, m, M)
-        dbit[0] = db[1]
-        Dl = Dl | Db
-    D = np.bitwise_or.reduce(np.stack([t.cpu().numpy() for t in comm.allgather(
-        torch.from_numpy(np.ascontiguousarray(Dl)).to(dev))]), axis=0).astype(np.uint8)
+    Dl0 = Dl
+    if G > 1:
+        last = torch.zeros(npl + 1, dtype=torch.int32, device=dev)
+        if nr:
+            last[0] = 1
+            last[1:] = R[:, ol[nr - 1]]
+        lasts = comm.allgather(last)
+        prev = next((lasts[k][1:] for k in range(r - 1, -1, -1) if int(lasts[k][0].item())), None)
+        if prev is not None and nr:
+            pair = torch.stack([prev, R[:, ol[0]]], dim=1).contiguous()
+            Db, db = ops.adjacent(pair, m, M)
+            dbit[0] = db[1]
+            Dl = Dl | Db
+        D = np.bitwise_or.reduce(np.stack([t.cpu().numpy() for t in comm.allgather(
+            torch.from_numpy(np.ascontiguousarray(Dl)).to(dev))]), axis=0).astype(np.uint8)
+    else:
+        D = Dl
 
     # a7: P_D of the slice for the global D (the sort's own P_D when no other slice added bits)
     if PDl is not None and np.array_equal(D, Dl0):
         packed = PDl
     else:
-        S2 = R[:, ol].contiguous() if nr else R
+        S2 = (R[:, ol].contiguous() if ol is not None else R[:, order.long()].contiguous()) if nr else R
         packed = ops.repack(S2, M, D) if not np.array_equal(D, M) else S2
 
-    nrs = [int(t.item()) for t in comm.allgather(torch.tensor([nr], dtype=torch.int64, device=dev))]
+    nrs = [nr] if G == 1 else [int(t.item()) for t in comm.allgather(torch.tensor([nr], dtype=torch.int64, device=dev))]
     out = dict(mask=D, popcount=cks.popcount(D), sort_mask=M, sort_bits=m, perm=perm, dbit=dbit, packed=packed,
                offset=sum(nrs[:r]), n_total=N, send_counts=send_counts, tree=None)
 
     # a8: a subtree per slice; the roots removed; the top layers over their children
     if tree and N:
         per = int(fanout * fill)
-        hs = [int(t.item()) for t in comm.allgather(torch.tensor([_height(nr, per)], dtype=torch.int64, device=dev))]
+        hs = [_height(nr, per)] if G == 1 else \
+            [int(t.item()) for t in comm.allgather(torch.tensor([_height(nr, per)], dtype=torch.int64, device=dev))]
         hmin = min(h for h in hs if h > 0)
         lstar = max(0, hmin - 2)
         first_rank = next(k for k in range(G) if nrs[k] > 0)
@@ -351,12 +415,13 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
             cnt = int(sub["shape"].level_nodes[lstar])
         span = per ** (lstar + 1)
         hi = torch.clamp(torch.arange(1, cnt + 1, device=dev, dtype=torch.int64) * span, max=nr) - 1
-        cnts = [int(t.item()) for t in comm.allgather(torch.tensor([cnt], dtype=torch.int64, device=dev))]
+        cnts = [cnt] if G == 1 else \
+            [int(t.item()) for t in comm.allgather(torch.tensor([cnt], dtype=torch.int64, device=dev))]
         pad = torch.zeros((max(1, max(cnts)), 2), dtype=torch.int32, device=dev)
         if cnt:
             pad[:cnt, 0] = perm[hi]
             pad[:cnt, 1] = sub["top_min"][:cnt].to(torch.int32)
-        allc = comm.allgather(pad)
+        allc = [pad] if G == 1 else comm.allgather(pad)
         top = None
         if r == 0 and sum(cnts) > 1:
             crid = torch.cat([t[:c, 0] for t, c in zip(allc, cnts)]).contiguous()

@@ -15,10 +15,13 @@ def wrap(name, f):
         return r
     return g
 class Ops(S.CudaOps): pass
-for nm in ["occupancy", "occupancy_mask", "compress", "partition", "repack", "sort_prefix", "adjacent", "bulkload"]:
+for nm in [k for k in vars(S.CudaOps) if not k.startswith("_")]:
     setattr(Ops, nm, staticmethod(wrap(nm, getattr(S.CudaOps, nm))))
 comm.alltoallv = wrap("alltoallv", comm.alltoallv)
 comm.allgather = wrap("allgather", comm.allgather)
+G = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+if G > 1:
+    print('use G = 1 (threads on one device share its SMs)')
 for i in range(3): S.build_sharded(keys, comm, ops=Ops)
 tim.clear()
 torch.cuda.synchronize(); t0 = time.perf_counter()

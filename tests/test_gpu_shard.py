@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import cksgen
+import oracle
 from shard_oracle_ops import check_slices
 
 torch = pytest.importorskip("torch")
@@ -16,7 +17,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from paper_2009_11543_b200 import shard  # noqa: E402
+from paper_2009_11543_b200 import cks, shard  # noqa: E402
 
 
 def run(keys, sizes, **kw):
@@ -36,6 +37,47 @@ def test_sharded_configs(cfg, G):
     check_slices(keys, outs)
     loads = [o["perm"].numel() for o in outs]
     assert max(loads) <= 1.5 * N / G + 64                  # regular sampling keeps the slices balanced
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_fused_and_alltoall_agree(cfg, G):
+    # the fused partition-and-send (every part written into its receiver's buffer by the digit
+    # pass) and the partition + all-to-all baseline give the same slices, equal to the oracle
+    keys = cksgen.config(cfg, n=90_001)
+    N = keys.shape[0]
+    sizes = [N // G] * (G - 1) + [N - (N // G) * (G - 1)]
+    a = run(keys, sizes, fused=True)
+    b = run(keys, sizes, fused=False)
+    check_slices(keys, a)
+    for x, y in zip(a, b):
+        assert torch.equal(x["perm"], y["perm"]) and torch.equal(x["dbit"], y["dbit"])
+        assert x["send_counts"] == y["send_counts"]
+
+
+def test_partition_send_vs_partition():
+    # cks_partition_count + cks_partition_send into one buffer laid out as the local partition
+    # must equal cks_partition (stable parts, row ids with the base)
+    keys = cksgen.config(5, n=70_001)
+    d = torch.from_numpy(keys).cuda()
+    M = oracle.byteocc_superset(keys)
+    P = cks.compress(d, M)
+    m = cks.popcount(M)
+    samples = np.concatenate([P[:, ::997].cpu().numpy().view(np.uint32),
+                              (np.arange(0, 70_001, 997, dtype=np.uint32) + 5)[None, :]], axis=0).T.copy()
+    spl = shard.pick_splitters(samples, 4)
+    q = torch.from_numpy(spl.view(np.int32)).cuda().reshape(-1, P.shape[0] + 1)
+    Pp, ridp, pc = cks.partition(P, m, q, 4, 5)
+    counts = cks.partition_count(P, m, q, 4, 5)
+    assert torch.equal(counts, pc)
+    outP = torch.empty_like(Pp)
+    outR = torch.empty_like(ridp)
+    starts = np.concatenate([[0], np.cumsum(counts.cpu().numpy())[:-1]])
+    n = P.shape[1]
+    cks.partition_send([outP.data_ptr() + 4 * int(s) for s in starts], [n] * 4,
+                       [outR.data_ptr() + 4 * int(s) for s in starts])
+    torch.cuda.synchronize()
+    assert torch.equal(outP, Pp) and torch.equal(outR, ridp)
 
 
 @pytest.mark.parametrize("sizes", [[0, 5000, 1], [4999, 0, 0, 2], [1, 1, 1]])
@@ -87,16 +129,21 @@ def test_partition_and_rank_vs_oracle_ops(bits, parts):
     assert np.array_equal(r.cpu().numpy(), re_.numpy())
 
 
-@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
-def test_sort_prefix_on_given_planes(cfg):
-    # cks_sort_prefix: the first build's sort from P_{D+} instead of key rows
+@pytest.mark.parametrize("cfg,n", [(2, 150_001), (3, 150_001), (4, 150_001), (5, 150_001), (5, 131_072),
+                                   (3, 98_304), (1, 65_536)])
+def test_sort_prefix_on_given_planes(cfg, n):
+    # cks_sort_prefix: the first build's sort from P_{D+} instead of key rows. n a multiple of 32
+    # with |M| a multiple of 32 (cfg5: 96, cfg3: 224, cfg1: 128) sorts the caller's planes in
+    # place of a left-aligned copy: they must come back unchanged
     import oracle
     from paper_2009_11543_b200 import cks
-    keys = cksgen.config(cfg, n=150_001)
+    keys = cksgen.config(cfg, n=n)
     kd = torch.from_numpy(keys).cuda()
     M = cks.superset_mask(kd)
     P = cks.compress(kd, M)
+    P0 = P.clone()
     order, dbit, D, PD = cks.sort_prefix(P, M, want_packed=True)
+    assert torch.equal(P, P0)
     ref = oracle.first_build(keys)
     assert np.array_equal(order.cpu().numpy().view(np.uint32), ref["perm"])
     assert np.array_equal(dbit.cpu().numpy().view(np.uint16), ref["dbit"])
