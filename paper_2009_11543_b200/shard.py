@@ -40,9 +40,11 @@ NONE = 0xFFFF
 
 class TorchComm:
     """Collectives over a torch.distributed process group (NCCL: CUDA tensors; gloo: the
-    tensors are staged through host memory). No peer pointers: the exchange is an NCCL
-    all-to-all (the baseline of DESIGN.md Sec. 7)."""
-    peer_access = False
+    tensors are staged through host memory). Peer buffers for the fused partition-and-send are
+    shared as CUDA IPC handles (torch.multiprocessing's reduction of a CUDA tensor: the peer
+    maps the owner's allocation; across GPUs the kernel's stores go over NVLink); peer_access =
+    False falls back to the partition + all-to-all baseline."""
+    peer_access = True
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -60,6 +62,23 @@ class TorchComm:
         out = [torch.empty_like(x) for _ in range(self.size)]
         self.dist.all_gather(out, x, group=self.group)
         return [o.to(t.device) for o in out]
+
+    def peer_tensors(self, tensors: tuple) -> list[tuple]:
+        """Every rank's `tensors` (CUDA), usable from this process: own rank as is, the others
+        opened from their CUDA IPC handles."""
+        from torch.multiprocessing.reductions import reduce_tensor
+        torch.cuda.current_stream().synchronize()
+        mine = [reduce_tensor(t) for t in tensors]
+        objs = [None] * self.size
+        self.dist.all_gather_object(objs, mine, group=self.group)
+        out = []
+        for d, o in enumerate(objs):
+            out.append(tuple(tensors) if d == self.rank else tuple(fn(*args) for fn, args in o))
+        return out
+
+    def barrier(self):
+        torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
 
     def alltoallv(self, t: torch.Tensor, send_counts: list[int], recv_counts: list[int] | None = None) -> torch.Tensor:
         """Rows [sum(send_counts[:d]), +send_counts[d]) of t go to rank d; returns the rows
@@ -118,6 +137,10 @@ class ThreadComm:
 
     def barrier(self):
         self.allgather_obj(None)
+
+    def peer_tensors(self, tensors: tuple) -> list[tuple]:
+        """Every rank's `tensors` (all ranks share the device and the address space)."""
+        return self.allgather_obj(tuple(tensors))
 
     def alltoallv(self, t: torch.Tensor, send_counts: list[int], recv_counts: list[int] | None = None) -> torch.Tensor:
         self._publish(list(torch.split(t.contiguous(), send_counts, dim=0)))
@@ -285,18 +308,22 @@ def _exchange_fused(comm, ops, P, m, q, off, npl, dev):
     pc = ops.partition_count(P, m, q, G, off)
     cm = torch.stack(comm.allgather(pc)).cpu().numpy()          # cm[s][d]: elements s sends to d
     nr = int(cm[:, r].sum())
-    R = torch.empty((npl, nr), dtype=torch.int32, device=dev)
-    rids = torch.empty(nr, dtype=torch.int32, device=dev)
-    peers = comm.allgather_obj((R.data_ptr(), rids.data_ptr(), nr))
+    # (one allocation per rank: its planes then its row ids, so one IPC handle serves both)
+    buf = torch.empty((npl + 1) * max(nr, 1), dtype=torch.int32, device=dev)
+    R = buf[:npl * nr].view(npl, nr)
+    rids = buf[npl * max(nr, 1):npl * max(nr, 1) + nr]
+    peers = comm.peer_tensors((buf,))
     dst_planes, dst_pitch, dst_rid = [], [], []
     for d in range(G):
-        pr, rr, pitch = peers[d]
+        pb = peers[d][0]
+        nd = int(cm[:, d].sum())
         at = int(cm[:r, d].sum())                                # this sender's start at receiver d
-        dst_planes.append(pr + 4 * at if npl else 0)
-        dst_pitch.append(pitch)
-        dst_rid.append(rr + 4 * at)
+        dst_planes.append(pb.data_ptr() + 4 * at if npl else 0)
+        dst_pitch.append(nd)
+        dst_rid.append(pb.data_ptr() + 4 * (npl * max(nd, 1) + at))
     ops.partition_send(dst_planes, dst_pitch, dst_rid, dev.index)
     comm.barrier()                                               # every sender's stream has completed
+    del peers
     return R, rids, [int(v) for v in cm[r]]
 
 
@@ -346,7 +373,7 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
 
     # a5: stable partition, the one exchange, one stable sort on P
     if fused is None:
-        fused = getattr(comm, "peer_access", False) and hasattr(ops, "partition_count")
+        fused = getattr(comm, "peer_access", False) and hasattr(ops, "partition_count") and keys.is_cuda
     if G == 1:                                                   # one part: the input order
         R, send_counts, rids = P, [n], None
     elif fused:

@@ -211,3 +211,48 @@ def test_sharded_odd_width():
     keys[:, :2] = rng.integers(0, 3, (40_001, 2), dtype=np.uint8)
     keys[rng.integers(0, 40_001, 500)] = keys[rng.integers(0, 40_001, 500)]
     check_slices(keys, run(keys, [10_000, 20_001, 10_000]))
+
+
+_IPC_SCRIPT = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+import cksgen
+from paper_2009_11543_b200 import shard
+rank, world = int(sys.argv[2]), int(sys.argv[3])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+torch.cuda.set_device(0)
+keys = cksgen.config(5, n=90_001)
+cut = [0, 40_000, 90_001] if world == 2 else [0, 30_000, 61_000, 90_001]
+o = shard.build_sharded(torch.from_numpy(keys[cut[rank]:cut[rank + 1]]).cuda(), shard.TorchComm(), fused=True)
+np.savez(sys.argv[1] + f".{rank}.npz", perm=o["perm"].cpu().numpy(), dbit=o["dbit"].cpu().numpy(), mask=o["mask"])
+dist.barrier()
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_fused_over_ipc_processes(tmp_path, world):
+    # the multi-process fused partition-and-send: ranks are processes (gloo for the small
+    # collectives), the receive buffers are shared as CUDA IPC handles and every sender's digit
+    # pass writes its parts into the other processes' buffers. All processes share cuda:0 here
+    # (no kernel waits on another rank); across GPUs the same stores go over NVLink
+    import socket
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    base = str(tmp_path / "r")
+    ps = [subprocess.Popen([sys.executable, "-c", _IPC_SCRIPT, base, str(r), str(world)], env=env, cwd=root)
+          for r in range(world)]
+    for p in ps:
+        assert p.wait(timeout=300) == 0
+    zs = [np.load(f"{base}.{r}.npz") for r in range(world)]
+    keys = cksgen.config(5, n=90_001)
+    ref = oracle.first_build(keys)
+    assert np.array_equal(np.concatenate([z["perm"] for z in zs]).view(np.uint32), ref["perm"])
+    assert np.array_equal(np.concatenate([z["dbit"] for z in zs]).view(np.uint16), ref["dbit"])
+    assert all(np.array_equal(z["mask"], ref["mask"]) for z in zs)
