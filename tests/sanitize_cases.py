@@ -110,9 +110,7 @@ def main(quick: bool):
 if __name__ == "__main__":
     args = sys.argv[1:]
     if "product" not in args:                          # default: the checked library
-        if not os.path.exists(_build.SO_CHECKED):
-            _build.build(checked=True)
-        cks.load_library(_build.SO_CHECKED)
+        cks.load_library(_build.build(checked=True))           # (rebuilt when stale)
         print("library:", _build.SO_CHECKED, flush=True)
     main("quick" in args)
     print("all cases ok", flush=True)
