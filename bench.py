@@ -152,8 +152,10 @@ def cpu_model() -> str:
 
 def oracle_stages(keys, threads: int) -> dict:
     """The oracle's first build by stage (SURVEY 8(d) oracle timing): (i) exact D = full-key
-    sort + adjacency, (ii) compress, (iii) compressed sort; plus the bulk load."""
+    sort + adjacency, (ii) compress, (iii) compressed sort; plus the bulk load. cpu_s / wall =
+    the parallelism it achieved (its compress is a single-threaded bit loop)."""
     import oracle
+    c0 = os.times()
     t0 = time.perf_counter()
     perm = oracle.sort_keys(keys, threads=threads)
     dbit, mask = oracle.adjacent_dbits(keys, perm)
@@ -164,8 +166,11 @@ def oracle_stages(keys, threads: int) -> dict:
     t3 = time.perf_counter()
     oracle.bulkload(perm, dbit, keys, 64, 1.0)
     t4 = time.perf_counter()
+    c1 = os.times()
+    cpu = (c1.user - c0.user) + (c1.system - c0.system)
     return {"exact_D_s": round(t1 - t0, 3), "compress_s": round(t2 - t1, 3), "compressed_sort_s": round(t3 - t2, 3),
-            "bulkload_s": round(t4 - t3, 3), "total_s": round(t4 - t0, 3)}
+            "bulkload_s": round(t4 - t3, 3), "total_s": round(t4 - t0, 3), "cpu_s": round(cpu, 3),
+            "effective_cores": round(cpu / (t4 - t0), 2) if t4 > t0 else None}
 
 
 def cpu_baseline(cfg: int, cfg_name: str, sample_n: int):
@@ -178,6 +183,8 @@ def cpu_baseline(cfg: int, cfg_name: str, sample_n: int):
     one_n = max(1, sample_n // 8)                           # one core (std::sort) on an eighth
     st1 = oracle_stages(keys[:one_n], 1)
     return {"value": sample_n / dt_total, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "cores_note": f"{threads} threads available to the parallel sort; the oracle's bit-loop compress is "
+                          f"single-threaded, so the run averaged {st['effective_cores']} busy cores (cpu_s / wall)",
             "sample": f"first {sample_n:,} keys of {cfg_name} (same generator), oracle first build "
                       f"(parallel full-key sort + adjacency + bit-loop compress + packed sort) + bulk load, "
                       f"{dt_total:.1f} s", "seconds": round(dt_total, 3),
@@ -459,6 +466,7 @@ def main():
         rms = max_over_ranks(e0.elapsed_time(e1) / rs, world, device)
         cks.set_verify(cks.VERIFY_PRIOR)
         assert np.array_equal(rb.mask, dmask)
+        assert torch.equal(rb.perm, builder.perm) and torch.equal(rb.dbit, builder.dbit)   # same column
         rebuild = {"ms_per_step": rms, "verified_ms_per_step": vms,
                    "note": "ms_per_step: the paper's rebuild (P:405-411), order check off; verified: with the "
                            "default order check of a prior mask against the key rows (cks_ctx_set_verify)", "value": n * world / (rms * 1e-3), "unit": UNIT, "sort_bits": int(rb.out.sort_bits),
@@ -487,6 +495,7 @@ def main():
                "timing": "host wall clock around cks_build_host_batch over all steps (it synchronises), "
                          "max over ranks"}
         assert np.array_equal(r["mask"], builder.mask)
+        assert np.array_equal(r["perm"], builder.perm[:n].cpu().numpy().view(np.uint32))   # the device build's
 
     # ---- NEXT-2: the same pipeline on the FULL key (M = all 8B bits, one LSD sort over them),
     # the GPU analog of the paper's full-key build, and the paper's Table 2/6 statistics

@@ -377,12 +377,18 @@ def test_full_size_config(cfg):
     assert np.array_equal(u16(b.dbit), dbit_ref)
     assert np.array_equal(b.mask & ~oracle.byteocc_superset(keys), np.zeros_like(b.mask))
     rng = np.random.default_rng(cfg)
-    idx = np.sort(rng.choice(keys.shape[0], 20_000, replace=False))
+    idx = np.sort(rng.choice(keys.shape[0], 1_000_000, replace=False))
     packed = u32(b.packed())
     assert np.array_equal(packed[:, idx], oracle.compress(keys[perm[idx]], b.mask))
-    T = int(b.shape.total_nodes)
-    rid = u32(b.tree["entry_rid"])[:T * 64]
-    assert np.array_equal(rid[:keys.shape[0]], perm)          # fill 1.0: leaf slots in order == perm
+    # the whole tree at full size: the oracle's bulk load of the verified order and D_i (inner
+    # D-bits computed directly on the full keys) must equal every node array
+    T, f = int(b.shape.total_nodes), 64
+    t = oracle.bulkload(perm, dbit_ref, keys, f, 1.0)
+    L0 = int(b.shape.level_nodes[0])
+    assert np.array_equal(u32(b.tree["node_cnt"])[:T], t["node_cnt"])
+    assert np.array_equal(u32(b.tree["entry_rid"])[:T * f], t["entry_rid"].ravel())
+    assert np.array_equal(u16(b.tree["entry_dbit"])[:T * f], t["entry_dbit"].ravel())
+    assert np.array_equal(u32(b.tree["entry_child"])[:(T - L0) * f], t["entry_child"][L0:].ravel())
 
 
 # ---- NEXT-1: sort by distinguishing prefixes (refinement rounds) -----------------------------
