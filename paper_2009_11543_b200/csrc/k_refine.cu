@@ -380,16 +380,17 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
           uint32_t* __restrict__ handled, uint8_t* __restrict__ any) {
     static_assert(WC >= 1 && WC <= 3 && (NP == 3 || NP == 4) && WC <= NP, "carried remaining words");
     constexpr int I = kTileItems;                                 // 8 positions per thread
-    __shared__ uint32_t s_pm[3];                                  // D of the CTA as P_M bit indices
+    // D of the CTA as a byte per P_M bit index (a plain byte store marks a bit: every writer
+    // stores 1, so the races are benign and no variable 64-bit shift is needed)
+    __shared__ uint8_t s_dm[32 * NP];
     __shared__ uint32_t s_cnt;
-    if (threadIdx.x < 3) s_pm[threadIdx.x] = 0;
+    for (uint32_t t = threadIdx.x; t < 32u * NP; t += blockDim.x) s_dm[t] = 0;
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31;
     // persistent CTAs: D and the counts are reduced once per CTA, not per tile (one global atomic
     // per D-bit per CTA)
-    unsigned long long dlo = 0;
-    uint32_t dhi = 0, hm = 0;
+    uint32_t hm = 0;
     const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t p0 = (tile * kRefThreads + threadIdx.x) * I;
@@ -427,7 +428,7 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
                 if (x) {
                     const uint32_t pmb = (uint32_t)__clzll((long long)x);   // < T <= 64
                     odb[j] = __ldg(R.moff + pmb);
-                    dlo |= 1ull << pmb;
+                    s_dm[pmb] = 1;
                 } else {
                     tb |= 1u << j;
                 }
@@ -515,7 +516,7 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
                 odb[j] = CKS_NONE_INTERNAL;
                 if (fd >= 0) {
                     odb[j] = __ldg(R.moff + fd);
-                    if (fd < 64) dlo |= 1ull << fd; else dhi |= 1u << (fd - 64);
+                    s_dm[fd] = 1;
                 }
             }
         }
@@ -587,7 +588,7 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
                 CKS_WD(j) = CKS_NONE_INTERNAL;
                 if (fd >= 0) {
                     CKS_WD(j) = __ldg(R.moff + fd);
-                    if (fd < 64) dlo |= 1ull << fd; else dhi |= 1u << (fd - 64);
+                    s_dm[fd] = 1;
                 }
             }
         };
@@ -650,22 +651,14 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
     }
     // G. counts and D
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        dlo |= __shfl_xor_sync(0xffffffffu, dlo, o);
-        dhi |= __shfl_xor_sync(0xffffffffu, dhi, o);
-        hm += __shfl_xor_sync(0xffffffffu, hm, o);
-    }
-    if (lane == 0) {
-        atomicOr(&s_pm[0], (uint32_t)dlo);
-        atomicOr(&s_pm[1], (uint32_t)(dlo >> 32));
-        atomicOr(&s_pm[2], dhi);
-        atomicAdd(&s_cnt, hm);
-    }
+    for (int o = 16; o > 0; o >>= 1) hm += __shfl_xor_sync(0xffffffffu, hm, o);
+    if (lane == 0) atomicAdd(&s_cnt, hm);
     __syncthreads();
-    if (threadIdx.x < 96 && (s_pm[threadIdx.x >> 5] >> (threadIdx.x & 31) & 1u)) {
-        const uint32_t d = __ldg(R.moff + threadIdx.x);
-        atomicOr(&dacc[d >> 5], 0x80000000u >> (d & 31));
-    }
+    for (uint32_t t = threadIdx.x; t < 32u * NP; t += blockDim.x)
+        if (s_dm[t]) {
+            const uint32_t d = __ldg(R.moff + t);
+            atomicOr(&dacc[d >> 5], 0x80000000u >> (d & 31));
+        }
     if (threadIdx.x == 0 && s_cnt) atomicAdd(handled, s_cnt);
 }
 
