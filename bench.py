@@ -575,7 +575,8 @@ def main():
         same_ds = bool(torch.equal(nodes, cks.paper_tree(keys, dsb.perm[:n], dsb.dbit[:n], 32, 0.9)))
         del dsb, pk_planes
         fused = {}
-        for name, src in (("rows", cks.PTREE_ROWS), ("ds", cks.PTREE_DS), ("carry", cks.PTREE_CARRY)):
+        for name, src in (("decode", cks.PTREE_DECODE), ("rows", cks.PTREE_ROWS), ("ds", cks.PTREE_DS),
+                          ("carry", cks.PTREE_CARRY)):
             fb = cks.Builder(n, B, device, fanout=64, fill=1.0, paper_tree_pk=32, paper_tree_fill=0.9,
                              paper_tree_source=src)
             fms = timed(lambda: fb(keys))
@@ -587,8 +588,10 @@ def main():
                             "paper_tree_height": int(ps.height), "ds_tree_equals_rows_tree": same_ds,
                             "paper_tree_note": "NEXT-3: 256-B nodes, leaf 12/14, inner 8/9 entries (fill 0.9), pk 32; "
                                                "paper_tree_ms: bits from the key rows (C(b)); paper_tree_ds_ms: A "
-                                               "from P_D + B + C(b) where needed; fused: C(a), the needed variant "
-                                               "bits carried through the sort (P:484-496)"})
+                                               "from P_D + B + C(b) where needed; fused into the build: decode (A "
+                                               "alone: every byte decoded from its D+ bits, the default), rows, ds, "
+                                               "carry (C(a), the needed variant bits carried through the sort), "
+                                               "P:484-496"})
         del nodes
 
     cpu = None

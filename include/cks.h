@@ -398,8 +398,13 @@ typedef struct {
     /* NEXT-3, optional: the paper-format index tree (cks_paper_tree's layout, identical bytes)
      * built by the same call from the sorted order; partial-key bits from the sources of
      * P:484-496 chosen by ptree_source:
-     *   CKS_PTREE_ROWS   C(b): every bit from the key row (random row reads; measured fastest
-     *                    on cfg5, DESIGN.md Sec. 6.3 -- the default);
+     *   CKS_PTREE_AUTO   DECODE when it applies, else ROWS (the default);
+     *   CKS_PTREE_DECODE source A alone: on a first build the sort mask is D+, whose bits at a
+     *                    byte position tell the byte values occurring there apart, so the
+     *                    sorted P_{D+} determines every key bit (per-byte decode tables from the
+     *                    superset pass; no row reads, no extra plane; CKS_EINVAL with a prior
+     *                    mask or the variant superset kind);
+     *   CKS_PTREE_ROWS   C(b): every bit from the key row (random row reads);
      *   CKS_PTREE_DS     A from the sorted P_D, B from the reference key for invariant bits, C(b)
      *                    rows only for the variant bits outside D;
      *   CKS_PTREE_CARRY  as DS, with C(a): the variant bits outside the sort mask that some
@@ -409,13 +414,15 @@ typedef struct {
      * cks_paper_tree_shape(n, ptree_fill) gives the node count. */
     uint8_t* ptree_nodes;     /* device u8[total_nodes][256] or NULL (no paper tree) */
     uint32_t ptree_pk;        /* partial key bits (<= 32) */
-    uint32_t ptree_source;    /* CKS_PTREE_ROWS (0) / CKS_PTREE_DS (1) / CKS_PTREE_CARRY (2) */
+    uint32_t ptree_source;    /* CKS_PTREE_AUTO (0) / _ROWS (1) / _DS (2) / _CARRY (3) / _DECODE (4) */
     double ptree_fill;        /* fill factor in (0, 1] */
 } cks_build_out;
 
-#define CKS_PTREE_ROWS 0
-#define CKS_PTREE_DS 1
-#define CKS_PTREE_CARRY 2
+#define CKS_PTREE_AUTO 0
+#define CKS_PTREE_ROWS 1
+#define CKS_PTREE_DS 2
+#define CKS_PTREE_CARRY 3
+#define CKS_PTREE_DECODE 4
 
 /* keys: device u8[n][key_bytes]; prior_mask: host u8[key_bytes] superset or NULL.
  * A prior mask must contain every distinction bit of THIS column (e.g. the D-bitmap of the

@@ -58,7 +58,7 @@ class BuildOut(ctypes.Structure):
                 ("ptree_fill", ctypes.c_double)]
 
 
-PTREE_ROWS, PTREE_DS, PTREE_CARRY = 0, 1, 2
+PTREE_AUTO, PTREE_ROWS, PTREE_DS, PTREE_CARRY, PTREE_DECODE = 0, 1, 2, 3, 4
 
 
 EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_set_timing", "cks_ctx_set_sort_mode",

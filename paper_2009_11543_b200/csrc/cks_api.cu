@@ -56,6 +56,7 @@ struct cks_ctx {
         anyt,                                                              // k_ref_reg: compaction tiles with ties left
         vbad,                                                              // k_verify_order result
         ptab,                                                              // cks_paper_tree_ds tables
+        pdec,                                                              // decode tree tables
         part_ptrs,                                                         // cks_partition_send pointer table
         keys2, perm2;                                                      // cks_build_host_batch: 2nd buffers
     // pinned host staging
@@ -71,6 +72,10 @@ struct cks_ctx {
     std::vector<uint8_t> pt_E;        // fused paper tree: partial-key bits appended to P_M (C(a))
     bool pt_on = false;
     uint32_t pt_npe = 0;              // planes actually appended by the last build_refine
+    // where the last build left P_M in sorted order (carried / single sort), for the decode tree
+    const uint32_t* spm = nullptr;
+    uint64_t spm_pitch = 0;
+    uint32_t spm_np = 0, spm_g0 = 0;
     PtreeEnt* h_ptab = nullptr;       // pinned staging of the paper tree's per-window table
     uint64_t ps_n = 0, ps_rid_base = 0; // cks_partition_count -> cks_partition_send state
     uint32_t ps_np = 0, ps_parts = 0;
@@ -162,7 +167,7 @@ T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
      &c->total, &c->pm, &c->pd, &c->cmp, &c->crid, &c->crid2, &c->posA, &c->posB, &c->posC, &c->segA, &c->segB,   \
      &c->segC, &c->runoff, &c->runpos, &c->runoff2, &c->runpos2, &c->tie, &c->keep, &c->done, &c->mlist,         \
      &c->wlist, &c->rcnt, &c->rtot, &c->part_in, &c->part_out, &c->anyt, &c->vbad, &c->keys2, &c->perm2,     \
-     &c->ptab, &c->part_ptrs}
+     &c->ptab, &c->part_ptrs, &c->pdec}
 
 // checked build: the canary band after every scratch buffer must be intact after a call
 // (synchronises); no-op otherwise
@@ -526,6 +531,12 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     }
     TRY(run_sort(ctx, pm + (uint64_t)(np - np0) * sp, sp, np0, 4 * np0, n, nullptr, 0, carried, sp, out->perm,
                  &sorted0, &sp0, dig0, false));
+    if (carry) {                                                 // sorted P_M (+ P_E below) stays here
+        ctx->spm = sorted0;
+        ctx->spm_pitch = sp0;
+        ctx->spm_np = np;
+        ctx->spm_g0 = 0;
+    }
     // round-0 adjacency; when rounds follow, fused with finishing the short runs inside a tile
     const bool no_tile = knobs().no_tile_runs;   // (experiments build only)
     const uint32_t* lo0 = np0 >= 2 ? sorted0 + (uint64_t)(np0 - 2) * sp0 : nullptr;
@@ -896,6 +907,10 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
     const uint32_t* sorted = nullptr;
     uint64_t spitch = sp;
     TRY(run_sort(ctx, cbuf, cpitch, np, k, n, nullptr, 0, nullptr, 0, out->perm, &sorted, &spitch));
+    ctx->spm = sorted;                                           // right-aligned P_M in sorted order
+    ctx->spm_pitch = spitch;
+    ctx->spm_np = np;
+    ctx->spm_g0 = 32 * np - m;
     mark(ctx, ST_SORT);
     // a6
     TRY(run_adjacent(ctx, sorted, spitch, m, n, M, B, out->mask, dbit));
@@ -985,6 +1000,56 @@ int run_ptree_ds(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     return CKS_OK;
 }
 
+// The decode tree (k_ptree.cu PkDec): per byte j, the M-bit projection of every byte value
+// occurring there (ctx->occ, from this build's superset pass) -> the value; M = D+ makes the
+// projections distinct, so the sorted P_M alone gives every key bit.
+int run_ptree_decode(cks_ctx* ctx, uint64_t n, uint32_t B, const uint8_t* M, const uint32_t* perm, const uint16_t* dbit,
+                     uint32_t pk, double fill, uint8_t* nodes) {
+    cks_tree_shape s;
+    const int rc = cks_paper_tree_shape(n, fill, &s);
+    if (rc != CKS_OK) return fail(ctx, rc, "bad paper-tree fill %f", fill);
+    std::vector<uint32_t> occ((size_t)B * 8);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(occ.data(), ctx->occ.p, occ.size() * 4, cudaMemcpyDeviceToHost));
+    // layout: rc u32[B] (rank | count << 16), off u32[B], then byte j's 2^c_j values at off[j]
+    std::vector<uint32_t> rcv(B), offv(B);
+    uint32_t rank = 0, dec_bytes = 0;
+    for (uint32_t j = 0; j < B; j++) {
+        const uint32_t c = (uint32_t)__builtin_popcount(M[j]);
+        rcv[j] = rank | (c << 16);
+        offv[j] = dec_bytes;
+        rank += c;
+        dec_bytes += 1u << c;
+    }
+    const size_t tb = (size_t)B * 8 + dec_bytes;
+    std::vector<uint8_t> h(tb, 0);
+    memcpy(h.data(), rcv.data(), (size_t)B * 4);
+    memcpy(h.data() + (size_t)B * 4, offv.data(), (size_t)B * 4);
+    uint8_t* dec = h.data() + (size_t)B * 8;
+    for (uint32_t j = 0; j < B; j++) {
+        const uint32_t mj = M[j];
+        for (uint32_t v = 0; v < 256; v++) {
+            if (!((occ[(size_t)j * 8 + (v >> 5)] >> (v & 31)) & 1u)) continue;
+            uint32_t proj = 0;                                       // M bits of v, MSB first
+            for (int b = 7; b >= 0; b--)
+                if ((mj >> b) & 1u) proj = (proj << 1) | ((v >> b) & 1u);
+            dec[offv[j] + proj] = (uint8_t)v;
+        }
+    }
+    TRY(ensure(ctx, ctx->pdec, tb + 16));
+    CK(cudaMemcpy(ctx->pdec.p, h.data(), tb, cudaMemcpyHostToDevice));
+    TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
+    TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+    int nl = 0;
+    CK(launch_ptree_decode(n, B, perm, dbit, pk, s.per_node, s.reserved, s.level_nodes, s.level_offset, s.height, nodes,
+                           as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl, ctx->spm,
+                           ctx->spm_pitch, ctx->spm_np, ctx->spm_g0, as<uint8_t>(ctx->pdec) + (size_t)B * 8,
+                           as<uint32_t>(ctx->pdec), as<uint32_t>(ctx->pdec) + B, dec_bytes));
+    ctx->launches += (uint64_t)nl;
+    BYTES((double)n * (4.0 * ctx->spm_np + 4.0 + 2.0) + (double)s.total_nodes * 256.0);
+    return CKS_OK;
+}
+
 int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* prior,
                  cks_build_out* out, bool keys_ready_for_mask) {
     std::vector<uint8_t> M(B, 0), V(B, 0);
@@ -1020,9 +1085,10 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     std::vector<uint8_t> ref(B, 0);
     ctx->pt_on = false;
     ctx->pt_npe = 0;
+    ctx->spm = nullptr;
     if (ptree) {
         if (out->ptree_pk > 32) return fail(ctx, CKS_EINVAL, "ptree_pk %u > 32", out->ptree_pk);
-        if (out->ptree_source > CKS_PTREE_CARRY)
+        if (out->ptree_source > CKS_PTREE_DECODE)
             return fail(ctx, CKS_EINVAL, "unknown ptree_source %u", out->ptree_source);
         CK(cudaEventSynchronize(ctx->plan_ev[2]));
         CK(cudaMemcpyAsync(ctx->h_small, keys, B, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1050,7 +1116,15 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     TRY(rc);
     if (ptree) {
         const uint16_t* db = out->dbit ? out->dbit : as<uint16_t>(ctx->dbit);
-        if (out->ptree_source == CKS_PTREE_ROWS) {                // C(b) for every bit
+        // DECODE: every bit from the sorted P_{D+} (a first build's byte-occupancy mask)
+        const bool decodable = !prior && out->superset_kind == CKS_SUPERSET_BYTEOCC && ctx->spm && n;
+        uint32_t src = out->ptree_source;
+        if (src == CKS_PTREE_AUTO) src = decodable ? CKS_PTREE_DECODE : CKS_PTREE_ROWS;
+        if (src == CKS_PTREE_DECODE && !decodable)
+            return fail(ctx, CKS_EINVAL, "ptree_source DECODE needs a first build with the byte-occupancy mask");
+        if (src == CKS_PTREE_DECODE) {
+            TRY(run_ptree_decode(ctx, n, B, M.data(), out->perm, db, out->ptree_pk, out->ptree_fill, out->ptree_nodes));
+        } else if (src == CKS_PTREE_ROWS) {                       // C(b) for every bit
             cks_tree_shape s;
             TRY(cks_paper_tree_shape(n, out->ptree_fill, &s) == CKS_OK ? CKS_OK
                     : fail(ctx, CKS_EINVAL, "bad paper-tree fill %f", out->ptree_fill));
@@ -1061,7 +1135,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
                             s.level_offset, s.height, out->ptree_nodes, as<uint16_t>(ctx->rmin0),
                             as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl));
             ctx->launches += (uint64_t)nl;
-        } else if (ctx->pt_npe) {                                       // A from the carried P_M | P_E, B, no rows
+        } else if (src == CKS_PTREE_CARRY && ctx->pt_npe) {                                       // A from the carried P_M | P_E, B, no rows
             const uint32_t npm = (m + 31) / 32;
             TRY(run_ptree_ds(ctx, keys, n, B, out->perm, db, as<uint32_t>(ctx->pd), scratch_pitch(n), npm + 1,
                              M.data(), 0, ctx->pt_E.data(), 32 * npm, V.data(), ref.data(), out->ptree_pk,

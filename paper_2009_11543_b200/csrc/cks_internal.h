@@ -214,6 +214,13 @@ struct PtreeDs {
     uint32_t gx, gy;           // first bit of X / Y counted from the MSB of the np planes
     const PtreeEnt* ent;       // device table, 8B + 1 entries
 };
+// partial keys decoded from the sorted P_{D+} alone (k_ptree.cu PkDec)
+cudaError_t launch_ptree_decode(uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit, uint32_t pk,
+                                uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
+                                const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
+                                uint16_t* rmin_b, int sms, cudaStream_t st, int* launches, const uint32_t* planes,
+                                uint64_t pitch, uint32_t np, uint32_t g0, const uint8_t* dec, const uint32_t* rc,
+                                const uint32_t* off, uint32_t dec_bytes);
 cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
                          uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
                          const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,

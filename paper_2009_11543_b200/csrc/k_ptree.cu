@@ -66,6 +66,8 @@ struct PkRows {
     const uint8_t* keys;
     uint32_t B;
     bool w8;
+    __host__ __device__ uint32_t smem_bytes() const { return 0u; }
+    __device__ __forceinline__ PkRows stage(uint8_t*) const { return *this; }
     __device__ __forceinline__ void pre(uint64_t, uint32_t (&)[4]) const {}
     __device__ __forceinline__ uint32_t get(uint64_t /*k*/, uint32_t rid, uint16_t d, uint32_t pk,
                                             const uint32_t (&)[4]) const {
@@ -87,6 +89,8 @@ struct PkDs {
     uint32_t gx, gy;                     // bit (from the MSB of the np planes) of segment X's / Y's
                                          // first compressed bit; X then Y (Y may be empty)
     const PtreeEnt* ent;                 // per window start p0 = D + 1 (0 for none), 8B + 1 entries
+    __host__ __device__ uint32_t smem_bytes() const { return 0u; }
+    __device__ __forceinline__ PkDs stage(uint8_t*) const { return *this; }
     // the plane words of sorted position k loaded ahead (np <= 4): the loads do not wait for the
     // per-window table lookup
     __device__ __forceinline__ void pre(uint64_t k, uint32_t (&w)[4]) const {
@@ -137,13 +141,107 @@ struct PkDs {
     }
 };
 
+// Source A extended ("decode"): with M = D+ (a first build) the compressed key determines the
+// whole key -- D+ at byte j is the D-bit set of the byte values occurring there, so their M-bit
+// projections are distinct (Theorem 2 on the byte column, reading R2) and a per-byte table maps
+// a projection back to the byte. Every partial-key bit comes from the sorted P_M: no rows, no
+// extra plane. Table: dec[j*256 + projection] = byte; rc[j] = rank of byte j's first M bit |
+// (its M-bit count << 16).
+struct PkDec {
+    const uint32_t* planes;              // sorted P_M (bit g0 from the MSB of the np planes = its first bit)
+    uint64_t pitch;
+    uint32_t np, g0, B;
+    const uint8_t* dec;                  // byte j's values at dec[off[j] + projection] (2^c_j entries)
+    const uint32_t* rc;                  // rank of byte j's first M bit | c_j << 16
+    const uint32_t* off;
+    uint32_t dec_bytes;                  // table bytes; staged in shared memory per CTA (random
+                                         // lane addresses: banks, not L1 wavefronts per line)
+    __host__ __device__ uint32_t smem_bytes() const { return dec_bytes ? 8 * B + ((dec_bytes + 15) & ~15u) : 0u; }
+    __device__ __forceinline__ PkDec stage(uint8_t* sm) const {
+        if (!dec_bytes) return *this;
+        uint32_t* src_rc = reinterpret_cast<uint32_t*>(sm);
+        uint32_t* src_off = src_rc + B;
+        uint8_t* src_dec = reinterpret_cast<uint8_t*>(src_off + B);
+        for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) { src_rc[i] = rc[i]; src_off[i] = off[i]; }
+        for (uint32_t i = threadIdx.x; i < dec_bytes; i += blockDim.x) src_dec[i] = dec[i];
+        __syncthreads();
+        PkDec t = *this;
+        t.rc = src_rc;
+        t.off = src_off;
+        t.dec = src_dec;
+        return t;
+    }
+    __device__ __forceinline__ void pre(uint64_t k, uint32_t (&w)[4]) const {
+#pragma unroll
+        for (int q = 0; q < 4; q++) w[q] = (np <= 4 && q < (int)np) ? __ldg(planes + (uint64_t)q * pitch + k) : 0u;
+    }
+    __device__ __forceinline__ static uint32_t pick(const uint32_t (&w)[4], int q) {
+        return q == 0 ? w[0] : q == 1 ? w[1] : q == 2 ? w[2] : w[3];
+    }
+    // c (1..8) bits of the planes from bit g (counted from the MSB), right-aligned
+    __device__ __forceinline__ uint32_t bits(uint64_t k, uint32_t g, uint32_t c, const uint32_t (&w)[4]) const {
+        const int q = (int)np - 1 - (int)(g >> 5);
+        const bool reg = np <= 4;
+        const uint32_t a = reg ? pick(w, q) : __ldg(planes + (uint64_t)q * pitch + k);
+        const uint32_t b = q >= 1 ? (reg ? pick(w, q - 1) : __ldg(planes + (uint64_t)(q - 1) * pitch + k)) : 0u;
+        const uint32_t v = (g & 31) ? __funnelshift_l(b, a, g & 31) : a;
+        return v >> (32 - c);
+    }
+    // the plane word q (from the prefetched words when np <= 4)
+    __device__ __forceinline__ uint32_t word(uint64_t k, int q, const uint32_t (&w)[4]) const {
+        if (q < 0) return 0u;
+        return np <= 4 ? pick(w, q) : __ldg(planes + (uint64_t)q * pitch + k);
+    }
+    __device__ __forceinline__ uint32_t get(uint64_t k, uint32_t rid, uint16_t d, uint32_t pk,
+                                            const uint32_t (&w)[4]) const {
+        if (pk == 0) return 0u;
+        const uint32_t p0 = d == CKS_NONE_INTERNAL ? 0u : (uint32_t)d + 1;
+        if (p0 >= 8 * B) return 0u;
+        const uint32_t j0 = p0 >> 3;
+        // the M bits of bytes j0 .. j0+4 are contiguous in P_M: one field of <= 40 bits
+        uint32_t cnt[5], tot = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            cnt[i] = j0 + i < B ? rc[j0 + i] >> 16 : 0u;
+            tot += cnt[i];
+        }
+        unsigned long long f = 0;                                  // left-aligned field
+        if (tot) {
+            const uint32_t g = g0 + (rc[j0] & 0xFFFFu);
+            const int q = (int)np - 1 - (int)(g >> 5);
+            const uint32_t a = word(k, q, w), b = word(k, q - 1, w), c = word(k, q - 2, w);
+            const uint32_t sh = g & 31;
+            const unsigned long long ab = ((unsigned long long)a << 32) | b;
+            f = sh ? (ab << sh) | (c >> (32 - sh)) : ab;
+        }
+        unsigned long long win = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint32_t c = cnt[i];
+            const uint32_t proj = c ? (uint32_t)(f >> (64 - c)) : 0u;
+            f <<= c;
+            const uint32_t v = j0 + i < B ? (uint32_t)dec[off[j0 + i] + proj] : 0u;
+            win = (win << 8) | v;
+        }
+        const uint32_t out = (uint32_t)(win >> (8 - (p0 & 7)));
+        return pk >= 32 ? out : out & ~(0xFFFFFFFFu >> pk);
+    }
+    __device__ __forceinline__ uint32_t get(uint64_t k, uint32_t rid, uint16_t d, uint32_t pk) const {
+        uint32_t w[4];
+        pre(k, w);
+        return get(k, rid, d, pk, w);
+    }
+};
+
 // leaves, thread per sorted key k (entry k % per of leaf k / per): the key-row reads of a
 // warp are independent (a thread per node would walk its entries serially)
 template <class Src>
 __global__ void __launch_bounds__(kPtThreads)
-k_ptree_leaf_entries(const Src src, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
+k_ptree_leaf_entries(const Src src0, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
                      const uint16_t* __restrict__ dbit, uint32_t pk, uint32_t per, uint64_t nleaves,
                      uint8_t* __restrict__ nodes) {
+    extern __shared__ __align__(16) uint8_t s_srctab[];
+    const Src src = src0.stage(s_srctab);
     constexpr int U = 4;                                          // keys in flight per thread
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < n; k0 += U * T) {
@@ -163,7 +261,7 @@ k_ptree_leaf_entries(const Src src, uint64_t n, uint32_t B, const uint32_t* __re
         for (int u = 0; u < U; u++) {
             const uint64_t k = k0 + u * T;
             if (k >= n) break;
-            const uint64_t j = k / per;
+            const uint64_t j = (uint32_t)k / per;                 // (n < 2^32: 32-bit division)
             const uint32_t e = (uint32_t)(k - j * per);
             uint4* nd = reinterpret_cast<uint4*>(nodes + j * 256);
             nd[2 + e] = make_uint4(pkv[u], (uint32_t)d[u] | (B << 16), rid[u], 0u);   // 32 + 16 e
@@ -191,49 +289,56 @@ k_ptree_leaf_min(const uint16_t* __restrict__ dbit, uint64_t n, uint32_t per, ui
     }
 }
 
-// thread per node of level `level` (>= 1)
+// level `level` (>= 1): a thread per entry slot (node j, entry e < 9): the child's highest key
+// (a random sorted position) is read by many threads at once; the e = 0 thread also writes the
+// header and the node's minimum D_k
 template <class Src>
 __global__ void __launch_bounds__(kPtThreads)
-k_ptree_inner(const Src src, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
+k_ptree_inner(const Src src0, uint64_t n, uint32_t B, const uint32_t* __restrict__ perm,
               uint32_t pk, uint32_t per, uint64_t nbelow, uint64_t cover_below, uint64_t below_off, uint64_t nnodes,
               uint64_t node_off, uint32_t level, const uint16_t* __restrict__ rmin_below, uint16_t* __restrict__ rmin,
               uint8_t* __restrict__ nodes) {
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnodes; j += (uint64_t)gridDim.x * blockDim.x) {
-        uint8_t* nd = nodes + (node_off + j) * 256;
-        uint2* w = reinterpret_cast<uint2*>(nd);
+    extern __shared__ __align__(16) uint8_t s_srctab[];
+    const Src src = src0.stage(s_srctab);
+    const uint64_t slots = nnodes * 9;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < slots; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = t < (1ull << 32) ? (uint64_t)((uint32_t)t / 9u) : t / 9;
+        const uint32_t e = (uint32_t)(t - j * 9);
+        uint2* w = reinterpret_cast<uint2*>(nodes + (node_off + j) * 256);
         const uint64_t c0 = j * per, c1 = min(c0 + per, nbelow);
         const uint32_t cnt = (uint32_t)(c1 - c0);
-        uint16_t mn = CKS_NONE_INTERNAL;
-        uint32_t last = 0;
-        for (uint32_t e = 0; e < 9u; e++) {
-            uint2 a = make_uint2(0, 0), b = make_uint2(0, 0), c = make_uint2(0, 0);
-            if (e < cnt) {
-                const uint64_t ch = c0 + e;
-                uint64_t hk = (ch + 1) * cover_below;                    // one past the child's highest key
-                if (hk > n) hk = n;
-                const uint64_t hi = hk - 1;
-                CKS_DCHECK(hi < n && ch < nbelow);
-                const uint32_t rid = __ldg(perm + hi);
+        uint2 a = make_uint2(0, 0), b = make_uint2(0, 0), c = make_uint2(0, 0);
+        auto hi_of = [&](uint64_t ch) {                              // the child's highest key
+            uint64_t hk = (ch + 1) * cover_below;
+            if (hk > n) hk = n;
+            return hk - 1;
+        };
+        if (e < cnt) {
+            const uint64_t ch = c0 + e, hi = hi_of(ch);
+            CKS_DCHECK(hi < n && ch < nbelow);
+            const uint32_t rid = __ldg(perm + hi);
+            const uint16_t d = ch == 0 ? (uint16_t)CKS_NONE_INTERNAL : __ldg(rmin_below + ch);   // vs the previous entry
+            const unsigned long long child = below_off + ch;
+            a = make_uint2(src.get(hi, rid, d, pk), (uint32_t)d | (B << 16));
+            b = make_uint2((uint32_t)child, (uint32_t)(child >> 32));
+            c = make_uint2(rid, 0u);
+        }
+        w[3 + 3 * e] = a;                                         // 24 + 24 e
+        w[4 + 3 * e] = b;
+        w[5 + 3 * e] = c;
+        if (e == 0) {
+            uint16_t mn = CKS_NONE_INTERNAL;
+            for (uint64_t ch = c0; ch < c1; ch++) {
                 const uint16_t rm = __ldg(rmin_below + ch);
                 mn = rm < mn ? rm : mn;
-                const uint16_t d = ch == 0 ? (uint16_t)CKS_NONE_INTERNAL : rm;   // vs the previous entry
-                last = rid;
-                const unsigned long long child = below_off + ch;
-                const uint32_t pkv = src.get(hi, rid, d, pk);
-                a = make_uint2(pkv, (uint32_t)d | (B << 16));
-                b = make_uint2((uint32_t)child, (uint32_t)(child >> 32));
-                c = make_uint2(rid, 0u);
             }
-            w[3 + 3 * e] = a;                                     // 24 + 24 e
-            w[4 + 3 * e] = b;
-            w[5 + 3 * e] = c;
+            w[0] = make_uint2(cnt | (level << 16), B);
+            w[1] = make_uint2(__ldg(perm + hi_of(c1 - 1)), 0u);
+            w[2] = make_uint2(0u, 0u);
+            w[30] = make_uint2(0u, 0u);                           // bytes 240..255
+            w[31] = make_uint2(0u, 0u);
+            rmin[j] = mn;
         }
-        w[0] = make_uint2(cnt | (level << 16), B);
-        w[1] = make_uint2(last, 0u);
-        w[2] = make_uint2(0u, 0u);
-        w[30] = make_uint2(0u, 0u);                               // bytes 240..255
-        w[31] = make_uint2(0u, 0u);
-        rmin[j] = mn;
     }
 }
 
@@ -251,15 +356,20 @@ static cudaError_t run_ptree(const Src& src, uint64_t n, uint32_t B, const uint3
                              uint16_t* rmin_b, int sms, cudaStream_t st, int* launches) {
     *launches = 0;
     if (n == 0 || height == 0) return cudaSuccess;
-    k_ptree_leaf_entries<Src><<<grid_pt(n, sms), kPtThreads, 0, st>>>(src, n, B, perm, dbit, pk, leaf_per,
-                                                                      level_nodes[0], nodes);
+    const uint32_t smem = src.smem_bytes();
+    if (smem > 48 * 1024) {
+        raise_smem_limit((const void*)k_ptree_leaf_entries<Src>, smem);
+        raise_smem_limit((const void*)k_ptree_inner<Src>, smem);
+    }
+    k_ptree_leaf_entries<Src><<<grid_pt(n, sms), kPtThreads, smem, st>>>(src, n, B, perm, dbit, pk, leaf_per,
+                                                                         level_nodes[0], nodes);
     k_ptree_leaf_min<<<grid_pt(level_nodes[0], sms), kPtThreads, 0, st>>>(dbit, n, leaf_per, level_nodes[0], rmin_a);
     *launches += 2;
     uint64_t cover = leaf_per;
     uint16_t* below = rmin_a;
     uint16_t* cur = rmin_b;
     for (uint32_t l = 1; l < height; l++) {
-        k_ptree_inner<Src><<<(unsigned)((level_nodes[l] + 31) / 32), 32, 0, st>>>(
+        k_ptree_inner<Src><<<grid_pt(level_nodes[l] * 9, sms), kPtThreads, smem, st>>>(
             src, n, B, perm, pk, inner_per, level_nodes[l - 1], cover, level_offset[l - 1], level_nodes[l],
             level_offset[l], l, below, cur, nodes);
         ++*launches;
@@ -269,6 +379,17 @@ static cudaError_t run_ptree(const Src& src, uint64_t n, uint32_t B, const uint3
         cur = t;
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_ptree_decode(uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit, uint32_t pk,
+                                uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
+                                const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
+                                uint16_t* rmin_b, int sms, cudaStream_t st, int* launches, const uint32_t* planes,
+                                uint64_t pitch, uint32_t np, uint32_t g0, const uint8_t* dec, const uint32_t* rc,
+                                const uint32_t* off, uint32_t dec_bytes) {
+    PkDec src{planes, pitch, np, g0, B, dec, rc, off, dec_bytes <= 96u * 1024u ? dec_bytes : 0u};
+    return run_ptree(src, n, B, perm, dbit, pk, leaf_per, inner_per, level_nodes, level_offset, height, nodes, rmin_a,
+                     rmin_b, sms, st, launches);
 }
 
 cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,

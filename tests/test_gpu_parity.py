@@ -543,7 +543,7 @@ def test_paper_tree_ds_sources_vs_oracle(cfg, n, pk, fill):
             cks.paper_tree_ds(None, N, B, perm, dbit, r["packed"], N, r["mask"], r["variant"], r["ref_key"], pk, fill)
 
 
-@pytest.mark.parametrize("src", [cks.PTREE_ROWS, cks.PTREE_DS, cks.PTREE_CARRY])
+@pytest.mark.parametrize("src", [cks.PTREE_AUTO, cks.PTREE_ROWS, cks.PTREE_DS, cks.PTREE_CARRY, cks.PTREE_DECODE])
 @pytest.mark.parametrize("cfg,n,pk,fill,ds", [(5, 120_001, 32, 0.9, False), (5, 70_001, 17, 1.0, True),
                                               (3, 90_000, 32, 0.9, True), (4, 50_000, 32, 0.9, False),
                                               (1, None, 24, 0.9, False), (2, 40_000, 32, 0.9, True)])
@@ -553,6 +553,11 @@ def test_build_fused_paper_tree(cfg, n, pk, fill, ds, src):
     # partial keys need ride through the sort as one more plane (C(a)); the build's own outputs
     # must not change
     keys = cksgen.config(cfg, n=n)
+    if src == cks.PTREE_DECODE and cfg in (1, 3, 4):
+        # DECODE reads the sorted P_{D+}, which these builds do not keep (P_M by row id)
+        with pytest.raises(cks.CksError):
+            cks.build(dev(keys), paper_tree_pk=pk, paper_tree_fill=fill, paper_tree_source=src)
+        return
     r = cks.build(dev(keys), paper_tree_pk=pk, paper_tree_fill=fill, ds_metadata=ds, paper_tree_source=src)
     check_build(keys, r)
     ref = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=pk, fill=fill)
@@ -572,6 +577,17 @@ def test_fused_paper_tree_forced_round0(T):
     check_build(keys, r)
     ref = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
     assert np.array_equal(r["paper_tree"].cpu().numpy(), ref["nodes"])
+
+
+def test_decode_tree_rejects_prior_mask():
+    # with a prior mask the sort mask need not separate every byte value: DECODE must refuse
+    keys = cksgen.config(5, n=50_000)
+    ref = oracle.first_build(keys)
+    with pytest.raises(cks.CksError):
+        cks.build(dev(keys), prior_mask=ref["mask"], paper_tree_pk=32, paper_tree_source=cks.PTREE_DECODE)
+    r = cks.build(dev(keys), prior_mask=ref["mask"], paper_tree_pk=32)          # AUTO: rows
+    t = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
+    assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
 
 
 def test_paper_tree_ds_all_variant_bits_compressed():
