@@ -575,11 +575,18 @@ def main():
         same_ds = bool(torch.equal(nodes, cks.paper_tree(keys, dsb.perm[:n], dsb.dbit[:n], 32, 0.9)))
         del dsb, pk_planes
         fused = {}
-        for name, src in (("decode", cks.PTREE_DECODE), ("rows", cks.PTREE_ROWS), ("ds", cks.PTREE_DS),
-                          ("carry", cks.PTREE_CARRY)):
+        for name, src in (("auto", cks.PTREE_AUTO), ("decode", cks.PTREE_DECODE), ("rows", cks.PTREE_ROWS),
+                          ("ds", cks.PTREE_DS), ("carry", cks.PTREE_CARRY)):
             fb = cks.Builder(n, B, device, fanout=64, fill=1.0, paper_tree_pk=32, paper_tree_fill=0.9,
                              paper_tree_source=src)
-            fms = timed(lambda: fb(keys))
+            try:
+                fms = timed(lambda: fb(keys))
+            except cks.CksError as e:                   # DECODE needs P_D+ kept sorted (the carried path)
+                if e.code != cks.CKS_EINVAL:
+                    raise
+                fused[name] = {"applicable": False, "reason": str(e)}
+                del fb
+                continue
             fused[name] = {"build_with_tree_ms": fms, "tree_extra_ms": fms - ms,
                            "equals_rows_tree": bool(torch.equal(fb.ptree[:fb.ptree_nodes], nodes))}
             del fb

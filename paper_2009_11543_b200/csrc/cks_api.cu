@@ -57,6 +57,7 @@ struct cks_ctx {
         vbad,                                                              // k_verify_order result
         ptab,                                                              // cks_paper_tree_ds tables
         pdec,                                                              // decode tree tables
+        psum0, psum1, phk, phr,                                            // paper-tree level summaries
         part_ptrs,                                                         // cks_partition_send pointer table
         keys2, perm2;                                                      // cks_build_host_batch: 2nd buffers
     // pinned host staging
@@ -160,6 +161,19 @@ int ensure(cks_ctx* ctx, DevBuf& b, size_t bytes, bool zero = false) {
 template <class T>
 T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
 
+// the paper tree's per-level scratch, sized by the leaf count
+int ptree_ws(cks_ctx* ctx, uint64_t nleaves, PtreeWs* ws) {
+    TRY(ensure(ctx, ctx->rmin0, (size_t)nleaves * 2 + 16));
+    TRY(ensure(ctx, ctx->rmin1, (size_t)nleaves * 2 + 16));
+    TRY(ensure(ctx, ctx->psum0, (size_t)nleaves * 8 + 16));
+    TRY(ensure(ctx, ctx->psum1, (size_t)nleaves * 8 + 16));
+    TRY(ensure(ctx, ctx->phk, (size_t)nleaves * 16 + 16));
+    TRY(ensure(ctx, ctx->phr, (size_t)nleaves * 4 + 16));
+    *ws = PtreeWs{{as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1)}, {as<uint2>(ctx->psum0), as<uint2>(ctx->psum1)},
+                  as<uint4>(ctx->phk), as<uint32_t>(ctx->phr)};
+    return CKS_OK;
+}
+
 // every scratch buffer of a context
 #define CKS_SCRATCH_LIST(c)                                                                                      \
     {&c->occ, &c->masks8, &c->planeA, &c->planeB, &c->ridA, &c->ridB, &c->dacc, &c->moff, &c->dbit, &c->rmin0, \
@@ -167,7 +181,7 @@ T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
      &c->total, &c->pm, &c->pd, &c->cmp, &c->crid, &c->crid2, &c->posA, &c->posB, &c->posC, &c->segA, &c->segB,   \
      &c->segC, &c->runoff, &c->runpos, &c->runoff2, &c->runpos2, &c->tie, &c->keep, &c->done, &c->mlist,         \
      &c->wlist, &c->rcnt, &c->rtot, &c->part_in, &c->part_out, &c->anyt, &c->vbad, &c->keys2, &c->perm2,     \
-     &c->ptab, &c->part_ptrs, &c->pdec}
+     &c->ptab, &c->part_ptrs, &c->pdec, &c->psum0, &c->psum1, &c->phk, &c->phr}
 
 // checked build: the canary band after every scratch buffer must be intact after a call
 // (synchronises); no-op otherwise
@@ -961,8 +975,8 @@ int run_ptree_ds(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     const int rc = cks_paper_tree_shape(n, fill, &s);
     if (rc != CKS_OK) return fail(ctx, rc, "bad paper-tree shape (fill %f)", fill);
     if (n == 0) return CKS_OK;
-    TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
-    TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+    PtreeWs ws;
+    TRY(ptree_ws(ctx, s.level_nodes[0], &ws));
     // per-window-start table (k_ptree.cu PkDs): for p0 = 0 .. 8B, the pk-bit window's X / Y /
     // invariant / row positions and the ranks of its first position in X and Y
     const uint32_t nb = 8 * B, nent = nb + 1;
@@ -994,7 +1008,7 @@ int run_ptree_ds(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     PtreeDs ds{planes, pitch, np, gx, gy, as<PtreeEnt>(ctx->ptab)};
     int nl = 0;
     CK(launch_ptree(keys, n, B, perm, dbit, pk, s.per_node, s.reserved, s.level_nodes, s.level_offset, s.height, nodes,
-                    as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl, &ds));
+                    ws, ctx->sms, ctx->stream, &nl, &ds));
     ctx->launches += (uint64_t)nl;
     BYTES((double)n * (4.0 * np + 4.0 + 2.0) + (double)s.total_nodes * 256.0);
     return CKS_OK;
@@ -1011,21 +1025,32 @@ int run_ptree_decode(cks_ctx* ctx, uint64_t n, uint32_t B, const uint8_t* M, con
     std::vector<uint32_t> occ((size_t)B * 8);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaMemcpy(occ.data(), ctx->occ.p, occ.size() * 4, cudaMemcpyDeviceToHost));
-    // layout: rc u32[B] (rank | count << 16), off u32[B], then byte j's 2^c_j values at off[j]
-    std::vector<uint32_t> rcv(B), offv(B);
-    uint32_t rank = 0, dec_bytes = 0;
+    // layout: pj uint4[B] (k_ptree.cu PkDec), then byte j's 2^c_j values at off[j], then one 0
+    std::vector<uint32_t> rank(B + 5, 0), cnt(B + 5, 0), off(B + 5, 0);
+    uint32_t r = 0, dec_bytes = 0;
     for (uint32_t j = 0; j < B; j++) {
-        const uint32_t c = (uint32_t)__builtin_popcount(M[j]);
-        rcv[j] = rank | (c << 16);
-        offv[j] = dec_bytes;
-        rank += c;
-        dec_bytes += 1u << c;
+        cnt[j] = (uint32_t)__builtin_popcount(M[j]);
+        rank[j] = r;
+        off[j] = dec_bytes;
+        r += cnt[j];
+        dec_bytes += 1u << cnt[j];
     }
-    const size_t tb = (size_t)B * 8 + dec_bytes;
+    const uint32_t zero = dec_bytes++;                              // bytes past the key
+    for (uint32_t j = B; j < B + 5; j++) off[j] = zero;
+    if (dec_bytes > 65536u || ctx->spm_g0 + r > 4096u)
+        return fail(ctx, CKS_EINVAL, "decode tables too large (%u bytes)", dec_bytes);
+    const size_t tb = (size_t)B * 16 + dec_bytes;
     std::vector<uint8_t> h(tb, 0);
-    memcpy(h.data(), rcv.data(), (size_t)B * 4);
-    memcpy(h.data() + (size_t)B * 4, offv.data(), (size_t)B * 4);
-    uint8_t* dec = h.data() + (size_t)B * 8;
+    uint32_t* pj = reinterpret_cast<uint32_t*>(h.data());
+    for (uint32_t j = 0; j < B; j++) {
+        uint32_t x = ctx->spm_g0 + rank[j];
+        for (uint32_t i = 0; i < 5; i++) x |= cnt[j + i] << (12 + 4 * i);
+        pj[4 * j + 0] = x;
+        pj[4 * j + 1] = off[j] | off[j + 1] << 16;
+        pj[4 * j + 2] = off[j + 2] | off[j + 3] << 16;
+        pj[4 * j + 3] = off[j + 4];
+    }
+    uint8_t* dec = h.data() + (size_t)B * 16;
     for (uint32_t j = 0; j < B; j++) {
         const uint32_t mj = M[j];
         for (uint32_t v = 0; v < 256; v++) {
@@ -1033,18 +1058,17 @@ int run_ptree_decode(cks_ctx* ctx, uint64_t n, uint32_t B, const uint8_t* M, con
             uint32_t proj = 0;                                       // M bits of v, MSB first
             for (int b = 7; b >= 0; b--)
                 if ((mj >> b) & 1u) proj = (proj << 1) | ((v >> b) & 1u);
-            dec[offv[j] + proj] = (uint8_t)v;
+            dec[off[j] + proj] = (uint8_t)v;
         }
     }
     TRY(ensure(ctx, ctx->pdec, tb + 16));
     CK(cudaMemcpy(ctx->pdec.p, h.data(), tb, cudaMemcpyHostToDevice));
-    TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
-    TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+    PtreeWs ws;
+    TRY(ptree_ws(ctx, s.level_nodes[0], &ws));
     int nl = 0;
     CK(launch_ptree_decode(n, B, perm, dbit, pk, s.per_node, s.reserved, s.level_nodes, s.level_offset, s.height, nodes,
-                           as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl, ctx->spm,
-                           ctx->spm_pitch, ctx->spm_np, ctx->spm_g0, as<uint8_t>(ctx->pdec) + (size_t)B * 8,
-                           as<uint32_t>(ctx->pdec), as<uint32_t>(ctx->pdec) + B, dec_bytes));
+                           ws, ctx->sms, ctx->stream, &nl, ctx->spm, ctx->spm_pitch, ctx->spm_np,
+                           as<uint4>(ctx->pdec), as<uint8_t>(ctx->pdec) + (size_t)B * 16, dec_bytes));
     ctx->launches += (uint64_t)nl;
     BYTES((double)n * (4.0 * ctx->spm_np + 4.0 + 2.0) + (double)s.total_nodes * 256.0);
     return CKS_OK;
@@ -1117,7 +1141,10 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     if (ptree) {
         const uint16_t* db = out->dbit ? out->dbit : as<uint16_t>(ctx->dbit);
         // DECODE: every bit from the sorted P_{D+} (a first build's byte-occupancy mask)
-        const bool decodable = !prior && out->superset_kind == CKS_SUPERSET_BYTEOCC && ctx->spm && n;
+        uint64_t dec_bytes = 1;                                   // the decode tables fit u16 offsets
+        for (uint32_t j = 0; j < B; j++) dec_bytes += 1ull << __builtin_popcount(M[j]);
+        const bool decodable =
+            !prior && out->superset_kind == CKS_SUPERSET_BYTEOCC && ctx->spm && n && dec_bytes <= 65536u;
         uint32_t src = out->ptree_source;
         if (src == CKS_PTREE_AUTO) src = decodable ? CKS_PTREE_DECODE : CKS_PTREE_ROWS;
         if (src == CKS_PTREE_DECODE && !decodable)
@@ -1128,12 +1155,11 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             cks_tree_shape s;
             TRY(cks_paper_tree_shape(n, out->ptree_fill, &s) == CKS_OK ? CKS_OK
                     : fail(ctx, CKS_EINVAL, "bad paper-tree fill %f", out->ptree_fill));
-            TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
-            TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+            PtreeWs ws;
+            TRY(ptree_ws(ctx, s.level_nodes[0], &ws));
             int nl = 0;
             CK(launch_ptree(keys, n, B, out->perm, db, out->ptree_pk, s.per_node, s.reserved, s.level_nodes,
-                            s.level_offset, s.height, out->ptree_nodes, as<uint16_t>(ctx->rmin0),
-                            as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl));
+                            s.level_offset, s.height, out->ptree_nodes, ws, ctx->sms, ctx->stream, &nl));
             ctx->launches += (uint64_t)nl;
         } else if (src == CKS_PTREE_CARRY && ctx->pt_npe) {                                       // A from the carried P_M | P_E, B, no rows
             const uint32_t npm = (m + 31) / 32;
@@ -1646,11 +1672,11 @@ int cks_paper_tree(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, co
     if (rc != CKS_OK) return fail(ctx, rc, "bad paper-tree shape (fill %f)", (double)fill);
     if (n == 0) return CKS_OK;
     CK(cudaSetDevice(ctx->device));
-    TRY(ensure(ctx, ctx->rmin0, (size_t)s.level_nodes[0] * 2 + 16));
-    TRY(ensure(ctx, ctx->rmin1, (size_t)s.level_nodes[0] * 2 + 16));
+    PtreeWs ws;
+    TRY(ptree_ws(ctx, s.level_nodes[0], &ws));
     int nl = 0;
     CK(launch_ptree(keys, n, B, perm, dbit, pk_bits, s.per_node, s.reserved, s.level_nodes, s.level_offset,
-                    s.height, nodes, as<uint16_t>(ctx->rmin0), as<uint16_t>(ctx->rmin1), ctx->sms, ctx->stream, &nl));
+                    s.height, nodes, ws, ctx->sms, ctx->stream, &nl));
     ctx->launches += (uint64_t)nl;
     return check_guards(ctx);
 }

@@ -214,16 +214,28 @@ struct PtreeDs {
     uint32_t gx, gy;           // first bit of X / Y counted from the MSB of the np planes
     const PtreeEnt* ent;       // device table, 8B + 1 entries
 };
-// partial keys decoded from the sorted P_{D+} alone (k_ptree.cu PkDec)
+// Per-level scratch of the tree build (every array sized by the leaf count + 16): the node
+// minima of D_k (rmin), per node {partial key of its highest key at the node's minimum D-bit,
+// highest key's row id} (sum) for the level above, and the plane words / row id of each leaf's
+// highest key (hk, hr) captured by the leaf kernel.
+struct PtreeWs {
+    uint16_t* rmin[2];
+    uint2* sum[2];
+    uint4* hk;
+    uint32_t* hr;
+};
+// partial keys decoded from the sorted P_{D+} alone (k_ptree.cu PkDec). pj: per byte j0 a uint4
+// {g | c_i << (12 + 4 i), off_0 | off_1 << 16, off_2 | off_3 << 16, off_4} for the bytes j0 .. j0+4
+// (g = first M bit of byte j0 from the MSB of the planes, c_i = M bits of byte j0+i, off_i = its
+// values in dec; bytes past the key: c = 0, off = the zero byte at dec[dec_bytes - 1]).
 cudaError_t launch_ptree_decode(uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit, uint32_t pk,
                                 uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
-                                const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
-                                uint16_t* rmin_b, int sms, cudaStream_t st, int* launches, const uint32_t* planes,
-                                uint64_t pitch, uint32_t np, uint32_t g0, const uint8_t* dec, const uint32_t* rc,
-                                const uint32_t* off, uint32_t dec_bytes);
+                                const uint64_t* level_offset, uint32_t height, uint8_t* nodes, const PtreeWs& ws,
+                                int sms, cudaStream_t st, int* launches, const uint32_t* planes, uint64_t pitch,
+                                uint32_t np, const uint4* pj, const uint8_t* dec, uint32_t dec_bytes);
 cudaError_t launch_ptree(const uint8_t* keys, uint64_t n, uint32_t B, const uint32_t* perm, const uint16_t* dbit,
                          uint32_t pk, uint32_t leaf_per, uint32_t inner_per, const uint64_t* level_nodes,
-                         const uint64_t* level_offset, uint32_t height, uint8_t* nodes, uint16_t* rmin_a,
-                         uint16_t* rmin_b, int sms, cudaStream_t st, int* launches, const PtreeDs* ds = nullptr);
+                         const uint64_t* level_offset, uint32_t height, uint8_t* nodes, const PtreeWs& ws, int sms,
+                         cudaStream_t st, int* launches, const PtreeDs* ds = nullptr);
 
 }  // namespace cks
