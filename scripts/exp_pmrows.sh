@@ -1,5 +1,6 @@
 # experiments build: P_M planes below round 0 row-major (CKS_PM_ROWS) and the widest run a CTA
-# sorts (CKS_REF_CTA_WORDS), on cfg4 / cfg3
+# sorts (CKS_REF_CTA_WORDS), on cfg4 / cfg3. The knobs live in scripts/pmrows.patch (measured,
+# not kept: DESIGN.md Sec. 6.2); apply it with `git apply scripts/pmrows.patch` first.
 CKS_EXPERIMENTS=1 python -c "from paper_2009_11543_b200 import _build; _build.build(force=True)" || exit 1
 for c in ${CFGS:-4 3}; do
   for pr in 0 1; do
