@@ -564,6 +564,23 @@ def test_build_fused_paper_tree(cfg, n, pk, fill, ds, src):
     assert np.array_equal(r["paper_tree"].cpu().numpy(), ref["nodes"])
 
 
+@pytest.mark.parametrize("src", [cks.PTREE_DECODE, cks.PTREE_ROWS, cks.PTREE_DS])
+@pytest.mark.parametrize("cfg", [5, 2])
+@pytest.mark.parametrize("n,fill,pk", [(1, 0.9, 32), (2, 0.9, 32), (13, 0.9, 32), (14, 1.0, 32), (15, 1.0, 32),
+                                       (25, 0.9, 5), (43, 0.23, 32), (1000, 0.23, 7), (12 * 8 * 8 + 1, 0.9, 32),
+                                       (12 * 8 * 8 * 8 + 11, 0.9, 31)])
+def test_fused_paper_tree_shapes(cfg, n, fill, pk, src):
+    # the tree's edge shapes through the fused build: one leaf (no inner level), a last leaf of
+    # one key (its unused slots zeroed by one thread), the smallest fill (3 per leaf, 2 per inner
+    # node), a root over a single child, and the per-level summaries on trees 2-4 levels high
+    keys = cksgen.config(cfg, n=n)
+    r = cks.build(dev(keys), paper_tree_pk=pk, paper_tree_fill=fill, paper_tree_source=src, ds_metadata=True)
+    check_build(keys, r)
+    ref = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=pk, fill=fill)
+    assert r["paper_tree"].shape[0] == sum(ref["levels"])
+    assert np.array_equal(r["paper_tree"].cpu().numpy(), ref["nodes"])
+
+
 @pytest.mark.parametrize("T", [24, 40, 64])
 def test_fused_paper_tree_forced_round0(T):
     # the appended plane through every round-0 width (T < 32 leaves 4 remaining words: the
