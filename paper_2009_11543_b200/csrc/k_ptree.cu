@@ -198,7 +198,7 @@ struct PkDec {
         } else {
             const int q = (int)np - 1 - (int)top;
             const uint32_t* p = planes + k;
-            a = __ldg(p + (uint64_t)q * pitch);
+            a = q >= 0 ? __ldg(p + (uint64_t)q * pitch) : 0u;            // (np = 0: an empty mask)
             b = q >= 1 ? __ldg(p + (uint64_t)(q - 1) * pitch) : 0u;
             c = q >= 2 ? __ldg(p + (uint64_t)(q - 2) * pitch) : 0u;
         }

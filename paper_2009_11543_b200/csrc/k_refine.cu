@@ -365,12 +365,14 @@ __device__ __forceinline__ void st8(uint32_t* a, uint64_t p0, uint64_t n, bool v
 //      k_ref_warp / k_ref_cta), as do runs longer than a thread.
 // Remaining key of a position (WC = qtop + 1 words, planes qtop .. 0 of the carried sorted P_M,
 // word 0 masked by fmask): WC 1: k = w0; WC 2: k = w0:w1; WC 3: k = w0:w1, x = w2.
+// Strict order of remaining keys. The row id is not compared: round 0 is a stable LSD sort of
+// the rows in input order (implicit, increasing row ids), so a tied run enters the networks in
+// increasing row-id order, and a transposition network that swaps only on "strictly less"
+// keeps equal keys in that order -- the (key, row id) order without comparing row ids.
 template <int WC>
-__device__ __forceinline__ bool rk_less(unsigned long long ka, uint32_t xa, uint32_t ra, unsigned long long kb,
-                                        uint32_t xb, uint32_t rb) {
-    if (ka != kb) return ka < kb;
-    if (WC == 3 && xa != xb) return xa < xb;
-    return ra < rb;
+__device__ __forceinline__ bool rk_less(unsigned long long ka, uint32_t xa, unsigned long long kb, uint32_t xb) {
+    if (WC == 3) return ka < kb || (ka == kb && xa < xb);
+    return ka < kb;
 }
 
 template <int WC, int NP>
@@ -482,7 +484,7 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
         }
         const uint32_t phases = __reduce_max_sync(0xffffffffu, runmax);
         auto cex = [&](int j) {
-            const bool sw = (hl >> (j + 1) & 1u) && rk_less<WC>(key[j + 1], kx[j + 1], vr[j + 1], key[j], kx[j], vr[j]);
+            const bool sw = (hl >> (j + 1) & 1u) && rk_less<WC>(key[j + 1], kx[j + 1], key[j], kx[j]);
             const unsigned long long ka = key[j], kb = key[j + 1];
             key[j] = sw ? kb : ka;
             key[j + 1] = sw ? ka : kb;
@@ -551,7 +553,7 @@ k_ref_reg(RunCtx R, const uint32_t* __restrict__ lo, const uint32_t* __restrict_
         auto wcex = [&](auto jc) {
             constexpr int j = decltype(jc)::value;
             const bool sw = (hl2 >> (j + 1) & 1u) &&
-                            rk_less<WC>(CKS_WK(j + 1), CKS_WX(j + 1), CKS_WR(j + 1), CKS_WK(j), CKS_WX(j), CKS_WR(j));
+                            rk_less<WC>(CKS_WK(j + 1), CKS_WX(j + 1), CKS_WK(j), CKS_WX(j));
             const unsigned long long ka = CKS_WK(j), kb = CKS_WK(j + 1);
             CKS_WK(j) = sw ? kb : ka;
             CKS_WK(j + 1) = sw ? ka : kb;
