@@ -96,6 +96,17 @@ def main(quick: bool):
     nodes = cks.paper_tree(d, perm, dbit, 32, 0.9)
     assert np.array_equal(nodes.cpu().numpy(), oracle.paper_tree(keys, ref["perm"], ref["dbit"], 32, 0.9)["nodes"])
     print("ok paper tree", flush=True)
+    # the fused tree from every partial-key source, including the degenerate shapes (one key:
+    # an empty mask; one leaf; a one-key last leaf)
+    for cfg, n in ((5, 1), (5, 13), (5, 25_009), (2, 15), (2, 20_001), (3, 9_001)):
+        keys = cksgen.config(cfg, n=n)
+        d = torch.from_numpy(keys).cuda()
+        srcs = [cks.PTREE_ROWS, cks.PTREE_DS, cks.PTREE_CARRY] + ([cks.PTREE_DECODE] if cfg != 3 else [])
+        for src in srcs:
+            r = cks.build(d, paper_tree_pk=32, paper_tree_fill=0.9, paper_tree_source=src, ds_metadata=True)
+            t = oracle.paper_tree(keys, u32(r["perm"]), r["dbit"].cpu().numpy().view(np.uint16), 32, 0.9)
+            assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"]), (cfg, n, src)
+    print("ok fused paper trees", flush=True)
     # the sharded path on one device (threads)
     from paper_2009_11543_b200 import shard
     keys = cksgen.config(5, n=30_000)
