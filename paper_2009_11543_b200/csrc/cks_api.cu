@@ -57,6 +57,7 @@ struct cks_ctx {
         vbad,                                                              // k_verify_order result
         ptab,                                                              // cks_paper_tree_ds tables
         pdec,                                                              // decode tree tables
+        rlist,                                                             // round 1's tied positions (a7)
         psum0, psum1, phk, phr,                                            // paper-tree level summaries
         part_ptrs,                                                         // cks_partition_send pointer table
         keys2, perm2;                                                      // cks_build_host_batch: 2nd buffers
@@ -181,7 +182,7 @@ int ptree_ws(cks_ctx* ctx, uint64_t nleaves, PtreeWs* ws) {
      &c->total, &c->pm, &c->pd, &c->cmp, &c->crid, &c->crid2, &c->posA, &c->posB, &c->posC, &c->segA, &c->segB,   \
      &c->segC, &c->runoff, &c->runpos, &c->runoff2, &c->runpos2, &c->tie, &c->keep, &c->done, &c->mlist,         \
      &c->wlist, &c->rcnt, &c->rtot, &c->part_in, &c->part_out, &c->anyt, &c->vbad, &c->keys2, &c->perm2,     \
-     &c->ptab, &c->part_ptrs, &c->pdec, &c->psum0, &c->psum1, &c->phk, &c->phr}
+     &c->ptab, &c->part_ptrs, &c->pdec, &c->psum0, &c->psum1, &c->phk, &c->phr, &c->rlist}
 
 // checked build: the canary band after every scratch buffer must be intact after a call
 // (synchronises); no-op otherwise
@@ -612,6 +613,10 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         return CKS_OK;
     };
     const bool log = knobs().refine_log;          // (experiments build only)
+    // a7 from the round-0 planes (below): they stay sorted except at round 1's tied positions,
+    // which are saved here (when few) and refreshed at the end; an LSD round reuses their buffers
+    bool lsd_refine = false, list1_ok = true;
+    uint64_t nlist1 = 0;
     int li = -1;                                                 // buffer of the current list
     for (uint32_t r = 1; T + 64 * (r - 1) < m; r++) {
         const uint32_t o = T + 64 * (r - 1);                     // first P_M bit of this round's chunk
@@ -629,6 +634,15 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         TRY(counts(&nn, &nseg));
         BYTES((double)nr * (1.0 + (pos ? 4.0 : 0.0)) + (double)nn * 8.0 + (double)nseg * 8.0);
         if (nn == 0) break;
+        if (r == 1 && !carry && keys) {
+            list1_ok = nn <= n / 4;
+            if (list1_ok) {
+                TRY(ensure(ctx, ctx->rlist, nn * 4));
+                CK(cudaMemcpyAsync(ctx->rlist.p, posA_, nn * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+                BYTES((double)nn * 8.0);
+                nlist1 = nn;
+            }
+        }
         // (2) finish short runs and runs of equal keys in place
         const int qtop = (int)np - 1 - (int)(o >> 5);            // plane holding bit o
         LAUNCH(launch_ref_local(pm, sp, np, qtop, moff, as<uint32_t>(ctx->runpos), segA_, as<uint32_t>(ctx->runoff),
@@ -673,6 +687,7 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             sv = as<uint32_t>(ctx->cmp);
             BYTES((double)nseg2 * 8.0 + (double)n2 * (4.0 + 8.0 + 12.0 + 4.0));   // row, chunk by row -> chunk, row
         } else {
+            lsd_refine = true;
             LAUNCH(launch_ref_gather(pm, sp, np, o, posB_, segB_, out->perm, n2, as<uint32_t>(ctx->cmp), cp,
                                      as<uint32_t>(ctx->crid), ctx->sms, ctx->stream));
             BYTES((double)n2 * (8.0 + 4.0 + 8.0 + 12.0 + 4.0));  // pos, seg, row, chunk by row -> list
@@ -720,6 +735,31 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             TRY(upload_plan(ctx, 1, &dplan));
             LAUNCH(launch_repack(sorted0, sp0, n, dplan, ctx->h_plan[1]->nsteps, npd, pd, sp, ctx->sms, ctx->stream));
             BYTES((double)n * 4.0 * (np + npd));
+            out->packed = pd;
+        } else if (keys && !carry && !lsd_refine && list1_ok && np0 == 2 &&
+                   [&] {                                          // every D bit in the round-0 planes
+                       std::vector<uint32_t> sub(np, 0);
+                       repack_words(M, out->mask, B, m, lead, sub);
+                       for (uint32_t q = 0; q + np0 < np; q++)
+                           if (sub[q]) return false;
+                       return true;
+                   }()) {
+            // the round-0 sorted planes (top 64 bits of P_M) hold every D bit: refresh the
+            // positions the refinement reordered from P_M by row, then repack -- no row gather
+            uint32_t* s0 = const_cast<uint32_t*>(sorted0);
+            if (nlist1) {
+                LAUNCH(launch_ref_refresh(as<uint32_t>(ctx->rlist), nlist1, out->perm, pm, sp, np, np0, s0, sp0,
+                                          ctx->sms, ctx->stream));
+                BYTES((double)nlist1 * (4.0 + 4.0 + 8.0 * np0));
+            }
+            std::vector<uint32_t> sub(np, 0);
+            repack_words(M, out->mask, B, m, lead, sub);
+            TRY(claim_slot(ctx, 1));
+            plan_repack(sub.data() + (np - np0), np0, ctx->h_plan[1]);
+            GatherPlan* dplan;
+            TRY(upload_plan(ctx, 1, &dplan));
+            LAUNCH(launch_repack(s0, sp0, n, dplan, ctx->h_plan[1]->nsteps, npd, pd, sp, ctx->sms, ctx->stream));
+            BYTES((double)n * 4.0 * (np0 + npd));
             out->packed = pd;
         } else if (keys) {
             TRY(run_compress(ctx, keys, n, B, out->mask, pd, sp, 0, out->perm));

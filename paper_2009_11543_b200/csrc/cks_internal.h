@@ -179,6 +179,9 @@ constexpr uint32_t kChunkCtaKeys = 4096;
 cudaError_t launch_ref_cta_chunk(const uint32_t* pm, uint64_t pitch, uint32_t np, uint32_t o, const uint32_t* perm,
                                  const uint32_t* run_off, const uint32_t* run_pos, uint64_t nseg, uint64_t nn,
                                  uint32_t* out, uint64_t opitch, uint32_t* orid, int sms, cudaStream_t st);
+cudaError_t launch_ref_refresh(const uint32_t* list, uint64_t nr, const uint32_t* perm, const uint32_t* pm,
+                              uint64_t pitch, uint32_t np, uint32_t np0, uint32_t* sorted, uint64_t spitch, int sms,
+                              cudaStream_t st);
 cudaError_t launch_ref_put(uint32_t* perm, const uint32_t* pos, const uint32_t* rid, uint64_t nr, const uint32_t* pm,
                            uint64_t pitch, uint32_t np, uint32_t* carried, int sms, cudaStream_t st);
 cudaError_t launch_fill_u16(uint16_t* out, uint64_t n, uint16_t v, cudaStream_t st);

@@ -986,6 +986,19 @@ k_ref_put(uint32_t* __restrict__ perm, const uint32_t* __restrict__ pos, const u
     }
 }
 
+// the round-0 sorted planes (np0 of them, the top of P_M) at the listed positions, from P_M by
+// the row id now there (the refinement reordered those positions; a7 repacks the planes)
+__global__ void __launch_bounds__(kRefThreads)
+k_ref_refresh(const uint32_t* __restrict__ list, uint64_t nr, const uint32_t* __restrict__ perm,
+              const uint32_t* __restrict__ pm, uint64_t pitch, uint32_t np, uint32_t np0, uint32_t* __restrict__ sorted,
+              uint64_t spitch) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = list[k], r = perm[p];
+        CKS_DCHECK(p < spitch && r < pitch);
+        for (uint32_t j = 0; j < np0; j++) sorted[(uint64_t)j * spitch + p] = __ldg(pm + (uint64_t)(np - np0 + j) * pitch + r);
+    }
+}
+
 // ---- launchers --------------------------------------------------------------------------------
 
 static unsigned grid_of(uint64_t work, int sms) {
@@ -1111,6 +1124,14 @@ cudaError_t launch_ref_cta_chunk(const uint32_t* pm, uint64_t pitch, uint32_t np
     raise_smem_limit((const void*)k_ref_cta_chunk, smem);
     k_ref_cta_chunk<<<(unsigned)g, kRefThreads, smem, st>>>(pm, pitch, np, o, perm, run_off, run_pos, nseg, nn, out,
                                                             opitch, orid);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_refresh(const uint32_t* list, uint64_t nr, const uint32_t* perm, const uint32_t* pm,
+                              uint64_t pitch, uint32_t np, uint32_t np0, uint32_t* sorted, uint64_t spitch, int sms,
+                              cudaStream_t st) {
+    if (nr == 0) return cudaSuccess;
+    k_ref_refresh<<<grid_of(nr, sms), kRefThreads, 0, st>>>(list, nr, perm, pm, pitch, np, np0, sorted, spitch);
     return cudaGetLastError();
 }
 

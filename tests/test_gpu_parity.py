@@ -704,3 +704,21 @@ def test_checked_library_cases():
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "libcks_checked.so" in r.stdout and "all cases ok" in r.stdout
+
+
+@pytest.mark.parametrize("T,n,seed", [(24, 50_000, 1), (16, 50_000, 2), (8, 30_000, 3), (24, 3_001, 4)])
+def test_packed_from_round0_planes(T, n, seed):
+    # a7 without a row gather: P_M of more than three planes (not carried), every D bit among the
+    # top 64 P_M bits (keys told apart in their first 12 bytes, letters a-h), and the positions
+    # the refinement reordered refreshed in the round-0 planes before the repack. T = 8 / 16
+    # ties so many keys that the round-1 list is not saved (the row-gather path instead)
+    rng = np.random.default_rng(seed)
+    keys = np.empty((n, 32), np.uint8)
+    keys[:, :12] = rng.integers(0x61, 0x69, size=(n, 12), dtype=np.uint8)
+    keys[:, 12:] = rng.integers(0, 256, size=(n, 20), dtype=np.uint8)
+    cks.set_round0_bits(T)
+    try:
+        r = cks.build(dev(keys))
+    finally:
+        cks.set_round0_bits(0)
+    check_build(keys, r)
