@@ -722,3 +722,24 @@ def test_packed_from_round0_planes(T, n, seed):
     finally:
         cks.set_round0_bits(0)
     check_build(keys, r)
+
+
+def test_abi_argument_errors():
+    # the header's error contract at the boundary: n >= 2^32 -> CKS_ERANGE (row ids are u32),
+    # key_bytes outside [1, 512] or a NULL key pointer with n > 0 -> CKS_EINVAL; nothing is
+    # launched (the pointer below addresses one row only)
+    import ctypes
+    L, c = cks._context(0)
+    keys = torch.zeros((1, 16), dtype=torch.uint8, device="cuda")
+    mask = np.zeros(512, np.uint8)
+    pc = ctypes.c_uint32()
+    p = ctypes.c_void_p(keys.data_ptr())
+    assert L.cks_superset_mask(c, p, 1 << 32, 16, cks.SUPERSET_BYTEOCC, mask.ctypes.data, ctypes.byref(pc)) == cks.CKS_ERANGE
+    assert L.cks_superset_mask(c, p, 1, 0, cks.SUPERSET_BYTEOCC, mask.ctypes.data, ctypes.byref(pc)) == cks.CKS_EINVAL
+    assert L.cks_superset_mask(c, p, 1, 513, cks.SUPERSET_BYTEOCC, mask.ctypes.data, ctypes.byref(pc)) == cks.CKS_EINVAL
+    assert L.cks_superset_mask(c, None, 5, 16, cks.SUPERSET_BYTEOCC, mask.ctypes.data, ctypes.byref(pc)) == cks.CKS_EINVAL
+    assert L.cks_superset_mask(c, None, 0, 16, cks.SUPERSET_BYTEOCC, mask.ctypes.data, ctypes.byref(pc)) == cks.CKS_OK
+    torch.cuda.synchronize()
+    # the context stays usable after the rejected calls
+    k = cksgen.config(1, n=1000)
+    check_build(k, cks.build(dev(k)))
