@@ -322,7 +322,7 @@ def main():
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--backend", default="nccl")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--cpu-sample", type=int, default=12_000_000)
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -496,6 +496,21 @@ def main():
                          "max over ranks"}
         assert np.array_equal(r["mask"], builder.mask)
         assert np.array_equal(r["perm"], builder.perm[:n].cpu().numpy().view(np.uint32))   # the device build's
+        # the bound: this box's pinned host->device copy rate for the same bytes (plain copies,
+        # no build), so e2e can be read against the link rather than the kernels
+        kd = torch.empty((n, B), dtype=torch.uint8, device=device)
+        kt = torch.from_numpy(keys_h)
+        kd.copy_(kt, non_blocking=True)
+        torch.cuda.synchronize(device)
+        t1 = time.perf_counter()
+        for _ in range(3):
+            kd.copy_(kt, non_blocking=True)
+        torch.cuda.synchronize(device)
+        h2d = n * B * 3 / (time.perf_counter() - t1)
+        del kd
+        e2e.update({"h2d_copy_gbs": h2d / 1e9, "frac_of_h2d_copy": (n * B / dt) / h2d,
+                    "bound": "PCIe host->device copy of the keys (h2d_copy_gbs: plain pinned copies of the "
+                             "same bytes on this box)"})
 
     # ---- NEXT-2: the same pipeline on the FULL key (M = all 8B bits, one LSD sort over them),
     # the GPU analog of the paper's full-key build, and the paper's Table 2/6 statistics
