@@ -101,8 +101,11 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
         backend = "nccl" if args.backend == "nccl" else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)                 # NCCL binds this rank's device from here on
         dist.init_process_group(backend=backend)
     return world, rank, local
 
