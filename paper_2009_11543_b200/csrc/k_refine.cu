@@ -711,10 +711,11 @@ k_ref_local(RunCtx R, const uint32_t* __restrict__ run_pos, const uint32_t* __re
             for (int j = 0; j < 4; j++)
                 if ((uint32_t)j < L) put_elem<W>(R, p0 + j, w[j], r[j], j ? w[j - 1] : nullptr, s_bm);
         } else if (L <= kLazyRun && !R.carried && (Wr > W || L <= kLocal)) {
-            // more remaining planes than registers: an insertion sort on row ids, words read
-            // from P_M by row as the comparisons need them (most pairs differ in the first)
-            auto cmp = [&](uint32_t a, uint32_t b, uint32_t* tt) -> int {
-                for (int c = 0; c < Wr; c++) {
+            // more remaining planes than registers: an insertion sort on row ids with every
+            // key's first remaining word loaded up front (L independent loads; most pairs
+            // differ there) and the deeper words read from P_M by row only for ties in it
+            auto deeper = [&](uint32_t a, uint32_t b, uint32_t* tt) -> int {
+                for (int c = 1; c < Wr; c++) {
                     const uint32_t wa = rem_word(R, c, 0, a), wb = rem_word(R, c, 0, b);
                     if (wa != wb) {
                         if (tt) *tt = 32u * (R.np - 1 - (uint32_t)(R.qtop - c)) + (uint32_t)__clz(wa ^ wb);
@@ -723,23 +724,33 @@ k_ref_local(RunCtx R, const uint32_t* __restrict__ run_pos, const uint32_t* __re
                 }
                 return 0;
             };
-            uint32_t r[kLazyRun];
+            auto cmp = [&](uint32_t fa, uint32_t a, uint32_t fb, uint32_t b, uint32_t* tt) -> int {
+                if (fa != fb) {
+                    if (tt) *tt = 32u * (R.np - 1 - (uint32_t)R.qtop) + (uint32_t)__clz(fa ^ fb);
+                    return fa < fb ? -1 : 1;
+                }
+                return deeper(a, b, tt);
+            };
+            uint32_t r[kLazyRun], f[kLazyRun];
             for (uint32_t j = 0; j < L; j++) r[j] = R.perm[p0 + j];
+            for (uint32_t j = 0; j < L; j++) f[j] = rem_word(R, 0, 0, r[j]);
             for (uint32_t j = 1; j < L; j++) {
-                const uint32_t x = r[j];
+                const uint32_t x = r[j], fx = f[j];
                 uint32_t i = j;
                 while (i > 0) {
-                    const int c = cmp(r[i - 1], x, nullptr);
+                    const int c = cmp(f[i - 1], r[i - 1], fx, x, nullptr);
                     if (c < 0 || (c == 0 && r[i - 1] < x)) break;
                     r[i] = r[i - 1];
+                    f[i] = f[i - 1];
                     i--;
                 }
                 r[i] = x;
+                f[i] = fx;
             }
             for (uint32_t j = 0; j < L; j++) {
                 R.perm[p0 + j] = r[j];
                 uint32_t tt = 0;
-                if (j && cmp(r[j - 1], r[j], &tt) != 0) {
+                if (j && cmp(f[j - 1], r[j - 1], f[j], r[j], &tt) != 0) {
                     const uint32_t d = R.moff[tt];
                     R.dbit[p0 + j] = (uint16_t)d;
                     const uint32_t b = 0x80000000u >> (d & 31);
