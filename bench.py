@@ -472,7 +472,9 @@ def main():
         assert torch.equal(rb.perm, builder.perm) and torch.equal(rb.dbit, builder.dbit)   # same column
         rebuild = {"ms_per_step": rms, "verified_ms_per_step": vms,
                    "note": "ms_per_step: the paper's rebuild (P:405-411), order check off; verified: with the "
-                           "default order check of a prior mask against the key rows (cks_ctx_set_verify)", "value": n * world / (rms * 1e-3), "unit": UNIT, "sort_bits": int(rb.out.sort_bits),
+                           "default check of a prior mask (cks_ctx_set_verify: the new keys' D+ inside the mask "
+                           "proves the order, else the row-gather order check)",
+                   "value": n * world / (rms * 1e-3), "unit": UNIT, "sort_bits": int(rb.out.sort_bits),
                    "steps": rs, "formula_bytes_per_key": sum(formula_bytes(B, int(rb.out.sort_bits)).values()) - B}
         del rb
 

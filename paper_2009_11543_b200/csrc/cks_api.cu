@@ -70,6 +70,7 @@ struct cks_ctx {
     uint32_t round0_bits = 0;         // forced width of refinement round 0 (0 = sampled)
     int verify = CKS_VERIFY_PRIOR;    // order check of the result against the key rows
     bool verify_now = false;          // ... for the build in progress
+    std::vector<uint8_t> unproven;    // the last prior mask the D+ test could not prove
     double path_bytes = 0.0;          // algorithmic bytes of every kernel of the last build
     std::vector<uint8_t> pt_E;        // fused paper tree: partial-key bits appended to P_M (C(a))
     bool pt_on = false;
@@ -1120,14 +1121,25 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     uint32_t m = 0;
     const bool ptree = out->ptree_nodes != nullptr && n > 0;
     const bool want_v = out->variant || ptree;
+    bool proven = false;                                 // prior mask shown to contain D
     if (prior) {
         memcpy(M.data(), prior, B);
         m = popcount_mask(M.data(), B);
-        if (want_v) {
-            // rebuild: the new variant bitmap needs one pass over the keys (P:413 step 3)
-            std::vector<uint8_t> tmp(B);
-            uint32_t mt = 0;
-            TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_VARIANT, tmp.data(), &mt, true, V.data()));
+        // the order check of a prior mask (CKS_VERIFY_PRIOR): first the sufficient test D+ of
+        // the new keys inside M (one sequential pass; D is inside D+, reading R2, so sorting by
+        // M gives the full-key order, Theorem 2), skipped for a mask that failed it before
+        const bool vprior = keys && n > 1 && ctx->verify == CKS_VERIFY_PRIOR;
+        const bool try_proof = vprior && !(ctx->unproven.size() == B && memcmp(ctx->unproven.data(), prior, B) == 0);
+        if (want_v || try_proof) {
+            // (rebuild: the new variant bitmap is the same pass, P:413 step 3)
+            std::vector<uint8_t> Dp(B);
+            uint32_t mp = 0;
+            TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_BYTEOCC, Dp.data(), &mp, true, V.data()));
+            if (vprior) {
+                proven = true;
+                for (uint32_t j = 0; j < B; j++) proven = proven && (Dp[j] & ~M[j]) == 0;
+                if (!proven) ctx->unproven.assign(prior, prior + B);
+            }
         }
     } else {
         int kind = out->superset_kind;
@@ -1173,7 +1185,8 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         ctx->pt_on = out->ptree_source == CKS_PTREE_CARRY && ne > 0 && ne <= 32;
     }
     mark(ctx, ST_MASK);
-    ctx->verify_now = keys && (ctx->verify == CKS_VERIFY_ALWAYS || (ctx->verify == CKS_VERIFY_PRIOR && prior));
+    ctx->verify_now =
+        keys && (ctx->verify == CKS_VERIFY_ALWAYS || (ctx->verify == CKS_VERIFY_PRIOR && prior && !proven));
     const int rc = build_from_mask(ctx, keys, n, B, M.data(), m, out);
     ctx->verify_now = false;
     ctx->pt_on = false;

@@ -743,3 +743,46 @@ def test_abi_argument_errors():
     # the context stays usable after the rejected calls
     k = cksgen.config(1, n=1000)
     check_build(k, cks.build(dev(k)))
+
+
+def test_prior_mask_proven_by_occupancy():
+    # CKS_VERIFY_PRIOR first tries the sufficient test D+(new keys) inside the prior mask (one
+    # occupancy pass: occupancy + finalize launches); only when it fails does the row-gather
+    # order check run, and a mask that failed is remembered (no occupancy pass next time)
+    def launches_of(fn):
+        torch.cuda.synchronize()
+        a = cks.launches()
+        r = fn()
+        torch.cuda.synchronize()
+        return r, cks.launches() - a
+
+    def rebuild(d, m, mode):
+        cks.set_verify(mode)
+        try:
+            return launches_of(lambda: cks.build(d, prior_mask=m))
+        finally:
+            cks.set_verify(cks.VERIFY_PRIOR)
+
+    # a prior mask holding D+ (at cfg5's full size the exact D is D+ itself; here, 60 k keys,
+    # the exact D is narrower) proves itself: no order check
+    keys = cksgen.config(5, n=60_000)
+    ref = oracle.first_build(keys)
+    d = dev(keys)
+    dplus = oracle.byteocc_superset(keys)
+    r_off, l_off = rebuild(d, dplus, cks.VERIFY_OFF)
+    r_pr, l_pr = rebuild(d, dplus, cks.VERIFY_PRIOR)
+    check_build(keys, r_pr)
+    assert l_pr == l_off + 2                                     # occupancy + finalize, no order check
+    # a stale superset of D+ (an extra bit) is proven as well and sorts right
+    stale = dplus.copy()
+    stale[0] |= 0x80
+    r_st, _ = rebuild(d, stale, cks.VERIFY_PRIOR)
+    check_build(keys, r_st)
+    # the exact D of 60 k keys is inside D+ but not equal: the test fails, the order check runs;
+    # the second rebuild with the same mask skips the occupancy pass
+    _, l_off = rebuild(d, ref["mask"], cks.VERIFY_OFF)
+    r1, l1 = rebuild(d, ref["mask"], cks.VERIFY_PRIOR)
+    r2, l2 = rebuild(d, ref["mask"], cks.VERIFY_PRIOR)
+    check_build(keys, r1)
+    check_build(keys, r2)
+    assert l1 > l2 > l_off and l1 - l2 == 2
