@@ -6,10 +6,14 @@
 // header, 9 entries of 24 bytes {partial key, distinction bit position, key length, child,
 // highest key}. Nodes hold floor(max fanout * fill) entries. The partial key
 // is the pk bits of the key following the entry's distinction bit position (reading
-// C14), read from the key row (option C(b) of P:491: dereference the record). A non-leaf
-// entry's distinction bit position is that of its child's highest key against the previous
-// entry's highest key = the minimum D_k over the child's keys (Lemma 1),
-// carried up the levels as per-node minima. Byte layout: DESIGN.md R16 / include/cks.h.
+// C14), from one of the paper's sources (the Pk* structs below): the key row
+// (C(b)), the sorted compressed key + reference key + rows for what neither holds (A, B,
+// C(b)), or the sorted P_{D+} alone (decode). A non-leaf entry's distinction bit position is
+// that of its child's highest key against the previous entry's highest key = the
+// minimum D_k over the child's keys (Lemma 1). Each level leaves, per node, a summary
+// for the level above (that minimum, the partial key of the node's highest key at it, and the
+// highest key's row id), so an inner entry is a sequential read of its child's summary.
+// Byte layout: DESIGN.md R16 / include/cks.h.
 #include <algorithm>
 
 #include "cks_internal.h"
