@@ -407,10 +407,11 @@ typedef struct {
      *   CKS_PTREE_DECODE source A alone: on a first build the sort mask is D+, whose bits at a
      *                    byte position tell the byte values occurring there apart, so the
      *                    sorted P_{D+} determines every key bit (per-byte decode tables from the
-     *                    superset pass; no row reads, no extra plane). Applies when the build
-     *                    keeps P_{D+} sorted (D+ of at most 96 bits, or the single-sort mode) and
-     *                    the tables (sum over bytes of 2^|D+ bits of the byte|) fit 64 KB;
-     *                    otherwise, or with a prior mask or the variant superset kind, CKS_EINVAL;
+     *                    superset pass; no row reads, no extra plane). Applies when the sort mask
+     *                    holds the keys' D+ (a first build, D+ or V; a rebuild whose prior mask
+     *                    the D+ test of CKS_VERIFY_PRIOR proved), the build keeps P_M sorted (at
+     *                    most 96 mask bits, or the single-sort mode) and the tables (sum over
+     *                    bytes of 2^|mask bits of the byte|) fit 64 KB; otherwise CKS_EINVAL;
      *   CKS_PTREE_ROWS   C(b): every bit from the key row (random row reads);
      *   CKS_PTREE_DS     A from the sorted P_D, B from the reference key for invariant bits, C(b)
      *                    rows only for the variant bits outside D;

@@ -1196,12 +1196,14 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         // DECODE: every bit from the sorted P_{D+} (a first build's byte-occupancy mask)
         uint64_t dec_bytes = 1;                                   // the decode tables fit u16 offsets
         for (uint32_t j = 0; j < B; j++) dec_bytes += 1ull << __builtin_popcount(M[j]);
-        const bool decodable =
-            !prior && out->superset_kind == CKS_SUPERSET_BYTEOCC && ctx->spm && n && dec_bytes <= 65536u;
+        // (the sort mask holds the keys' D+ -- a first build's D+ or V, or a prior mask the D+
+        // test proved -- so its bits at byte j tell the byte values occurring there apart, and
+        // ctx->occ is these keys' occupancy)
+        const bool decodable = (!prior || proven) && ctx->spm && n && dec_bytes <= 65536u;
         uint32_t src = out->ptree_source;
         if (src == CKS_PTREE_AUTO) src = decodable ? CKS_PTREE_DECODE : CKS_PTREE_ROWS;
         if (src == CKS_PTREE_DECODE && !decodable)
-            return fail(ctx, CKS_EINVAL, "ptree_source DECODE needs a first build with the byte-occupancy mask");
+            return fail(ctx, CKS_EINVAL, "ptree_source DECODE needs a sort mask holding the keys' D+ (a first build, or a proven prior mask) kept sorted");
         if (src == CKS_PTREE_DECODE) {
             TRY(run_ptree_decode(ctx, n, B, M.data(), out->perm, db, out->ptree_pk, out->ptree_fill, out->ptree_nodes));
         } else if (src == CKS_PTREE_ROWS) {                       // C(b) for every bit

@@ -598,11 +598,38 @@ def test_fused_paper_tree_forced_round0(T):
 
 def test_decode_tree_rejects_prior_mask():
     # with a prior mask the sort mask need not separate every byte value: DECODE must refuse
+    # unless the D+ test proved the mask (then it holds D+ and decodes like a first build)
     keys = cksgen.config(5, n=50_000)
     ref = oracle.first_build(keys)
     with pytest.raises(cks.CksError):
         cks.build(dev(keys), prior_mask=ref["mask"], paper_tree_pk=32, paper_tree_source=cks.PTREE_DECODE)
     r = cks.build(dev(keys), prior_mask=ref["mask"], paper_tree_pk=32)          # AUTO: rows
+    t = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
+    assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
+    dplus = oracle.byteocc_superset(keys)
+    for src in (cks.PTREE_DECODE, cks.PTREE_AUTO):
+        r = cks.build(dev(keys), prior_mask=dplus, paper_tree_pk=32, paper_tree_source=src)
+        check_build(keys, r)
+        t = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
+        assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
+    cks.set_verify(cks.VERIFY_OFF)                                  # no D+ test: not proven
+    try:
+        with pytest.raises(cks.CksError):
+            cks.build(dev(keys), prior_mask=dplus, paper_tree_pk=32, paper_tree_source=cks.PTREE_DECODE)
+    finally:
+        cks.set_verify(cks.VERIFY_PRIOR)
+
+
+def test_decode_tree_with_variant_superset():
+    # V contains D+, so a first build sorted by V decodes as well (wider per-byte tables). Bytes
+    # from {0x00, 0x03}: D+ = one bit per byte, V = two; 16 bits fit one LSD sort, whose sorted
+    # planes the decode reads
+    rng = np.random.default_rng(7)
+    keys = rng.choice(np.array([0, 3], np.uint8), size=(40_000, 8))
+    assert oracle.popcount(oracle.variant_bitmap(keys)) == 16 and oracle.popcount(oracle.byteocc_superset(keys)) == 8
+    r = cks.build(dev(keys), superset_kind=cks.SUPERSET_VARIANT, paper_tree_pk=32,
+                  paper_tree_source=cks.PTREE_DECODE)
+    check_build(keys, r)
     t = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
     assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
 
