@@ -805,6 +805,7 @@ def test_prior_mask_proven_by_occupancy():
     stale[0] |= 0x80
     r_st, _ = rebuild(d, stale, cks.VERIFY_PRIOR)
     check_build(keys, r_st)
+    assert r_st["sort_bits"] == oracle.popcount(stale)             # the paper's rebuild: by the given mask
     # the exact D of 60 k keys is inside D+ but not equal: the test fails, the order check runs;
     # the second rebuild with the same mask skips the occupancy pass
     _, l_off = rebuild(d, ref["mask"], cks.VERIFY_OFF)
