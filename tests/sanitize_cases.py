@@ -107,6 +107,19 @@ def main(quick: bool):
             t = oracle.paper_tree(keys, u32(r["perm"]), r["dbit"].cpu().numpy().view(np.uint16), 32, 0.9)
             assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"]), (cfg, n, src)
     print("ok fused paper trees", flush=True)
+    # rebuilds: a prior mask the D+ test proves (with the decode tree), and one it cannot
+    # (the row-gather order check, twice: the second skips the occupancy pass)
+    keys = cksgen.config(5, n=30_001)
+    ref = oracle.first_build(keys)
+    d = torch.from_numpy(keys).cuda()
+    dplus = oracle.byteocc_superset(keys)
+    r = cks.build(d, prior_mask=dplus, paper_tree_pk=32, paper_tree_source=cks.PTREE_DECODE)
+    check(keys, r)
+    t = oracle.paper_tree(keys, u32(r["perm"]), r["dbit"].cpu().numpy().view(np.uint16), 32, 0.9)
+    assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
+    for _ in range(2):
+        check(keys, cks.build(d, prior_mask=ref["mask"]))
+    print("ok proven / unproven rebuilds", flush=True)
     # the sharded path on one device (threads)
     from paper_2009_11543_b200 import shard
     keys = cksgen.config(5, n=30_000)
