@@ -814,3 +814,19 @@ def test_prior_mask_proven_by_occupancy():
     check_build(keys, r1)
     check_build(keys, r2)
     assert l1 > l2 > l_off and l1 - l2 == 2
+
+
+@pytest.mark.parametrize("cfg,n", [(1, None), (3, 30_001), (4, 20_003), (2, 50_000)])
+def test_decode_tree_single_sort_plane_counts(cfg, n):
+    # the decode source over every plane count: one LSD sort keeps P_{D+} sorted whatever its
+    # width -- cfg2 1 plane, cfg1 4 (the register path's largest), cfg3 7 and cfg4 12 (the
+    # generic path reading the planes from memory)
+    keys = cksgen.config(cfg, n=n)
+    cks.set_sort_mode(cks.SORT_SINGLE)
+    try:
+        r = cks.build(dev(keys), paper_tree_pk=32, paper_tree_source=cks.PTREE_DECODE)
+    finally:
+        cks.set_sort_mode(cks.SORT_PREFIX_AUTO)
+    check_build(keys, r)
+    t = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
+    assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
