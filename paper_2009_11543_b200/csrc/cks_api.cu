@@ -49,7 +49,7 @@ struct cks_ctx {
     cudaEvent_t ev[ST_N] = {};
     cudaEvent_t plan_ev[3] = {};      // guards the pinned staging slots
     // scratch
-    DevBuf occ, masks8, planeA, planeB, ridA, ridB, dacc, moff, dbit,
+    DevBuf occ, occ_s, masks8, planeA, planeB, ridA, ridB, dacc, moff, dbit,
         rmin0, rmin1, plan[3], keys, perm_scratch, tile_off, chunk_tot, total,
         pm, pd, cmp, crid, crid2, posA, posB, posC, segA, segB, segC, runoff, runpos, runoff2, runpos2, tie, keep, done, mlist, wlist, rcnt, rtot,   // NEXT-1
         part_in, part_out,                                                 // NEXT-4
@@ -69,6 +69,10 @@ struct cks_ctx {
     int refine = CKS_SORT_PREFIX_AUTO; // first build by distinguishing prefixes (NEXT-1)
     uint32_t round0_bits = 0;         // forced width of refinement round 0 (0 = sampled)
     int verify = CKS_VERIFY_PRIOR;    // order check of the result against the key rows
+    uint32_t* spec_occ = nullptr;     // speculative first build: the compress marks the occupancy here
+    uint64_t spec_retries = 0;        // ... builds redone because the sample's mask fell short
+    bool spec_pending = false;        // ... the full D+ / V are on their way to h_small + 4096
+    cudaEvent_t spec_ev = nullptr;
     bool verify_now = false;          // ... for the build in progress
     std::vector<uint8_t> unproven;    // the last prior mask the D+ test could not prove
     double path_bytes = 0.0;          // algorithmic bytes of every kernel of the last build
@@ -163,6 +167,23 @@ int ensure(cks_ctx* ctx, DevBuf& b, size_t bytes, bool zero = false) {
 template <class T>
 T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
 
+// speculative first build (build_common): sampled rows for the mask, smallest column
+constexpr uint32_t kSpecSamples = 65536;
+constexpr uint64_t kSpecMinKeys = 1u << 20;
+constexpr size_t kSpecHostOff = 4096;             // the full D+ and V in h_small (2B bytes)
+
+// right after the speculative compress: the keys' D+ and V from the occupancy it marked, copied
+// to the host behind the build (checked at its end without a stall)
+int spec_enqueue(cks_ctx* ctx, uint64_t n, uint32_t B) {
+    LAUNCH(launch_occ_finalize(as<uint32_t>(ctx->occ), B, n, as<uint8_t>(ctx->masks8), as<uint8_t>(ctx->masks8) + B,
+                               ctx->stream));
+    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ctx->h_small) + kSpecHostOff, ctx->masks8.p, (size_t)B * 2,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaEventRecord(ctx->spec_ev, ctx->stream));
+    ctx->spec_pending = true;
+    return CKS_OK;
+}
+
 // the paper tree's per-level scratch, sized by the leaf count
 int ptree_ws(cks_ctx* ctx, uint64_t nleaves, PtreeWs* ws) {
     TRY(ensure(ctx, ctx->rmin0, (size_t)nleaves * 2 + 16));
@@ -178,7 +199,7 @@ int ptree_ws(cks_ctx* ctx, uint64_t nleaves, PtreeWs* ws) {
 
 // every scratch buffer of a context
 #define CKS_SCRATCH_LIST(c)                                                                                      \
-    {&c->occ, &c->masks8, &c->planeA, &c->planeB, &c->ridA, &c->ridB, &c->dacc, &c->moff, &c->dbit, &c->rmin0, \
+    {&c->occ, &c->occ_s, &c->masks8, &c->planeA, &c->planeB, &c->ridA, &c->ridB, &c->dacc, &c->moff, &c->dbit, &c->rmin0, \
      &c->rmin1, &c->plan[0], &c->plan[1], &c->plan[2], &c->keys, &c->perm_scratch, &c->tile_off, &c->chunk_tot, \
      &c->total, &c->pm, &c->pd, &c->cmp, &c->crid, &c->crid2, &c->posA, &c->posB, &c->posC, &c->segA, &c->segB,   \
      &c->segC, &c->runoff, &c->runpos, &c->runoff2, &c->runpos2, &c->tie, &c->keep, &c->done, &c->mlist,         \
@@ -267,14 +288,16 @@ inline uint64_t scratch_pitch(uint64_t n) { return (n + 31) & ~31ull; }
 
 // a2 + a3
 int run_compress(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* mask,
-                 uint32_t* planes, uint64_t pitch, uint32_t lead = 0, const uint32_t* rows = nullptr) {
+                 uint32_t* planes, uint64_t pitch, uint32_t lead = 0, const uint32_t* rows = nullptr,
+                 uint32_t* occ = nullptr) {
     TRY(claim_slot(ctx, 0));
     plan_compress(mask, B, ctx->h_plan[0]);
     uint32_t m = ctx->h_plan[0]->out_bits, np = (m + 31) / 32;
     if (n == 0 || m == 0) return CKS_OK;
     GatherPlan* dplan;
     TRY(upload_plan(ctx, 0, &dplan));
-    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, planes, pitch, ctx->sms, ctx->stream, lead, rows));
+    LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], np, planes, pitch, ctx->sms, ctx->stream, lead, rows,
+                           occ));
     BYTES((double)n * (B + 4.0 * np + (rows ? 4.0 : 0.0)));
     return CKS_OK;
 }
@@ -492,7 +515,8 @@ int build_refine(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             CK(cudaEventRecord(ctx->aux_ev[1], ctx->aux_stream));
         }
         LAUNCH(launch_compress(keys, n, B, dplan, ctx->h_plan[0], npm, pm + (uint64_t)npe * sp, sp, ctx->sms,
-                               ctx->stream, lead));
+                               ctx->stream, lead, nullptr, ctx->spec_occ));
+        if (ctx->spec_occ) TRY(spec_enqueue(ctx, n, B));
         if (npe) {                                               // P_E, left-aligned in plane 0
             TRY(claim_slot(ctx, 2));
             plan_compress(E, B, ctx->h_plan[2]);
@@ -955,7 +979,8 @@ int build_from_mask(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, c
         cbuf = const_cast<uint32_t*>(planes_in);                  // (read only: the first pass writes elsewhere)
         cpitch = n;
     } else {
-        TRY(run_compress(ctx, keys, n, B, M, cbuf, sp));
+        TRY(run_compress(ctx, keys, n, B, M, cbuf, sp, 0, nullptr, ctx->spec_occ));
+        if (ctx->spec_occ && n && m) TRY(spec_enqueue(ctx, n, B));
     }
     mark(ctx, ST_COMPRESS);
     // a4 + a5
@@ -1121,6 +1146,13 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     uint32_t m = 0;
     const bool ptree = out->ptree_nodes != nullptr && n > 0;
     const bool want_v = out->variant || ptree;
+    // the speculative mask (first builds of large columns whose compress can mark occupancy;
+    // not when the build must return V or the DS tree, which need the mask's pass first)
+    const bool spec = !prior && keys && keys_ready_for_mask && knobs().spec_mask &&
+                      out->superset_kind == CKS_SUPERSET_BYTEOCC && !want_v && !out->ref_key &&
+                      n >= kSpecMinKeys && B >= 32 && compress_marks_occupancy(keys, B);   // (narrow keys: the
+                                                                          // separate pass is cheap; cfg2 lost 13 us)
+    ctx->spec_occ = nullptr;
     bool proven = false;                                 // prior mask shown to contain D
     if (prior) {
         memcpy(M.data(), prior, B);
@@ -1141,6 +1173,25 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
                 if (!proven) ctx->unproven.assign(prior, prior + B);
             }
         }
+    } else if (spec) {
+        // speculative first build: M' = D+ of a strided row sample (a subset of the rows, so
+        // M' is inside the keys' D+); the compress marks every key's bytes on the way, and the
+        // full D+ is compared with M' after the build (below) -- the keys are read once for both
+        TRY(ensure(ctx, ctx->occ_s, (size_t)B * 8 * 4));
+        TRY(ensure(ctx, ctx->occ, (size_t)B * 8 * 4));
+        TRY(ensure(ctx, ctx->masks8, (size_t)B * 2));
+        CK(cudaMemsetAsync(ctx->occ_s.p, 0, (size_t)B * 8 * 4, ctx->stream));
+        CK(cudaMemsetAsync(ctx->occ.p, 0, (size_t)B * 8 * 4, ctx->stream));
+        LAUNCH(launch_occupancy_sample(keys, n, B, kSpecSamples, as<uint32_t>(ctx->occ_s), ctx->stream));
+        BYTES((double)kSpecSamples * B);
+        LAUNCH(launch_occ_finalize(as<uint32_t>(ctx->occ_s), B, n, as<uint8_t>(ctx->masks8),
+                                   as<uint8_t>(ctx->masks8) + B, ctx->stream));
+        CK(cudaEventSynchronize(ctx->plan_ev[2]));
+        CK(cudaMemcpyAsync(ctx->h_small, ctx->masks8.p, B, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        memcpy(M.data(), ctx->h_small, B);
+        m = popcount_mask(M.data(), B);
+        ctx->spec_occ = as<uint32_t>(ctx->occ);
     } else {
         int kind = out->superset_kind;
         TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask, V.data()));
@@ -1187,7 +1238,31 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     mark(ctx, ST_MASK);
     ctx->verify_now =
         keys && (ctx->verify == CKS_VERIFY_ALWAYS || (ctx->verify == CKS_VERIFY_PRIOR && prior && !proven));
-    const int rc = build_from_mask(ctx, keys, n, B, M.data(), m, out);
+    ctx->spec_pending = false;
+    int rc = build_from_mask(ctx, keys, n, B, M.data(), m, out);
+    ctx->spec_occ = nullptr;
+    if (rc == CKS_OK && spec) {
+        // the keys' D+ from the occupancy the compress marked: equal to M' -> the build stands
+        // (M' holds D+ holds D: Theorem 2); else (the sample missed a byte value that adds a
+        // D+ bit) build again by the full D+, no further pass over the keys for the mask
+        std::vector<uint8_t> Mp(M);
+        uint32_t mf = 0;
+        if (ctx->spec_pending) {
+            CK(cudaEventSynchronize(ctx->spec_ev));
+            const uint8_t* h = reinterpret_cast<const uint8_t*>(ctx->h_small) + kSpecHostOff;
+            memcpy(M.data(), h, B);
+            memcpy(V.data(), h + B, B);
+            mf = popcount_mask(M.data(), B);
+        } else {                                                  // (nothing was compressed: m' = 0)
+            TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_BYTEOCC, M.data(), &mf, true, V.data()));
+        }
+        ctx->spec_pending = false;
+        if (mf != m || memcmp(M.data(), Mp.data(), B) != 0) {
+            ctx->spec_retries++;
+            m = mf;
+            rc = build_from_mask(ctx, keys, n, B, M.data(), m, out);
+        }
+    }
     ctx->verify_now = false;
     ctx->pt_on = false;
     TRY(rc);
@@ -1263,6 +1338,7 @@ int cks_ctx_create(int device, void* stream, cks_ctx** out) {
     if (ok) ok = cudaMallocHost(&ctx->h_small, 8192) == cudaSuccess;
     if (ok) ok = cudaMallocHost(&ctx->h_tot, 64) == cudaSuccess;
     if (ok) ok = cudaEventCreateWithFlags(&ctx->ptab_ev, cudaEventDisableTiming) == cudaSuccess;
+    if (ok) ok = cudaEventCreateWithFlags(&ctx->spec_ev, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < 3 && ok; i++) ok = cudaEventRecord(ctx->plan_ev[i], ctx->stream) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -1291,6 +1367,7 @@ int cks_ctx_destroy(cks_ctx* ctx) {
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->h_ptab) cudaFreeHost(ctx->h_ptab);
     if (ctx->ptab_ev) cudaEventDestroy(ctx->ptab_ev);
+    if (ctx->spec_ev) cudaEventDestroy(ctx->spec_ev);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
     for (int i = 0; i < 6; i++)

@@ -60,6 +60,7 @@ struct Knobs {
     int lsd_ws = 1;            // warp-specialised downsweep on full tiles
     int lsd_debug = 0;         // timing-only modes with wrong results (experiments build only)
     int ref_cta = 2048;        // longest run one CTA sorts in the refinement
+    int spec_mask = 1;         // first build: mask from a row sample, occupancy marked by the compress
     bool no_tile_runs = false; // round-0 adjacency without in-tile run finishing
     bool no_kernel_events = false;
     bool refine_log = false;
@@ -90,7 +91,14 @@ cudaError_t launch_prefix_sample(const uint8_t* keys, uint64_t n, uint32_t B, co
 // rows != NULL: key i is keys[rows[i]] (compress in a given order).
 cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
                             const GatherPlan* hplan, uint32_t out_planes, uint32_t* planes, uint64_t pitch,
-                            int sms, cudaStream_t st, uint32_t lead = 0, const uint32_t* rows = nullptr);
+                            int sms, cudaStream_t st, uint32_t lead = 0, const uint32_t* rows = nullptr,
+                            uint32_t* occ = nullptr);
+// occ != NULL (no row list): the compress also ORs every key byte's occupancy into occ
+// (u32[B][8]) -- the fixed widths only (compress_marks_occupancy)
+bool compress_marks_occupancy(const uint8_t* keys, uint32_t B);
+// occupancy (u32[B][8], OR-ed in) of `samples` rows strided over the n keys (B in 8/16/32/64)
+cudaError_t launch_occupancy_sample(const uint8_t* keys, uint64_t n, uint32_t B, uint32_t samples, uint32_t* occ,
+                                    cudaStream_t st);
 cudaError_t launch_repack(const uint32_t* in_planes, uint64_t in_pitch, uint64_t n, const GatherPlan* dplan,
                           uint32_t nsteps, uint32_t out_planes, uint32_t* out, uint64_t out_pitch, int sms,
                           cudaStream_t st, const uint32_t* rows = nullptr);

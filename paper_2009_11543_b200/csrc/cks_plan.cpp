@@ -37,6 +37,7 @@ const Knobs& knobs() {
         k.ref_cta = env("CKS_REF_CTA", 2048);
         if (k.ref_cta < 0) k.ref_cta = 0;
         if (k.ref_cta > 2048) k.ref_cta = 2048;
+        k.spec_mask = env("CKS_SPEC_MASK", 1);
         k.no_tile_runs = getenv("CKS_NO_TILE_RUNS") != nullptr;
         k.no_kernel_events = getenv("CKS_NO_KERNEL_EVENTS") != nullptr;
         k.refine_log = getenv("CKS_REFINE_LOG") != nullptr;

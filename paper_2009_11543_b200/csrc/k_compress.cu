@@ -16,6 +16,7 @@
 #include <string.h>
 
 #include "cks_internal.h"
+#include "k_occ_flags.cuh"
 
 namespace cks {
 
@@ -240,6 +241,49 @@ k_compress_fixed(const uint8_t* __restrict__ keys, uint64_t n, const __grid_cons
     }
 }
 
+// The speculative first build's compress (cks_api.cu build_common): k_compress_fixed<B, 1>
+// by a mask taken from a sample of the rows, marking every key byte's occupancy on the way (the
+// byte-occupancy superset pass fused into the compress: the keys are read once). The caller
+// compares the full occupancy's D+ with the mask afterwards and compresses again if they differ.
+template <int B>
+__global__ void __launch_bounds__(kCompressThreads)
+k_compress_occ(const uint8_t* __restrict__ keys, uint64_t n, const __grid_constant__ FixedPlan<B / 4> plan,
+               uint32_t* __restrict__ planes, uint64_t pitch, uint32_t np, uint32_t toppad, uint32_t* __restrict__ occ) {
+    constexpr int NW = B / 4;
+    __shared__ __align__(16) uint8_t flag[B * kRowBytes];
+    for (uint32_t i = threadIdx.x; i < B * kRowBytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(flag)[i] = 0;
+    __syncthreads();
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) {
+        uint32_t w[NW];
+        load_key<B>(keys + i * B, w);
+#pragma unroll
+        for (int k = 0; k < NW; k++)
+#pragma unroll
+            for (int b = 0; b < 4; b++) flag[(4 * k + b) * kRowBytes + __byte_perm(w[k], 0, 0x4440 + b)] = 1;
+        unsigned long long acc = 0;                          // pending bits, left-aligned
+        uint32_t accbits = toppad, q = np - 1;
+#pragma unroll
+        for (int k = 0; k < NW; k++) {                       // most significant end of P first
+            if (plan.mask[k] == 0) continue;
+            uint32_t x = bswap32(w[k]) & plan.mask[k];
+#pragma unroll
+            for (int s = 0; s < 5; s++) x = mad_u32(x & plan.mv[k][s], (1u << (1u << s)) - 1u, x);
+            acc |= ((unsigned long long)x << 32) >> accbits;
+            accbits += plan.cnt[k];
+            if (accbits >= 32) {
+                planes[(uint64_t)q * pitch + i] = (uint32_t)(acc >> 32);
+                acc <<= 32;
+                accbits -= 32;
+                q--;
+            }
+        }
+        if (accbits) planes[(uint64_t)q * pitch + i] = (uint32_t)(acc >> 32);
+    }
+    __syncthreads();
+    fold_flags<B>(flag, occ);
+}
+
 // Row-list variant for B in {32, 64} (a7: P_D from the key rows in sorted order): the random
 // rows are loaded cooperatively, B/16 lanes per row with one 16-byte load each, into a
 // shared-memory tile of 256 rows (odd 16-byte row stride), then each thread compresses its
@@ -304,7 +348,7 @@ k_compress_rows(const uint8_t* __restrict__ keys, uint64_t n, const __grid_const
 
 template <int B>
 static void launch_fixed(const uint8_t* keys, uint64_t n, const GatherPlan* hplan, uint32_t* planes, uint64_t pitch,
-                         uint32_t np, uint32_t lead, const uint32_t* rows, int grid, cudaStream_t st) {
+                         uint32_t np, uint32_t lead, const uint32_t* rows, int grid, cudaStream_t st, uint32_t* occ) {
     FixedPlan<B / 4> fp;
     memset(&fp, 0, sizeof(fp));
     for (uint32_t s = 0; s < hplan->nsteps; s++) {
@@ -323,6 +367,7 @@ static void launch_fixed(const uint8_t* keys, uint64_t n, const GatherPlan* hpla
         }
     }
     if (rows) k_compress_fixed<B, 4><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, np, toppad, rows);
+    else if (occ) k_compress_occ<B><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, np, toppad, occ);
     else k_compress_fixed<B, 1><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, np, toppad, rows);
 }
 
@@ -333,21 +378,26 @@ static int grid_for(uint64_t work, int per_sm, int sms) {
     return (int)(want < cap ? want : cap);
 }
 
+bool compress_marks_occupancy(const uint8_t* keys, uint32_t B) {
+    return ((uintptr_t)keys & 15) == 0 && (B == 8 || B == 16 || B == 32 || B == 64);
+}
+
 cudaError_t launch_compress(const uint8_t* keys, uint64_t n, uint32_t B, const GatherPlan* dplan,
                             const GatherPlan* hplan, uint32_t np, uint32_t* planes, uint64_t pitch, int sms,
-                            cudaStream_t st, uint32_t lead, const uint32_t* rows) {
+                            cudaStream_t st, uint32_t lead, const uint32_t* rows, uint32_t* occ) {
     if (n == 0 || np == 0) return cudaSuccess;
     const uint32_t nsteps = hplan->nsteps;
-    if (((uintptr_t)keys & 15) == 0 && (B == 8 || B == 16 || B == 32 || B == 64)) {
+    if (compress_marks_occupancy(keys, B)) {
         int grid = grid_for(n, 8, sms);
         switch (B) {
-            case 8: launch_fixed<8>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st); break;
-            case 16: launch_fixed<16>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st); break;
-            case 32: launch_fixed<32>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st); break;
-            default: launch_fixed<64>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st); break;
+            case 8: launch_fixed<8>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st, occ); break;
+            case 16: launch_fixed<16>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st, occ); break;
+            case 32: launch_fixed<32>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st, occ); break;
+            default: launch_fixed<64>(keys, n, hplan, planes, pitch, np, lead, rows, grid, st, occ); break;
         }
         return cudaGetLastError();
     }
+    if (occ) return cudaErrorInvalidValue;                       // (occupancy marking: fixed widths only)
     if ((B & 15) == 0 && ((uintptr_t)keys & 15) == 0 && !rows) {
         uint32_t S16 = (B >> 4) | 1;
         size_t smem = (size_t)kCompressThreads * S16 * 16;

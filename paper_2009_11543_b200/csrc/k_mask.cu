@@ -11,6 +11,7 @@
 // words are padded to a stride of 9 so that positions 16 apart (read by the two halves of
 // a warp when B = 32) fall in different banks.
 #include "cks_internal.h"
+#include "k_occ_flags.cuh"
 
 namespace cks {
 
@@ -128,26 +129,6 @@ __global__ void k_occ_finalize(const uint32_t* __restrict__ occ, uint32_t B, uin
 // bytes so that rows start in different banks.
 // Each thread keeps U 16-byte chunks in flight. The flags are folded into the u32 bitsets
 // at the end.
-constexpr int kRowBytes = 260;
-
-// fold: thread per (position, word): 32 flags -> one u32
-template <int B>
-__device__ __forceinline__ void fold_flags(const uint8_t* flag, uint32_t* __restrict__ occ_g) {
-    for (uint32_t i = threadIdx.x; i < B * 8; i += blockDim.x) {
-        const uint8_t* f = flag + (i >> 3) * kRowBytes + (i & 7) * 32;
-        uint32_t bits = 0;
-#pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-            uint32_t q = *reinterpret_cast<const uint32_t*>(f + k);
-            bits |= ((q & 0xFF) ? 1u : 0u) << k;
-            bits |= ((q & 0xFF00) ? 1u : 0u) << (k + 1);
-            bits |= ((q & 0xFF0000) ? 1u : 0u) << (k + 2);
-            bits |= ((q & 0xFF000000) ? 1u : 0u) << (k + 3);
-        }
-        if (bits) atomicOr(&occ_g[i], bits);
-    }
-}
-
 template <int B>
 __global__ void __launch_bounds__(256) k_occupancy_bytes(const uint8_t* __restrict__ keys, uint64_t nchunks,
                                                          uint32_t* __restrict__ occ_g) {
@@ -247,6 +228,52 @@ cudaError_t launch_occupancy(const uint8_t* keys, uint64_t n, uint32_t B, uint32
         int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
         raise_smem_limit((const void*)k_occupancy_generic, smem);
         k_occupancy_generic<<<grid, 256, smem, st>>>(keys, n, B, occ);
+    }
+    return cudaGetLastError();
+}
+
+// Occupancy of a strided sample of rows (thread per sampled row, B in {8, 16, 32, 64}, 16-byte
+// aligned keys): the speculative first build's mask (cks_api.cu build_common). Row i*step for
+// i < samples.
+template <int B>
+__global__ void __launch_bounds__(256) k_occupancy_sample(const uint8_t* __restrict__ keys, uint64_t step,
+                                                          uint32_t samples, uint32_t* __restrict__ occ_g) {
+    __shared__ __align__(16) uint8_t flag[B * kRowBytes];
+    for (uint32_t i = threadIdx.x; i < B * kRowBytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(flag)[i] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < samples; i += gridDim.x * blockDim.x) {
+        const uint8_t* row = keys + (uint64_t)i * step * B;
+#pragma unroll
+        for (int u = 0; u < (B >= 16 ? B / 16 : 1); u++) {
+            uint32_t w[4];
+            if (B >= 16) {
+                const int4 v = __ldg(reinterpret_cast<const int4*>(row) + u);
+                w[0] = (uint32_t)v.x; w[1] = (uint32_t)v.y; w[2] = (uint32_t)v.z; w[3] = (uint32_t)v.w;
+            } else {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(row));
+                w[0] = v.x; w[1] = v.y; w[2] = 0; w[3] = 0;
+            }
+#pragma unroll
+            for (int b = 0; b < (B >= 16 ? 16 : B); b++)
+                flag[(16 * u + b) * kRowBytes + __byte_perm(w[b >> 2], 0, 0x4440 + (b & 3))] = 1;
+        }
+    }
+    __syncthreads();
+    fold_flags<B>(flag, occ_g);
+}
+
+cudaError_t launch_occupancy_sample(const uint8_t* keys, uint64_t n, uint32_t B, uint32_t samples, uint32_t* occ,
+                                    cudaStream_t st) {
+    if (n == 0 || samples == 0) return cudaSuccess;
+    const uint64_t step = n / samples ? n / samples : 1;
+    const uint32_t cnt = (uint32_t)(n / step < samples ? n / step : samples);
+    const unsigned grid = (cnt + 255) / 256 < 64 ? (cnt + 255) / 256 : 64;
+    switch (B) {
+        case 8: k_occupancy_sample<8><<<grid, 256, 0, st>>>(keys, step, cnt, occ); break;
+        case 16: k_occupancy_sample<16><<<grid, 256, 0, st>>>(keys, step, cnt, occ); break;
+        case 32: k_occupancy_sample<32><<<grid, 256, 0, st>>>(keys, step, cnt, occ); break;
+        case 64: k_occupancy_sample<64><<<grid, 256, 0, st>>>(keys, step, cnt, occ); break;
+        default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }

@@ -120,6 +120,14 @@ def main(quick: bool):
     for _ in range(2):
         check(keys, cks.build(d, prior_mask=ref["mask"]))
     print("ok proven / unproven rebuilds", flush=True)
+    # the speculative first build (>= 2^20 keys): the sample's mask holds, and one that falls
+    # short (an unsampled row with a new byte value) is built again
+    for keys in (cksgen.config(5, n=1_100_001), cksgen.config(3, n=1_100_001)):
+        check(keys, cks.build(torch.from_numpy(keys).cuda()))
+    keys = np.random.default_rng(3).integers(0, 8, size=(1_100_001, 32), dtype=np.uint8)
+    keys[555_555, 7] = 0x80
+    check(keys, cks.build(torch.from_numpy(keys).cuda()))
+    print("ok speculative first builds", flush=True)
     # the sharded path on one device (threads)
     from paper_2009_11543_b200 import shard
     keys = cksgen.config(5, n=30_000)

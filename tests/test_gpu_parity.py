@@ -830,3 +830,33 @@ def test_decode_tree_single_sort_plane_counts(cfg, n):
     check_build(keys, r)
     t = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
     assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
+
+
+@pytest.mark.parametrize("values", [2, 8])
+def test_speculative_mask_retry(values):
+    # first builds of >= 2^20 keys take the mask from a strided row sample and let the compress
+    # mark the occupancy; when the sample misses a byte value that adds a D+ bit, the build is
+    # redone by the full D+. Here one unsampled row carries a value no other row has at byte 3
+    # (2 values per byte: one LSD sort; 8: the sort by distinguishing prefixes)
+    n = 2_000_003
+    rng = np.random.default_rng(11)
+    keys = rng.integers(0, values, size=(n, 32), dtype=np.uint8)
+    keys[:, 0] = rng.integers(0, 256, size=n, dtype=np.uint8)
+    keys[777_777, 3] = 0x80                                       # not on the sample's stride
+    d = dev(keys)
+    torch.cuda.synchronize()
+    a = cks.launches()
+    r = cks.build(d)
+    torch.cuda.synchronize()
+    l_retry = cks.launches() - a
+    check_build(keys, r)
+    assert r["sort_bits"] == oracle.popcount(oracle.byteocc_superset(keys))   # sorted by the full D+
+    keys[777_777, 3] = 0x01                                       # the sample now sees every value
+    d = dev(keys)
+    torch.cuda.synchronize()
+    a = cks.launches()
+    r = cks.build(d)
+    torch.cuda.synchronize()
+    l_plain = cks.launches() - a
+    check_build(keys, r)
+    assert l_retry > l_plain                                      # the first build ran twice
