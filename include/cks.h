@@ -99,11 +99,12 @@ int cks_ctx_set_round0_bits(cks_ctx* ctx, uint32_t bits);
  *   CKS_VERIFY_OFF     never;
  *   CKS_VERIFY_PRIOR   when the caller passes a prior mask (default; the library's own
  *                      superset masks contain D by construction, reading R2). A sufficient
- *                      test runs first: one sequential pass gives the new keys' byte-
- *                      occupancy superset D+ (reading R2: D is inside it), and when D+ lies
- *                      inside the prior mask the order is right by Theorem 2 and the
- *                      row-gather check is skipped; a mask that failed the test is remembered
- *                      by the context, which then goes straight to the row-gather check;
+ *                      test runs first: the new keys' byte-occupancy superset D+ (reading R2:
+ *                      D is inside it; marked by the rebuild's compress, or one sequential
+ *                      pass), and when D+ lies inside the prior mask the order is right by
+ *                      Theorem 2 and the row-gather check is skipped; a mask that
+ *                      failed the test is remembered by the context, which then goes straight
+ *                      to the row-gather check;
  *   CKS_VERIFY_ALWAYS  every build. */
 #define CKS_VERIFY_OFF 0
 #define CKS_VERIFY_PRIOR 1

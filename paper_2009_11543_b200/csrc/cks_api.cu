@@ -72,6 +72,7 @@ struct cks_ctx {
     uint32_t* spec_occ = nullptr;     // speculative first build: the compress marks the occupancy here
     uint64_t spec_retries = 0;        // ... builds redone because the sample's mask fell short
     bool spec_pending = false;        // ... the full D+ / V are on their way to h_small + 4096
+    std::vector<uint8_t> proof_mask;  // rebuild: prior mask whose D+ test rides on the compress
     cudaEvent_t spec_ev = nullptr;
     bool verify_now = false;          // ... for the build in progress
     std::vector<uint8_t> unproven;    // the last prior mask the D+ test could not prove
@@ -922,6 +923,16 @@ int run_bulkload_top(cks_ctx* ctx, const uint32_t* child_rid, const uint16_t* ch
 // (ctx->verify_now): CKS_ERANGE if the sort mask was not a superset of the distinction bits.
 int verify_if(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const cks_build_out* out) {
     if (!ctx->verify_now || !keys || n < 2) return CKS_OK;
+    if (!ctx->proof_mask.empty() && ctx->spec_pending) {
+        // rebuild: the D+ test on the occupancy the compress marked (finalised long ago)
+        CK(cudaEventSynchronize(ctx->spec_ev));
+        const uint8_t* dp = reinterpret_cast<const uint8_t*>(ctx->h_small) + kSpecHostOff;
+        bool proven = true;
+        for (uint32_t j = 0; j < B; j++) proven = proven && (dp[j] & ~ctx->proof_mask[j]) == 0;
+        ctx->spec_pending = false;
+        if (proven) return CKS_OK;
+        ctx->unproven = ctx->proof_mask;
+    }
     TRY(ensure(ctx, ctx->vbad, 16));
     LAUNCH(launch_verify_order(keys, B, out->perm, n, as<unsigned long long>(ctx->vbad), ctx->sms, ctx->stream));
     BYTES((double)n * (4.0 + B));
@@ -1148,6 +1159,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     const bool want_v = out->variant || ptree;
     // the speculative mask (first builds of large columns whose compress can mark occupancy;
     // not when the build must return V or the DS tree, which need the mask's pass first)
+    ctx->proof_mask.clear();
     const bool spec = !prior && keys && keys_ready_for_mask && knobs().spec_mask &&
                       out->superset_kind == CKS_SUPERSET_BYTEOCC && !want_v && !out->ref_key &&
                       n >= kSpecMinKeys && B >= 32 && compress_marks_occupancy(keys, B);   // (narrow keys: the
@@ -1162,7 +1174,15 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         // M gives the full-key order, Theorem 2), skipped for a mask that failed it before
         const bool vprior = keys && n > 1 && ctx->verify == CKS_VERIFY_PRIOR;
         const bool try_proof = vprior && !(ctx->unproven.size() == B && memcmp(ctx->unproven.data(), prior, B) == 0);
-        if (want_v || try_proof) {
+        if (try_proof && !want_v && compress_marks_occupancy(keys, B)) {
+            // the test rides on the compress: it marks the occupancy, the D+ is finalised behind
+            // it, and the order check (verify_if, after the sort) first tests D+ inside M
+            TRY(ensure(ctx, ctx->occ, (size_t)B * 8 * 4));
+            TRY(ensure(ctx, ctx->masks8, (size_t)B * 2));
+            CK(cudaMemsetAsync(ctx->occ.p, 0, (size_t)B * 8 * 4, ctx->stream));
+            ctx->spec_occ = as<uint32_t>(ctx->occ);
+            ctx->proof_mask.assign(prior, prior + B);
+        } else if (want_v || try_proof) {
             // (rebuild: the new variant bitmap is the same pass, P:413 step 3)
             std::vector<uint8_t> Dp(B);
             uint32_t mp = 0;
@@ -1241,6 +1261,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     ctx->spec_pending = false;
     int rc = build_from_mask(ctx, keys, n, B, M.data(), m, out);
     ctx->spec_occ = nullptr;
+    ctx->proof_mask.clear();
     if (rc == CKS_OK && spec) {
         // the keys' D+ from the occupancy the compress marked: equal to M' -> the build stands
         // (M' holds D+ holds D: Theorem 2); else (the sample missed a byte value that adds a

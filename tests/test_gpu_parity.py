@@ -773,9 +773,10 @@ def test_abi_argument_errors():
 
 
 def test_prior_mask_proven_by_occupancy():
-    # CKS_VERIFY_PRIOR first tries the sufficient test D+(new keys) inside the prior mask (one
-    # occupancy pass: occupancy + finalize launches); only when it fails does the row-gather
-    # order check run, and a mask that failed is remembered (no occupancy pass next time)
+    # CKS_VERIFY_PRIOR first tries the sufficient test D+(new keys) inside the prior mask (the
+    # compress marks the occupancy; one finalize launch more than a rebuild without the check);
+    # only when it fails does the row-gather order check run, and a mask that failed is
+    # remembered (no occupancy marking next time)
     def launches_of(fn):
         torch.cuda.synchronize()
         a = cks.launches()
@@ -799,7 +800,7 @@ def test_prior_mask_proven_by_occupancy():
     r_off, l_off = rebuild(d, dplus, cks.VERIFY_OFF)
     r_pr, l_pr = rebuild(d, dplus, cks.VERIFY_PRIOR)
     check_build(keys, r_pr)
-    assert l_pr == l_off + 2                                     # occupancy + finalize, no order check
+    assert l_pr == l_off + 1                                     # finalize only, no order check
     # a stale superset of D+ (an extra bit) is proven as well and sorts right
     stale = dplus.copy()
     stale[0] |= 0x80
@@ -813,7 +814,7 @@ def test_prior_mask_proven_by_occupancy():
     r2, l2 = rebuild(d, ref["mask"], cks.VERIFY_PRIOR)
     check_build(keys, r1)
     check_build(keys, r2)
-    assert l1 > l2 > l_off and l1 - l2 == 2
+    assert l1 > l2 > l_off and l1 - l2 == 1
 
 
 @pytest.mark.parametrize("cfg,n", [(1, None), (3, 30_001), (4, 20_003), (2, 50_000)])
