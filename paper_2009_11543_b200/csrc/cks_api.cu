@@ -1158,10 +1158,12 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     const bool ptree = out->ptree_nodes != nullptr && n > 0;
     const bool want_v = out->variant || ptree;
     // the speculative mask (first builds of large columns whose compress can mark occupancy;
-    // not when the build must return V or the DS tree, which need the mask's pass first)
+    // V comes out of the same occupancy after the build -- not with the C(a) tree source, whose
+    // carried plane needs V before the sort)
     ctx->proof_mask.clear();
     const bool spec = !prior && keys && keys_ready_for_mask && knobs().spec_mask &&
-                      out->superset_kind == CKS_SUPERSET_BYTEOCC && !want_v && !out->ref_key &&
+                      out->superset_kind == CKS_SUPERSET_BYTEOCC &&
+                      !(ptree && out->ptree_source == CKS_PTREE_CARRY) &&
                       n >= kSpecMinKeys && B >= 32 && compress_marks_occupancy(keys, B);   // (narrow keys: the
                                                                           // separate pass is cheap; cfg2 lost 13 us)
     ctx->spec_occ = nullptr;
@@ -1216,7 +1218,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         int kind = out->superset_kind;
         TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask, V.data()));
     }
-    if (out->variant) memcpy(out->variant, V.data(), B);
+    if (out->variant && !spec) memcpy(out->variant, V.data(), B);
     if (out->ref_key) {                                  // the reference key (row 0's key)
         if (n) {
             CK(cudaEventSynchronize(ctx->plan_ev[2]));
@@ -1278,6 +1280,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             TRY(run_superset(ctx, keys, n, B, CKS_SUPERSET_BYTEOCC, M.data(), &mf, true, V.data()));
         }
         ctx->spec_pending = false;
+        if (out->variant) memcpy(out->variant, V.data(), B);
         if (mf != m || memcmp(M.data(), Mp.data(), B) != 0) {
             ctx->spec_retries++;
             m = mf;

@@ -861,3 +861,15 @@ def test_speculative_mask_retry(values):
     l_plain = cks.launches() - a
     check_build(keys, r)
     assert l_retry > l_plain                                      # the first build ran twice
+
+
+@pytest.mark.parametrize("cfg,src", [(5, cks.PTREE_AUTO), (5, cks.PTREE_DS), (3, cks.PTREE_ROWS), (2, cks.PTREE_DECODE)])
+def test_speculative_build_with_tree_and_metadata(cfg, src):
+    # the speculative first build (>= 2^20 keys) with the DS-metadata and the paper tree: V and
+    # the decode tables come from the occupancy the compress marked
+    keys = cksgen.config(cfg, n=1_200_007)
+    r = cks.build(dev(keys), paper_tree_pk=32, paper_tree_source=src, ds_metadata=True)
+    check_build(keys, r)
+    assert np.array_equal(r["variant"], oracle.variant_bitmap(keys)) and np.array_equal(r["ref_key"], keys[0])
+    t = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
+    assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
