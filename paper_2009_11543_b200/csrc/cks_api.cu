@@ -1161,6 +1161,15 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     // V comes out of the same occupancy after the build -- not with the C(a) tree source, whose
     // carried plane needs V before the sort)
     ctx->proof_mask.clear();
+    struct Reset {                                       // every exit: no marking request outlives the call
+        cks_ctx* c;
+        ~Reset() {
+            c->spec_occ = nullptr;
+            c->spec_pending = false;
+            c->proof_mask.clear();
+            c->verify_now = false;
+        }
+    } reset{ctx};
     const bool spec = !prior && keys && keys_ready_for_mask && knobs().spec_mask &&
                       out->superset_kind == CKS_SUPERSET_BYTEOCC &&
                       !(ptree && out->ptree_source == CKS_PTREE_CARRY) &&
