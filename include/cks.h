@@ -437,6 +437,11 @@ typedef struct {
  * A prior mask must contain every distinction bit of THIS column (e.g. the D-bitmap of the
  * last build when no key was inserted since); with the default order check a mask
  * that does not returns CKS_ERANGE (see cks_ctx_set_verify).
+ * Without a prior mask, columns of at least 2^20 keys of 32 or 64 bytes (16-byte aligned)
+ * take the sort mask from a strided sample of 65536 rows and the compress marks every key's
+ * byte occupancy on the way; the column's D+ is compared with the sample's at the end and the
+ * build is run again by it when they differ. The result is the same as with a separate
+ * superset pass; sort_bits reports the mask finally used.
  * Synchronises: after the superset mask, once per refinement round (to size the next
  * round), after the exact D is known, and after the order check when it runs. */
 int cks_build(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes,
