@@ -425,6 +425,8 @@ typedef struct {
     uint32_t ptree_pk;        /* partial key bits (<= 32) */
     uint32_t ptree_source;    /* CKS_PTREE_AUTO (0) / _ROWS (1) / _DS (2) / _CARRY (3) / _DECODE (4) */
     double ptree_fill;        /* fill factor in (0, 1] */
+    uint8_t* sort_mask;       /* host u8[key_bytes] or NULL: receives the mask the sort ran on (the
+                                 first build's D+ or V, the prior mask of a rebuild) */
 } cks_build_out;
 
 #define CKS_PTREE_AUTO 0

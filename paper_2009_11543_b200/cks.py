@@ -55,7 +55,7 @@ class BuildOut(ctypes.Structure):
                 ("rounds", ctypes.c_uint32), ("round0_bits", ctypes.c_uint32), ("refined_keys", ctypes.c_uint64),
                 ("variant", ctypes.c_void_p), ("ref_key", ctypes.c_void_p),
                 ("ptree_nodes", ctypes.c_void_p), ("ptree_pk", ctypes.c_uint32), ("ptree_source", ctypes.c_uint32),
-                ("ptree_fill", ctypes.c_double)]
+                ("ptree_fill", ctypes.c_double), ("sort_mask", ctypes.c_void_p)]
 
 
 PTREE_AUTO, PTREE_ROWS, PTREE_DS, PTREE_CARRY, PTREE_DECODE = 0, 1, 2, 3, 4
@@ -554,6 +554,7 @@ class Builder:
                  paper_tree_source: int = 0):
         self.n, self.B = n, B
         self.mask = np.zeros(B, np.uint8)
+        self.sort_mask = np.zeros(B, np.uint8)                   # the mask the sort ran on
         # DS-metadata: variant bitmap and reference key, recomputed by the build
         self.variant = np.zeros(B, np.uint8) if ds_metadata else None
         self.ref_key = np.zeros(B, np.uint8) if ds_metadata else None
@@ -563,6 +564,7 @@ class Builder:
         self.tree = alloc_tree(self.shape, device) if tree else None
         self.out = BuildOut()
         self.out.mask = self.mask.ctypes.data
+        self.out.sort_mask = self.sort_mask.ctypes.data
         self.out.perm = self.perm.data_ptr()
         self.out.dbit = self.dbit.data_ptr() if self.dbit is not None else None
         if self.tree is not None:
@@ -620,7 +622,8 @@ def build(keys: torch.Tensor, prior_mask=None, fanout: int = 64, fill: float = 1
                 paper_tree_pk=paper_tree_pk, paper_tree_fill=paper_tree_fill, paper_tree_source=paper_tree_source)
     b(keys, prior_mask)
     o = b.out
-    r = dict(mask=b.mask.copy(), popcount=int(o.popcount), sort_bits=int(o.sort_bits), passes=int(o.passes),
+    r = dict(mask=b.mask.copy(), popcount=int(o.popcount), sort_bits=int(o.sort_bits), sort_mask=b.sort_mask.copy(),
+             passes=int(o.passes),
              perm=b.perm[:n], dbit=b.dbit[:n] if b.dbit is not None else None, packed=b.packed(),
              tree=b.tree, shape=b.shape, height=int(o.height))
     if ds_metadata:

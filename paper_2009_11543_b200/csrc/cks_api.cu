@@ -1299,6 +1299,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     ctx->verify_now = false;
     ctx->pt_on = false;
     TRY(rc);
+    if (out->sort_mask) memcpy(out->sort_mask, M.data(), B);
     if (ptree) {
         const uint16_t* db = out->dbit ? out->dbit : as<uint16_t>(ctx->dbit);
         // DECODE: every bit from the sorted P_{D+} (a first build's byte-occupancy mask)

@@ -202,6 +202,11 @@ class CudaOps:
     bulkload_block = staticmethod(cks.bulkload_block)
     bulkload_top = staticmethod(cks.bulkload_top)
 
+    @staticmethod
+    def first_build(keys, superset_kind):
+        """One shard: the fused single first build (no tree: the sharded tree format follows)."""
+        return cks.build(keys, superset_kind=superset_kind, tree=False)
+
 
 # ---- host logic ----------------------------------------------------------------------------
 
@@ -348,6 +353,17 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
                     packed=torch.zeros((0, 0), dtype=torch.int32, device=dev), offset=0, n_total=0,
                     send_counts=[0] * G, tree=None)
 
+    if G == 1 and hasattr(ops, "first_build"):
+        # one shard, one part: the single first build (its mask from a row sample and the
+        # compress marking the occupancy), then the sharded tree format
+        fb = ops.first_build(keys, superset_kind)
+        out = dict(mask=fb["mask"], popcount=fb["popcount"], sort_mask=fb["sort_mask"], sort_bits=fb["sort_bits"],
+                   perm=fb["perm"], dbit=fb["dbit"], packed=fb["packed"], offset=0, n_total=N, send_counts=[n],
+                   tree=None)
+        if tree:
+            out["tree"] = _slice_tree(comm, ops, out["perm"], out["dbit"], n, [n], fanout, fill, dev)
+        return out
+
     # a1: D+ of the whole column from the union of the shard occupancies
     occ = ops.occupancy(keys)
     M = ops.occupancy_mask(occ[None] if G == 1 else torch.stack(comm.allgather(occ)), N, superset_kind)
@@ -430,29 +446,36 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
 
     # a8: a subtree per slice; the roots removed; the top layers over their children
     if tree and N:
-        per = int(fanout * fill)
-        hs = [_height(nr, per)] if G == 1 else \
-            [int(t.item()) for t in comm.allgather(torch.tensor([_height(nr, per)], dtype=torch.int64, device=dev))]
-        hmin = min(h for h in hs if h > 0)
-        lstar = max(0, hmin - 2)
-        first_rank = next(k for k in range(G) if nrs[k] > 0)
-        sub, cnt = None, 0
-        if nr:
-            sub = ops.bulkload_block(perm, dbit, fanout, fill, r == first_rank, lstar + 1)
-            cnt = int(sub["shape"].level_nodes[lstar])
-        span = per ** (lstar + 1)
-        hi = torch.clamp(torch.arange(1, cnt + 1, device=dev, dtype=torch.int64) * span, max=nr) - 1
-        cnts = [cnt] if G == 1 else \
-            [int(t.item()) for t in comm.allgather(torch.tensor([cnt], dtype=torch.int64, device=dev))]
-        pad = torch.zeros((max(1, max(cnts)), 2), dtype=torch.int32, device=dev)
-        if cnt:
-            pad[:cnt, 0] = perm[hi]
-            pad[:cnt, 1] = sub["top_min"][:cnt].to(torch.int32)
-        allc = [pad] if G == 1 else comm.allgather(pad)
-        top = None
-        if r == 0 and sum(cnts) > 1:
-            crid = torch.cat([t[:c, 0] for t, c in zip(allc, cnts)]).contiguous()
-            cmin = torch.cat([t[:c, 1] for t, c in zip(allc, cnts)]).to(torch.int16).contiguous()
-            top = ops.bulkload_top(crid, cmin, fanout, fill)
-        out["tree"] = dict(sub=sub, lstar=lstar, children=cnts, top=top, fanout=fanout, fill=fill, sizes=nrs)
+        out["tree"] = _slice_tree(comm, ops, perm, dbit, nr, nrs, fanout, fill, dev)
     return out
+
+
+def _slice_tree(comm, ops, perm, dbit, nr: int, nrs: list, fanout: int, fill: float, dev) -> dict:
+    """this slice's subtree (levels 0..l*), its roots' children gathered, rank 0 builds the
+    top layers over them."""
+    G, r = comm.size, comm.rank
+    per = int(fanout * fill)
+    hs = [_height(nr, per)] if G == 1 else \
+        [int(t.item()) for t in comm.allgather(torch.tensor([_height(nr, per)], dtype=torch.int64, device=dev))]
+    hmin = min(h for h in hs if h > 0)
+    lstar = max(0, hmin - 2)
+    first_rank = next(k for k in range(G) if nrs[k] > 0)
+    sub, cnt = None, 0
+    if nr:
+        sub = ops.bulkload_block(perm, dbit, fanout, fill, r == first_rank, lstar + 1)
+        cnt = int(sub["shape"].level_nodes[lstar])
+    span = per ** (lstar + 1)
+    hi = torch.clamp(torch.arange(1, cnt + 1, device=dev, dtype=torch.int64) * span, max=nr) - 1
+    cnts = [cnt] if G == 1 else \
+        [int(t.item()) for t in comm.allgather(torch.tensor([cnt], dtype=torch.int64, device=dev))]
+    pad = torch.zeros((max(1, max(cnts)), 2), dtype=torch.int32, device=dev)
+    if cnt:
+        pad[:cnt, 0] = perm[hi]
+        pad[:cnt, 1] = sub["top_min"][:cnt].to(torch.int32)
+    allc = [pad] if G == 1 else comm.allgather(pad)
+    top = None
+    if r == 0 and sum(cnts) > 1:
+        crid = torch.cat([t[:c, 0] for t, c in zip(allc, cnts)]).contiguous()
+        cmin = torch.cat([t[:c, 1] for t, c in zip(allc, cnts)]).to(torch.int16).contiguous()
+        top = ops.bulkload_top(crid, cmin, fanout, fill)
+    return dict(sub=sub, lstar=lstar, children=cnts, top=top, fanout=fanout, fill=fill, sizes=nrs)

@@ -194,6 +194,7 @@ def test_build_configs_vs_oracle(cfg):
     keys = cksgen.config(cfg, n=200_003 if cfg > 1 else None)
     r = cks.build(dev(keys))
     check_build(keys, r)
+    assert np.array_equal(r["sort_mask"], oracle.byteocc_superset(keys))      # the mask the sort ran on
 
 
 @pytest.mark.parametrize("kind", [cks.SUPERSET_VARIANT, cks.SUPERSET_BYTEOCC])
@@ -852,6 +853,7 @@ def test_speculative_mask_retry(values):
     l_retry = cks.launches() - a
     check_build(keys, r)
     assert r["sort_bits"] == oracle.popcount(oracle.byteocc_superset(keys))   # sorted by the full D+
+    assert np.array_equal(r["sort_mask"], oracle.byteocc_superset(keys))
     keys[777_777, 3] = 0x01                                       # the sample now sees every value
     d = dev(keys)
     torch.cuda.synchronize()
