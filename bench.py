@@ -257,24 +257,28 @@ def run_sharded(args, world, rank, local):
     for _ in range(args.warmup):
         out = shard.build_sharded(keys, comm)
     torch.cuda.synchronize(device)
-    cks.set_timing(True)
     k_ms = k_bytes = 0.0
     launches0 = cks.launches()
     barrier(world)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(args.steps):
+    every = max(1, args.steps // 10)                        # sampled kernel events, as run_single
+    for i in range(args.steps):
+        sample = (i + 1) % every == 0
+        if sample:
+            cks.set_timing(True)
         out = shard.build_sharded(keys, comm)
-        kms, kby, _ = cks.kernel_stats()
-        k_ms += kms
-        k_bytes += kby
+        if sample:
+            kms, kby, _ = cks.kernel_stats()
+            k_ms += kms
+            k_bytes += kby
+            cks.set_timing(False)
     ev1.record(stream)
     torch.cuda.synchronize(device)
     clk = clocks.stop()
     barrier(world)
     gpu_launches = cks.launches() - launches0
-    cks.set_timing(False)
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_max = max_over_ranks(ms, world, device)
     peak, peak_src = measured_peaks()
