@@ -212,6 +212,7 @@ def test_rebuild_with_prior_mask():
     stale = ref["mask"] | np.packbits(rng.random(8 * 64) < 0.1)
     r = cks.build(dev(keys), prior_mask=stale)
     assert positions(r["mask"]) <= positions(stale)
+    assert np.array_equal(r["sort_mask"], stale)                  # a rebuild sorts by the given mask
     check_build(keys, r)
     # after deletions the old D stays a valid (extended) mask
     sub = keys[::3].copy()
