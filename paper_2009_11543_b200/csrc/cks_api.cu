@@ -171,6 +171,7 @@ T* as(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
 // speculative first build (build_common): sampled rows for the mask, smallest column
 constexpr uint32_t kSpecSamples = 65536;
 constexpr uint64_t kSpecMinKeys = 1u << 20;
+constexpr uint32_t kSpecMinB = 32;                // (8-byte keys: cfg2 0.556 ms without, 0.560 with)
 constexpr size_t kSpecHostOff = 4096;             // the full D+ and V in h_small (2B bytes)
 
 // right after the speculative compress: the keys' D+ and V from the occupancy it marked, copied
@@ -1173,8 +1174,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
     const bool spec = !prior && keys && keys_ready_for_mask && knobs().spec_mask &&
                       out->superset_kind == CKS_SUPERSET_BYTEOCC &&
                       !(ptree && out->ptree_source == CKS_PTREE_CARRY) &&
-                      n >= kSpecMinKeys && B >= 32 && compress_marks_occupancy(keys, B);   // (narrow keys: the
-                                                                          // separate pass is cheap; cfg2 lost 13 us)
+                      n >= kSpecMinKeys && B >= kSpecMinB && compress_marks_occupancy(keys, B);
     ctx->spec_occ = nullptr;
     bool proven = false;                                 // prior mask shown to contain D
     if (prior) {
