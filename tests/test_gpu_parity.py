@@ -876,3 +876,22 @@ def test_speculative_build_with_tree_and_metadata(cfg, src):
     assert np.array_equal(r["variant"], oracle.variant_bitmap(keys)) and np.array_equal(r["ref_key"], keys[0])
     t = oracle.paper_tree(keys, u32(r["perm"]), u16(r["dbit"]), pk=32, fill=0.9)
     assert np.array_equal(r["paper_tree"].cpu().numpy(), t["nodes"])
+
+
+def test_speculative_build_through_every_entry():
+    # the speculative first build behind the north-star call cks_distinction_mask, with the
+    # order check on every build, and with keys that are not 16-byte aligned (no speculation)
+    keys = cksgen.config(3, n=1_100_003)
+    d = dev(keys)
+    ref = oracle.first_build(keys)
+    mask, perm = cks.distinction_mask(d)
+    assert np.array_equal(mask, ref["mask"]) and np.array_equal(u32(perm), ref["perm"])
+    cks.set_verify(cks.VERIFY_ALWAYS)
+    try:
+        check_build(keys, cks.build(d))
+    finally:
+        cks.set_verify(cks.VERIFY_PRIOR)
+    raw = torch.zeros(keys.size + 8, dtype=torch.uint8, device="cuda")
+    view = raw[8:].view(keys.shape)                                # 8-byte aligned only
+    view.copy_(d)
+    check_build(keys, cks.build(view))
