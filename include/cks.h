@@ -110,6 +110,12 @@ int cks_ctx_set_round0_bits(cks_ctx* ctx, uint32_t bits);
 #define CKS_VERIFY_PRIOR 1
 #define CKS_VERIFY_ALWAYS 2
 int cks_ctx_set_verify(cks_ctx* ctx, int mode);
+/* The speculative first build (cks_build): 1 = on (default), 0 = every
+ * first build runs its own superset pass before the compress. The result is the same either
+ * way; a column whose row sample keeps missing byte values pays a second build when on. */
+int cks_ctx_set_speculative_mask(cks_ctx* ctx, int enable);
+/* First builds that took the speculative mask, and those of them run again by the full D+. */
+int cks_ctx_speculation_stats(const cks_ctx* ctx, uint64_t* builds, uint64_t* retries);
 /* Stage times (ms) of the last timed cks_build: a1 mask, a3 compress, a4 histograms+scan,
  * a5 LSD passes, a6 adjacency, a7 repack, a8 bulk load, total. Synchronises. Returns the
  * count written (0 if timing was off). */

@@ -68,6 +68,7 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
            "cks_partition", "cks_sort_prefix", "cks_bulkload_block", "cks_bulkload_top",
            "cks_build_host_batch", "cks_ctx_set_round0_bits", "cks_ctx_set_verify",
+           "cks_ctx_set_speculative_mask", "cks_ctx_speculation_stats",
            "cks_ctx_path_bytes", "cks_paper_tree_ds", "cks_partition_count", "cks_partition_send"]
 
 
@@ -89,6 +90,8 @@ def load_library(path: str | None = None):
     L.cks_ctx_set_sort_mode.argtypes = [p, i32]
     L.cks_ctx_set_round0_bits.argtypes = [p, u32]
     L.cks_ctx_set_verify.argtypes = [p, i32]
+    L.cks_ctx_set_speculative_mask.argtypes = [p, i32]
+    L.cks_ctx_speculation_stats.argtypes = [p, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
     L.cks_ctx_path_bytes.argtypes = [p, ctypes.POINTER(ctypes.c_double)]
     L.cks_ctx_stage_ms.argtypes = [p, ctypes.POINTER(f32), i32]
     L.cks_ctx_launches.argtypes = [p]
@@ -220,6 +223,21 @@ def set_verify(mode: int, device: int | None = None):
     """Order check of later builds against the key rows (cks_ctx_set_verify)."""
     L, c = _context(device)
     _check(L, c, L.cks_ctx_set_verify(c, int(mode)))
+
+
+def set_speculative_mask(enable: bool, device: int | None = None):
+    """First builds take the mask from a row sample and let the compress mark the occupancy
+    (default on; cks_ctx_set_speculative_mask)."""
+    L, c = _context(device)
+    _check(L, c, L.cks_ctx_set_speculative_mask(c, 1 if enable else 0))
+
+
+def speculation_stats(device: int | None = None) -> tuple[int, int]:
+    """(speculative first builds, of them rebuilt by the full D+) on this thread's context."""
+    L, c = _context(device)
+    b, r = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(L, c, L.cks_ctx_speculation_stats(c, ctypes.byref(b), ctypes.byref(r)))
+    return int(b.value), int(r.value)
 
 
 def stage_ms() -> list[float]:

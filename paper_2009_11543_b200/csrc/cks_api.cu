@@ -71,6 +71,8 @@ struct cks_ctx {
     int verify = CKS_VERIFY_PRIOR;    // order check of the result against the key rows
     uint32_t* spec_occ = nullptr;     // speculative first build: the compress marks the occupancy here
     uint64_t spec_retries = 0;        // ... builds redone because the sample's mask fell short
+    uint64_t spec_builds = 0;         // ... builds that took the speculative mask
+    bool spec_on = true;              // cks_ctx_set_speculative_mask
     bool spec_pending = false;        // ... the full D+ / V are on their way to h_small + 4096
     std::vector<uint8_t> proof_mask;  // rebuild: prior mask whose D+ test rides on the compress
     cudaEvent_t spec_ev = nullptr;
@@ -1171,7 +1173,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
             c->verify_now = false;
         }
     } reset{ctx};
-    const bool spec = !prior && keys && keys_ready_for_mask && knobs().spec_mask &&
+    const bool spec = !prior && keys && keys_ready_for_mask && knobs().spec_mask && ctx->spec_on &&
                       out->superset_kind == CKS_SUPERSET_BYTEOCC &&
                       !(ptree && out->ptree_source == CKS_PTREE_CARRY) &&
                       n >= kSpecMinKeys && B >= kSpecMinB && compress_marks_occupancy(keys, B);
@@ -1223,6 +1225,7 @@ int build_common(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, cons
         memcpy(M.data(), ctx->h_small, B);
         m = popcount_mask(M.data(), B);
         ctx->spec_occ = as<uint32_t>(ctx->occ);
+        ctx->spec_builds++;
     } else {
         int kind = out->superset_kind;
         TRY(run_superset(ctx, keys, n, B, kind, M.data(), &m, keys_ready_for_mask, V.data()));
@@ -1441,6 +1444,19 @@ int cks_ctx_set_sort_mode(cks_ctx* ctx, int mode) {
 int cks_ctx_set_round0_bits(cks_ctx* ctx, uint32_t bits) {
     if (!ctx || bits > 64 || (bits & 7)) return CKS_EINVAL;
     ctx->round0_bits = bits;
+    return CKS_OK;
+}
+
+int cks_ctx_set_speculative_mask(cks_ctx* ctx, int enable) {
+    if (!ctx) return CKS_EINVAL;
+    ctx->spec_on = enable != 0;
+    return CKS_OK;
+}
+
+int cks_ctx_speculation_stats(const cks_ctx* ctx, uint64_t* builds, uint64_t* retries) {
+    if (!ctx) return CKS_EINVAL;
+    if (builds) *builds = ctx->spec_builds;
+    if (retries) *retries = ctx->spec_retries;
     return CKS_OK;
 }
 

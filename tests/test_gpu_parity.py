@@ -849,9 +849,12 @@ def test_speculative_mask_retry(values):
     d = dev(keys)
     torch.cuda.synchronize()
     a = cks.launches()
+    s0 = cks.speculation_stats()
     r = cks.build(d)
     torch.cuda.synchronize()
     l_retry = cks.launches() - a
+    s1 = cks.speculation_stats()
+    assert (s1[0] - s0[0], s1[1] - s0[1]) == (1, 1)               # speculated, rebuilt once
     check_build(keys, r)
     assert r["sort_bits"] == oracle.popcount(oracle.byteocc_superset(keys))   # sorted by the full D+
     assert np.array_equal(r["sort_mask"], oracle.byteocc_superset(keys))
@@ -862,8 +865,16 @@ def test_speculative_mask_retry(values):
     r = cks.build(d)
     torch.cuda.synchronize()
     l_plain = cks.launches() - a
+    s2 = cks.speculation_stats()
+    assert (s2[0] - s1[0], s2[1] - s1[1]) == (1, 0)
     check_build(keys, r)
     assert l_retry > l_plain                                      # the first build ran twice
+    cks.set_speculative_mask(False)                               # its own superset pass instead
+    try:
+        check_build(keys, cks.build(d))
+        assert cks.speculation_stats() == s2
+    finally:
+        cks.set_speculative_mask(True)
 
 
 @pytest.mark.parametrize("cfg,src", [(5, cks.PTREE_AUTO), (5, cks.PTREE_DS), (3, cks.PTREE_ROWS), (2, cks.PTREE_DECODE)])
