@@ -77,7 +77,10 @@ int cks_ctx_create(int device, void* stream, cks_ctx** out);
 int cks_ctx_destroy(cks_ctx* ctx);
 /* Replace the borrowed stream used by subsequent calls. */
 int cks_ctx_set_stream(cks_ctx* ctx, void* stream);
-/* 1 = record per-stage CUDA events in cks_build (read with cks_ctx_stage_ms). */
+/* 1 = record per-stage CUDA events in cks_build (read with cks_ctx_stage_ms) and the dominant
+ * kernel's own events (cks_ctx_kernel_stats). The event records sit between kernels that are
+ * otherwise chained by programmatic dependent launch, so a timed build is slower (cfg5:
+ * ~0.06 ms); bench.py times one build in ten this way. */
 int cks_ctx_set_timing(cks_ctx* ctx, int enable);
 /* How cks_build / cks_distinction_mask sort (the result is the same):
  *   CKS_SORT_SINGLE       one stable LSD sort over all m = |M| bits of P_M;
