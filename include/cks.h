@@ -196,6 +196,17 @@ int cks_adjacent_dbits(cks_ctx* ctx, const uint32_t* sorted_packed, uint32_t pac
  * over shards (bitwise OR; NCCL has no OR reduction, so: all-gather + cks_occupancy_mask)
  * is the occupancy of the whole column. */
 int cks_occupancy(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, uint32_t* occ_out);
+/* The speculative mask of the sharded first build: cks_occupancy_sample
+ * is the occupancy of `samples` rows strided over this shard (occ_out overwritten; keys of 8,
+ * 16, 32 or 64 bytes, 16-byte aligned, else the whole shard's occupancy); cks_compress_marking
+ * is cks_compress that also writes the shard's full occupancy to occ_out (overwritten) from the
+ * same read of the keys (the same key widths; CKS_EINVAL otherwise). The union of the sampled
+ * occupancies gives a mask M' inside the column's D+; when the union of the marked ones gives
+ * the same D+, P_M' is the column's P_{D+}. Asynchronous. */
+int cks_occupancy_sample(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, uint32_t samples,
+                         uint32_t* occ_out);
+int cks_compress_marking(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t key_bytes, const uint8_t* mask,
+                         uint32_t* packed_out, uint32_t* occ_out);
 
 /* cks_occupancy_mask: the superset mask of the union of `nocc` occupancies (device
  * u32[nocc][key_bytes*8], e.g. the all-gathered shard occupancies), n_total = keys over all

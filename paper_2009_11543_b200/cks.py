@@ -68,7 +68,8 @@ EXPORTS = ["cks_ctx_create", "cks_ctx_destroy", "cks_ctx_set_stream", "cks_ctx_s
            "cks_build", "cks_build_host", "cks_occupancy", "cks_occupancy_mask", "cks_rank_sorted", "cks_repack",
            "cks_partition", "cks_sort_prefix", "cks_bulkload_block", "cks_bulkload_top",
            "cks_build_host_batch", "cks_ctx_set_round0_bits", "cks_ctx_set_verify",
-           "cks_ctx_set_speculative_mask", "cks_ctx_speculation_stats",
+           "cks_ctx_set_speculative_mask", "cks_ctx_speculation_stats", "cks_occupancy_sample",
+           "cks_compress_marking",
            "cks_ctx_path_bytes", "cks_paper_tree_ds", "cks_partition_count", "cks_partition_send"]
 
 
@@ -115,6 +116,8 @@ def load_library(path: str | None = None):
     L.cks_build.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     L.cks_build_host.argtypes = [p, p, u64, u32, p, ctypes.POINTER(BuildOut)]
     L.cks_occupancy.argtypes = [p, p, u64, u32, p]
+    L.cks_occupancy_sample.argtypes = [p, p, u64, u32, u32, p]
+    L.cks_compress_marking.argtypes = [p, p, u64, u32, p, p, p]
     L.cks_occupancy_mask.argtypes = [p, p, u32, u32, u64, i32, p, ctypes.POINTER(u32)]
     L.cks_rank_sorted.argtypes = [p, p, u32, u64, p, u64, p, u32, p]
     L.cks_repack.argtypes = [p, p, p, p, u32, u64, p]
@@ -333,6 +336,33 @@ def occupancy(keys: torch.Tensor) -> torch.Tensor:
     occ = torch.empty(B * 8, dtype=torch.int32, device=keys.device)
     _check(L, c, L.cks_occupancy(c, _ptr(keys), n, B, _ptr(occ)))
     return occ
+
+
+def occupancy_sample(keys: torch.Tensor, samples: int) -> torch.Tensor:
+    """int32[B*8]: occupancy of `samples` rows strided over these keys (cks_occupancy_sample)."""
+    n, B = _keys(keys)
+    L, c = _context(keys.device.index)
+    occ = torch.empty(B * 8, dtype=torch.int32, device=keys.device)
+    _check(L, c, L.cks_occupancy_sample(c, _ptr(keys), n, B, int(samples), _ptr(occ)))
+    return occ
+
+
+def compress_marking(keys: torch.Tensor, mask):
+    """(P planes as compress(), int32[B*8] occupancy of all these keys) from one read of the
+    keys (cks_compress_marking)."""
+    n, B = _keys(keys)
+    L, c = _context(keys.device.index)
+    m = _host_mask(mask, B)
+    out = torch.empty((nplanes(popcount(m)), n), dtype=torch.int32, device=keys.device)
+    occ = torch.empty(B * 8, dtype=torch.int32, device=keys.device)
+    _check(L, c, L.cks_compress_marking(c, _ptr(keys), n, B, m.ctypes.data, _ptr(out) if out.numel() else None,
+                                        _ptr(occ)))
+    return out, occ
+
+
+def marks_occupancy(keys: torch.Tensor) -> bool:
+    """Whether compress_marking applies (16-byte aligned keys of 8/16/32/64 bytes)."""
+    return keys.shape[1] in (8, 16, 32, 64) and keys.data_ptr() % 16 == 0
 
 
 def occupancy_mask(occs: torch.Tensor, n_total: int, kind: int = SUPERSET_BYTEOCC) -> np.ndarray:

@@ -1542,6 +1542,40 @@ int cks_occupancy(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, uin
     return CKS_OK;
 }
 
+int cks_occupancy_sample(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, uint32_t samples,
+                         uint32_t* occ_out) {
+    TRY(check_keys(ctx, keys, n, B));
+    if (!occ_out) return fail(ctx, CKS_EINVAL, "occ_out is NULL");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemsetAsync(occ_out, 0, (size_t)B * 8 * 4, ctx->stream));
+    if (n && compress_marks_occupancy(keys, B) && samples && samples < n) {
+        LAUNCH(launch_occupancy_sample(keys, n, B, samples, occ_out, ctx->stream));
+        BYTES((double)samples * B);
+    } else if (n) {
+        LAUNCH(launch_occupancy(keys, n, B, occ_out, ctx->sms, ctx->stream));
+        BYTES((double)n * B);
+    }
+    return CKS_OK;
+}
+
+int cks_compress_marking(cks_ctx* ctx, const uint8_t* keys, uint64_t n, uint32_t B, const uint8_t* mask,
+                         uint32_t* packed_out, uint32_t* occ_out) {
+    TRY(check_keys(ctx, keys, n, B));
+    if (!mask || !occ_out) return fail(ctx, CKS_EINVAL, "mask or occ_out is NULL");
+    if (n && !compress_marks_occupancy(keys, B))
+        return fail(ctx, CKS_EINVAL, "cks_compress_marking needs 16-byte aligned keys of 8, 16, 32 or 64 bytes");
+    const uint32_t m = popcount_mask(mask, B);
+    if (n && m && !packed_out) return fail(ctx, CKS_EINVAL, "packed_out is NULL");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemsetAsync(occ_out, 0, (size_t)B * 8 * 4, ctx->stream));
+    if (n && m) {
+        TRY(run_compress(ctx, keys, n, B, mask, packed_out, n, 0, nullptr, occ_out));
+    } else if (n) {                                               // (no planes: the occupancy alone)
+        LAUNCH(launch_occupancy(keys, n, B, occ_out, ctx->sms, ctx->stream));
+    }
+    return check_guards(ctx);
+}
+
 int cks_occupancy_mask(cks_ctx* ctx, const uint32_t* occ, uint32_t nocc, uint32_t B, uint64_t n_total, int kind,
                        uint8_t* mask_out, uint32_t* popcount_out) {
     if (!ctx) return CKS_EINVAL;

@@ -183,8 +183,11 @@ class ThreadComm:
 class CudaOps:
     """The per-shard steps as libcks kernels (the product path; no CPU fallback)."""
     occupancy = staticmethod(cks.occupancy)
+    occupancy_sample = staticmethod(cks.occupancy_sample)
     occupancy_mask = staticmethod(cks.occupancy_mask)
     compress = staticmethod(cks.compress)
+    compress_marking = staticmethod(cks.compress_marking)
+    marks_occupancy = staticmethod(cks.marks_occupancy)
     partition = staticmethod(cks.partition)
     partition_count = staticmethod(cks.partition_count)
     partition_send = staticmethod(cks.partition_send)
@@ -332,6 +335,17 @@ def _exchange_fused(comm, ops, P, m, q, off, npl, dev):
     return R, rids, [int(v) for v in cm[r]]
 
 
+SPEC_MIN_KEYS = 1 << 20          # (as the single build, cks_api.cu kSpecMinKeys)
+SPEC_SAMPLES = 65536             # rows over the whole column, split over the shards
+
+
+def _all(comm, flag: bool, dev) -> bool:
+    """Whether every rank's flag is set (one all-gather)."""
+    if comm.size == 1:
+        return bool(flag)
+    return all(int(t.item()) for t in comm.allgather(torch.tensor([1 if flag else 0], dtype=torch.int64, device=dev)))
+
+
 def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int = 256, fanout: int = 64,
                   fill: float = 1.0, tree: bool = True, superset_kind: int = cks.SUPERSET_BYTEOCC,
                   fused: bool | None = None) -> dict:
@@ -364,14 +378,27 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
             out["tree"] = _slice_tree(comm, ops, out["perm"], out["dbit"], n, [n], fanout, fill, dev)
         return out
 
-    # a1: D+ of the whole column from the union of the shard occupancies
-    occ = ops.occupancy(keys)
-    M = ops.occupancy_mask(occ[None] if G == 1 else torch.stack(comm.allgather(occ)), N, superset_kind)
+    # a1 + a3: D+ of the whole column from the union of the shard occupancies, and P_{D+}. Large
+    # columns of 32/64-byte keys read the keys once for both (the speculative mask, DESIGN.md
+    # Sec. 1.0): the union of strided row samples gives M' (inside D+), the compress by M' marks
+    # every key's occupancy, and the union of those gives D+; the rare M' != D+ compresses again
+    spec = (hasattr(ops, "compress_marking") and superset_kind == cks.SUPERSET_BYTEOCC and N >= SPEC_MIN_KEYS
+            and B >= 32 and _all(comm, ops.marks_occupancy(keys) or n == 0, dev))   # (same answer on every rank)
+    if spec:
+        occ_s = ops.occupancy_sample(keys, max(1, SPEC_SAMPLES // G))
+        Ms = ops.occupancy_mask(torch.stack(comm.allgather(occ_s)), N, superset_kind)
+        P, occ = ops.compress_marking(keys, Ms)
+        M = ops.occupancy_mask(torch.stack(comm.allgather(occ)), N, superset_kind)
+        if not np.array_equal(M, Ms):
+            P = ops.compress(keys, M)
+        speculative = "held" if np.array_equal(M, Ms) else "retried"
+    else:
+        occ = ops.occupancy(keys)
+        M = ops.occupancy_mask(occ[None] if G == 1 else torch.stack(comm.allgather(occ)), N, superset_kind)
+        P = ops.compress(keys, M)
+        speculative = None
     m = cks.popcount(M)
     npl = cks.nplanes(m)
-
-    # a3
-    P = ops.compress(keys, M)
 
     # splitters from a regular sample of every shard (none with one shard)
     q = None
@@ -442,7 +469,8 @@ def build_sharded(keys: torch.Tensor, comm, ops=CudaOps, samples_per_rank: int =
 
     nrs = [nr] if G == 1 else [int(t.item()) for t in comm.allgather(torch.tensor([nr], dtype=torch.int64, device=dev))]
     out = dict(mask=D, popcount=cks.popcount(D), sort_mask=M, sort_bits=m, perm=perm, dbit=dbit, packed=packed,
-               offset=sum(nrs[:r]), n_total=N, send_counts=send_counts, tree=None)
+               offset=sum(nrs[:r]), n_total=N, send_counts=send_counts, tree=None,
+               speculative=speculative)
 
     # a8: a subtree per slice; the roots removed; the top layers over their children
     if tree and N:

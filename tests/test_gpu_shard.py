@@ -86,6 +86,23 @@ def test_sharded_ragged_and_empty_shards(sizes):
     check_slices(keys, run(keys, sizes, samples_per_rank=8))
 
 
+@pytest.mark.parametrize("case", ["cfg5", "cfg3", "retry", "ragged"])
+def test_sharded_speculative_mask(case):
+    # >= 2^20 keys of 32/64 bytes: the mask from the shards' row samples, the occupancy marked by
+    # the compress; a key byte value no sample saw (rows 555_556 and 1_650_001 are off the
+    # 33-row sample stride of both shards) makes the union D+ larger and the shards compress again
+    if case == "retry":
+        keys = np.random.default_rng(3).integers(0, 8, size=(2_200_001, 32), dtype=np.uint8)
+        keys[555_556, 7] = 0x80
+        keys[1_650_001, 30] = 0x40
+    else:
+        keys = cksgen.config(5 if case != "cfg3" else 3, n=2_200_001)
+    sizes = [1_100_000, 1_100_001] if case != "ragged" else [1_700_000, 0, 500_001]
+    outs = run(keys, sizes, tree=False)
+    assert all(o["speculative"] == ("retried" if case == "retry" else "held") for o in outs)
+    check_slices(keys, outs)
+
+
 def test_sharded_duplicates_and_equal_keys():
     rng = np.random.default_rng(5)
     dup = np.repeat(rng.integers(0, 256, (30, 24), dtype=np.uint8), 400, axis=0)[rng.permutation(12000)]

@@ -71,6 +71,46 @@ def test_sharded_threads_oracle_ops(name, keys, sizes):
     check_slices(keys, outs)
 
 
+class SpecOracleOps(OracleOps):
+    """OracleOps with the speculative-mask steps: the strided row sample of cks_occupancy_sample
+    (step = n // samples, at least 1) and a compress that also returns the occupancy."""
+
+    def occupancy_sample(self, keys, samples):
+        k = keys.cpu().numpy()
+        n = k.shape[0]
+        step = max(n // samples, 1) if n else 1
+        cnt = min(n // step, samples) if n else 0
+        return _occ(k[np.arange(cnt, dtype=np.int64) * step])
+
+    def compress_marking(self, keys, mask):
+        return self.compress(keys, mask), self.occupancy(keys)
+
+    def marks_occupancy(self, keys):
+        return True
+
+
+def _occ(k):
+    return torch.from_numpy(occupancy_np(k).view(np.int32))
+
+
+@pytest.mark.parametrize("samples,expect", [(4096, "held"), (6, "retried")])
+@pytest.mark.parametrize("sizes", [[2500, 2501], [4000, 0, 1001]])
+def test_sharded_speculative_mask_host_logic(monkeypatch, samples, expect, sizes):
+    # the G > 1 speculative mask (shard.build_sharded): every rank takes the same branch, a
+    # sample covering every row holds, a 2-3 row sample misses byte values and the shards
+    # compress again with the union D+; the slices equal the oracle's single build either way
+    monkeypatch.setattr(shard, "SPEC_MIN_KEYS", 1000)
+    monkeypatch.setattr(shard, "SPEC_SAMPLES", samples)
+    keys = cksgen.config(5, n=sum(sizes))
+    rows = split_rows(keys.shape[0], sizes)
+    ops = SpecOracleOps(keys)
+    shards = [torch.from_numpy(np.ascontiguousarray(keys[a:b])) for a, b in rows]
+    outs = shard.ThreadComm.run(len(sizes), lambda comm, k: shard.build_sharded(k, comm, ops=ops,
+                                                                                 samples_per_rank=16), shards)
+    assert [o["speculative"] for o in outs] == [expect] * len(sizes)
+    check_slices(keys, outs)
+
+
 def free_port() -> int:
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
