@@ -451,6 +451,20 @@ def test_refine_runs_of_equal_keys():
     check_build(keys, cks.build(dev(keys)))
 
 
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_refine_run_boundaries(shuffle):
+    # runs of equal keys whose ends fall on and next to the compaction's boundaries: a thread's
+    # 16 flags, a warp's 512, a tile's 4096 (runs inside one, across two, filling one exactly),
+    # singletons between them, a ragged end; every round compacts them again
+    rng = np.random.default_rng(17)
+    lens = [1, 15, 16, 1, 17, 2, 14, 496, 512, 1, 511, 3585, 4096, 1, 4095, 2, 4097, 8192, 3, 1, 1, 7] * 3
+    base = np.unique(rng.integers(0, 256, (len(lens) + 50, 24), dtype=np.uint8), axis=0)[:len(lens)]
+    keys = np.repeat(base, lens, axis=0)
+    if shuffle:
+        keys = keys[rng.permutation(keys.shape[0])]
+    check_build(keys, cks.build(dev(keys)))
+
+
 @pytest.mark.parametrize("cfg", [3, 5])
 def test_sort_modes_agree(cfg):
     # single full-width sort, auto and forced prefix refinement: the same (key, row id) order,
