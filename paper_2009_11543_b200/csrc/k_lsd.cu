@@ -170,18 +170,25 @@ k_chunk_scan(const LsdPassArgs a, uint32_t nchunks) {
     pdl_trigger();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t d = blockIdx.x * 32 + lane;
-    if (warp == 0) {                                         // bucket base of digit d
-        uint32_t run = 0;
-        for (uint32_t e = 0; e < blockIdx.x * 32; e++) run += a.total[e];
-        uint32_t x = a.total[d];
-#pragma unroll
+    if (warp < 8) {                                          // bucket bases: a scan of all 256 totals
+        const uint32_t v = a.total[threadIdx.x];             // (one load each; the earlier serial sum
+        uint32_t x = v;                                      // of the lower digits' totals took up to
+#pragma unroll                                               // 224 dependent L2 reads, ~10 us a pass)
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
-        s_base[lane] = run + x - a.total[d];
+        s_part[warp][lane] = x - v;                          // exclusive inside the warp
+        if (lane == 31) s_part[8][warp] = x;                 // warp total
+    }
+    __syncthreads();
+    if (warp == (int)blockIdx.x) {                           // this CTA's 32 digits = warp blockIdx.x
+        uint32_t run = 0;
+        for (int w = 0; w < (int)blockIdx.x; w++) run += s_part[8][w];
+        s_base[lane] = run + s_part[warp][lane];
         if (a.bbase) a.bbase[d] = s_base[lane];              // (scatter-to-parts passes)
     }
+    __syncthreads();
     const uint32_t per = (nchunks + 31) / 32;
     const uint32_t c0 = warp * per, c1 = min(c0 + per, nchunks);
     uint32_t sum = 0;
