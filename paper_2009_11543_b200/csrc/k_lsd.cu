@@ -596,19 +596,34 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
                     dg[i] = digit_of(dslot[wofs + i * 32 + lane], sel);
                     peers[i] = match_bits<8>(dg[i]);
                 }
-                uint32_t old[RI];
+                if constexpr (!SCATTER && SH::TILE == 4096) {
 #pragma unroll
-                for (int i = 0; i < RI; i++) {
-                    const uint32_t lower = __popc(peers[i] & ltm);
-                    asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %1, 0;\n mov.u32 %0, 0;\n"
-                                 " @p atom.shared.add.u32 %0, [%2], %3;\n}"
-                                 : "=r"(old[i]) : "r"(lower), "r"(hbase + dg[i] * 4), "r"((uint32_t)__popc(peers[i]))
-                                 : "memory");
-                    pos[i] = lower;
-                    __syncwarp();                                // item i's reservations before item i+1's
+                    for (int i = 0; i < RI; i++) {
+                        // every lane reads its digit's warp-private bin (peers read the same word:
+                        // a broadcast), then the digit's leader advances it by the peer count -- a
+                        // plain load and store instead of an atomic with return and a shuffle
+                        const uint32_t lower = __popc(peers[i] & ltm);
+                        const uint32_t o = h[dg[i]];
+                        __syncwarp();                            // every read of item i before its writes
+                        if (lower == 0) h[dg[i]] = o + (uint32_t)__popc(peers[i]);
+                        pos[i] = lower + o;
+                        __syncwarp();                            // item i's reservations before item i+1's
+                    }
+                } else {                                         // (ptxas C7600 on these shapes with the above)
+                    uint32_t old[RI];
+#pragma unroll
+                    for (int i = 0; i < RI; i++) {
+                        const uint32_t lower = __popc(peers[i] & ltm);
+                        asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %1, 0;\n mov.u32 %0, 0;\n"
+                                     " @p atom.shared.add.u32 %0, [%2], %3;\n}"
+                                     : "=r"(old[i]) : "r"(lower), "r"(hbase + dg[i] * 4), "r"((uint32_t)__popc(peers[i]))
+                                     : "memory");
+                        pos[i] = lower;
+                        __syncwarp();                            // item i's reservations before item i+1's
+                    }
+#pragma unroll
+                    for (int i = 0; i < RI; i++) pos[i] += __shfl_sync(0xFFFFFFFFu, old[i], __ffs(peers[i]) - 1);
                 }
-#pragma unroll
-                for (int i = 0; i < RI; i++) pos[i] += __shfl_sync(0xFFFFFFFFu, old[i], __ffs(peers[i]) - 1);
             }
             named_sync(1, kRT);
             {
