@@ -723,7 +723,11 @@ k_downsweep_ws(const LsdPassArgs a, uint32_t nfull) {
 // 16 below 8192 tiles (cfg3/cfg4 and the refinement's lists lose parallelism with 32)
 static uint32_t chunk_for(uint64_t tiles) {
     if (knobs().lsd_chunk > 0) return (uint32_t)knobs().lsd_chunk;
-    return tiles >= 8192 ? 32u : 16u;
+    // three waves of upsweep CTAs over B200's 148 SMs with equal chunks (cfg5: 12,207 tiles ->
+    // 28-tile chunks, 436 CTAs; fixed 32-tile chunks left a third wave of 86 CTAs on 148 SMs),
+    // at least 8 tiles a chunk
+    const uint64_t c = (tiles + 3 * 148 - 1) / (3 * 148);
+    return c < 8 ? 8u : (uint32_t)c;
 }
 
 uint64_t lsd_tile_keys() { return (uint64_t)kSortThreads * knobs().lsd_items; }
