@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "sort or build_configs or full_size" > gpurun_out/q_pytest.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/q_pytest.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "${K:-sort or build_configs or full_size or refine}" > gpurun_out/q_pytest.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/q_pytest.log
 for c in ${CFGS:-5 2}; do
 timeout 300 python bench.py --steps 60 --warmup 5 --no-e2e --no-cpu-baseline --no-full-key --no-rebuild --config $c > gpurun_out/q_bench$c.json 2> gpurun_out/q_bench$c.err; echo "bench rc $?"
 python - $c <<'PY'
