@@ -15,6 +15,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <utility>
+
 #include "cks_internal.h"
 #include "k_occ_flags.cuh"
 
@@ -284,6 +286,67 @@ k_compress_occ(const uint8_t* __restrict__ keys, uint64_t n, const __grid_consta
     fold_flags<B>(flag, occ);
 }
 
+// Uniform-width masks (every key word holds C mask bits, e.g. cfg5's ACGT: 3 bits a byte, 12 a
+// word; cfg3: 28) with P_M left-aligned (no top padding): every field's plane and shift are
+// compile-time, so the plane words are assembled by constant shifts and stored once each -- no
+// running bit count, no per-word plane test (k_compress_fixed / k_compress_occ keep those for
+// any mask). OCC: also marks the byte occupancy as k_compress_occ does.
+template <int B, int C, bool OCC>
+__global__ void __launch_bounds__(kCompressThreads)
+k_compress_uni(const uint8_t* __restrict__ keys, uint64_t n, const __grid_constant__ FixedPlan<B / 4> plan,
+               uint32_t* __restrict__ planes, uint64_t pitch, uint32_t* __restrict__ occ) {
+    constexpr int NW = B / 4, M = NW * C, NP = (M + 31) / 32;
+    __shared__ __align__(16) uint8_t flag[OCC ? B * kRowBytes : 16];
+    if (OCC) {
+        for (uint32_t i = threadIdx.x; i < B * kRowBytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(flag)[i] = 0;
+        __syncthreads();
+    }
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) {
+        uint32_t w[NW];
+        load_key<B>(keys + i * B, w);
+        if (OCC) {
+#pragma unroll
+            for (int k = 0; k < NW; k++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) flag[(4 * k + b) * kRowBytes + __byte_perm(w[k], 0, 0x4440 + b)] = 1;
+        }
+        uint32_t out[NP];
+#pragma unroll
+        for (int q = 0; q < NP; q++) out[q] = 0;
+#pragma unroll
+        for (int k = 0; k < NW; k++) {
+            uint32_t x = bswap32(w[k]) & plan.mask[k];
+#pragma unroll
+            for (int s = 0; s < 5; s++) x = mad_u32(x & plan.mv[k][s], (1u << (1u << s)) - 1u, x);
+            // x: the word's C-bit field, left-aligned; it starts at bit k*C of P_M (from the MSB)
+            const int off = k * C, q = NP - 1 - off / 32, r = off % 32;
+            out[q] |= r ? x >> r : x;
+            if (r + C > 32) out[q - 1] |= x << (32 - r);
+        }
+#pragma unroll
+        for (int q = 0; q < NP; q++) planes[(uint64_t)q * pitch + i] = out[q];
+    }
+    if (OCC) {
+        __syncthreads();
+        fold_flags<B>(flag, occ);
+    }
+}
+
+template <int B, int C>
+static void launch_uni_c(const uint8_t* keys, uint64_t n, const FixedPlan<B / 4>& fp, uint32_t* planes, uint64_t pitch,
+                         int grid, cudaStream_t st, uint32_t* occ) {
+    if (occ) k_compress_uni<B, C, true><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, occ);
+    else k_compress_uni<B, C, false><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, occ);
+}
+
+template <int B, int... Cs>
+static bool launch_uni(int c, std::integer_sequence<int, Cs...>, const uint8_t* keys, uint64_t n,
+                       const FixedPlan<B / 4>& fp, uint32_t* planes, uint64_t pitch, int grid, cudaStream_t st,
+                       uint32_t* occ) {
+    return ((c == Cs + 1 ? (launch_uni_c<B, Cs + 1>(keys, n, fp, planes, pitch, grid, st, occ), true) : false) || ...);
+}
+
 // Row-list variant for B in {32, 64} (a7: P_D from the key rows in sorted order): the random
 // rows are loaded cooperatively, B/16 lanes per row with one 16-byte load each, into a
 // shared-memory tile of 256 rows (odd 16-byte row stride), then each thread compresses its
@@ -365,6 +428,15 @@ static void launch_fixed(const uint8_t* keys, uint64_t n, const GatherPlan* hpla
             k_compress_rows<B><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, np, toppad, rows);
             return;
         }
+    }
+    if constexpr (B == 32) {
+        // every word holds the same number of mask bits and P_M is left-aligned: the
+        // compile-time layout (k_compress_uni)
+        bool uni = !rows && toppad == 0 && fp.cnt[0] > 0;
+        for (int k = 1; k < B / 4 && uni; k++) uni = fp.cnt[k] == fp.cnt[0];
+        if (uni && launch_uni<B>((int)fp.cnt[0], std::make_integer_sequence<int, 32>{}, keys, n, fp, planes, pitch,
+                                 grid, st, occ))
+            return;
     }
     if (rows) k_compress_fixed<B, 4><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, np, toppad, rows);
     else if (occ) k_compress_occ<B><<<grid, kCompressThreads, 0, st>>>(keys, n, fp, planes, pitch, np, toppad, occ);

@@ -79,6 +79,40 @@ def test_compress_random_masks(B):
         assert np.array_equal(got, oracle.compress(keys, mask))
 
 
+@pytest.mark.parametrize("C", [1, 3, 4, 7, 12, 13, 28, 31, 32])
+def test_compress_uniform_word_masks(C):
+    # masks with the same number C of bits in every 4-byte key word (the compile-time layout of
+    # k_compress_uni when P_M has no top padding: C % 4 == 0 here, right-aligned 8C-bit P), with
+    # and without the occupancy marking
+    from shard_oracle_ops import occupancy_np
+    rng = np.random.default_rng(100 + C)
+    bits = np.zeros(256, np.uint8)
+    for w in range(8):
+        bits[32 * w + rng.choice(32, size=C, replace=False)] = 1
+    mask = np.packbits(bits)
+    keys = cksgen.uniform(50_003, 32, seed=C)
+    d = dev(keys)
+    ref = oracle.compress(keys, mask)
+    assert np.array_equal(u32(cks.compress(d, mask)), ref)
+    planes, occ = cks.compress_marking(d, mask)
+    assert np.array_equal(u32(planes), ref)
+    assert np.array_equal(occ.cpu().numpy().view(np.uint32), occupancy_np(keys))
+
+
+@pytest.mark.parametrize("values", [2, 128])
+def test_speculative_build_uniform_alphabet(values):
+    # first builds (>= 2^20 keys, the speculative mask) whose D+ has the same bits in every byte:
+    # {0, 1}: 1 bit a byte, m = 32, one LSD sort; 0..127: 7 bits, m = 224, sort by prefixes --
+    # the compress marking the occupancy with the compile-time layout (C = 4 and 28 bits a word)
+    rng = np.random.default_rng(values)
+    keys = rng.integers(0, values, size=(1_100_003, 32), dtype=np.uint8)
+    keys[:, :3] = keys[rng.integers(0, 50_000, size=keys.shape[0]), :3]
+    s0 = cks.speculation_stats()
+    r = cks.build(dev(keys))
+    assert cks.speculation_stats()[0] == s0[0] + 1
+    check_build(keys, r)
+
+
 def test_compress_table3_mask():
     from conftest import load_bit_rows
     m = load_bit_rows("table3_indbtab_dbitmap.txt")
