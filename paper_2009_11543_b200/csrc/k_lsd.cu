@@ -191,9 +191,18 @@ k_chunk_scan(const LsdPassArgs a, uint32_t nchunks) {
     __syncthreads();
     const uint32_t per = (nchunks + 31) / 32;
     const uint32_t c0 = warp * per, c1 = min(c0 + per, nchunks);
+    // up to kKeep of the warp's chunk totals stay in registers for the write-back below (one
+    // read of chunk_tot instead of two: cfg5 has 436 chunks, 14 a warp)
+    constexpr uint32_t kKeep = 16;
+    uint32_t keep[kKeep];
     uint32_t sum = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < kKeep; i++) {
+        keep[i] = c0 + i < c1 ? a.chunk_tot[(uint64_t)(c0 + i) * kRadix + d] : 0u;
+        sum += keep[i];
+    }
 #pragma unroll 8
-    for (uint32_t c = c0; c < c1; c++) sum += a.chunk_tot[(uint64_t)c * kRadix + d];
+    for (uint32_t c = c0 + kKeep; c < c1; c++) sum += a.chunk_tot[(uint64_t)c * kRadix + d];
     s_part[warp][lane] = sum;
     __syncthreads();
     if (warp == 0) {
@@ -206,8 +215,14 @@ k_chunk_scan(const LsdPassArgs a, uint32_t nchunks) {
     }
     __syncthreads();
     uint32_t run = s_part[warp][lane];
+#pragma unroll
+    for (uint32_t i = 0; i < kKeep; i++)
+        if (c0 + i < c1) {
+            a.chunk_tot[(uint64_t)(c0 + i) * kRadix + d] = run;
+            run += keep[i];
+        }
 #pragma unroll 8
-    for (uint32_t c = c0; c < c1; c++) {
+    for (uint32_t c = c0 + kKeep; c < c1; c++) {
         uint32_t* p = a.chunk_tot + (uint64_t)c * kRadix + d;
         uint32_t v = *p;
         *p = run;
